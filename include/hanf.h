@@ -1,0 +1,218 @@
+/*
+ * hanf.h -- C-ABI of the B200 HyperANF engine (libhanf.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The
+ * reference (/root/reference/proj/include/hyperanf/) is a header-only C++20
+ * library with no FFI; its engine surface is the C++ API in engine.hpp.
+ * Each entry point below names the reference interface it replaces.  The
+ * C++ wrapper include/hyperanf_b200/engine.hpp restores that exact surface
+ * (class names, argument meaning, exception types) on top of this ABI, and
+ * paper_1011_5599_b200/ mirrors it for Python.
+ *
+ * Conventions:
+ *  - plain pointers and sizes only; no exceptions cross the ABI;
+ *  - every call returns a hanf_status; hanf_last_error() gives the
+ *    thread-local message of the last failure;
+ *  - graph arrays are caller-owned and copied to HBM at create time;
+ *    device buffers are engine-owned;
+ *  - a handle is driven by one host thread.
+ */
+#ifndef HANF_H
+#define HANF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t hanf_status;
+#define HANF_OK 0
+#define HANF_INVALID_ARGUMENT 1 /* std::invalid_argument: engine.hpp:71-74, hll.hpp:45-48 */
+#define HANF_GUARD 2            /* hyperanf::GuardError: engine.hpp:255-258 */
+#define HANF_OUT_OF_RANGE 3     /* std::out_of_range: hll.hpp:233-235 */
+#define HANF_CUDA_ERROR 4       /* std::runtime_error (device failure) */
+#define HANF_OUT_OF_MEMORY 5    /* std::bad_alloc / cudaErrorMemoryAllocation */
+#define HANF_CAPACITY 6         /* caller-provided output buffer too small */
+#define HANF_IO_ERROR 7         /* hyperanf::IoError: errors.hpp:13-15 */
+#define HANF_PARSE_ERROR 8      /* hyperanf::ParseError: errors.hpp:8-10 */
+
+typedef struct hanf_engine hanf_engine;
+typedef struct hanf_graph hanf_graph;
+
+/* Read-only CSR view; replaces `const Graph&` (graph.hpp:23-69): num_nodes
+ * (:46), num_arcs (:47), offsets() u64[n+1] (:56), arcs() u32[a] (:57).
+ * Successor lists need not be sorted or deduplicated for the engine (a
+ * union is order- and duplicate-insensitive), but Graph always is. */
+typedef struct {
+  uint64_t n;
+  uint64_t num_arcs;
+  const uint64_t* offsets;
+  const uint32_t* arcs;
+} hanf_graph_view;
+
+/* EngineConfig (engine.hpp:32-46) plus B200 options.  No option changes a
+ * single result bit except the sketch parameters (bucket_bits,
+ * register_bits, seed) and the termination rule, exactly as in the
+ * reference (README.md:117-120). */
+typedef struct {
+  uint32_t bucket_bits;       /* b, m = 2^b registers (default 7) */
+  uint32_t register_bits;     /* r; 0 = 5 below 2^32 nodes, else 6 (engine.hpp:79-80) */
+  uint64_t seed;              /* hash seed */
+  uint32_t threads;           /* CPU scheduling knob; accepted and ignored */
+  uint64_t task_size;         /* CPU scheduling knob; accepted and ignored */
+  double systolic_threshold;  /* (0, 1], default 0.25 */
+  int32_t termination;        /* 0 stabilisation, 1 threshold */
+  double eps_inc;             /* threshold mode: relative increment floor */
+  uint64_t max_iterations;    /* 0 = n + 1 */
+  int32_t spill_to_disk;      /* accepted and ignored: HBM holds both generations */
+  int32_t track_modified;     /* skip unmodified successors (time only) */
+  int32_t use_systolic;       /* worklist bookkeeping (time only) */
+  /* --- B200 options ---------------------------------------------------- */
+  int32_t device;             /* CUDA device ordinal (default 0) */
+  int32_t exact_sum;          /* 1 (default): N(t) total summed on the host in the
+                                 reference's order -> bit-identical to
+                                 engine.hpp:115-117; 0: deterministic device tree */
+  uint64_t shard_begin;       /* node range [shard_begin, shard_end) this engine */
+  uint64_t shard_end;         /* updates; (0, 0) = all nodes (single GPU) */
+} hanf_config;
+
+/* IterationReport (engine.hpp:48-51) */
+typedef struct {
+  double sum;
+  uint64_t modified;
+} hanf_iteration_report;
+
+/* SketchParams (hll.hpp:36-70) */
+typedef struct {
+  uint32_t bucket_bits;
+  uint32_t registers;
+  uint32_t register_bits;
+  uint32_t words_per_counter; /* W = ceil(m*r/64), hll.hpp:58-60 */
+  double alpha;               /* hll.hpp:27-34 */
+  uint64_t seed;
+} hanf_sketch_params;
+
+/* ---- configuration ------------------------------------------------------ */
+/* EngineConfig{} defaults (engine.hpp:32-46) + B200 defaults. */
+hanf_status hanf_config_init(hanf_config* cfg);
+/* SketchParams::make (hll.hpp:43-56): validates b in [4,20], r in [5,8]. */
+hanf_status hanf_sketch_params_make(uint32_t bucket_bits, uint64_t seed,
+                                    uint32_t register_bits,
+                                    hanf_sketch_params* out);
+
+/* ---- engine lifecycle ------------------------------------------------- */
+/* NfEngine::NfEngine(const Graph&, EngineConfig) (engine.hpp:70-90):
+ * validates the config, uploads the CSR to HBM, seeds counter v with item
+ * v under `seed` (engine.hpp:84-85) on the device. */
+hanf_status hanf_create(const hanf_graph_view* graph, const hanf_config* cfg,
+                        hanf_engine** out);
+void hanf_destroy(hanf_engine* engine);
+/* Re-seeds the counters and rewinds to iteration 0 (a fresh NfEngine on
+ * the same graph, without re-uploading it). */
+hanf_status hanf_reset(hanf_engine* engine);
+
+/* ---- the hot path -------------------------------------------------------- */
+/* NfEngine::sum_estimates() (engine.hpp:100-118). */
+hanf_status hanf_sum_estimates(hanf_engine* engine, double* sum);
+/* NfEngine::step() (engine.hpp:122-228): one iteration; counters become
+ * the register-wise max over each node and its successors. */
+hanf_status hanf_step(hanf_engine* engine, hanf_iteration_report* report);
+/* NfEngine::run_to_stabilisation() (engine.hpp:233-275).  values/modified
+ * receive N(0..T) and modified(0..T) (T+1 entries, clamped non-decreasing);
+ * HANF_CAPACITY if capacity < T+1 (length still reports T+1);
+ * HANF_GUARD when the iteration cap is exceeded. */
+hanf_status hanf_run_to_stabilisation(hanf_engine* engine, double* values,
+                                      uint64_t* modified, uint64_t capacity,
+                                      uint64_t* length, double* wall_seconds);
+/* Copies the N(t)/modified vectors of the last run_to_stabilisation (the
+ * engine keeps them, so a HANF_CAPACITY result can be fetched in full). */
+hanf_status hanf_last_result(const hanf_engine* engine, double* values,
+                             uint64_t* modified, uint64_t capacity,
+                             uint64_t* length);
+/* estimate_nf(const Graph&, const EngineConfig&) (engine.hpp:295-298). */
+hanf_status hanf_estimate_nf(const hanf_graph_view* graph, const hanf_config* cfg,
+                             double* values, uint64_t* modified,
+                             uint64_t capacity, uint64_t* length,
+                             double* wall_seconds);
+
+/* ---- accessors ----------------------------------------------------------- */
+/* NfEngine::counters() (engine.hpp:94) -> CounterArray::data() (hll.hpp:224):
+ * copies counters [first, first+count) in the reference packing (W u64
+ * words each) to dst.  HANF_OUT_OF_RANGE past n. */
+hanf_status hanf_read_counters(hanf_engine* engine, uint64_t first,
+                               uint64_t count, uint64_t* dst);
+hanf_status hanf_params(const hanf_engine* engine, hanf_sketch_params* out); /* :92 */
+hanf_status hanf_iteration(const hanf_engine* engine, uint64_t* t);          /* :95 */
+hanf_status hanf_systolic_active(const hanf_engine* engine, int32_t* active); /* :96 */
+hanf_status hanf_num_nodes(const hanf_engine* engine, uint64_t* n);
+/* Thread-local message of the last failing call on this thread. */
+const char* hanf_last_error(void);
+
+/* ---- device plumbing (bench, multi-GPU orchestration) -------------------- */
+/* cudaStream_t the engine launches on (as void*). */
+hanf_status hanf_stream(const hanf_engine* engine, void** stream);
+/* Kernels launched by this engine since creation. */
+hanf_status hanf_launch_count(const hanf_engine* engine, uint64_t* launches);
+/* Device buffers of the engine, for collectives over the node shards. */
+typedef struct {
+  void* next_counters;     /* u64[n*W]: the generation being written by step */
+  void* next_modified;     /* u64[ceil(n/64)] bitmap of counters changed by step */
+  void* block_sums;        /* f64[ceil(n/64)] per-64-counter estimate sums */
+  uint64_t words_per_counter;
+  uint64_t blocks;         /* ceil(n/64) */
+  uint64_t shard_begin, shard_end; /* node range updated by this engine */
+} hanf_buffers;
+hanf_status hanf_device_buffers(hanf_engine* engine, hanf_buffers* out);
+/* Sharded step, phase 1: compute this engine's node range into the next
+ * generation (device-side; returns immediately, stream-ordered). */
+hanf_status hanf_shard_compute(hanf_engine* engine);
+/* Sharded step, phase 2 (after the next-generation shards, modified bitmap
+ * and block sums of every rank have been exchanged into this engine's
+ * buffers): swap generations and produce the IterationReport. */
+hanf_status hanf_shard_commit(hanf_engine* engine, hanf_iteration_report* report);
+
+/* ---- stats.hpp (host arithmetic on N(t)) ---------------------------------- */
+/* cdf_from_nf + distribution_from_cdf (stats.hpp:33-60). */
+hanf_status hanf_distance_distribution(const double* nf, uint64_t length,
+                                       double* mean, double* variance,
+                                       double* spid);
+/* effective_diameter (stats.hpp:65-77). */
+hanf_status hanf_effective_diameter(const double* nf, uint64_t length,
+                                    double alpha, int32_t interpolated,
+                                    double* out);
+
+/* ---- graphs: CSR construction, generators, HBG1 ----------------------------- */
+/* Graph::from_edges (graph.hpp:29-44): sort + dedupe; ids must be < n. */
+hanf_status hanf_graph_from_edges(uint64_t n, const uint32_t* src,
+                                  const uint32_t* dst, uint64_t count,
+                                  hanf_graph** out);
+/* Reference fixtures: gen_uniform_random (graph.hpp:262-285) and
+ * gen_clique_path (graph.hpp:238-258), same bits. */
+hanf_status hanf_gen_uniform_random(uint64_t n, double d, uint64_t seed,
+                                    hanf_graph** out);
+hanf_status hanf_gen_clique_path(uint64_t k, uint64_t l, hanf_graph** out);
+/* BASELINE.json synthetic configs. */
+hanf_status hanf_gen_erdos_renyi(uint64_t n, double mean_degree, uint64_t seed,
+                                 hanf_graph** out);
+hanf_status hanf_gen_rmat(uint32_t scale, uint32_t edge_factor, double a,
+                          double b, double c, uint64_t seed,
+                          uint64_t permute_seed, hanf_graph** out);
+hanf_status hanf_gen_copying(uint64_t n, double exponent, double mean_degree,
+                             uint64_t max_degree, double copy_prob,
+                             uint64_t window, uint64_t seed, hanf_graph** out);
+hanf_status hanf_gen_barabasi_albert(uint64_t n, uint32_t m, uint64_t seed,
+                                     uint64_t permute_seed, hanf_graph** out);
+/* transpose (graph.hpp:72-84). */
+hanf_status hanf_graph_transpose(const hanf_graph* g, hanf_graph** out);
+/* HBG1 CSR cache (graph.hpp:178-218, FORMATS.md:13-23). */
+hanf_status hanf_graph_save_csr(const hanf_graph* g, const char* path);
+hanf_status hanf_graph_load_csr(const char* path, hanf_graph** out);
+hanf_status hanf_graph_view_of(const hanf_graph* g, hanf_graph_view* view);
+void hanf_graph_free(hanf_graph* g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HANF_H */

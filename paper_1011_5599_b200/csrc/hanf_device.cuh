@@ -1,0 +1,347 @@
+// hanf_device.cuh -- register layout, broadword max and estimator for sm_100a.
+//
+// Counters keep the reference packing bit for bit (hll.hpp:19-22, 183-240;
+// FORMATS.md:25-41): counter i = u64 words [i*W, (i+1)*W), register j =
+// bits [j*r, (j+1)*r) from the LSB of word 0, straddling words, padding 0.
+//
+// On the GPU the words are handled as 32-bit limbs (the native ALU width).
+// A counter is processed in "chunks": a chunk is a whole lcm(64, r)-bit
+// period of the packing (or the whole counter when it is shorter), so the
+// per-limb high/low register masks are compile-time immediates and chunks
+// are independent of each other.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+
+namespace hanf {
+
+template <int I>
+using ic = std::integral_constant<int, I>;
+
+// Compile-time loop: f(ic<B>{}), ..., f(ic<E-1>{}).
+template <int B, int E, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+  if constexpr (B < E) {
+    f(ic<B>{});
+    sfor<B + 1, E>(f);
+  }
+}
+
+// Register layout of one chunk: NREG registers of R bits.
+template <int R, int NREG>
+struct Layout {
+  static constexpr int kR = R;
+  static constexpr int kNReg = NREG;
+  static constexpr int kBits = NREG * R;
+  static constexpr int kLimbs = (kBits + 31) / 32;  // limbs holding register bits
+  static constexpr int kWords = (kBits + 63) / 64;  // storage words of the chunk
+  static constexpr uint32_t kMul = (1u << R) - 1;   // lane spread multiplier
+
+  // High bit of every register that falls in limb i (PackedMax's H,
+  // broadword.hpp:81-86, restated per 32-bit limb).
+  __host__ __device__ static constexpr uint32_t high(int i) {
+    uint32_t m = 0;
+    for (int j = 0; j < NREG; ++j) {
+      const int hb = j * R + R - 1;
+      if (hb >= 32 * i && hb < 32 * i + 32) m |= 1u << (hb - 32 * i);
+    }
+    return m;
+  }
+  // Does a register straddle the boundary between limb i-1 and limb i?
+  // Only there can a borrow cross limbs: every other register has its
+  // minuend high bit forced (broadword.hpp:23-25).
+  __host__ __device__ static constexpr bool straddle(int i) {
+    return i > 0 && i < kLimbs && (32 * i) % R != 0;
+  }
+  // End (exclusive) of the borrow chain starting at limb s.
+  __host__ __device__ static constexpr int chain_end(int s) {
+    int e = s + 1;
+    while (e < kLimbs && straddle(e)) ++e;
+    return e;
+  }
+};
+
+// d[S..S+N) = a[S..S+N) - b[S..S+N) as one multi-precision number (borrow
+// chain in the carry flag).  One asm statement per chain so nothing can
+// clobber the flag between links.
+template <int S, int N, int L>
+__device__ __forceinline__ void sub_chain(uint32_t (&d)[L], const uint32_t (&a)[L],
+                                          const uint32_t (&b)[L]) {
+  static_assert(N >= 1 && N <= 7, "chain length");
+  if constexpr (N == 1) {
+    d[S] = a[S] - b[S];
+  } else if constexpr (N == 2) {
+    asm("sub.cc.u32 %0, %2, %4;\n\tsubc.u32 %1, %3, %5;"
+        : "=r"(d[S]), "=r"(d[S + 1])
+        : "r"(a[S]), "r"(a[S + 1]), "r"(b[S]), "r"(b[S + 1]));
+  } else if constexpr (N == 3) {
+    asm("sub.cc.u32 %0, %3, %6;\n\tsubc.cc.u32 %1, %4, %7;\n\tsubc.u32 %2, %5, %8;"
+        : "=r"(d[S]), "=r"(d[S + 1]), "=r"(d[S + 2])
+        : "r"(a[S]), "r"(a[S + 1]), "r"(a[S + 2]), "r"(b[S]), "r"(b[S + 1]),
+          "r"(b[S + 2]));
+  } else if constexpr (N == 4) {
+    asm("sub.cc.u32 %0, %4, %8;\n\tsubc.cc.u32 %1, %5, %9;\n\t"
+        "subc.cc.u32 %2, %6, %10;\n\tsubc.u32 %3, %7, %11;"
+        : "=r"(d[S]), "=r"(d[S + 1]), "=r"(d[S + 2]), "=r"(d[S + 3])
+        : "r"(a[S]), "r"(a[S + 1]), "r"(a[S + 2]), "r"(a[S + 3]), "r"(b[S]),
+          "r"(b[S + 1]), "r"(b[S + 2]), "r"(b[S + 3]));
+  } else if constexpr (N == 5) {
+    asm("sub.cc.u32 %0, %5, %10;\n\tsubc.cc.u32 %1, %6, %11;\n\t"
+        "subc.cc.u32 %2, %7, %12;\n\tsubc.cc.u32 %3, %8, %13;\n\t"
+        "subc.u32 %4, %9, %14;"
+        : "=r"(d[S]), "=r"(d[S + 1]), "=r"(d[S + 2]), "=r"(d[S + 3]), "=r"(d[S + 4])
+        : "r"(a[S]), "r"(a[S + 1]), "r"(a[S + 2]), "r"(a[S + 3]), "r"(a[S + 4]),
+          "r"(b[S]), "r"(b[S + 1]), "r"(b[S + 2]), "r"(b[S + 3]), "r"(b[S + 4]));
+  } else if constexpr (N == 6) {
+    asm("sub.cc.u32 %0, %6, %12;\n\tsubc.cc.u32 %1, %7, %13;\n\t"
+        "subc.cc.u32 %2, %8, %14;\n\tsubc.cc.u32 %3, %9, %15;\n\t"
+        "subc.cc.u32 %4, %10, %16;\n\tsubc.u32 %5, %11, %17;"
+        : "=r"(d[S]), "=r"(d[S + 1]), "=r"(d[S + 2]), "=r"(d[S + 3]), "=r"(d[S + 4]),
+          "=r"(d[S + 5])
+        : "r"(a[S]), "r"(a[S + 1]), "r"(a[S + 2]), "r"(a[S + 3]), "r"(a[S + 4]),
+          "r"(a[S + 5]), "r"(b[S]), "r"(b[S + 1]), "r"(b[S + 2]), "r"(b[S + 3]),
+          "r"(b[S + 4]), "r"(b[S + 5]));
+  } else {
+    asm("sub.cc.u32 %0, %7, %14;\n\tsubc.cc.u32 %1, %8, %15;\n\t"
+        "subc.cc.u32 %2, %9, %16;\n\tsubc.cc.u32 %3, %10, %17;\n\t"
+        "subc.cc.u32 %4, %11, %18;\n\tsubc.cc.u32 %5, %12, %19;\n\t"
+        "subc.u32 %6, %13, %20;"
+        : "=r"(d[S]), "=r"(d[S + 1]), "=r"(d[S + 2]), "=r"(d[S + 3]), "=r"(d[S + 4]),
+          "=r"(d[S + 5]), "=r"(d[S + 6])
+        : "r"(a[S]), "r"(a[S + 1]), "r"(a[S + 2]), "r"(a[S + 3]), "r"(a[S + 4]),
+          "r"(a[S + 5]), "r"(a[S + 6]), "r"(b[S]), "r"(b[S + 1]), "r"(b[S + 2]),
+          "r"(b[S + 3]), "r"(b[S + 4]), "r"(b[S + 5]), "r"(b[S + 6]));
+  }
+}
+
+template <class Lay, int S, int L>
+__device__ __forceinline__ void sub_chains(uint32_t (&d)[L], const uint32_t (&a)[L],
+                                           const uint32_t (&b)[L]) {
+  if constexpr (S < Lay::kLimbs) {
+    constexpr int E = Lay::chain_end(S);
+    sub_chain<S, E - S>(d, a, b);
+    sub_chains<Lay, E>(d, a, b);
+  }
+}
+
+// x <- register-wise max(x, y) over one chunk (the semantics of
+// PackedMax::max_into, broadword.hpp:94-130).
+//
+// Pass 1 is the reference's comparison: lt = high bit of every lane where
+// x < y, from d = (x|H) - (y&~H) with the borrow rippling only through
+// straddling registers.  Pass 2 spreads each lt bit over its r-bit lane
+// with one 32x32->64 multiply by (2^r - 1) of the lane's low bit (the high
+// half carries straddling lanes into the next limb), replacing the
+// reference's second borrow chain; the select is one LOP3.
+template <class Lay>
+__device__ __forceinline__ void swar_max(uint32_t (&x)[Lay::kLimbs],
+                                         const uint32_t (&y)[Lay::kLimbs]) {
+  constexpr int NL = Lay::kLimbs;
+  constexpr int R = Lay::kR;
+  uint32_t a[NL], b[NL], d[NL], lt[NL];
+  sfor<0, NL>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    constexpr uint32_t H = Lay::high(i);
+    a[i] = x[i] | H;
+    b[i] = y[i] & ~H;
+  });
+  sub_chains<Lay, 0>(d, a, b);
+  sfor<0, NL>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    constexpr uint32_t H = Lay::high(i);
+    lt[i] = ((d[i] | (x[i] ^ y[i])) ^ (x[i] | ~y[i])) & H;
+  });
+  uint32_t carry = 0;
+  sfor<0, NL>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    uint32_t u;
+    if constexpr (i + 1 < NL)
+      u = __funnelshift_r(lt[i], lt[i + 1], R - 1);
+    else
+      u = lt[i] >> (R - 1);
+    const uint64_t w = static_cast<uint64_t>(u) * Lay::kMul;
+    const uint32_t spread = static_cast<uint32_t>(w) | carry;
+    carry = static_cast<uint32_t>(w >> 32);
+    x[i] = (x[i] & ~spread) | (y[i] & spread);
+  });
+}
+
+// Loads one chunk (Lay::kWords u64 words at p) into limbs; padding limbs
+// beyond kLimbs are dropped (they are zero by the layout contract).
+template <class Lay, bool kVec16>
+__device__ __forceinline__ void load_chunk(uint32_t (&v)[Lay::kLimbs], const uint64_t* p) {
+  constexpr int NW = Lay::kWords;
+  constexpr int NL = Lay::kLimbs;
+  if constexpr (kVec16 && NW % 2 == 0) {
+    sfor<0, NW / 2>([&](auto I) {
+      constexpr int k = decltype(I)::value;
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(p) + k);
+      if constexpr (4 * k + 0 < NL) v[4 * k + 0] = q.x;
+      if constexpr (4 * k + 1 < NL) v[4 * k + 1] = q.y;
+      if constexpr (4 * k + 2 < NL) v[4 * k + 2] = q.z;
+      if constexpr (4 * k + 3 < NL) v[4 * k + 3] = q.w;
+    });
+  } else {
+    sfor<0, NW>([&](auto I) {
+      constexpr int k = decltype(I)::value;
+      const uint2 q = __ldg(reinterpret_cast<const uint2*>(p) + k);
+      if constexpr (2 * k + 0 < NL) v[2 * k + 0] = q.x;
+      if constexpr (2 * k + 1 < NL) v[2 * k + 1] = q.y;
+    });
+  }
+}
+
+// Same, through the coherent path (data written earlier in this kernel).
+template <class Lay>
+__device__ __forceinline__ void load_chunk_coherent(uint32_t (&v)[Lay::kLimbs],
+                                                    const uint64_t* p) {
+  constexpr int NW = Lay::kWords;
+  constexpr int NL = Lay::kLimbs;
+  sfor<0, NW>([&](auto I) {
+    constexpr int k = decltype(I)::value;
+    const uint64_t q = __ldcg(p + k);
+    if constexpr (2 * k + 0 < NL) v[2 * k + 0] = static_cast<uint32_t>(q);
+    if constexpr (2 * k + 1 < NL) v[2 * k + 1] = static_cast<uint32_t>(q >> 32);
+  });
+}
+
+template <class Lay, bool kVec16>
+__device__ __forceinline__ void store_chunk(uint64_t* p, const uint32_t (&v)[Lay::kLimbs]) {
+  constexpr int NW = Lay::kWords;
+  constexpr int NL = Lay::kLimbs;
+  auto limb = [&](auto I) -> uint32_t {
+    constexpr int i = decltype(I)::value;
+    if constexpr (i < NL) return v[i]; else return 0u;
+  };
+  if constexpr (kVec16 && NW % 2 == 0) {
+    sfor<0, NW / 2>([&](auto I) {
+      constexpr int k = decltype(I)::value;
+      uint4 q;
+      q.x = limb(ic<4 * k + 0>{});
+      q.y = limb(ic<4 * k + 1>{});
+      q.z = limb(ic<4 * k + 2>{});
+      q.w = limb(ic<4 * k + 3>{});
+      reinterpret_cast<uint4*>(p)[k] = q;
+    });
+  } else {
+    sfor<0, NW>([&](auto I) {
+      constexpr int k = decltype(I)::value;
+      uint2 q;
+      q.x = limb(ic<2 * k + 0>{});
+      q.y = limb(ic<2 * k + 1>{});
+      reinterpret_cast<uint2*>(p)[k] = q;
+    });
+  }
+}
+
+template <class Lay>
+__device__ __forceinline__ bool limbs_differ(const uint32_t (&x)[Lay::kLimbs],
+                                             const uint32_t (&y)[Lay::kLimbs]) {
+  uint32_t diff = 0;
+  sfor<0, Lay::kLimbs>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    diff |= x[i] ^ y[i];
+  });
+  return diff != 0;
+}
+
+template <class Lay>
+__device__ __forceinline__ void shfl_max(uint32_t (&x)[Lay::kLimbs], int offset) {
+  uint32_t y[Lay::kLimbs];
+  sfor<0, Lay::kLimbs>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    y[i] = __shfl_xor_sync(0xffffffffu, x[i], offset);
+  });
+  swar_max<Lay>(x, y);
+}
+
+// ---------------------------------------------------------------------------
+// Estimator (counter_estimate, hll.hpp:122-141), bit-exact.
+//
+// r = 5: every term 2^-M of the reference's harmonic sum is a multiple of
+// 2^-31 and there are at most 2^20 of them, so the sequential double sum is
+// exact and equals S * 2^-31 with the integer S = sum 2^(31-M) (< 2^51).
+// r >= 6: terms go down to 2^-61, so the reference's rounding sequence is
+// replayed with sequential double adds in register order.
+// raw = ((alpha*m)*m)/harmonic with IEEE round-to-nearest operations, and
+// linear counting m*log(m/z) comes from a host table built with the same
+// libm call as the reference (log_table[z], z = 1..m).
+// ---------------------------------------------------------------------------
+struct EstimateParams {
+  double alpha;
+  double m;       // registers, as double
+  uint32_t registers;
+  uint32_t register_bits;
+  uint32_t words;
+  const double* log_table;  // [m+1]
+};
+
+__device__ __forceinline__ uint32_t read_register(const uint64_t* c, uint32_t r, uint32_t j) {
+  const uint32_t bit = j * r;
+  const uint32_t word = bit >> 6;
+  const uint32_t off = bit & 63;
+  uint64_t v = c[word] >> off;
+  if (off + r > 64) v |= c[word + 1] << (64 - off);
+  return static_cast<uint32_t>(v) & ((1u << r) - 1);
+}
+
+__device__ __forceinline__ double finish_estimate(const EstimateParams& p, double harmonic,
+                                                  uint32_t zeros) {
+  const double raw = __ddiv_rn(__dmul_rn(__dmul_rn(p.alpha, p.m), p.m), harmonic);
+  if (raw <= __dmul_rn(2.5, p.m) && zeros > 0) return p.log_table[zeros];
+  return raw;
+}
+
+// Generic path: any (m, r) the reference accepts.
+__device__ inline double estimate_counter_generic(const uint64_t* c, const EstimateParams& p) {
+  uint32_t zeros = 0;
+  if (p.register_bits == 5) {
+    uint64_t s = 0;
+    for (uint32_t j = 0; j < p.registers; ++j) {
+      const uint32_t reg = read_register(c, 5, j);
+      s += 1ull << (31 - reg);
+      zeros += reg == 0;
+    }
+    return finish_estimate(p, __dmul_rn(static_cast<double>(s), 0x1p-31), zeros);
+  }
+  double harmonic = 0.0;
+  for (uint32_t j = 0; j < p.registers; ++j) {
+    const uint32_t reg = read_register(c, p.register_bits, j);
+    harmonic = __dadd_rn(harmonic, __longlong_as_double(static_cast<long long>(1023 - reg) << 52));
+    zeros += reg == 0;
+  }
+  return finish_estimate(p, harmonic, zeros);
+}
+
+// Fast path for r = 5 with a compile-time register count: the counter is
+// read as 32-bit limbs and every register is extracted with one funnel
+// shift; 2^(31-M) is one wrapping funnel shift of 0x80000000.
+template <int M>
+__device__ __forceinline__ double estimate_counter_r5(const uint64_t* c, const EstimateParams& p) {
+  constexpr int kLimbs = (M * 5 + 31) / 32;
+  constexpr int kWords = (M * 5 + 63) / 64;
+  uint32_t v[kLimbs + 1];
+  sfor<0, kWords>([&](auto I) {
+    constexpr int k = decltype(I)::value;
+    const uint64_t q = c[k];
+    if constexpr (2 * k < kLimbs + 1) v[2 * k] = static_cast<uint32_t>(q);
+    if constexpr (2 * k + 1 < kLimbs + 1) v[2 * k + 1] = static_cast<uint32_t>(q >> 32);
+  });
+  if constexpr (2 * kWords < kLimbs + 1) v[kLimbs] = 0;
+  uint64_t s = 0;
+  uint32_t zeros = 0;
+  sfor<0, M>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    constexpr int bit = j * 5;
+    constexpr int limb = bit / 32;
+    constexpr int off = bit % 32;
+    const uint32_t raw = __funnelshift_r(v[limb], v[limb + 1], off);  // low 5 bits = M_j
+    const uint32_t term = __funnelshift_r(0x80000000u, 0u, raw);  // 2^(31 - M_j), shift mod 32
+    s += term;
+    zeros += term >> 31;
+  });
+  return finish_estimate(p, __dmul_rn(static_cast<double>(s), 0x1p-31), zeros);
+}
+
+}  // namespace hanf

@@ -1,0 +1,709 @@
+// hanf_engine.cu -- host engine behind the C-ABI (include/hanf.h).
+//
+// Restates the NfEngine surface (engine.hpp:68-298) over device state:
+//   - CSR of the node range this engine updates, resident in HBM;
+//   - two counter generations (reference packing, hll.hpp:183-240);
+//   - two "modified" bitmaps (bit v <-> modified_[v], engine.hpp:287), word
+//     i of which is exactly the dirty flag of 64-counter block i (:206);
+//   - cached per-counter estimates and per-block sums (engine.hpp:288).
+// The union/estimate/reduce kernels live in hanf_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <iostream>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/hanf.h"
+#include "hanf_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+hanf_status fail(hanf_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+hanf_status cuda_fail(cudaError_t e, const char* what) {
+  const hanf_status st =
+      e == cudaErrorMemoryAllocation ? HANF_OUT_OF_MEMORY : HANF_CUDA_ERROR;
+  return fail(st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define HANF_CUDA(expr)                                   \
+  do {                                                    \
+    const cudaError_t _e = (expr);                        \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr);   \
+  } while (0)
+
+// hll.hpp:27-34
+double alpha_for_registers(unsigned m) {
+  switch (m) {
+    case 16: return 0.673;
+    case 32: return 0.697;
+    case 64: return 0.709;
+    default: return 0.7213 / (1.0 + 1.079 / static_cast<double>(m));
+  }
+}
+
+// SketchParams::make, hll.hpp:43-56 (same messages)
+hanf_status make_params(uint32_t b, uint64_t seed, uint32_t r, hanf_sketch_params* p) {
+  if (b < 4 || b > 20) return fail(HANF_INVALID_ARGUMENT, "bucket bits must be in [4, 20]");
+  if (r < 5 || r > 8) return fail(HANF_INVALID_ARGUMENT, "register width must be in [5, 8]");
+  p->bucket_bits = b;
+  p->registers = 1u << b;
+  p->register_bits = r;
+  p->words_per_counter = (p->registers * r + 63) / 64;
+  p->alpha = alpha_for_registers(p->registers);
+  p->seed = seed;
+  return HANF_OK;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  cudaError_t alloc(size_t n) {
+    count = n;
+    return cudaMalloc(&p, sizeof(T) * (n ? n : 1));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+};
+
+}  // namespace
+
+namespace hanf_host_detail {
+void set_error(const std::string& s) { g_last_error = s; }
+}  // namespace hanf_host_detail
+
+struct hanf_engine {
+  hanf_config cfg{};
+  hanf_sketch_params params{};
+  uint64_t n = 0;
+  uint64_t lo = 0, hi = 0;   // node shard [lo, hi)
+  uint64_t blocks = 0;       // ceil(n / 64)
+  uint64_t words = 0;        // W
+  int device = 0;
+  cudaStream_t stream = nullptr;
+
+  DevBuf<uint64_t> offsets;  // offsets[lo..hi] (absolute arc indices)
+  DevBuf<uint32_t> succ;     // arcs [offsets[lo], offsets[hi])
+  uint64_t succ_base = 0;
+  DevBuf<uint64_t> cnt[2];
+  DevBuf<uint64_t> mod[2];
+  DevBuf<double> est;
+  DevBuf<double> block_sums;
+  DevBuf<double> log_table;
+  DevBuf<uint32_t> order;
+  DevBuf<uint32_t> hub_node;
+  DevBuf<uint64_t> hub_begin, hub_end;
+  DevBuf<uint64_t> partials;
+  DevBuf<uint32_t> hub_nodes, hub_first, hub_count;
+  DevBuf<hanf::ReduceOut> reduce;
+  hanf::TaskTable tasks{};
+  uint32_t num_hubs = 0;
+
+  hanf::ReduceOut* h_reduce = nullptr;  // pinned: total + count
+  double* h_block_sums = nullptr;       // pinned: exact_sum mode
+
+  int cur = 0;               // index of the current generation
+  uint64_t t = 0;            // iteration()
+  bool stale_valid = false;  // next[v] may lag where mod[cur] is set
+  bool systolic = false;     // systolic_active(), engine.hpp:210-216
+  double last_sum = 0.0;     // sum_estimates() of the current generation
+  std::vector<double> result_values;      // last run_to_stabilisation
+  std::vector<uint64_t> result_modified;
+  uint64_t launches = 0;
+
+  ~hanf_engine() {
+    if (device >= 0) cudaSetDevice(device);
+    offsets.free(); succ.free();
+    for (int i = 0; i < 2; ++i) { cnt[i].free(); mod[i].free(); }
+    est.free(); block_sums.free(); log_table.free(); order.free();
+    hub_node.free(); hub_begin.free(); hub_end.free(); partials.free();
+    hub_nodes.free(); hub_first.free(); hub_count.free(); reduce.free();
+    if (h_reduce) cudaFreeHost(h_reduce);
+    if (h_block_sums) cudaFreeHost(h_block_sums);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+// Builds the warp-task table of the union kernel for nodes [lo, hi):
+// class 0 = hub chunks, classes 1..6 = G = 32..1 lanes per node, nodes in
+// descending out-degree (stable in node id).  Degree-0 nodes get no task:
+// their counter never changes and both generations hold it from seeding.
+hanf_status build_tasks(hanf_engine* e, const uint64_t* offsets) {
+  const uint64_t lo = e->lo, hi = e->hi;
+  const uint32_t maxd = hanf::kHubDegree;
+  std::vector<uint64_t> hist(maxd + 2, 0);
+  uint64_t hub_chunks = 0, hubs = 0;
+  for (uint64_t v = lo; v < hi; ++v) {
+    const uint64_t d = offsets[v + 1] - offsets[v];
+    if (d == 0) continue;
+    if (d > maxd) {
+      ++hubs;
+      hub_chunks += (d + hanf::kHubChunk - 1) / hanf::kHubChunk;
+    } else {
+      ++hist[d];
+    }
+  }
+  auto log2g_of = [](uint64_t d) {
+    uint32_t g = 0;
+    while ((32ull << g) < d) ++g;  // G = 2^g lanes, each <= 32 arcs
+    return g;
+  };
+  // class c (1..6) <-> log2g = 6 - c
+  uint64_t class_count[hanf::kNumClasses] = {};
+  for (uint64_t d = 1; d <= maxd; ++d) class_count[6 - log2g_of(d)] += hist[d];
+  // positions: descending degree => classes 1..6 in order, degrees high->low
+  std::vector<uint64_t> pos(maxd + 2, 0);
+  uint64_t p = 0;
+  for (uint64_t d = maxd; d >= 1; --d) {
+    pos[d] = p;
+    p += hist[d];
+  }
+  const uint64_t light = p;
+  std::vector<uint32_t> order(light ? light : 1);
+  std::vector<uint32_t> hub_node(hub_chunks ? hub_chunks : 1);
+  std::vector<uint64_t> hub_begin(hub_chunks ? hub_chunks : 1), hub_end(hub_chunks ? hub_chunks : 1);
+  std::vector<uint32_t> hubs_v(hubs ? hubs : 1), hubs_first(hubs ? hubs : 1), hubs_count(hubs ? hubs : 1);
+  // hubs in descending degree too
+  std::vector<std::pair<uint64_t, uint32_t>> hub_list;
+  hub_list.reserve(hubs);
+  for (uint64_t v = lo; v < hi; ++v) {
+    const uint64_t d = offsets[v + 1] - offsets[v];
+    if (d == 0) continue;
+    if (d > maxd)
+      hub_list.emplace_back(d, static_cast<uint32_t>(v));
+    else
+      order[pos[d]++] = static_cast<uint32_t>(v);
+  }
+  std::stable_sort(hub_list.begin(), hub_list.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  uint64_t c = 0;
+  for (uint64_t h = 0; h < hub_list.size(); ++h) {
+    const uint32_t v = hub_list[h].second;
+    const uint64_t s = offsets[v], en = offsets[v + 1];
+    hubs_v[h] = v;
+    hubs_first[h] = static_cast<uint32_t>(c);
+    uint32_t k = 0;
+    for (uint64_t a = s; a < en; a += hanf::kHubChunk, ++k, ++c) {
+      hub_node[c] = v;
+      hub_begin[c] = a;
+      hub_end[c] = std::min<uint64_t>(en, a + hanf::kHubChunk);
+    }
+    hubs_count[h] = k;
+  }
+  if (light > 0xffffffffull || hub_chunks > 0xffffffffull)
+    return fail(HANF_INVALID_ARGUMENT, "too many nodes in one engine shard");
+
+  hanf::TaskTable& tt = e->tasks;
+  uint64_t warps = 0, items = 0;
+  tt.warp_begin[0] = 0;
+  tt.item_begin[0] = 0;
+  tt.item_end[0] = static_cast<uint32_t>(hub_chunks);
+  tt.log2g[0] = 5;
+  warps += hub_chunks;
+  for (int k = 1; k < hanf::kNumClasses; ++k) {
+    const uint32_t lg = 6 - k;
+    tt.log2g[k] = lg;
+    tt.warp_begin[k] = static_cast<uint32_t>(warps);
+    tt.item_begin[k] = static_cast<uint32_t>(items);
+    items += class_count[k];
+    tt.item_end[k] = static_cast<uint32_t>(items);
+    const uint64_t per = 32u >> lg;
+    warps += (class_count[k] + per - 1) / per;
+  }
+  if (warps > 0x7fffffffull / 32) return fail(HANF_INVALID_ARGUMENT, "task table overflow");
+  tt.warp_begin[hanf::kNumClasses] = static_cast<uint32_t>(warps);
+  e->num_hubs = static_cast<uint32_t>(hubs);
+
+  cudaStream_t s = e->stream;
+  HANF_CUDA(e->order.alloc(order.size()));
+  HANF_CUDA(cudaMemcpyAsync(e->order.p, order.data(), sizeof(uint32_t) * order.size(),
+                            cudaMemcpyHostToDevice, s));
+  HANF_CUDA(e->hub_node.alloc(hub_node.size()));
+  HANF_CUDA(e->hub_begin.alloc(hub_begin.size()));
+  HANF_CUDA(e->hub_end.alloc(hub_end.size()));
+  HANF_CUDA(cudaMemcpyAsync(e->hub_node.p, hub_node.data(), sizeof(uint32_t) * hub_node.size(),
+                            cudaMemcpyHostToDevice, s));
+  HANF_CUDA(cudaMemcpyAsync(e->hub_begin.p, hub_begin.data(), sizeof(uint64_t) * hub_begin.size(),
+                            cudaMemcpyHostToDevice, s));
+  HANF_CUDA(cudaMemcpyAsync(e->hub_end.p, hub_end.data(), sizeof(uint64_t) * hub_end.size(),
+                            cudaMemcpyHostToDevice, s));
+  HANF_CUDA(e->partials.alloc(static_cast<size_t>(hub_chunks ? hub_chunks : 1) * e->words));
+  HANF_CUDA(e->hub_nodes.alloc(hubs_v.size()));
+  HANF_CUDA(e->hub_first.alloc(hubs_first.size()));
+  HANF_CUDA(e->hub_count.alloc(hubs_count.size()));
+  HANF_CUDA(cudaMemcpyAsync(e->hub_nodes.p, hubs_v.data(), sizeof(uint32_t) * hubs_v.size(),
+                            cudaMemcpyHostToDevice, s));
+  HANF_CUDA(cudaMemcpyAsync(e->hub_first.p, hubs_first.data(), sizeof(uint32_t) * hubs_first.size(),
+                            cudaMemcpyHostToDevice, s));
+  HANF_CUDA(cudaMemcpyAsync(e->hub_count.p, hubs_count.data(), sizeof(uint32_t) * hubs_count.size(),
+                            cudaMemcpyHostToDevice, s));
+  return HANF_OK;
+}
+
+// Recomputes estimates of the counters flagged in `dirty` (all when null)
+// for blocks [b0, b1) of generation g.
+hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t b0, uint64_t b1) {
+  hanf::EstimateArgs a{};
+  a.counters = e->cnt[g].p;
+  a.dirty = dirty;
+  a.est = e->est.p;
+  a.block_sums = e->block_sums.p;
+  a.n = e->n;
+  a.block_begin = b0;
+  a.block_end = b1;
+  a.alpha = e->params.alpha;
+  a.m = static_cast<double>(e->params.registers);
+  a.registers = e->params.registers;
+  a.register_bits = e->params.register_bits;
+  a.words = e->params.words_per_counter;
+  a.log_table = e->log_table.p;
+  HANF_CUDA(hanf::launch_estimate(a, e->stream, &e->launches));
+  return HANF_OK;
+}
+
+// Total of the block sums and popcount of bitmap `bits` over all blocks;
+// waits for the stream.  exact_sum: the total is redone on the host in the
+// reference's order (engine.hpp:115-117).
+hanf_status reduce_totals(hanf_engine* e, const uint64_t* bits, double* total, uint64_t* count) {
+  HANF_CUDA(hanf::launch_reduce(e->block_sums.p, bits, 0, e->blocks, e->reduce.p, e->stream,
+                                &e->launches));
+  HANF_CUDA(cudaMemcpyAsync(e->h_reduce, e->reduce.p, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                            e->stream));
+  if (e->cfg.exact_sum)
+    HANF_CUDA(cudaMemcpyAsync(e->h_block_sums, e->block_sums.p, sizeof(double) * e->blocks,
+                              cudaMemcpyDeviceToHost, e->stream));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->cfg.exact_sum) {
+    double s = 0.0;
+    for (uint64_t b = 0; b < e->blocks; ++b) s += e->h_block_sums[b];
+    *total = s;
+  } else {
+    *total = e->h_reduce->total;
+  }
+  *count = e->h_reduce->count;
+  return HANF_OK;
+}
+
+// Seeds both generations (every engine seeds all n counters: seeding is a
+// pure function of (v, seed), so shards need no exchange) and computes N(0).
+hanf_status seed_all(hanf_engine* e) {
+  e->cur = 0;
+  e->t = 0;
+  e->stale_valid = false;
+  e->systolic = false;
+  HANF_CUDA(hanf::launch_seed(e->cnt[0].p, e->cnt[1].p, e->mod[0].p, e->n, 0, e->n,
+                              e->params.bucket_bits, e->params.register_bits,
+                              e->params.words_per_counter, e->params.seed, e->stream,
+                              &e->launches));
+  HANF_CUDA(cudaMemsetAsync(e->mod[1].p, 0, sizeof(uint64_t) * e->blocks, e->stream));
+  hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
+  if (st != HANF_OK) return st;
+  uint64_t count = 0;
+  return reduce_totals(e, e->mod[0].p, &e->last_sum, &count);
+}
+
+hanf_status validate_config(const hanf_config* cfg) {
+  if (cfg->systolic_threshold <= 0.0 || cfg->systolic_threshold > 1.0)
+    return fail(HANF_INVALID_ARGUMENT, "systolic threshold must be in (0, 1]");
+  if (cfg->termination == 1 && cfg->eps_inc <= 0.0)
+    return fail(HANF_INVALID_ARGUMENT, "threshold termination needs eps_inc > 0");
+  if (cfg->termination != 0 && cfg->termination != 1)
+    return fail(HANF_INVALID_ARGUMENT, "termination must be 0 (stabilisation) or 1 (threshold)");
+  return HANF_OK;
+}
+
+hanf_status compute_local(hanf_engine* e) {
+  const int g = e->cur, ng = 1 - e->cur;
+  const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
+  HANF_CUDA(cudaMemsetAsync(e->mod[ng].p + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
+  hanf::UnionArgs a{};
+  a.offsets = e->offsets.p - e->lo;
+  a.succ = e->succ.p;
+  a.succ_base = e->succ_base;
+  a.cur = e->cnt[g].p;
+  a.next = e->cnt[ng].p;
+  a.mod_cur = e->mod[g].p;
+  a.mod_next = e->mod[ng].p;
+  a.order = e->order.p;
+  a.hub_node = e->hub_node.p;
+  a.hub_begin = e->hub_begin.p;
+  a.hub_end = e->hub_end.p;
+  a.partials = e->partials.p;
+  a.words = e->params.words_per_counter;
+  a.check_mod = (e->cfg.track_modified && e->t > 0) ? 1 : 0;
+  a.stale_valid = e->stale_valid ? 1 : 0;
+  a.tasks = e->tasks;
+  HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers, e->stream,
+                               &e->launches));
+  hanf::HubArgs h{};
+  h.cur = a.cur;
+  h.next = a.next;
+  h.mod_cur = a.mod_cur;
+  h.mod_next = a.mod_next;
+  h.hub_nodes = e->hub_nodes.p;
+  h.hub_first = e->hub_first.p;
+  h.hub_count = e->hub_count.p;
+  h.partials = e->partials.p;
+  h.num_hubs = e->num_hubs;
+  h.words = a.words;
+  h.stale_valid = a.stale_valid;
+  HANF_CUDA(hanf::launch_hub_finalize(h, e->params.register_bits, e->params.registers,
+                                      e->stream, &e->launches));
+  return run_estimates(e, ng, e->mod[ng].p, w0, w1);
+}
+
+hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
+  const int ng = 1 - e->cur;
+  double total = 0.0;
+  uint64_t count = 0;
+  const hanf_status st = reduce_totals(e, e->mod[ng].p, &total, &count);
+  if (st != HANF_OK) return st;
+  e->cur = ng;                                     // std::swap, engine.hpp:198-200
+  e->stale_valid = true;
+  if (e->cfg.use_systolic && !e->systolic && count > 0 &&
+      static_cast<double>(count) < e->cfg.systolic_threshold * static_cast<double>(e->n))
+    e->systolic = true;                            // engine.hpp:211-216
+  ++e->t;
+  e->last_sum = total;
+  rep->sum = total;
+  rep->modified = count;
+  return HANF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hanf_last_error(void) { return g_last_error.c_str(); }
+
+hanf_status hanf_config_init(hanf_config* cfg) {
+  if (!cfg) return fail(HANF_INVALID_ARGUMENT, "null config");
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->bucket_bits = 7;          // engine.hpp:33-45
+  cfg->register_bits = 0;
+  cfg->seed = 0;
+  cfg->threads = 1;
+  cfg->task_size = 0;
+  cfg->systolic_threshold = 0.25;
+  cfg->termination = 0;
+  cfg->eps_inc = 0.0;
+  cfg->max_iterations = 0;
+  cfg->spill_to_disk = 0;
+  cfg->track_modified = 1;
+  cfg->use_systolic = 1;
+  cfg->device = 0;
+  cfg->exact_sum = 1;
+  cfg->shard_begin = 0;
+  cfg->shard_end = 0;
+  return HANF_OK;
+}
+
+hanf_status hanf_sketch_params_make(uint32_t b, uint64_t seed, uint32_t r, hanf_sketch_params* out) {
+  if (!out) return fail(HANF_INVALID_ARGUMENT, "null output");
+  return make_params(b, seed, r, out);
+}
+
+hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, hanf_engine** out) {
+  if (!g || !cfg_in || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  hanf_status st = validate_config(cfg_in);
+  if (st != HANF_OK) return st;
+  const uint64_t n = g->n;
+  if (n > (1ull << 32)) return fail(HANF_INVALID_ARGUMENT, "graph too large for 32-bit node ids");
+  if (n > 0 && !g->offsets) return fail(HANF_INVALID_ARGUMENT, "null offsets");
+  if (n > 0 && g->offsets[n] != g->num_arcs)
+    return fail(HANF_INVALID_ARGUMENT, "offsets[n] must equal the arc count");
+  if (g->num_arcs > 0 && !g->arcs) return fail(HANF_INVALID_ARGUMENT, "null arcs");
+
+  hanf_config cfg = *cfg_in;
+  if (cfg.max_iterations == 0) cfg.max_iterations = n + 1;  // engine.hpp:78
+  uint32_t r = cfg.register_bits;
+  if (r == 0) r = n < (1ull << 32) ? 5 : 6;                  // engine.hpp:79-80
+  hanf_sketch_params params;
+  st = make_params(cfg.bucket_bits, cfg.seed, r, &params);
+  if (st != HANF_OK) return st;
+  uint64_t lo = cfg.shard_begin, hi = cfg.shard_end;
+  if (lo == 0 && hi == 0) hi = n;
+  if (lo > hi || hi > n) return fail(HANF_INVALID_ARGUMENT, "shard range outside [0, n]");
+  if ((lo & 63) != 0 || ((hi & 63) != 0 && hi != n))
+    return fail(HANF_INVALID_ARGUMENT, "shard boundaries must be multiples of 64 nodes");
+
+  hanf_engine* e = new (std::nothrow) hanf_engine();
+  if (!e) return fail(HANF_OUT_OF_MEMORY, "engine allocation failed");
+  e->device = cfg.device;
+  e->cfg = cfg;
+  e->params = params;
+  e->n = n;
+  e->lo = lo;
+  e->hi = hi;
+  e->blocks = (n + 63) / 64;
+  e->words = params.words_per_counter;
+
+  auto bail = [&](hanf_status s) {
+    const std::string msg = g_last_error;
+    delete e;
+    g_last_error = msg;
+    return s;
+  };
+#define HANF_TRY(expr)                                                  \
+  do {                                                                  \
+    const cudaError_t _e = (expr);                                      \
+    if (_e != cudaSuccess) return bail(cuda_fail(_e, #expr));           \
+  } while (0)
+
+  HANF_TRY(cudaSetDevice(cfg.device));
+  HANF_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  const uint64_t nw = n * e->words;
+  HANF_TRY(e->cnt[0].alloc(nw));
+  HANF_TRY(e->cnt[1].alloc(nw));
+  HANF_TRY(e->mod[0].alloc(e->blocks));
+  HANF_TRY(e->mod[1].alloc(e->blocks));
+  HANF_TRY(e->est.alloc(n));
+  HANF_TRY(e->block_sums.alloc(e->blocks));
+  HANF_TRY(e->reduce.alloc(1));
+  HANF_TRY(cudaMallocHost(&e->h_reduce, sizeof(hanf::ReduceOut)));
+  if (cfg.exact_sum)
+    HANF_TRY(cudaMallocHost(&e->h_block_sums, sizeof(double) * (e->blocks ? e->blocks : 1)));
+
+  // CSR of the shard: offsets[lo..hi], arcs [offsets[lo], offsets[hi])
+  if (n > 0) {
+    HANF_TRY(e->offsets.alloc(hi - lo + 1));
+    HANF_TRY(cudaMemcpyAsync(e->offsets.p, g->offsets + lo, sizeof(uint64_t) * (hi - lo + 1),
+                             cudaMemcpyHostToDevice, e->stream));
+    e->succ_base = g->offsets[lo];
+    const uint64_t arcs = g->offsets[hi] - g->offsets[lo];
+    HANF_TRY(e->succ.alloc(arcs));
+    if (arcs)
+      HANF_TRY(cudaMemcpyAsync(e->succ.p, g->arcs + e->succ_base, sizeof(uint32_t) * arcs,
+                               cudaMemcpyHostToDevice, e->stream));
+    for (uint64_t v = lo; v < hi; ++v)
+      if (g->offsets[v + 1] < g->offsets[v])
+        return bail(fail(HANF_INVALID_ARGUMENT, "offsets must be non-decreasing"));
+    for (uint64_t i = g->offsets[lo]; i < g->offsets[hi]; ++i)
+      if (g->arcs[i] >= n) return bail(fail(HANF_INVALID_ARGUMENT, "arc endpoint out of range"));
+  }
+
+  // linear-counting table m*log(m/z), same expression as hll.hpp:139
+  {
+    const double m = static_cast<double>(params.registers);
+    std::vector<double> table(params.registers + 1, 0.0);
+    for (uint32_t z = 1; z <= params.registers; ++z)
+      table[z] = m * std::log(m / static_cast<double>(z));
+    HANF_TRY(e->log_table.alloc(table.size()));
+    HANF_TRY(cudaMemcpy(e->log_table.p, table.data(), sizeof(double) * table.size(),
+                        cudaMemcpyHostToDevice));
+  }
+  if (n > 0) {
+    st = build_tasks(e, g->offsets);
+    if (st != HANF_OK) return bail(st);
+    st = seed_all(e);
+    if (st != HANF_OK) return bail(st);
+  }
+#undef HANF_TRY
+  *out = e;
+  return HANF_OK;
+}
+
+void hanf_destroy(hanf_engine* e) { delete e; }
+
+hanf_status hanf_reset(hanf_engine* e) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (e->n == 0) {
+    e->t = 0;
+    return HANF_OK;
+  }
+  HANF_CUDA(cudaSetDevice(e->device));
+  return seed_all(e);
+}
+
+hanf_status hanf_sum_estimates(hanf_engine* e, double* sum) {
+  if (!e || !sum) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *sum = e->n == 0 ? 0.0 : e->last_sum;
+  return HANF_OK;
+}
+
+hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
+  if (!e || !rep) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->n == 0) {                       // engine.hpp:124
+    rep->sum = 0.0;
+    rep->modified = 0;
+    return HANF_OK;
+  }
+  HANF_CUDA(cudaSetDevice(e->device));
+  hanf_status st = compute_local(e);
+  if (st != HANF_OK) return st;
+  return commit(e, rep);
+}
+
+hanf_status hanf_shard_compute(hanf_engine* e) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (e->n == 0) return HANF_OK;
+  HANF_CUDA(cudaSetDevice(e->device));
+  return compute_local(e);
+}
+
+hanf_status hanf_shard_commit(hanf_engine* e, hanf_iteration_report* rep) {
+  if (!e || !rep) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->n == 0) {
+    rep->sum = 0.0;
+    rep->modified = 0;
+    return HANF_OK;
+  }
+  HANF_CUDA(cudaSetDevice(e->device));
+  return commit(e, rep);
+}
+
+hanf_status hanf_run_to_stabilisation(hanf_engine* e, double* values, uint64_t* modified,
+                                      uint64_t capacity, uint64_t* length, double* wall) {
+  if (!e || !length) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  const auto start = std::chrono::steady_clock::now();
+  *length = 0;
+  if (wall) *wall = 0.0;
+  if (e->n == 0) return HANF_OK;         // engine.hpp:240
+  if (e->cfg.termination == 1) {         // engine.hpp:242-250
+    std::cerr << "warning: threshold termination can stop before the counters "
+                 "stabilise and truncate the neighbourhood function; on graphs "
+                 "where large components hang off a narrow path (two cliques "
+                 "joined by a one-way path) the resulting cdf and effective "
+                 "diameter are arbitrarily wrong. Use stabilisation for "
+                 "trustworthy results.\n";
+  }
+  std::vector<double> vals;
+  std::vector<uint64_t> mods;
+  vals.push_back(e->last_sum);
+  mods.push_back(e->n);
+  for (;;) {
+    if (vals.size() - 1 >= e->cfg.max_iterations)
+      return fail(HANF_GUARD, "engine: iteration cap " + std::to_string(e->cfg.max_iterations) +
+                                  " exceeded; pathological input or bug");
+    hanf_iteration_report rep;
+    const hanf_status st = hanf_step(e, &rep);
+    if (st != HANF_OK) return st;
+    if (rep.modified == 0) break;
+    const double prev = vals.back();
+    vals.push_back(rep.sum);
+    mods.push_back(rep.modified);
+    if (e->cfg.termination == 1 && prev > 0.0) {
+      const double rel = (rep.sum - prev) / prev;
+      if (rel < e->cfg.eps_inc) break;
+    }
+  }
+  for (size_t t = 1; t < vals.size(); ++t) vals[t] = std::max(vals[t], vals[t - 1]);
+  *length = vals.size();
+  e->result_values = vals;
+  e->result_modified = mods;
+  if (wall)
+    *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+  if (capacity < vals.size())
+    return fail(HANF_CAPACITY, "output capacity " + std::to_string(capacity) + " < " +
+                                   std::to_string(vals.size()) + " values");
+  if (values) std::copy(vals.begin(), vals.end(), values);
+  if (modified) std::copy(mods.begin(), mods.end(), modified);
+  return HANF_OK;
+}
+
+hanf_status hanf_last_result(const hanf_engine* e, double* values, uint64_t* modified,
+                             uint64_t capacity, uint64_t* length) {
+  if (!e || !length) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *length = e->result_values.size();
+  if (capacity < e->result_values.size())
+    return fail(HANF_CAPACITY, "output capacity too small");
+  if (values) std::copy(e->result_values.begin(), e->result_values.end(), values);
+  if (modified) std::copy(e->result_modified.begin(), e->result_modified.end(), modified);
+  return HANF_OK;
+}
+
+hanf_status hanf_estimate_nf(const hanf_graph_view* g, const hanf_config* cfg, double* values,
+                             uint64_t* modified, uint64_t capacity, uint64_t* length,
+                             double* wall) {
+  const auto start = std::chrono::steady_clock::now();
+  hanf_engine* e = nullptr;
+  hanf_status st = hanf_create(g, cfg, &e);
+  if (st != HANF_OK) return st;
+  st = hanf_run_to_stabilisation(e, values, modified, capacity, length, nullptr);
+  hanf_destroy(e);
+  if (wall)
+    *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+  return st;
+}
+
+hanf_status hanf_read_counters(hanf_engine* e, uint64_t first, uint64_t count, uint64_t* dst) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (first > e->n || count > e->n - first)
+    return fail(HANF_OUT_OF_RANGE, "counter index out of range");
+  if (count == 0) return HANF_OK;
+  if (!dst) return fail(HANF_INVALID_ARGUMENT, "null destination");
+  HANF_CUDA(cudaSetDevice(e->device));
+  HANF_CUDA(cudaMemcpyAsync(dst, e->cnt[e->cur].p + first * e->words,
+                            sizeof(uint64_t) * count * e->words, cudaMemcpyDeviceToHost,
+                            e->stream));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  return HANF_OK;
+}
+
+hanf_status hanf_params(const hanf_engine* e, hanf_sketch_params* out) {
+  if (!e || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *out = e->params;
+  return HANF_OK;
+}
+
+hanf_status hanf_iteration(const hanf_engine* e, uint64_t* t) {
+  if (!e || !t) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *t = e->t;
+  return HANF_OK;
+}
+
+hanf_status hanf_systolic_active(const hanf_engine* e, int32_t* active) {
+  if (!e || !active) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *active = e->systolic ? 1 : 0;
+  return HANF_OK;
+}
+
+hanf_status hanf_num_nodes(const hanf_engine* e, uint64_t* n) {
+  if (!e || !n) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *n = e->n;
+  return HANF_OK;
+}
+
+hanf_status hanf_stream(const hanf_engine* e, void** stream) {
+  if (!e || !stream) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *stream = static_cast<void*>(e->stream);
+  return HANF_OK;
+}
+
+hanf_status hanf_launch_count(const hanf_engine* e, uint64_t* launches) {
+  if (!e || !launches) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *launches = e->launches;
+  return HANF_OK;
+}
+
+hanf_status hanf_device_buffers(hanf_engine* e, hanf_buffers* out) {
+  if (!e || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  const int ng = 1 - e->cur;
+  out->next_counters = e->cnt[ng].p;
+  out->next_modified = e->mod[ng].p;
+  out->block_sums = e->block_sums.p;
+  out->words_per_counter = e->words;
+  out->blocks = e->blocks;
+  out->shard_begin = e->lo;
+  out->shard_end = e->hi;
+  return HANF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,263 @@
+"""The HyperANF engine: Python mirror of ``hyperanf::NfEngine`` (engine.hpp).
+
+Every method is a thin call through the C-ABI of libhanf.so, whose union,
+estimate and reduction kernels run on the B200.  Names, argument meaning and
+error behaviour follow the reference:
+
+    EngineConfig      engine.hpp:32-46
+    IterationReport   engine.hpp:48-51
+    NfEstimate        engine.hpp:53-66
+    NfEngine          engine.hpp:68-292
+    estimate_nf       engine.hpp:295-298
+    SketchParams      hll.hpp:36-70
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from ctypes import POINTER, c_double, c_int32, c_uint64, c_void_p
+from dataclasses import dataclass, field
+from typing import List
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+from .graph import Graph
+
+
+class Termination(enum.IntEnum):
+    stabilisation = 0
+    threshold = 1
+
+
+@dataclass
+class EngineConfig:
+    bucket_bits: int = 7
+    register_bits: int = 0          # 0: 5 below 2^32 nodes, 6 otherwise
+    seed: int = 0
+    threads: int = 1                # CPU scheduling knob (accepted, no effect)
+    task_size: int = 0              # CPU scheduling knob (accepted, no effect)
+    systolic_threshold: float = 0.25
+    termination: Termination = Termination.stabilisation
+    eps_inc: float = 0.0
+    max_iterations: int = 0         # 0: n + 1
+    spill_to_disk: bool = False     # accepted; HBM holds both generations
+    track_modified: bool = True
+    use_systolic: bool = True
+    # B200 options: never change a result bit
+    device: int = 0
+    exact_sum: bool = True          # N(t) total in the reference's summation order
+    shard_begin: int = 0
+    shard_end: int = 0
+
+    def to_c(self) -> _lib.Config:
+        c = _lib.Config()
+        check(lib().hanf_config_init(ctypes.byref(c)))
+        c.bucket_bits = self.bucket_bits
+        c.register_bits = self.register_bits
+        c.seed = self.seed & 0xFFFFFFFFFFFFFFFF
+        c.threads = self.threads
+        c.task_size = self.task_size
+        c.systolic_threshold = self.systolic_threshold
+        c.termination = int(self.termination)
+        c.eps_inc = self.eps_inc
+        c.max_iterations = self.max_iterations
+        c.spill_to_disk = int(self.spill_to_disk)
+        c.track_modified = int(self.track_modified)
+        c.use_systolic = int(self.use_systolic)
+        c.device = self.device
+        c.exact_sum = int(self.exact_sum)
+        c.shard_begin = self.shard_begin
+        c.shard_end = self.shard_end
+        return c
+
+
+@dataclass
+class IterationReport:
+    sum: float = 0.0
+    modified: int = 0
+
+
+@dataclass
+class NfEstimate:
+    n: int = 0
+    m: int = 0
+    seed: int = 0
+    termination: Termination = Termination.stabilisation
+    values: List[float] = field(default_factory=list)
+    modified: List[int] = field(default_factory=list)
+    wall_seconds: float = 0.0
+    exact: bool = False
+
+    def iterations(self) -> int:
+        return 0 if not self.values else len(self.values) - 1
+
+
+@dataclass
+class SketchParams:
+    bucket_bits: int = 7
+    registers: int = 128
+    register_bits: int = 5
+    alpha: float = 0.0
+    seed: int = 0
+    words: int = 10
+
+    @staticmethod
+    def make(bucket_bits: int, seed: int, register_bits: int = 5) -> "SketchParams":
+        """hll.hpp:43-56 (raises ValueError like std::invalid_argument)."""
+        p = _lib.SketchParamsC()
+        check(lib().hanf_sketch_params_make(bucket_bits, seed & 0xFFFFFFFFFFFFFFFF,
+                                            register_bits, ctypes.byref(p)))
+        return SketchParams._from_c(p)
+
+    @staticmethod
+    def _from_c(p: _lib.SketchParamsC) -> "SketchParams":
+        return SketchParams(p.bucket_bits, p.registers, p.register_bits, p.alpha, p.seed,
+                            p.words_per_counter)
+
+    def words_per_counter(self) -> int:
+        return self.words
+
+    def max_register_value(self) -> int:
+        return (1 << self.register_bits) - 1
+
+
+class NfEngine:
+    """Neighbourhood-function estimator over one HLL counter per node.
+
+    The engine keeps its own copy of the graph in HBM (the reference keeps
+    a non-owning pointer; the caller's Graph may be dropped after
+    construction here)."""
+
+    def __init__(self, graph: Graph, cfg: EngineConfig = None):
+        cfg = cfg or EngineConfig()
+        self._cfg = cfg
+        self._graph = graph
+        self._h = c_void_p()
+        view = graph.view()
+        ccfg = cfg.to_c()
+        check(lib().hanf_create(ctypes.byref(view), ctypes.byref(ccfg), ctypes.byref(self._h)))
+        p = _lib.SketchParamsC()
+        check(lib().hanf_params(self._h, ctypes.byref(p)))
+        self._params = SketchParams._from_c(p)
+
+    def close(self) -> None:
+        if self._h:
+            lib().hanf_destroy(self._h)
+            self._h = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- reference surface (engine.hpp:92-96) ---------------------------------
+    def params(self) -> SketchParams:
+        return self._params
+
+    def config(self) -> EngineConfig:
+        return self._cfg
+
+    def iteration(self) -> int:
+        t = c_uint64()
+        check(lib().hanf_iteration(self._h, ctypes.byref(t)))
+        return t.value
+
+    def systolic_active(self) -> bool:
+        a = c_int32()
+        check(lib().hanf_systolic_active(self._h, ctypes.byref(a)))
+        return bool(a.value)
+
+    def counters(self, first: int = 0, count: int = None) -> np.ndarray:
+        """CounterArray::data() (hll.hpp:224-226): u64[count * W] in the
+        reference packing, copied from HBM."""
+        n = self._graph.num_nodes()
+        if count is None:
+            count = n - first
+        out = np.empty(max(count, 0) * self._params.words, dtype=np.uint64)
+        check(lib().hanf_read_counters(self._h, first, count,
+                                       out.ctypes.data_as(POINTER(c_uint64))))
+        return out
+
+    def counter(self, i: int) -> np.ndarray:
+        """CounterArray::counter(i) (hll.hpp:196-205); IndexError past n."""
+        return self.counters(i, 1)
+
+    def sum_estimates(self) -> float:
+        s = c_double()
+        check(lib().hanf_sum_estimates(self._h, ctypes.byref(s)))
+        return s.value
+
+    def step(self) -> IterationReport:
+        r = _lib.IterationReportC()
+        check(lib().hanf_step(self._h, ctypes.byref(r)))
+        return IterationReport(r.sum, r.modified)
+
+    def run_to_stabilisation(self) -> NfEstimate:
+        """engine.hpp:233-275: N(0..T), clamped non-decreasing; the
+        stabilising no-change iteration is not recorded."""
+        n = self._graph.num_nodes()
+        cap = 64
+        vals = np.empty(cap, dtype=np.float64)
+        mods = np.empty(cap, dtype=np.uint64)
+        length = c_uint64()
+        wall = c_double()
+        st = lib().hanf_run_to_stabilisation(
+            self._h, vals.ctypes.data_as(POINTER(c_double)),
+            mods.ctypes.data_as(POINTER(c_uint64)), cap, ctypes.byref(length),
+            ctypes.byref(wall))
+        if st == _lib.CAPACITY:
+            cap = length.value
+            vals = np.empty(cap, dtype=np.float64)
+            mods = np.empty(cap, dtype=np.uint64)
+            st = lib().hanf_last_result(self._h, vals.ctypes.data_as(POINTER(c_double)),
+                                        mods.ctypes.data_as(POINTER(c_uint64)), cap,
+                                        ctypes.byref(length))
+        check(st)
+        L = length.value
+        return NfEstimate(n=n, m=self._params.registers, seed=self._params.seed,
+                          termination=self._cfg.termination,
+                          values=[float(x) for x in vals[:L]],
+                          modified=[int(x) for x in mods[:L]], wall_seconds=wall.value)
+
+    # -- B200 plumbing ------------------------------------------------------------
+    def reset(self) -> None:
+        """Re-seed and rewind to iteration 0 (no graph re-upload)."""
+        check(lib().hanf_reset(self._h))
+
+    def stream(self) -> int:
+        s = c_void_p()
+        check(lib().hanf_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    def launch_count(self) -> int:
+        c = c_uint64()
+        check(lib().hanf_launch_count(self._h, ctypes.byref(c)))
+        return c.value
+
+    def device_buffers(self) -> _lib.BuffersC:
+        b = _lib.BuffersC()
+        check(lib().hanf_device_buffers(self._h, ctypes.byref(b)))
+        return b
+
+    def shard_compute(self) -> None:
+        check(lib().hanf_shard_compute(self._h))
+
+    def shard_commit(self) -> IterationReport:
+        r = _lib.IterationReportC()
+        check(lib().hanf_shard_commit(self._h, ctypes.byref(r)))
+        return IterationReport(r.sum, r.modified)
+
+
+def estimate_nf(g: Graph, cfg: EngineConfig = None) -> NfEstimate:
+    """engine.hpp:295-298: seed counters, run, return the estimate."""
+    with NfEngine(g, cfg or EngineConfig()) as engine:
+        return engine.run_to_stabilisation()
