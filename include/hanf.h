@@ -155,6 +155,12 @@ const char* hanf_last_error(void);
 hanf_status hanf_stream(const hanf_engine* engine, void** stream);
 /* Kernels launched by this engine since creation. */
 hanf_status hanf_launch_count(const hanf_engine* engine, uint64_t* launches);
+/* Phase timing with CUDA events on the engine stream (off by default):
+ * union sweep (union + hub kernels), estimates + block sums, totals.
+ * Accumulated over the steps since the last hanf_set_timing(e, 1). */
+hanf_status hanf_set_timing(hanf_engine* engine, int32_t enable);
+hanf_status hanf_timing(const hanf_engine* engine, double* union_ms,
+                        double* estimate_ms, double* reduce_ms, uint64_t* steps);
 /* Device buffers of the engine, for collectives over the node shards. */
 typedef struct {
   void* next_counters;     /* u64[n*W]: the generation being written by step */

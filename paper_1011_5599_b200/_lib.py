@@ -74,6 +74,9 @@ _SIGNATURES = {
     "hanf_stream": [_P, POINTER(_P)],
     "hanf_launch_count": [_P, POINTER(c_uint64)],
     "hanf_device_buffers": [_P, POINTER(BuffersC)],
+    "hanf_set_timing": [_P, c_int32],
+    "hanf_timing": [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double),
+                    POINTER(c_uint64)],
     "hanf_shard_compute": [_P],
     "hanf_shard_commit": [_P, POINTER(IterationReportC)],
     "hanf_distance_distribution": [POINTER(c_double), c_uint64, POINTER(c_double),

@@ -124,8 +124,15 @@ struct hanf_engine {
   std::vector<double> result_values;      // last run_to_stabilisation
   std::vector<uint64_t> result_modified;
   uint64_t launches = 0;
+  // phase timing (hanf_set_timing)
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double union_ms = 0.0, estimate_ms = 0.0, reduce_ms = 0.0;
+  uint64_t timed_steps = 0;
 
   ~hanf_engine() {
+    for (auto& x : ev)
+      if (x) cudaEventDestroy(x);
     if (device >= 0) cudaSetDevice(device);
     offsets.free(); succ.free();
     for (int i = 0; i < 2; ++i) { cnt[i].free(); mod[i].free(); }
@@ -280,15 +287,27 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
 // Total of the block sums and popcount of bitmap `bits` over all blocks;
 // waits for the stream.  exact_sum: the total is redone on the host in the
 // reference's order (engine.hpp:115-117).
-hanf_status reduce_totals(hanf_engine* e, const uint64_t* bits, double* total, uint64_t* count) {
+hanf_status reduce_totals(hanf_engine* e, const uint64_t* bits, double* total, uint64_t* count,
+                          bool in_step = false) {
   HANF_CUDA(hanf::launch_reduce(e->block_sums.p, bits, 0, e->blocks, e->reduce.p, e->stream,
                                 &e->launches));
+  if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
   HANF_CUDA(cudaMemcpyAsync(e->h_reduce, e->reduce.p, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                             e->stream));
   if (e->cfg.exact_sum)
     HANF_CUDA(cudaMemcpyAsync(e->h_block_sums, e->block_sums.p, sizeof(double) * e->blocks,
                               cudaMemcpyDeviceToHost, e->stream));
   HANF_CUDA(cudaStreamSynchronize(e->stream));
+  if (in_step && e->timing) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    HANF_CUDA(cudaEventElapsedTime(&a, e->ev[0], e->ev[1]));
+    HANF_CUDA(cudaEventElapsedTime(&b, e->ev[1], e->ev[2]));
+    HANF_CUDA(cudaEventElapsedTime(&c, e->ev[2], e->ev[3]));
+    e->union_ms += a;
+    e->estimate_ms += b;
+    e->reduce_ms += c;
+    ++e->timed_steps;
+  }
   if (e->cfg.exact_sum) {
     double s = 0.0;
     for (uint64_t b = 0; b < e->blocks; ++b) s += e->h_block_sums[b];
@@ -332,6 +351,7 @@ hanf_status compute_local(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
   HANF_CUDA(cudaMemsetAsync(e->mod[ng].p + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
+  if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
   hanf::UnionArgs a{};
   a.offsets = e->offsets.p - e->lo;
   a.succ = e->succ.p;
@@ -365,14 +385,18 @@ hanf_status compute_local(hanf_engine* e) {
   h.stale_valid = a.stale_valid;
   HANF_CUDA(hanf::launch_hub_finalize(h, e->params.register_bits, e->params.registers,
                                       e->stream, &e->launches));
-  return run_estimates(e, ng, e->mod[ng].p, w0, w1);
+  if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
+  const hanf_status st = run_estimates(e, ng, e->mod[ng].p, w0, w1);
+  if (st != HANF_OK) return st;
+  if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
+  return HANF_OK;
 }
 
 hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
   const int ng = 1 - e->cur;
   double total = 0.0;
   uint64_t count = 0;
-  const hanf_status st = reduce_totals(e, e->mod[ng].p, &total, &count);
+  const hanf_status st = reduce_totals(e, e->mod[ng].p, &total, &count, true);
   if (st != HANF_OK) return st;
   e->cur = ng;                                     // std::swap, engine.hpp:198-200
   e->stale_valid = true;
@@ -690,6 +714,27 @@ hanf_status hanf_stream(const hanf_engine* e, void** stream) {
 hanf_status hanf_launch_count(const hanf_engine* e, uint64_t* launches) {
   if (!e || !launches) return fail(HANF_INVALID_ARGUMENT, "null argument");
   *launches = e->launches;
+  return HANF_OK;
+}
+
+hanf_status hanf_set_timing(hanf_engine* e, int32_t enable) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  HANF_CUDA(cudaSetDevice(e->device));
+  for (auto& x : e->ev)
+    if (!x) HANF_CUDA(cudaEventCreate(&x));
+  e->timing = enable != 0;
+  e->union_ms = e->estimate_ms = e->reduce_ms = 0.0;
+  e->timed_steps = 0;
+  return HANF_OK;
+}
+
+hanf_status hanf_timing(const hanf_engine* e, double* union_ms, double* estimate_ms,
+                        double* reduce_ms, uint64_t* steps) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (union_ms) *union_ms = e->union_ms;
+  if (estimate_ms) *estimate_ms = e->estimate_ms;
+  if (reduce_ms) *reduce_ms = e->reduce_ms;
+  if (steps) *steps = e->timed_steps;
   return HANF_OK;
 }
 

@@ -243,6 +243,17 @@ class NfEngine:
         check(lib().hanf_launch_count(self._h, ctypes.byref(c)))
         return c.value
 
+    def set_timing(self, enable: bool = True) -> None:
+        """CUDA-event phase timing on the engine stream (resets the totals)."""
+        check(lib().hanf_set_timing(self._h, int(enable)))
+
+    def timing(self) -> dict:
+        u, e, r, n = c_double(), c_double(), c_double(), c_uint64()
+        check(lib().hanf_timing(self._h, ctypes.byref(u), ctypes.byref(e), ctypes.byref(r),
+                                ctypes.byref(n)))
+        return {"union_ms": u.value, "estimate_ms": e.value, "reduce_ms": r.value,
+                "steps": n.value}
+
     def device_buffers(self) -> _lib.BuffersC:
         b = _lib.BuffersC()
         check(lib().hanf_device_buffers(self._h, ctypes.byref(b)))

@@ -1,0 +1,162 @@
+"""Node-range sharding of the HyperANF iteration across GPUs (one process per
+GPU, torch.distributed for the plumbing).
+
+Every rank holds the full previous generation (successor gathers are
+random), computes the next generation for its contiguous node range, and
+the shards are exchanged once per iteration: the next-generation counter
+rows, the "modified" bitmap words and the 64-counter block sums.  Each
+rank then reduces N(t) and the modified count over the full arrays, so all
+ranks agree on the report without a separate all-reduce.  Exchange = an
+in-place all-gather when the shards are equal (n a multiple of 64*world),
+else one broadcast per owner.
+
+The local engine is anything with shard_compute() / exchange_buffers() /
+shard_commit() / before_exchange() / after_exchange(): the CUDA engine
+(`LocalCudaShard`) in production, a CPU emulation in the gloo tests.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .engine import EngineConfig, IterationReport, NfEngine, NfEstimate
+
+
+def shard_ranges(n: int, world: int) -> List[Tuple[int, int]]:
+    """Contiguous node ranges, each a multiple of 64 nodes (the last one may
+    be short or empty), so bitmap words and block sums split cleanly."""
+    per = -(-n // world) if world else n
+    per = -(-per // 64) * 64
+    return [(min(k * per, n), min((k + 1) * per, n)) for k in range(world)]
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ holder for a raw device pointer."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def device_tensor(ptr: int, count: int, dtype: torch.dtype, device: torch.device):
+    typestr = {torch.int64: "<i8", torch.float64: "<f8"}[dtype]
+    return torch.as_tensor(_CudaArray(ptr, count, typestr), device=device)
+
+
+class LocalCudaShard:
+    """The CUDA engine restricted to one node range."""
+
+    def __init__(self, graph, cfg: EngineConfig, lo: int, hi: int, device: torch.device):
+        self.engine = NfEngine(graph, dataclasses.replace(cfg, shard_begin=lo, shard_end=hi))
+        self.n = graph.num_nodes()
+        self.device = device
+        self.stream = torch.cuda.ExternalStream(self.engine.stream(), device=device)
+
+    def shard_compute(self):
+        self.engine.shard_compute()
+
+    def before_exchange(self):
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+
+    def after_exchange(self):
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+
+    def exchange_buffers(self):
+        """(full tensor, elements per 64-node unit) for the three buffers the
+        next commit reads; the generation flips every step, so re-fetch."""
+        b = self.engine.device_buffers()
+        blocks = int(b.blocks)
+        W = int(b.words_per_counter)
+        counters = device_tensor(b.next_counters, self.n * W, torch.int64, self.device)
+        modified = device_tensor(b.next_modified, blocks, torch.int64, self.device)
+        sums = device_tensor(b.block_sums, blocks, torch.float64, self.device)
+        return [(counters, 64 * W, W), (modified, 1, None), (sums, 1, None)]
+
+    def shard_commit(self) -> IterationReport:
+        return self.engine.shard_commit()
+
+    def sum_estimates(self) -> float:
+        return self.engine.sum_estimates()
+
+    def close(self):
+        self.engine.close()
+
+
+class ShardedNfEngine:
+    """NfEngine across `world` ranks (engine.hpp:122-275 semantics)."""
+
+    def __init__(self, graph, cfg: EngineConfig, rank: int, world: int, local=None,
+                 group=None):
+        self.n = graph.num_nodes()
+        self.cfg = cfg
+        self.rank, self.world, self.group = rank, world, group
+        self.ranges = shard_ranges(self.n, world)
+        lo, hi = self.ranges[rank]
+        if local is None:
+            local = LocalCudaShard(graph, cfg, lo, hi, torch.device("cuda", torch.cuda.current_device()))
+        self.local = local
+
+    def _exchange(self, tensor: torch.Tensor, unit: int, per_node):
+        """Gives every rank the owners' slices of `tensor`.  unit = elements
+        per 64 nodes; per_node = elements per node (counters) or None."""
+        spans = []
+        for lo, hi in self.ranges:
+            if per_node is not None:
+                spans.append((lo * per_node, hi * per_node))
+            else:
+                spans.append((lo // 64, -(-hi // 64)))
+        sizes = [e - b for b, e in spans]
+        if len(set(sizes)) == 1 and spans[-1][1] == tensor.numel():
+            dist.all_gather_into_tensor(tensor, tensor[spans[self.rank][0]:spans[self.rank][1]],
+                                        group=self.group)
+        else:
+            for k, (b, e) in enumerate(spans):
+                if e > b:
+                    view = tensor[b:e]
+                    dist.broadcast(view, src=k, group=self.group)
+
+    def step(self) -> IterationReport:
+        if self.n == 0:
+            return IterationReport(0.0, 0)
+        self.local.shard_compute()
+        self.local.before_exchange()
+        for tensor, unit, per_node in self.local.exchange_buffers():
+            self._exchange(tensor, unit, per_node)
+        self.local.after_exchange()
+        return self.local.shard_commit()
+
+    def sum_estimates(self) -> float:
+        return self.local.sum_estimates()
+
+    def run_to_stabilisation(self) -> NfEstimate:
+        """engine.hpp:233-275 over the sharded step."""
+        est = NfEstimate(n=self.n, m=1 << self.cfg.bucket_bits, seed=self.cfg.seed,
+                         termination=self.cfg.termination)
+        if self.n == 0:
+            return est
+        cap = self.cfg.max_iterations or (self.n + 1)
+        est.values.append(self.sum_estimates())
+        est.modified.append(self.n)
+        while True:
+            if len(est.values) - 1 >= cap:
+                from ._lib import GuardError
+                raise GuardError(f"engine: iteration cap {cap} exceeded; pathological input or bug")
+            rep = self.step()
+            if rep.modified == 0:
+                break
+            prev = est.values[-1]
+            est.values.append(rep.sum)
+            est.modified.append(rep.modified)
+            if int(self.cfg.termination) == 1 and prev > 0.0:
+                if (rep.sum - prev) / prev < self.cfg.eps_inc:
+                    break
+        for t in range(1, len(est.values)):
+            est.values[t] = max(est.values[t], est.values[t - 1])
+        return est
+
+    def close(self):
+        self.local.close()
