@@ -28,6 +28,15 @@ __device__ __forceinline__ void sfor(F&& f) {
   }
 }
 
+// d = LUT(a, b, c) with the PTX lop3 truth-table convention (a=0xF0,
+// b=0xCC, c=0xAA).
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return d;
+}
+
 // Register layout of one chunk: NREG registers of R bits.
 template <int R, int NREG>
 struct Layout {
@@ -163,7 +172,7 @@ __device__ __forceinline__ void swar_max(uint32_t (&x)[Lay::kLimbs],
     const uint64_t w = static_cast<uint64_t>(u) * Lay::kMul;
     const uint32_t spread = static_cast<uint32_t>(w) | carry;
     carry = static_cast<uint32_t>(w >> 32);
-    x[i] = (x[i] & ~spread) | (y[i] & spread);
+    x[i] = lop3<0xD8>(x[i], y[i], spread);  // (x & ~spread) | (y & spread)
   });
 }
 
@@ -342,6 +351,151 @@ __device__ __forceinline__ double estimate_counter_r5(const uint64_t* c, const E
     zeros += term >> 31;
   });
   return finish_estimate(p, __dmul_rn(static_cast<double>(s), 0x1p-31), zeros);
+}
+
+// ---------------------------------------------------------------------------
+// 256-bit window gathers (sm_100 LDG.E.ENL2.256).  Counter w of a layout
+// with a W-word stride starts at byte 8*W*w, i.e. q = (W*w) mod 4 words into
+// its 32-byte block.  The counter is read as K aligned 32-byte loads (one
+// L1 wavefront each; the 8-byte loads they replace cost one per word) and
+// shifted down by q words with selects.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ldg256(uint32_t (&v)[8], const uint64_t* p) {
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+
+template <int NW>
+struct Window {
+  // worst-case word offset inside the 32-byte block, over all counters
+  static constexpr int kMaxQ = (NW % 4 == 0) ? 0 : ((NW % 2 == 0) ? 2 : 3);
+  static constexpr int kLoads = (kMaxQ + NW + 3) / 4;
+  static constexpr int kLimbs = 8 * kLoads;
+};
+
+// Issues the window loads of counter w (row stride NW words).
+template <int NW>
+__device__ __forceinline__ void window_load(uint32_t (&raw)[Window<NW>::kLoads][8],
+                                            const uint64_t* base, uint32_t w) {
+  const uint64_t word = static_cast<uint64_t>(w) * NW;
+  const uint64_t* p = base + (word & ~3ull);
+  sfor<0, Window<NW>::kLoads>([&](auto I) {
+    constexpr int k = decltype(I)::value;
+    ldg256(raw[k], p + 4 * k);
+  });
+}
+
+// Extracts the counter's limbs from its window: limb i = raw limb 2q + i.
+template <class Lay, int NW>
+__device__ __forceinline__ void window_extract(uint32_t (&x)[Lay::kLimbs],
+                                               const uint32_t (&raw)[Window<NW>::kLoads][8],
+                                               uint32_t w) {
+  constexpr int NL = Lay::kLimbs;
+  constexpr int WL = Window<NW>::kLimbs;
+  const uint32_t q = (w * NW) & 3u;
+  auto at = [&](int i) -> uint32_t { return raw[i / 8][i % 8]; };
+  if constexpr (Window<NW>::kMaxQ == 0) {
+    sfor<0, NL>([&](auto I) { x[decltype(I)::value] = at(decltype(I)::value); });
+  } else if constexpr (Window<NW>::kMaxQ == 2) {
+    const bool s2 = q & 2u;
+    sfor<0, NL>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      x[i] = s2 ? at(i + 4) : at(i);
+    });
+  } else {
+    const bool s2 = q & 2u, s1 = q & 1u;
+    constexpr int TL = NL + 2 < WL - 4 ? NL + 2 : WL - 4;  // limbs kept after the 2-word step
+    uint32_t t[TL];
+    sfor<0, TL>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      t[i] = s2 ? at(i + 4) : at(i);
+    });
+    sfor<0, NL>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      if constexpr (i + 2 < TL)
+        x[i] = s1 ? t[i + 2] : t[i];
+      else
+        x[i] = t[i];  // unreachable limb pairing (q=1 never needs it)
+    });
+  }
+}
+
+// 128-bit windows: counter w (W words, W odd) starts q = (W*w) mod 2 words
+// into its 16-byte block; ceil((W+1)/2) aligned 16-byte loads, one select.
+template <int NW>
+struct Window128 {
+  static_assert(NW % 2 == 1, "even strides are 16-byte aligned already");
+  static constexpr int kLoads = (NW + 2) / 2;
+};
+
+template <int NW>
+__device__ __forceinline__ void window128_load(uint4 (&raw)[Window128<NW>::kLoads],
+                                               const uint64_t* base, uint32_t w) {
+  const uint64_t word = static_cast<uint64_t>(w) * NW;
+  const uint4* p = reinterpret_cast<const uint4*>(base + (word & ~1ull));
+  sfor<0, Window128<NW>::kLoads>([&](auto I) {
+    constexpr int k = decltype(I)::value;
+    raw[k] = __ldg(p + k);
+  });
+}
+
+template <class Lay, int NW>
+__device__ __forceinline__ void window128_extract(uint32_t (&x)[Lay::kLimbs],
+                                                  const uint4 (&raw)[Window128<NW>::kLoads],
+                                                  uint32_t w) {
+  const bool s1 = (w * NW) & 1u;
+  auto at = [&](int i) -> uint32_t {
+    const uint4& q = raw[i / 4];
+    switch (i % 4) {
+      case 0: return q.x;
+      case 1: return q.y;
+      case 2: return q.z;
+      default: return q.w;
+    }
+  };
+  sfor<0, Lay::kLimbs>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    x[i] = s1 ? at(i + 2) : at(i);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Estimator from a counter held in limbs (single-chunk layouts), same
+// arithmetic as estimate_counter_* above.
+// ---------------------------------------------------------------------------
+template <class Lay>
+__device__ __forceinline__ double estimate_limbs(const uint32_t (&x)[Lay::kLimbs],
+                                                 const EstimateParams& p) {
+  constexpr int R = Lay::kR;
+  constexpr int NL = Lay::kLimbs;
+  auto limb = [&](int i) -> uint32_t { return i < NL ? x[i] : 0u; };
+  uint32_t zeros = 0;
+  if constexpr (R == 5) {
+    uint64_t s = 0;
+    sfor<0, Lay::kNReg>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      constexpr int bit = j * 5;
+      const uint32_t raw = __funnelshift_r(limb(bit / 32), limb(bit / 32 + 1), bit % 32);
+      const uint32_t term = __funnelshift_r(0x80000000u, 0u, raw);  // 2^(31 - M_j)
+      s += term;
+      zeros += term >> 31;
+    });
+    return finish_estimate(p, __dmul_rn(static_cast<double>(s), 0x1p-31), zeros);
+  } else {
+    double harmonic = 0.0;
+    sfor<0, Lay::kNReg>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      constexpr int bit = j * R;
+      const uint32_t reg =
+          __funnelshift_r(limb(bit / 32), limb(bit / 32 + 1), bit % 32) & ((1u << R) - 1);
+      harmonic = __dadd_rn(harmonic,
+                           __longlong_as_double(static_cast<long long>(1023 - reg) << 52));
+      zeros += reg == 0;
+    });
+    return finish_estimate(p, harmonic, zeros);
+  }
 }
 
 }  // namespace hanf

@@ -13,8 +13,10 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <iostream>
+#include <thread>
 #include <new>
 #include <string>
 #include <vector>
@@ -96,22 +98,22 @@ struct hanf_engine {
   int device = 0;
   cudaStream_t stream = nullptr;
 
-  DevBuf<uint64_t> offsets;  // offsets[lo..hi] (absolute arc indices)
-  DevBuf<uint32_t> succ;     // arcs [offsets[lo], offsets[hi])
-  uint64_t succ_base = 0;
   DevBuf<uint64_t> cnt[2];
   DevBuf<uint64_t> mod[2];
   DevBuf<double> est;
   DevBuf<double> block_sums;
   DevBuf<double> log_table;
-  DevBuf<uint32_t> order;
-  DevBuf<uint32_t> hub_node;
-  DevBuf<uint64_t> hub_begin, hub_end;
+  DevBuf<uint32_t> order;     // light nodes, descending out-degree
+  DevBuf<hanf::WarpTask> wtasks;
+  DevBuf<uint32_t> tos;       // task-ordered successor ids (see build_tasks)
+  uint64_t tos_words = 0;
+  uint32_t num_wtasks = 0;
+  DevBuf<uint32_t> hub_node;  // per hub chunk
   DevBuf<uint64_t> partials;
   DevBuf<uint32_t> hub_nodes, hub_first, hub_count;
   DevBuf<hanf::ReduceOut> reduce;
-  hanf::TaskTable tasks{};
   uint32_t num_hubs = 0;
+  int gather_mode = 1;        // union gathers: 0 words, 1 16-byte, 2 32-byte windows
 
   hanf::ReduceOut* h_reduce = nullptr;  // pinned: total + count
   double* h_block_sums = nullptr;       // pinned: exact_sum mode
@@ -121,6 +123,7 @@ struct hanf_engine {
   bool stale_valid = false;  // next[v] may lag where mod[cur] is set
   bool systolic = false;     // systolic_active(), engine.hpp:210-216
   double last_sum = 0.0;     // sum_estimates() of the current generation
+  uint64_t last_count = 0;   // modified count of the last step (n after seeding)
   std::vector<double> result_values;      // last run_to_stabilisation
   std::vector<uint64_t> result_modified;
   uint64_t launches = 0;
@@ -134,10 +137,9 @@ struct hanf_engine {
     for (auto& x : ev)
       if (x) cudaEventDestroy(x);
     if (device >= 0) cudaSetDevice(device);
-    offsets.free(); succ.free();
     for (int i = 0; i < 2; ++i) { cnt[i].free(); mod[i].free(); }
     est.free(); block_sums.free(); log_table.free(); order.free();
-    hub_node.free(); hub_begin.free(); hub_end.free(); partials.free();
+    wtasks.free(); tos.free(); hub_node.free(); partials.free();
     hub_nodes.free(); hub_first.free(); hub_count.free(); reduce.free();
     if (h_reduce) cudaFreeHost(h_reduce);
     if (h_block_sums) cudaFreeHost(h_block_sums);
@@ -147,119 +149,161 @@ struct hanf_engine {
 
 namespace {
 
-// Builds the warp-task table of the union kernel for nodes [lo, hi):
-// class 0 = hub chunks, classes 1..6 = G = 32..1 lanes per node, nodes in
-// descending out-degree (stable in node id).  Degree-0 nodes get no task:
-// their counter never changes and both generations hold it from seeding.
-hanf_status build_tasks(hanf_engine* e, const uint64_t* offsets) {
+// Builds the union sweep's work for nodes [lo, hi) (once per graph):
+//  - nodes with out-degree > kHubDegree: chunks of kHubChunk arcs, one warp
+//    each, plus one finalize warp per node (hub_nodes/first/count);
+//  - nodes with out-degree 1..kHubDegree ("light"): sorted by descending
+//    degree (stable in id), G = next_pow2(ceil(deg/32)) lanes per node,
+//    32/G nodes of one class per warp;
+//  - the task-ordered successor array: warp w owns rows [tos/32, +trips) of
+//    32 ids; lane (node slot j, sub) reads successor i*G + sub of node j in
+//    row i, or the zero row n past the end of the list.
+// Degree-0 nodes get no task: their counters never change and both
+// generations hold them from seeding.
+hanf_status build_tasks(hanf_engine* e, const uint64_t* offsets, const uint32_t* succ) {
   const uint64_t lo = e->lo, hi = e->hi;
   const uint32_t maxd = hanf::kHubDegree;
+  const uint32_t zero = static_cast<uint32_t>(e->n);
   std::vector<uint64_t> hist(maxd + 2, 0);
-  uint64_t hub_chunks = 0, hubs = 0;
+  std::vector<std::pair<uint64_t, uint32_t>> hub_list;
+  uint64_t hub_chunks = 0;
   for (uint64_t v = lo; v < hi; ++v) {
     const uint64_t d = offsets[v + 1] - offsets[v];
     if (d == 0) continue;
     if (d > maxd) {
-      ++hubs;
+      hub_list.emplace_back(d, static_cast<uint32_t>(v));
       hub_chunks += (d + hanf::kHubChunk - 1) / hanf::kHubChunk;
     } else {
       ++hist[d];
     }
+  }
+  std::stable_sort(hub_list.begin(), hub_list.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::vector<uint64_t> pos(maxd + 2, 0);
+  uint64_t light = 0;
+  for (uint64_t d = maxd; d >= 1; --d) {
+    pos[d] = light;
+    light += hist[d];
+  }
+  if (light > 0xffffffffull || hub_chunks > 0xffffffffull)
+    return fail(HANF_INVALID_ARGUMENT, "too many nodes in one engine shard");
+  std::vector<uint32_t> order(light ? light : 1);
+  std::vector<uint32_t> ldeg(light ? light : 1);
+  for (uint64_t v = lo; v < hi; ++v) {
+    const uint64_t d = offsets[v + 1] - offsets[v];
+    if (d == 0 || d > maxd) continue;
+    ldeg[pos[d]] = static_cast<uint32_t>(d);
+    order[pos[d]++] = static_cast<uint32_t>(v);
   }
   auto log2g_of = [](uint64_t d) {
     uint32_t g = 0;
     while ((32ull << g) < d) ++g;  // G = 2^g lanes, each <= 32 arcs
     return g;
   };
-  // class c (1..6) <-> log2g = 6 - c
-  uint64_t class_count[hanf::kNumClasses] = {};
-  for (uint64_t d = 1; d <= maxd; ++d) class_count[6 - log2g_of(d)] += hist[d];
-  // positions: descending degree => classes 1..6 in order, degrees high->low
-  std::vector<uint64_t> pos(maxd + 2, 0);
-  uint64_t p = 0;
-  for (uint64_t d = maxd; d >= 1; --d) {
-    pos[d] = p;
-    p += hist[d];
-  }
-  const uint64_t light = p;
-  std::vector<uint32_t> order(light ? light : 1);
+  // warp tasks: hub chunks first (longest nodes first), then light classes
+  std::vector<hanf::WarpTask> tasks;
+  tasks.reserve(hub_chunks + light / 1 + 1);
   std::vector<uint32_t> hub_node(hub_chunks ? hub_chunks : 1);
-  std::vector<uint64_t> hub_begin(hub_chunks ? hub_chunks : 1), hub_end(hub_chunks ? hub_chunks : 1);
-  std::vector<uint32_t> hubs_v(hubs ? hubs : 1), hubs_first(hubs ? hubs : 1), hubs_count(hubs ? hubs : 1);
-  // hubs in descending degree too
-  std::vector<std::pair<uint64_t, uint32_t>> hub_list;
-  hub_list.reserve(hubs);
-  for (uint64_t v = lo; v < hi; ++v) {
-    const uint64_t d = offsets[v + 1] - offsets[v];
-    if (d == 0) continue;
-    if (d > maxd)
-      hub_list.emplace_back(d, static_cast<uint32_t>(v));
-    else
-      order[pos[d]++] = static_cast<uint32_t>(v);
-  }
-  std::stable_sort(hub_list.begin(), hub_list.end(),
-                   [](const auto& a, const auto& b) { return a.first > b.first; });
-  uint64_t c = 0;
-  for (uint64_t h = 0; h < hub_list.size(); ++h) {
+  std::vector<uint64_t> chunk_begin(hub_chunks ? hub_chunks : 1);
+  std::vector<uint32_t> hubs_v(hub_list.size() + 1), hubs_first(hub_list.size() + 1),
+      hubs_count(hub_list.size() + 1);
+  uint64_t tos = 0, c = 0;
+  for (size_t h = 0; h < hub_list.size(); ++h) {
     const uint32_t v = hub_list[h].second;
     const uint64_t s = offsets[v], en = offsets[v + 1];
     hubs_v[h] = v;
     hubs_first[h] = static_cast<uint32_t>(c);
     uint32_t k = 0;
     for (uint64_t a = s; a < en; a += hanf::kHubChunk, ++k, ++c) {
+      const uint64_t len = std::min<uint64_t>(hanf::kHubChunk, en - a);
       hub_node[c] = v;
-      hub_begin[c] = a;
-      hub_end[c] = std::min<uint64_t>(en, a + hanf::kHubChunk);
+      chunk_begin[c] = a;
+      const uint16_t trips = static_cast<uint16_t>((len + 31) / 32);
+      tasks.push_back(hanf::WarpTask{tos, static_cast<uint32_t>(c), trips, 5, 0});
+      tos += 32ull * trips;
     }
     hubs_count[h] = k;
   }
-  if (light > 0xffffffffull || hub_chunks > 0xffffffffull)
-    return fail(HANF_INVALID_ARGUMENT, "too many nodes in one engine shard");
-
-  hanf::TaskTable& tt = e->tasks;
-  uint64_t warps = 0, items = 0;
-  tt.warp_begin[0] = 0;
-  tt.item_begin[0] = 0;
-  tt.item_end[0] = static_cast<uint32_t>(hub_chunks);
-  tt.log2g[0] = 5;
-  warps += hub_chunks;
-  for (int k = 1; k < hanf::kNumClasses; ++k) {
-    const uint32_t lg = 6 - k;
-    tt.log2g[k] = lg;
-    tt.warp_begin[k] = static_cast<uint32_t>(warps);
-    tt.item_begin[k] = static_cast<uint32_t>(items);
-    items += class_count[k];
-    tt.item_end[k] = static_cast<uint32_t>(items);
-    const uint64_t per = 32u >> lg;
-    warps += (class_count[k] + per - 1) / per;
+  for (uint64_t i = 0; i < light;) {
+    const uint32_t lg = log2g_of(ldeg[i]);
+    const uint32_t per = 32u >> lg;
+    uint64_t cnt = 0;
+    while (cnt < per && i + cnt < light && log2g_of(ldeg[i + cnt]) == lg) ++cnt;
+    const uint32_t G = 1u << lg;
+    const uint16_t trips = static_cast<uint16_t>((ldeg[i] + G - 1) / G);
+    tasks.push_back(hanf::WarpTask{tos, static_cast<uint32_t>(i), trips,
+                                   static_cast<uint8_t>(lg), static_cast<uint8_t>(cnt)});
+    tos += 32ull * trips;
+    i += cnt;
   }
-  if (warps > 0x7fffffffull / 32) return fail(HANF_INVALID_ARGUMENT, "task table overflow");
-  tt.warp_begin[hanf::kNumClasses] = static_cast<uint32_t>(warps);
-  e->num_hubs = static_cast<uint32_t>(hubs);
-
-  cudaStream_t s = e->stream;
+  if (tasks.size() > 0x7fffffffull / 32) return fail(HANF_INVALID_ARGUMENT, "task table overflow");
+  std::vector<uint32_t> tos_ids;
+  try {
+    tos_ids.assign(tos ? tos : 1, zero);
+  } catch (const std::bad_alloc&) {
+    return fail(HANF_OUT_OF_MEMORY, "task-ordered successor array allocation failed");
+  }
+  auto fill = [&](uint64_t t0, uint64_t t1) {
+    for (uint64_t t = t0; t < t1; ++t) {
+      const hanf::WarpTask& w = tasks[t];
+      uint32_t* dst = tos_ids.data() + w.tos;
+      if (w.nodes == 0) {
+        const uint64_t a = chunk_begin[w.item];
+        const uint64_t len = std::min<uint64_t>(hanf::kHubChunk, offsets[hub_node[w.item] + 1] - a);
+        for (uint64_t k = 0; k < len; ++k) dst[k] = succ[a + k];
+      } else {
+        const uint32_t G = 1u << w.lg;
+        for (uint32_t j = 0; j < w.nodes; ++j) {
+          const uint32_t v = order[w.item + j];
+          const uint64_t s = offsets[v], d = offsets[v + 1] - s;
+          for (uint64_t k = 0; k < d; ++k) {
+            const uint64_t i = k / G, sub = k % G;
+            dst[32 * i + j * G + sub] = succ[s + k];
+          }
+        }
+      }
+    }
+  };
+  {
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const uint64_t T = tasks.size();
+    if (T > 4096 && nt > 1) {
+      std::vector<std::thread> pool;
+      for (unsigned p = 0; p < nt; ++p) pool.emplace_back(fill, T * p / nt, T * (p + 1) / nt);
+      for (auto& th : pool) th.join();
+    } else {
+      fill(0, T);
+    }
+  }
+  e->num_wtasks = static_cast<uint32_t>(tasks.size());
+  e->num_hubs = static_cast<uint32_t>(hub_list.size());
+  e->tos_words = tos;
+  cudaStream_t st = e->stream;
   HANF_CUDA(e->order.alloc(order.size()));
   HANF_CUDA(cudaMemcpyAsync(e->order.p, order.data(), sizeof(uint32_t) * order.size(),
-                            cudaMemcpyHostToDevice, s));
+                            cudaMemcpyHostToDevice, st));
+  HANF_CUDA(e->wtasks.alloc(tasks.size()));
+  if (!tasks.empty())
+    HANF_CUDA(cudaMemcpyAsync(e->wtasks.p, tasks.data(), sizeof(hanf::WarpTask) * tasks.size(),
+                              cudaMemcpyHostToDevice, st));
+  HANF_CUDA(e->tos.alloc(tos_ids.size()));
+  HANF_CUDA(cudaMemcpyAsync(e->tos.p, tos_ids.data(), sizeof(uint32_t) * tos_ids.size(),
+                            cudaMemcpyHostToDevice, st));
   HANF_CUDA(e->hub_node.alloc(hub_node.size()));
-  HANF_CUDA(e->hub_begin.alloc(hub_begin.size()));
-  HANF_CUDA(e->hub_end.alloc(hub_end.size()));
   HANF_CUDA(cudaMemcpyAsync(e->hub_node.p, hub_node.data(), sizeof(uint32_t) * hub_node.size(),
-                            cudaMemcpyHostToDevice, s));
-  HANF_CUDA(cudaMemcpyAsync(e->hub_begin.p, hub_begin.data(), sizeof(uint64_t) * hub_begin.size(),
-                            cudaMemcpyHostToDevice, s));
-  HANF_CUDA(cudaMemcpyAsync(e->hub_end.p, hub_end.data(), sizeof(uint64_t) * hub_end.size(),
-                            cudaMemcpyHostToDevice, s));
+                            cudaMemcpyHostToDevice, st));
   HANF_CUDA(e->partials.alloc(static_cast<size_t>(hub_chunks ? hub_chunks : 1) * e->words));
   HANF_CUDA(e->hub_nodes.alloc(hubs_v.size()));
   HANF_CUDA(e->hub_first.alloc(hubs_first.size()));
   HANF_CUDA(e->hub_count.alloc(hubs_count.size()));
   HANF_CUDA(cudaMemcpyAsync(e->hub_nodes.p, hubs_v.data(), sizeof(uint32_t) * hubs_v.size(),
-                            cudaMemcpyHostToDevice, s));
+                            cudaMemcpyHostToDevice, st));
   HANF_CUDA(cudaMemcpyAsync(e->hub_first.p, hubs_first.data(), sizeof(uint32_t) * hubs_first.size(),
-                            cudaMemcpyHostToDevice, s));
+                            cudaMemcpyHostToDevice, st));
   HANF_CUDA(cudaMemcpyAsync(e->hub_count.p, hubs_count.data(), sizeof(uint32_t) * hubs_count.size(),
-                            cudaMemcpyHostToDevice, s));
+                            cudaMemcpyHostToDevice, st));
+  // the staging vectors are freed on return: make sure the copies are done
+  HANF_CUDA(cudaStreamSynchronize(st));
   return HANF_OK;
 }
 
@@ -334,6 +378,7 @@ hanf_status seed_all(hanf_engine* e) {
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
   if (st != HANF_OK) return st;
   uint64_t count = 0;
+  e->last_count = e->n;
   return reduce_totals(e, e->mod[0].p, &e->last_sum, &count);
 }
 
@@ -353,24 +398,30 @@ hanf_status compute_local(hanf_engine* e) {
   HANF_CUDA(cudaMemsetAsync(e->mod[ng].p + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
   hanf::UnionArgs a{};
-  a.offsets = e->offsets.p - e->lo;
-  a.succ = e->succ.p;
-  a.succ_base = e->succ_base;
+  a.tos = e->tos.p;
+  a.wtasks = e->wtasks.p;
+  a.num_wtasks = e->num_wtasks;
+  a.zero_row = static_cast<uint32_t>(e->n);
+  const bool fused = hanf::fused_estimates(e->params.register_bits, e->params.registers);
+  a.est = fused ? e->est.p : nullptr;
+  a.ep = hanf::EstimateParams{e->params.alpha, static_cast<double>(e->params.registers),
+                              e->params.registers, e->params.register_bits,
+                              e->params.words_per_counter, e->log_table.p};
   a.cur = e->cnt[g].p;
   a.next = e->cnt[ng].p;
   a.mod_cur = e->mod[g].p;
   a.mod_next = e->mod[ng].p;
   a.order = e->order.p;
   a.hub_node = e->hub_node.p;
-  a.hub_begin = e->hub_begin.p;
-  a.hub_end = e->hub_end.p;
   a.partials = e->partials.p;
   a.words = e->params.words_per_counter;
-  a.check_mod = (e->cfg.track_modified && e->t > 0) ? 1 : 0;
+  // skipping unmodified successors costs a bitmap probe per arc and saves
+  // a counter gather per skipped arc: worth it once most counters settled
+  a.check_mod = (e->cfg.track_modified && e->t > 0 &&
+                 2 * e->last_count < e->n) ? 1 : 0;
   a.stale_valid = e->stale_valid ? 1 : 0;
-  a.tasks = e->tasks;
-  HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers, e->stream,
-                               &e->launches));
+  HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers,
+                               e->gather_mode, e->stream, &e->launches));
   hanf::HubArgs h{};
   h.cur = a.cur;
   h.next = a.next;
@@ -383,11 +434,18 @@ hanf_status compute_local(hanf_engine* e) {
   h.num_hubs = e->num_hubs;
   h.words = a.words;
   h.stale_valid = a.stale_valid;
+  h.est = a.est;
+  h.ep = a.ep;
   HANF_CUDA(hanf::launch_hub_finalize(h, e->params.register_bits, e->params.registers,
                                       e->stream, &e->launches));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
-  const hanf_status st = run_estimates(e, ng, e->mod[ng].p, w0, w1);
-  if (st != HANF_OK) return st;
+  if (fused) {
+    HANF_CUDA(hanf::launch_block_sums(e->est.p, e->mod[ng].p, e->block_sums.p, e->n, w0, w1,
+                                      e->stream, &e->launches));
+  } else {
+    const hanf_status st = run_estimates(e, ng, e->mod[ng].p, w0, w1);
+    if (st != HANF_OK) return st;
+  }
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   return HANF_OK;
 }
@@ -405,6 +463,7 @@ hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
     e->systolic = true;                            // engine.hpp:211-216
   ++e->t;
   e->last_sum = total;
+  e->last_count = count;
   rep->sum = total;
   rep->modified = count;
   return HANF_OK;
@@ -493,9 +552,15 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
 
   HANF_TRY(cudaSetDevice(cfg.device));
   HANF_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-  const uint64_t nw = n * e->words;
+  // row n is an all-zero counter (the union kernels' padding target); 8
+  // extra words keep the 256-bit window loads of the last rows in bounds
+  const uint64_t nw = (n + 1) * e->words + 8;
   HANF_TRY(e->cnt[0].alloc(nw));
   HANF_TRY(e->cnt[1].alloc(nw));
+  HANF_TRY(cudaMemsetAsync(e->cnt[0].p + n * e->words, 0, sizeof(uint64_t) * (e->words + 8),
+                           e->stream));
+  HANF_TRY(cudaMemsetAsync(e->cnt[1].p + n * e->words, 0, sizeof(uint64_t) * (e->words + 8),
+                           e->stream));
   HANF_TRY(e->mod[0].alloc(e->blocks));
   HANF_TRY(e->mod[1].alloc(e->blocks));
   HANF_TRY(e->est.alloc(n));
@@ -505,23 +570,16 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   if (cfg.exact_sum)
     HANF_TRY(cudaMallocHost(&e->h_block_sums, sizeof(double) * (e->blocks ? e->blocks : 1)));
 
-  // CSR of the shard: offsets[lo..hi], arcs [offsets[lo], offsets[hi])
+  // the CSR itself is not kept on the device: build_tasks lays the shard's
+  // successor ids out in task order (the only form the union sweep reads)
   if (n > 0) {
-    HANF_TRY(e->offsets.alloc(hi - lo + 1));
-    HANF_TRY(cudaMemcpyAsync(e->offsets.p, g->offsets + lo, sizeof(uint64_t) * (hi - lo + 1),
-                             cudaMemcpyHostToDevice, e->stream));
-    e->succ_base = g->offsets[lo];
-    const uint64_t arcs = g->offsets[hi] - g->offsets[lo];
-    HANF_TRY(e->succ.alloc(arcs));
-    if (arcs)
-      HANF_TRY(cudaMemcpyAsync(e->succ.p, g->arcs + e->succ_base, sizeof(uint32_t) * arcs,
-                               cudaMemcpyHostToDevice, e->stream));
     for (uint64_t v = lo; v < hi; ++v)
       if (g->offsets[v + 1] < g->offsets[v])
         return bail(fail(HANF_INVALID_ARGUMENT, "offsets must be non-decreasing"));
     for (uint64_t i = g->offsets[lo]; i < g->offsets[hi]; ++i)
       if (g->arcs[i] >= n) return bail(fail(HANF_INVALID_ARGUMENT, "arc endpoint out of range"));
   }
+  if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
 
   // linear-counting table m*log(m/z), same expression as hll.hpp:139
   {
@@ -534,7 +592,7 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
                         cudaMemcpyHostToDevice));
   }
   if (n > 0) {
-    st = build_tasks(e, g->offsets);
+    st = build_tasks(e, g->offsets, g->arcs);
     if (st != HANF_OK) return bail(st);
     st = seed_all(e);
     if (st != HANF_OK) return bail(st);

@@ -6,42 +6,41 @@
 
 #include <cstdint>
 
+#include "hanf_device.cuh"
+
 namespace hanf {
 
-// Warp-task classes of the union kernel.
-// Class 0 holds hub chunks (one warp per <= kHubChunk arcs of a node with
-// out-degree > kHubDegree, writing a partial counter); classes 1..6 hold
-// nodes handled by G = 32, 16, 8, 4, 2, 1 lanes each, ordered by
-// descending degree so the longest tasks start first.
-constexpr int kNumClasses = 7;
+// Union sweep work decomposition (see hanf_kernels.cu and build_tasks):
+// nodes with out-degree > kHubDegree are split into chunks of kHubChunk arcs.
 constexpr uint32_t kHubDegree = 1024;
 constexpr uint32_t kHubChunk = 1024;
 
-struct TaskTable {
-  uint32_t warp_begin[kNumClasses + 1];  // prefix of warp counts; [7] = total warps
-  uint32_t item_begin[kNumClasses];      // first index into order[] / hub arrays
-  uint32_t item_end[kNumClasses];
-  uint32_t log2g[kNumClasses];           // lanes per node = 1 << log2g
+struct WarpTask {      // 16 bytes, one per warp of the union launch
+  uint64_t tos;        // first id of this warp in the task-ordered successor array
+  uint32_t item;       // light: first index into order[]; hub: chunk index
+  uint16_t trips;      // id rows of 32 (= max successors per lane)
+  uint8_t lg;          // log2(lanes per node)
+  uint8_t nodes;       // light: nodes in this warp (<= 32 >> lg); 0 = hub chunk
 };
 
 struct UnionArgs {
-  const uint64_t* offsets;   // CSR offsets (global node ids, absolute arc index)
-  const uint32_t* succ;      // CSR successor ids
+  const uint32_t* tos;       // task-ordered successor ids
+  const WarpTask* wtasks;
+  uint32_t num_wtasks;
   const uint64_t* cur;       // generation t (read only)
   uint64_t* next;            // generation t+1
   const uint64_t* mod_cur;   // bitmap: counters changed by the previous step
   uint64_t* mod_next;        // bitmap: counters changed by this step (pre-zeroed)
-  const uint32_t* order;     // node ids of classes 1..6
+  const uint32_t* order;     // node ids of light tasks
   const uint32_t* hub_node;  // per hub chunk: node
-  const uint64_t* hub_begin; // per hub chunk: arc range
-  const uint64_t* hub_end;
   uint64_t* partials;        // per hub chunk: partial counter (W words)
-  uint64_t succ_base;        // arc index of succ[0] (shard-local CSR)
   uint32_t words;            // W
   uint32_t chunks;           // chunks per counter
+  uint32_t zero_row;         // index of the all-zero counter row (= n)
   int32_t check_mod;         // skip successors whose bit is clear in mod_cur
   int32_t stale_valid;       // next[v] may be stale where mod_cur[v] is set
-  TaskTable tasks;
+  double* est;               // per-counter estimates (nullptr: not fused)
+  EstimateParams ep;
 };
 
 struct HubArgs {
@@ -57,6 +56,8 @@ struct HubArgs {
   uint32_t words;
   uint32_t chunks;
   int32_t stale_valid;
+  double* est;
+  EstimateParams ep;
 };
 
 struct EstimateArgs {
@@ -82,10 +83,16 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint32_t register_bits, uint32_t words, uint64_t seed,
                         cudaStream_t s, uint64_t* launches);
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits,
-                         uint32_t registers, cudaStream_t s, uint64_t* launches);
+                         uint32_t registers, int gather_mode, cudaStream_t s,
+                         uint64_t* launches);
 cudaError_t launch_hub_finalize(const HubArgs& args, uint32_t register_bits,
                                 uint32_t registers, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* launches);
+// true when the union kernels compute estimates themselves (single-chunk layouts)
+bool fused_estimates(uint32_t register_bits, uint32_t registers);
+cudaError_t launch_block_sums(const double* est, const uint64_t* dirty, double* block_sums,
+                              uint64_t n, uint64_t b0, uint64_t b1, cudaStream_t s,
+                              uint64_t* launches);
 constexpr int kReduceCtas = 296;
 constexpr int kReduceThreads = 256;
 struct ReduceOut {

@@ -84,116 +84,152 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
 }
 
 // ---------------------------------------------------------------------------
-// Union sweep.  One launch covers every node with out-degree >= 1:
-//   class 0      hub chunks: a warp takes <= kHubChunk arcs of one node and
-//                writes the partial maximum to `partials`;
-//   classes 1-6  G = 32..1 lanes per node (G = next_pow2(ceil(deg/32)), so
-//                every lane walks <= 32 arcs), nodes in descending degree.
-// Each lane keeps a running register file in 32-bit limbs and folds in
-// successor counters U at a time (U independent gathers in flight); the G
-// lanes of a node then combine with butterfly shuffles.  The lead lane
-// compares with the old counter (changed == any register grew), writes the
-// next generation where it changed or where next[v] is stale, and sets the
-// node's bit in mod_next.
+// Union sweep.  One launch covers every node with out-degree >= 1, one warp
+// per WarpTask (built once per graph, hanf_engine.cu build_tasks):
+//   light task  32/G nodes with G = next_pow2(ceil(deg/32)) lanes each (so a
+//               lane walks <= 32 arcs), nodes of equal class in descending
+//               degree;
+//   hub chunk   <= kHubChunk arcs of one node with out-degree > kHubDegree;
+//               the warp writes its partial maximum to `partials`.
+// The successor ids are read from the task-ordered successor array (TOS):
+// warp row i holds the 32 ids its lanes fold in trip i (lane = node slot *
+// G + sub, id = successor i*G + sub of that node; padding = the all-zero
+// counter row n), so every id row is one coalesced 128-byte load and the
+// trip count is warp-uniform.  Each lane keeps a running register file in
+// 32-bit limbs and folds U successor counters per trip (swar_max); the G
+// lanes of a node combine with butterfly shuffles; the lead lane compares
+// with the old counter, writes the next generation where it changed or
+// where next[v] is stale, estimates a changed counter from its registers
+// (single-chunk layouts) and sets the node's bit in mod_next.
+// Successor gathers: GMODE 0 = per-word loads, 1 = 16-byte windows,
+// 2 = 32-byte windows (fewer L1 wavefronts, more selects).
 // ---------------------------------------------------------------------------
 template <class Lay>
 __device__ __forceinline__ void zero_limbs(uint32_t (&x)[Lay::kLimbs]) {
   sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = 0u; });
 }
 
-template <int R, int NREG, int U, bool kVec16>
+template <class Lay, int GMODE, bool kVec16>
+struct Gather;
+
+template <class Lay, bool kVec16>
+struct Gather<Lay, 0, kVec16> {
+  uint32_t v[Lay::kLimbs];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
+                                        uint32_t woff) {
+    load_chunk<Lay, kVec16>(v, cur + static_cast<uint64_t>(w) * words + woff);
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
+    sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = v[decltype(I)::value]; });
+  }
+};
+
+template <class Lay, bool kVec16>
+struct Gather<Lay, 1, kVec16> {
+  uint4 raw[Window128<Lay::kWords>::kLoads];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t) {
+    window128_load<Lay::kWords>(raw, cur, w);
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
+    window128_extract<Lay, Lay::kWords>(x, raw, w);
+  }
+};
+
+template <class Lay, bool kVec16>
+struct Gather<Lay, 2, kVec16> {
+  uint32_t raw[Window<Lay::kWords>::kLoads][8];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t) {
+    window_load<Lay::kWords>(raw, cur, w);
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
+    window_extract<Lay, Lay::kWords>(x, raw, w);
+  }
+};
+
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+template <int R, int NREG, int U, int GMODE, bool kVec16>
 __global__ void __launch_bounds__(256) union_kernel(const UnionArgs args) {
   using Lay = Layout<R, NREG>;
   constexpr int NL = Lay::kLimbs;
   constexpr int NW = Lay::kWords;
-  const TaskTable& tt = args.tasks;
+  using G_t = Gather<Lay, GMODE, kVec16>;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  if (gw >= tt.warp_begin[kNumClasses]) return;
-  int c = 0;
-#pragma unroll
-  for (int k = 1; k < kNumClasses; ++k)
-    if (gw >= tt.warp_begin[k]) c = k;
-  const uint32_t lg = tt.log2g[c];
+  if (gw >= args.num_wtasks) return;
+  const WarpTask task = args.wtasks[gw];
+  const bool hub = task.nodes == 0;
+  const uint32_t lg = hub ? 5u : task.lg;
   const uint32_t G = 1u << lg;
   const uint32_t sub = lane & (G - 1);
-  const bool hub = c == 0;
-  const uint32_t wi = gw - tt.warp_begin[c];
-
-  uint32_t item, v = 0;
-  uint64_t s = 0, e = 0;
-  bool active;
+  const uint32_t zero_row = args.zero_row;
+  uint32_t v = zero_row;
+  bool active = true;
   if (hub) {
-    item = tt.item_begin[0] + wi;
-    active = true;
-    v = args.hub_node[item];
-    s = args.hub_begin[item];
-    e = args.hub_end[item];
+    v = args.hub_node[task.item];
   } else {
-    item = tt.item_begin[c] + wi * (32u >> lg) + (lane >> lg);
-    active = item < tt.item_end[c];
-    if (active) {
-      v = args.order[item];
-      s = args.offsets[v];
-      e = args.offsets[v + 1];
-    }
+    const uint32_t j = lane >> lg;
+    active = j < task.nodes;
+    if (active) v = args.order[task.item + j];
   }
   const bool lead = active && sub == 0 && !hub;
   bool stale = false;
   if (lead && args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
   const uint64_t* __restrict__ cur = args.cur;
-  const uint32_t* __restrict__ succ = args.succ - args.succ_base;
+  const uint32_t* __restrict__ ids = args.tos + task.tos + lane;
   const uint32_t words = args.words;
+  const uint32_t trips = task.trips;
 
   bool any_changed = false;
   for (uint32_t ch = 0; ch < args.chunks; ++ch) {
     const uint32_t woff = ch * NW;
     uint32_t acc[NL];
-    if (lead)
-      load_chunk<Lay, kVec16>(acc, cur + static_cast<uint64_t>(v) * words + woff);
-    else
-      zero_limbs<Lay>(acc);
-
-    for (uint64_t k = s + sub; k < e; k += static_cast<uint64_t>(G) * U) {
+    uint32_t own[NL];
+    {
+      G_t g;
+      g.issue(cur, lead ? v : zero_row, words, woff);
+      g.extract(own, lead ? v : zero_row);
+    }
+    sfor<0, NL>([&](auto I) { acc[decltype(I)::value] = own[decltype(I)::value]; });
+    for (uint32_t i = 0; i < trips; i += U) {
       uint32_t w[U];
-      bool ok[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const uint64_t kk = k + static_cast<uint64_t>(j) * G;
-        ok[j] = kk < e;
-        w[j] = ok[j] ? __ldg(succ + kk) : 0u;
-      }
+      for (int j = 0; j < U; ++j)
+        w[j] = (i + j < trips) ? ld_stream_u32(ids + 32 * (i + j)) : zero_row;
       if (args.check_mod) {
 #pragma unroll
         for (int j = 0; j < U; ++j)
-          if (ok[j]) ok[j] = (__ldg(args.mod_cur + (w[j] >> 6)) >> (w[j] & 63)) & 1;
+          if (!((__ldg(args.mod_cur + (w[j] >> 6)) >> (w[j] & 63)) & 1)) w[j] = zero_row;
       }
-      uint32_t y[U][NL];
+      G_t g[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) g[j].issue(cur, w[j], words, woff);
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        if (ok[j])
-          load_chunk<Lay, kVec16>(y[j], cur + static_cast<uint64_t>(w[j]) * words + woff);
-        else
-          zero_limbs<Lay>(y[j]);
+        uint32_t y[NL];
+        g[j].extract(y, w[j]);
+        swar_max<Lay>(acc, y);
       }
-#pragma unroll
-      for (int j = 0; j < U; ++j) swar_max<Lay>(acc, y[j]);
     }
     for (uint32_t off = G >> 1; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
 
     if (hub) {
       if (lane == 0)
-        store_chunk<Lay, kVec16>(args.partials + static_cast<uint64_t>(item) * words + woff, acc);
-    } else if (lead) {
-      uint32_t own[NL];
-      load_chunk<Lay, kVec16>(own, cur + static_cast<uint64_t>(v) * words + woff);
-      const bool changed = limbs_differ<Lay>(acc, own);
+        store_chunk<Lay, kVec16>(args.partials + static_cast<uint64_t>(task.item) * words + woff,
+                                 acc);
+    } else {
+      const bool changed = lead && limbs_differ<Lay>(acc, own);
       any_changed |= changed;
-      if (changed || stale)
+      if (changed || (lead && stale))
         store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
+      if (changed && args.est) args.est[v] = estimate_limbs<Lay>(acc, args.ep);
     }
   }
-  if (lead && any_changed)
+  if (any_changed)
     atomicOr(reinterpret_cast<unsigned long long*>(args.mod_next) + (v >> 6),
              1ull << (v & 63));
 }
@@ -234,6 +270,7 @@ __global__ void __launch_bounds__(256) hub_finalize_kernel(const HubArgs args) {
       any_changed |= changed;
       if (changed || stale)
         store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
+      if (changed && args.est) args.est[v] = estimate_limbs<Lay>(acc, args.ep);
     }
   }
   if (lane == 0 && any_changed)
@@ -261,19 +298,20 @@ KernelChoice choose(uint32_t r, uint32_t m) {
   }
 }
 
-template <int R, int NREG, int U, bool V>
+template <int R, int NREG, int U, int GM, bool V>
 cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   a.chunks = chunks;
-  const uint32_t warps = a.tasks.warp_begin[kNumClasses];
-  if (warps == 0) return cudaSuccess;
-  const uint32_t blocks = (warps + 7) / 8;
-  union_kernel<R, NREG, U, V><<<blocks, 256, 0, s>>>(a);
+  if (chunks != 1) a.est = nullptr;  // estimates need the whole counter in registers
+  if (a.num_wtasks == 0) return cudaSuccess;
+  const uint32_t blocks = (a.num_wtasks + 7) / 8;
+  union_kernel<R, NREG, U, GM, V><<<blocks, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int R, int NREG, bool V>
 cudaError_t hub_launch(HubArgs a, uint32_t chunks, cudaStream_t s) {
   a.chunks = chunks;
+  if (chunks != 1) a.est = nullptr;
   if (a.num_hubs == 0) return cudaSuccess;
   const uint32_t blocks = (a.num_hubs + 7) / 8;
   hub_finalize_kernel<R, NREG, V><<<blocks, 256, 0, s>>>(a);
@@ -281,23 +319,36 @@ cudaError_t hub_launch(HubArgs a, uint32_t chunks, cudaStream_t s) {
 }
 }  // namespace
 
+bool fused_estimates(uint32_t register_bits, uint32_t registers) {
+  return choose(register_bits, registers).chunks == 1;
+}
+
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t registers,
-                         cudaStream_t s, uint64_t* launches) {
+                         int gather_mode, cudaStream_t s, uint64_t* launches) {
   const KernelChoice k = choose(register_bits, registers);
-  if (args.tasks.warp_begin[kNumClasses] == 0) return cudaSuccess;
+  if (args.num_wtasks == 0) return cudaSuccess;
   ++*launches;
   const uint32_t ch = static_cast<uint32_t>(k.chunks);
+  const bool single = ch == 1;
   switch (k.r * 1000 + k.nreg) {
-    case 5016: return union_launch<5, 16, 4, true>(args, ch, s);
-    case 5032: return union_launch<5, 32, 4, false>(args, ch, s);
-    case 5064: return union_launch<5, 64, 4, false>(args, ch, s);
-    case 5128: return union_launch<5, 128, 2, true>(args, ch, s);
-    case 6016: return union_launch<6, 16, 4, true>(args, ch, s);
-    case 6032: return union_launch<6, 32, 4, false>(args, ch, s);
-    case 7016: return union_launch<7, 16, 4, true>(args, ch, s);
-    case 7032: return union_launch<7, 32, 4, true>(args, ch, s);
-    case 7064: return union_launch<7, 64, 2, false>(args, ch, s);
-    default: return union_launch<8, 16, 4, true>(args, ch, s);
+    case 5016: return union_launch<5, 16, 4, 0, true>(args, ch, s);
+    case 5032:
+      if (single && gather_mode == 2) return union_launch<5, 32, 4, 2, false>(args, ch, s);
+      if (single && gather_mode == 1) return union_launch<5, 32, 4, 1, false>(args, ch, s);
+      return union_launch<5, 32, 4, 0, false>(args, ch, s);
+    case 5064:
+      if (single && gather_mode == 2) return union_launch<5, 64, 4, 2, false>(args, ch, s);
+      if (single && gather_mode == 1) return union_launch<5, 64, 4, 1, false>(args, ch, s);
+      return union_launch<5, 64, 4, 0, false>(args, ch, s);
+    case 5128:
+      if (gather_mode == 2) return union_launch<5, 128, 2, 2, true>(args, ch, s);
+      return union_launch<5, 128, 2, 0, true>(args, ch, s);
+    case 6016: return union_launch<6, 16, 4, 0, true>(args, ch, s);
+    case 6032: return union_launch<6, 32, 4, 0, false>(args, ch, s);
+    case 7016: return union_launch<7, 16, 4, 0, true>(args, ch, s);
+    case 7032: return union_launch<7, 32, 4, 0, true>(args, ch, s);
+    case 7064: return union_launch<7, 64, 2, 0, false>(args, ch, s);
+    default: return union_launch<8, 16, 4, 0, true>(args, ch, s);
   }
 }
 
@@ -319,6 +370,44 @@ cudaError_t launch_hub_finalize(const HubArgs& args, uint32_t register_bits, uin
     case 7064: return hub_launch<7, 64, false>(args, ch, s);
     default: return hub_launch<8, 16, true>(args, ch, s);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Block sums from cached estimates (union kernels wrote est[v] for every
+// changed counter): one thread per 64-counter block, sequential in index
+// order (engine.hpp:109-111); clean blocks keep their cached sum (:105).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+block_sum_kernel(const double* __restrict__ est, const uint64_t* __restrict__ dirty,
+                 double* __restrict__ block_sums, uint64_t n, uint64_t b0, uint64_t b1) {
+  const uint64_t b = b0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (b >= b1) return;
+  if (dirty[b] == 0) return;
+  const uint64_t first = b * 64;
+  const uint32_t last = n - first < 64 ? static_cast<uint32_t>(n - first) : 64u;
+  double sum = 0.0;
+  if (last == 64) {
+    const double2* p = reinterpret_cast<const double2*>(est + first);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double2 q = __ldg(p + k);
+      sum = __dadd_rn(sum, q.x);
+      sum = __dadd_rn(sum, q.y);
+    }
+  } else {
+    for (uint32_t i = 0; i < last; ++i) sum = __dadd_rn(sum, est[first + i]);
+  }
+  block_sums[b] = sum;
+}
+
+cudaError_t launch_block_sums(const double* est, const uint64_t* dirty, double* block_sums,
+                              uint64_t n, uint64_t b0, uint64_t b1, cudaStream_t s,
+                              uint64_t* launches) {
+  if (b1 <= b0) return cudaSuccess;
+  const uint64_t blocks = (b1 - b0 + 255) / 256;
+  block_sum_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(est, dirty, block_sums, n, b0, b1);
+  ++*launches;
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
