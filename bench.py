@@ -261,7 +261,6 @@ def main():
     for _ in range(args.warmup):
         engine.reset()
         do_step()
-    engine.set_timing(True)
     step_launches = 0
     total_ms = 0.0
     barrier()
@@ -280,7 +279,16 @@ def main():
             total_ms += start.elapsed_time(end)
             step_launches += engine.launch_count() - launches_before  # the step's kernels only
     barrier()
+    # kernel phases for the roofline: CUDA events between the kernels on the
+    # engine stream (ungraphed steps, same kernels), same flush protocol
+    engine.set_timing(True)
+    for _ in range(max(3, min(args.steps, 10))):
+        engine.reset()
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        do_step()
     timing = engine.timing()
+    engine.set_timing(False)
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -342,11 +350,12 @@ def main():
                        "sum_mode": "device (deterministic tree)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "union sweep (union_kernel + hub_finalize)",
+                         "kernel": "union_kernel (successor gather + broadword max + fused estimator)",
                          "kernel_ms": union_ms, "algorithmic_bytes": B,
                          "peak_source": peak_src,
-                         "phases_ms": {k: timing[k] / max(1, timing["steps"])
-                                       for k in ("union_ms", "estimate_ms", "reduce_ms")}},
+                         "phases_ms": {"union": timing["union_ms"] / max(1, timing["steps"]),
+                                       "estimate": timing["estimate_ms"] / max(1, timing["steps"]),
+                                       "finish": timing["reduce_ms"] / max(1, timing["steps"])}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": step_launches,

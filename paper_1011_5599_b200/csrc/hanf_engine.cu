@@ -110,10 +110,12 @@ struct hanf_engine {
   uint32_t num_wtasks = 0;
   DevBuf<uint32_t> hub_node;  // per hub chunk
   DevBuf<uint64_t> partials;
-  DevBuf<uint32_t> hub_nodes, hub_first, hub_count;
+  DevBuf<uint32_t> hub_nodes, hub_first, hub_count, chunk_hub, hub_ticket;
   DevBuf<hanf::ReduceOut> reduce;
+  DevBuf<double> reduce_sums;
+  DevBuf<unsigned long long> reduce_counts;
   uint32_t num_hubs = 0;
-  int gather_mode = 1;        // union gathers: 0 words, 1 16-byte, 2 32-byte windows
+  int gather_mode = -1;       // union kernel variant (-1: per-layout default)
 
   hanf::ReduceOut* h_reduce = nullptr;  // pinned: total + count
   double* h_block_sums = nullptr;       // pinned: exact_sum mode
@@ -132,15 +134,27 @@ struct hanf_engine {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double union_ms = 0.0, estimate_ms = 0.0, reduce_ms = 0.0;
   uint64_t timed_steps = 0;
+  // CUDA graphs of the single-GPU step: [cur][check_mod][stale_valid]
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t kernels = 0;
+  };
+  StepGraph graphs[2][2][2];
+  bool use_graphs = true;
 
   ~hanf_engine() {
+    for (auto& a : graphs)
+      for (auto& b : a)
+        for (auto& c : b)
+          if (c.exec) cudaGraphExecDestroy(c.exec);
     for (auto& x : ev)
       if (x) cudaEventDestroy(x);
     if (device >= 0) cudaSetDevice(device);
     for (int i = 0; i < 2; ++i) { cnt[i].free(); mod[i].free(); }
     est.free(); block_sums.free(); log_table.free(); order.free();
     wtasks.free(); tos.free(); hub_node.free(); partials.free();
-    hub_nodes.free(); hub_first.free(); hub_count.free(); reduce.free();
+    hub_nodes.free(); hub_first.free(); hub_count.free(); chunk_hub.free(); hub_ticket.free();
+    reduce.free(); reduce_sums.free(); reduce_counts.free();
     if (h_reduce) cudaFreeHost(h_reduce);
     if (h_block_sums) cudaFreeHost(h_block_sums);
     if (stream) cudaStreamDestroy(stream);
@@ -204,6 +218,7 @@ hanf_status build_tasks(hanf_engine* e, const uint64_t* offsets, const uint32_t*
   std::vector<hanf::WarpTask> tasks;
   tasks.reserve(hub_chunks + light / 1 + 1);
   std::vector<uint32_t> hub_node(hub_chunks ? hub_chunks : 1);
+  std::vector<uint32_t> chunk_hub(hub_chunks ? hub_chunks : 1);
   std::vector<uint64_t> chunk_begin(hub_chunks ? hub_chunks : 1);
   std::vector<uint32_t> hubs_v(hub_list.size() + 1), hubs_first(hub_list.size() + 1),
       hubs_count(hub_list.size() + 1);
@@ -217,6 +232,7 @@ hanf_status build_tasks(hanf_engine* e, const uint64_t* offsets, const uint32_t*
     for (uint64_t a = s; a < en; a += hanf::kHubChunk, ++k, ++c) {
       const uint64_t len = std::min<uint64_t>(hanf::kHubChunk, en - a);
       hub_node[c] = v;
+      chunk_hub[c] = static_cast<uint32_t>(h);
       chunk_begin[c] = a;
       const uint16_t trips = static_cast<uint16_t>((len + 31) / 32);
       tasks.push_back(hanf::WarpTask{tos, static_cast<uint32_t>(c), trips, 5, 0});
@@ -293,6 +309,11 @@ hanf_status build_tasks(hanf_engine* e, const uint64_t* offsets, const uint32_t*
   HANF_CUDA(cudaMemcpyAsync(e->hub_node.p, hub_node.data(), sizeof(uint32_t) * hub_node.size(),
                             cudaMemcpyHostToDevice, st));
   HANF_CUDA(e->partials.alloc(static_cast<size_t>(hub_chunks ? hub_chunks : 1) * e->words));
+  HANF_CUDA(e->chunk_hub.alloc(chunk_hub.size()));
+  HANF_CUDA(cudaMemcpyAsync(e->chunk_hub.p, chunk_hub.data(), sizeof(uint32_t) * chunk_hub.size(),
+                            cudaMemcpyHostToDevice, st));
+  HANF_CUDA(e->hub_ticket.alloc(hubs_v.size()));
+  HANF_CUDA(cudaMemsetAsync(e->hub_ticket.p, 0, sizeof(uint32_t) * hubs_v.size(), st));
   HANF_CUDA(e->hub_nodes.alloc(hubs_v.size()));
   HANF_CUDA(e->hub_first.alloc(hubs_first.size()));
   HANF_CUDA(e->hub_count.alloc(hubs_count.size()));
@@ -328,19 +349,33 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
   return HANF_OK;
 }
 
-// Total of the block sums and popcount of bitmap `bits` over all blocks;
-// waits for the stream.  exact_sum: the total is redone on the host in the
-// reference's order (engine.hpp:115-117).
-hanf_status reduce_totals(hanf_engine* e, const uint64_t* bits, double* total, uint64_t* count,
-                          bool in_step = false) {
-  HANF_CUDA(hanf::launch_reduce(e->block_sums.p, bits, 0, e->blocks, e->reduce.p, e->stream,
-                                &e->launches));
+// Block sums of [b0, b1) from the cached estimates (when `recompute`), then
+// the total of all block sums and the popcount of `bits`; waits for the
+// stream.  exact_sum: the total is redone on the host in the reference's
+// order (engine.hpp:115-117).
+hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute, uint64_t b0,
+                           uint64_t b1, bool in_step) {
+  hanf::FinishArgs f{};
+  f.est = recompute ? e->est.p : nullptr;
+  f.bits = bits;
+  f.block_sums = e->block_sums.p;
+  f.out = e->reduce.p;
+  f.n = e->n;
+  f.blocks = e->blocks;
+  f.b0 = b0;
+  f.b1 = b1;
+  if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
+  HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
   HANF_CUDA(cudaMemcpyAsync(e->h_reduce, e->reduce.p, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                             e->stream));
   if (e->cfg.exact_sum)
     HANF_CUDA(cudaMemcpyAsync(e->h_block_sums, e->block_sums.p, sizeof(double) * e->blocks,
                               cudaMemcpyDeviceToHost, e->stream));
+  return HANF_OK;
+}
+
+hanf_status finish_complete(hanf_engine* e, double* total, uint64_t* count, bool in_step) {
   HANF_CUDA(cudaStreamSynchronize(e->stream));
   if (in_step && e->timing) {
     float a = 0.f, b = 0.f, c = 0.f;
@@ -363,6 +398,13 @@ hanf_status reduce_totals(hanf_engine* e, const uint64_t* bits, double* total, u
   return HANF_OK;
 }
 
+hanf_status finish(hanf_engine* e, const uint64_t* bits, bool recompute, uint64_t b0, uint64_t b1,
+                   double* total, uint64_t* count, bool in_step = false) {
+  const hanf_status st = finish_enqueue(e, bits, recompute, b0, b1, in_step);
+  if (st != HANF_OK) return st;
+  return finish_complete(e, total, count, in_step);
+}
+
 // Seeds both generations (every engine seeds all n counters: seeding is a
 // pure function of (v, seed), so shards need no exchange) and computes N(0).
 hanf_status seed_all(hanf_engine* e) {
@@ -379,7 +421,7 @@ hanf_status seed_all(hanf_engine* e) {
   if (st != HANF_OK) return st;
   uint64_t count = 0;
   e->last_count = e->n;
-  return reduce_totals(e, e->mod[0].p, &e->last_sum, &count);
+  return finish(e, e->mod[0].p, false, 0, 0, &e->last_sum, &count);
 }
 
 hanf_status validate_config(const hanf_config* cfg) {
@@ -414,6 +456,11 @@ hanf_status compute_local(hanf_engine* e) {
   a.order = e->order.p;
   a.hub_node = e->hub_node.p;
   a.partials = e->partials.p;
+  a.chunk_hub = e->chunk_hub.p;
+  a.hub_nodes = e->hub_nodes.p;
+  a.hub_first = e->hub_first.p;
+  a.hub_count = e->hub_count.p;
+  a.hub_ticket = e->hub_ticket.p;
   a.words = e->params.words_per_counter;
   // skipping unmodified successors costs a bitmap probe per arc and saves
   // a counter gather per skipped arc: worth it once most counters settled
@@ -422,41 +469,37 @@ hanf_status compute_local(hanf_engine* e) {
   a.stale_valid = e->stale_valid ? 1 : 0;
   HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers,
                                e->gather_mode, e->stream, &e->launches));
-  hanf::HubArgs h{};
-  h.cur = a.cur;
-  h.next = a.next;
-  h.mod_cur = a.mod_cur;
-  h.mod_next = a.mod_next;
-  h.hub_nodes = e->hub_nodes.p;
-  h.hub_first = e->hub_first.p;
-  h.hub_count = e->hub_count.p;
-  h.partials = e->partials.p;
-  h.num_hubs = e->num_hubs;
-  h.words = a.words;
-  h.stale_valid = a.stale_valid;
-  h.est = a.est;
-  h.ep = a.ep;
-  HANF_CUDA(hanf::launch_hub_finalize(h, e->params.register_bits, e->params.registers,
-                                      e->stream, &e->launches));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
-  if (fused) {
-    HANF_CUDA(hanf::launch_block_sums(e->est.p, e->mod[ng].p, e->block_sums.p, e->n, w0, w1,
-                                      e->stream, &e->launches));
-  } else {
+  const bool sharded = e->lo != 0 || e->hi != e->n;
+  if (!fused) {
     const hanf_status st = run_estimates(e, ng, e->mod[ng].p, w0, w1);
     if (st != HANF_OK) return st;
+  } else if (sharded) {
+    // block sums of this shard now: they are exchanged before commit
+    hanf::FinishArgs f{e->est.p, e->mod[ng].p, e->block_sums.p, e->reduce.p, e->n, e->blocks, w0, w1};
+    HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   }
-  if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   return HANF_OK;
 }
 
-hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
+bool commit_recomputes(const hanf_engine* e) {
+  // single GPU with fused estimates: the block sums are recomputed in the
+  // same launch as the totals
+  const bool sharded = e->lo != 0 || e->hi != e->n;
+  return !sharded && hanf::fused_estimates(e->params.register_bits, e->params.registers);
+}
+
+hanf_status commit_enqueue(hanf_engine* e) {
   const int ng = 1 - e->cur;
+  return finish_enqueue(e, e->mod[ng].p, commit_recomputes(e), 0, e->blocks, true);
+}
+
+hanf_status commit_complete(hanf_engine* e, hanf_iteration_report* rep) {
   double total = 0.0;
   uint64_t count = 0;
-  const hanf_status st = reduce_totals(e, e->mod[ng].p, &total, &count, true);
+  const hanf_status st = finish_complete(e, &total, &count, true);
   if (st != HANF_OK) return st;
-  e->cur = ng;                                     // std::swap, engine.hpp:198-200
+  e->cur = 1 - e->cur;                             // std::swap, engine.hpp:198-200
   e->stale_valid = true;
   if (e->cfg.use_systolic && !e->systolic && count > 0 &&
       static_cast<double>(count) < e->cfg.systolic_threshold * static_cast<double>(e->n))
@@ -467,6 +510,40 @@ hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
   rep->sum = total;
   rep->modified = count;
   return HANF_OK;
+}
+
+hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
+  const hanf_status st = commit_enqueue(e);
+  if (st != HANF_OK) return st;
+  return commit_complete(e, rep);
+}
+
+// One single-GPU step as a CUDA graph (memset + union + finish + read-back),
+// captured once per (generation parity, check_mod, stale_valid) and replayed.
+hanf_status step_graphed(hanf_engine* e, hanf_iteration_report* rep) {
+  const int check = (e->cfg.track_modified && e->t > 0 && 2 * e->last_count < e->n) ? 1 : 0;
+  hanf_engine::StepGraph& G = e->graphs[e->cur][check][e->stale_valid ? 1 : 0];
+  if (!G.exec) {
+    const uint64_t before = e->launches;
+    cudaGraph_t graph = nullptr;
+    HANF_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    hanf_status st = compute_local(e);
+    if (st == HANF_OK) st = commit_enqueue(e);
+    const cudaError_t ce = cudaStreamEndCapture(e->stream, &graph);
+    if (st != HANF_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+    const cudaError_t ie = cudaGraphInstantiate(&G.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return cuda_fail(ie, "cudaGraphInstantiate");
+    G.kernels = e->launches - before;
+    e->launches = before;
+  }
+  HANF_CUDA(cudaGraphLaunch(G.exec, e->stream));
+  e->launches += G.kernels;
+  return commit_complete(e, rep);
 }
 
 }  // namespace
@@ -566,6 +643,15 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   HANF_TRY(e->est.alloc(n));
   HANF_TRY(e->block_sums.alloc(e->blocks));
   HANF_TRY(e->reduce.alloc(1));
+  {
+    const uint64_t ctas = (e->blocks + hanf::kFinishThreads - 1) / hanf::kFinishThreads;
+    HANF_TRY(e->reduce_sums.alloc(ctas));
+    HANF_TRY(e->reduce_counts.alloc(ctas));
+    hanf::ReduceOut init{};
+    init.partial_sum = e->reduce_sums.p;
+    init.partial_count = e->reduce_counts.p;
+    HANF_TRY(cudaMemcpy(e->reduce.p, &init, sizeof(init), cudaMemcpyHostToDevice));
+  }
   HANF_TRY(cudaMallocHost(&e->h_reduce, sizeof(hanf::ReduceOut)));
   if (cfg.exact_sum)
     HANF_TRY(cudaMallocHost(&e->h_block_sums, sizeof(double) * (e->blocks ? e->blocks : 1)));
@@ -580,6 +666,8 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
       if (g->arcs[i] >= n) return bail(fail(HANF_INVALID_ARGUMENT, "arc endpoint out of range"));
   }
   if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
+  if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
+  if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
 
   // linear-counting table m*log(m/z), same expression as hll.hpp:139
   {
@@ -628,6 +716,8 @@ hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
     return HANF_OK;
   }
   HANF_CUDA(cudaSetDevice(e->device));
+  // phase timing needs events between the kernels: run ungraphed then
+  if (e->use_graphs && !e->timing) return step_graphed(e, rep);
   hanf_status st = compute_local(e);
   if (st != HANF_OK) return st;
   return commit(e, rep);

@@ -34,29 +34,17 @@ struct UnionArgs {
   const uint32_t* order;     // node ids of light tasks
   const uint32_t* hub_node;  // per hub chunk: node
   uint64_t* partials;        // per hub chunk: partial counter (W words)
+  const uint32_t* chunk_hub; // per hub chunk: hub index
+  const uint32_t* hub_nodes; // per hub: node, first chunk, chunk count
+  const uint32_t* hub_first;
+  const uint32_t* hub_count;
+  uint32_t* hub_ticket;      // per hub: chunks finished this step (self-resetting)
   uint32_t words;            // W
   uint32_t chunks;           // chunks per counter
   uint32_t zero_row;         // index of the all-zero counter row (= n)
   int32_t check_mod;         // skip successors whose bit is clear in mod_cur
   int32_t stale_valid;       // next[v] may be stale where mod_cur[v] is set
   double* est;               // per-counter estimates (nullptr: not fused)
-  EstimateParams ep;
-};
-
-struct HubArgs {
-  const uint64_t* cur;
-  uint64_t* next;
-  const uint64_t* mod_cur;
-  uint64_t* mod_next;
-  const uint32_t* hub_nodes;      // distinct hub nodes
-  const uint32_t* hub_first;      // first chunk of each hub
-  const uint32_t* hub_count;      // chunks of each hub
-  const uint64_t* partials;
-  uint32_t num_hubs;
-  uint32_t words;
-  uint32_t chunks;
-  int32_t stale_valid;
-  double* est;
   EstimateParams ep;
 };
 
@@ -83,25 +71,30 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint32_t register_bits, uint32_t words, uint64_t seed,
                         cudaStream_t s, uint64_t* launches);
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits,
-                         uint32_t registers, int gather_mode, cudaStream_t s,
+                         uint32_t registers, int variant, cudaStream_t s,
                          uint64_t* launches);
-cudaError_t launch_hub_finalize(const HubArgs& args, uint32_t register_bits,
-                                uint32_t registers, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* launches);
 // true when the union kernels compute estimates themselves (single-chunk layouts)
 bool fused_estimates(uint32_t register_bits, uint32_t registers);
-cudaError_t launch_block_sums(const double* est, const uint64_t* dirty, double* block_sums,
-                              uint64_t n, uint64_t b0, uint64_t b1, cudaStream_t s,
-                              uint64_t* launches);
-constexpr int kReduceCtas = 296;
-constexpr int kReduceThreads = 256;
+
+// Step epilogue (block sums + totals), see finish_kernel.
+constexpr int kFinishThreads = 64;
 struct ReduceOut {
   double total;
   unsigned long long count;
-  double partial_sum[kReduceCtas];
-  unsigned long long partial_count[kReduceCtas];
+  unsigned int ticket;
+  double* partial_sum;              // [ceil(blocks / kFinishThreads)]
+  unsigned long long* partial_count;
 };
-cudaError_t launch_reduce(const double* block_sums, const uint64_t* bits, uint64_t begin,
-                          uint64_t end, ReduceOut* out, cudaStream_t s, uint64_t* launches);
+struct FinishArgs {
+  const double* est;      // per-counter estimates (nullptr: block sums are current)
+  const uint64_t* bits;   // modified bitmap = dirty flags of the blocks
+  double* block_sums;
+  ReduceOut* out;
+  uint64_t n;
+  uint64_t blocks;        // totals over [0, blocks)
+  uint64_t b0, b1;        // block sums recomputed over [b0, b1)
+};
+cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
 
 }  // namespace hanf

@@ -152,8 +152,50 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   return v;
 }
 
-template <int R, int NREG, int U, int GMODE, bool kVec16>
-__global__ void __launch_bounds__(256) union_kernel(const UnionArgs args) {
+// Max over a split node's chunk partials and its own counter (one warp),
+// then the usual commit.  Partials were written by other warps of the same
+// launch: read through L2 (ld.cg) after the ticket handshake.
+template <class Lay, bool kVec16>
+__device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, uint32_t lane) {
+  constexpr int NL = Lay::kLimbs;
+  constexpr int NW = Lay::kWords;
+  const uint32_t v = args.hub_nodes[h];
+  const uint32_t first = args.hub_first[h];
+  const uint32_t count = args.hub_count[h];
+  const uint32_t words = args.words;
+  bool stale = false;
+  if (args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
+  bool any_changed = false;
+  for (uint32_t ch = 0; ch < args.chunks; ++ch) {
+    const uint32_t woff = ch * NW;
+    uint32_t acc[NL];
+    if (lane == 0)
+      load_chunk<Lay, kVec16>(acc, args.cur + static_cast<uint64_t>(v) * words + woff);
+    else
+      zero_limbs<Lay>(acc);
+    for (uint32_t i = lane; i < count; i += 32) {
+      uint32_t y[NL];
+      load_chunk_coherent<Lay>(y, args.partials + static_cast<uint64_t>(first + i) * words + woff);
+      swar_max<Lay>(acc, y);
+    }
+    for (uint32_t off = 16; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
+    if (lane == 0) {
+      uint32_t own[NL];
+      load_chunk<Lay, kVec16>(own, args.cur + static_cast<uint64_t>(v) * words + woff);
+      const bool changed = limbs_differ<Lay>(acc, own);
+      any_changed |= changed;
+      if (changed || stale)
+        store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
+      if (changed && args.est) args.est[v] = estimate_limbs<Lay>(acc, args.ep);
+    }
+  }
+  if (lane == 0 && any_changed)
+    atomicOr(reinterpret_cast<unsigned long long*>(args.mod_next) + (v >> 6),
+             1ull << (v & 63));
+}
+
+template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) {
   using Lay = Layout<R, NREG>;
   constexpr int NL = Lay::kLimbs;
   constexpr int NW = Lay::kWords;
@@ -232,50 +274,20 @@ __global__ void __launch_bounds__(256) union_kernel(const UnionArgs args) {
   if (any_changed)
     atomicOr(reinterpret_cast<unsigned long long*>(args.mod_next) + (v >> 6),
              1ull << (v & 63));
-}
-
-// One warp per split node: max over its chunk partials and its own counter.
-template <int R, int NREG, bool kVec16>
-__global__ void __launch_bounds__(256) hub_finalize_kernel(const HubArgs args) {
-  using Lay = Layout<R, NREG>;
-  constexpr int NL = Lay::kLimbs;
-  constexpr int NW = Lay::kWords;
-  const uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  if (h >= args.num_hubs) return;
-  const uint32_t v = args.hub_nodes[h];
-  const uint32_t first = args.hub_first[h];
-  const uint32_t count = args.hub_count[h];
-  const uint32_t words = args.words;
-  bool stale = false;
-  if (args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
-  bool any_changed = false;
-  for (uint32_t ch = 0; ch < args.chunks; ++ch) {
-    const uint32_t woff = ch * NW;
-    uint32_t acc[NL];
-    if (lane == 0)
-      load_chunk<Lay, kVec16>(acc, args.cur + static_cast<uint64_t>(v) * words + woff);
-    else
-      zero_limbs<Lay>(acc);
-    for (uint32_t i = lane; i < count; i += 32) {
-      uint32_t y[NL];
-      load_chunk_coherent<Lay>(y, args.partials + static_cast<uint64_t>(first + i) * words + woff);
-      swar_max<Lay>(acc, y);
-    }
-    for (uint32_t off = 16; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
+  if (hub) {
+    // the last chunk of a split node to finish folds all its partials
+    const uint32_t h = args.chunk_hub[task.item];
+    uint32_t last = 0;
     if (lane == 0) {
-      uint32_t own[NL];
-      load_chunk<Lay, kVec16>(own, args.cur + static_cast<uint64_t>(v) * words + woff);
-      const bool changed = limbs_differ<Lay>(acc, own);
-      any_changed |= changed;
-      if (changed || stale)
-        store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
-      if (changed && args.est) args.est[v] = estimate_limbs<Lay>(acc, args.ep);
+      __threadfence();
+      last = atomicAdd(args.hub_ticket + h, 1u) == args.hub_count[h] - 1;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      __threadfence();
+      finalize_hub<Lay, kVec16>(args, h, lane);
+      if (lane == 0) args.hub_ticket[h] = 0;  // ready for the next step
     }
   }
-  if (lane == 0 && any_changed)
-    atomicOr(reinterpret_cast<unsigned long long*>(args.mod_next) + (v >> 6),
-             1ull << (v & 63));
 }
 
 namespace {
@@ -298,33 +310,26 @@ KernelChoice choose(uint32_t r, uint32_t m) {
   }
 }
 
-template <int R, int NREG, int U, int GM, bool V>
+template <int R, int NREG, int U, int GM, bool V, int MINB = 1>
 cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   a.chunks = chunks;
   if (chunks != 1) a.est = nullptr;  // estimates need the whole counter in registers
   if (a.num_wtasks == 0) return cudaSuccess;
   const uint32_t blocks = (a.num_wtasks + 7) / 8;
-  union_kernel<R, NREG, U, GM, V><<<blocks, 256, 0, s>>>(a);
+  union_kernel<R, NREG, U, GM, V, MINB><<<blocks, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-template <int R, int NREG, bool V>
-cudaError_t hub_launch(HubArgs a, uint32_t chunks, cudaStream_t s) {
-  a.chunks = chunks;
-  if (chunks != 1) a.est = nullptr;
-  if (a.num_hubs == 0) return cudaSuccess;
-  const uint32_t blocks = (a.num_hubs + 7) / 8;
-  hub_finalize_kernel<R, NREG, V><<<blocks, 256, 0, s>>>(a);
-  return cudaGetLastError();
-}
 }  // namespace
 
 bool fused_estimates(uint32_t register_bits, uint32_t registers) {
   return choose(register_bits, registers).chunks == 1;
 }
 
+// variant < 0 picks the measured best gather for the layout (profiles/);
+// variants >= 0 select alternatives for experiments (HANF_GATHER).
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t registers,
-                         int gather_mode, cudaStream_t s, uint64_t* launches) {
+                         int variant, cudaStream_t s, uint64_t* launches) {
   const KernelChoice k = choose(register_bits, registers);
   if (args.num_wtasks == 0) return cudaSuccess;
   ++*launches;
@@ -333,15 +338,26 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
   switch (k.r * 1000 + k.nreg) {
     case 5016: return union_launch<5, 16, 4, 0, true>(args, ch, s);
     case 5032:
-      if (single && gather_mode == 2) return union_launch<5, 32, 4, 2, false>(args, ch, s);
-      if (single && gather_mode == 1) return union_launch<5, 32, 4, 1, false>(args, ch, s);
+      if (single) switch (variant) {
+          case 0: return union_launch<5, 32, 4, 0, false>(args, ch, s);
+          case 2: return union_launch<5, 32, 4, 2, false>(args, ch, s);
+          case 3: return union_launch<5, 32, 2, 1, false>(args, ch, s);
+          default: return union_launch<5, 32, 4, 1, false>(args, ch, s);
+        }
       return union_launch<5, 32, 4, 0, false>(args, ch, s);
     case 5064:
-      if (single && gather_mode == 2) return union_launch<5, 64, 4, 2, false>(args, ch, s);
-      if (single && gather_mode == 1) return union_launch<5, 64, 4, 1, false>(args, ch, s);
+      if (single) switch (variant) {
+          case 0: return union_launch<5, 64, 4, 0, false>(args, ch, s);
+          case 1: return union_launch<5, 64, 4, 1, false>(args, ch, s);
+          case 2: return union_launch<5, 64, 4, 2, false>(args, ch, s);
+          case 3: return union_launch<5, 64, 2, 2, false>(args, ch, s);
+          case 5: return union_launch<5, 64, 2, 2, false, 6>(args, ch, s);
+          case 6: return union_launch<5, 64, 4, 1, false, 5>(args, ch, s);
+          default: return union_launch<5, 64, 2, 1, false>(args, ch, s);
+        }
       return union_launch<5, 64, 4, 0, false>(args, ch, s);
     case 5128:
-      if (gather_mode == 2) return union_launch<5, 128, 2, 2, true>(args, ch, s);
+      if (variant == 2) return union_launch<5, 128, 2, 2, true>(args, ch, s);
       return union_launch<5, 128, 2, 0, true>(args, ch, s);
     case 6016: return union_launch<6, 16, 4, 0, true>(args, ch, s);
     case 6032: return union_launch<6, 32, 4, 0, false>(args, ch, s);
@@ -350,64 +366,6 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
     case 7064: return union_launch<7, 64, 2, 0, false>(args, ch, s);
     default: return union_launch<8, 16, 4, 0, true>(args, ch, s);
   }
-}
-
-cudaError_t launch_hub_finalize(const HubArgs& args, uint32_t register_bits, uint32_t registers,
-                                cudaStream_t s, uint64_t* launches) {
-  if (args.num_hubs == 0) return cudaSuccess;
-  const KernelChoice k = choose(register_bits, registers);
-  ++*launches;
-  const uint32_t ch = static_cast<uint32_t>(k.chunks);
-  switch (k.r * 1000 + k.nreg) {
-    case 5016: return hub_launch<5, 16, true>(args, ch, s);
-    case 5032: return hub_launch<5, 32, false>(args, ch, s);
-    case 5064: return hub_launch<5, 64, false>(args, ch, s);
-    case 5128: return hub_launch<5, 128, true>(args, ch, s);
-    case 6016: return hub_launch<6, 16, true>(args, ch, s);
-    case 6032: return hub_launch<6, 32, false>(args, ch, s);
-    case 7016: return hub_launch<7, 16, true>(args, ch, s);
-    case 7032: return hub_launch<7, 32, true>(args, ch, s);
-    case 7064: return hub_launch<7, 64, false>(args, ch, s);
-    default: return hub_launch<8, 16, true>(args, ch, s);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Block sums from cached estimates (union kernels wrote est[v] for every
-// changed counter): one thread per 64-counter block, sequential in index
-// order (engine.hpp:109-111); clean blocks keep their cached sum (:105).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-block_sum_kernel(const double* __restrict__ est, const uint64_t* __restrict__ dirty,
-                 double* __restrict__ block_sums, uint64_t n, uint64_t b0, uint64_t b1) {
-  const uint64_t b = b0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (b >= b1) return;
-  if (dirty[b] == 0) return;
-  const uint64_t first = b * 64;
-  const uint32_t last = n - first < 64 ? static_cast<uint32_t>(n - first) : 64u;
-  double sum = 0.0;
-  if (last == 64) {
-    const double2* p = reinterpret_cast<const double2*>(est + first);
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const double2 q = __ldg(p + k);
-      sum = __dadd_rn(sum, q.x);
-      sum = __dadd_rn(sum, q.y);
-    }
-  } else {
-    for (uint32_t i = 0; i < last; ++i) sum = __dadd_rn(sum, est[first + i]);
-  }
-  block_sums[b] = sum;
-}
-
-cudaError_t launch_block_sums(const double* est, const uint64_t* dirty, double* block_sums,
-                              uint64_t n, uint64_t b0, uint64_t b1, cudaStream_t s,
-                              uint64_t* launches) {
-  if (b1 <= b0) return cudaSuccess;
-  const uint64_t blocks = (b1 - b0 + 255) / 256;
-  block_sum_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(est, dirty, block_sums, n, b0, b1);
-  ++*launches;
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -467,82 +425,106 @@ cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* 
 }
 
 // ---------------------------------------------------------------------------
-// Deterministic total of block sums [begin, end) and popcount of the
-// modified bitmap over the same blocks: a fixed partition into kReduceCtas
-// contiguous ranges, fixed per-thread strides and a fixed tree, so reruns
-// are bit-identical (the reference's sequential order of the total is
-// reproduced on the host when exact_sum is set).
+// Step epilogue, one launch: CTA c owns the fixed range of 64-counter blocks
+// [c*256, c*256+256) (one thread per block).
+//  1. blocks in [b0, b1) whose dirty word is non-zero get their sum
+//     recomputed from the cached per-counter estimates, sequentially in
+//     index order (engine.hpp:109-111); other blocks keep their cached sum
+//     (engine.hpp:105);
+//  2. the CTA reduces its range (fixed tree) and the popcount of the
+//     modified bitmap over it (engine.hpp:202-208) into partial[c];
+//  3. the last CTA to finish (ticket) reduces the partials in a fixed order
+//     into out->total / out->count and re-arms the ticket.
+// Every order is fixed, so N(t) is bit-identical across runs; the
+// reference's own sequential total is redone on the host under exact_sum.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double block_tree_sum(double v, double* sh) {
+__device__ __forceinline__ double cta_tree_sum(double v, double* sh) {
   const int t = threadIdx.x;
   sh[t] = v;
   __syncthreads();
-  for (int w = kReduceThreads / 2; w >= 1; w >>= 1) {
+  for (int w = kFinishThreads / 2; w >= 1; w >>= 1) {
     if (t < w) sh[t] = __dadd_rn(sh[t], sh[t + w]);
     __syncthreads();
   }
-  return sh[0];
+  const double r = sh[0];
+  __syncthreads();
+  return r;
 }
 
-__device__ __forceinline__ unsigned long long block_count_sum(unsigned long long v,
-                                                              unsigned long long* sh) {
+__device__ __forceinline__ unsigned long long cta_count_sum(unsigned long long v,
+                                                            unsigned long long* sh) {
   const int t = threadIdx.x;
   sh[t] = v;
   __syncthreads();
-  for (int w = kReduceThreads / 2; w >= 1; w >>= 1) {
+  for (int w = kFinishThreads / 2; w >= 1; w >>= 1) {
     if (t < w) sh[t] += sh[t + w];
     __syncthreads();
   }
-  return sh[0];
+  const unsigned long long r = sh[0];
+  __syncthreads();
+  return r;
 }
 
-// Level 1: CTA b reduces the fixed range [begin + b*per, ...) of the block
-// sums and of the modified bitmap (bitmap word i <-> block i).
-__global__ void __launch_bounds__(kReduceThreads)
-reduce_level1(const double* __restrict__ x, const uint64_t* __restrict__ bits, uint64_t begin,
-              uint64_t end, ReduceOut* __restrict__ out) {
-  __shared__ double sh[kReduceThreads];
-  __shared__ unsigned long long shc[kReduceThreads];
-  const uint64_t len = end - begin;
-  const uint64_t per = (len + kReduceCtas - 1) / kReduceCtas;
-  const uint64_t lo = begin + blockIdx.x * per;
-  const uint64_t hi = lo + per < end ? lo + per : end;
-  double acc = 0.0;
+__global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs a) {
+  __shared__ double sh[kFinishThreads];
+  __shared__ unsigned long long shc[kFinishThreads];
+  __shared__ bool is_last;
+  const uint64_t b = static_cast<uint64_t>(blockIdx.x) * kFinishThreads + threadIdx.x;
+  double sum = 0.0;
   unsigned long long cnt = 0;
-  for (uint64_t i = lo + threadIdx.x; i < hi; i += kReduceThreads) {
-    acc = __dadd_rn(acc, x[i]);
-    cnt += __popcll(bits[i]);
+  if (b < a.blocks) {
+    const uint64_t word = a.bits[b];
+    cnt = __popcll(word);
+    if (a.est && word != 0 && b >= a.b0 && b < a.b1) {
+      const uint64_t first = b * 64;
+      const uint32_t last = a.n - first < 64 ? static_cast<uint32_t>(a.n - first) : 64u;
+      if (last == 64) {
+        const double2* p = reinterpret_cast<const double2*>(a.est + first);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const double2 q = p[k];
+          sum = __dadd_rn(sum, q.x);
+          sum = __dadd_rn(sum, q.y);
+        }
+      } else {
+        for (uint32_t i = 0; i < last; ++i) sum = __dadd_rn(sum, a.est[first + i]);
+      }
+      a.block_sums[b] = sum;
+    } else {
+      sum = a.block_sums[b];
+    }
   }
-  const double total = block_tree_sum(acc, sh);
-  const unsigned long long count = block_count_sum(cnt, shc);
+  const double cta_sum = cta_tree_sum(sum, sh);
+  const unsigned long long cta_cnt = cta_count_sum(cnt, shc);
   if (threadIdx.x == 0) {
-    out->partial_sum[blockIdx.x] = total;
-    out->partial_count[blockIdx.x] = count;
+    a.out->partial_sum[blockIdx.x] = cta_sum;
+    a.out->partial_count[blockIdx.x] = cta_cnt;
+    __threadfence();
+    is_last = atomicAdd(&a.out->ticket, 1u) == gridDim.x - 1;
   }
-}
-
-__global__ void __launch_bounds__(kReduceThreads) reduce_level2(ReduceOut* __restrict__ out) {
-  __shared__ double sh[kReduceThreads];
-  __shared__ unsigned long long shc[kReduceThreads];
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
   double acc = 0.0;
-  unsigned long long cnt = 0;
-  for (int i = threadIdx.x; i < kReduceCtas; i += kReduceThreads) {
-    acc = __dadd_rn(acc, out->partial_sum[i]);
-    cnt += out->partial_count[i];
+  unsigned long long c = 0;
+  for (uint32_t i = threadIdx.x; i < gridDim.x; i += kFinishThreads) {
+    acc = __dadd_rn(acc, __ldcg(&a.out->partial_sum[i]));
+    c += __ldcg(&a.out->partial_count[i]);
   }
-  const double total = block_tree_sum(acc, sh);
-  const unsigned long long count = block_count_sum(cnt, shc);
+  const double total = cta_tree_sum(acc, sh);
+  const unsigned long long count = cta_count_sum(c, shc);
   if (threadIdx.x == 0) {
-    out->total = total;
-    out->count = count;
+    a.out->total = total;
+    a.out->count = count;
+    a.out->ticket = 0;
   }
 }
 
-cudaError_t launch_reduce(const double* block_sums, const uint64_t* bits, uint64_t begin,
-                          uint64_t end, ReduceOut* out, cudaStream_t s, uint64_t* launches) {
-  reduce_level1<<<kReduceCtas, kReduceThreads, 0, s>>>(block_sums, bits, begin, end, out);
-  reduce_level2<<<1, kReduceThreads, 0, s>>>(out);
-  *launches += 2;
+cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches) {
+  if (a.blocks == 0) return cudaSuccess;
+  const uint64_t ctas = (a.blocks + kFinishThreads - 1) / kFinishThreads;
+  finish_kernel<<<static_cast<uint32_t>(ctas), kFinishThreads, 0, s>>>(a);
+  ++*launches;
   return cudaGetLastError();
 }
 
