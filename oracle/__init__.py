@@ -80,6 +80,7 @@ class Port:
         L.or_counter_estimate.argtypes = [POINTER(c_uint64), POINTER(_Params)]
         L.or_naive_union.argtypes = [POINTER(c_uint64), POINTER(c_uint64), POINTER(_Params)]
         L.or_packed_max_into.argtypes = [POINTER(_Params), POINTER(c_uint64), POINTER(c_uint64)]
+        L.or_selftest_straddle.restype = c_uint64
         L.or_graph_from_edges.argtypes = [c_uint64, POINTER(c_uint32), POINTER(c_uint32),
                                           c_uint64, POINTER(_Graph)]
         L.or_graph_transpose.argtypes = [POINTER(_Graph), POINTER(_Graph)]
@@ -103,6 +104,12 @@ class Port:
         L.or_engine_systolic_active.argtypes = [c_void_p]
         L.or_engine_run.argtypes = [c_void_p, POINTER(c_double), POINTER(c_uint64), c_uint64,
                                     POINTER(c_uint64)]
+        L.or_exact_nf.argtypes = [POINTER(c_uint64), POINTER(c_uint32), c_uint64,
+                                  POINTER(c_uint64), c_uint64, POINTER(c_uint64)]
+        L.or_clique_path_nf.restype = c_uint64
+        L.or_clique_path_nf.argtypes = [c_uint64, c_uint64, c_uint64]
+        L.or_counter_of_ball.argtypes = [POINTER(c_uint64), POINTER(c_uint32), c_uint64,
+                                         c_uint32, c_uint64, POINTER(_Params), POINTER(c_uint64)]
         L.or_distance_distribution.argtypes = [POINTER(c_double), c_uint64, POINTER(c_double),
                                                POINTER(c_double), POINTER(c_double)]
         L.or_effective_diameter.argtypes = [POINTER(c_double), c_uint64, c_double, c_int,
@@ -169,6 +176,27 @@ class Port:
         if self.L.or_graph_from_edges(n, _u32p(src), _u32p(dst), src.size, ctypes.byref(g)):
             raise ValueError("arc endpoint out of range")
         return self._take(g)
+
+    def exact_nf(self, n, offsets, succ):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        succ = np.ascontiguousarray(succ, dtype=np.uint32)
+        vals = np.zeros(n + 2, dtype=np.uint64)
+        ln = c_uint64()
+        if self.L.or_exact_nf(_u64p(offsets), _u32p(succ), n, _u64p(vals), vals.size,
+                              ctypes.byref(ln)):
+            raise RuntimeError("exact_nf capacity")
+        return [int(x) for x in vals[:ln.value]]
+
+    def clique_path_nf(self, k, l, t):
+        return self.L.or_clique_path_nf(k, l, t)
+
+    def counter_of_ball(self, n, offsets, succ, v, radius, p):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        succ = np.ascontiguousarray(succ, dtype=np.uint32)
+        out = np.zeros(p.words, dtype=np.uint64)
+        self.L.or_counter_of_ball(_u64p(offsets), _u32p(succ), n, v, radius, ctypes.byref(p),
+                                  _u64p(out))
+        return out
 
     # engine -----------------------------------------------------------------
     def engine(self, n, offsets, succ, **cfg):

@@ -158,12 +158,11 @@ static void packed_masks(const or_params* p, uint64_t* low, uint64_t* high) {
   }
 }
 
-int or_packed_max_into(const or_params* p, uint64_t* dst, const uint64_t* src) {
+/* max_into with caller-provided masks and scratch (the engine builds the
+ * masks once, as PackedMax's constructor does) */
+static int packed_max_with(const or_params* p, const uint64_t* low, const uint64_t* high,
+                           uint64_t* scratch, uint64_t* dst, const uint64_t* src) {
   const unsigned w = p->words;
-  uint64_t* low = (uint64_t*)malloc(sizeof(uint64_t) * w * 3);
-  uint64_t* high = low + w;
-  uint64_t* scratch = high + w;
-  packed_masks(p, low, high);
   uint64_t borrow = 0;
   for (unsigned i = 0; i < w; ++i) { /* pass 1: broadword.hpp:98-110 */
     const uint64_t x = dst[i], y = src[i], h = high[i];
@@ -194,8 +193,40 @@ int or_packed_max_into(const or_params* p, uint64_t* dst, const uint64_t* src) {
     changed |= res != dst[i];
     dst[i] = res;
   }
+  return changed;
+}
+
+int or_packed_max_into(const or_params* p, uint64_t* dst, const uint64_t* src) {
+  const unsigned w = p->words;
+  uint64_t* low = (uint64_t*)malloc(sizeof(uint64_t) * w * 3);
+  packed_masks(p, low, low + w);
+  const int changed = packed_max_with(p, low, low + w, low + 2 * w, dst, src);
   free(low);
   return changed;
+}
+
+/* broadword == naive over every value pair of two straddling registers
+ * (test_hll.cpp:145-169, registers 12/13 of m=16, r=5): mismatch count */
+uint64_t or_selftest_straddle(void) {
+  or_params p;
+  or_params_make(4, 0, 5, &p);
+  uint64_t a[2], b[2], n[2], mism = 0;
+  for (unsigned x12 = 0; x12 < 32; ++x12)
+    for (unsigned x13 = 0; x13 < 32; ++x13)
+      for (unsigned y12 = 0; y12 < 32; ++y12)
+        for (unsigned y13 = 0; y13 < 32; ++y13) {
+          a[0] = a[1] = b[0] = b[1] = 0;
+          or_write_register(a, &p, 12, x12);
+          or_write_register(a, &p, 13, x13);
+          or_write_register(b, &p, 12, y12);
+          or_write_register(b, &p, 13, y13);
+          n[0] = a[0];
+          n[1] = a[1];
+          const int cb = or_packed_max_into(&p, a, b);
+          const int cn = or_naive_union(n, b, &p);
+          mism += (a[0] != n[0] || a[1] != n[1] || cb != cn);
+        }
+  return mism;
 }
 
 /* ===================================================================== */
@@ -311,6 +342,9 @@ int or_gen_clique_path(uint64_t k, uint64_t l, or_graph* out) {
 #define OR_KBLOCK 64 /* engine.hpp:278 */
 
 struct or_engine {
+  uint64_t* low;           /* PackedMax masks, broadword.hpp:75-87 */
+  uint64_t* high;
+  uint64_t* scratch;
   const uint64_t* offsets; /* borrowed, engine.hpp:281 */
   const uint32_t* succ;
   uint64_t n;
@@ -362,6 +396,10 @@ or_engine* or_engine_create(const uint64_t* offsets, const uint32_t* succ,
     *status = 1;
     return NULL;
   }
+  e->low = (uint64_t*)malloc(sizeof(uint64_t) * e->params.words * 3);
+  e->high = e->low + e->params.words;
+  e->scratch = e->high + e->params.words;
+  packed_masks(&e->params, e->low, e->high);
   const uint64_t words = (uint64_t)e->params.words * (n ? n : 1);
   e->current = (uint64_t*)calloc(words, sizeof(uint64_t));
   e->next = NULL;
@@ -381,7 +419,7 @@ or_engine* or_engine_create(const uint64_t* offsets, const uint32_t* succ,
 void or_engine_destroy(or_engine* e) {
   if (!e) return;
   free(e->current); free(e->next); free(e->modified); free(e->next_modified);
-  free(e->signalled); free(e->block_sums); free(e->block_dirty);
+  free(e->signalled); free(e->block_sums); free(e->block_dirty); free(e->low);
   if (e->have_transpose) or_graph_free(&e->transpose);
   free(e);
 }
@@ -428,7 +466,8 @@ void or_engine_step(or_engine* e, double* sum, uint64_t* modified) {
       for (uint64_t i = e->offsets[v]; i < e->offsets[v + 1]; ++i) {
         const uint32_t s = e->succ[i];
         if (e->cfg.track_modified && !e->modified[s]) continue;
-        changed |= or_packed_max_into(&e->params, dst, e->current + (uint64_t)s * words);
+        changed |= packed_max_with(&e->params, e->low, e->high, e->scratch, dst,
+                                   e->current + (uint64_t)s * words);
       }
     }
     e->next_modified[v] = changed ? 1 : 0;
@@ -493,6 +532,92 @@ int or_engine_run(or_engine* e, double* values, uint64_t* modified,
     if (values[t] < values[t - 1]) values[t] = values[t - 1];
   *len = count;
   return 0;
+}
+
+/* ===================================================================== */
+/* oracle.hpp, tests/test_util.hpp                                       */
+/* ===================================================================== */
+
+/* oracle.hpp:38-104 (single-threaded; guards not restated) */
+int or_exact_nf(const uint64_t* offsets, const uint32_t* succ, uint64_t n,
+                uint64_t* values, uint64_t cap, uint64_t* len) {
+  *len = 0;
+  if (n == 0) {
+    if (cap < 1) return 5;
+    values[0] = 0;
+    *len = 1;
+    return 0;
+  }
+  uint32_t* stamp = (uint32_t*)calloc(n, sizeof(uint32_t));
+  uint32_t* dist = (uint32_t*)calloc(n, sizeof(uint32_t));
+  uint32_t* queue = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint64_t* hist = (uint64_t*)calloc(n + 1, sizeof(uint64_t));
+  uint64_t depth = 1;
+  for (uint64_t src = 0; src < n; ++src) {
+    const uint32_t mark = (uint32_t)src + 1;
+    uint64_t head = 0, tail = 0;
+    queue[tail++] = (uint32_t)src;
+    stamp[src] = mark;
+    dist[src] = 0;
+    for (; head < tail; ++head) {
+      const uint32_t v = queue[head];
+      const uint32_t dv = dist[v];
+      if (dv + 1 > depth) depth = dv + 1;
+      ++hist[dv];
+      for (uint64_t i = offsets[v]; i < offsets[v + 1]; ++i) {
+        const uint32_t w = succ[i];
+        if (stamp[w] == mark) continue;
+        stamp[w] = mark;
+        dist[w] = dv + 1;
+        queue[tail++] = w;
+      }
+    }
+  }
+  *len = depth;
+  int rc = 0;
+  if (cap < depth) {
+    rc = 5;
+  } else {
+    uint64_t acc = 0;
+    for (uint64_t d = 0; d < depth; ++d) {
+      acc += hist[d];
+      values[d] = acc;
+    }
+  }
+  free(stamp); free(dist); free(queue); free(hist);
+  return rc;
+}
+
+/* oracle.hpp:107-113 */
+uint64_t or_clique_path_nf(uint64_t k, uint64_t l, uint64_t t) {
+  if (t == 0) return 2 * k + l;
+  if (t <= l) return (t + 1) * (4 * k + 2 * l - t) / 2 - 2 * k + 2 * k * k;
+  return (l + 1) * (4 * k + l) / 2 - 2 * k + 3 * k * k;
+}
+
+/* test_util.hpp:16-41: counter fed exactly B(v, radius) */
+void or_counter_of_ball(const uint64_t* offsets, const uint32_t* succ, uint64_t n,
+                        uint32_t v, uint64_t radius, const or_params* p, uint64_t* dst) {
+  uint32_t* dist = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint32_t* queue = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  for (uint64_t i = 0; i < n; ++i) dist[i] = 0xffffffffu;
+  memset(dst, 0, sizeof(uint64_t) * p->words);
+  uint64_t head = 0, tail = 0;
+  queue[tail++] = v;
+  dist[v] = 0;
+  for (; head < tail; ++head) {
+    const uint32_t x = queue[head];
+    if (dist[x] > radius) break;
+    or_counter_add(dst, p, x);
+    for (uint64_t i = offsets[x]; i < offsets[x + 1]; ++i) {
+      const uint32_t w = succ[i];
+      if (dist[w] != 0xffffffffu) continue;
+      dist[w] = dist[x] + 1;
+      queue[tail++] = w;
+    }
+  }
+  free(dist);
+  free(queue);
 }
 
 /* ===================================================================== */

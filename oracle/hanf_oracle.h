@@ -53,6 +53,8 @@ int or_naive_union(uint64_t* dst, const uint64_t* src, const or_params* p); /* 1
 
 /* ---- broadword.hpp: PackedMax (75-130) ------------------------------ */
 int or_packed_max_into(const or_params* p, uint64_t* dst, const uint64_t* src);
+/* test_hll.cpp:145-169: exhaustive straddling pair, returns mismatches */
+uint64_t or_selftest_straddle(void);
 
 /* ---- graph.hpp ------------------------------------------------------ */
 typedef struct {
@@ -102,6 +104,18 @@ int or_engine_systolic_active(const or_engine* e);
  * returns 0 ok, 2 guard (iteration cap), 5 capacity too small. */
 int or_engine_run(or_engine* e, double* values, uint64_t* modified,
                   uint64_t cap, uint64_t* len);
+
+/* ---- oracle.hpp / tests/test_util.hpp ------------------------------- */
+/* exact_nf (oracle.hpp:38-104): BFS from every source; values[t] = ordered
+ * pairs within distance t.  *len = depth.  5 = capacity too small. */
+int or_exact_nf(const uint64_t* offsets, const uint32_t* succ, uint64_t n,
+                uint64_t* values, uint64_t cap, uint64_t* len);
+/* clique_path_nf (oracle.hpp:107-113) */
+uint64_t or_clique_path_nf(uint64_t k, uint64_t l, uint64_t t);
+/* counter_of(ball(v, t)) (test_util.hpp:16-41): the counter a node must hold
+ * after t iterations.  dst: W words. */
+void or_counter_of_ball(const uint64_t* offsets, const uint32_t* succ, uint64_t n,
+                        uint32_t v, uint64_t radius, const or_params* p, uint64_t* dst);
 
 /* ---- stats.hpp ------------------------------------------------------ */
 /* cdf_from_nf + distribution_from_cdf, stats.hpp:33-60. -1 on bad input. */

@@ -1,0 +1,155 @@
+"""Multi-rank path on CPU: ShardedNfEngine (paper_1011_5599_b200/sharded.py)
+over torch.distributed/gloo with world_size 2 and 3, each rank driving a CPU
+emulation of one CUDA shard engine (same buffers, same exchange contract).
+The sharded run must equal the single-engine reference run bit for bit."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+class EmulatedShard:
+    """CPU stand-in for LocalCudaShard: next-generation rows of [lo, hi),
+    the modified bitmap words and 64-counter block sums, exchanged by the
+    orchestrator, then a commit over the full arrays (hanf_engine.cu
+    compute_local/commit semantics, arithmetic from the oracle)."""
+
+    def __init__(self, graph, cfg, lo, hi):
+        import oracle
+        self.port = oracle.port()
+        self.n = graph.num_nodes()
+        self.off, self.succ = graph.offsets(), graph.arcs()
+        self.lo, self.hi = lo, hi
+        r = cfg.register_bits or 5
+        self.p = self.port.params(cfg.bucket_bits, cfg.seed, r)
+        W = self.p.words
+        self.W = W
+        self.cur = np.zeros((self.n, W), dtype=np.uint64)
+        for v in range(self.n):
+            self.cur[v] = self.port.counter_of(self.p, [v])
+        self.next = self.cur.copy()
+        nb = (self.n + 63) // 64
+        self.mod_cur = np.zeros(nb, dtype=np.uint64)
+        self.mod_next = np.zeros(nb, dtype=np.uint64)
+        self.est = np.array([self.port.estimate(self.cur[v], self.p) for v in range(self.n)])
+        self.block_sums = np.zeros(nb)
+        for b in range(nb):
+            s = 0.0
+            for v in range(64 * b, min(64 * b + 64, self.n)):
+                s += self.est[v]
+            self.block_sums[b] = s
+        self.t = 0
+        self.last_sum = float(np.sum(self.block_sums[:0]))
+        self.last_sum = self._total()
+
+    def _total(self):
+        s = 0.0
+        for x in self.block_sums:
+            s += x
+        return s
+
+    def sum_estimates(self):
+        return self.last_sum
+
+    def shard_compute(self):
+        lo, hi = self.lo, self.hi
+        self.mod_next[lo // 64:-(-hi // 64)] = 0
+        for v in range(lo, hi):
+            acc = self.cur[v].copy()
+            for i in range(int(self.off[v]), int(self.off[v + 1])):
+                self.port.packed_max_into(self.p, acc, np.ascontiguousarray(self.cur[self.succ[i]]))
+            self.next[v] = acc
+            if not np.array_equal(acc, self.cur[v]):
+                self.mod_next[v >> 6] |= np.uint64(1) << np.uint64(v & 63)
+                self.est[v] = self.port.estimate(acc, self.p)
+        for b in range(lo // 64, -(-hi // 64)):
+            if self.mod_next[b]:
+                s = 0.0
+                for v in range(64 * b, min(64 * b + 64, self.n)):
+                    s += self.est[v]
+                self.block_sums[b] = s
+
+    def before_exchange(self):
+        pass
+
+    def after_exchange(self):
+        pass
+
+    def exchange_buffers(self):
+        counters = torch.from_numpy(self.next.reshape(-1).view(np.int64))
+        modified = torch.from_numpy(self.mod_next.view(np.int64))
+        sums = torch.from_numpy(self.block_sums)
+        return [(counters, 64 * self.W, self.W), (modified, 1, None), (sums, 1, None)]
+
+    def shard_commit(self):
+        from paper_1011_5599_b200.engine import IterationReport
+        count = int(sum(bin(int(w)).count("1") for w in self.mod_next))
+        total = self._total()
+        self.cur, self.next = self.next, self.cur.copy()
+        self.next[:] = self.cur
+        self.mod_cur, self.mod_next = self.mod_next, self.mod_cur
+        self.t += 1
+        self.last_sum = total
+        return IterationReport(total, count)
+
+    def close(self):
+        pass
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, spec, out):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1011_5599_b200 as hanf
+    from paper_1011_5599_b200.sharded import ShardedNfEngine, shard_ranges
+    g = hanf.gen_uniform_random(*spec["graph"])
+    cfg = hanf.EngineConfig(bucket_bits=spec["b"], seed=spec["seed"])
+    lo, hi = shard_ranges(g.num_nodes(), world)[rank]
+    eng = ShardedNfEngine(g, cfg, rank, world, local=EmulatedShard(g, cfg, lo, hi))
+    est = eng.run_to_stabilisation()
+    out[rank] = (est.values, est.modified, eng.local.cur.copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,graph", [(2, (256, 4, 5)), (3, (200, 3, 9)), (2, (130, 2, 1))])
+def test_sharded_run_matches_single_engine(port, world, graph):
+    spec = {"graph": graph, "b": 6, "seed": 42}
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker, args=(world, _free_port(), spec, out), nprocs=world,
+                       join=True, start_method="spawn")
+    n, off, succ = port.gen_uniform_random(*graph)
+    vals, mods = port.engine(n, off, succ, bucket_bits=6, seed=42).run()
+    final = port.engine(n, off, succ, bucket_bits=6, seed=42)
+    while final.step()[1]:
+        pass
+    for r in range(world):
+        v, m, cur = out[r]
+        assert v == vals and m == mods
+        assert np.array_equal(cur.reshape(-1), final.counters())
+
+
+def test_shard_ranges():
+    from paper_1011_5599_b200.sharded import shard_ranges
+    assert shard_ranges(1 << 20, 8) == [(k << 17, (k + 1) << 17) for k in range(8)]
+    r = shard_ranges(1000, 3)
+    assert r[0][0] == 0 and r[-1][1] == 1000
+    assert all(lo % 64 == 0 for lo, _ in r)
+    assert all(r[i][1] == r[i + 1][0] for i in range(2))
+    assert shard_ranges(10, 4)[1:] == [(10, 10)] * 3
