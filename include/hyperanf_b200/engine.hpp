@@ -1,0 +1,281 @@
+// hyperanf_b200/engine.hpp -- C++ drop-in for the reference engine surface
+// (/root/reference/proj/include/hyperanf/engine.hpp) over the C-ABI of
+// libhanf.so (include/hanf.h).  Header-only; link with -lhanf.
+//
+// Replacing the reference path is a namespace change:
+//
+//     const hyperanf::Graph g = ...;                    // unchanged
+//     hyperanf::EngineConfig cfg = ...;                 // unchanged
+//     auto est = hyperanf_b200::estimate_nf(g, hyperanf_b200::from_reference(cfg));
+//
+// Any graph type with num_nodes(), offsets() (u64, n+1) and arcs() (u32)
+// is accepted (graph.hpp:46-57), hyperanf::Graph included.  Types, member
+// names, argument meaning and exception types follow the reference:
+//   EngineConfig      engine.hpp:32-46      IterationReport  engine.hpp:48-51
+//   NfEstimate        engine.hpp:53-66      NfEngine         engine.hpp:68-292
+//   estimate_nf       engine.hpp:295-298    SketchParams     hll.hpp:36-70
+//   std::invalid_argument / GuardError / std::out_of_range / IoError /
+//   ParseError as the reference throws them (errors.hpp, hll.hpp:233-235).
+#pragma once
+
+#include <cstdint>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../hanf.h"
+
+namespace hyperanf_b200 {
+
+struct ParseError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct IoError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct GuardError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(hanf_status st) {
+  if (st == HANF_OK) return;
+  const std::string msg = hanf_last_error();
+  switch (st) {
+    case HANF_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case HANF_GUARD: throw GuardError(msg);
+    case HANF_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case HANF_OUT_OF_MEMORY: throw std::bad_alloc();
+    case HANF_IO_ERROR: throw IoError(msg);
+    case HANF_PARSE_ERROR: throw ParseError(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+enum class Termination { stabilisation, threshold };
+
+inline const char* to_string(Termination t) {
+  return t == Termination::stabilisation ? "stabilisation" : "threshold";
+}
+
+struct EngineConfig {
+  unsigned bucket_bits = 7;
+  unsigned register_bits = 0;
+  std::uint64_t seed = 0;
+  unsigned threads = 1;           // CPU knob, accepted (no effect on the GPU)
+  std::uint64_t task_size = 0;    // CPU knob, accepted
+  double systolic_threshold = 0.25;
+  Termination termination = Termination::stabilisation;
+  double eps_inc = 0.0;
+  std::uint64_t max_iterations = 0;
+  bool spill_to_disk = false;     // accepted: HBM holds both generations
+  bool track_modified = true;
+  bool use_systolic = true;
+  // B200 options (never change a result bit)
+  int device = 0;
+  bool exact_sum = true;
+  std::uint64_t shard_begin = 0, shard_end = 0;
+
+  hanf_config to_c() const {
+    hanf_config c;
+    check(hanf_config_init(&c));
+    c.bucket_bits = bucket_bits;
+    c.register_bits = register_bits;
+    c.seed = seed;
+    c.threads = threads;
+    c.task_size = task_size;
+    c.systolic_threshold = systolic_threshold;
+    c.termination = termination == Termination::threshold ? 1 : 0;
+    c.eps_inc = eps_inc;
+    c.max_iterations = max_iterations;
+    c.spill_to_disk = spill_to_disk;
+    c.track_modified = track_modified;
+    c.use_systolic = use_systolic;
+    c.device = device;
+    c.exact_sum = exact_sum;
+    c.shard_begin = shard_begin;
+    c.shard_end = shard_end;
+    return c;
+  }
+};
+
+// Converts a reference hyperanf::EngineConfig (any type with the same
+// member names) field by field.
+template <class RefConfig>
+EngineConfig from_reference(const RefConfig& r) {
+  EngineConfig c;
+  c.bucket_bits = r.bucket_bits;
+  c.register_bits = r.register_bits;
+  c.seed = r.seed;
+  c.threads = r.threads;
+  c.task_size = r.task_size;
+  c.systolic_threshold = r.systolic_threshold;
+  c.termination = static_cast<int>(r.termination) == 0 ? Termination::stabilisation
+                                                       : Termination::threshold;
+  c.eps_inc = r.eps_inc;
+  c.max_iterations = r.max_iterations;
+  c.spill_to_disk = r.spill_to_disk;
+  c.track_modified = r.track_modified;
+  c.use_systolic = r.use_systolic;
+  return c;
+}
+
+struct IterationReport {
+  double sum = 0.0;
+  std::uint64_t modified = 0;
+};
+
+struct NfEstimate {
+  std::uint64_t n = 0;
+  unsigned m = 0;
+  std::uint64_t seed = 0;
+  Termination termination = Termination::stabilisation;
+  std::vector<double> values;
+  std::vector<std::uint64_t> modified;
+  double wall_seconds = 0.0;
+  bool exact = false;
+  std::uint64_t iterations() const noexcept { return values.empty() ? 0 : values.size() - 1; }
+};
+
+struct SketchParams {
+  unsigned bucket_bits = 7, registers = 128, register_bits = 5;
+  double alpha = 0.0;
+  std::uint64_t seed = 0;
+  unsigned words = 10;
+  static SketchParams make(unsigned b, std::uint64_t seed, unsigned r = 5) {
+    hanf_sketch_params p;
+    check(hanf_sketch_params_make(b, seed, r, &p));
+    return from_c(p);
+  }
+  static SketchParams from_c(const hanf_sketch_params& p) {
+    SketchParams s;
+    s.bucket_bits = p.bucket_bits;
+    s.registers = p.registers;
+    s.register_bits = p.register_bits;
+    s.alpha = p.alpha;
+    s.seed = p.seed;
+    s.words = p.words_per_counter;
+    return s;
+  }
+  unsigned words_per_counter() const noexcept { return words; }
+  unsigned max_register_value() const noexcept { return (1u << register_bits) - 1; }
+};
+
+template <class G>
+hanf_graph_view view_of(const G& g) {
+  hanf_graph_view v;
+  v.n = g.num_nodes();
+  v.num_arcs = g.arcs().size();
+  v.offsets = g.offsets().data();
+  v.arcs = g.arcs().data();
+  return v;
+}
+
+class NfEngine {
+ public:
+  template <class G>
+  NfEngine(const G& graph, EngineConfig cfg) : cfg_(cfg), n_(graph.num_nodes()) {
+    const hanf_graph_view v = view_of(graph);
+    const hanf_config c = cfg_.to_c();
+    check(hanf_create(&v, &c, &h_));
+    hanf_sketch_params p;
+    check(hanf_params(h_, &p));
+    params_ = SketchParams::from_c(p);
+  }
+  NfEngine(const NfEngine&) = delete;
+  NfEngine& operator=(const NfEngine&) = delete;
+  ~NfEngine() { hanf_destroy(h_); }
+
+  const SketchParams& params() const noexcept { return params_; }
+  const EngineConfig& config() const noexcept { return cfg_; }
+  // CounterArray::data() of the current generation, reference packing
+  std::vector<std::uint64_t> counters() const {
+    std::vector<std::uint64_t> out(static_cast<size_t>(n_) * params_.words);
+    check(hanf_read_counters(h_, 0, n_, out.data()));
+    return out;
+  }
+  std::vector<std::uint64_t> counter(std::uint64_t i) const {
+    std::vector<std::uint64_t> out(params_.words);
+    check(hanf_read_counters(h_, i, 1, out.data()));
+    return out;
+  }
+  std::uint64_t iteration() const {
+    std::uint64_t t = 0;
+    check(hanf_iteration(h_, &t));
+    return t;
+  }
+  bool systolic_active() const {
+    int32_t a = 0;
+    check(hanf_systolic_active(h_, &a));
+    return a != 0;
+  }
+  double sum_estimates() {
+    double s = 0.0;
+    check(hanf_sum_estimates(h_, &s));
+    return s;
+  }
+  IterationReport step() {
+    hanf_iteration_report r;
+    check(hanf_step(h_, &r));
+    return {r.sum, r.modified};
+  }
+  NfEstimate run_to_stabilisation() {
+    NfEstimate est;
+    est.n = n_;
+    est.m = params_.registers;
+    est.seed = params_.seed;
+    est.termination = cfg_.termination;
+    std::uint64_t len = 0;
+    double wall = 0.0;
+    std::vector<double> vals(64);
+    std::vector<std::uint64_t> mods(64);
+    hanf_status st = hanf_run_to_stabilisation(h_, vals.data(), mods.data(), vals.size(), &len, &wall);
+    if (st == HANF_CAPACITY) {
+      vals.resize(len);
+      mods.resize(len);
+      st = hanf_last_result(h_, vals.data(), mods.data(), len, &len);
+    }
+    check(st);
+    vals.resize(len);
+    mods.resize(len);
+    est.values = std::move(vals);
+    est.modified = std::move(mods);
+    est.wall_seconds = wall;
+    return est;
+  }
+  void reset() { check(hanf_reset(h_)); }
+  hanf_engine* handle() noexcept { return h_; }
+
+ private:
+  EngineConfig cfg_;
+  std::uint64_t n_ = 0;
+  SketchParams params_;
+  hanf_engine* h_ = nullptr;
+};
+
+template <class G>
+NfEstimate estimate_nf(const G& g, const EngineConfig& cfg) {
+  NfEngine engine(g, cfg);
+  return engine.run_to_stabilisation();
+}
+
+// stats.hpp:44-77 on an N(t) vector
+struct DistanceDistribution {
+  double mean = 0.0, variance = 0.0, spid = 0.0;
+};
+inline DistanceDistribution distance_distribution(const std::vector<double>& nf) {
+  DistanceDistribution d;
+  check(hanf_distance_distribution(nf.data(), nf.size(), &d.mean, &d.variance, &d.spid));
+  return d;
+}
+inline double effective_diameter(const std::vector<double>& nf, double alpha = 0.9,
+                                 bool interpolated = false) {
+  double out = 0.0;
+  check(hanf_effective_diameter(nf.data(), nf.size(), alpha, interpolated ? 1 : 0, &out));
+  return out;
+}
+
+}  // namespace hyperanf_b200

@@ -1,0 +1,105 @@
+// dropin_test.cpp -- the C++ drop-in check: the reference engine
+// (hyperanf::NfEngine, compiled from the reference's own headers) and the
+// B200 engine behind include/hyperanf_b200/engine.hpp run on the SAME
+// hyperanf::Graph objects, in lockstep.  Test infrastructure: built by
+// oracle/Makefile into oracle/_ref/ (it contains reference code), run by
+// tests/test_gpu_dropin.py on the GPU box.  Exit 0 = every check passed.
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hyperanf/engine.hpp"
+#include "hyperanf/graph.hpp"
+#include "hyperanf/stats.hpp"
+#include "hyperanf_b200/engine.hpp"
+
+namespace {
+int failures = 0;
+void expect(bool ok, const std::string& what) {
+  if (!ok) {
+    ++failures;
+    std::printf("FAIL %s\n", what.c_str());
+  }
+}
+
+void lockstep(const hyperanf::Graph& g, const hyperanf::EngineConfig& cfg, const char* name) {
+  hyperanf::NfEngine ref(g, cfg);
+  hyperanf_b200::NfEngine gpu(g, hyperanf_b200::from_reference(cfg));
+  const auto& rc = ref.counters();
+  expect(ref.sum_estimates() == gpu.sum_estimates(), std::string(name) + " N(0)");
+  expect(std::vector<std::uint64_t>(rc.data(), rc.data() + rc.word_count()) == gpu.counters(),
+         std::string(name) + " seeded counters");
+  for (std::uint64_t t = 1; t <= g.num_nodes() + 1; ++t) {
+    const auto a = ref.step();
+    const auto b = gpu.step();
+    const auto& c = ref.counters();
+    const bool same = a.sum == b.sum && a.modified == b.modified &&
+                      std::vector<std::uint64_t>(c.data(), c.data() + c.word_count()) ==
+                          gpu.counters() &&
+                      ref.systolic_active() == gpu.systolic_active() &&
+                      ref.iteration() == gpu.iteration();
+    expect(same, std::string(name) + " step " + std::to_string(t));
+    if (!same || a.modified == 0) break;
+  }
+  const auto ea = hyperanf::estimate_nf(g, cfg);
+  const auto eb = hyperanf_b200::estimate_nf(g, hyperanf_b200::from_reference(cfg));
+  expect(ea.values == eb.values && ea.modified == eb.modified, std::string(name) + " estimate_nf");
+  if (!ea.values.empty() && ea.values.back() > 0) {
+    const auto da = hyperanf::distribution_from_cdf(hyperanf::cdf_from_nf(ea.values));
+    const auto db = hyperanf_b200::distance_distribution(eb.values);
+    expect(da.spid == db.spid && da.mean == db.mean, std::string(name) + " spid");
+    expect(hyperanf::effective_diameter(ea.values, 0.9, true) ==
+               hyperanf_b200::effective_diameter(eb.values, 0.9, true),
+           std::string(name) + " interpolated effective diameter");
+  }
+}
+}  // namespace
+
+int main() {
+  struct Case {
+    hyperanf::Graph g;
+    unsigned b, r;
+    std::uint64_t seed;
+    const char* name;
+  };
+  std::vector<std::pair<std::uint32_t, std::uint32_t>> path;
+  for (std::uint32_t v = 0; v + 1 < 64; ++v) path.emplace_back(v, v + 1);
+  std::vector<Case> cases;
+  cases.push_back({hyperanf::gen_uniform_random(60, 3, 21), 6, 6, 77, "balls60 r6"});
+  cases.push_back({hyperanf::gen_uniform_random(500, 5, 31), 7, 0, 8, "ur500"});
+  cases.push_back({hyperanf::gen_clique_path(260, 10), 8, 0, 42, "clique-path 260/10"});
+  cases.push_back({hyperanf::gen_clique_path(1100, 3), 6, 0, 42, "clique-path 1100/3 (hubs)"});
+  cases.push_back({hyperanf::Graph::from_edges(64, path), 6, 0, 2, "64-path"});
+  cases.push_back({hyperanf::gen_uniform_random(20000, 12, 5), 5, 0, 1, "ur20000 b5"});
+  cases.push_back({hyperanf::gen_uniform_random(3000, 7, 9), 9, 0, 3, "ur3000 b9"});
+  for (const auto& c : cases) {
+    hyperanf::EngineConfig cfg;
+    cfg.bucket_bits = c.b;
+    cfg.register_bits = c.r;
+    cfg.seed = c.seed;
+    lockstep(c.g, cfg, c.name);
+  }
+  // error behaviour: same exception types as the reference
+  const hyperanf::Graph one = hyperanf::Graph::from_edges(1, {});
+  hyperanf::EngineConfig bad;
+  bad.systolic_threshold = 0.0;
+  try {
+    hyperanf_b200::NfEngine e(one, hyperanf_b200::from_reference(bad));
+    expect(false, "invalid systolic threshold accepted");
+  } catch (const std::invalid_argument&) {
+  }
+  hyperanf::EngineConfig capped;
+  capped.bucket_bits = 6;
+  capped.seed = 1;
+  capped.max_iterations = 2;
+  try {
+    hyperanf_b200::estimate_nf(hyperanf::gen_clique_path(4, 8),
+                               hyperanf_b200::from_reference(capped));
+    expect(false, "iteration cap not enforced");
+  } catch (const hyperanf_b200::GuardError&) {
+  }
+  std::printf("dropin_test: %zu graphs, %d failures\n", cases.size(), failures);
+  return failures == 0 ? 0 : 1;
+}
