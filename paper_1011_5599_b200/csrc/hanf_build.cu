@@ -1,0 +1,400 @@
+// hanf_build.cu -- builds the union sweep's work on the device, once per
+// graph (NfEngine construction, engine.hpp:70-90):
+//
+//   1. degrees of the shard's nodes; bad CSR input (decreasing offsets, arc
+//      endpoint >= n) raises a flag instead of a host pass over the arcs;
+//   2. nodes with out-degree >= 1 sorted by descending degree, stable in id
+//      (CUB radix sort of (~deg, id));
+//   3. nodes of out-degree > kHubDegree are split into kHubChunk-arc chunks
+//      (one warp each); the others form "light" warps of 32/G nodes with
+//      G = next_pow2(ceil(deg/32)) lanes per node;
+//   4. the task-ordered successor array (TOS): warp w owns rows
+//      [tos/32, tos/32 + trips) of 32 ids, lane (node slot j, sub) holding
+//      successor i*G + sub of node j in row i, or the zero row n.
+// All buffers come from the stream-ordered pool (cudaMallocAsync).
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cstdint>
+#include <vector>
+
+#include "hanf_internal.h"
+
+namespace hanf {
+namespace {
+
+__host__ __device__ __forceinline__ uint32_t log2g_of(uint64_t d) {
+  uint32_t g = 0;
+  while ((32ull << g) < d) ++g;  // G = 2^g lanes, each walks <= 32 arcs
+  return g;
+}
+
+// keys = ~deg (descending degree), vals = node; degree-0 nodes get the
+// largest key and sort to the tail.  Counts hubs and degree-0 nodes.
+__global__ void degree_keys_kernel(const uint64_t* __restrict__ off, uint64_t lo, uint64_t count,
+                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                   unsigned long long* __restrict__ counters, int* __restrict__ bad) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  unsigned long long hubs = 0, zeros = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += stride) {
+    const uint64_t a = off[i], b = off[i + 1];
+    if (b < a) {
+      *bad = 1;
+      keys[i] = 0xffffffffu;
+      vals[i] = static_cast<uint32_t>(lo + i);
+      ++zeros;
+      continue;
+    }
+    const uint64_t d = b - a;
+    keys[i] = d == 0 ? 0xffffffffu : ~static_cast<uint32_t>(d < 0xfffffffeull ? d : 0xfffffffeull);
+    vals[i] = static_cast<uint32_t>(lo + i);
+    hubs += d > kHubDegree;
+    zeros += d == 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    hubs += __shfl_down_sync(0xffffffffu, hubs, o);
+    zeros += __shfl_down_sync(0xffffffffu, zeros, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (hubs) atomicAdd(counters + 0, hubs);
+    if (zeros) atomicAdd(counters + 1, zeros);
+  }
+}
+
+// Boundaries of the light classes in the sorted order: first index whose
+// degree is <= 32 << (lg - 1), for lg = 5..1 (class lg = [start_lg, start_{lg-1})).
+__global__ void class_bounds_kernel(const uint32_t* __restrict__ sorted_keys, uint64_t begin,
+                                    uint64_t end, unsigned long long* __restrict__ bounds) {
+  const int lg = threadIdx.x;  // bounds[lg] = first index with log2g(deg) < lg, lg = 1..5
+  if (lg < 1 || lg > 5) return;
+  const uint64_t cap = 32ull << (lg - 1);
+  uint64_t a = begin, b = end;
+  while (a < b) {
+    const uint64_t mid = (a + b) / 2;
+    const uint64_t d = static_cast<uint32_t>(~sorted_keys[mid]);
+    if (d > cap) a = mid + 1; else b = mid;
+  }
+  bounds[lg] = a;
+}
+
+// per-hub chunk counts
+__global__ void hub_chunks_kernel(const uint64_t* __restrict__ off, uint64_t lo,
+                                  const uint32_t* __restrict__ hub_nodes, uint32_t hubs,
+                                  uint32_t* __restrict__ chunks) {
+  const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= hubs) return;
+  const uint32_t v = hub_nodes[h];
+  const uint64_t d = off[v - lo + 1] - off[v - lo];
+  chunks[h] = static_cast<uint32_t>((d + kHubChunk - 1) / kHubChunk);
+}
+
+// hub chunk tables + their warp tasks (trips) in task slots [0, C)
+__global__ void hub_tasks_kernel(const uint64_t* __restrict__ off, uint64_t lo,
+                                 const uint32_t* __restrict__ hub_nodes, uint32_t hubs,
+                                 const uint32_t* __restrict__ hub_first,
+                                 const uint32_t* __restrict__ hub_count,
+                                 uint32_t* __restrict__ chunk_node, uint32_t* __restrict__ chunk_hub,
+                                 uint64_t* __restrict__ chunk_begin, WarpTask* __restrict__ tasks,
+                                 uint64_t* __restrict__ trips) {
+  const uint32_t h = blockIdx.x;
+  if (h >= hubs) return;
+  const uint32_t v = hub_nodes[h];
+  const uint64_t s = off[v - lo], e = off[v - lo + 1];
+  for (uint32_t k = threadIdx.x; k < hub_count[h]; k += blockDim.x) {
+    const uint32_t c = hub_first[h] + k;
+    const uint64_t a = s + static_cast<uint64_t>(k) * kHubChunk;
+    const uint64_t len = e - a < kHubChunk ? e - a : kHubChunk;
+    chunk_node[c] = v;
+    chunk_hub[c] = h;
+    chunk_begin[c] = a;
+    const uint16_t t = static_cast<uint16_t>((len + 31) / 32);
+    tasks[c] = WarpTask{0, c, t, 5, 0};
+    trips[c] = t;
+  }
+}
+
+// light warp tasks: slots [C, C + W); class table passed by value
+struct LightClasses {
+  uint64_t item_begin[6];   // index into order[] where class lg starts (lg = 0..5)
+  uint64_t item_end[6];
+  uint64_t warp_begin[6];   // task slots of class lg, relative to the first light slot;
+  uint64_t warp_end[6];     // heavier classes first
+  uint64_t total;
+};
+
+__global__ void light_tasks_kernel(const uint64_t* __restrict__ off, uint64_t lo,
+                                   const uint32_t* __restrict__ order, LightClasses lc,
+                                   uint64_t first_slot, WarpTask* __restrict__ tasks,
+                                   uint64_t* __restrict__ trips) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < lc.total;
+       w += stride) {
+    int lg = 5;
+    while (lg > 0 && !(w >= lc.warp_begin[lg] && w < lc.warp_end[lg])) --lg;
+    const uint32_t per = 32u >> lg;
+    const uint64_t item = lc.item_begin[lg] + (w - lc.warp_begin[lg]) * per;
+    const uint64_t rem = lc.item_end[lg] - item;
+    const uint32_t nodes = static_cast<uint32_t>(rem < per ? rem : per);
+    const uint32_t v = order[item];
+    const uint64_t d = off[v - lo + 1] - off[v - lo];
+    const uint32_t G = 1u << lg;
+    const uint16_t t = static_cast<uint16_t>((d + G - 1) / G);
+    tasks[first_slot + w] = WarpTask{0, static_cast<uint32_t>(item), t, static_cast<uint8_t>(lg),
+                                     static_cast<uint8_t>(nodes)};
+    trips[first_slot + w] = t;
+  }
+}
+
+__global__ void set_tos_kernel(WarpTask* __restrict__ tasks, const uint64_t* __restrict__ scan,
+                               uint64_t count) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < count;
+       w += stride)
+    tasks[w].tos = scan[w] * 32;
+}
+
+// One warp per task writes its TOS rows (padding = zero row) and checks the
+// successor ids it copies.
+__global__ void __launch_bounds__(256)
+fill_tos_kernel(const uint64_t* __restrict__ off, uint64_t lo, const uint32_t* __restrict__ succ,
+                uint64_t succ_base, const uint32_t* __restrict__ order,
+                const uint64_t* __restrict__ chunk_begin, const uint32_t* __restrict__ chunk_node,
+                const WarpTask* __restrict__ tasks, uint64_t num_tasks, uint32_t n,
+                uint32_t* __restrict__ tos, int* __restrict__ bad) {
+  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  bool out_of_range = false;
+  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+       w < num_tasks; w += warps) {
+    const WarpTask t = tasks[w];
+    uint32_t* dst = tos + t.tos;
+    for (uint32_t i = lane; i < 32u * t.trips; i += 32) dst[i] = n;
+    __syncwarp();
+    if (t.nodes == 0) {
+      const uint64_t a = chunk_begin[t.item];
+      const uint32_t v = chunk_node[t.item];
+      const uint64_t e = off[v - lo + 1];
+      const uint64_t len = e - a < kHubChunk ? e - a : kHubChunk;
+      for (uint32_t k = lane; k < len; k += 32) {
+        const uint32_t id = succ[a + k - succ_base];
+        out_of_range |= id >= n;
+        dst[k] = id;
+      }
+    } else {
+      const uint32_t G = 1u << t.lg;
+      for (uint32_t j = 0; j < t.nodes; ++j) {
+        const uint32_t v = order[t.item + j];
+        const uint64_t s = off[v - lo], d = off[v - lo + 1] - s;
+        for (uint64_t k = lane; k < d; k += 32) {
+          const uint32_t id = succ[s + k - succ_base];
+          out_of_range |= id >= n;
+          dst[32 * (k >> t.lg) + j * G + (k & (G - 1))] = id;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, out_of_range) && lane == 0) *bad = 1;
+}
+
+template <class T>
+cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), s);
+}
+
+}  // namespace
+
+#define HANF_BUILD_TRY(expr)                    \
+  do {                                          \
+    const cudaError_t _e = (expr);              \
+    if (_e != cudaSuccess) return _e;           \
+  } while (0)
+
+cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
+                               uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
+                               TaskBuild* out, int* bad_input, uint64_t* launches) {
+  *out = TaskBuild{};
+  *bad_input = 0;
+  const uint64_t count = hi - lo;
+  const uint32_t threads = 256;
+  auto grid = [&](uint64_t items) {
+    uint64_t b = (items + threads - 1) / threads;
+    if (b > 148ull * 32) b = 148ull * 32;
+    return static_cast<uint32_t>(b ? b : 1);
+  };
+  uint32_t *keys = nullptr, *vals = nullptr, *skeys = nullptr, *svals = nullptr;
+  unsigned long long* counters = nullptr;
+  int* d_bad = nullptr;
+  HANF_BUILD_TRY(pool_alloc(&keys, count, s));
+  HANF_BUILD_TRY(pool_alloc(&vals, count, s));
+  HANF_BUILD_TRY(pool_alloc(&skeys, count, s));
+  HANF_BUILD_TRY(pool_alloc(&svals, count, s));
+  HANF_BUILD_TRY(pool_alloc(&counters, 8, s));
+  HANF_BUILD_TRY(pool_alloc(&d_bad, 1, s));
+  HANF_BUILD_TRY(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), s));
+  HANF_BUILD_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+  degree_keys_kernel<<<grid(count), threads, 0, s>>>(d_off, lo, count, keys, vals, counters, d_bad);
+  ++*launches;
+  HANF_BUILD_TRY(cudaGetLastError());
+  size_t temp_bytes = 0;
+  HANF_BUILD_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, skeys, vals, svals,
+                                                 static_cast<int64_t>(count), 0, 32, s));
+  void* temp = nullptr;
+  HANF_BUILD_TRY(cudaMallocAsync(&temp, temp_bytes ? temp_bytes : 1, s));
+  HANF_BUILD_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, skeys, vals, svals,
+                                                 static_cast<int64_t>(count), 0, 32, s));
+  ++*launches;
+  HANF_BUILD_TRY(cudaFreeAsync(temp, s));
+  unsigned long long h_counts[8] = {};
+  HANF_BUILD_TRY(cudaMemcpyAsync(h_counts, counters, sizeof(h_counts), cudaMemcpyDeviceToHost, s));
+  HANF_BUILD_TRY(cudaStreamSynchronize(s));
+  const uint64_t hubs = h_counts[0], zeros = h_counts[1];
+  const uint64_t light = count - zeros - hubs;
+  if (hubs > 0xffffffffull || light > 0xffffffffull) return cudaErrorInvalidValue;
+
+  // light class boundaries (sorted order: hubs, then light by desc degree)
+  unsigned long long* d_bounds = counters;  // reuse: bounds[1..5]
+  class_bounds_kernel<<<1, 32, 0, s>>>(skeys, hubs, hubs + light, d_bounds);
+  ++*launches;
+  HANF_BUILD_TRY(cudaGetLastError());
+  unsigned long long b[8] = {};
+  HANF_BUILD_TRY(cudaMemcpyAsync(b, d_bounds, sizeof(b), cudaMemcpyDeviceToHost, s));
+  HANF_BUILD_TRY(cudaStreamSynchronize(s));
+  // class lg (lanes 2^lg) = sorted positions [b[lg+1], b[lg]) with b[6] = hubs, b[0] = end
+  uint64_t start[7];
+  start[6] = hubs;
+  for (int lg = 5; lg >= 1; --lg) start[lg] = b[lg];
+  start[0] = hubs + light;
+  LightClasses lc{};
+  uint64_t warps = 0;
+  for (int lg = 5; lg >= 0; --lg) {
+    // class lg covers degrees (32 << (lg-1), 32 << lg]: positions [start[lg+1], start[lg])
+    const uint64_t a = start[lg + 1], e = start[lg];
+    lc.item_begin[lg] = a - hubs;  // index into order (light nodes only)
+    lc.item_end[lg] = e - hubs;
+    lc.warp_begin[lg] = warps;
+    const uint64_t per = 32u >> lg;
+    warps += (e - a + per - 1) / per;
+    lc.warp_end[lg] = warps;
+  }
+  lc.total = warps;
+
+  // hub tables
+  TaskBuild& o = *out;
+  o.num_hubs = static_cast<uint32_t>(hubs);
+  HANF_BUILD_TRY(pool_alloc(&o.hub_nodes, hubs, s));
+  HANF_BUILD_TRY(pool_alloc(&o.hub_first, hubs, s));
+  HANF_BUILD_TRY(pool_alloc(&o.hub_count, hubs, s));
+  HANF_BUILD_TRY(pool_alloc(&o.hub_ticket, hubs, s));
+  HANF_BUILD_TRY(cudaMemsetAsync(o.hub_ticket, 0, sizeof(uint32_t) * (hubs ? hubs : 1), s));
+  if (hubs) {
+    HANF_BUILD_TRY(cudaMemcpyAsync(o.hub_nodes, svals, sizeof(uint32_t) * hubs,
+                                   cudaMemcpyDeviceToDevice, s));
+    hub_chunks_kernel<<<static_cast<uint32_t>((hubs + 255) / 256), 256, 0, s>>>(
+        d_off, lo, o.hub_nodes, static_cast<uint32_t>(hubs), o.hub_count);
+    ++*launches;
+    HANF_BUILD_TRY(cudaGetLastError());
+  }
+  uint64_t chunks = 0;
+  if (hubs) {
+    size_t tb = 0;
+    HANF_BUILD_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, o.hub_count, o.hub_first,
+                                                 static_cast<int64_t>(hubs), s));
+    void* t2 = nullptr;
+    HANF_BUILD_TRY(cudaMallocAsync(&t2, tb ? tb : 1, s));
+    HANF_BUILD_TRY(cub::DeviceScan::ExclusiveSum(t2, tb, o.hub_count, o.hub_first,
+                                                 static_cast<int64_t>(hubs), s));
+    ++*launches;
+    HANF_BUILD_TRY(cudaFreeAsync(t2, s));
+    uint32_t last_first = 0, last_count = 0;
+    HANF_BUILD_TRY(cudaMemcpyAsync(&last_first, o.hub_first + hubs - 1, 4, cudaMemcpyDeviceToHost, s));
+    HANF_BUILD_TRY(cudaMemcpyAsync(&last_count, o.hub_count + hubs - 1, 4, cudaMemcpyDeviceToHost, s));
+    HANF_BUILD_TRY(cudaStreamSynchronize(s));
+    chunks = static_cast<uint64_t>(last_first) + last_count;
+  }
+  const uint64_t num_tasks = chunks + warps;
+  if (num_tasks > 0x7fffffffull / 32) return cudaErrorInvalidValue;
+  o.num_chunks = static_cast<uint32_t>(chunks);
+  o.num_wtasks = static_cast<uint32_t>(num_tasks);
+  HANF_BUILD_TRY(pool_alloc(&o.chunk_node, chunks, s));
+  HANF_BUILD_TRY(pool_alloc(&o.chunk_hub, chunks, s));
+  uint64_t* chunk_begin = nullptr;
+  HANF_BUILD_TRY(pool_alloc(&chunk_begin, chunks, s));
+  HANF_BUILD_TRY(pool_alloc(&o.wtasks, num_tasks, s));
+  uint64_t *trips = nullptr, *scan = nullptr;
+  HANF_BUILD_TRY(pool_alloc(&trips, num_tasks + 1, s));
+  HANF_BUILD_TRY(pool_alloc(&scan, num_tasks + 1, s));
+  HANF_BUILD_TRY(pool_alloc(&o.order, light, s));
+  if (light)
+    HANF_BUILD_TRY(cudaMemcpyAsync(o.order, svals + hubs, sizeof(uint32_t) * light,
+                                   cudaMemcpyDeviceToDevice, s));
+  if (hubs) {
+    hub_tasks_kernel<<<static_cast<uint32_t>(hubs), 128, 0, s>>>(
+        d_off, lo, o.hub_nodes, static_cast<uint32_t>(hubs), o.hub_first, o.hub_count,
+        o.chunk_node, o.chunk_hub, chunk_begin, o.wtasks, trips);
+    ++*launches;
+    HANF_BUILD_TRY(cudaGetLastError());
+  }
+  if (warps) {
+    light_tasks_kernel<<<grid(warps), threads, 0, s>>>(d_off, lo, o.order, lc, chunks, o.wtasks,
+                                                       trips);
+    ++*launches;
+    HANF_BUILD_TRY(cudaGetLastError());
+  }
+  HANF_BUILD_TRY(cudaMemsetAsync(trips + num_tasks, 0, sizeof(uint64_t), s));
+  {
+    size_t tb = 0;
+    HANF_BUILD_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, trips, scan,
+                                                 static_cast<int64_t>(num_tasks + 1), s));
+    void* t3 = nullptr;
+    HANF_BUILD_TRY(cudaMallocAsync(&t3, tb ? tb : 1, s));
+    HANF_BUILD_TRY(cub::DeviceScan::ExclusiveSum(t3, tb, trips, scan,
+                                                 static_cast<int64_t>(num_tasks + 1), s));
+    ++*launches;
+    HANF_BUILD_TRY(cudaFreeAsync(t3, s));
+  }
+  uint64_t rows = 0;
+  HANF_BUILD_TRY(cudaMemcpyAsync(&rows, scan + num_tasks, 8, cudaMemcpyDeviceToHost, s));
+  HANF_BUILD_TRY(cudaStreamSynchronize(s));
+  if (num_tasks) {
+    set_tos_kernel<<<grid(num_tasks), threads, 0, s>>>(o.wtasks, scan, num_tasks);
+    ++*launches;
+    HANF_BUILD_TRY(cudaGetLastError());
+  }
+  o.tos_words = rows * 32;
+  HANF_BUILD_TRY(pool_alloc(&o.tos, o.tos_words, s));
+  if (num_tasks) {
+    fill_tos_kernel<<<grid(num_tasks * 32), threads, 0, s>>>(
+        d_off, lo, d_succ, succ_base, o.order, chunk_begin, o.chunk_node, o.wtasks, num_tasks,
+        static_cast<uint32_t>(n), o.tos, d_bad);
+    ++*launches;
+    HANF_BUILD_TRY(cudaGetLastError());
+  }
+  int h_bad = 0;
+  HANF_BUILD_TRY(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HANF_BUILD_TRY(cudaFreeAsync(keys, s));
+  HANF_BUILD_TRY(cudaFreeAsync(vals, s));
+  HANF_BUILD_TRY(cudaFreeAsync(skeys, s));
+  HANF_BUILD_TRY(cudaFreeAsync(svals, s));
+  HANF_BUILD_TRY(cudaFreeAsync(counters, s));
+  HANF_BUILD_TRY(cudaFreeAsync(d_bad, s));
+  HANF_BUILD_TRY(cudaFreeAsync(chunk_begin, s));
+  HANF_BUILD_TRY(cudaFreeAsync(trips, s));
+  HANF_BUILD_TRY(cudaFreeAsync(scan, s));
+  HANF_BUILD_TRY(cudaStreamSynchronize(s));
+  *bad_input = h_bad;
+  return cudaSuccess;
+}
+
+void free_tasks_device(TaskBuild* t, cudaStream_t s) {
+  void* ptrs[] = {t->order, t->wtasks, t->tos, t->chunk_node, t->chunk_hub,
+                  t->hub_nodes, t->hub_first, t->hub_count, t->hub_ticket};
+  for (void* p : ptrs)
+    if (p) cudaFreeAsync(p, s);
+  *t = TaskBuild{};
+}
+
+}  // namespace hanf

@@ -1,12 +1,16 @@
 // hanf_engine.cu -- host engine behind the C-ABI (include/hanf.h).
 //
 // Restates the NfEngine surface (engine.hpp:68-298) over device state:
-//   - CSR of the node range this engine updates, resident in HBM;
-//   - two counter generations (reference packing, hll.hpp:183-240);
+//   - the union sweep's work, built on the device from the caller's CSR
+//     (hanf_build.cu); the CSR itself is not kept;
+//   - two counter generations (reference packing, hll.hpp:183-240) plus an
+//     all-zero row n;
 //   - two "modified" bitmaps (bit v <-> modified_[v], engine.hpp:287), word
 //     i of which is exactly the dirty flag of 64-counter block i (:206);
 //   - cached per-counter estimates and per-block sums (engine.hpp:288).
-// The union/estimate/reduce kernels live in hanf_kernels.cu.
+// Device memory comes from the stream-ordered pool (cudaMallocAsync, kept
+// cached across engines), pinned host staging from a process-wide cache, so
+// creating and destroying engines (estimate_nf) costs no allocator syncs.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -16,7 +20,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <iostream>
-#include <thread>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -69,18 +74,65 @@ hanf_status make_params(uint32_t b, uint64_t seed, uint32_t r, hanf_sketch_param
 }
 
 template <class T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t count = 0;
-  cudaError_t alloc(size_t n) {
-    count = n;
-    return cudaMalloc(&p, sizeof(T) * (n ? n : 1));
+cudaError_t palloc(T** p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), s);
+}
+template <class T>
+void pfree(T*& p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+  p = nullptr;
+}
+
+// Keep freed device memory in the pool (no release at synchronisation).
+void configure_pool(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t threshold = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
   }
-  void free() {
-    if (p) cudaFree(p);
-    p = nullptr;
+  done.push_back(device);
+}
+
+// Process-wide cache of pinned host blocks (cudaMallocHost / cudaFreeHost
+// synchronise the device; engines borrow and return blocks instead).
+class PinnedCache {
+ public:
+  void* get(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      auto it = free_.lower_bound(bytes);
+      if (it != free_.end()) {
+        void* p = it->second;
+        sizes_[p] = it->first;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes ? bytes : 1) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu_);
+    sizes_[p] = bytes;
+    return p;
   }
+  void put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lock(mu_);
+    free_.emplace(sizes_[p], p);
+  }
+
+ private:
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+  std::map<void*, size_t> sizes_;
 };
+PinnedCache& pinned() {
+  static PinnedCache* c = new PinnedCache();  // never destroyed: outlives engines
+  return *c;
+}
 
 }  // namespace
 
@@ -98,27 +150,20 @@ struct hanf_engine {
   int device = 0;
   cudaStream_t stream = nullptr;
 
-  DevBuf<uint64_t> cnt[2];
-  DevBuf<uint64_t> mod[2];
-  DevBuf<double> est;
-  DevBuf<double> block_sums;
-  DevBuf<double> log_table;
-  DevBuf<uint32_t> order;     // light nodes, descending out-degree
-  DevBuf<hanf::WarpTask> wtasks;
-  DevBuf<uint32_t> tos;       // task-ordered successor ids (see build_tasks)
-  uint64_t tos_words = 0;
-  uint32_t num_wtasks = 0;
-  DevBuf<uint32_t> hub_node;  // per hub chunk
-  DevBuf<uint64_t> partials;
-  DevBuf<uint32_t> hub_nodes, hub_first, hub_count, chunk_hub, hub_ticket;
-  DevBuf<hanf::ReduceOut> reduce;
-  DevBuf<double> reduce_sums;
-  DevBuf<unsigned long long> reduce_counts;
-  uint32_t num_hubs = 0;
+  uint64_t* cnt[2] = {nullptr, nullptr};  // (n + 1) * W words + 8 (window loads)
+  uint64_t* mod[2] = {nullptr, nullptr};  // blocks words
+  double* est = nullptr;                  // n
+  double* block_sums = nullptr;           // blocks
+  double* log_table = nullptr;            // m + 1
+  uint64_t* partials = nullptr;           // hub chunks * W
+  hanf::TaskBuild tasks;
+  hanf::ReduceOut* reduce = nullptr;
+  double* reduce_sums = nullptr;
+  unsigned long long* reduce_counts = nullptr;
   int gather_mode = -1;       // union kernel variant (-1: per-layout default)
 
-  hanf::ReduceOut* h_reduce = nullptr;  // pinned: total + count
-  double* h_block_sums = nullptr;       // pinned: exact_sum mode
+  hanf::ReduceOut* h_reduce = nullptr;  // pinned (cache): total + count
+  double* h_block_sums = nullptr;       // pinned (cache): exact_sum mode
 
   int cur = 0;               // index of the current generation
   uint64_t t = 0;            // iteration()
@@ -143,199 +188,45 @@ struct hanf_engine {
   bool use_graphs = true;
 
   ~hanf_engine() {
+    if (device >= 0) cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
     for (auto& a : graphs)
       for (auto& b : a)
         for (auto& c : b)
           if (c.exec) cudaGraphExecDestroy(c.exec);
     for (auto& x : ev)
       if (x) cudaEventDestroy(x);
-    if (device >= 0) cudaSetDevice(device);
-    for (int i = 0; i < 2; ++i) { cnt[i].free(); mod[i].free(); }
-    est.free(); block_sums.free(); log_table.free(); order.free();
-    wtasks.free(); tos.free(); hub_node.free(); partials.free();
-    hub_nodes.free(); hub_first.free(); hub_count.free(); chunk_hub.free(); hub_ticket.free();
-    reduce.free(); reduce_sums.free(); reduce_counts.free();
-    if (h_reduce) cudaFreeHost(h_reduce);
-    if (h_block_sums) cudaFreeHost(h_block_sums);
-    if (stream) cudaStreamDestroy(stream);
+    if (stream) {
+      for (int i = 0; i < 2; ++i) {
+        pfree(cnt[i], stream);
+        pfree(mod[i], stream);
+      }
+      pfree(est, stream);
+      pfree(block_sums, stream);
+      pfree(log_table, stream);
+      pfree(partials, stream);
+      pfree(reduce, stream);
+      pfree(reduce_sums, stream);
+      pfree(reduce_counts, stream);
+      hanf::free_tasks_device(&tasks, stream);
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+    pinned().put(h_reduce);
+    pinned().put(h_block_sums);
   }
 };
 
 namespace {
 
-// Builds the union sweep's work for nodes [lo, hi) (once per graph):
-//  - nodes with out-degree > kHubDegree: chunks of kHubChunk arcs, one warp
-//    each, plus one finalize warp per node (hub_nodes/first/count);
-//  - nodes with out-degree 1..kHubDegree ("light"): sorted by descending
-//    degree (stable in id), G = next_pow2(ceil(deg/32)) lanes per node,
-//    32/G nodes of one class per warp;
-//  - the task-ordered successor array: warp w owns rows [tos/32, +trips) of
-//    32 ids; lane (node slot j, sub) reads successor i*G + sub of node j in
-//    row i, or the zero row n past the end of the list.
-// Degree-0 nodes get no task: their counters never change and both
-// generations hold them from seeding.
-hanf_status build_tasks(hanf_engine* e, const uint64_t* offsets, const uint32_t* succ) {
-  const uint64_t lo = e->lo, hi = e->hi;
-  const uint32_t maxd = hanf::kHubDegree;
-  const uint32_t zero = static_cast<uint32_t>(e->n);
-  std::vector<uint64_t> hist(maxd + 2, 0);
-  std::vector<std::pair<uint64_t, uint32_t>> hub_list;
-  uint64_t hub_chunks = 0;
-  for (uint64_t v = lo; v < hi; ++v) {
-    const uint64_t d = offsets[v + 1] - offsets[v];
-    if (d == 0) continue;
-    if (d > maxd) {
-      hub_list.emplace_back(d, static_cast<uint32_t>(v));
-      hub_chunks += (d + hanf::kHubChunk - 1) / hanf::kHubChunk;
-    } else {
-      ++hist[d];
-    }
-  }
-  std::stable_sort(hub_list.begin(), hub_list.end(),
-                   [](const auto& a, const auto& b) { return a.first > b.first; });
-  std::vector<uint64_t> pos(maxd + 2, 0);
-  uint64_t light = 0;
-  for (uint64_t d = maxd; d >= 1; --d) {
-    pos[d] = light;
-    light += hist[d];
-  }
-  if (light > 0xffffffffull || hub_chunks > 0xffffffffull)
-    return fail(HANF_INVALID_ARGUMENT, "too many nodes in one engine shard");
-  std::vector<uint32_t> order(light ? light : 1);
-  std::vector<uint32_t> ldeg(light ? light : 1);
-  for (uint64_t v = lo; v < hi; ++v) {
-    const uint64_t d = offsets[v + 1] - offsets[v];
-    if (d == 0 || d > maxd) continue;
-    ldeg[pos[d]] = static_cast<uint32_t>(d);
-    order[pos[d]++] = static_cast<uint32_t>(v);
-  }
-  auto log2g_of = [](uint64_t d) {
-    uint32_t g = 0;
-    while ((32ull << g) < d) ++g;  // G = 2^g lanes, each <= 32 arcs
-    return g;
-  };
-  // warp tasks: hub chunks first (longest nodes first), then light classes
-  std::vector<hanf::WarpTask> tasks;
-  tasks.reserve(hub_chunks + light / 1 + 1);
-  std::vector<uint32_t> hub_node(hub_chunks ? hub_chunks : 1);
-  std::vector<uint32_t> chunk_hub(hub_chunks ? hub_chunks : 1);
-  std::vector<uint64_t> chunk_begin(hub_chunks ? hub_chunks : 1);
-  std::vector<uint32_t> hubs_v(hub_list.size() + 1), hubs_first(hub_list.size() + 1),
-      hubs_count(hub_list.size() + 1);
-  uint64_t tos = 0, c = 0;
-  for (size_t h = 0; h < hub_list.size(); ++h) {
-    const uint32_t v = hub_list[h].second;
-    const uint64_t s = offsets[v], en = offsets[v + 1];
-    hubs_v[h] = v;
-    hubs_first[h] = static_cast<uint32_t>(c);
-    uint32_t k = 0;
-    for (uint64_t a = s; a < en; a += hanf::kHubChunk, ++k, ++c) {
-      const uint64_t len = std::min<uint64_t>(hanf::kHubChunk, en - a);
-      hub_node[c] = v;
-      chunk_hub[c] = static_cast<uint32_t>(h);
-      chunk_begin[c] = a;
-      const uint16_t trips = static_cast<uint16_t>((len + 31) / 32);
-      tasks.push_back(hanf::WarpTask{tos, static_cast<uint32_t>(c), trips, 5, 0});
-      tos += 32ull * trips;
-    }
-    hubs_count[h] = k;
-  }
-  for (uint64_t i = 0; i < light;) {
-    const uint32_t lg = log2g_of(ldeg[i]);
-    const uint32_t per = 32u >> lg;
-    uint64_t cnt = 0;
-    while (cnt < per && i + cnt < light && log2g_of(ldeg[i + cnt]) == lg) ++cnt;
-    const uint32_t G = 1u << lg;
-    const uint16_t trips = static_cast<uint16_t>((ldeg[i] + G - 1) / G);
-    tasks.push_back(hanf::WarpTask{tos, static_cast<uint32_t>(i), trips,
-                                   static_cast<uint8_t>(lg), static_cast<uint8_t>(cnt)});
-    tos += 32ull * trips;
-    i += cnt;
-  }
-  if (tasks.size() > 0x7fffffffull / 32) return fail(HANF_INVALID_ARGUMENT, "task table overflow");
-  std::vector<uint32_t> tos_ids;
-  try {
-    tos_ids.assign(tos ? tos : 1, zero);
-  } catch (const std::bad_alloc&) {
-    return fail(HANF_OUT_OF_MEMORY, "task-ordered successor array allocation failed");
-  }
-  auto fill = [&](uint64_t t0, uint64_t t1) {
-    for (uint64_t t = t0; t < t1; ++t) {
-      const hanf::WarpTask& w = tasks[t];
-      uint32_t* dst = tos_ids.data() + w.tos;
-      if (w.nodes == 0) {
-        const uint64_t a = chunk_begin[w.item];
-        const uint64_t len = std::min<uint64_t>(hanf::kHubChunk, offsets[hub_node[w.item] + 1] - a);
-        for (uint64_t k = 0; k < len; ++k) dst[k] = succ[a + k];
-      } else {
-        const uint32_t G = 1u << w.lg;
-        for (uint32_t j = 0; j < w.nodes; ++j) {
-          const uint32_t v = order[w.item + j];
-          const uint64_t s = offsets[v], d = offsets[v + 1] - s;
-          for (uint64_t k = 0; k < d; ++k) {
-            const uint64_t i = k / G, sub = k % G;
-            dst[32 * i + j * G + sub] = succ[s + k];
-          }
-        }
-      }
-    }
-  };
-  {
-    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const uint64_t T = tasks.size();
-    if (T > 4096 && nt > 1) {
-      std::vector<std::thread> pool;
-      for (unsigned p = 0; p < nt; ++p) pool.emplace_back(fill, T * p / nt, T * (p + 1) / nt);
-      for (auto& th : pool) th.join();
-    } else {
-      fill(0, T);
-    }
-  }
-  e->num_wtasks = static_cast<uint32_t>(tasks.size());
-  e->num_hubs = static_cast<uint32_t>(hub_list.size());
-  e->tos_words = tos;
-  cudaStream_t st = e->stream;
-  HANF_CUDA(e->order.alloc(order.size()));
-  HANF_CUDA(cudaMemcpyAsync(e->order.p, order.data(), sizeof(uint32_t) * order.size(),
-                            cudaMemcpyHostToDevice, st));
-  HANF_CUDA(e->wtasks.alloc(tasks.size()));
-  if (!tasks.empty())
-    HANF_CUDA(cudaMemcpyAsync(e->wtasks.p, tasks.data(), sizeof(hanf::WarpTask) * tasks.size(),
-                              cudaMemcpyHostToDevice, st));
-  HANF_CUDA(e->tos.alloc(tos_ids.size()));
-  HANF_CUDA(cudaMemcpyAsync(e->tos.p, tos_ids.data(), sizeof(uint32_t) * tos_ids.size(),
-                            cudaMemcpyHostToDevice, st));
-  HANF_CUDA(e->hub_node.alloc(hub_node.size()));
-  HANF_CUDA(cudaMemcpyAsync(e->hub_node.p, hub_node.data(), sizeof(uint32_t) * hub_node.size(),
-                            cudaMemcpyHostToDevice, st));
-  HANF_CUDA(e->partials.alloc(static_cast<size_t>(hub_chunks ? hub_chunks : 1) * e->words));
-  HANF_CUDA(e->chunk_hub.alloc(chunk_hub.size()));
-  HANF_CUDA(cudaMemcpyAsync(e->chunk_hub.p, chunk_hub.data(), sizeof(uint32_t) * chunk_hub.size(),
-                            cudaMemcpyHostToDevice, st));
-  HANF_CUDA(e->hub_ticket.alloc(hubs_v.size()));
-  HANF_CUDA(cudaMemsetAsync(e->hub_ticket.p, 0, sizeof(uint32_t) * hubs_v.size(), st));
-  HANF_CUDA(e->hub_nodes.alloc(hubs_v.size()));
-  HANF_CUDA(e->hub_first.alloc(hubs_first.size()));
-  HANF_CUDA(e->hub_count.alloc(hubs_count.size()));
-  HANF_CUDA(cudaMemcpyAsync(e->hub_nodes.p, hubs_v.data(), sizeof(uint32_t) * hubs_v.size(),
-                            cudaMemcpyHostToDevice, st));
-  HANF_CUDA(cudaMemcpyAsync(e->hub_first.p, hubs_first.data(), sizeof(uint32_t) * hubs_first.size(),
-                            cudaMemcpyHostToDevice, st));
-  HANF_CUDA(cudaMemcpyAsync(e->hub_count.p, hubs_count.data(), sizeof(uint32_t) * hubs_count.size(),
-                            cudaMemcpyHostToDevice, st));
-  // the staging vectors are freed on return: make sure the copies are done
-  HANF_CUDA(cudaStreamSynchronize(st));
-  return HANF_OK;
-}
-
 // Recomputes estimates of the counters flagged in `dirty` (all when null)
 // for blocks [b0, b1) of generation g.
 hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t b0, uint64_t b1) {
   hanf::EstimateArgs a{};
-  a.counters = e->cnt[g].p;
+  a.counters = e->cnt[g];
   a.dirty = dirty;
-  a.est = e->est.p;
-  a.block_sums = e->block_sums.p;
+  a.est = e->est;
+  a.block_sums = e->block_sums;
   a.n = e->n;
   a.block_begin = b0;
   a.block_end = b1;
@@ -344,7 +235,7 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
   a.registers = e->params.registers;
   a.register_bits = e->params.register_bits;
   a.words = e->params.words_per_counter;
-  a.log_table = e->log_table.p;
+  a.log_table = e->log_table;
   HANF_CUDA(hanf::launch_estimate(a, e->stream, &e->launches));
   return HANF_OK;
 }
@@ -356,10 +247,10 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
 hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute, uint64_t b0,
                            uint64_t b1, bool in_step) {
   hanf::FinishArgs f{};
-  f.est = recompute ? e->est.p : nullptr;
+  f.est = recompute ? e->est : nullptr;
   f.bits = bits;
-  f.block_sums = e->block_sums.p;
-  f.out = e->reduce.p;
+  f.block_sums = e->block_sums;
+  f.out = e->reduce;
   f.n = e->n;
   f.blocks = e->blocks;
   f.b0 = b0;
@@ -367,10 +258,10 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
-  HANF_CUDA(cudaMemcpyAsync(e->h_reduce, e->reduce.p, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+  HANF_CUDA(cudaMemcpyAsync(e->h_reduce, e->reduce, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                             e->stream));
   if (e->cfg.exact_sum)
-    HANF_CUDA(cudaMemcpyAsync(e->h_block_sums, e->block_sums.p, sizeof(double) * e->blocks,
+    HANF_CUDA(cudaMemcpyAsync(e->h_block_sums, e->block_sums, sizeof(double) * e->blocks,
                               cudaMemcpyDeviceToHost, e->stream));
   return HANF_OK;
 }
@@ -412,16 +303,16 @@ hanf_status seed_all(hanf_engine* e) {
   e->t = 0;
   e->stale_valid = false;
   e->systolic = false;
-  HANF_CUDA(hanf::launch_seed(e->cnt[0].p, e->cnt[1].p, e->mod[0].p, e->n, 0, e->n,
+  HANF_CUDA(hanf::launch_seed(e->cnt[0], e->cnt[1], e->mod[0], e->n, 0, e->n,
                               e->params.bucket_bits, e->params.register_bits,
                               e->params.words_per_counter, e->params.seed, e->stream,
                               &e->launches));
-  HANF_CUDA(cudaMemsetAsync(e->mod[1].p, 0, sizeof(uint64_t) * e->blocks, e->stream));
+  HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
   if (st != HANF_OK) return st;
   uint64_t count = 0;
   e->last_count = e->n;
-  return finish(e, e->mod[0].p, false, 0, 0, &e->last_sum, &count);
+  return finish(e, e->mod[0], false, 0, 0, &e->last_sum, &count);
 }
 
 hanf_status validate_config(const hanf_config* cfg) {
@@ -437,30 +328,30 @@ hanf_status validate_config(const hanf_config* cfg) {
 hanf_status compute_local(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
-  HANF_CUDA(cudaMemsetAsync(e->mod[ng].p + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
+  HANF_CUDA(cudaMemsetAsync(e->mod[ng] + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
   hanf::UnionArgs a{};
-  a.tos = e->tos.p;
-  a.wtasks = e->wtasks.p;
-  a.num_wtasks = e->num_wtasks;
+  a.tos = e->tasks.tos;
+  a.wtasks = e->tasks.wtasks;
+  a.num_wtasks = e->tasks.num_wtasks;
   a.zero_row = static_cast<uint32_t>(e->n);
   const bool fused = hanf::fused_estimates(e->params.register_bits, e->params.registers);
-  a.est = fused ? e->est.p : nullptr;
+  a.est = fused ? e->est : nullptr;
   a.ep = hanf::EstimateParams{e->params.alpha, static_cast<double>(e->params.registers),
                               e->params.registers, e->params.register_bits,
-                              e->params.words_per_counter, e->log_table.p};
-  a.cur = e->cnt[g].p;
-  a.next = e->cnt[ng].p;
-  a.mod_cur = e->mod[g].p;
-  a.mod_next = e->mod[ng].p;
-  a.order = e->order.p;
-  a.hub_node = e->hub_node.p;
-  a.partials = e->partials.p;
-  a.chunk_hub = e->chunk_hub.p;
-  a.hub_nodes = e->hub_nodes.p;
-  a.hub_first = e->hub_first.p;
-  a.hub_count = e->hub_count.p;
-  a.hub_ticket = e->hub_ticket.p;
+                              e->params.words_per_counter, e->log_table};
+  a.cur = e->cnt[g];
+  a.next = e->cnt[ng];
+  a.mod_cur = e->mod[g];
+  a.mod_next = e->mod[ng];
+  a.order = e->tasks.order;
+  a.hub_node = e->tasks.chunk_node;
+  a.partials = e->partials;
+  a.chunk_hub = e->tasks.chunk_hub;
+  a.hub_nodes = e->tasks.hub_nodes;
+  a.hub_first = e->tasks.hub_first;
+  a.hub_count = e->tasks.hub_count;
+  a.hub_ticket = e->tasks.hub_ticket;
   a.words = e->params.words_per_counter;
   // skipping unmodified successors costs a bitmap probe per arc and saves
   // a counter gather per skipped arc: worth it once most counters settled
@@ -472,11 +363,11 @@ hanf_status compute_local(hanf_engine* e) {
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
   const bool sharded = e->lo != 0 || e->hi != e->n;
   if (!fused) {
-    const hanf_status st = run_estimates(e, ng, e->mod[ng].p, w0, w1);
+    const hanf_status st = run_estimates(e, ng, e->mod[ng], w0, w1);
     if (st != HANF_OK) return st;
   } else if (sharded) {
     // block sums of this shard now: they are exchanged before commit
-    hanf::FinishArgs f{e->est.p, e->mod[ng].p, e->block_sums.p, e->reduce.p, e->n, e->blocks, w0, w1};
+    hanf::FinishArgs f{e->est, e->mod[ng], e->block_sums, e->reduce, e->n, e->blocks, w0, w1};
     HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   }
   return HANF_OK;
@@ -491,7 +382,7 @@ bool commit_recomputes(const hanf_engine* e) {
 
 hanf_status commit_enqueue(hanf_engine* e) {
   const int ng = 1 - e->cur;
-  return finish_enqueue(e, e->mod[ng].p, commit_recomputes(e), 0, e->blocks, true);
+  return finish_enqueue(e, e->mod[ng], commit_recomputes(e), 0, e->blocks, true);
 }
 
 hanf_status commit_complete(hanf_engine* e, hanf_iteration_report* rep) {
@@ -585,10 +476,11 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   hanf_status st = validate_config(cfg_in);
   if (st != HANF_OK) return st;
   const uint64_t n = g->n;
-  if (n > (1ull << 32)) return fail(HANF_INVALID_ARGUMENT, "graph too large for 32-bit node ids");
+  if (n > (1ull << 32) - 1)
+    return fail(HANF_INVALID_ARGUMENT, "graph too large for 32-bit node ids");
   if (n > 0 && !g->offsets) return fail(HANF_INVALID_ARGUMENT, "null offsets");
-  if (n > 0 && g->offsets[n] != g->num_arcs)
-    return fail(HANF_INVALID_ARGUMENT, "offsets[n] must equal the arc count");
+  if (n > 0 && (g->offsets[0] != 0 || g->offsets[n] != g->num_arcs))
+    return fail(HANF_INVALID_ARGUMENT, "offsets must run from 0 to the arc count");
   if (g->num_arcs > 0 && !g->arcs) return fail(HANF_INVALID_ARGUMENT, "null arcs");
 
   hanf_config cfg = *cfg_in;
@@ -614,6 +506,9 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   e->hi = hi;
   e->blocks = (n + 63) / 64;
   e->words = params.words_per_counter;
+  if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
+  if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
+  if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
 
   auto bail = [&](hanf_status s) {
     const std::string msg = g_last_error;
@@ -628,60 +523,73 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   } while (0)
 
   HANF_TRY(cudaSetDevice(cfg.device));
+  configure_pool(cfg.device);
   HANF_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  cudaStream_t s = e->stream;
   // row n is an all-zero counter (the union kernels' padding target); 8
   // extra words keep the 256-bit window loads of the last rows in bounds
   const uint64_t nw = (n + 1) * e->words + 8;
-  HANF_TRY(e->cnt[0].alloc(nw));
-  HANF_TRY(e->cnt[1].alloc(nw));
-  HANF_TRY(cudaMemsetAsync(e->cnt[0].p + n * e->words, 0, sizeof(uint64_t) * (e->words + 8),
-                           e->stream));
-  HANF_TRY(cudaMemsetAsync(e->cnt[1].p + n * e->words, 0, sizeof(uint64_t) * (e->words + 8),
-                           e->stream));
-  HANF_TRY(e->mod[0].alloc(e->blocks));
-  HANF_TRY(e->mod[1].alloc(e->blocks));
-  HANF_TRY(e->est.alloc(n));
-  HANF_TRY(e->block_sums.alloc(e->blocks));
-  HANF_TRY(e->reduce.alloc(1));
+  HANF_TRY(palloc(&e->cnt[0], nw, s));
+  HANF_TRY(palloc(&e->cnt[1], nw, s));
+  HANF_TRY(cudaMemsetAsync(e->cnt[0] + n * e->words, 0, sizeof(uint64_t) * (e->words + 8), s));
+  HANF_TRY(cudaMemsetAsync(e->cnt[1] + n * e->words, 0, sizeof(uint64_t) * (e->words + 8), s));
+  HANF_TRY(palloc(&e->mod[0], e->blocks, s));
+  HANF_TRY(palloc(&e->mod[1], e->blocks, s));
+  HANF_TRY(palloc(&e->est, n, s));
+  HANF_TRY(palloc(&e->block_sums, e->blocks, s));
   {
     const uint64_t ctas = (e->blocks + hanf::kFinishThreads - 1) / hanf::kFinishThreads;
-    HANF_TRY(e->reduce_sums.alloc(ctas));
-    HANF_TRY(e->reduce_counts.alloc(ctas));
+    HANF_TRY(palloc(&e->reduce, 1, s));
+    HANF_TRY(palloc(&e->reduce_sums, ctas, s));
+    HANF_TRY(palloc(&e->reduce_counts, ctas, s));
     hanf::ReduceOut init{};
-    init.partial_sum = e->reduce_sums.p;
-    init.partial_count = e->reduce_counts.p;
-    HANF_TRY(cudaMemcpy(e->reduce.p, &init, sizeof(init), cudaMemcpyHostToDevice));
+    init.partial_sum = e->reduce_sums;
+    init.partial_count = e->reduce_counts;
+    HANF_TRY(cudaMemcpyAsync(e->reduce, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    HANF_TRY(cudaStreamSynchronize(s));  // `init` is a stack object
   }
-  HANF_TRY(cudaMallocHost(&e->h_reduce, sizeof(hanf::ReduceOut)));
-  if (cfg.exact_sum)
-    HANF_TRY(cudaMallocHost(&e->h_block_sums, sizeof(double) * (e->blocks ? e->blocks : 1)));
-
-  // the CSR itself is not kept on the device: build_tasks lays the shard's
-  // successor ids out in task order (the only form the union sweep reads)
-  if (n > 0) {
-    for (uint64_t v = lo; v < hi; ++v)
-      if (g->offsets[v + 1] < g->offsets[v])
-        return bail(fail(HANF_INVALID_ARGUMENT, "offsets must be non-decreasing"));
-    for (uint64_t i = g->offsets[lo]; i < g->offsets[hi]; ++i)
-      if (g->arcs[i] >= n) return bail(fail(HANF_INVALID_ARGUMENT, "arc endpoint out of range"));
+  e->h_reduce = static_cast<hanf::ReduceOut*>(pinned().get(sizeof(hanf::ReduceOut)));
+  if (!e->h_reduce) return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
+  if (cfg.exact_sum) {
+    e->h_block_sums = static_cast<double*>(pinned().get(sizeof(double) * (e->blocks ? e->blocks : 1)));
+    if (!e->h_block_sums) return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
   }
-  if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
-  if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
-  if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
-
   // linear-counting table m*log(m/z), same expression as hll.hpp:139
   {
     const double m = static_cast<double>(params.registers);
     std::vector<double> table(params.registers + 1, 0.0);
     for (uint32_t z = 1; z <= params.registers; ++z)
       table[z] = m * std::log(m / static_cast<double>(z));
-    HANF_TRY(e->log_table.alloc(table.size()));
-    HANF_TRY(cudaMemcpy(e->log_table.p, table.data(), sizeof(double) * table.size(),
-                        cudaMemcpyHostToDevice));
+    HANF_TRY(palloc(&e->log_table, table.size(), s));
+    HANF_TRY(cudaMemcpyAsync(e->log_table, table.data(), sizeof(double) * table.size(),
+                             cudaMemcpyHostToDevice, s));
+    HANF_TRY(cudaStreamSynchronize(s));
   }
   if (n > 0) {
-    st = build_tasks(e, g->offsets, g->arcs);
-    if (st != HANF_OK) return bail(st);
+    // the shard's CSR goes to the device only to build the tasks (it is
+    // laid out again in task order there) and is released afterwards
+    const uint64_t a0 = g->offsets[lo], a1 = g->offsets[hi];
+    uint64_t* d_off = nullptr;
+    uint32_t* d_succ = nullptr;
+    HANF_TRY(palloc(&d_off, hi - lo + 1, s));
+    HANF_TRY(palloc(&d_succ, a1 - a0, s));
+    HANF_TRY(cudaMemcpyAsync(d_off, g->offsets + lo, sizeof(uint64_t) * (hi - lo + 1),
+                             cudaMemcpyHostToDevice, s));
+    if (a1 > a0)
+      HANF_TRY(cudaMemcpyAsync(d_succ, g->arcs + a0, sizeof(uint32_t) * (a1 - a0),
+                               cudaMemcpyHostToDevice, s));
+    int bad = 0;
+    const cudaError_t be =
+        hanf::build_tasks_device(d_off, d_succ, lo, hi, a0, n, s, &e->tasks, &bad, &e->launches);
+    pfree(d_off, s);
+    pfree(d_succ, s);
+    if (be == cudaErrorInvalidValue)
+      return bail(fail(HANF_INVALID_ARGUMENT, "too many nodes or tasks in one engine shard"));
+    HANF_TRY(be);
+    if (bad)
+      return bail(fail(HANF_INVALID_ARGUMENT,
+                       "arc endpoint out of range or offsets not non-decreasing"));
+    HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->words, s));
     st = seed_all(e);
     if (st != HANF_OK) return bail(st);
   }
@@ -691,6 +599,7 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
 }
 
 void hanf_destroy(hanf_engine* e) { delete e; }
+
 
 hanf_status hanf_reset(hanf_engine* e) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
@@ -822,7 +731,7 @@ hanf_status hanf_read_counters(hanf_engine* e, uint64_t first, uint64_t count, u
   if (count == 0) return HANF_OK;
   if (!dst) return fail(HANF_INVALID_ARGUMENT, "null destination");
   HANF_CUDA(cudaSetDevice(e->device));
-  HANF_CUDA(cudaMemcpyAsync(dst, e->cnt[e->cur].p + first * e->words,
+  HANF_CUDA(cudaMemcpyAsync(dst, e->cnt[e->cur] + first * e->words,
                             sizeof(uint64_t) * count * e->words, cudaMemcpyDeviceToHost,
                             e->stream));
   HANF_CUDA(cudaStreamSynchronize(e->stream));
@@ -889,9 +798,9 @@ hanf_status hanf_timing(const hanf_engine* e, double* union_ms, double* estimate
 hanf_status hanf_device_buffers(hanf_engine* e, hanf_buffers* out) {
   if (!e || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
   const int ng = 1 - e->cur;
-  out->next_counters = e->cnt[ng].p;
-  out->next_modified = e->mod[ng].p;
-  out->block_sums = e->block_sums.p;
+  out->next_counters = e->cnt[ng];
+  out->next_modified = e->mod[ng];
+  out->block_sums = e->block_sums;
   out->words_per_counter = e->words;
   out->blocks = e->blocks;
   out->shard_begin = e->lo;

@@ -23,6 +23,30 @@ struct WarpTask {      // 16 bytes, one per warp of the union launch
   uint8_t nodes;       // light: nodes in this warp (<= 32 >> lg); 0 = hub chunk
 };
 
+// Device-built work of the union sweep (hanf_build.cu); pool allocations.
+struct TaskBuild {
+  uint32_t* order = nullptr;       // light nodes, descending degree
+  WarpTask* wtasks = nullptr;      // hub chunks first, then light warps (heavy first)
+  uint32_t* tos = nullptr;         // task-ordered successor ids
+  uint64_t tos_words = 0;
+  uint32_t num_wtasks = 0;
+  uint32_t* chunk_node = nullptr;  // per hub chunk: node, hub index
+  uint32_t* chunk_hub = nullptr;
+  uint32_t num_chunks = 0;
+  uint32_t* hub_nodes = nullptr;   // per hub: node, first chunk, chunks, ticket
+  uint32_t* hub_first = nullptr;
+  uint32_t* hub_count = nullptr;
+  uint32_t* hub_ticket = nullptr;
+  uint32_t num_hubs = 0;
+};
+// Builds the tasks of nodes [lo, hi) from the shard's CSR on the device
+// (d_off = offsets[lo..hi], d_succ = arcs from index succ_base).  Sets
+// *bad_input when offsets decrease or an arc endpoint is >= n.
+cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
+                               uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
+                               TaskBuild* out, int* bad_input, uint64_t* launches);
+void free_tasks_device(TaskBuild* t, cudaStream_t s);
+
 struct UnionArgs {
   const uint32_t* tos;       // task-ordered successor ids
   const WarpTask* wtasks;
