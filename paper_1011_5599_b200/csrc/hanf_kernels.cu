@@ -468,8 +468,28 @@ __device__ __forceinline__ unsigned long long cta_count_sum(unsigned long long v
 __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs a) {
   __shared__ double sh[kFinishThreads];
   __shared__ unsigned long long shc[kFinishThreads];
+  __shared__ double tile[kFinishThreads * (64 + 1)];  // row = one block's 64 estimates
   __shared__ bool is_last;
-  const uint64_t b = static_cast<uint64_t>(blockIdx.x) * kFinishThreads + threadIdx.x;
+  const uint32_t t = threadIdx.x;
+  const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kFinishThreads;
+  const uint64_t b = b0 + t;
+  // stage the estimates of this CTA's dirty blocks with coalesced async
+  // copies (row k = block b0 + k, thread t copies column t of every row),
+  // so the sequential per-block sums below read shared memory only
+  if (a.est) {
+    for (uint32_t k = 0; k < kFinishThreads; ++k) {
+      const uint64_t bk = b0 + k;
+      if (bk >= a.blocks || bk < a.b0 || bk >= a.b1) continue;
+      if (a.bits[bk] == 0) continue;
+      const uint64_t e = bk * 64 + t;
+      if (e < a.n) {
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tile[k * 65 + t]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(a.est + e));
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
   double sum = 0.0;
   unsigned long long cnt = 0;
   if (b < a.blocks) {
@@ -478,17 +498,8 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
     if (a.est && word != 0 && b >= a.b0 && b < a.b1) {
       const uint64_t first = b * 64;
       const uint32_t last = a.n - first < 64 ? static_cast<uint32_t>(a.n - first) : 64u;
-      if (last == 64) {
-        const double2* p = reinterpret_cast<const double2*>(a.est + first);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const double2 q = p[k];
-          sum = __dadd_rn(sum, q.x);
-          sum = __dadd_rn(sum, q.y);
-        }
-      } else {
-        for (uint32_t i = 0; i < last; ++i) sum = __dadd_rn(sum, a.est[first + i]);
-      }
+      const double* row = tile + t * 65;
+      for (uint32_t i = 0; i < last; ++i) sum = __dadd_rn(sum, row[i]);  // engine.hpp:109-111
       a.block_sums[b] = sum;
     } else {
       sum = a.block_sums[b];
