@@ -230,13 +230,11 @@ __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) 
   for (uint32_t ch = 0; ch < args.chunks; ++ch) {
     const uint32_t woff = ch * NW;
     uint32_t acc[NL];
-    uint32_t own[NL];
     {
       G_t g;
       g.issue(cur, lead ? v : zero_row, words, woff);
-      g.extract(own, lead ? v : zero_row);
+      g.extract(acc, lead ? v : zero_row);
     }
-    sfor<0, NL>([&](auto I) { acc[decltype(I)::value] = own[decltype(I)::value]; });
     for (uint32_t i = 0; i < trips; i += U) {
       uint32_t w[U];
 #pragma unroll
@@ -264,6 +262,14 @@ __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) 
         store_chunk<Lay, kVec16>(args.partials + static_cast<uint64_t>(task.item) * words + woff,
                                  acc);
     } else {
+      // the old counter is re-read (L1/L2 hit) rather than kept live in
+      // registers across the loop
+      uint32_t own[NL];
+      {
+        G_t g;
+        g.issue(cur, lead ? v : zero_row, words, woff);
+        g.extract(own, lead ? v : zero_row);
+      }
       const bool changed = lead && limbs_differ<Lay>(acc, own);
       any_changed |= changed;
       if (changed || (lead && stale))
@@ -353,7 +359,10 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
           case 3: return union_launch<5, 64, 2, 2, false>(args, ch, s);
           case 5: return union_launch<5, 64, 2, 2, false, 6>(args, ch, s);
           case 6: return union_launch<5, 64, 4, 1, false, 5>(args, ch, s);
-          default: return union_launch<5, 64, 2, 1, false>(args, ch, s);
+          case 7: return union_launch<5, 64, 2, 1, false, 4>(args, ch, s);
+          case 10: return union_launch<5, 64, 2, 1, false>(args, ch, s);
+          case 9: return union_launch<5, 64, 2, 2, false, 4>(args, ch, s);
+          default: return union_launch<5, 64, 3, 1, false, 4>(args, ch, s);
         }
       return union_launch<5, 64, 4, 0, false>(args, ch, s);
     case 5128:
@@ -476,11 +485,13 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
   // stage the estimates of this CTA's dirty blocks with coalesced async
   // copies (row k = block b0 + k, thread t copies column t of every row),
   // so the sequential per-block sums below read shared memory only
+  __shared__ uint64_t dirty[kFinishThreads];
+  dirty[t] = (b < a.blocks && b >= a.b0 && b < a.b1) ? a.bits[b] : 0;
+  __syncthreads();
   if (a.est) {
     for (uint32_t k = 0; k < kFinishThreads; ++k) {
       const uint64_t bk = b0 + k;
-      if (bk >= a.blocks || bk < a.b0 || bk >= a.b1) continue;
-      if (a.bits[bk] == 0) continue;
+      if (dirty[k] == 0) continue;
       const uint64_t e = bk * 64 + t;
       if (e < a.n) {
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tile[k * 65 + t]));
