@@ -143,49 +143,95 @@ __device__ __forceinline__ void sub_chains(uint32_t (&d)[L], const uint32_t (&a)
 // with one 32x32->64 multiply by (2^r - 1) of the lane's low bit (the high
 // half carries straddling lanes into the next limb), replacing the
 // reference's second borrow chain; the select is one LOP3.
+//
+// The chunk is processed one borrow chain at a time (limbs [S, E) joined by
+// straddling registers).  At a chain end the next limb starts with a whole
+// register, so no lt bit needs to cross (funnel input 0) and the spread
+// carry is 0: chains are independent, which keeps the live temporaries to
+// one chain's worth.
+template <class Lay, int S>
+__device__ __forceinline__ void swar_chain(uint32_t (&x)[Lay::kLimbs],
+                                           const uint32_t (&y)[Lay::kLimbs]) {
+  constexpr int NL = Lay::kLimbs;
+  constexpr int R = Lay::kR;
+  if constexpr (S < NL) {
+    constexpr int E = Lay::chain_end(S);
+    uint32_t a[NL], b[NL], d[NL], lt[NL];
+    sfor<S, E>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      constexpr uint32_t H = Lay::high(i);
+      a[i] = x[i] | H;
+      b[i] = y[i] & ~H;
+    });
+    sub_chain<S, E - S>(d, a, b);
+    sfor<S, E>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      constexpr uint32_t H = Lay::high(i);
+      lt[i] = lop3<0x2B>(d[i], x[i], y[i]) & H;  // ((d | (x^y)) ^ (x | ~y)) & H
+    });
+    uint32_t carry = 0;
+    sfor<S, E>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      uint32_t u;
+      if constexpr (i + 1 < E)
+        u = __funnelshift_r(lt[i], lt[i + 1], R - 1);
+      else
+        u = lt[i] >> (R - 1);
+      const uint64_t w = static_cast<uint64_t>(u) * Lay::kMul;
+      const uint32_t spread = static_cast<uint32_t>(w) | carry;
+      carry = static_cast<uint32_t>(w >> 32);
+      x[i] = lop3<0xD8>(x[i], y[i], spread);  // (x & ~spread) | (y & spread)
+    });
+    swar_chain<Lay, E>(x, y);
+  }
+}
+
 template <class Lay>
 __device__ __forceinline__ void swar_max(uint32_t (&x)[Lay::kLimbs],
                                          const uint32_t (&y)[Lay::kLimbs]) {
-  constexpr int NL = Lay::kLimbs;
-  constexpr int R = Lay::kR;
-  uint32_t a[NL], b[NL], d[NL], lt[NL];
-  sfor<0, NL>([&](auto I) {
-    constexpr int i = decltype(I)::value;
-    constexpr uint32_t H = Lay::high(i);
-    a[i] = x[i] | H;
-    b[i] = y[i] & ~H;
-  });
-  sub_chains<Lay, 0>(d, a, b);
-  sfor<0, NL>([&](auto I) {
-    constexpr int i = decltype(I)::value;
-    constexpr uint32_t H = Lay::high(i);
-    lt[i] = ((d[i] | (x[i] ^ y[i])) ^ (x[i] | ~y[i])) & H;
-  });
-  uint32_t carry = 0;
-  sfor<0, NL>([&](auto I) {
-    constexpr int i = decltype(I)::value;
-    uint32_t u;
-    if constexpr (i + 1 < NL)
-      u = __funnelshift_r(lt[i], lt[i + 1], R - 1);
-    else
-      u = lt[i] >> (R - 1);
-    const uint64_t w = static_cast<uint64_t>(u) * Lay::kMul;
-    const uint32_t spread = static_cast<uint32_t>(w) | carry;
-    carry = static_cast<uint32_t>(w >> 32);
-    x[i] = lop3<0xD8>(x[i], y[i], spread);  // (x & ~spread) | (y & spread)
-  });
+  swar_chain<Lay, 0>(x, y);
+}
+
+// Counter loads with a cache policy: 0 = read-only path (L1 allocating, a
+// miss fills the whole 128-byte line), 1 = ld.cg (L2 only, sector
+// granular), 2 = ld.nc with L1::no_allocate.
+template <int kPol>
+__device__ __forceinline__ uint4 ld16(const uint4* p) {
+  uint4 v;
+  if constexpr (kPol == 0) {
+    v = __ldg(p);
+  } else if constexpr (kPol == 1) {
+    asm("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  } else {
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  }
+  return v;
+}
+template <int kPol>
+__device__ __forceinline__ uint2 ld8(const uint2* p) {
+  uint2 v;
+  if constexpr (kPol == 0) {
+    v = __ldg(p);
+  } else if constexpr (kPol == 1) {
+    asm("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  } else {
+    asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  }
+  return v;
 }
 
 // Loads one chunk (Lay::kWords u64 words at p) into limbs; padding limbs
 // beyond kLimbs are dropped (they are zero by the layout contract).
-template <class Lay, bool kVec16>
+template <class Lay, bool kVec16, int kPol = 0>
 __device__ __forceinline__ void load_chunk(uint32_t (&v)[Lay::kLimbs], const uint64_t* p) {
   constexpr int NW = Lay::kWords;
   constexpr int NL = Lay::kLimbs;
   if constexpr (kVec16 && NW % 2 == 0) {
     sfor<0, NW / 2>([&](auto I) {
       constexpr int k = decltype(I)::value;
-      const uint4 q = __ldg(reinterpret_cast<const uint4*>(p) + k);
+      const uint4 q = ld16<kPol>(reinterpret_cast<const uint4*>(p) + k);
       if constexpr (4 * k + 0 < NL) v[4 * k + 0] = q.x;
       if constexpr (4 * k + 1 < NL) v[4 * k + 1] = q.y;
       if constexpr (4 * k + 2 < NL) v[4 * k + 2] = q.z;
@@ -194,7 +240,7 @@ __device__ __forceinline__ void load_chunk(uint32_t (&v)[Lay::kLimbs], const uin
   } else {
     sfor<0, NW>([&](auto I) {
       constexpr int k = decltype(I)::value;
-      const uint2 q = __ldg(reinterpret_cast<const uint2*>(p) + k);
+      const uint2 q = ld8<kPol>(reinterpret_cast<const uint2*>(p) + k);
       if constexpr (2 * k + 0 < NL) v[2 * k + 0] = q.x;
       if constexpr (2 * k + 1 < NL) v[2 * k + 1] = q.y;
     });
@@ -430,14 +476,14 @@ struct Window128 {
   static constexpr int kLoads = (NW + 2) / 2;
 };
 
-template <int NW>
+template <int NW, int kPol = 0>
 __device__ __forceinline__ void window128_load(uint4 (&raw)[Window128<NW>::kLoads],
                                                const uint64_t* base, uint32_t w) {
   const uint64_t word = static_cast<uint64_t>(w) * NW;
   const uint4* p = reinterpret_cast<const uint4*>(base + (word & ~1ull));
   sfor<0, Window128<NW>::kLoads>([&](auto I) {
     constexpr int k = decltype(I)::value;
-    raw[k] = __ldg(p + k);
+    raw[k] = ld16<kPol>(p + k);
   });
 }
 

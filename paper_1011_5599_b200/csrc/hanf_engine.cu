@@ -524,6 +524,8 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
 
   HANF_TRY(cudaSetDevice(cfg.device));
   configure_pool(cfg.device);
+  if (const char* l2 = std::getenv("HANF_L2_FETCH"))
+    HANF_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::atoi(l2)));
   HANF_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   cudaStream_t s = e->stream;
   // row n is an all-zero counter (the union kernels' padding target); 8

@@ -109,6 +109,7 @@ __device__ __forceinline__ void zero_limbs(uint32_t (&x)[Lay::kLimbs]) {
   sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = 0u; });
 }
 
+// GMODE = gather kind + 10 * cache policy (ld16/ld8).
 template <class Lay, int GMODE, bool kVec16>
 struct Gather;
 
@@ -125,15 +126,45 @@ struct Gather<Lay, 0, kVec16> {
 };
 
 template <class Lay, bool kVec16>
-struct Gather<Lay, 1, kVec16> {
+struct Gather<Lay, 10, kVec16> {
+  uint32_t v[Lay::kLimbs];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
+                                        uint32_t woff) {
+    load_chunk<Lay, kVec16, 1>(v, cur + static_cast<uint64_t>(w) * words + woff);
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
+    sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = v[decltype(I)::value]; });
+  }
+};
+
+template <class Lay, bool kVec16>
+struct Gather<Lay, 20, kVec16> {
+  uint32_t v[Lay::kLimbs];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
+                                        uint32_t woff) {
+    load_chunk<Lay, kVec16, 2>(v, cur + static_cast<uint64_t>(w) * words + woff);
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
+    sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = v[decltype(I)::value]; });
+  }
+};
+
+template <class Lay, int POL>
+struct Gather128 {
   uint4 raw[Window128<Lay::kWords>::kLoads];
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t) {
-    window128_load<Lay::kWords>(raw, cur, w);
+    window128_load<Lay::kWords, POL>(raw, cur, w);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
     window128_extract<Lay, Lay::kWords>(x, raw, w);
   }
 };
+template <class Lay, bool kVec16>
+struct Gather<Lay, 1, kVec16> : Gather128<Lay, 0> {};
+template <class Lay, bool kVec16>
+struct Gather<Lay, 11, kVec16> : Gather128<Lay, 1> {};
+template <class Lay, bool kVec16>
+struct Gather<Lay, 21, kVec16> : Gather128<Lay, 2> {};
 
 template <class Lay, bool kVec16>
 struct Gather<Lay, 2, kVec16> {
@@ -348,6 +379,13 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
           case 0: return union_launch<5, 32, 4, 0, false>(args, ch, s);
           case 2: return union_launch<5, 32, 4, 2, false>(args, ch, s);
           case 3: return union_launch<5, 32, 2, 1, false>(args, ch, s);
+          case 7: return union_launch<5, 32, 4, 1, false, 4>(args, ch, s);
+          case 8: return union_launch<5, 32, 4, 0, false, 4>(args, ch, s);
+          case 9: return union_launch<5, 32, 8, 1, false, 3>(args, ch, s);
+          case 11: return union_launch<5, 32, 4, 11, false>(args, ch, s);
+          case 12: return union_launch<5, 32, 4, 21, false>(args, ch, s);
+          case 13: return union_launch<5, 32, 4, 10, false>(args, ch, s);
+          case 14: return union_launch<5, 32, 8, 11, false, 3>(args, ch, s);
           default: return union_launch<5, 32, 4, 1, false>(args, ch, s);
         }
       return union_launch<5, 32, 4, 0, false>(args, ch, s);
@@ -361,13 +399,23 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
           case 6: return union_launch<5, 64, 4, 1, false, 5>(args, ch, s);
           case 7: return union_launch<5, 64, 2, 1, false, 4>(args, ch, s);
           case 10: return union_launch<5, 64, 2, 1, false>(args, ch, s);
+          case 11: return union_launch<5, 64, 3, 11, false, 4>(args, ch, s);
+          case 12: return union_launch<5, 64, 3, 21, false, 4>(args, ch, s);
+          case 13: return union_launch<5, 64, 4, 10, false>(args, ch, s);
           case 9: return union_launch<5, 64, 2, 2, false, 4>(args, ch, s);
           default: return union_launch<5, 64, 3, 1, false, 4>(args, ch, s);
         }
       return union_launch<5, 64, 4, 0, false>(args, ch, s);
     case 5128:
-      if (variant == 2) return union_launch<5, 128, 2, 2, true>(args, ch, s);
-      return union_launch<5, 128, 2, 0, true>(args, ch, s);
+      switch (variant) {
+        case 2: return union_launch<5, 128, 2, 2, true>(args, ch, s);
+        case 7: return union_launch<5, 128, 2, 0, true, 3>(args, ch, s);
+        case 8: return union_launch<5, 128, 1, 0, true, 4>(args, ch, s);
+        case 9: return union_launch<5, 128, 1, 2, true, 4>(args, ch, s);
+        case 11: return union_launch<5, 128, 2, 10, true, 3>(args, ch, s);
+        case 12: return union_launch<5, 128, 2, 20, true, 3>(args, ch, s);
+        default: return union_launch<5, 128, 2, 0, true, 3>(args, ch, s);
+      }
     case 6016: return union_launch<6, 16, 4, 0, true>(args, ch, s);
     case 6032: return union_launch<6, 32, 4, 0, false>(args, ch, s);
     case 7016: return union_launch<7, 16, 4, 0, true>(args, ch, s);
