@@ -169,6 +169,9 @@ __device__ __forceinline__ void swar_chain(uint32_t (&x)[Lay::kLimbs],
       constexpr uint32_t H = Lay::high(i);
       lt[i] = lop3<0x2B>(d[i], x[i], y[i]) & H;  // ((d | (x^y)) ^ (x | ~y)) & H
     });
+    // spread_i = low(u_i * (2^r - 1)) | high(u_{i-1} * (2^r - 1)); the two
+    // never overlap, so the carry rides in as the addend of the 32x32+64
+    // multiply-add (one IMAD.WIDE per limb, no OR)
     uint32_t carry = 0;
     sfor<S, E>([&](auto I) {
       constexpr int i = decltype(I)::value;
@@ -177,8 +180,8 @@ __device__ __forceinline__ void swar_chain(uint32_t (&x)[Lay::kLimbs],
         u = __funnelshift_r(lt[i], lt[i + 1], R - 1);
       else
         u = lt[i] >> (R - 1);
-      const uint64_t w = static_cast<uint64_t>(u) * Lay::kMul;
-      const uint32_t spread = static_cast<uint32_t>(w) | carry;
+      const uint64_t w = static_cast<uint64_t>(u) * Lay::kMul + carry;
+      const uint32_t spread = static_cast<uint32_t>(w);
       carry = static_cast<uint32_t>(w >> 32);
       x[i] = lop3<0xD8>(x[i], y[i], spread);  // (x & ~spread) | (y & spread)
     });

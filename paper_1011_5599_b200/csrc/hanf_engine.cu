@@ -157,6 +157,17 @@ struct hanf_engine {
   double* log_table = nullptr;            // m + 1
   uint64_t* partials = nullptr;           // hub chunks * W
   hanf::TaskBuild tasks;
+  // shard CSR (kept for the worklist step) and its lazily built transpose
+  uint64_t* csr_off = nullptr;
+  uint32_t* csr_succ = nullptr;
+  uint64_t succ_base = 0;
+  unsigned long long* tr_off = nullptr;
+  uint32_t* tr_succ = nullptr;
+  uint64_t* sig = nullptr;
+  uint32_t* mod_list = nullptr;
+  uint32_t* work = nullptr;
+  unsigned int* lens = nullptr;
+  bool sparse_ok = false;     // layout supported and HANF_NO_SPARSE unset
   hanf::ReduceOut* reduce = nullptr;
   double* reduce_sums = nullptr;
   unsigned long long* reduce_counts = nullptr;
@@ -179,12 +190,13 @@ struct hanf_engine {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double union_ms = 0.0, estimate_ms = 0.0, reduce_ms = 0.0;
   uint64_t timed_steps = 0;
-  // CUDA graphs of the single-GPU step: [cur][check_mod][stale_valid]
+  // CUDA graphs of the single-GPU step: [cur][step_mode][stale_valid]
   struct StepGraph {
     cudaGraphExec_t exec = nullptr;
     uint64_t kernels = 0;
+    uint32_t uses = 0;  // captured on the second use (capture costs ~1 step)
   };
-  StepGraph graphs[2][2][2];
+  StepGraph graphs[2][3][2];
   bool use_graphs = true;
 
   ~hanf_engine() {
@@ -208,6 +220,14 @@ struct hanf_engine {
       pfree(reduce, stream);
       pfree(reduce_sums, stream);
       pfree(reduce_counts, stream);
+      pfree(csr_off, stream);
+      pfree(csr_succ, stream);
+      pfree(tr_off, stream);
+      pfree(tr_succ, stream);
+      pfree(sig, stream);
+      pfree(mod_list, stream);
+      pfree(work, stream);
+      pfree(lens, stream);
       hanf::free_tasks_device(&tasks, stream);
       cudaStreamSynchronize(stream);
       cudaStreamDestroy(stream);
@@ -325,11 +345,76 @@ hanf_status validate_config(const hanf_config* cfg) {
   return HANF_OK;
 }
 
+// Step kind for the current state: 0 dense sweep, 1 dense sweep skipping
+// unmodified successors, 2 worklist step (engine.hpp:210-224).  All three
+// produce the same bits; only the time differs.
+int step_mode(const hanf_engine* e) {
+  if (!e->cfg.track_modified || e->t == 0) return 0;
+  if (e->sparse_ok && e->stale_valid && 32 * e->last_count < e->n) return 2;
+  return 2 * e->last_count < e->n ? 1 : 0;
+}
+
+// Builds the transpose and worklist scratch on first use (outside any
+// graph capture).
+hanf_status ensure_sparse(hanf_engine* e) {
+  if (e->tr_off) return HANF_OK;
+  cudaStream_t s = e->stream;
+  HANF_CUDA(hanf::build_transpose_device(e->csr_off, e->csr_succ, e->lo, e->hi, e->succ_base, e->n,
+                                         s, &e->tr_off, &e->tr_succ, &e->launches));
+  HANF_CUDA(palloc(&e->sig, e->blocks, s));
+  HANF_CUDA(palloc(&e->mod_list, e->n, s));
+  HANF_CUDA(palloc(&e->work, e->hi - e->lo, s));
+  HANF_CUDA(palloc(&e->lens, 2, s));
+  HANF_CUDA(cudaStreamSynchronize(s));
+  return HANF_OK;
+}
+
+hanf_status compute_sparse(hanf_engine* e) {
+  const int g = e->cur, ng = 1 - e->cur;
+  const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
+  hanf::SparseArgs a{};
+  a.off = e->csr_off;
+  a.succ = e->csr_succ;
+  a.succ_base = e->succ_base;
+  a.node_base = e->lo;
+  a.cur = e->cnt[g];
+  a.next = e->cnt[ng];
+  a.mod_cur = e->mod[g];
+  a.mod_next = e->mod[ng];
+  a.est = e->est;
+  a.ep = hanf::EstimateParams{e->params.alpha, static_cast<double>(e->params.registers),
+                              e->params.registers, e->params.register_bits,
+                              e->params.words_per_counter, e->log_table};
+  a.words = e->params.words_per_counter;
+  a.tr_off = e->tr_off;
+  a.tr_succ = e->tr_succ;
+  a.sig = e->sig;
+  a.mod_list = e->mod_list;
+  a.work = e->work;
+  a.lens = e->lens;
+  a.n = e->n;
+  a.blocks = e->blocks;
+  a.hi = e->hi;
+  HANF_CUDA(hanf::launch_sparse_step(a, w0, w1, e->params.register_bits, e->params.registers,
+                                     e->stream, &e->launches));
+  return HANF_OK;
+}
+
 hanf_status compute_local(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
   HANF_CUDA(cudaMemsetAsync(e->mod[ng] + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
+  if (step_mode(e) == 2 && e->tr_off) {
+    const hanf_status st = compute_sparse(e);
+    if (st != HANF_OK) return st;
+    if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
+    if (e->lo != 0 || e->hi != e->n) {
+      hanf::FinishArgs f{e->est, e->mod[ng], e->block_sums, e->reduce, e->n, e->blocks, w0, w1};
+      HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
+    }
+    return HANF_OK;
+  }
   hanf::UnionArgs a{};
   a.tos = e->tasks.tos;
   a.wtasks = e->tasks.wtasks;
@@ -355,8 +440,7 @@ hanf_status compute_local(hanf_engine* e) {
   a.words = e->params.words_per_counter;
   // skipping unmodified successors costs a bitmap probe per arc and saves
   // a counter gather per skipped arc: worth it once most counters settled
-  a.check_mod = (e->cfg.track_modified && e->t > 0 &&
-                 2 * e->last_count < e->n) ? 1 : 0;
+  a.check_mod = step_mode(e) != 0 ? 1 : 0;
   a.stale_valid = e->stale_valid ? 1 : 0;
   HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers,
                                e->gather_mode, e->stream, &e->launches));
@@ -412,8 +496,17 @@ hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
 // One single-GPU step as a CUDA graph (memset + union + finish + read-back),
 // captured once per (generation parity, check_mod, stale_valid) and replayed.
 hanf_status step_graphed(hanf_engine* e, hanf_iteration_report* rep) {
-  const int check = (e->cfg.track_modified && e->t > 0 && 2 * e->last_count < e->n) ? 1 : 0;
-  hanf_engine::StepGraph& G = e->graphs[e->cur][check][e->stale_valid ? 1 : 0];
+  const int mode = step_mode(e);
+  if (mode == 2) {
+    const hanf_status st = ensure_sparse(e);
+    if (st != HANF_OK) return st;
+  }
+  hanf_engine::StepGraph& G = e->graphs[e->cur][mode][e->stale_valid ? 1 : 0];
+  if (!G.exec && ++G.uses < 2) {
+    hanf_status st = compute_local(e);
+    if (st != HANF_OK) return st;
+    return commit(e, rep);
+  }
   if (!G.exec) {
     const uint64_t before = e->launches;
     cudaGraph_t graph = nullptr;
@@ -509,6 +602,16 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
+  // The worklist step is opt-in (HANF_SPARSE=1): on the BASELINE R-MAT
+  // graphs the late iterations' changed counters are hubs whose predecessor
+  // sets cover most of the graph, and the dense sweep with skipping wins
+  // (profiles/r01_sparse.md).
+  e->sparse_ok = hanf::sparse_supported(params.register_bits, params.registers) &&
+                 hanf::fused_estimates(params.register_bits, params.registers);
+  {
+    const char* sp = std::getenv("HANF_SPARSE");
+    e->sparse_ok = e->sparse_ok && sp && std::atoi(sp) != 0;
+  }
 
   auto bail = [&](hanf_status s) {
     const std::string msg = g_last_error;
@@ -583,8 +686,9 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
     int bad = 0;
     const cudaError_t be =
         hanf::build_tasks_device(d_off, d_succ, lo, hi, a0, n, s, &e->tasks, &bad, &e->launches);
-    pfree(d_off, s);
-    pfree(d_succ, s);
+    e->csr_off = d_off;
+    e->csr_succ = d_succ;
+    e->succ_base = a0;
     if (be == cudaErrorInvalidValue)
       return bail(fail(HANF_INVALID_ARGUMENT, "too many nodes or tasks in one engine shard"));
     HANF_TRY(be);
@@ -629,6 +733,10 @@ hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
   HANF_CUDA(cudaSetDevice(e->device));
   // phase timing needs events between the kernels: run ungraphed then
   if (e->use_graphs && !e->timing) return step_graphed(e, rep);
+  if (step_mode(e) == 2) {
+    const hanf_status sst = ensure_sparse(e);
+    if (sst != HANF_OK) return sst;
+  }
   hanf_status st = compute_local(e);
   if (st != HANF_OK) return st;
   return commit(e, rep);
@@ -638,6 +746,10 @@ hanf_status hanf_shard_compute(hanf_engine* e) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
   if (e->n == 0) return HANF_OK;
   HANF_CUDA(cudaSetDevice(e->device));
+  if (step_mode(e) == 2) {
+    const hanf_status sst = ensure_sparse(e);
+    if (sst != HANF_OK) return sst;
+  }
   return compute_local(e);
 }
 

@@ -47,6 +47,36 @@ cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, ui
                                TaskBuild* out, int* bad_input, uint64_t* launches);
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
+// Worklist ("systolic") step, hanf_sparse.cu.
+struct SparseArgs {
+  const uint64_t* off;        // shard CSR offsets (index v - node_base)
+  const uint32_t* succ;       // shard CSR arcs (index arc - succ_base)
+  uint64_t succ_base;
+  uint64_t node_base;
+  const uint64_t* cur;
+  uint64_t* next;
+  const uint64_t* mod_cur;
+  uint64_t* mod_next;
+  double* est;
+  EstimateParams ep;
+  uint32_t words;
+  const unsigned long long* tr_off;  // transpose of the shard's arcs: preds of every node
+  const uint32_t* tr_succ;
+  uint64_t* sig;              // scratch bitmap (signalled nodes)
+  uint32_t* mod_list;         // scratch: modified nodes
+  uint32_t* work;             // scratch: worklist
+  unsigned int* lens;         // [0] modified, [1] worklist
+  const unsigned int* work_len;
+  uint64_t n, blocks, hi;
+};
+cudaError_t build_transpose_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
+                                   uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
+                                   unsigned long long** tr_off, uint32_t** tr_succ,
+                                   uint64_t* launches);
+cudaError_t launch_sparse_step(const SparseArgs& a, uint64_t w0, uint64_t w1, uint32_t register_bits,
+                               uint32_t registers, cudaStream_t s, uint64_t* launches);
+bool sparse_supported(uint32_t register_bits, uint32_t registers);
+
 struct UnionArgs {
   const uint32_t* tos;       // task-ordered successor ids
   const WarpTask* wtasks;

@@ -1,0 +1,234 @@
+// hanf_sparse.cu -- the worklist ("systolic") step, engine.hpp:210-224.
+//
+// Once few counters change per iteration, scanning every arc is wasted: a
+// counter can only grow if one of its successors changed in the previous
+// iteration.  The sparse step
+//   1. lists the counters that changed (the modified bitmap),
+//   2. signals their predecessors through the transpose (built once, on the
+//      device, from the shard's CSR; graph.hpp:72-84),
+//   3. forms the worklist = signalled nodes plus nodes whose next-generation
+//      slot is stale (changed last step), and
+//   4. recomputes only those, one warp per node, gathering only successors
+//      whose modified bit is set (engine.hpp:173).
+// The results are bit-identical to the dense sweep (skipping is exact, as
+// in the reference: test_engine.cpp:162-184).
+#include <cuda_runtime.h>
+
+#include <cub/device/device_scan.cuh>
+
+#include <cstdint>
+
+#include "hanf_device.cuh"
+#include "hanf_internal.h"
+
+namespace hanf {
+namespace {
+
+// ---- transpose (counting sort by destination; row order is irrelevant) ----
+__global__ void tr_count_kernel(const uint32_t* __restrict__ succ, uint64_t arcs,
+                                unsigned long long* __restrict__ count) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < arcs;
+       i += stride)
+    atomicAdd(count + succ[i], 1ull);
+}
+
+__global__ void tr_scatter_kernel(const uint64_t* __restrict__ off, uint64_t lo, uint64_t count,
+                                  const uint32_t* __restrict__ succ, uint64_t succ_base,
+                                  unsigned long long* __restrict__ cursor,
+                                  uint32_t* __restrict__ tr_succ) {
+  // one warp per source node
+  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+       i < count; i += warps) {
+    const uint64_t s = off[i], e = off[i + 1];
+    for (uint64_t k = s + lane; k < e; k += 32) {
+      const uint32_t w = succ[k - succ_base];
+      const unsigned long long pos = atomicAdd(cursor + w, 1ull);
+      tr_succ[pos] = static_cast<uint32_t>(lo + i);
+    }
+  }
+}
+
+// ---- worklist -------------------------------------------------------------
+// list of set bits of `bits` over words [w0, w1) (order unspecified)
+__global__ void bits_to_list_kernel(const uint64_t* __restrict__ bits, const uint64_t* __restrict__ extra,
+                                    uint64_t w0, uint64_t w1, uint64_t n,
+                                    uint32_t* __restrict__ list, unsigned int* __restrict__ len) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = w0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < w1;
+       w += stride) {
+    uint64_t word = bits[w] | (extra ? extra[w] : 0ull);
+    if (!word) continue;
+    const unsigned int c = __popcll(word);
+    unsigned int pos = atomicAdd(len, c);
+    while (word) {
+      const int b = __ffsll(static_cast<long long>(word)) - 1;
+      word &= word - 1;
+      const uint64_t v = (w << 6) + b;
+      if (v < n) list[pos++] = static_cast<uint32_t>(v);
+    }
+  }
+}
+
+// signalled[pred] = 1 for every predecessor (in this shard) of a listed node
+__global__ void signal_kernel(const uint32_t* __restrict__ list, const unsigned int* __restrict__ len,
+                              const unsigned long long* __restrict__ tr_off,
+                              const uint32_t* __restrict__ tr_succ, uint64_t* __restrict__ sig) {
+  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned int m = *len;
+  for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
+       i += warps) {
+    const uint32_t u = list[i];
+    const uint64_t s = tr_off[u], e = tr_off[u + 1];
+    for (uint64_t k = s + lane; k < e; k += 32) {
+      const uint32_t p = tr_succ[k];
+      atomicOr(reinterpret_cast<unsigned long long*>(sig) + (p >> 6), 1ull << (p & 63));
+    }
+  }
+}
+
+// ---- sparse union: one warp per worklist node -----------------------------
+template <int R, int NREG, bool kVec16>
+__global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
+  using Lay = Layout<R, NREG>;
+  constexpr int NL = Lay::kLimbs;
+  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned int m = *a.work_len;
+  const uint32_t words = a.words;
+  for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
+       i += warps) {
+    const uint32_t v = a.work[i];
+    const uint64_t s = a.off[v - a.node_base], e = a.off[v - a.node_base + 1];
+    uint32_t acc[NL];
+    if (lane == 0)
+      load_chunk<Lay, kVec16>(acc, a.cur + static_cast<uint64_t>(v) * words);
+    else
+      sfor<0, NL>([&](auto I) { acc[decltype(I)::value] = 0u; });
+    for (uint64_t k = s + lane; k < e; k += 32) {
+      const uint32_t w = a.succ[k - a.succ_base];
+      if ((__ldg(a.mod_cur + (w >> 6)) >> (w & 63)) & 1) {
+        uint32_t y[NL];
+        load_chunk<Lay, kVec16>(y, a.cur + static_cast<uint64_t>(w) * words);
+        swar_max<Lay>(acc, y);
+      }
+    }
+    for (uint32_t off = 16; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
+    if (lane == 0) {
+      uint32_t own[NL];
+      load_chunk<Lay, kVec16>(own, a.cur + static_cast<uint64_t>(v) * words);
+      const bool changed = limbs_differ<Lay>(acc, own);
+      const bool stale = (a.mod_cur[v >> 6] >> (v & 63)) & 1;
+      if (changed || stale) store_chunk<Lay, kVec16>(a.next + static_cast<uint64_t>(v) * words, acc);
+      if (changed) {
+        a.est[v] = estimate_limbs<Lay>(acc, a.ep);
+        atomicOr(reinterpret_cast<unsigned long long*>(a.mod_next) + (v >> 6), 1ull << (v & 63));
+      }
+    }
+  }
+}
+
+template <int R, int NREG, bool V>
+cudaError_t sparse_launch(const SparseArgs& a, uint32_t blocks, cudaStream_t s) {
+  sparse_union_kernel<R, NREG, V><<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t build_transpose_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
+                                   uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
+                                   unsigned long long** tr_off, uint32_t** tr_succ,
+                                   uint64_t* launches) {
+  const uint64_t count = hi - lo;
+  uint64_t arcs = 0;
+  if (count) {
+    uint64_t first = 0, last = 0;
+    cudaError_t e = cudaMemcpyAsync(&first, d_off, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&last, d_off + count, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    arcs = last - first;
+  }
+  unsigned long long* cnt = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&cnt), sizeof(unsigned long long) * (n + 1), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMallocAsync(reinterpret_cast<void**>(tr_off), sizeof(unsigned long long) * (n + 1), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMallocAsync(reinterpret_cast<void**>(tr_succ), sizeof(uint32_t) * (arcs ? arcs : 1), s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (n + 1), s);
+  if (arcs) {
+    const uint32_t blocks = 148 * 16;
+    tr_count_kernel<<<blocks, 256, 0, s>>>(d_succ, arcs, cnt);
+    ++*launches;
+  }
+  size_t tb = 0;
+  e = cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, *tr_off, static_cast<int64_t>(n + 1), s);
+  if (e != cudaSuccess) return e;
+  void* temp = nullptr;
+  e = cudaMallocAsync(&temp, tb ? tb : 1, s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(temp, tb, cnt, *tr_off, static_cast<int64_t>(n + 1), s);
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  cudaFreeAsync(temp, s);
+  // cursor = tr_off (copy), then scatter
+  e = cudaMemcpyAsync(cnt, *tr_off, sizeof(unsigned long long) * (n + 1), cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return e;
+  if (arcs) {
+    tr_scatter_kernel<<<148 * 16, 256, 0, s>>>(d_off, lo, count, d_succ, succ_base, cnt, *tr_succ);
+    ++*launches;
+  }
+  cudaFreeAsync(cnt, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sparse_step(const SparseArgs& a, uint64_t w0, uint64_t w1, uint32_t register_bits,
+                               uint32_t registers, cudaStream_t s, uint64_t* launches) {
+  const uint32_t blocks = 148 * 8;
+  // modified list (whole bitmap: successors anywhere signal this shard)
+  cudaError_t e = cudaMemsetAsync(a.lens, 0, 2 * sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  bits_to_list_kernel<<<blocks, 256, 0, s>>>(a.mod_cur, nullptr, 0, a.blocks, a.n, a.mod_list,
+                                            a.lens);
+  ++*launches;
+  e = cudaMemsetAsync(a.sig + w0, 0, sizeof(uint64_t) * (w1 - w0), s);
+  if (e != cudaSuccess) return e;
+  signal_kernel<<<blocks, 256, 0, s>>>(a.mod_list, a.lens, a.tr_off, a.tr_succ, a.sig);
+  ++*launches;
+  // worklist = signalled | stale, restricted to this shard
+  bits_to_list_kernel<<<blocks, 256, 0, s>>>(a.sig, a.mod_cur, w0, w1, a.hi, a.work, a.lens + 1);
+  ++*launches;
+  SparseArgs b = a;
+  b.work_len = a.lens + 1;
+  ++*launches;
+  switch (register_bits * 1000 + registers) {
+    case 5032: return sparse_launch<5, 32, false>(b, blocks, s);
+    case 5064: return sparse_launch<5, 64, false>(b, blocks, s);
+    case 5128: return sparse_launch<5, 128, true>(b, blocks, s);
+    case 5016: return sparse_launch<5, 16, true>(b, blocks, s);
+    case 6016: return sparse_launch<6, 16, true>(b, blocks, s);
+    case 6032: return sparse_launch<6, 32, false>(b, blocks, s);
+    case 7016: return sparse_launch<7, 16, true>(b, blocks, s);
+    case 7032: return sparse_launch<7, 32, true>(b, blocks, s);
+    case 7064: return sparse_launch<7, 64, false>(b, blocks, s);
+    case 8016: return sparse_launch<8, 16, true>(b, blocks, s);
+    default: return cudaErrorInvalidValue;  // multi-chunk layouts use the dense sweep
+  }
+}
+
+bool sparse_supported(uint32_t register_bits, uint32_t registers) {
+  switch (register_bits * 1000 + registers) {
+    case 5032: case 5064: case 5128: case 5016: case 6016: case 6032:
+    case 7016: case 7032: case 7064: case 8016:
+      return true;
+    default:
+      return false;
+  }
+}
+
+}  // namespace hanf

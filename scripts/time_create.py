@@ -20,3 +20,12 @@ for ex in (True, False):
         print(f"  step {t+1}: {1e3*(t1-t0):.3f} ms modified {r.modified}")
         if r.modified == 0: break
     e.close()
+print("--- second engine, ungraphed")
+os.environ["HANF_NO_GRAPHS"] = "1"
+for rep in range(2):
+    e = h.NfEngine(pg, h.EngineConfig(bucket_bits=6, seed=42, exact_sum=False))
+    for t in range(9):
+        t0 = time.perf_counter(); r = e.step(); t1 = time.perf_counter()
+        print(f"  step {t+1}: {1e3*(t1-t0):.3f} ms modified {r.modified}")
+        if r.modified == 0: break
+    e.close()

@@ -351,3 +351,14 @@ def test_launch_accounting(hanf):
         before = e.launch_count()
         e.step()
         assert e.launch_count() - before >= 2  # union sweep + finish
+
+
+def test_worklist_step_parity(hanf, port, monkeypatch):
+    """The opt-in worklist step (HANF_SPARSE=1, engine.hpp:210-224 systolic
+    mode) changes time only: lockstep bit-exact with the oracle."""
+    monkeypatch.setenv("HANF_SPARSE", "1")
+    for g in (hanf.gen_rmat(12, 16, 0.57, 0.19, 0.19, 2, 3),
+              hanf.Graph.from_edges(300, [(v, v + 1) for v in range(299)]),
+              hanf.gen_clique_path(30, 40)):
+        for b in (5, 6, 7):
+            lockstep(hanf, port, g, bucket_bits=b, seed=9)
