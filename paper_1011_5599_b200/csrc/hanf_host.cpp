@@ -132,17 +132,27 @@ hanf_status build_csr(uint64_t n, const uint32_t* src, const uint32_t* dst, uint
   if (!g) return fail(HANF_OUT_OF_MEMORY, "graph allocation failed");
   try {
     g->n = n;
+    // counting sort by source, parallel: atomic row counts, prefix sum,
+    // atomic row cursors (the order inside a row does not matter, rows are
+    // sorted next)
     std::vector<uint64_t> deg(n + 1, 0);
-    // histogram (serial over a shared array is fine at these sizes; the
-    // scatter below dominates)
-    for (uint64_t i = 0; i < count; ++i)
-      if (!(drop_self_loops && src[i] == dst[i])) ++deg[src[i] + 1];
+    parallel_for(count, [&](uint64_t b, uint64_t e) {
+      for (uint64_t i = b; i < e; ++i)
+        if (!(drop_self_loops && src[i] == dst[i]))
+          std::atomic_ref<uint64_t>(deg[src[i] + 1]).fetch_add(1, std::memory_order_relaxed);
+    });
     for (uint64_t v = 0; v < n; ++v) deg[v + 1] += deg[v];
     std::vector<uint32_t> tmp(deg[n]);
     {
       std::vector<uint64_t> cursor(deg.begin(), deg.end() - 1);
-      for (uint64_t i = 0; i < count; ++i)
-        if (!(drop_self_loops && src[i] == dst[i])) tmp[cursor[src[i]]++] = dst[i];
+      parallel_for(count, [&](uint64_t b, uint64_t e) {
+        for (uint64_t i = b; i < e; ++i)
+          if (!(drop_self_loops && src[i] == dst[i])) {
+            const uint64_t pos =
+                std::atomic_ref<uint64_t>(cursor[src[i]]).fetch_add(1, std::memory_order_relaxed);
+            tmp[pos] = dst[i];
+          }
+      });
     }
     // sort + unique each row, compute new degrees
     std::vector<uint64_t> newdeg(n + 1, 0);
