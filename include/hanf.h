@@ -163,12 +163,13 @@ hanf_status hanf_timing(const hanf_engine* engine, double* union_ms,
                         double* estimate_ms, double* reduce_ms, uint64_t* steps);
 /* Device buffers of the engine, for collectives over the node shards. */
 typedef struct {
-  void* next_counters;     /* u64[n*W]: the generation being written by step */
+  void* next_counters;     /* u64[n*row_pitch]: the generation being written by step */
   void* next_modified;     /* u64[ceil(n/64)] bitmap of counters changed by step */
   void* block_sums;        /* f64[ceil(n/64)] per-64-counter estimate sums */
   uint64_t words_per_counter;
   uint64_t blocks;         /* ceil(n/64) */
   uint64_t shard_begin, shard_end; /* node range updated by this engine */
+  uint64_t row_pitch;      /* u64 words between consecutive counters (>= W) */
 } hanf_buffers;
 hanf_status hanf_device_buffers(hanf_engine* engine, hanf_buffers* out);
 /* Sharded step, phase 1: compute this engine's node range into the next

@@ -45,7 +45,7 @@ class BuffersC(Structure):
     _fields_ = [("next_counters", c_void_p), ("next_modified", c_void_p),
                 ("block_sums", c_void_p), ("words_per_counter", c_uint64),
                 ("blocks", c_uint64), ("shard_begin", c_uint64),
-                ("shard_end", c_uint64)]
+                ("shard_end", c_uint64), ("row_pitch", c_uint64)]
 
 
 # status codes (hanf.h)

@@ -147,15 +147,16 @@ struct hanf_engine {
   uint64_t lo = 0, hi = 0;   // node shard [lo, hi)
   uint64_t blocks = 0;       // ceil(n / 64)
   uint64_t words = 0;        // W
+  uint64_t pitch = 0;        // row pitch in words (hanf::row_pitch)
   int device = 0;
   cudaStream_t stream = nullptr;
 
-  uint64_t* cnt[2] = {nullptr, nullptr};  // (n + 1) * W words + 8 (window loads)
+  uint64_t* cnt[2] = {nullptr, nullptr};  // (n + 1) * pitch words + 8 (window loads)
   uint64_t* mod[2] = {nullptr, nullptr};  // blocks words
   double* est = nullptr;                  // n
   double* block_sums = nullptr;           // blocks
   double* log_table = nullptr;            // m + 1
-  uint64_t* partials = nullptr;           // hub chunks * W
+  uint64_t* partials = nullptr;           // hub chunks * pitch
   hanf::TaskBuild tasks;
   // shard CSR (kept for the worklist step) and its lazily built transpose
   uint64_t* csr_off = nullptr;
@@ -254,7 +255,7 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
   a.m = static_cast<double>(e->params.registers);
   a.registers = e->params.registers;
   a.register_bits = e->params.register_bits;
-  a.words = e->params.words_per_counter;
+  a.pitch = static_cast<uint32_t>(e->pitch);
   a.log_table = e->log_table;
   HANF_CUDA(hanf::launch_estimate(a, e->stream, &e->launches));
   return HANF_OK;
@@ -325,7 +326,8 @@ hanf_status seed_all(hanf_engine* e) {
   e->systolic = false;
   HANF_CUDA(hanf::launch_seed(e->cnt[0], e->cnt[1], e->mod[0], e->n, 0, e->n,
                               e->params.bucket_bits, e->params.register_bits,
-                              e->params.words_per_counter, e->params.seed, e->stream,
+                              e->params.words_per_counter, static_cast<uint32_t>(e->pitch),
+                              e->params.seed, e->stream,
                               &e->launches));
   HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
@@ -385,7 +387,7 @@ hanf_status compute_sparse(hanf_engine* e) {
   a.ep = hanf::EstimateParams{e->params.alpha, static_cast<double>(e->params.registers),
                               e->params.registers, e->params.register_bits,
                               e->params.words_per_counter, e->log_table};
-  a.words = e->params.words_per_counter;
+  a.pitch = static_cast<uint32_t>(e->pitch);
   a.tr_off = e->tr_off;
   a.tr_succ = e->tr_succ;
   a.sig = e->sig;
@@ -437,7 +439,7 @@ hanf_status compute_local(hanf_engine* e) {
   a.hub_first = e->tasks.hub_first;
   a.hub_count = e->tasks.hub_count;
   a.hub_ticket = e->tasks.hub_ticket;
-  a.words = e->params.words_per_counter;
+  a.pitch = static_cast<uint32_t>(e->pitch);
   // skipping unmodified successors costs a bitmap probe per arc and saves
   // a counter gather per skipped arc: worth it once most counters settled
   a.check_mod = step_mode(e) != 0 ? 1 : 0;
@@ -599,6 +601,7 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   e->hi = hi;
   e->blocks = (n + 63) / 64;
   e->words = params.words_per_counter;
+  e->pitch = hanf::row_pitch(params.register_bits, params.registers, params.words_per_counter);
   if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
@@ -633,11 +636,11 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   cudaStream_t s = e->stream;
   // row n is an all-zero counter (the union kernels' padding target); 8
   // extra words keep the 256-bit window loads of the last rows in bounds
-  const uint64_t nw = (n + 1) * e->words + 8;
+  const uint64_t nw = (n + 1) * e->pitch + 8;
   HANF_TRY(palloc(&e->cnt[0], nw, s));
   HANF_TRY(palloc(&e->cnt[1], nw, s));
-  HANF_TRY(cudaMemsetAsync(e->cnt[0] + n * e->words, 0, sizeof(uint64_t) * (e->words + 8), s));
-  HANF_TRY(cudaMemsetAsync(e->cnt[1] + n * e->words, 0, sizeof(uint64_t) * (e->words + 8), s));
+  HANF_TRY(cudaMemsetAsync(e->cnt[0] + n * e->pitch, 0, sizeof(uint64_t) * (e->pitch + 8), s));
+  HANF_TRY(cudaMemsetAsync(e->cnt[1] + n * e->pitch, 0, sizeof(uint64_t) * (e->pitch + 8), s));
   HANF_TRY(palloc(&e->mod[0], e->blocks, s));
   HANF_TRY(palloc(&e->mod[1], e->blocks, s));
   HANF_TRY(palloc(&e->est, n, s));
@@ -695,7 +698,7 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
     if (bad)
       return bail(fail(HANF_INVALID_ARGUMENT,
                        "arc endpoint out of range or offsets not non-decreasing"));
-    HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->words, s));
+    HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
     st = seed_all(e);
     if (st != HANF_OK) return bail(st);
   }
@@ -845,9 +848,11 @@ hanf_status hanf_read_counters(hanf_engine* e, uint64_t first, uint64_t count, u
   if (count == 0) return HANF_OK;
   if (!dst) return fail(HANF_INVALID_ARGUMENT, "null destination");
   HANF_CUDA(cudaSetDevice(e->device));
-  HANF_CUDA(cudaMemcpyAsync(dst, e->cnt[e->cur] + first * e->words,
-                            sizeof(uint64_t) * count * e->words, cudaMemcpyDeviceToHost,
-                            e->stream));
+  // rows are `pitch` words apart on the device, W apart in the reference
+  // packing the caller expects
+  HANF_CUDA(cudaMemcpy2DAsync(dst, sizeof(uint64_t) * e->words, e->cnt[e->cur] + first * e->pitch,
+                              sizeof(uint64_t) * e->pitch, sizeof(uint64_t) * e->words, count,
+                              cudaMemcpyDeviceToHost, e->stream));
   HANF_CUDA(cudaStreamSynchronize(e->stream));
   return HANF_OK;
 }
@@ -916,6 +921,7 @@ hanf_status hanf_device_buffers(hanf_engine* e, hanf_buffers* out) {
   out->next_modified = e->mod[ng];
   out->block_sums = e->block_sums;
   out->words_per_counter = e->words;
+  out->row_pitch = e->pitch;
   out->blocks = e->blocks;
   out->shard_begin = e->lo;
   out->shard_end = e->hi;

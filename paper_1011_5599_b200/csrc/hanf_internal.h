@@ -59,7 +59,7 @@ struct SparseArgs {
   uint64_t* mod_next;
   double* est;
   EstimateParams ep;
-  uint32_t words;
+  uint32_t pitch;             // row pitch (u64 words between counters)
   const unsigned long long* tr_off;  // transpose of the shard's arcs: preds of every node
   const uint32_t* tr_succ;
   uint64_t* sig;              // scratch bitmap (signalled nodes)
@@ -87,13 +87,13 @@ struct UnionArgs {
   uint64_t* mod_next;        // bitmap: counters changed by this step (pre-zeroed)
   const uint32_t* order;     // node ids of light tasks
   const uint32_t* hub_node;  // per hub chunk: node
-  uint64_t* partials;        // per hub chunk: partial counter (W words)
+  uint64_t* partials;        // per hub chunk: partial counter (pitch words)
   const uint32_t* chunk_hub; // per hub chunk: hub index
   const uint32_t* hub_nodes; // per hub: node, first chunk, chunk count
   const uint32_t* hub_first;
   const uint32_t* hub_count;
   uint32_t* hub_ticket;      // per hub: chunks finished this step (self-resetting)
-  uint32_t words;            // W
+  uint32_t pitch;            // row pitch in u64 words (>= W, see row_pitch)
   uint32_t chunks;           // chunks per counter
   uint32_t zero_row;         // index of the all-zero counter row (= n)
   int32_t check_mod;         // skip successors whose bit is clear in mod_cur
@@ -115,14 +115,14 @@ struct EstimateArgs {
   double m;
   uint32_t registers;
   uint32_t register_bits;
-  uint32_t words;
+  uint32_t pitch;            // row pitch in u64 words
   const double* log_table;
 };
 
 // Launchers (hanf_kernels.cu).  All are stream-ordered and asynchronous.
 cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
-                        uint32_t register_bits, uint32_t words, uint64_t seed,
+                        uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
                         cudaStream_t s, uint64_t* launches);
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits,
                          uint32_t registers, int variant, cudaStream_t s,
@@ -130,6 +130,14 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits,
 cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* launches);
 // true when the union kernels compute estimates themselves (single-chunk layouts)
 bool fused_estimates(uint32_t register_bits, uint32_t registers);
+// Row pitch of the counter arrays.  W = 3 rows are padded to 4 words: every
+// counter is then one aligned 32-byte sector read by one 256-bit load
+// (unpadded, half of them straddle two sectors); measured +5% on the
+// DRAM-bound BA graph.  Padding W = 5 or 10 to 8 or 12 cuts load
+// instructions but not L1 wavefronts (a scattered 256-bit load costs two)
+// and grows the L2 footprint: measured 4-7% slower, so those keep pitch W
+// (profiles/r01_row_pitch.md).
+uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words);
 
 // Step epilogue (block sums + totals), see finish_kernel.
 constexpr int kFinishThreads = 64;

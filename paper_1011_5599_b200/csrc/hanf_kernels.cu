@@ -11,8 +11,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "hanf_device.cuh"
+
 #include "hanf_internal.h"
 
 namespace hanf {
@@ -32,7 +34,7 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // hash.hpp:8-
 __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
                             uint64_t* __restrict__ mod, uint64_t n, uint64_t node_begin,
                             uint64_t node_end, uint32_t bucket_bits, uint32_t register_bits,
-                            uint32_t words, uint64_t seed_mix) {
+                            uint32_t words, uint32_t pitch, uint64_t seed_mix) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = node_begin + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
        v < node_end; v += stride) {
@@ -45,9 +47,9 @@ __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
     const uint64_t bit = static_cast<uint64_t>(bucket) * register_bits;
     const uint64_t wi = bit >> 6;
     const uint32_t off = bit & 63;
-    uint64_t* ca = a + v * words;
-    uint64_t* cb = b + v * words;
-    for (uint32_t k = 0; k < words; ++k) {
+    uint64_t* ca = a + v * pitch;
+    uint64_t* cb = b + v * pitch;
+    for (uint32_t k = 0; k < pitch; ++k) {  // padding words beyond W stay 0
       uint64_t word = 0;
       if (k == wi) word |= static_cast<uint64_t>(rho) << off;
       if (k == wi + 1 && off + register_bits > 64) word |= static_cast<uint64_t>(rho) >> (64 - off);
@@ -69,7 +71,7 @@ __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
 
 cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
-                        uint32_t register_bits, uint32_t words, uint64_t seed,
+                        uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
                         cudaStream_t s, uint64_t* launches) {
   if (node_end <= node_begin) return cudaSuccess;
   const uint64_t items = node_end - node_begin;
@@ -77,7 +79,7 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
   uint64_t blocks = (items + threads - 1) / threads;
   if (blocks > 148ull * 64) blocks = 148ull * 64;
   seed_kernel<<<static_cast<uint32_t>(blocks), threads, 0, s>>>(
-      a, b, mod, n, node_begin, node_end, bucket_bits, register_bits, words,
+      a, b, mod, n, node_begin, node_end, bucket_bits, register_bits, words, pitch,
       mix64(seed ^ 0x9e3779b97f4a7c15ULL));
   ++*launches;
   return cudaGetLastError();
@@ -177,6 +179,25 @@ struct Gather<Lay, 2, kVec16> {
   }
 };
 
+// GMODE 3: rows padded to a multiple of 4 words (row_pitch): counter w
+// starts a 32-byte block, ceil(W/4) aligned 256-bit loads, no shifts.
+template <class Lay, bool kVec16>
+struct Gather<Lay, 3, kVec16> {
+  static constexpr int K = (Lay::kWords + 3) / 4;
+  uint32_t raw[K][8];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t pitch,
+                                        uint32_t woff) {
+    const uint64_t* p = cur + static_cast<uint64_t>(w) * pitch + woff;
+    sfor<0, K>([&](auto I) { ldg256(raw[decltype(I)::value], p + 4 * decltype(I)::value); });
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
+    sfor<0, Lay::kLimbs>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      x[i] = raw[i / 8][i % 8];
+    });
+  }
+};
+
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -193,7 +214,7 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
   const uint32_t v = args.hub_nodes[h];
   const uint32_t first = args.hub_first[h];
   const uint32_t count = args.hub_count[h];
-  const uint32_t words = args.words;
+  const uint32_t words = args.pitch;
   bool stale = false;
   if (args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
   bool any_changed = false;
@@ -225,7 +246,7 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
              1ull << (v & 63));
 }
 
-template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1>
+template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1, bool PF = false>
 __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) {
   using Lay = Layout<R, NREG>;
   constexpr int NL = Lay::kLimbs;
@@ -254,7 +275,7 @@ __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) 
   if (lead && args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
   const uint64_t* __restrict__ cur = args.cur;
   const uint32_t* __restrict__ ids = args.tos + task.tos + lane;
-  const uint32_t words = args.words;
+  const uint32_t words = args.pitch;
   const uint32_t trips = task.trips;
 
   bool any_changed = false;
@@ -266,11 +287,26 @@ __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) 
       g.issue(cur, lead ? v : zero_row, words, woff);
       g.extract(acc, lead ? v : zero_row);
     }
+    // PF: the ids of trip group i+U are requested before group i's gathers
+    // so the id load latency overlaps the gathers instead of preceding them.
+    uint32_t wn[U];
+    if (PF) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) wn[j] = (j < trips) ? ld_stream_u32(ids + 32 * j) : zero_row;
+    }
     for (uint32_t i = 0; i < trips; i += U) {
       uint32_t w[U];
+      if (PF) {
 #pragma unroll
-      for (int j = 0; j < U; ++j)
-        w[j] = (i + j < trips) ? ld_stream_u32(ids + 32 * (i + j)) : zero_row;
+        for (int j = 0; j < U; ++j) {
+          w[j] = wn[j];
+          wn[j] = (i + U + j < trips) ? ld_stream_u32(ids + 32 * (i + U + j)) : zero_row;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          w[j] = (i + j < trips) ? ld_stream_u32(ids + 32 * (i + j)) : zero_row;
+      }
       if (args.check_mod) {
 #pragma unroll
         for (int j = 0; j < U; ++j)
@@ -347,13 +383,13 @@ KernelChoice choose(uint32_t r, uint32_t m) {
   }
 }
 
-template <int R, int NREG, int U, int GM, bool V, int MINB = 1>
+template <int R, int NREG, int U, int GM, bool V, int MINB = 1, bool PF = false>
 cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   a.chunks = chunks;
   if (chunks != 1) a.est = nullptr;  // estimates need the whole counter in registers
   if (a.num_wtasks == 0) return cudaSuccess;
   const uint32_t blocks = (a.num_wtasks + 7) / 8;
-  union_kernel<R, NREG, U, GM, V, MINB><<<blocks, 256, 0, s>>>(a);
+  union_kernel<R, NREG, U, GM, V, MINB, PF><<<blocks, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -361,6 +397,15 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
 
 bool fused_estimates(uint32_t register_bits, uint32_t registers) {
   return choose(register_bits, registers).chunks == 1;
+}
+
+uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words) {
+  if (choose(register_bits, registers).chunks != 1) return words;
+  if (const char* env = std::getenv("HANF_PITCH")) {
+    if (env[0] == '0') return words;
+    if (env[0] == '1') return (words + 3) & ~3u;  // experiments: pad every layout
+  }
+  return words == 3 ? 4 : words;
 }
 
 // variant < 0 picks the measured best gather for the layout (profiles/);
@@ -372,6 +417,26 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
   ++*launches;
   const uint32_t ch = static_cast<uint32_t>(k.chunks);
   const bool single = ch == 1;
+  if (single && args.pitch % 4 == 0) switch (k.r * 1000 + k.nreg) {
+      case 5032:
+        if (variant == 30) return union_launch<5, 32, 4, 3, false, 4, true>(args, ch, s);
+        return union_launch<5, 32, 4, 3, false, 1, true>(args, ch, s);
+      case 5064:
+        switch (variant) {
+          case 30: return union_launch<5, 64, 2, 3, false, 4, true>(args, ch, s);
+          case 31: return union_launch<5, 64, 4, 3, false, 3, true>(args, ch, s);
+          case 32: return union_launch<5, 64, 3, 3, false, 3, true>(args, ch, s);
+          case 33: return union_launch<5, 64, 3, 3, false, 4, false>(args, ch, s);
+          default: return union_launch<5, 64, 3, 3, false, 4, true>(args, ch, s);
+        }
+      case 5128:
+        if (variant == 30) return union_launch<5, 128, 1, 3, false, 4, true>(args, ch, s);
+        return union_launch<5, 128, 2, 3, false, 3, true>(args, ch, s);
+      case 6032: return union_launch<6, 32, 4, 3, false, 1, true>(args, ch, s);
+      case 7032: return union_launch<7, 32, 4, 3, false, 1, true>(args, ch, s);
+      case 7064: return union_launch<7, 64, 2, 3, false, 1, true>(args, ch, s);
+      default: break;
+    }
   switch (k.r * 1000 + k.nreg) {
     case 5016: return union_launch<5, 16, 4, 0, true>(args, ch, s);
     case 5032:
@@ -386,7 +451,8 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
           case 12: return union_launch<5, 32, 4, 21, false>(args, ch, s);
           case 13: return union_launch<5, 32, 4, 10, false>(args, ch, s);
           case 14: return union_launch<5, 32, 8, 11, false, 3>(args, ch, s);
-          default: return union_launch<5, 32, 4, 1, false>(args, ch, s);
+          case 20: return union_launch<5, 32, 4, 1, false, 1, true>(args, ch, s);
+          default: return union_launch<5, 32, 4, 1, false, 1, true>(args, ch, s);
         }
       return union_launch<5, 32, 4, 0, false>(args, ch, s);
     case 5064:
@@ -403,7 +469,10 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
           case 12: return union_launch<5, 64, 3, 21, false, 4>(args, ch, s);
           case 13: return union_launch<5, 64, 4, 10, false>(args, ch, s);
           case 9: return union_launch<5, 64, 2, 2, false, 4>(args, ch, s);
-          default: return union_launch<5, 64, 3, 1, false, 4>(args, ch, s);
+          case 20: return union_launch<5, 64, 3, 1, false, 4, true>(args, ch, s);
+          case 21: return union_launch<5, 64, 2, 1, false, 4, true>(args, ch, s);
+          case 22: return union_launch<5, 64, 3, 1, false, 4>(args, ch, s);
+          default: return union_launch<5, 64, 3, 1, false, 4, true>(args, ch, s);
         }
       return union_launch<5, 64, 4, 0, false>(args, ch, s);
     case 5128:
@@ -414,7 +483,9 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
         case 9: return union_launch<5, 128, 1, 2, true, 4>(args, ch, s);
         case 11: return union_launch<5, 128, 2, 10, true, 3>(args, ch, s);
         case 12: return union_launch<5, 128, 2, 20, true, 3>(args, ch, s);
-        default: return union_launch<5, 128, 2, 0, true, 3>(args, ch, s);
+        case 20: return union_launch<5, 128, 2, 0, true, 3, true>(args, ch, s);
+        case 22: return union_launch<5, 128, 2, 0, true, 3>(args, ch, s);
+        default: return union_launch<5, 128, 2, 0, true, 3, true>(args, ch, s);
       }
     case 6016: return union_launch<6, 16, 4, 0, true>(args, ch, s);
     case 6032: return union_launch<6, 32, 4, 0, false>(args, ch, s);
@@ -441,15 +512,15 @@ __global__ void __launch_bounds__(64) estimate_kernel(const EstimateArgs args) {
   if (word == 0) return;
   const uint32_t t = threadIdx.x;
   const uint64_t v = blk * 64 + t;
-  EstimateParams p{args.alpha, args.m, args.registers, args.register_bits, args.words,
+  EstimateParams p{args.alpha, args.m, args.registers, args.register_bits, args.pitch,
                    args.log_table};
   double e = 0.0;
   if (v < args.n) {
     if ((word >> t) & 1) {
       if constexpr (M > 0)
-        e = estimate_counter_r5<M>(args.counters + v * args.words, p);
+        e = estimate_counter_r5<M>(args.counters + v * args.pitch, p);
       else
-        e = estimate_counter_generic(args.counters + v * args.words, p);
+        e = estimate_counter_generic(args.counters + v * args.pitch, p);
       args.est[v] = e;
     } else {
       e = args.est[v];

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
   const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const unsigned int m = *a.work_len;
-  const uint32_t words = a.words;
+  const uint32_t words = a.pitch;
   for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
        i += warps) {
     const uint32_t v = a.work[i];

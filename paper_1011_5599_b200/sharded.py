@@ -70,7 +70,7 @@ class LocalCudaShard:
         next commit reads; the generation flips every step, so re-fetch."""
         b = self.engine.device_buffers()
         blocks = int(b.blocks)
-        W = int(b.words_per_counter)
+        W = int(b.row_pitch)  # u64 words per counter row on the device (>= W)
         counters = device_tensor(b.next_counters, self.n * W, torch.int64, self.device)
         modified = device_tensor(b.next_modified, blocks, torch.int64, self.device)
         sums = device_tensor(b.block_sums, blocks, torch.float64, self.device)

@@ -1,5 +1,5 @@
 """Dev aid: union-kernel variant x L2 fetch granularity sweep on one config.
-    python scripts/sweep.py CONFIG "v1,v2,..." "l2a,l2b,..." """
+    python scripts/sweep.py CONFIG "v1,v2,..." "l2a,l2b,..." (or "ENV=VAL,..." instead of L2 fetch sizes)"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -14,7 +14,10 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for l2 in l2s:
     for v in variants:
         os.environ["HANF_GATHER"] = v
-        os.environ["HANF_L2_FETCH"] = l2
+        if "=" in l2:
+            k_, v_ = l2.split("=", 1); os.environ[k_] = v_
+        else:
+            os.environ["HANF_L2_FETCH"] = l2
         e = h.NfEngine(g, h.EngineConfig(bucket_bits=b, seed=42, exact_sum=False))
         e.reset(); e.step()
         e.set_timing(True)

@@ -362,3 +362,17 @@ def test_worklist_step_parity(hanf, port, monkeypatch):
               hanf.gen_clique_path(30, 40)):
         for b in (5, 6, 7):
             lockstep(hanf, port, g, bucket_bits=b, seed=9)
+
+
+@pytest.mark.parametrize("env", [{"HANF_PITCH": "1"}, {"HANF_PITCH": "0"},
+                                 {"HANF_GATHER": "22"}, {"HANF_GATHER": "2"},
+                                 {"HANF_PITCH": "1", "HANF_GATHER": "30"}])
+def test_row_pitch_and_gather_variants(hanf, port, monkeypatch, env):
+    """Padded rows (aligned 256-bit gathers), unpadded rows and the
+    alternative gather kernels change time only: counters read back in the
+    reference packing and bit-exact in lockstep with the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for g in (hanf.gen_rmat(11, 16, 0.57, 0.19, 0.19, 4, 6), hanf.gen_clique_path(20, 9)):
+        for b, r in [(4, 5), (5, 5), (6, 5), (7, 5), (5, 6), (5, 7), (6, 7)]:
+            lockstep(hanf, port, g, bucket_bits=b, register_bits=r, seed=77)
