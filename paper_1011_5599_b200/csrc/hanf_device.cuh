@@ -547,4 +547,61 @@ __device__ __forceinline__ double estimate_limbs(const uint32_t (&x)[Lay::kLimbs
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA row gathers (sm_100 cp.async.bulk.tensor ... tile::gather4).  The
+// counter array is described to the TMA unit as a 2-D tensor of `pitch`
+// u64 columns x (n + 1) rows; one gather4 copies 4 whole rows (given by
+// index) into shared memory and signals an mbarrier with the byte count.
+// Gathers then bypass the LSU/L1 data pipe: the rows reach the SM as bulk
+// transfers and are read back with LDS.128.  Opt-in: on the BASELINE
+// graphs it is slower than LDG windows (profiles/r01_tma_gather.md).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "HANF_MBAR_WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HANF_MBAR_WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void* dst, const void* map, uint64_t* bar, uint32_t r0,
+                                            uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(0), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3)
+      : "memory");
+}
+
+// Loads a counter row (16-byte aligned, pitch >= 2*ceil(kWords/2) words)
+// with 128-bit loads; works on shared and global addresses.
+template <class Lay>
+__device__ __forceinline__ void load_row16(uint32_t (&v)[Lay::kLimbs], const void* p) {
+  constexpr int NL = Lay::kLimbs;
+  constexpr int NQ = (Lay::kWords + 1) / 2;
+  sfor<0, NQ>([&](auto I) {
+    constexpr int k = decltype(I)::value;
+    const uint4 q = reinterpret_cast<const uint4*>(p)[k];
+    if constexpr (4 * k + 0 < NL) v[4 * k + 0] = q.x;
+    if constexpr (4 * k + 1 < NL) v[4 * k + 1] = q.y;
+    if constexpr (4 * k + 2 < NL) v[4 * k + 2] = q.z;
+    if constexpr (4 * k + 3 < NL) v[4 * k + 3] = q.w;
+  });
+}
+
 }  // namespace hanf

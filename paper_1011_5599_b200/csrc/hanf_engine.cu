@@ -11,6 +11,8 @@
 // Device memory comes from the stream-ordered pool (cudaMallocAsync, kept
 // cached across engines), pinned host staging from a process-wide cache, so
 // creating and destroying engines (estimate_nf) costs no allocator syncs.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -81,6 +83,31 @@ template <class T>
 void pfree(T*& p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
   p = nullptr;
+}
+
+// TMA descriptor of a counter generation: a 2-D tensor of `pitch` u64
+// columns x (n + 1) rows, box = one whole row (gather4 takes 4 row indices).
+// The encoder is a driver entry point (no libcuda link dependency).
+cudaError_t encode_rows_map(CUtensorMap* map, const uint64_t* base, uint64_t rows, uint64_t pitch) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      encode = nullptr;
+  });
+  if (!encode) return cudaErrorNotSupported;
+  cuuint64_t gdim[2] = {pitch, rows};
+  cuuint64_t gstride[1] = {pitch * 8};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(pitch), 1};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(base),
+                            gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 // Keep freed device memory in the pool (no release at synchronisation).
@@ -173,6 +200,8 @@ struct hanf_engine {
   double* reduce_sums = nullptr;
   unsigned long long* reduce_counts = nullptr;
   int gather_mode = -1;       // union kernel variant (-1: per-layout default)
+  bool tma = false;           // gather successor rows with TMA gather4
+  CUtensorMap tmap[2];        // descriptors of cnt[0], cnt[1]
 
   hanf::ReduceOut* h_reduce = nullptr;  // pinned (cache): total + count
   double* h_block_sums = nullptr;       // pinned (cache): exact_sum mode
@@ -445,7 +474,8 @@ hanf_status compute_local(hanf_engine* e) {
   a.check_mod = step_mode(e) != 0 ? 1 : 0;
   a.stale_valid = e->stale_valid ? 1 : 0;
   HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers,
-                               e->gather_mode, e->stream, &e->launches));
+                               e->gather_mode, e->tma ? &e->tmap[g] : nullptr, e->stream,
+                               &e->launches));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
   const bool sharded = e->lo != 0 || e->hi != e->n;
   if (!fused) {
@@ -641,6 +671,12 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   HANF_TRY(palloc(&e->cnt[1], nw, s));
   HANF_TRY(cudaMemsetAsync(e->cnt[0] + n * e->pitch, 0, sizeof(uint64_t) * (e->pitch + 8), s));
   HANF_TRY(cudaMemsetAsync(e->cnt[1] + n * e->pitch, 0, sizeof(uint64_t) * (e->pitch + 8), s));
+  e->tma = hanf::use_tma(params.register_bits, params.registers, static_cast<uint32_t>(e->pitch)) &&
+           n + 1 <= 0xffffffffull;
+  if (e->tma) {
+    HANF_TRY(encode_rows_map(&e->tmap[0], e->cnt[0], n + 1, e->pitch));
+    HANF_TRY(encode_rows_map(&e->tmap[1], e->cnt[1], n + 1, e->pitch));
+  }
   HANF_TRY(palloc(&e->mod[0], e->blocks, s));
   HANF_TRY(palloc(&e->mod[1], e->blocks, s));
   HANF_TRY(palloc(&e->est, n, s));

@@ -2,6 +2,7 @@
 // kernel launchers (not part of the public ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -124,20 +125,22 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
                         uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
                         cudaStream_t s, uint64_t* launches);
+// map: TMA descriptor of args.cur for the gather4 kernel (nullptr: LDG
+// gathers; only single-chunk layouts with an even pitch take it)
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits,
-                         uint32_t registers, int variant, cudaStream_t s,
-                         uint64_t* launches);
+                         uint32_t registers, int variant, const CUtensorMap* map,
+                         cudaStream_t s, uint64_t* launches);
 cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* launches);
 // true when the union kernels compute estimates themselves (single-chunk layouts)
 bool fused_estimates(uint32_t register_bits, uint32_t registers);
-// Row pitch of the counter arrays.  W = 3 rows are padded to 4 words: every
-// counter is then one aligned 32-byte sector read by one 256-bit load
-// (unpadded, half of them straddle two sectors); measured +5% on the
-// DRAM-bound BA graph.  Padding W = 5 or 10 to 8 or 12 cuts load
-// instructions but not L1 wavefronts (a scattered 256-bit load costs two)
-// and grows the L2 footprint: measured 4-7% slower, so those keep pitch W
-// (profiles/r01_row_pitch.md).
+// Row pitch of the counter arrays (u64 words between counters): W, except
+// W = 3 which is padded to one aligned 32-byte sector
+// (profiles/r01_row_pitch.md).  With TMA gathers (opt-in HANF_TMA=1,
+// single-chunk layouts) rows are padded to an even word count: gather4
+// moves whole 16-byte-multiple rows.
 uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words);
+// true when the engine should build TMA descriptors and gather with them
+bool use_tma(uint32_t register_bits, uint32_t registers, uint32_t pitch);
 
 // Step epilogue (block sums + totals), see finish_kernel.
 constexpr int kFinishThreads = 64;

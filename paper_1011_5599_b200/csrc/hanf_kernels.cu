@@ -8,6 +8,7 @@
 //                      (hll.hpp:122-141, engine.hpp:100-113), dirty blocks only
 //   reduce kernels     deterministic total of the block sums and the modified
 //                      count (engine.hpp:115-117, 202-208)
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -246,6 +247,57 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
              1ull << (v & 63));
 }
 
+// Folds the G lanes of each node, then either stores a hub chunk's partial
+// or compares with the old counter (own_load) and commits the changed /
+// stale rows, estimating changed counters from registers.
+template <class Lay, bool kVec16, class OwnLoad>
+__device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTask& task, bool hub,
+                                            bool lead, uint32_t v, bool stale,
+                                            uint32_t (&acc)[Lay::kLimbs], uint32_t woff,
+                                            uint32_t G, bool& any_changed, OwnLoad own_load) {
+  constexpr int NL = Lay::kLimbs;
+  const uint32_t words = args.pitch;
+  for (uint32_t off = G >> 1; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
+  if (hub) {
+    if ((threadIdx.x & 31) == 0)
+      store_chunk<Lay, kVec16>(args.partials + static_cast<uint64_t>(task.item) * words + woff,
+                               acc);
+  } else {
+    // the old counter is re-read (L1/L2 hit) rather than kept live in
+    // registers across the loop
+    uint32_t own[NL];
+    own_load(own);
+    const bool changed = lead && limbs_differ<Lay>(acc, own);
+    any_changed |= changed;
+    if (changed || (lead && stale))
+      store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
+    if (changed && args.est) args.est[v] = estimate_limbs<Lay>(acc, args.ep);
+  }
+}
+
+// Sets the node's modified bit; the last chunk of a split node to finish
+// folds all its partials (ticket handshake).
+template <class Lay, bool kVec16>
+__device__ __forceinline__ void task_finish(const UnionArgs& args, const WarpTask& task, bool hub,
+                                            uint32_t v, bool any_changed, uint32_t lane) {
+  if (any_changed)
+    atomicOr(reinterpret_cast<unsigned long long*>(args.mod_next) + (v >> 6),
+             1ull << (v & 63));
+  if (hub) {
+    const uint32_t h = args.chunk_hub[task.item];
+    uint32_t last = 0;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(args.hub_ticket + h, 1u) == args.hub_count[h] - 1;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      __threadfence();
+      finalize_hub<Lay, kVec16>(args, h, lane);
+      if (lane == 0) args.hub_ticket[h] = 0;  // ready for the next step
+    }
+  }
+}
+
 template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1, bool PF = false>
 __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) {
   using Lay = Layout<R, NREG>;
@@ -322,45 +374,112 @@ __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) 
         swar_max<Lay>(acc, y);
       }
     }
-    for (uint32_t off = G >> 1; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
+    node_commit<Lay, kVec16>(args, task, hub, lead, v, stale, acc, woff, G, any_changed,
+                             [&](uint32_t (&own)[NL]) {
+                               G_t g;
+                               g.issue(cur, lead ? v : zero_row, words, woff);
+                               g.extract(own, lead ? v : zero_row);
+                             });
+  }
+  task_finish<Lay, kVec16>(args, task, hub, v, any_changed, lane);
+}
 
-    if (hub) {
-      if (lane == 0)
-        store_chunk<Lay, kVec16>(args.partials + static_cast<uint64_t>(task.item) * words + woff,
-                                 acc);
-    } else {
-      // the old counter is re-read (L1/L2 hit) rather than kept live in
-      // registers across the loop
-      uint32_t own[NL];
-      {
-        G_t g;
-        g.issue(cur, lead ? v : zero_row, words, woff);
-        g.extract(own, lead ? v : zero_row);
-      }
-      const bool changed = lead && limbs_differ<Lay>(acc, own);
-      any_changed |= changed;
-      if (changed || (lead && stale))
-        store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
-      if (changed && args.est) args.est[v] = estimate_limbs<Lay>(acc, args.ep);
-    }
-  }
-  if (any_changed)
-    atomicOr(reinterpret_cast<unsigned long long*>(args.mod_next) + (v >> 6),
-             1ull << (v & 63));
+// ---------------------------------------------------------------------------
+// Union sweep with TMA row gathers (single-chunk layouts, even pitch).  Same
+// tasks, TOS rows and commit as union_kernel; the successor counters of
+// trip t land in stage t mod S of the warp's shared-memory ring: lane 0
+// arms the stage's mbarrier with the byte count, lanes 0-7 each issue one
+// gather4 for the rows of lanes 4k..4k+3, and every lane reads its own row
+// back once the barrier's phase completes.  S - 1 trips are in flight
+// while one is folded; the loads never touch the LSU data pipe, which
+// bounds the LDG gather (profiles/r01_tma_gather.md).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr uint32_t tma_slot_bytes(uint32_t pitch) {
+  return (4 * pitch * 8 + 127) & ~127u;  // gather4 destinations are 128-byte aligned
+}
+__host__ __device__ constexpr uint32_t tma_smem_bytes(uint32_t pitch, int S) {
+  return 1024 + 8 * S * 8 * tma_slot_bytes(pitch);
+}
+
+template <int R, int NREG, int S, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    union_tma_kernel(const UnionArgs args, const __grid_constant__ CUtensorMap map) {
+  using Lay = Layout<R, NREG>;
+  constexpr int NL = Lay::kLimbs;
+  static_assert(8 * S * 8 <= 1024, "barrier area");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * 8 + warp;
+  if (gw >= args.num_wtasks) return;
+  const uint32_t pitch = args.pitch;
+  const uint32_t row_bytes = pitch * 8;
+  const uint32_t slot = tma_slot_bytes(pitch);
+  const uint32_t stage_bytes = 8 * slot;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * S;
+  uint8_t* ring = smem + 1024 + warp * S * stage_bytes;
+  const uint32_t my_off = (lane >> 2) * slot + (lane & 3) * row_bytes;
+  if (lane < S) mbar_init(bars + lane, 1);
+  mbar_init_fence();
+  __syncwarp();
+
+  const WarpTask task = args.wtasks[gw];
+  const bool hub = task.nodes == 0;
+  const uint32_t lg = hub ? 5u : task.lg;
+  const uint32_t G = 1u << lg;
+  const uint32_t sub = lane & (G - 1);
+  const uint32_t zero_row = args.zero_row;
+  uint32_t v = zero_row;
+  bool active = true;
   if (hub) {
-    // the last chunk of a split node to finish folds all its partials
-    const uint32_t h = args.chunk_hub[task.item];
-    uint32_t last = 0;
-    if (lane == 0) {
-      __threadfence();
-      last = atomicAdd(args.hub_ticket + h, 1u) == args.hub_count[h] - 1;
-    }
-    if (__shfl_sync(0xffffffffu, last, 0)) {
-      __threadfence();
-      finalize_hub<Lay, kVec16>(args, h, lane);
-      if (lane == 0) args.hub_ticket[h] = 0;  // ready for the next step
+    v = args.hub_node[task.item];
+  } else {
+    const uint32_t j = lane >> lg;
+    active = j < task.nodes;
+    if (active) v = args.order[task.item + j];
+  }
+  const bool lead = active && sub == 0 && !hub;
+  bool stale = false;
+  if (lead && args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
+  const uint64_t* __restrict__ cur = args.cur;
+  const uint32_t* __restrict__ ids = args.tos + task.tos + lane;
+  const uint32_t trips = task.trips;
+
+  uint32_t fs = 0;  // next stage to fill
+  auto fill = [&](uint32_t t) {
+    uint32_t w = ld_stream_u32(ids + 32 * t);
+    if (args.check_mod && !((__ldg(args.mod_cur + (w >> 6)) >> (w & 63)) & 1)) w = zero_row;
+    if (lane == 0) mbar_expect_tx(bars + fs, 32 * row_bytes);
+    const uint32_t r0 = __shfl_sync(0xffffffffu, w, (4 * lane + 0) & 31);
+    const uint32_t r1 = __shfl_sync(0xffffffffu, w, (4 * lane + 1) & 31);
+    const uint32_t r2 = __shfl_sync(0xffffffffu, w, (4 * lane + 2) & 31);
+    const uint32_t r3 = __shfl_sync(0xffffffffu, w, (4 * lane + 3) & 31);
+    if (lane < 8) tma_gather4(ring + fs * stage_bytes + lane * slot, &map, bars + fs, r0, r1, r2, r3);
+    fs = fs + 1 == S ? 0 : fs + 1;
+  };
+
+  uint32_t acc[NL];
+  load_row16<Lay>(acc, cur + static_cast<uint64_t>(lead ? v : zero_row) * pitch);
+  const uint32_t pre = trips < S - 1 ? trips : S - 1;
+  for (uint32_t t = 0; t < pre; ++t) fill(t);
+  uint32_t us = 0, ph = 0;
+  for (uint32_t t = 0; t < trips; ++t) {
+    __syncwarp();  // every lane is done with the stage refilled next
+    if (t + S - 1 < trips) fill(t + S - 1);
+    mbar_wait(bars + us, ph);
+    uint32_t y[NL];
+    load_row16<Lay>(y, ring + us * stage_bytes + my_off);
+    swar_max<Lay>(acc, y);
+    if (++us == S) {
+      us = 0;
+      ph ^= 1;
     }
   }
+  bool any_changed = false;
+  node_commit<Lay, false>(args, task, hub, lead, v, stale, acc, 0, G, any_changed,
+                          [&](uint32_t (&own)[NL]) {
+                            load_row16<Lay>(own, cur + static_cast<uint64_t>(lead ? v : zero_row) * pitch);
+                          });
+  task_finish<Lay, false>(args, task, hub, v, any_changed, lane);
 }
 
 namespace {
@@ -393,11 +512,38 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int R, int NREG, int S, int MINB>
+cudaError_t union_tma_launch(UnionArgs a, const CUtensorMap* map, cudaStream_t s) {
+  a.chunks = 1;
+  if (a.num_wtasks == 0) return cudaSuccess;
+  const uint32_t smem = tma_smem_bytes(a.pitch, S);
+  static bool attr_set = false;  // per instantiation; first call is outside capture
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(union_tma_kernel<R, NREG, S, MINB>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const uint32_t blocks = (a.num_wtasks + 7) / 8;
+  union_tma_kernel<R, NREG, S, MINB><<<blocks, 256, smem, s>>>(a, *map);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool fused_estimates(uint32_t register_bits, uint32_t registers) {
   return choose(register_bits, registers).chunks == 1;
 }
+
+namespace {
+// Opt-in (HANF_TMA=1): measured slower than the LDG window gathers on the
+// BASELINE graphs (profiles/r01_tma_gather.md).
+bool tma_env_enabled() {
+  const char* env = std::getenv("HANF_TMA");
+  return env && env[0] == '1';
+}
+}  // namespace
 
 uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words) {
   if (choose(register_bits, registers).chunks != 1) return words;
@@ -405,18 +551,43 @@ uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words) {
     if (env[0] == '0') return words;
     if (env[0] == '1') return (words + 3) & ~3u;  // experiments: pad every layout
   }
+  if (tma_env_enabled()) return (words + 1) & ~1u;
   return words == 3 ? 4 : words;
+}
+
+bool use_tma(uint32_t register_bits, uint32_t registers, uint32_t pitch) {
+  return choose(register_bits, registers).chunks == 1 && pitch % 2 == 0 && tma_env_enabled();
 }
 
 // variant < 0 picks the measured best gather for the layout (profiles/);
 // variants >= 0 select alternatives for experiments (HANF_GATHER).
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t registers,
-                         int variant, cudaStream_t s, uint64_t* launches) {
+                         int variant, const CUtensorMap* map, cudaStream_t s,
+                         uint64_t* launches) {
   const KernelChoice k = choose(register_bits, registers);
   if (args.num_wtasks == 0) return cudaSuccess;
   ++*launches;
   const uint32_t ch = static_cast<uint32_t>(k.chunks);
   const bool single = ch == 1;
+  if (map && single) switch (k.r * 1000 + k.nreg) {
+      case 5016: return union_tma_launch<5, 16, 4, 4>(args, map, s);
+      case 5032: return union_tma_launch<5, 32, 4, 4>(args, map, s);
+      case 5064:
+        switch (variant) {
+          case 40: return union_tma_launch<5, 64, 2, 4>(args, map, s);
+          case 41: return union_tma_launch<5, 64, 4, 3>(args, map, s);
+          case 42: return union_tma_launch<5, 64, 3, 3>(args, map, s);
+          default: return union_tma_launch<5, 64, 3, 4>(args, map, s);
+        }
+      case 5128: return union_tma_launch<5, 128, 3, 3>(args, map, s);
+      case 6016: return union_tma_launch<6, 16, 4, 4>(args, map, s);
+      case 6032: return union_tma_launch<6, 32, 4, 4>(args, map, s);
+      case 7016: return union_tma_launch<7, 16, 4, 4>(args, map, s);
+      case 7032: return union_tma_launch<7, 32, 4, 4>(args, map, s);
+      case 7064: return union_tma_launch<7, 64, 3, 3>(args, map, s);
+      case 8016: return union_tma_launch<8, 16, 4, 4>(args, map, s);
+      default: break;
+    }
   if (single && args.pitch % 4 == 0) switch (k.r * 1000 + k.nreg) {
       case 5032:
         if (variant == 30) return union_launch<5, 32, 4, 3, false, 4, true>(args, ch, s);
