@@ -46,7 +46,7 @@ KEYS = [
 ]
 
 
-def launches(path, tag):
+def launches(path, tag, command):
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
@@ -54,8 +54,8 @@ def launches(path, tag):
     for r in rows[1:]:
         d[r[ki].split("(")[0]].append(float(r[vi].replace(",", "")))
     lines = [f"# {tag}: kernel launch list (ncu --metrics gpu__time_duration.sum --clock-control none)",
-             "", "Cold-cache, serialised replay of `python bench.py --steps 2 --warmup 1 "
-             "--no-cpu-baseline --no-e2e` (seeding and flushes included): compare shares, "
+             "", "Cold-cache, serialised replay of `" + command + "` "
+             "(engine builds, seeding and flushes included): compare shares, "
              "not absolutes.", "", "| kernel | launches | mean µs | min µs |", "|---|---|---|---|"]
     for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {len(v)} | {sum(v)/len(v)/1e3:.1f} | {min(v)/1e3:.1f} |")
@@ -93,12 +93,13 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--full")
     ap.add_argument("--tag", required=True)
+    ap.add_argument("--command", default="python bench.py --steps 2 --warmup 1")
     ap.add_argument("--config", type=int, default=2)
     a = ap.parse_args()
     os.makedirs(PROFILES, exist_ok=True)
     if a.launches:
         with open(os.path.join(PROFILES, f"{a.tag}_launches.md"), "w") as f:
-            f.write(launches(a.launches, a.tag))
+            f.write(launches(a.launches, a.tag, a.command))
     if a.full:
         text, per = full(a.full, a.tag)
         with open(os.path.join(PROFILES, f"{a.tag}_ncu_full.md"), "w") as f:
