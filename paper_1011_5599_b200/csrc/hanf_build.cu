@@ -215,7 +215,8 @@ cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
 
 cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
                                uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
-                               TaskBuild* out, int* bad_input, uint64_t* launches) {
+                               cudaEvent_t succ_ready, TaskBuild* out, int* bad_input,
+                               uint64_t* launches) {
   *out = TaskBuild{};
   *bad_input = 0;
   const uint64_t count = hi - lo;
@@ -366,6 +367,7 @@ cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, ui
   }
   o.tos_words = rows * 32;
   HANF_BUILD_TRY(pool_alloc(&o.tos, o.tos_words, s));
+  if (succ_ready) HANF_BUILD_TRY(cudaStreamWaitEvent(s, succ_ready, 0));
   if (num_tasks) {
     fill_tos_kernel<<<grid(num_tasks * 32), threads, 0, s>>>(
         d_off, lo, d_succ, succ_base, o.order, chunk_begin, o.chunk_node, o.wtasks, num_tasks,

@@ -124,6 +124,37 @@ void configure_pool(int device) {
   done.push_back(device);
 }
 
+// Process-wide cache of non-blocking streams per device (creating and
+// destroying a stream costs ~0.05 ms each, a measurable share of a
+// one-shot estimate_nf).  Streams are returned idle (synchronised).
+class StreamCache {
+ public:
+  cudaError_t get(int device, cudaStream_t* s) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      auto& v = free_[device];
+      if (!v.empty()) {
+        *s = v.back();
+        v.pop_back();
+        return cudaSuccess;
+      }
+    }
+    return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+  }
+  void put(int device, cudaStream_t s) {
+    std::lock_guard<std::mutex> lock(mu_);
+    free_[device].push_back(s);
+  }
+
+ private:
+  std::mutex mu_;
+  std::map<int, std::vector<cudaStream_t>> free_;
+};
+StreamCache& streams() {
+  static StreamCache* c = new StreamCache();  // never destroyed: outlives static engines
+  return *c;
+}
+
 // Process-wide cache of pinned host blocks (cudaMallocHost / cudaFreeHost
 // synchronise the device; engines borrow and return blocks instead).
 class PinnedCache {
@@ -191,11 +222,14 @@ struct hanf_engine {
   uint64_t succ_base = 0;
   unsigned long long* tr_off = nullptr;
   uint32_t* tr_succ = nullptr;
+  uint64_t shard_arcs = 0;
   uint64_t* sig = nullptr;
-  uint32_t* mod_list = nullptr;
+  unsigned long long* mod_list = nullptr;
   uint32_t* work = nullptr;
+  uint32_t* hub_tasks = nullptr;
+  uint32_t* hub_index = nullptr;
   unsigned int* lens = nullptr;
-  bool sparse_ok = false;     // layout supported and HANF_NO_SPARSE unset
+  bool sparse_ok = false;     // worklist step allowed (layout, graph size, HANF_SPARSE)
   hanf::ReduceOut* reduce = nullptr;
   double* reduce_sums = nullptr;
   unsigned long long* reduce_counts = nullptr;
@@ -224,18 +258,33 @@ struct hanf_engine {
   struct StepGraph {
     cudaGraphExec_t exec = nullptr;
     uint64_t kernels = 0;
-    uint32_t uses = 0;  // captured on the second use (capture costs ~1 step)
+    uint32_t uses = 0;  // captured on the third use: capture + instantiate +
+                        // destroy cost more than a one-shot run's few replays
   };
   StepGraph graphs[2][3][2];
   bool use_graphs = true;
 
   ~hanf_engine() {
+    static const bool prof = [] {
+      const char* p = std::getenv("HANF_PROFILE");
+      return p && p[0] == '1';
+    }();
+    auto t0 = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+      if (!prof) return;
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[hanf] destroy %-10s %8.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - t0).count());
+      t0 = now;
+    };
     if (device >= 0) cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    phase("sync");
     for (auto& a : graphs)
       for (auto& b : a)
         for (auto& c : b)
           if (c.exec) cudaGraphExecDestroy(c.exec);
+    phase("graphs");
     for (auto& x : ev)
       if (x) cudaEventDestroy(x);
     if (stream) {
@@ -257,10 +306,15 @@ struct hanf_engine {
       pfree(sig, stream);
       pfree(mod_list, stream);
       pfree(work, stream);
+      pfree(hub_tasks, stream);
+      pfree(hub_index, stream);
       pfree(lens, stream);
       hanf::free_tasks_device(&tasks, stream);
-      cudaStreamSynchronize(stream);
-      cudaStreamDestroy(stream);
+      if (cudaStreamSynchronize(stream) == cudaSuccess)
+        streams().put(device, stream);
+      else
+        cudaStreamDestroy(stream);
+      phase("free");
     }
     pinned().put(h_reduce);
     pinned().put(h_block_sums);
@@ -381,7 +435,7 @@ hanf_status validate_config(const hanf_config* cfg) {
 // produce the same bits; only the time differs.
 int step_mode(const hanf_engine* e) {
   if (!e->cfg.track_modified || e->t == 0) return 0;
-  if (e->sparse_ok && e->stale_valid && 32 * e->last_count < e->n) return 2;
+  if (e->sparse_ok && !e->tma && e->stale_valid && 32 * e->last_count < e->n) return 2;
   return 2 * e->last_count < e->n ? 1 : 0;
 }
 
@@ -393,11 +447,43 @@ hanf_status ensure_sparse(hanf_engine* e) {
   HANF_CUDA(hanf::build_transpose_device(e->csr_off, e->csr_succ, e->lo, e->hi, e->succ_base, e->n,
                                          s, &e->tr_off, &e->tr_succ, &e->launches));
   HANF_CUDA(palloc(&e->sig, e->blocks, s));
-  HANF_CUDA(palloc(&e->mod_list, e->n, s));
-  HANF_CUDA(palloc(&e->work, e->hi - e->lo, s));
-  HANF_CUDA(palloc(&e->lens, 2, s));
+  // one signal task per kSignalChunk predecessors of a modified node
+  HANF_CUDA(palloc(&e->mod_list, e->n + e->shard_arcs / hanf::kSignalChunk + 64, s));
+  HANF_CUDA(palloc(&e->work, e->hi - e->lo + 1, s));
+  HANF_CUDA(palloc(&e->hub_tasks, e->tasks.num_chunks + 1ull, s));
+  HANF_CUDA(hanf::build_hub_index(e->tasks.hub_nodes, e->tasks.num_hubs, e->n, s, &e->hub_index,
+                                  &e->launches));
+  HANF_CUDA(palloc(&e->lens, 3, s));
   HANF_CUDA(cudaStreamSynchronize(s));
   return HANF_OK;
+}
+
+hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
+  hanf::UnionArgs a{};
+  a.tos = e->tasks.tos;
+  a.wtasks = e->tasks.wtasks;
+  a.num_wtasks = e->tasks.num_wtasks;
+  a.zero_row = static_cast<uint32_t>(e->n);
+  const bool fused = hanf::fused_estimates(e->params.register_bits, e->params.registers);
+  a.est = fused ? e->est : nullptr;
+  a.ep = hanf::EstimateParams{e->params.alpha, static_cast<double>(e->params.registers),
+                              e->params.registers, e->params.register_bits,
+                              e->params.words_per_counter, e->log_table};
+  a.cur = e->cnt[g];
+  a.next = e->cnt[ng];
+  a.mod_cur = e->mod[g];
+  a.mod_next = e->mod[ng];
+  a.order = e->tasks.order;
+  a.hub_node = e->tasks.chunk_node;
+  a.partials = e->partials;
+  a.chunk_hub = e->tasks.chunk_hub;
+  a.hub_nodes = e->tasks.hub_nodes;
+  a.hub_first = e->tasks.hub_first;
+  a.hub_count = e->tasks.hub_count;
+  a.hub_ticket = e->tasks.hub_ticket;
+  a.pitch = static_cast<uint32_t>(e->pitch);
+  a.stale_valid = e->stale_valid ? 1 : 0;
+  return a;
 }
 
 hanf_status compute_sparse(hanf_engine* e) {
@@ -422,12 +508,27 @@ hanf_status compute_sparse(hanf_engine* e) {
   a.sig = e->sig;
   a.mod_list = e->mod_list;
   a.work = e->work;
+  a.hub_tasks = e->hub_tasks;
   a.lens = e->lens;
+  a.hub_index = e->hub_index;
+  a.hub_first = e->tasks.hub_first;
+  a.hub_count = e->tasks.hub_count;
   a.n = e->n;
   a.blocks = e->blocks;
   a.hi = e->hi;
   HANF_CUDA(hanf::launch_sparse_step(a, w0, w1, e->params.register_bits, e->params.registers,
                                      e->stream, &e->launches));
+  if (e->tasks.num_chunks) {
+    // worklist hubs: their chunk tasks through the dense kernel (skipping
+    // unmodified successors), chunk partials folded by the usual ticket
+    hanf::UnionArgs u = union_args(e, g, ng);
+    u.check_mod = 1;
+    u.task_list = e->hub_tasks;
+    u.task_count = e->lens + 2;
+    u.num_wtasks = e->tasks.num_chunks;
+    HANF_CUDA(hanf::launch_union(u, e->params.register_bits, e->params.registers, e->gather_mode,
+                                 nullptr, e->stream, &e->launches));
+  }
   return HANF_OK;
 }
 
@@ -446,33 +547,11 @@ hanf_status compute_local(hanf_engine* e) {
     }
     return HANF_OK;
   }
-  hanf::UnionArgs a{};
-  a.tos = e->tasks.tos;
-  a.wtasks = e->tasks.wtasks;
-  a.num_wtasks = e->tasks.num_wtasks;
-  a.zero_row = static_cast<uint32_t>(e->n);
-  const bool fused = hanf::fused_estimates(e->params.register_bits, e->params.registers);
-  a.est = fused ? e->est : nullptr;
-  a.ep = hanf::EstimateParams{e->params.alpha, static_cast<double>(e->params.registers),
-                              e->params.registers, e->params.register_bits,
-                              e->params.words_per_counter, e->log_table};
-  a.cur = e->cnt[g];
-  a.next = e->cnt[ng];
-  a.mod_cur = e->mod[g];
-  a.mod_next = e->mod[ng];
-  a.order = e->tasks.order;
-  a.hub_node = e->tasks.chunk_node;
-  a.partials = e->partials;
-  a.chunk_hub = e->tasks.chunk_hub;
-  a.hub_nodes = e->tasks.hub_nodes;
-  a.hub_first = e->tasks.hub_first;
-  a.hub_count = e->tasks.hub_count;
-  a.hub_ticket = e->tasks.hub_ticket;
-  a.pitch = static_cast<uint32_t>(e->pitch);
+  hanf::UnionArgs a = union_args(e, g, ng);
   // skipping unmodified successors costs a bitmap probe per arc and saves
   // a counter gather per skipped arc: worth it once most counters settled
   a.check_mod = step_mode(e) != 0 ? 1 : 0;
-  a.stale_valid = e->stale_valid ? 1 : 0;
+  const bool fused = a.est != nullptr;
   HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers,
                                e->gather_mode, e->tma ? &e->tmap[g] : nullptr, e->stream,
                                &e->launches));
@@ -534,7 +613,7 @@ hanf_status step_graphed(hanf_engine* e, hanf_iteration_report* rep) {
     if (st != HANF_OK) return st;
   }
   hanf_engine::StepGraph& G = e->graphs[e->cur][mode][e->stale_valid ? 1 : 0];
-  if (!G.exec && ++G.uses < 2) {
+  if (!G.exec && ++G.uses < 3) {
     hanf_status st = compute_local(e);
     if (st != HANF_OK) return st;
     return commit(e, rep);
@@ -598,6 +677,7 @@ hanf_status hanf_sketch_params_make(uint32_t b, uint64_t seed, uint32_t r, hanf_
 hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, hanf_engine** out) {
   if (!g || !cfg_in || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
+  const auto t_create0 = std::chrono::steady_clock::now();
   hanf_status st = validate_config(cfg_in);
   if (st != HANF_OK) return st;
   const uint64_t n = g->n;
@@ -635,15 +715,19 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
-  // The worklist step is opt-in (HANF_SPARSE=1): on the BASELINE R-MAT
-  // graphs the late iterations' changed counters are hubs whose predecessor
-  // sets cover most of the graph, and the dense sweep with skipping wins
-  // (profiles/r01_sparse.md).
+  // Worklist step (HANF_SPARSE=0 disables): taken once fewer than n/32
+  // counters changed (the measured crossover on the long-diameter copying
+  // graph) on graphs with >= 2^22 arcs (below that one dense launch costs
+  // less than the worklist's launches); profiles/r01_sparse.md.
   e->sparse_ok = hanf::sparse_supported(params.register_bits, params.registers) &&
-                 hanf::fused_estimates(params.register_bits, params.registers);
+                 hanf::fused_estimates(params.register_bits, params.registers) &&
+                 n > 0 && g->offsets[hi] - g->offsets[lo] >= (1ull << 22);
   {
     const char* sp = std::getenv("HANF_SPARSE");
-    e->sparse_ok = e->sparse_ok && sp && std::atoi(sp) != 0;
+    if (sp && sp[0] == '0') e->sparse_ok = false;
+    if (sp && sp[0] == '1')  // tests: force it on every supported graph
+      e->sparse_ok = hanf::sparse_supported(params.register_bits, params.registers) &&
+                     hanf::fused_estimates(params.register_bits, params.registers);
   }
 
   auto bail = [&](hanf_status s) {
@@ -662,7 +746,7 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   configure_pool(cfg.device);
   if (const char* l2 = std::getenv("HANF_L2_FETCH"))
     HANF_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::atoi(l2)));
-  HANF_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  HANF_TRY(streams().get(cfg.device, &e->stream));
   cudaStream_t s = e->stream;
   // row n is an all-zero counter (the union kernels' padding target); 8
   // extra words keep the 256-bit window loads of the last rows in bounds
@@ -709,34 +793,81 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
                              cudaMemcpyHostToDevice, s));
     HANF_TRY(cudaStreamSynchronize(s));
   }
+  // HANF_PROFILE=1: print the create phases (synchronising between them)
+  static const bool prof = [] {
+    const char* p = std::getenv("HANF_PROFILE");
+    return p && p[0] == '1';
+  }();
+  auto t_prev = t_create0;
+  auto phase = [&](const char* what) {
+    if (!prof) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hanf] create %-10s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_prev).count());
+    t_prev = now;
+  };
+  phase("alloc");
   if (n > 0) {
-    // the shard's CSR goes to the device only to build the tasks (it is
-    // laid out again in task order there) and is released afterwards
+    // the shard's CSR goes to the device to build the tasks (it is laid
+    // out again in task order there) and stays for the worklist step
     const uint64_t a0 = g->offsets[lo], a1 = g->offsets[hi];
     uint64_t* d_off = nullptr;
     uint32_t* d_succ = nullptr;
     HANF_TRY(palloc(&d_off, hi - lo + 1, s));
     HANF_TRY(palloc(&d_succ, a1 - a0, s));
+    // offsets first on the engine stream; the arcs follow on a helper
+    // stream while the engine stream seeds and sorts by degree (only the
+    // TOS fill waits for them)
+    cudaStream_t s2 = nullptr;
+    HANF_TRY(streams().get(cfg.device, &s2));
+    cudaEvent_t ev_off = nullptr, ev_arcs = nullptr;
+    struct UploadGuard {  // the helper stream is idle again before anything is freed
+      int dev;
+      cudaStream_t st;
+      cudaEvent_t a, b;
+      ~UploadGuard() {
+        if (cudaStreamSynchronize(st) == cudaSuccess)
+          streams().put(dev, st);
+        else
+          cudaStreamDestroy(st);
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+      }
+    } guard{cfg.device, s2, nullptr, nullptr};
+    HANF_TRY(cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming));
+    guard.a = ev_off;
+    HANF_TRY(cudaEventCreateWithFlags(&ev_arcs, cudaEventDisableTiming));
+    guard.b = ev_arcs;
     HANF_TRY(cudaMemcpyAsync(d_off, g->offsets + lo, sizeof(uint64_t) * (hi - lo + 1),
                              cudaMemcpyHostToDevice, s));
+    HANF_TRY(cudaEventRecord(ev_off, s));
+    HANF_TRY(cudaStreamWaitEvent(s2, ev_off, 0));
     if (a1 > a0)
       HANF_TRY(cudaMemcpyAsync(d_succ, g->arcs + a0, sizeof(uint32_t) * (a1 - a0),
-                               cudaMemcpyHostToDevice, s));
+                               cudaMemcpyHostToDevice, s2));
+    HANF_TRY(cudaEventRecord(ev_arcs, s2));
+    phase("offsets");
+    st = seed_all(e);
+    if (st != HANF_OK) return bail(st);
+    phase("seed");
     int bad = 0;
-    const cudaError_t be =
-        hanf::build_tasks_device(d_off, d_succ, lo, hi, a0, n, s, &e->tasks, &bad, &e->launches);
+    const cudaError_t be = hanf::build_tasks_device(d_off, d_succ, lo, hi, a0, n, s, ev_arcs,
+                                                    &e->tasks, &bad, &e->launches);
+    // (also on the build's error paths) frees on `s` come after the upload
+    HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
     e->csr_off = d_off;
     e->csr_succ = d_succ;
     e->succ_base = a0;
+    e->shard_arcs = a1 - a0;
     if (be == cudaErrorInvalidValue)
       return bail(fail(HANF_INVALID_ARGUMENT, "too many nodes or tasks in one engine shard"));
     HANF_TRY(be);
     if (bad)
       return bail(fail(HANF_INVALID_ARGUMENT,
                        "arc endpoint out of range or offsets not non-decreasing"));
+    phase("build");
     HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
-    st = seed_all(e);
-    if (st != HANF_OK) return bail(st);
   }
 #undef HANF_TRY
   *out = e;

@@ -42,10 +42,13 @@ struct TaskBuild {
 };
 // Builds the tasks of nodes [lo, hi) from the shard's CSR on the device
 // (d_off = offsets[lo..hi], d_succ = arcs from index succ_base).  Sets
-// *bad_input when offsets decrease or an arc endpoint is >= n.
+// *bad_input when offsets decrease or an arc endpoint is >= n.  Only the
+// final TOS fill reads d_succ: it waits for `succ_ready` (when non-null),
+// so the arcs upload overlaps the degree sort and task layout.
 cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
                                uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
-                               TaskBuild* out, int* bad_input, uint64_t* launches);
+                               cudaEvent_t succ_ready, TaskBuild* out, int* bad_input,
+                               uint64_t* launches);
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
 // Worklist ("systolic") step, hanf_sparse.cu.
@@ -64,12 +67,21 @@ struct SparseArgs {
   const unsigned long long* tr_off;  // transpose of the shard's arcs: preds of every node
   const uint32_t* tr_succ;
   uint64_t* sig;              // scratch bitmap (signalled nodes)
-  uint32_t* mod_list;         // scratch: modified nodes
-  uint32_t* work;             // scratch: worklist
-  unsigned int* lens;         // [0] modified, [1] worklist
+  unsigned long long* mod_list;  // scratch: (modified node << 32 | predecessor chunk)
+  uint32_t* work;             // scratch: worklist (nodes of out-degree <= kHubDegree)
+  uint32_t* hub_tasks;        // scratch: chunk tasks of worklist hubs (dense kernel)
+  unsigned int* lens;         // [0] modified chunks, [1] worklist, [2] hub tasks
   const unsigned int* work_len;
+  const uint32_t* hub_index;  // node -> hub (UINT32_MAX: not a hub)
+  const uint32_t* hub_first;  // per hub: first chunk task, chunk count
+  const uint32_t* hub_count;
   uint64_t n, blocks, hi;
 };
+// predecessors signalled per warp task of the signal kernel
+constexpr uint32_t kSignalChunk = 256;
+// node -> hub index map for the worklist step (UINT32_MAX elsewhere)
+cudaError_t build_hub_index(const uint32_t* hub_nodes, uint32_t hubs, uint64_t n, cudaStream_t s,
+                            uint32_t** out, uint64_t* launches);
 cudaError_t build_transpose_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
                                    uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
                                    unsigned long long** tr_off, uint32_t** tr_succ,
@@ -101,6 +113,8 @@ struct UnionArgs {
   int32_t stale_valid;       // next[v] may be stale where mod_cur[v] is set
   double* est;               // per-counter estimates (nullptr: not fused)
   EstimateParams ep;
+  const uint32_t* task_list;       // non-null: run only these task indices
+  const unsigned int* task_count;  // (device) length of task_list
 };
 
 struct EstimateArgs {

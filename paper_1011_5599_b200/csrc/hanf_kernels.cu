@@ -298,16 +298,14 @@ __device__ __forceinline__ void task_finish(const UnionArgs& args, const WarpTas
   }
 }
 
-template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1, bool PF = false>
-__global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) {
+template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB, bool PF>
+__device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_index,
+                                           uint32_t lane) {
   using Lay = Layout<R, NREG>;
   constexpr int NL = Lay::kLimbs;
   constexpr int NW = Lay::kWords;
   using G_t = Gather<Lay, GMODE, kVec16>;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  if (gw >= args.num_wtasks) return;
-  const WarpTask task = args.wtasks[gw];
+  const WarpTask task = args.wtasks[task_index];
   const bool hub = task.nodes == 0;
   const uint32_t lg = hub ? 5u : task.lg;
   const uint32_t G = 1u << lg;
@@ -382,6 +380,23 @@ __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) 
                              });
   }
   task_finish<Lay, kVec16>(args, task, hub, v, any_changed, lane);
+}
+
+// One warp per task; with a task list (the worklist step's hub chunks) the
+// warps stride over the listed task indices instead.
+template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1, bool PF = false>
+__global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) {
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (args.task_list) {
+    const uint32_t count = *args.task_count;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = gw; i < count; i += nw)
+      union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, args.task_list[i], lane);
+    return;
+  }
+  if (gw >= args.num_wtasks) return;
+  union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, gw, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -507,7 +522,8 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   a.chunks = chunks;
   if (chunks != 1) a.est = nullptr;  // estimates need the whole counter in registers
   if (a.num_wtasks == 0) return cudaSuccess;
-  const uint32_t blocks = (a.num_wtasks + 7) / 8;
+  uint32_t blocks = (a.num_wtasks + 7) / 8;
+  if (a.task_list && blocks > 148 * 4) blocks = 148 * 4;
   union_kernel<R, NREG, U, GM, V, MINB, PF><<<blocks, 256, 0, s>>>(a);
   return cudaGetLastError();
 }

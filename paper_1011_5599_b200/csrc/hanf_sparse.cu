@@ -52,42 +52,104 @@ __global__ void tr_scatter_kernel(const uint64_t* __restrict__ off, uint64_t lo,
 }
 
 // ---- worklist -------------------------------------------------------------
-// list of set bits of `bits` over words [w0, w1) (order unspecified)
-__global__ void bits_to_list_kernel(const uint64_t* __restrict__ bits, const uint64_t* __restrict__ extra,
-                                    uint64_t w0, uint64_t w1, uint64_t n,
-                                    uint32_t* __restrict__ list, unsigned int* __restrict__ len) {
+// Modified nodes as signal tasks: one entry per kSignalChunk predecessors,
+// so a node with a huge in-degree is spread over many warps.
+__global__ void modified_chunks_kernel(const uint64_t* __restrict__ bits, uint64_t words,
+                                       uint64_t n, const unsigned long long* __restrict__ tr_off,
+                                       unsigned long long* __restrict__ list,
+                                       unsigned int* __restrict__ len) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t w = w0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < w1;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < words;
        w += stride) {
-    uint64_t word = bits[w] | (extra ? extra[w] : 0ull);
+    uint64_t word = bits[w];
     if (!word) continue;
-    const unsigned int c = __popcll(word);
-    unsigned int pos = atomicAdd(len, c);
-    while (word) {
-      const int b = __ffsll(static_cast<long long>(word)) - 1;
-      word &= word - 1;
-      const uint64_t v = (w << 6) + b;
-      if (v < n) list[pos++] = static_cast<uint32_t>(v);
+    unsigned int total = 0;
+    for (uint64_t x = word; x; x &= x - 1) {
+      const uint64_t v = (w << 6) + (__ffsll(static_cast<long long>(x)) - 1);
+      if (v < n)
+        total += static_cast<unsigned int>((tr_off[v + 1] - tr_off[v] + kSignalChunk - 1) /
+                                           kSignalChunk);
+    }
+    if (!total) continue;
+    unsigned int pos = atomicAdd(len, total);
+    for (; word; word &= word - 1) {
+      const uint64_t v = (w << 6) + (__ffsll(static_cast<long long>(word)) - 1);
+      if (v >= n) continue;
+      const uint64_t c = (tr_off[v + 1] - tr_off[v] + kSignalChunk - 1) / kSignalChunk;
+      for (uint64_t k = 0; k < c; ++k) list[pos++] = (v << 32) | k;
     }
   }
 }
 
-// signalled[pred] = 1 for every predecessor (in this shard) of a listed node
-__global__ void signal_kernel(const uint32_t* __restrict__ list, const unsigned int* __restrict__ len,
+// signalled[pred] = 1 for the predecessors (in this shard) of each listed
+// chunk; the 8 ids per lane are loaded before any atomic is issued
+__global__ void signal_kernel(const unsigned long long* __restrict__ list,
+                              const unsigned int* __restrict__ len,
                               const unsigned long long* __restrict__ tr_off,
                               const uint32_t* __restrict__ tr_succ, uint64_t* __restrict__ sig) {
+  constexpr int kPer = kSignalChunk / 32;
   const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const unsigned int m = *len;
   for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
        i += warps) {
-    const uint32_t u = list[i];
-    const uint64_t s = tr_off[u], e = tr_off[u + 1];
-    for (uint64_t k = s + lane; k < e; k += 32) {
-      const uint32_t p = tr_succ[k];
-      atomicOr(reinterpret_cast<unsigned long long*>(sig) + (p >> 6), 1ull << (p & 63));
+    const unsigned long long e = list[i];
+    const uint32_t u = static_cast<uint32_t>(e >> 32);
+    const uint64_t s = tr_off[u] + (e & 0xffffffffull) * kSignalChunk;
+    const uint64_t t = tr_off[u + 1];
+    uint32_t p[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const uint64_t k = s + lane + 32 * j;
+      p[j] = k < t ? tr_succ[k] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (p[j] != 0xffffffffu)
+        atomicOr(reinterpret_cast<unsigned long long*>(sig) + (p[j] >> 6), 1ull << (p[j] & 63));
+  }
+}
+
+// worklist = signalled | stale over this shard's words: hubs contribute all
+// their chunk tasks (run by the dense kernel), other nodes a worklist entry
+__global__ void worklist_kernel(const uint64_t* __restrict__ sig, const uint64_t* __restrict__ stale,
+                                uint64_t w0, uint64_t w1, uint64_t hi,
+                                const uint32_t* __restrict__ hub_index,
+                                const uint32_t* __restrict__ hub_first,
+                                const uint32_t* __restrict__ hub_count,
+                                uint32_t* __restrict__ work, uint32_t* __restrict__ hub_tasks,
+                                unsigned int* __restrict__ lens) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = w0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < w1;
+       w += stride) {
+    uint64_t word = sig[w] | stale[w];
+    const uint64_t first = w << 6;
+    if (first + 64 > hi) word &= hi > first ? (~0ull >> (first + 64 - hi)) : 0ull;
+    if (!word) continue;
+    unsigned int light = 0, chunks = 0;
+    for (uint64_t x = word; x; x &= x - 1) {
+      const uint32_t v = static_cast<uint32_t>(first + __ffsll(static_cast<long long>(x)) - 1);
+      const uint32_t h = hub_index[v];
+      if (h == 0xffffffffu) ++light; else chunks += hub_count[h];
+    }
+    unsigned int pl = light ? atomicAdd(lens + 1, light) : 0;
+    unsigned int ph = chunks ? atomicAdd(lens + 2, chunks) : 0;
+    for (; word; word &= word - 1) {
+      const uint32_t v = static_cast<uint32_t>(first + __ffsll(static_cast<long long>(word)) - 1);
+      const uint32_t h = hub_index[v];
+      if (h == 0xffffffffu) {
+        work[pl++] = v;
+      } else {
+        for (uint32_t k = 0; k < hub_count[h]; ++k) hub_tasks[ph++] = hub_first[h] + k;
+      }
     }
   }
+}
+
+__global__ void hub_index_kernel(const uint32_t* __restrict__ hub_nodes, uint32_t hubs,
+                                 uint32_t* __restrict__ index) {
+  const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h < hubs) index[hub_nodes[h]] = h;
 }
 
 // ---- sparse union: one warp per worklist node -----------------------------
@@ -99,6 +161,7 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   const unsigned int m = *a.work_len;
   const uint32_t words = a.pitch;
+  const uint32_t zero_row = static_cast<uint32_t>(a.n);
   for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
        i += warps) {
     const uint32_t v = a.work[i];
@@ -108,12 +171,25 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
       load_chunk<Lay, kVec16>(acc, a.cur + static_cast<uint64_t>(v) * words);
     else
       sfor<0, NL>([&](auto I) { acc[decltype(I)::value] = 0u; });
-    for (uint64_t k = s + lane; k < e; k += 32) {
-      const uint32_t w = a.succ[k - a.succ_base];
-      if ((__ldg(a.mod_cur + (w >> 6)) >> (w & 63)) & 1) {
-        uint32_t y[NL];
-        load_chunk<Lay, kVec16>(y, a.cur + static_cast<uint64_t>(w) * words);
-        swar_max<Lay>(acc, y);
+    // out-degree <= kHubDegree here (hubs run as dense chunk tasks): at
+    // most 32 successors per lane, ids and bitmap probes loaded 4 at a time
+    for (uint64_t k0 = s + lane; k0 < e; k0 += 128) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t k = k0 + 32 * j;
+        w[j] = k < e ? a.succ[k - a.succ_base] : zero_row;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (!((__ldg(a.mod_cur + (w[j] >> 6)) >> (w[j] & 63)) & 1)) w[j] = zero_row;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (w[j] != zero_row) {
+          uint32_t y[NL];
+          load_chunk<Lay, kVec16>(y, a.cur + static_cast<uint64_t>(w[j]) * words);
+          swar_max<Lay>(acc, y);
+        }
       }
     }
     for (uint32_t off = 16; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
@@ -190,18 +266,18 @@ cudaError_t build_transpose_device(const uint64_t* d_off, const uint32_t* d_succ
 cudaError_t launch_sparse_step(const SparseArgs& a, uint64_t w0, uint64_t w1, uint32_t register_bits,
                                uint32_t registers, cudaStream_t s, uint64_t* launches) {
   const uint32_t blocks = 148 * 8;
-  // modified list (whole bitmap: successors anywhere signal this shard)
-  cudaError_t e = cudaMemsetAsync(a.lens, 0, 2 * sizeof(unsigned int), s);
+  cudaError_t e = cudaMemsetAsync(a.lens, 0, 3 * sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
-  bits_to_list_kernel<<<blocks, 256, 0, s>>>(a.mod_cur, nullptr, 0, a.blocks, a.n, a.mod_list,
-                                            a.lens);
+  // modified chunks (whole bitmap: successors anywhere signal this shard)
+  modified_chunks_kernel<<<blocks, 256, 0, s>>>(a.mod_cur, a.blocks, a.n, a.tr_off, a.mod_list,
+                                               a.lens);
   ++*launches;
   e = cudaMemsetAsync(a.sig + w0, 0, sizeof(uint64_t) * (w1 - w0), s);
   if (e != cudaSuccess) return e;
   signal_kernel<<<blocks, 256, 0, s>>>(a.mod_list, a.lens, a.tr_off, a.tr_succ, a.sig);
   ++*launches;
-  // worklist = signalled | stale, restricted to this shard
-  bits_to_list_kernel<<<blocks, 256, 0, s>>>(a.sig, a.mod_cur, w0, w1, a.hi, a.work, a.lens + 1);
+  worklist_kernel<<<blocks, 256, 0, s>>>(a.sig, a.mod_cur, w0, w1, a.hi, a.hub_index, a.hub_first,
+                                         a.hub_count, a.work, a.hub_tasks, a.lens);
   ++*launches;
   SparseArgs b = a;
   b.work_len = a.lens + 1;
@@ -219,6 +295,19 @@ cudaError_t launch_sparse_step(const SparseArgs& a, uint64_t w0, uint64_t w1, ui
     case 8016: return sparse_launch<8, 16, true>(b, blocks, s);
     default: return cudaErrorInvalidValue;  // multi-chunk layouts use the dense sweep
   }
+}
+
+cudaError_t build_hub_index(const uint32_t* hub_nodes, uint32_t hubs, uint64_t n, cudaStream_t s,
+                            uint32_t** out, uint64_t* launches) {
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(out), sizeof(uint32_t) * (n ? n : 1), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(*out, 0xff, sizeof(uint32_t) * (n ? n : 1), s);
+  if (e != cudaSuccess) return e;
+  if (hubs) {
+    hub_index_kernel<<<(hubs + 255) / 256, 256, 0, s>>>(hub_nodes, hubs, *out);
+    ++*launches;
+  }
+  return cudaGetLastError();
 }
 
 bool sparse_supported(uint32_t register_bits, uint32_t registers) {
