@@ -230,6 +230,8 @@ struct hanf_engine {
   uint32_t* hub_index = nullptr;
   unsigned int* lens = nullptr;
   bool sparse_ok = false;     // worklist step allowed (layout, graph size, HANF_SPARSE)
+  uint32_t sparse_after = 8;  // eligible steps before the transpose is built
+  uint32_t sparse_wanted_steps = 0;
   hanf::ReduceOut* reduce = nullptr;
   double* reduce_sums = nullptr;
   unsigned long long* reduce_counts = nullptr;
@@ -433,10 +435,21 @@ hanf_status validate_config(const hanf_config* cfg) {
 // Step kind for the current state: 0 dense sweep, 1 dense sweep skipping
 // unmodified successors, 2 worklist step (engine.hpp:210-224).  All three
 // produce the same bits; only the time differs.
+bool sparse_wanted(const hanf_engine* e) {
+  return e->cfg.track_modified && e->t != 0 && e->sparse_ok && !e->tma && e->stale_valid &&
+         32 * e->last_count < e->n;
+}
 int step_mode(const hanf_engine* e) {
   if (!e->cfg.track_modified || e->t == 0) return 0;
-  if (e->sparse_ok && !e->tma && e->stale_valid && 32 * e->last_count < e->n) return 2;
+  // the transpose costs about as much as 8 skip sweeps of the same arcs
+  // (profiles/r01_sparse.md): build it (ski-rental style) only once that
+  // many steps would have used it, so short runs never pay for it
+  if (sparse_wanted(e) && (e->tr_off || e->sparse_wanted_steps >= e->sparse_after)) return 2;
   return 2 * e->last_count < e->n ? 1 : 0;
+}
+// Called once at the start of every step, before step_mode.
+void note_step(hanf_engine* e) {
+  if (sparse_wanted(e) && !e->tr_off) ++e->sparse_wanted_steps;
 }
 
 // Builds the transpose and worklist scratch on first use (outside any
@@ -725,9 +738,11 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   {
     const char* sp = std::getenv("HANF_SPARSE");
     if (sp && sp[0] == '0') e->sparse_ok = false;
-    if (sp && sp[0] == '1')  // tests: force it on every supported graph
+    if (sp && sp[0] == '1') {  // tests: force it on every supported graph, at once
       e->sparse_ok = hanf::sparse_supported(params.register_bits, params.registers) &&
                      hanf::fused_estimates(params.register_bits, params.registers);
+      e->sparse_after = 1;
+    }
   }
 
   auto bail = [&](hanf_status s) {
@@ -901,6 +916,7 @@ hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
     return HANF_OK;
   }
   HANF_CUDA(cudaSetDevice(e->device));
+  note_step(e);
   // phase timing needs events between the kernels: run ungraphed then
   if (e->use_graphs && !e->timing) return step_graphed(e, rep);
   if (step_mode(e) == 2) {
@@ -916,6 +932,7 @@ hanf_status hanf_shard_compute(hanf_engine* e) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
   if (e->n == 0) return HANF_OK;
   HANF_CUDA(cudaSetDevice(e->device));
+  note_step(e);
   if (step_mode(e) == 2) {
     const hanf_status sst = ensure_sparse(e);
     if (sst != HANF_OK) return sst;

@@ -11,8 +11,12 @@ for cfgno in [int(c) for c in sys.argv[1].split(",")]:
     g = make()
     print(name, flush=True)
     rows = {}
-    for mode in ("0", "1"):
-        os.environ["HANF_SPARSE"] = mode
+    modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1"]
+    for mode in modes:
+        if mode == "default":
+            os.environ.pop("HANF_SPARSE", None)
+        else:
+            os.environ["HANF_SPARSE"] = mode
         for rep in range(2):  # second run: graphs captured, transpose built
             e = h.NfEngine(g, h.EngineConfig(bucket_bits=b, seed=42, exact_sum=False))
             if rep == 1:
@@ -25,7 +29,8 @@ for cfgno in [int(c) for c in sys.argv[1].split(",")]:
                     break
             e.close()
         rows[mode] = times
-    pairs = list(zip(rows["0"], rows["1"]))
+    pairs = list(zip(rows[modes[0]], rows[modes[1]]))
+    print("columns:", modes)
     if len(pairs) <= 40:
         print(f"{'t':>3} {'modified':>10} {'dense+skip ms':>14} {'worklist ms':>12}")
         for t, ((a, m), (c, _)) in enumerate(pairs, 1):
@@ -41,4 +46,4 @@ for cfgno in [int(c) for c in sys.argv[1].split(",")]:
         for k in sorted(buckets):
             n_, sa, sc = buckets[k]
             print(f"{k:>8} {n_:>6} {sa / n_:>14.3f} {sc / n_:>12.3f}")
-    print(f"total {sum(x for x, _ in rows['0']):.3f} ms vs {sum(x for x, _ in rows['1']):.3f} ms", flush=True)
+    print(f"total {sum(x for x, _ in rows[modes[0]]):.3f} ms vs {sum(x for x, _ in rows[modes[1]]):.3f} ms", flush=True)
