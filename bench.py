@@ -303,13 +303,12 @@ def main():
 
     e2e = None
     if not args.no_e2e and world == 1:
-        # whole estimate_nf through the C-ABI from pinned host memory
-        off_pin = torch.from_numpy(g.offsets().view("int64")).pin_memory()
-        arc_pin = torch.from_numpy(g.arcs().view("int32")).pin_memory()
-        pinned = hanf.Graph.__new__(hanf.Graph)
-        pinned._n = n
-        pinned._offsets = off_pin.numpy().view("uint64")
-        pinned._arcs = arc_pin.numpy().view("uint32")
+        # whole estimate_nf through the C-ABI from pinned host memory: the
+        # caller's CSR (fresh numpy arrays) page-locked in place with
+        # Graph.pin() (hanf_pin_host).  torch.pin_memory() buffers are not
+        # used: on these VMs their H2D rate varies 21-55 GB/s from buffer to
+        # buffer, registered huge-page memory holds 55 (profiles/r01_h2d.md)
+        pinned = hanf.Graph(n, g.offsets().copy(), g.arcs().copy()).pin()
         e2e_cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank)
         hanf.estimate_nf(pinned, e2e_cfg)     # warm (context, allocator)
         runs, iters, wall = min(args.steps, 5), 0, 0.0
@@ -318,6 +317,8 @@ def main():
             t0 = time.perf_counter()
             est = hanf.estimate_nf(pinned, e2e_cfg)
             wall += time.perf_counter() - t0
+            if os.environ.get("BENCH_DEBUG"):
+                print(f"e2e run {1e3 * (time.perf_counter() - t0):.3f} ms", file=sys.stderr)
             iters += est.iterations() + 1       # + the stabilising iteration
         blocks = (n + 63) // 64
         per_run_iters = iters / runs

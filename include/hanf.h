@@ -219,6 +219,16 @@ hanf_status hanf_graph_load_csr(const char* path, hanf_graph** out);
 hanf_status hanf_graph_view_of(const hanf_graph* g, hanf_graph_view* view);
 void hanf_graph_free(hanf_graph* g);
 
+/* (new: the reference keeps graphs in pageable vectors) Page-locks the host
+ * range [p, p + bytes) in place (cudaHostRegister) so hanf_create uploads
+ * it by DMA at full link rate instead of through a bounce buffer; pair
+ * with hanf_unpin_host before the memory is freed.  Large allocations made
+ * with transparent huge pages (numpy, or madvise(MADV_HUGEPAGE)) register
+ * as few IOMMU mappings and reach ~55 GB/s H2D on B200 hosts
+ * (profiles/r01_h2d.md). */
+hanf_status hanf_pin_host(const void* p, uint64_t bytes);
+hanf_status hanf_unpin_host(const void* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -97,6 +97,8 @@ _SIGNATURES = {
     "hanf_graph_save_csr": [_P, c_char_p],
     "hanf_graph_load_csr": [c_char_p, POINTER(_P)],
     "hanf_graph_view_of": [_P, POINTER(GraphView)],
+    "hanf_pin_host": [_P, c_uint64],
+    "hanf_unpin_host": [_P],
 }
 _VOID = {"hanf_destroy": [_P], "hanf_graph_free": [_P]}
 

@@ -1098,6 +1098,18 @@ hanf_status hanf_timing(const hanf_engine* e, double* union_ms, double* estimate
   return HANF_OK;
 }
 
+hanf_status hanf_pin_host(const void* p, uint64_t bytes) {
+  if (!p || bytes == 0) return fail(HANF_INVALID_ARGUMENT, "null or empty host range");
+  HANF_CUDA(cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterPortable));
+  return HANF_OK;
+}
+
+hanf_status hanf_unpin_host(const void* p) {
+  if (!p) return fail(HANF_INVALID_ARGUMENT, "null host pointer");
+  HANF_CUDA(cudaHostUnregister(const_cast<void*>(p)));
+  return HANF_OK;
+}
+
 hanf_status hanf_device_buffers(hanf_engine* e, hanf_buffers* out) {
   if (!e || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
   const int ng = 1 - e->cur;

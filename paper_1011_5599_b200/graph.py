@@ -18,9 +18,10 @@ from ._lib import check, lib
 class Graph:
     """Immutable directed graph in CSR layout (graph.hpp:23-69)."""
 
-    __slots__ = ("_n", "_offsets", "_arcs")
+    __slots__ = ("_n", "_offsets", "_arcs", "_pinned")
 
     def __init__(self, n: int = 0, offsets=None, arcs=None):
+        self._pinned = []
         self._n = int(n)
         self._offsets = (np.zeros(1, dtype=np.uint64) if offsets is None
                          else np.ascontiguousarray(offsets, dtype=np.uint64))
@@ -58,6 +59,27 @@ class Graph:
             n, src.ctypes.data_as(POINTER(c_uint32)), dst.ctypes.data_as(POINTER(c_uint32)),
             src.size, ctypes.byref(h)))
         return Graph._adopt(h)
+
+    # -- page-locking for uploads (new; hanf_pin_host) -------------------------
+    def pin(self) -> "Graph":
+        """Page-locks the CSR arrays in place so engines upload them by DMA
+        at full link rate; undone by unpin() or when the graph is freed."""
+        for arr in (self._offsets, self._arcs):
+            if arr.nbytes and not any(p == arr.ctypes.data for p in self._pinned):
+                check(lib().hanf_pin_host(c_void_p(arr.ctypes.data), arr.nbytes))
+                self._pinned.append(arr.ctypes.data)
+        return self
+
+    def unpin(self) -> None:
+        while self._pinned:
+            check(lib().hanf_unpin_host(c_void_p(self._pinned.pop())))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_pinned", None):
+                self.unpin()
+        except Exception:
+            pass
 
     # -- accessors (graph.hpp:46-57) ----------------------------------------
     def num_nodes(self) -> int:

@@ -377,3 +377,17 @@ def test_row_pitch_and_gather_variants(hanf, port, monkeypatch, env):
     for g in (hanf.gen_rmat(11, 16, 0.57, 0.19, 0.19, 4, 6), hanf.gen_clique_path(20, 9)):
         for b, r in [(4, 5), (5, 5), (6, 5), (7, 5), (5, 6), (5, 7), (6, 7)]:
             lockstep(hanf, port, g, bucket_bits=b, register_bits=r, seed=77)
+
+
+def test_pinned_graph_upload(hanf):
+    """Graph.pin() (hanf_pin_host) changes the upload path only."""
+    g = hanf.gen_rmat(12, 16, 0.57, 0.19, 0.19, 5, 9)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=3)
+    a = hanf.estimate_nf(g, cfg)
+    p = hanf.Graph(g.num_nodes(), g.offsets().copy(), g.arcs().copy()).pin()
+    b = hanf.estimate_nf(p, cfg)
+    p.unpin()
+    p.unpin()  # idempotent
+    assert list(a.values) == list(b.values) and list(a.modified) == list(b.modified)
+    with pytest.raises(Exception):
+        hanf._lib.check(hanf._lib.lib().hanf_pin_host(None, 8))
