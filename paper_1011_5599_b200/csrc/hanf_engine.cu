@@ -211,7 +211,7 @@ struct hanf_engine {
 
   uint64_t* cnt[2] = {nullptr, nullptr};  // (n + 1) * pitch words + 8 (window loads)
   uint64_t* mod[2] = {nullptr, nullptr};  // blocks words
-  double* est = nullptr;                  // n
+  double* est = nullptr;                  // n, in original id order
   double* block_sums = nullptr;           // blocks
   double* log_table = nullptr;            // m + 1
   uint64_t* partials = nullptr;           // hub chunks * pitch
@@ -237,6 +237,13 @@ struct hanf_engine {
   unsigned long long* reduce_counts = nullptr;
   int gather_mode = -1;       // union kernel variant (-1: per-layout default)
   bool tma = false;           // gather successor rows with TMA gather4
+  // locality relabelling (hanf_relabel.cu): the device works on rows;
+  // order[row] = original id, perm[id] = row; dirty[g] = original-id
+  // bitmaps of changed counters for the block sums (mod[g] is in rows)
+  bool relabel = false;
+  uint32_t* order = nullptr;
+  uint32_t* perm = nullptr;
+  uint64_t* dirty[2] = {nullptr, nullptr};
   CUtensorMap tmap[2];        // descriptors of cnt[0], cnt[1]
 
   hanf::ReduceOut* h_reduce = nullptr;  // pinned (cache): total + count
@@ -310,6 +317,10 @@ struct hanf_engine {
       pfree(work, stream);
       pfree(hub_tasks, stream);
       pfree(hub_index, stream);
+      pfree(order, stream);
+      pfree(perm, stream);
+      pfree(dirty[0], stream);
+      pfree(dirty[1], stream);
       pfree(lens, stream);
       hanf::free_tasks_device(&tasks, stream);
       if (cudaStreamSynchronize(stream) == cudaSuccess)
@@ -324,6 +335,29 @@ struct hanf_engine {
 };
 
 namespace {
+
+// Do the graph's ids carry locality?  Median |u - w| over the middle
+// successor of up to 4096 evenly spaced nodes, against n/64: the copying
+// model's windows (+-2^12 of 2^24) pass, permuted R-MAT / BA ids do not.
+bool ids_local(const hanf_graph_view* g) {
+  const uint64_t n = g->n;
+  std::vector<uint64_t> d;
+  d.reserve(4096);
+  const uint64_t step = n > 4096 ? n / 4096 : 1;
+  for (uint64_t u = 0; u < n && d.size() < 4096; u += step) {
+    const uint64_t a = g->offsets[u], b = g->offsets[u + 1];
+    if (b <= a || b > g->num_arcs) continue;  // (malformed rows are rejected later)
+    const uint64_t w = g->arcs[a + (b - a) / 2];
+    d.push_back(w > u ? w - u : u - w);
+  }
+  if (d.empty()) return true;
+  std::nth_element(d.begin(), d.begin() + d.size() / 2, d.end());
+  return d[d.size() / 2] < n / 64;
+}
+
+// Bitmap of the counters changed into generation g, in original ids (what
+// the block sums and the modified count read).
+uint64_t* dirty_of(const hanf_engine* e, int g) { return e->relabel ? e->dirty[g] : e->mod[g]; }
 
 // Recomputes estimates of the counters flagged in `dirty` (all when null)
 // for blocks [b0, b1) of generation g.
@@ -342,6 +376,7 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
   a.register_bits = e->params.register_bits;
   a.pitch = static_cast<uint32_t>(e->pitch);
   a.log_table = e->log_table;
+  a.row_of = e->perm;  // blocks are original ids; counters are read from their rows
   HANF_CUDA(hanf::launch_estimate(a, e->stream, &e->launches));
   return HANF_OK;
 }
@@ -412,14 +447,19 @@ hanf_status seed_all(hanf_engine* e) {
   HANF_CUDA(hanf::launch_seed(e->cnt[0], e->cnt[1], e->mod[0], e->n, 0, e->n,
                               e->params.bucket_bits, e->params.register_bits,
                               e->params.words_per_counter, static_cast<uint32_t>(e->pitch),
-                              e->params.seed, e->stream,
+                              e->params.seed, e->order, e->stream,
                               &e->launches));
   HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
+  if (e->relabel) {  // every counter was seeded: all ones in both id spaces
+    HANF_CUDA(cudaMemcpyAsync(e->dirty[0], e->mod[0], sizeof(uint64_t) * e->blocks,
+                              cudaMemcpyDeviceToDevice, e->stream));
+    HANF_CUDA(cudaMemsetAsync(e->dirty[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
+  }
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
   if (st != HANF_OK) return st;
   uint64_t count = 0;
   e->last_count = e->n;
-  return finish(e, e->mod[0], false, 0, 0, &e->last_sum, &count);
+  return finish(e, dirty_of(e, 0), false, 0, 0, &e->last_sum, &count);
 }
 
 hanf_status validate_config(const hanf_config* cfg) {
@@ -496,6 +536,8 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.hub_ticket = e->tasks.hub_ticket;
   a.pitch = static_cast<uint32_t>(e->pitch);
   a.stale_valid = e->stale_valid ? 1 : 0;
+  a.orig_of = e->order;
+  a.dirty_next = e->relabel ? e->dirty[ng] : nullptr;
   return a;
 }
 
@@ -524,6 +566,8 @@ hanf_status compute_sparse(hanf_engine* e) {
   a.hub_tasks = e->hub_tasks;
   a.lens = e->lens;
   a.hub_index = e->hub_index;
+  a.orig_of = e->order;
+  a.dirty_next = e->relabel ? e->dirty[ng] : nullptr;
   a.hub_first = e->tasks.hub_first;
   a.hub_count = e->tasks.hub_count;
   a.n = e->n;
@@ -549,6 +593,8 @@ hanf_status compute_local(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
   HANF_CUDA(cudaMemsetAsync(e->mod[ng] + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
+  if (e->relabel)  // unsharded: the whole original-id bitmap
+    HANF_CUDA(cudaMemsetAsync(e->dirty[ng], 0, sizeof(uint64_t) * e->blocks, e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
   if (step_mode(e) == 2 && e->tr_off) {
     const hanf_status st = compute_sparse(e);
@@ -571,7 +617,7 @@ hanf_status compute_local(hanf_engine* e) {
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
   const bool sharded = e->lo != 0 || e->hi != e->n;
   if (!fused) {
-    const hanf_status st = run_estimates(e, ng, e->mod[ng], w0, w1);
+    const hanf_status st = run_estimates(e, ng, dirty_of(e, ng), w0, w1);
     if (st != HANF_OK) return st;
   } else if (sharded) {
     // block sums of this shard now: they are exchanged before commit
@@ -590,7 +636,7 @@ bool commit_recomputes(const hanf_engine* e) {
 
 hanf_status commit_enqueue(hanf_engine* e) {
   const int ng = 1 - e->cur;
-  return finish_enqueue(e, e->mod[ng], commit_recomputes(e), 0, e->blocks, true);
+  return finish_enqueue(e, dirty_of(e, ng), commit_recomputes(e), 0, e->blocks, true);
 }
 
 hanf_status commit_complete(hanf_engine* e, hanf_iteration_report* rep) {
@@ -745,6 +791,18 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
     }
   }
 
+  // Locality relabelling (hanf_relabel.cu), unsharded engines only:
+  // HANF_RELABEL=1/0 forces it; by default graphs whose counters do not fit
+  // in L2 (one generation > 64 MB) and whose ids show no locality (sampled
+  // successors far from their source) are renumbered by degree.
+  if (lo == 0 && hi == n && n > 0) {
+    const char* rl = std::getenv("HANF_RELABEL");
+    if (rl && (rl[0] == '0' || rl[0] == '1'))
+      e->relabel = rl[0] == '1';
+    else
+      e->relabel = (n + 1) * e->pitch * 8 > (64ull << 20) && !ids_local(g);
+  }
+
   auto bail = [&](hanf_status s) {
     const std::string msg = g_last_error;
     delete e;
@@ -863,6 +921,27 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
                                cudaMemcpyHostToDevice, s2));
     HANF_TRY(cudaEventRecord(ev_arcs, s2));
     phase("offsets");
+    if (e->relabel) {
+      // renumber rows by degree (needs the arcs; the seed needs the order)
+      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+      hanf::RelabelOut r;
+      const cudaError_t re = hanf::relabel_device(d_off, d_succ, n, a1 - a0, s, &r, &e->launches);
+      cudaFreeAsync(d_off, s);  // the caller-order CSR is not needed any more
+      cudaFreeAsync(d_succ, s);
+      d_off = r.off;
+      d_succ = r.succ;
+      e->order = r.order;
+      e->perm = r.perm;
+      e->csr_off = d_off;  // owned by the engine from here on
+      e->csr_succ = d_succ;
+      HANF_TRY(re);
+      if (r.bad)
+        return bail(fail(HANF_INVALID_ARGUMENT,
+                         "arc endpoint out of range or offsets not non-decreasing"));
+      HANF_TRY(palloc(&e->dirty[0], e->blocks, s));
+      HANF_TRY(palloc(&e->dirty[1], e->blocks, s));
+      phase("relabel");
+    }
     st = seed_all(e);
     if (st != HANF_OK) return bail(st);
     phase("seed");
@@ -1032,6 +1111,22 @@ hanf_status hanf_read_counters(hanf_engine* e, uint64_t first, uint64_t count, u
   if (count == 0) return HANF_OK;
   if (!dst) return fail(HANF_INVALID_ARGUMENT, "null destination");
   HANF_CUDA(cudaSetDevice(e->device));
+  if (e->relabel) {
+    // counter of original id first + i lives in row perm[first + i]
+    uint64_t* tmp = nullptr;
+    HANF_CUDA(palloc(&tmp, count * e->words, e->stream));
+    cudaError_t ce = hanf::launch_gather_rows(e->cnt[e->cur], e->perm, first, count,
+                                              static_cast<uint32_t>(e->pitch),
+                                              static_cast<uint32_t>(e->words), tmp, e->stream,
+                                              &e->launches);
+    if (ce == cudaSuccess)
+      ce = cudaMemcpyAsync(dst, tmp, sizeof(uint64_t) * count * e->words, cudaMemcpyDeviceToHost,
+                           e->stream);
+    cudaFreeAsync(tmp, e->stream);
+    HANF_CUDA(ce);
+    HANF_CUDA(cudaStreamSynchronize(e->stream));
+    return HANF_OK;
+  }
   // rows are `pitch` words apart on the device, W apart in the reference
   // packing the caller expects
   HANF_CUDA(cudaMemcpy2DAsync(dst, sizeof(uint64_t) * e->words, e->cnt[e->cur] + first * e->pitch,

@@ -51,6 +51,24 @@ cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, ui
                                uint64_t* launches);
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
+// Locality relabelling (hanf_relabel.cu): rows renumbered by descending
+// total degree; order[row] = original id, perm[id] = row; off/succ = the
+// relabelled CSR (pool allocations, caller frees).  bad = malformed input.
+struct RelabelOut {
+  uint32_t* order = nullptr;
+  uint32_t* perm = nullptr;
+  uint64_t* off = nullptr;
+  uint32_t* succ = nullptr;
+  int bad = 0;
+};
+cudaError_t relabel_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n, uint64_t arcs,
+                           cudaStream_t s, RelabelOut* out, uint64_t* launches);
+// rows perm[first + i] (or first + i) of `counters`, W words each, packed
+// densely into dst (device)
+cudaError_t launch_gather_rows(const uint64_t* counters, const uint32_t* perm, uint64_t first,
+                               uint64_t count, uint32_t pitch, uint32_t words, uint64_t* dst,
+                               cudaStream_t s, uint64_t* launches);
+
 // Worklist ("systolic") step, hanf_sparse.cu.
 struct SparseArgs {
   const uint64_t* off;        // shard CSR offsets (index v - node_base)
@@ -72,6 +90,8 @@ struct SparseArgs {
   uint32_t* hub_tasks;        // scratch: chunk tasks of worklist hubs (dense kernel)
   unsigned int* lens;         // [0] modified chunks, [1] worklist, [2] hub tasks
   const unsigned int* work_len;
+  const uint32_t* orig_of;    // row -> original id (for dirty_next)
+  uint64_t* dirty_next;       // original-id bitmap of changed counters (nullptr: = mod_next)
   const uint32_t* hub_index;  // node -> hub (UINT32_MAX: not a hub)
   const uint32_t* hub_first;  // per hub: first chunk task, chunk count
   const uint32_t* hub_count;
@@ -113,6 +133,8 @@ struct UnionArgs {
   int32_t stale_valid;       // next[v] may be stale where mod_cur[v] is set
   double* est;               // per-counter estimates (nullptr: not fused)
   EstimateParams ep;
+  const uint32_t* orig_of;         // row -> original id (for dirty_next)
+  uint64_t* dirty_next;            // original-id bitmap of changed counters (nullptr: = mod_next)
   const uint32_t* task_list;       // non-null: run only these task indices
   const unsigned int* task_count;  // (device) length of task_list
 };
@@ -132,13 +154,14 @@ struct EstimateArgs {
   uint32_t register_bits;
   uint32_t pitch;            // row pitch in u64 words
   const double* log_table;
+  const uint32_t* row_of;    // original id -> row (nullptr: identity labels)
 };
 
 // Launchers (hanf_kernels.cu).  All are stream-ordered and asynchronous.
 cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
                         uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
-                        cudaStream_t s, uint64_t* launches);
+                        const uint32_t* orig_of, cudaStream_t s, uint64_t* launches);
 // map: TMA descriptor of args.cur for the gather4 kernel (nullptr: LDG
 // gathers; only single-chunk layouts with an even pitch take it)
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits,

@@ -35,11 +35,14 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // hash.hpp:8-
 __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
                             uint64_t* __restrict__ mod, uint64_t n, uint64_t node_begin,
                             uint64_t node_end, uint32_t bucket_bits, uint32_t register_bits,
-                            uint32_t words, uint32_t pitch, uint64_t seed_mix) {
+                            uint32_t words, uint32_t pitch, uint64_t seed_mix,
+                            const uint32_t* __restrict__ orig_of) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = node_begin + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
        v < node_end; v += stride) {
-    const uint64_t h = mix64(v ^ seed_mix);  // item_hash, hash.hpp:20-22
+    // counter_add(v, v): the item is the node's original id (hash.hpp:20-22)
+    const uint64_t item = orig_of ? orig_of[v] : v;
+    const uint64_t h = mix64(item ^ seed_mix);
     const uint32_t bucket = static_cast<uint32_t>(h >> (64 - bucket_bits));
     const uint64_t rest = h << bucket_bits;
     uint32_t rho = rest == 0 ? (64 - bucket_bits) + 1 : __clzll(rest) + 1;
@@ -73,7 +76,7 @@ __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
 cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
                         uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
-                        cudaStream_t s, uint64_t* launches) {
+                        const uint32_t* orig_of, cudaStream_t s, uint64_t* launches) {
   if (node_end <= node_begin) return cudaSuccess;
   const uint64_t items = node_end - node_begin;
   const uint32_t threads = 256;
@@ -81,7 +84,7 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
   if (blocks > 148ull * 64) blocks = 148ull * 64;
   seed_kernel<<<static_cast<uint32_t>(blocks), threads, 0, s>>>(
       a, b, mod, n, node_begin, node_end, bucket_bits, register_bits, words, pitch,
-      mix64(seed ^ 0x9e3779b97f4a7c15ULL));
+      mix64(seed ^ 0x9e3779b97f4a7c15ULL), orig_of);
   ++*launches;
   return cudaGetLastError();
 }
@@ -205,6 +208,21 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   return v;
 }
 
+// Records that counter row v changed: its bit in the row-space bitmap (skips
+// and worklist) and, under relabelling, in the original-id bitmap the block
+// sums and counts use.
+__device__ __forceinline__ uint32_t est_slot(const uint32_t* orig_of, uint32_t v) {
+  return orig_of ? orig_of[v] : v;
+}
+__device__ __forceinline__ void mark_changed(uint64_t* mod_next, uint64_t* dirty_next,
+                                             const uint32_t* orig_of, uint32_t v) {
+  atomicOr(reinterpret_cast<unsigned long long*>(mod_next) + (v >> 6), 1ull << (v & 63));
+  if (dirty_next) {
+    const uint32_t o = orig_of[v];
+    atomicOr(reinterpret_cast<unsigned long long*>(dirty_next) + (o >> 6), 1ull << (o & 63));
+  }
+}
+
 // Max over a split node's chunk partials and its own counter (one warp),
 // then the usual commit.  Partials were written by other warps of the same
 // launch: read through L2 (ld.cg) after the ticket handshake.
@@ -239,12 +257,10 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
       any_changed |= changed;
       if (changed || stale)
         store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
-      if (changed && args.est) args.est[v] = estimate_limbs<Lay>(acc, args.ep);
+      if (changed && args.est) args.est[est_slot(args.orig_of, v)] = estimate_limbs<Lay>(acc, args.ep);
     }
   }
-  if (lane == 0 && any_changed)
-    atomicOr(reinterpret_cast<unsigned long long*>(args.mod_next) + (v >> 6),
-             1ull << (v & 63));
+  if (lane == 0 && any_changed) mark_changed(args.mod_next, args.dirty_next, args.orig_of, v);
 }
 
 // Folds the G lanes of each node, then either stores a hub chunk's partial
@@ -271,7 +287,7 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
     any_changed |= changed;
     if (changed || (lead && stale))
       store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
-    if (changed && args.est) args.est[v] = estimate_limbs<Lay>(acc, args.ep);
+    if (changed && args.est) args.est[est_slot(args.orig_of, v)] = estimate_limbs<Lay>(acc, args.ep);
   }
 }
 
@@ -280,9 +296,7 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
 template <class Lay, bool kVec16>
 __device__ __forceinline__ void task_finish(const UnionArgs& args, const WarpTask& task, bool hub,
                                             uint32_t v, bool any_changed, uint32_t lane) {
-  if (any_changed)
-    atomicOr(reinterpret_cast<unsigned long long*>(args.mod_next) + (v >> 6),
-             1ull << (v & 63));
+  if (any_changed) mark_changed(args.mod_next, args.dirty_next, args.orig_of, v);
   if (hub) {
     const uint32_t h = args.chunk_hub[task.item];
     uint32_t last = 0;
@@ -704,10 +718,11 @@ __global__ void __launch_bounds__(64) estimate_kernel(const EstimateArgs args) {
   double e = 0.0;
   if (v < args.n) {
     if ((word >> t) & 1) {
+      const uint64_t row = args.row_of ? args.row_of[v] : v;  // v is an original id
       if constexpr (M > 0)
-        e = estimate_counter_r5<M>(args.counters + v * args.pitch, p);
+        e = estimate_counter_r5<M>(args.counters + row * args.pitch, p);
       else
-        e = estimate_counter_generic(args.counters + v * args.pitch, p);
+        e = estimate_counter_generic(args.counters + row * args.pitch, p);
       args.est[v] = e;
     } else {
       e = args.est[v];
@@ -852,6 +867,32 @@ cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launche
   if (a.blocks == 0) return cudaSuccess;
   const uint64_t ctas = (a.blocks + kFinishThreads - 1) / kFinishThreads;
   finish_kernel<<<static_cast<uint32_t>(ctas), kFinishThreads, 0, s>>>(a);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// Counter read-back under relabelling: row perm[first + i] -> dst row i.
+__global__ void gather_rows_kernel(const uint64_t* __restrict__ counters,
+                                   const uint32_t* __restrict__ perm, uint64_t first,
+                                   uint64_t count, uint32_t pitch, uint32_t words,
+                                   uint64_t* __restrict__ dst) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+       k < count * words; k += stride) {
+    const uint64_t i = k / words, w = k % words;
+    const uint64_t row = perm ? perm[first + i] : first + i;
+    dst[k] = counters[row * pitch + w];
+  }
+}
+
+cudaError_t launch_gather_rows(const uint64_t* counters, const uint32_t* perm, uint64_t first,
+                               uint64_t count, uint32_t pitch, uint32_t words, uint64_t* dst,
+                               cudaStream_t s, uint64_t* launches) {
+  if (count == 0) return cudaSuccess;
+  uint64_t blocks = (count * words + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  gather_rows_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(counters, perm, first, count,
+                                                                   pitch, words, dst);
   ++*launches;
   return cudaGetLastError();
 }

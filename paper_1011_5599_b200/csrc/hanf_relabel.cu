@@ -1,0 +1,224 @@
+// hanf_relabel.cu -- locality relabelling of the graph on the device
+// (engine-internal layout; results are bit-identical to the reference).
+//
+// Gathers dominate the union sweep, and a node's counter is gathered once
+// per in-arc.  On graphs whose ids carry no locality (R-MAT / BA with
+// permuted ids) the hot counters are scattered one per 128-byte line.
+// Renumbering nodes by descending total degree packs the hot counters
+// together (profiles/r01_relabel.md).  Graphs whose ids are already local
+// (the copying model's windows) keep their labels: hanf_engine.cu decides
+// with a sampled locality test.
+//
+// The engine works on the relabelled CSR in "row" space (counters and the
+// modified bitmaps the skips and the worklist read); everything the caller
+// sees stays in the original id space:
+//   order[row] = original id   (seed hash input; a changed row writes its
+//                               estimate to est[order[row]] and sets its
+//                               bit in the original-id dirty bitmap)
+//   perm[id]   = row           (counter read-back; the estimate kernel of
+//                               multi-chunk layouts reads row perm[id])
+// so N(t) is still summed over original-id blocks in the reference order.
+// Scattering the estimates at update time beat gathering them at sum time
+// (finish_kernel 13 -> 50 us on config 2 with the gather).
+//
+// Relabelling pays where the counters do not fit in L2 (measured 2.4x on
+// R-MAT 26, 1.25x on BA 2^25).  On the L2-resident config 2 it gains 5% on
+// the union sweep but costs ~1 ms at create (the seed and task build can no
+// longer overlap the upload), so it is off there by default.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cstdint>
+
+#include "hanf_internal.h"
+
+namespace hanf {
+namespace {
+
+__global__ void indegree_kernel(const uint32_t* __restrict__ succ, uint64_t arcs, uint64_t n,
+                                uint32_t* __restrict__ indeg, int* __restrict__ bad) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  bool oob = false;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < arcs;
+       i += stride) {
+    const uint32_t w = succ[i];
+    if (w < n)
+      atomicAdd(indeg + w, 1u);
+    else
+      oob = true;
+  }
+  if (oob) *bad = 1;
+}
+
+// keys = ~(out-degree + in-degree): descending total degree, stable in id
+__global__ void score_keys_kernel(const uint64_t* __restrict__ off, uint64_t n,
+                                  const uint32_t* __restrict__ indeg, uint32_t* __restrict__ keys,
+                                  uint32_t* __restrict__ vals, int* __restrict__ bad) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < n;
+       v += stride) {
+    const uint64_t a = off[v], b = off[v + 1];
+    uint64_t d = 0;
+    if (b < a)
+      *bad = 1;
+    else
+      d = b - a;
+    const uint64_t score = d + indeg[v];
+    keys[v] = ~static_cast<uint32_t>(score < 0xffffffffull ? score : 0xffffffffull);
+    vals[v] = static_cast<uint32_t>(v);
+  }
+}
+
+// perm[order[r]] = r; new degree of row r (for the offsets scan)
+__global__ void invert_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ order,
+                              uint64_t n, uint32_t* __restrict__ perm, uint64_t* __restrict__ ndeg) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r <= n;
+       r += stride) {
+    if (r == n) {
+      ndeg[n] = 0;
+      continue;
+    }
+    const uint32_t v = order[r];
+    perm[v] = static_cast<uint32_t>(r);
+    const uint64_t a = off[v], b = off[v + 1];
+    ndeg[r] = b >= a ? b - a : 0;
+  }
+}
+
+// Arc-parallel rewrite: warp w owns old arcs [w*1024, (w+1)*1024), lane l
+// arcs base + l + 32j.  Each lane finds its first arc's source row by
+// binary search and then walks forward, so hub rows cost no more than any
+// other 1024 arcs.  Arc i of node u lands at noff[perm[u]] + (i - off[u])
+// as perm[succ[i]].
+__global__ void rewrite_arcs_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ succ,
+                                    uint64_t n, uint64_t arcs, const uint32_t* __restrict__ perm,
+                                    const uint64_t* __restrict__ noff, uint32_t* __restrict__ out) {
+  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t wb = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+       wb * 1024 < arcs; wb += warps) {
+    const uint64_t first = wb * 1024 + lane;
+    if (first >= arcs) continue;
+    // last u with off[u] <= first
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) / 2;
+      if (off[mid] <= first) lo = mid; else hi = mid - 1;
+    }
+    uint64_t u = lo;
+    uint64_t dst_base = 0, src_base = 0;
+    bool have = false;
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint64_t i = first + 32ull * j;
+      if (i >= arcs) break;
+      bool moved = !have;
+      while (u < n && off[u + 1] <= i) {
+        ++u;
+        moved = true;
+      }
+      if (u >= n) break;  // malformed offsets (flagged by score_keys_kernel)
+      if (moved) {
+        src_base = off[u];
+        dst_base = noff[perm[u]];
+        have = true;
+      }
+      const uint64_t pos = dst_base + (i - src_base);
+      const uint32_t w = succ[i];
+      if (pos < arcs) out[pos] = w < n ? perm[w] : 0u;
+    }
+  }
+}
+
+template <class T>
+cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), s);
+}
+
+}  // namespace
+
+#define HANF_RELABEL_TRY(expr)          \
+  do {                                  \
+    const cudaError_t _e = (expr);      \
+    if (_e != cudaSuccess) return _e;   \
+  } while (0)
+
+cudaError_t relabel_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n, uint64_t arcs,
+                           cudaStream_t s, RelabelOut* out, uint64_t* launches) {
+  *out = RelabelOut{};
+  if (n == 0) return cudaSuccess;
+  const uint32_t threads = 256;
+  auto grid = [](uint64_t items) {
+    const uint64_t b = (items + 255) / 256;
+    return static_cast<uint32_t>(b < 148ull * 32 ? (b ? b : 1) : 148ull * 32);
+  };
+  uint32_t *indeg = nullptr, *keys = nullptr, *vals = nullptr, *skeys = nullptr;
+  int* d_bad = nullptr;
+  uint64_t* ndeg = nullptr;
+  HANF_RELABEL_TRY(pool_alloc(&indeg, n, s));
+  HANF_RELABEL_TRY(pool_alloc(&d_bad, 1, s));
+  HANF_RELABEL_TRY(cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * n, s));
+  HANF_RELABEL_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+  if (arcs) {
+    indegree_kernel<<<grid(arcs), threads, 0, s>>>(d_succ, arcs, n, indeg, d_bad);
+    ++*launches;
+  }
+  HANF_RELABEL_TRY(pool_alloc(&keys, n, s));
+  HANF_RELABEL_TRY(pool_alloc(&vals, n, s));
+  score_keys_kernel<<<grid(n), threads, 0, s>>>(d_off, n, indeg, keys, vals, d_bad);
+  ++*launches;
+  HANF_RELABEL_TRY(cudaFreeAsync(indeg, s));
+  HANF_RELABEL_TRY(pool_alloc(&skeys, n, s));
+  HANF_RELABEL_TRY(pool_alloc(&out->order, n, s));
+  {
+    size_t tb = 0;
+    HANF_RELABEL_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, skeys, vals, out->order,
+                                                     static_cast<int64_t>(n), 0, 32, s));
+    void* temp = nullptr;
+    HANF_RELABEL_TRY(cudaMallocAsync(&temp, tb ? tb : 1, s));
+    HANF_RELABEL_TRY(cub::DeviceRadixSort::SortPairs(temp, tb, keys, skeys, vals, out->order,
+                                                     static_cast<int64_t>(n), 0, 32, s));
+    ++*launches;
+    HANF_RELABEL_TRY(cudaFreeAsync(temp, s));
+  }
+  HANF_RELABEL_TRY(cudaFreeAsync(keys, s));
+  HANF_RELABEL_TRY(cudaFreeAsync(vals, s));
+  HANF_RELABEL_TRY(cudaFreeAsync(skeys, s));
+  HANF_RELABEL_TRY(pool_alloc(&out->perm, n, s));
+  HANF_RELABEL_TRY(pool_alloc(&ndeg, n + 1, s));
+  invert_kernel<<<grid(n + 1), threads, 0, s>>>(d_off, out->order, n, out->perm, ndeg);
+  ++*launches;
+  HANF_RELABEL_TRY(pool_alloc(&out->off, n + 1, s));
+  {
+    size_t tb = 0;
+    HANF_RELABEL_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, ndeg, out->off,
+                                                   static_cast<int64_t>(n + 1), s));
+    void* temp = nullptr;
+    HANF_RELABEL_TRY(cudaMallocAsync(&temp, tb ? tb : 1, s));
+    HANF_RELABEL_TRY(cub::DeviceScan::ExclusiveSum(temp, tb, ndeg, out->off,
+                                                   static_cast<int64_t>(n + 1), s));
+    ++*launches;
+    HANF_RELABEL_TRY(cudaFreeAsync(temp, s));
+  }
+  HANF_RELABEL_TRY(cudaFreeAsync(ndeg, s));
+  HANF_RELABEL_TRY(pool_alloc(&out->succ, arcs, s));
+  if (arcs) {
+    const uint64_t blocks = (arcs + 1023) / 1024;  // warp blocks of 1024 arcs
+    uint64_t ctas = (blocks + 7) / 8;
+    if (ctas > 148ull * 16) ctas = 148ull * 16;
+    rewrite_arcs_kernel<<<static_cast<uint32_t>(ctas), threads, 0, s>>>(d_off, d_succ, n, arcs,
+                                                                       out->perm, out->off,
+                                                                       out->succ);
+    ++*launches;
+  }
+  int h_bad = 0;
+  HANF_RELABEL_TRY(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HANF_RELABEL_TRY(cudaFreeAsync(d_bad, s));
+  HANF_RELABEL_TRY(cudaStreamSynchronize(s));
+  out->bad = h_bad;
+  return cudaGetLastError();
+}
+
+}  // namespace hanf

@@ -200,8 +200,12 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
       const bool stale = (a.mod_cur[v >> 6] >> (v & 63)) & 1;
       if (changed || stale) store_chunk<Lay, kVec16>(a.next + static_cast<uint64_t>(v) * words, acc);
       if (changed) {
-        a.est[v] = estimate_limbs<Lay>(acc, a.ep);
+        a.est[a.orig_of ? a.orig_of[v] : v] = estimate_limbs<Lay>(acc, a.ep);
         atomicOr(reinterpret_cast<unsigned long long*>(a.mod_next) + (v >> 6), 1ull << (v & 63));
+        if (a.dirty_next) {
+          const uint32_t o = a.orig_of[v];
+          atomicOr(reinterpret_cast<unsigned long long*>(a.dirty_next) + (o >> 6), 1ull << (o & 63));
+        }
       }
     }
   }

@@ -367,7 +367,9 @@ def test_worklist_step_parity(hanf, port, monkeypatch):
 @pytest.mark.parametrize("env", [{"HANF_PITCH": "1"}, {"HANF_PITCH": "0"},
                                  {"HANF_GATHER": "22"}, {"HANF_GATHER": "2"},
                                  {"HANF_PITCH": "1", "HANF_GATHER": "30"},
-                                 {"HANF_TMA": "1"}, {"HANF_TMA": "1", "HANF_GATHER": "40"}])
+                                 {"HANF_TMA": "1"}, {"HANF_TMA": "1", "HANF_GATHER": "40"},
+                                 {"HANF_RELABEL": "1"}, {"HANF_RELABEL": "1", "HANF_SPARSE": "1"},
+                                 {"HANF_RELABEL": "1", "HANF_PITCH": "0"}])
 def test_row_pitch_and_gather_variants(hanf, port, monkeypatch, env):
     """Padded rows (aligned 256-bit gathers), unpadded rows and the
     alternative gather kernels change time only: counters read back in the
@@ -391,3 +393,28 @@ def test_pinned_graph_upload(hanf):
     assert list(a.values) == list(b.values) and list(a.modified) == list(b.modified)
     with pytest.raises(Exception):
         hanf._lib.check(hanf._lib.lib().hanf_pin_host(None, 8))
+
+
+@pytest.mark.parametrize("idx", range(28))
+def test_golden_trace_relabelled(hanf, traces, idx, monkeypatch):
+    """Degree relabelling is an internal layout: every golden iteration,
+    counter read-back and N(t) bit is unchanged (HANF_RELABEL=1 forces it
+    on graphs the default heuristic leaves alone)."""
+    monkeypatch.setenv("HANF_RELABEL", "1")
+    test_golden_trace(hanf, traces, idx)
+
+
+def test_relabel_multichunk_and_readback(hanf, port, monkeypatch):
+    """Relabelled multi-chunk layouts (separate estimate kernel over
+    original-id blocks) and partial counter read-back ranges."""
+    monkeypatch.setenv("HANF_RELABEL", "1")
+    g = hanf.gen_rmat(11, 8, 0.57, 0.19, 0.19, 8, 1)
+    for b, r in [(8, 5), (9, 5), (7, 6), (8, 7), (6, 8)]:
+        lockstep(hanf, port, g, bucket_bits=b, register_bits=r, seed=5, max_steps=4)
+    with hanf.NfEngine(g, hanf.EngineConfig(bucket_bits=6, seed=5)) as e:
+        e.step()
+        full = e.counters()
+        W = e.params().words
+        for first, count in [(0, 1), (17, 33), (g.num_nodes() - 5, 5)]:
+            part = e.counters(first, count)
+            assert np.array_equal(part, full[first * W:(first + count) * W])
