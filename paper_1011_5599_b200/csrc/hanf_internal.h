@@ -52,7 +52,7 @@ cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, ui
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
 // Locality relabelling (hanf_relabel.cu): rows renumbered by descending
-// total degree; order[row] = original id, perm[id] = row; off/succ = the
+// out-degree; order[row] = original id, perm[id] = row; off/succ = the
 // relabelled CSR (pool allocations, caller frees).  bad = malformed input.
 struct RelabelOut {
   uint32_t* order = nullptr;

@@ -4,7 +4,7 @@
 // Gathers dominate the union sweep, and a node's counter is gathered once
 // per in-arc.  On graphs whose ids carry no locality (R-MAT / BA with
 // permuted ids) the hot counters are scattered one per 128-byte line.
-// Renumbering nodes by descending total degree packs the hot counters
+// Renumbering nodes by descending out-degree packs the hot counters
 // together (profiles/r01_relabel.md).  Graphs whose ids are already local
 // (the copying model's windows) keep their labels: hanf_engine.cu decides
 // with a sampled locality test.
@@ -40,25 +40,13 @@
 namespace hanf {
 namespace {
 
-__global__ void indegree_kernel(const uint32_t* __restrict__ succ, uint64_t arcs, uint64_t n,
-                                uint32_t* __restrict__ indeg, int* __restrict__ bad) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  bool oob = false;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < arcs;
-       i += stride) {
-    const uint32_t w = succ[i];
-    if (w < n)
-      atomicAdd(indeg + w, 1u);
-    else
-      oob = true;
-  }
-  if (oob) *bad = 1;
-}
-
-// keys = ~(out-degree + in-degree): descending total degree, stable in id
+// keys = ~out-degree: descending out-degree, stable in id.  (Total degree
+// needs an in-degree pass of contended atomics - 160 ms on R-MAT 28 - and
+// measured no better: R-MAT's and BA's in- and out-degrees go together, and
+// rows in out-degree order make the union's task order match the row order.)
 __global__ void score_keys_kernel(const uint64_t* __restrict__ off, uint64_t n,
-                                  const uint32_t* __restrict__ indeg, uint32_t* __restrict__ keys,
-                                  uint32_t* __restrict__ vals, int* __restrict__ bad) {
+                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                  int* __restrict__ bad) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < n;
        v += stride) {
@@ -68,8 +56,7 @@ __global__ void score_keys_kernel(const uint64_t* __restrict__ off, uint64_t n,
       *bad = 1;
     else
       d = b - a;
-    const uint64_t score = d + indeg[v];
-    keys[v] = ~static_cast<uint32_t>(score < 0xffffffffull ? score : 0xffffffffull);
+    keys[v] = ~static_cast<uint32_t>(d < 0xffffffffull ? d : 0xffffffffull);
     vals[v] = static_cast<uint32_t>(v);
   }
 }
@@ -103,9 +90,11 @@ __global__ void invert_kernel(const uint64_t* __restrict__ off, const uint32_t* 
 __global__ void rewrite_arcs_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ succ,
                                     uint64_t n, uint64_t arcs, const uint32_t* __restrict__ order,
                                     const uint32_t* __restrict__ perm,
-                                    const uint64_t* __restrict__ noff, uint32_t* __restrict__ out) {
+                                    const uint64_t* __restrict__ noff, uint32_t* __restrict__ out,
+                                    int* __restrict__ bad) {
   const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  bool oob = false;
   for (uint64_t wb = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
        wb * 1024 < arcs; wb += warps) {
     const uint64_t base = wb * 1024;
@@ -128,7 +117,10 @@ __global__ void rewrite_arcs_kernel(const uint64_t* __restrict__ off, const uint
         if (r < n) {  // else malformed offsets (flagged by score_keys_kernel)
           const uint64_t src = off[order[r]] + (i - noff[r]);
           const uint32_t w = src < arcs ? succ[src] : 0xffffffffu;
-          val = w < n ? perm[w] : 0u;
+          if (w < n)
+            val = perm[w];
+          else
+            oob = true;
         }
         out[i] = val;
       }
@@ -136,6 +128,7 @@ __global__ void rewrite_arcs_kernel(const uint64_t* __restrict__ off, const uint
       if (base + 32ull * (j + 1) >= arcs) break;
     }
   }
+  if (oob) *bad = 1;  // arc endpoint >= n
 }
 
 template <class T>
@@ -173,23 +166,15 @@ cudaError_t relabel_device(const uint64_t* d_off, const uint32_t* d_succ, uint64
     const uint64_t b = (items + 255) / 256;
     return static_cast<uint32_t>(b < 148ull * 32 ? (b ? b : 1) : 148ull * 32);
   };
-  uint32_t *indeg = nullptr, *keys = nullptr, *vals = nullptr, *skeys = nullptr;
+  uint32_t *keys = nullptr, *vals = nullptr, *skeys = nullptr;
   int* d_bad = nullptr;
   uint64_t* ndeg = nullptr;
-  HANF_RELABEL_TRY(pool_alloc(&indeg, n, s));
   HANF_RELABEL_TRY(pool_alloc(&d_bad, 1, s));
-  HANF_RELABEL_TRY(cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * n, s));
   HANF_RELABEL_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-  if (arcs) {
-    indegree_kernel<<<grid(arcs), threads, 0, s>>>(d_succ, arcs, n, indeg, d_bad);
-    ++*launches;
-  }
-  phase("indegree");
   HANF_RELABEL_TRY(pool_alloc(&keys, n, s));
   HANF_RELABEL_TRY(pool_alloc(&vals, n, s));
-  score_keys_kernel<<<grid(n), threads, 0, s>>>(d_off, n, indeg, keys, vals, d_bad);
+  score_keys_kernel<<<grid(n), threads, 0, s>>>(d_off, n, keys, vals, d_bad);
   ++*launches;
-  HANF_RELABEL_TRY(cudaFreeAsync(indeg, s));
   HANF_RELABEL_TRY(pool_alloc(&skeys, n, s));
   HANF_RELABEL_TRY(pool_alloc(&out->order, n, s));
   {
@@ -231,7 +216,7 @@ cudaError_t relabel_device(const uint64_t* d_off, const uint32_t* d_succ, uint64
     uint64_t ctas = (blocks + 7) / 8;
     if (ctas > 148ull * 16) ctas = 148ull * 16;
     rewrite_arcs_kernel<<<static_cast<uint32_t>(ctas), threads, 0, s>>>(
-        d_off, d_succ, n, arcs, out->order, out->perm, out->off, out->succ);
+        d_off, d_succ, n, arcs, out->order, out->perm, out->off, out->succ, d_bad);
     ++*launches;
   }
   phase("arcs");
