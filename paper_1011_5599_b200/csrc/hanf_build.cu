@@ -33,14 +33,14 @@ __host__ __device__ __forceinline__ uint32_t log2g_of(uint64_t d) {
 
 // keys = ~deg (descending degree), vals = node; degree-0 nodes get the
 // largest key and sort to the tail.  Counts hubs and degree-0 nodes.
-__global__ void degree_keys_kernel(const uint64_t* __restrict__ off, uint64_t lo, uint64_t count,
+__global__ void degree_keys_kernel(const CsrView g, uint64_t lo, uint64_t count,
                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                    unsigned long long* __restrict__ counters, int* __restrict__ bad) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   unsigned long long hubs = 0, zeros = 0;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += stride) {
-    const uint64_t a = off[i], b = off[i + 1];
+    const uint64_t a = g.begin(lo + i), b = g.end(lo + i);
     if (b < a) {
       *bad = 1;
       keys[i] = 0xffffffffu;
@@ -81,18 +81,18 @@ __global__ void class_bounds_kernel(const uint32_t* __restrict__ sorted_keys, ui
 }
 
 // per-hub chunk counts
-__global__ void hub_chunks_kernel(const uint64_t* __restrict__ off, uint64_t lo,
+__global__ void hub_chunks_kernel(const CsrView g,
                                   const uint32_t* __restrict__ hub_nodes, uint32_t hubs,
                                   uint32_t* __restrict__ chunks) {
   const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h >= hubs) return;
   const uint32_t v = hub_nodes[h];
-  const uint64_t d = off[v - lo + 1] - off[v - lo];
+  const uint64_t d = g.end(v) - g.begin(v);
   chunks[h] = static_cast<uint32_t>((d + kHubChunk - 1) / kHubChunk);
 }
 
 // hub chunk tables + their warp tasks (trips) in task slots [0, C)
-__global__ void hub_tasks_kernel(const uint64_t* __restrict__ off, uint64_t lo,
+__global__ void hub_tasks_kernel(const CsrView g,
                                  const uint32_t* __restrict__ hub_nodes, uint32_t hubs,
                                  const uint32_t* __restrict__ hub_first,
                                  const uint32_t* __restrict__ hub_count,
@@ -102,7 +102,7 @@ __global__ void hub_tasks_kernel(const uint64_t* __restrict__ off, uint64_t lo,
   const uint32_t h = blockIdx.x;
   if (h >= hubs) return;
   const uint32_t v = hub_nodes[h];
-  const uint64_t s = off[v - lo], e = off[v - lo + 1];
+  const uint64_t s = g.begin(v), e = g.end(v);
   for (uint32_t k = threadIdx.x; k < hub_count[h]; k += blockDim.x) {
     const uint32_t c = hub_first[h] + k;
     const uint64_t a = s + static_cast<uint64_t>(k) * kHubChunk;
@@ -125,7 +125,7 @@ struct LightClasses {
   uint64_t total;
 };
 
-__global__ void light_tasks_kernel(const uint64_t* __restrict__ off, uint64_t lo,
+__global__ void light_tasks_kernel(const CsrView g,
                                    const uint32_t* __restrict__ order, LightClasses lc,
                                    uint64_t first_slot, WarpTask* __restrict__ tasks,
                                    uint64_t* __restrict__ trips) {
@@ -139,7 +139,7 @@ __global__ void light_tasks_kernel(const uint64_t* __restrict__ off, uint64_t lo
     const uint64_t rem = lc.item_end[lg] - item;
     const uint32_t nodes = static_cast<uint32_t>(rem < per ? rem : per);
     const uint32_t v = order[item];
-    const uint64_t d = off[v - lo + 1] - off[v - lo];
+    const uint64_t d = g.end(v) - g.begin(v);
     const uint32_t G = 1u << lg;
     const uint16_t t = static_cast<uint16_t>((d + G - 1) / G);
     tasks[first_slot + w] = WarpTask{0, static_cast<uint32_t>(item), t, static_cast<uint8_t>(lg),
@@ -159,8 +159,7 @@ __global__ void set_tos_kernel(WarpTask* __restrict__ tasks, const uint64_t* __r
 // One warp per task writes its TOS rows (padding = zero row) and checks the
 // successor ids it copies.
 __global__ void __launch_bounds__(256)
-fill_tos_kernel(const uint64_t* __restrict__ off, uint64_t lo, const uint32_t* __restrict__ succ,
-                uint64_t succ_base, const uint32_t* __restrict__ order,
+fill_tos_kernel(const CsrView g, const uint32_t* __restrict__ order,
                 const uint64_t* __restrict__ chunk_begin, const uint32_t* __restrict__ chunk_node,
                 const WarpTask* __restrict__ tasks, uint64_t num_tasks, uint32_t n,
                 uint32_t* __restrict__ tos, int* __restrict__ bad) {
@@ -176,10 +175,10 @@ fill_tos_kernel(const uint64_t* __restrict__ off, uint64_t lo, const uint32_t* _
     if (t.nodes == 0) {
       const uint64_t a = chunk_begin[t.item];
       const uint32_t v = chunk_node[t.item];
-      const uint64_t e = off[v - lo + 1];
+      const uint64_t e = g.end(v);
       const uint64_t len = e - a < kHubChunk ? e - a : kHubChunk;
       for (uint32_t k = lane; k < len; k += 32) {
-        const uint32_t id = succ[a + k - succ_base];
+        const uint32_t id = g.id(a + k);
         out_of_range |= id >= n;
         dst[k] = id;
       }
@@ -187,9 +186,9 @@ fill_tos_kernel(const uint64_t* __restrict__ off, uint64_t lo, const uint32_t* _
       const uint32_t G = 1u << t.lg;
       for (uint32_t j = 0; j < t.nodes; ++j) {
         const uint32_t v = order[t.item + j];
-        const uint64_t s = off[v - lo], d = off[v - lo + 1] - s;
+        const uint64_t s = g.begin(v), d = g.end(v) - s;
         for (uint64_t k = lane; k < d; k += 32) {
-          const uint32_t id = succ[s + k - succ_base];
+          const uint32_t id = g.id(s + k);
           out_of_range |= id >= n;
           dst[32 * (k >> t.lg) + j * G + (k & (G - 1))] = id;
         }
@@ -213,10 +212,9 @@ cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
     if (_e != cudaSuccess) return _e;           \
   } while (0)
 
-cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
-                               uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
-                               cudaEvent_t succ_ready, TaskBuild* out, int* bad_input,
-                               uint64_t* launches) {
+cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
+                               cudaStream_t s, cudaEvent_t succ_ready, TaskBuild* out,
+                               int* bad_input, uint64_t* launches) {
   *out = TaskBuild{};
   *bad_input = 0;
   const uint64_t count = hi - lo;
@@ -237,7 +235,7 @@ cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, ui
   HANF_BUILD_TRY(pool_alloc(&d_bad, 1, s));
   HANF_BUILD_TRY(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), s));
   HANF_BUILD_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-  degree_keys_kernel<<<grid(count), threads, 0, s>>>(d_off, lo, count, keys, vals, counters, d_bad);
+  degree_keys_kernel<<<grid(count), threads, 0, s>>>(g, lo, count, keys, vals, counters, d_bad);
   ++*launches;
   HANF_BUILD_TRY(cudaGetLastError());
   size_t temp_bytes = 0;
@@ -295,7 +293,7 @@ cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, ui
     HANF_BUILD_TRY(cudaMemcpyAsync(o.hub_nodes, svals, sizeof(uint32_t) * hubs,
                                    cudaMemcpyDeviceToDevice, s));
     hub_chunks_kernel<<<static_cast<uint32_t>((hubs + 255) / 256), 256, 0, s>>>(
-        d_off, lo, o.hub_nodes, static_cast<uint32_t>(hubs), o.hub_count);
+        g, o.hub_nodes, static_cast<uint32_t>(hubs), o.hub_count);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
   }
@@ -334,13 +332,13 @@ cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, ui
                                    cudaMemcpyDeviceToDevice, s));
   if (hubs) {
     hub_tasks_kernel<<<static_cast<uint32_t>(hubs), 128, 0, s>>>(
-        d_off, lo, o.hub_nodes, static_cast<uint32_t>(hubs), o.hub_first, o.hub_count,
+        g, o.hub_nodes, static_cast<uint32_t>(hubs), o.hub_first, o.hub_count,
         o.chunk_node, o.chunk_hub, chunk_begin, o.wtasks, trips);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
   }
   if (warps) {
-    light_tasks_kernel<<<grid(warps), threads, 0, s>>>(d_off, lo, o.order, lc, chunks, o.wtasks,
+    light_tasks_kernel<<<grid(warps), threads, 0, s>>>(g, o.order, lc, chunks, o.wtasks,
                                                        trips);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
@@ -370,7 +368,7 @@ cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, ui
   if (succ_ready) HANF_BUILD_TRY(cudaStreamWaitEvent(s, succ_ready, 0));
   if (num_tasks) {
     fill_tos_kernel<<<grid(num_tasks * 32), threads, 0, s>>>(
-        d_off, lo, d_succ, succ_base, o.order, chunk_begin, o.chunk_node, o.wtasks, num_tasks,
+        g, o.order, chunk_begin, o.chunk_node, o.wtasks, num_tasks,
         static_cast<uint32_t>(n), o.tos, d_bad);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());

@@ -243,6 +243,7 @@ struct hanf_engine {
   bool relabel = false;
   uint32_t* order = nullptr;
   uint32_t* perm = nullptr;
+  uint64_t* rl_off = nullptr;  // relabelled offsets until the worklist needs the CSR
   uint64_t* dirty[2] = {nullptr, nullptr};
   CUtensorMap tmap[2];        // descriptors of cnt[0], cnt[1]
 
@@ -319,6 +320,7 @@ struct hanf_engine {
       pfree(hub_index, stream);
       pfree(order, stream);
       pfree(perm, stream);
+      pfree(rl_off, stream);
       pfree(dirty[0], stream);
       pfree(dirty[1], stream);
       pfree(lens, stream);
@@ -497,6 +499,20 @@ void note_step(hanf_engine* e) {
 hanf_status ensure_sparse(hanf_engine* e) {
   if (e->tr_off) return HANF_OK;
   cudaStream_t s = e->stream;
+  if (e->relabel && e->rl_off) {
+    // the transpose is built from the relabelled CSR; the caller-order
+    // copy is not needed after that
+    uint32_t* succ = nullptr;
+    int bad = 0;
+    const hanf::RelabelOut r{e->order, e->perm, e->rl_off};
+    HANF_CUDA(hanf::relabel_arcs_device(e->csr_off, e->csr_succ, e->n, e->shard_arcs, r, s, &succ,
+                                        &bad, &e->launches));
+    pfree(e->csr_off, s);
+    pfree(e->csr_succ, s);
+    e->csr_off = e->rl_off;
+    e->csr_succ = succ;
+    e->rl_off = nullptr;
+  }
   HANF_CUDA(hanf::build_transpose_device(e->csr_off, e->csr_succ, e->lo, e->hi, e->succ_base, e->n,
                                          s, &e->tr_off, &e->tr_succ, &e->launches));
   HANF_CUDA(palloc(&e->sig, e->blocks, s));
@@ -922,22 +938,13 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
     HANF_TRY(cudaEventRecord(ev_arcs, s2));
     phase("offsets");
     if (e->relabel) {
-      // renumber rows by degree (needs the arcs; the seed needs the order)
-      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+      // renumber rows by out-degree (offsets only: overlaps the arcs upload)
       hanf::RelabelOut r;
-      const cudaError_t re = hanf::relabel_device(d_off, d_succ, n, a1 - a0, s, &r, &e->launches);
-      cudaFreeAsync(d_off, s);  // the caller-order CSR is not needed any more
-      cudaFreeAsync(d_succ, s);
-      d_off = r.off;
-      d_succ = r.succ;
+      const cudaError_t re = hanf::relabel_order_device(d_off, n, s, &r, &e->launches);
       e->order = r.order;
       e->perm = r.perm;
-      e->csr_off = d_off;  // owned by the engine from here on
-      e->csr_succ = d_succ;
+      e->rl_off = r.off;
       HANF_TRY(re);
-      if (r.bad)
-        return bail(fail(HANF_INVALID_ARGUMENT,
-                         "arc endpoint out of range or offsets not non-decreasing"));
       HANF_TRY(palloc(&e->dirty[0], e->blocks, s));
       HANF_TRY(palloc(&e->dirty[1], e->blocks, s));
       phase("relabel");
@@ -946,8 +953,10 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
     if (st != HANF_OK) return bail(st);
     phase("seed");
     int bad = 0;
-    const cudaError_t be = hanf::build_tasks_device(d_off, d_succ, lo, hi, a0, n, s, ev_arcs,
-                                                    &e->tasks, &bad, &e->launches);
+    // relabelled: row v's successors are the caller's arcs of order[v], through perm
+    const hanf::CsrView view{d_off, lo, d_succ, a0, e->order, e->perm, n};
+    const cudaError_t be =
+        hanf::build_tasks_device(view, lo, hi, n, s, ev_arcs, &e->tasks, &bad, &e->launches);
     // (also on the build's error paths) frees on `s` come after the upload
     HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
     e->csr_off = d_off;

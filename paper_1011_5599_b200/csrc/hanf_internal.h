@@ -40,29 +40,53 @@ struct TaskBuild {
   uint32_t* hub_ticket = nullptr;
   uint32_t num_hubs = 0;
 };
-// Builds the tasks of nodes [lo, hi) from the shard's CSR on the device
-// (d_off = offsets[lo..hi], d_succ = arcs from index succ_base).  Sets
-// *bad_input when offsets decrease or an arc endpoint is >= n.  Only the
-// final TOS fill reads d_succ: it waits for `succ_ready` (when non-null),
-// so the arcs upload overlaps the degree sort and task layout.
-cudaError_t build_tasks_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t lo,
-                               uint64_t hi, uint64_t succ_base, uint64_t n, cudaStream_t s,
-                               cudaEvent_t succ_ready, TaskBuild* out, int* bad_input,
-                               uint64_t* launches);
+// The CSR as the task build reads it: node (row) v's successors are arcs
+// [begin(v), end(v)) of `succ` (from index succ_base), each mapped through
+// `perm` when the graph is relabelled (row v = original id orig_of[v];
+// `off` is then indexed by original id, lo = 0).
+struct CsrView {
+  const uint64_t* off;
+  uint64_t lo;
+  const uint32_t* succ;
+  uint64_t succ_base;
+  const uint32_t* orig_of;  // nullptr: identity labels (off indexed by v - lo)
+  const uint32_t* perm;
+  uint64_t n;
+  __device__ __forceinline__ uint64_t begin(uint64_t v) const {
+    return orig_of ? off[orig_of[v]] : off[v - lo];
+  }
+  __device__ __forceinline__ uint64_t end(uint64_t v) const {
+    return orig_of ? off[orig_of[v] + 1] : off[v - lo + 1];
+  }
+  __device__ __forceinline__ uint32_t id(uint64_t k) const {
+    const uint32_t w = succ[k - succ_base];
+    return perm && w < n ? perm[w] : w;  // out-of-range ids stay out of range (flagged)
+  }
+};
+// Builds the tasks of nodes [lo, hi) from the shard's CSR on the device.
+// Sets *bad_input when offsets decrease or an arc endpoint is >= n.  Only
+// the final TOS fill reads the arcs: it waits for `succ_ready` (when
+// non-null), so the arcs upload overlaps the degree sort and task layout.
+cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
+                               cudaStream_t s, cudaEvent_t succ_ready, TaskBuild* out,
+                               int* bad_input, uint64_t* launches);
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
 // Locality relabelling (hanf_relabel.cu): rows renumbered by descending
-// out-degree; order[row] = original id, perm[id] = row; off/succ = the
-// relabelled CSR (pool allocations, caller frees).  bad = malformed input.
+// out-degree, from the offsets alone; order[row] = original id, perm[id] =
+// row, off = the relabelled offsets (pool allocations, caller frees).
 struct RelabelOut {
   uint32_t* order = nullptr;
   uint32_t* perm = nullptr;
   uint64_t* off = nullptr;
-  uint32_t* succ = nullptr;
-  int bad = 0;
 };
-cudaError_t relabel_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n, uint64_t arcs,
-                           cudaStream_t s, RelabelOut* out, uint64_t* launches);
+cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, cudaStream_t s, RelabelOut* out,
+                                 uint64_t* launches);
+// The relabelled arcs (only the worklist step's transpose needs them; the
+// union sweep's TOS is filled through CsrView).  *bad = arc endpoint >= n.
+cudaError_t relabel_arcs_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n,
+                                uint64_t arcs, const RelabelOut& r, cudaStream_t s,
+                                uint32_t** succ_out, int* bad, uint64_t* launches);
 // rows perm[first + i] (or first + i) of `counters`, W words each, packed
 // densely into dst (device)
 cudaError_t launch_gather_rows(const uint64_t* counters, const uint32_t* perm, uint64_t first,

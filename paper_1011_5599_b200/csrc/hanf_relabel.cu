@@ -144,33 +144,39 @@ cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
     if (_e != cudaSuccess) return _e;   \
   } while (0)
 
-cudaError_t relabel_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n, uint64_t arcs,
-                           cudaStream_t s, RelabelOut* out, uint64_t* launches) {
-  *out = RelabelOut{};
-  if (n == 0) return cudaSuccess;
-  const uint32_t threads = 256;
-  static const bool prof = [] {
+namespace {
+struct Phases {  // HANF_PROFILE=1: synchronising phase times
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  bool on = [] {
     const char* p = std::getenv("HANF_PROFILE");
     return p && p[0] == '1';
   }();
-  auto t_prev = std::chrono::steady_clock::now();
-  auto phase = [&](const char* what) {  // HANF_PROFILE=1: synchronising phase times
-    if (!prof) return;
+  void operator()(const char* what) {
+    if (!on) return;
     cudaStreamSynchronize(s);
     const auto now = std::chrono::steady_clock::now();
     std::fprintf(stderr, "[hanf]   relabel %-8s %8.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(now - t_prev).count());
-    t_prev = now;
-  };
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
+cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, cudaStream_t s, RelabelOut* out,
+                                 uint64_t* launches) {
+  *out = RelabelOut{};
+  if (n == 0) return cudaSuccess;
+  Phases phase{s};
+  const uint32_t threads = 256;
   auto grid = [](uint64_t items) {
     const uint64_t b = (items + 255) / 256;
     return static_cast<uint32_t>(b < 148ull * 32 ? (b ? b : 1) : 148ull * 32);
   };
   uint32_t *keys = nullptr, *vals = nullptr, *skeys = nullptr;
-  int* d_bad = nullptr;
+  int* d_bad = nullptr;  // decreasing offsets: the task build flags them too
   uint64_t* ndeg = nullptr;
   HANF_RELABEL_TRY(pool_alloc(&d_bad, 1, s));
-  HANF_RELABEL_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
   HANF_RELABEL_TRY(pool_alloc(&keys, n, s));
   HANF_RELABEL_TRY(pool_alloc(&vals, n, s));
   score_keys_kernel<<<grid(n), threads, 0, s>>>(d_off, n, keys, vals, d_bad);
@@ -191,6 +197,7 @@ cudaError_t relabel_device(const uint64_t* d_off, const uint32_t* d_succ, uint64
   HANF_RELABEL_TRY(cudaFreeAsync(keys, s));
   HANF_RELABEL_TRY(cudaFreeAsync(vals, s));
   HANF_RELABEL_TRY(cudaFreeAsync(skeys, s));
+  HANF_RELABEL_TRY(cudaFreeAsync(d_bad, s));
   phase("sort");
   HANF_RELABEL_TRY(pool_alloc(&out->perm, n, s));
   HANF_RELABEL_TRY(pool_alloc(&ndeg, n + 1, s));
@@ -210,21 +217,33 @@ cudaError_t relabel_device(const uint64_t* d_off, const uint32_t* d_succ, uint64
   }
   HANF_RELABEL_TRY(cudaFreeAsync(ndeg, s));
   phase("offsets");
-  HANF_RELABEL_TRY(pool_alloc(&out->succ, arcs, s));
+  return cudaGetLastError();
+}
+
+cudaError_t relabel_arcs_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n,
+                                uint64_t arcs, const RelabelOut& r, cudaStream_t s,
+                                uint32_t** succ_out, int* bad, uint64_t* launches) {
+  *succ_out = nullptr;
+  *bad = 0;
+  Phases phase{s};
+  int* d_bad = nullptr;
+  HANF_RELABEL_TRY(pool_alloc(&d_bad, 1, s));
+  HANF_RELABEL_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+  HANF_RELABEL_TRY(pool_alloc(succ_out, arcs, s));
   if (arcs) {
     const uint64_t blocks = (arcs + 1023) / 1024;  // warp blocks of 1024 arcs
     uint64_t ctas = (blocks + 7) / 8;
     if (ctas > 148ull * 16) ctas = 148ull * 16;
-    rewrite_arcs_kernel<<<static_cast<uint32_t>(ctas), threads, 0, s>>>(
-        d_off, d_succ, n, arcs, out->order, out->perm, out->off, out->succ, d_bad);
+    rewrite_arcs_kernel<<<static_cast<uint32_t>(ctas), 256, 0, s>>>(
+        d_off, d_succ, n, arcs, r.order, r.perm, r.off, *succ_out, d_bad);
     ++*launches;
   }
-  phase("arcs");
   int h_bad = 0;
   HANF_RELABEL_TRY(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   HANF_RELABEL_TRY(cudaFreeAsync(d_bad, s));
   HANF_RELABEL_TRY(cudaStreamSynchronize(s));
-  out->bad = h_bad;
+  phase("arcs");
+  *bad = h_bad;
   return cudaGetLastError();
 }
 
