@@ -169,9 +169,11 @@ __device__ __forceinline__ void swar_chain(uint32_t (&x)[Lay::kLimbs],
       constexpr uint32_t H = Lay::high(i);
       lt[i] = lop3<0x2B>(d[i], x[i], y[i]) & H;  // ((d | (x^y)) ^ (x | ~y)) & H
     });
-    // spread_i = low(u_i * (2^r - 1)) | high(u_{i-1} * (2^r - 1)); the two
-    // never overlap, so the carry rides in as the addend of the 32x32+64
-    // multiply-add (one IMAD.WIDE per limb, no OR)
+    // spread_i = low(u_i * (2^r - 1)) | high(u_{i-1} * (2^r - 1)).  The two
+    // never overlap, so the low word is one 32-bit multiply-add with the
+    // carry as addend (it cannot overflow) and the next carry is the high
+    // word alone: IMAD + IMAD.HI on the FMA pipe, no OR and no register
+    // pair (an IMAD.WIDE with a 64-bit addend costs two moves per limb)
     uint32_t carry = 0;
     sfor<S, E>([&](auto I) {
       constexpr int i = decltype(I)::value;
@@ -180,9 +182,8 @@ __device__ __forceinline__ void swar_chain(uint32_t (&x)[Lay::kLimbs],
         u = __funnelshift_r(lt[i], lt[i + 1], R - 1);
       else
         u = lt[i] >> (R - 1);
-      const uint64_t w = static_cast<uint64_t>(u) * Lay::kMul + carry;
-      const uint32_t spread = static_cast<uint32_t>(w);
-      carry = static_cast<uint32_t>(w >> 32);
+      const uint32_t spread = u * Lay::kMul + carry;
+      if constexpr (i + 1 < E) carry = __umulhi(u, Lay::kMul);
       x[i] = lop3<0xD8>(x[i], y[i], spread);  // (x & ~spread) | (y & spread)
     });
     swar_chain<Lay, E>(x, y);

@@ -672,8 +672,15 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
           case 9: return union_launch<5, 64, 2, 2, false, 4>(args, ch, s);
           case 20: return union_launch<5, 64, 3, 1, false, 4, true>(args, ch, s);
           case 21: return union_launch<5, 64, 2, 1, false, 4, true>(args, ch, s);
+          case 23: return union_launch<5, 64, 2, 1, false, 5, true>(args, ch, s);
+          case 24: return union_launch<5, 64, 2, 1, false, 6, true>(args, ch, s);
+          case 25: return union_launch<5, 64, 3, 1, false, 4, true>(args, ch, s);  // r01 default
+          case 26: return union_launch<5, 64, 1, 1, false, 6, true>(args, ch, s);
+          case 27: return union_launch<5, 64, 1, 1, false, 8, true>(args, ch, s);
           case 22: return union_launch<5, 64, 3, 1, false, 4>(args, ch, s);
-          default: return union_launch<5, 64, 3, 1, false, 4, true>(args, ch, s);
+          // U = 3, <= 48 registers (5 CTAs/SM), next-trip id prefetch: +2%
+          // on config 2 and +1% on R-MAT 26 over 64 registers
+          default: return union_launch<5, 64, 3, 1, false, 5, true>(args, ch, s);
         }
       return union_launch<5, 64, 4, 0, false>(args, ch, s);
     case 5128:

@@ -5,8 +5,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import bench
 import paper_1011_5599_b200 as h
-cfgno = int(sys.argv[1]); variants = sys.argv[2].split(","); l2s = sys.argv[3].split(",")
-name, make, b = bench.workload(cfgno)
+cfgno = sys.argv[1]; variants = sys.argv[2].split(","); l2s = sys.argv[3].split(",")
+if cfgno.startswith("rmat"):  # R-MAT scale k, config-2 parameters (dev sizes between 2 and 5)
+    k = int(cfgno[4:])
+    name, make, b = (f"R-MAT {k} (ef 16, ids permuted)",
+                     lambda: h.gen_rmat(k, 16, 0.57, 0.19, 0.19, 1, 7), 6)
+else:
+    name, make, b = bench.workload(int(cfgno))
 t0 = time.time(); g = make(); print(name, "gen", round(time.time() - t0, 1), "s", flush=True)
 import ctypes
 cudart = ctypes.CDLL("libcudart.so") if False else None
