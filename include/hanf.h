@@ -211,6 +211,15 @@ hanf_status hanf_gen_copying(uint64_t n, double exponent, double mean_degree,
                              uint64_t window, uint64_t seed, hanf_graph** out);
 hanf_status hanf_gen_barabasi_albert(uint64_t n, uint32_t m, uint64_t seed,
                                      uint64_t permute_seed, hanf_graph** out);
+/* (new) The same graphs built on GPU `device` with device
+ * radix sorts: Graph::from_edges (graph.hpp:29-44) and the R-MAT generator,
+ * bit-identical CSR to hanf_graph_from_edges / hanf_gen_rmat, returned in
+ * host memory.  HANF_CUDA_ERROR without a device. */
+hanf_status hanf_graph_from_edges_gpu(int32_t device, uint64_t n, const uint32_t* src,
+                                      const uint32_t* dst, uint64_t count, hanf_graph** out);
+hanf_status hanf_gen_rmat_gpu(int32_t device, uint32_t scale, uint32_t edge_factor, double a,
+                              double b, double c, uint64_t seed, uint64_t permute_seed,
+                              hanf_graph** out);
 /* transpose (graph.hpp:72-84). */
 hanf_status hanf_graph_transpose(const hanf_graph* g, hanf_graph** out);
 /* HBG1 CSR cache (graph.hpp:178-218, FORMATS.md:13-23). */

@@ -98,6 +98,10 @@ _SIGNATURES = {
     "hanf_graph_load_csr": [c_char_p, POINTER(_P)],
     "hanf_graph_view_of": [_P, POINTER(GraphView)],
     "hanf_pin_host": [_P, c_uint64],
+    "hanf_graph_from_edges_gpu": [c_int32, c_uint64, POINTER(c_uint32), POINTER(c_uint32),
+                                  c_uint64, POINTER(_P)],
+    "hanf_gen_rmat_gpu": [c_int32, c_uint32, c_uint32, c_double, c_double, c_double, c_uint64,
+                          c_uint64, POINTER(_P)],
     "hanf_unpin_host": [_P],
 }
 _VOID = {"hanf_destroy": [_P], "hanf_graph_free": [_P]}

@@ -16,16 +16,8 @@
 #include <vector>
 
 #include "../../include/hanf.h"
-
-namespace hanf_host_detail {  // defined in hanf_engine.cu (one error slot)
-void set_error(const std::string& s);
-}
-
-struct hanf_graph {
-  uint64_t n = 0;
-  std::vector<uint64_t> offsets{0};
-  std::vector<uint32_t> succ;
-};
+#include "hanf_graph_internal.h"
+#include "hanf_rng.h"
 
 namespace {
 
@@ -59,14 +51,7 @@ void parallel_for(uint64_t total, const std::function<void(uint64_t, uint64_t)>&
 // hash.hpp:8-15 / 27-55 (the reference's own mixers, used so that the
 // reference fixtures gen_uniform_random / gen_clique_path are reproduced
 // bit for bit).
-constexpr uint64_t mix64(uint64_t z) {
-  z ^= z >> 33;
-  z *= 0xff51afd7ed558ccdULL;
-  z ^= z >> 33;
-  z *= 0xc4ceb9fe1a85ec53ULL;
-  z ^= z >> 33;
-  return z;
-}
+using hanf_rng::mix64;
 struct SplitMix64 {
   uint64_t state;
   uint64_t next() {
@@ -85,38 +70,9 @@ struct SplitMix64 {
   double next_double() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
 };
 
-// Counter-based stream: value k of stream (seed, key).  Used by the
-// synthetic-config generators so every arc is a pure function of its index
-// (generation parallelises and is identical on any thread count).
-inline uint64_t hash3(uint64_t seed, uint64_t key, uint64_t k) {
-  return mix64(mix64(seed ^ 0x5851f42d4c957f2dULL) ^ mix64(key * 0x9e3779b97f4a7c15ULL + k));
-}
-inline double u01(uint64_t h) { return static_cast<double>(h >> 11) * 0x1.0p-53; }
-
-// Random bijection on [0, 2^bits) (4-round Feistel network keyed by seed),
-// bits >= 2.  Used to permute node ids.
-struct Feistel {
-  uint32_t bits, lbits, rbits;
-  uint64_t keys[4];
-  Feistel(uint32_t b, uint64_t seed) : bits(b), lbits(b / 2), rbits(b - b / 2) {
-    for (int i = 0; i < 4; ++i) keys[i] = mix64(seed * 4 + i + 0x7f4a7c15ULL);
-  }
-  uint64_t operator()(uint64_t x) const {
-    // unbalanced Feistel on (l: lbits, r: rbits), alternating sides; a
-    // cycle-walk keeps the result inside [0, 2^bits) (it always is here).
-    uint64_t l = x >> rbits, r = x & ((1ull << rbits) - 1);
-    uint32_t lb = lbits, rb = rbits;
-    for (int i = 0; i < 4; ++i) {
-      const uint64_t f = mix64(r ^ keys[i]) & ((1ull << lb) - 1);
-      const uint64_t nl = r, nr = l ^ f;
-      // swap roles: new left has rb bits, new right has lb bits
-      l = nl;
-      r = nr;
-      std::swap(lb, rb);
-    }
-    return (l << rb) | r;
-  }
-};
+using hanf_rng::Feistel;
+using hanf_rng::hash3;
+using hanf_rng::u01;
 
 // Graph::from_edges (graph.hpp:29-44): ids < n checked; rows sorted and
 // deduplicated.  Parallel counting sort by source, then per-row sort.
@@ -300,14 +256,8 @@ hanf_status hanf_gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double
   }
   parallel_for(draws, [&](uint64_t lo, uint64_t hi) {
     for (uint64_t i = lo; i < hi; ++i) {
-      uint64_t u = 0, v = 0, h = 0;
-      for (uint32_t level = 0; level < scale; ++level) {
-        if ((level & 3) == 0) h = hash3(seed, i, level >> 2);
-        const uint32_t r = static_cast<uint32_t>(h >> (16 * (level & 3))) & 0xffff;
-        const uint64_t bu = r >= tb, bv = (r >= ta && r < tb) || r >= tc;
-        u = (u << 1) | bu;
-        v = (v << 1) | bv;
-      }
+      uint64_t u = 0, v = 0;
+      hanf_rng::rmat_draw(seed, i, scale, ta, tb, tc, &u, &v);
       src[i] = static_cast<uint32_t>(perm(u));
       dst[i] = static_cast<uint32_t>(perm(v));
     }

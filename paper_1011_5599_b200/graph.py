@@ -47,17 +47,21 @@ class Graph:
         return Graph(n, offsets, arcs)
 
     @staticmethod
-    def from_edges(n: int, edges) -> "Graph":
-        """graph.hpp:29-44: sorts each successor list and collapses duplicates."""
+    def from_edges(n: int, edges, device: int = None) -> "Graph":
+        """graph.hpp:29-44: sorts each successor list and collapses duplicates.
+        device=k builds the same CSR with device radix sorts on GPU k."""
         e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
         if e.size and (e.min() < 0 or e.max() >= n):
             raise ValueError("arc endpoint out of range")
         src = np.ascontiguousarray(e[:, 0], dtype=np.uint32)
         dst = np.ascontiguousarray(e[:, 1], dtype=np.uint32)
         h = c_void_p()
-        check(lib().hanf_graph_from_edges(
-            n, src.ctypes.data_as(POINTER(c_uint32)), dst.ctypes.data_as(POINTER(c_uint32)),
-            src.size, ctypes.byref(h)))
+        args = (n, src.ctypes.data_as(POINTER(c_uint32)), dst.ctypes.data_as(POINTER(c_uint32)),
+                src.size, ctypes.byref(h))
+        if device is None:
+            check(lib().hanf_graph_from_edges(*args))
+        else:
+            check(lib().hanf_graph_from_edges_gpu(device, *args))
         return Graph._adopt(h)
 
     # -- page-locking for uploads (new; hanf_pin_host) -------------------------
@@ -157,11 +161,16 @@ def gen_erdos_renyi(n: int, mean_degree: float, seed: int) -> Graph:
 
 
 def gen_rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
-             c: float = 0.19, seed: int = 1, permute_seed: int = 7) -> Graph:
-    """BASELINE configs 2/5: R-MAT, self-loops and duplicates removed, ids permuted."""
+             c: float = 0.19, seed: int = 1, permute_seed: int = 7, device: int = None) -> Graph:
+    """BASELINE configs 2/5: R-MAT, self-loops and duplicates removed, ids
+    permuted.  device=k generates the same graph on GPU k (hanf_gen_rmat_gpu)."""
     h = c_void_p()
-    check(lib().hanf_gen_rmat(scale, edge_factor, a, b, c, seed, permute_seed,
-                              ctypes.byref(h)))
+    if device is None:
+        check(lib().hanf_gen_rmat(scale, edge_factor, a, b, c, seed, permute_seed,
+                                  ctypes.byref(h)))
+    else:
+        check(lib().hanf_gen_rmat_gpu(device, scale, edge_factor, a, b, c, seed, permute_seed,
+                                      ctypes.byref(h)))
     return Graph._adopt(h)
 
 
