@@ -112,6 +112,10 @@ void hanf_destroy(hanf_engine* engine);
 /* Re-seeds the counters and rewinds to iteration 0 (a fresh NfEngine on
  * the same graph, without re-uploading it). */
 hanf_status hanf_reset(hanf_engine* engine);
+/* (new) hanf_reset under another HLL seed: the next run of a multi-seed
+ * experiment (main.cpp:263-283 runs estimate_nf for seeds base + i) reuses
+ * the uploaded graph, its task layout and its step graphs. */
+hanf_status hanf_reseed(hanf_engine* engine, uint64_t seed);
 
 /* ---- the hot path -------------------------------------------------------- */
 /* NfEngine::sum_estimates() (engine.hpp:100-118). */

@@ -58,6 +58,7 @@ _SIGNATURES = {
     "hanf_sketch_params_make": [c_uint32, c_uint64, c_uint32, POINTER(SketchParamsC)],
     "hanf_create": [POINTER(GraphView), POINTER(Config), POINTER(_P)],
     "hanf_reset": [_P],
+    "hanf_reseed": [_P, c_uint64],
     "hanf_sum_estimates": [_P, POINTER(c_double)],
     "hanf_step": [_P, POINTER(IterationReportC)],
     "hanf_run_to_stabilisation": [_P, POINTER(c_double), POINTER(c_uint64), c_uint64,

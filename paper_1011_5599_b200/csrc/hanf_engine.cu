@@ -990,6 +990,13 @@ hanf_status hanf_reset(hanf_engine* e) {
   return seed_all(e);
 }
 
+hanf_status hanf_reseed(hanf_engine* e, uint64_t seed) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  e->cfg.seed = seed;
+  e->params.seed = seed;  // only the seeding hash reads it (engine.hpp:84-85)
+  return hanf_reset(e);
+}
+
 hanf_status hanf_sum_estimates(hanf_engine* e, double* sum) {
   if (!e || !sum) return fail(HANF_INVALID_ARGUMENT, "null argument");
   *sum = e->n == 0 ? 0.0 : e->last_sum;

@@ -233,6 +233,15 @@ class NfEngine:
         """Re-seed and rewind to iteration 0 (no graph re-upload)."""
         check(lib().hanf_reset(self._h))
 
+    def reseed(self, seed: int) -> None:
+        """reset() under another HLL seed (hanf_reseed): the next run of a
+        multi-seed experiment without re-uploading the graph."""
+        check(lib().hanf_reseed(self._h, seed & 0xFFFFFFFFFFFFFFFF))
+        self._cfg.seed = seed
+        p = _lib.SketchParamsC()
+        check(lib().hanf_params(self._h, ctypes.byref(p)))
+        self._params = SketchParams._from_c(p)
+
     def stream(self) -> int:
         s = c_void_p()
         check(lib().hanf_stream(self._h, ctypes.byref(s)))
@@ -272,3 +281,23 @@ def estimate_nf(g: Graph, cfg: EngineConfig = None) -> NfEstimate:
     """engine.hpp:295-298: seed counters, run, return the estimate."""
     with NfEngine(g, cfg or EngineConfig()) as engine:
         return engine.run_to_stabilisation()
+
+
+def multirun(g: Graph, cfg: EngineConfig = None, runs: int = 10, base_seed: int = None):
+    """The reference's multirun (main.cpp:263-283): estimate_nf for seeds
+    base_seed + i, i < runs (base_seed defaults to cfg.seed).  One engine:
+    the graph is uploaded and laid out once, then re-seeded per run.
+    Aggregate with stats.aggregate_runs."""
+    import dataclasses
+    cfg = dataclasses.replace(cfg) if cfg is not None else EngineConfig()
+    base = cfg.seed if base_seed is None else base_seed
+    out = []
+    if runs <= 0:
+        return out
+    cfg.seed = base
+    with NfEngine(g, cfg) as engine:
+        for i in range(runs):
+            if i:
+                engine.reseed(base + i)
+            out.append(engine.run_to_stabilisation())
+    return out

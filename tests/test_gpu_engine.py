@@ -418,3 +418,17 @@ def test_relabel_multichunk_and_readback(hanf, port, monkeypatch):
         for first, count in [(0, 1), (17, 33), (g.num_nodes() - 5, 5)]:
             part = e.counters(first, count)
             assert np.array_equal(part, full[first * W:(first + count) * W])
+
+
+def test_multirun_reseed(hanf):
+    """multirun (main.cpp:263-283): one engine re-seeded per run gives each
+    seed's estimate_nf bit for bit; aggregate_runs takes the list."""
+    g = hanf.gen_rmat(12, 16, 0.57, 0.19, 0.19, 2, 4)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=100)
+    runs = hanf.multirun(g, cfg, runs=4)
+    assert cfg.seed == 100  # caller's config untouched
+    for i, r in enumerate(runs):
+        ref = hanf.estimate_nf(g, hanf.EngineConfig(bucket_bits=6, seed=100 + i))
+        assert r.values == ref.values and r.modified == ref.modified and r.seed == 100 + i
+    rep = hanf.aggregate_runs(runs)
+    assert rep is not None
