@@ -117,6 +117,16 @@ hanf_status hanf_reset(hanf_engine* engine);
  * the uploaded graph, its task layout and its step graphs. */
 hanf_status hanf_reseed(hanf_engine* engine, uint64_t seed);
 
+/* HCA1 counter snapshots (hll.hpp:241-305): the current counters written
+ * byte for byte as the reference's save_counters writes them.  restore
+ * loads a snapshot with the engine's (b, r, n, seed) into both generations
+ * and resumes at `iteration` with every counter marked modified (the next
+ * step recomputes every node: exact, whatever the snapshot's history);
+ * HANF_PARSE_ERROR / HANF_IO_ERROR / HANF_INVALID_ARGUMENT on a bad or
+ * mismatched file. */
+hanf_status hanf_save_counters(hanf_engine* engine, const char* path);
+hanf_status hanf_restore_counters(hanf_engine* engine, const char* path, uint64_t iteration);
+
 /* ---- the hot path -------------------------------------------------------- */
 /* NfEngine::sum_estimates() (engine.hpp:100-118). */
 hanf_status hanf_sum_estimates(hanf_engine* engine, double* sum);

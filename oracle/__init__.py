@@ -310,6 +310,7 @@ class Ref:
         L.ref_engine_counters.argtypes = [vp, POINTER(c_uint64)]
         L.ref_engine_iteration.restype = c_uint64
         L.ref_engine_iteration.argtypes = [vp]
+        L.ref_engine_save_counters.argtypes = [vp, ctypes.c_char_p]
         L.ref_engine_systolic_active.argtypes = [vp]
         L.ref_engine_run.argtypes = [vp, POINTER(c_double), POINTER(c_uint64), c_uint64,
                                      POINTER(c_uint64), POINTER(c_double)]
@@ -433,6 +434,10 @@ class RefEngine:
 
     def iteration(self):
         return self.L.ref_engine_iteration(self.h)
+
+    def save_counters(self, path):
+        """The reference's own HCA1 writer (hll.hpp:275-286)."""
+        assert self.L.ref_engine_save_counters(self.h, str(path).encode()) == 0
 
     def systolic_active(self):
         return bool(self.L.ref_engine_systolic_active(self.h))

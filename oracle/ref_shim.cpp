@@ -112,6 +112,15 @@ const uint64_t* ref_engine_counters(const void* e, uint64_t* word_count) {
   return c.data();
 }
 uint64_t ref_engine_iteration(const void* e) { return static_cast<const NfEngine*>(e)->iteration(); }
+// hll.hpp:275-286 save_counters of the engine's current counters; 0 ok, 4 io
+int ref_engine_save_counters(const void* e, const char* path) {
+  try {
+    hyperanf::save_counters(static_cast<const NfEngine*>(e)->counters(), path);
+    return 0;
+  } catch (...) {
+    return 4;
+  }
+}
 int ref_engine_systolic_active(const void* e) { return static_cast<const NfEngine*>(e)->systolic_active(); }
 
 // NfEngine::run_to_stabilisation (engine.hpp:233-275).  0 ok, 1 invalid,

@@ -59,6 +59,8 @@ _SIGNATURES = {
     "hanf_create": [POINTER(GraphView), POINTER(Config), POINTER(_P)],
     "hanf_reset": [_P],
     "hanf_reseed": [_P, c_uint64],
+    "hanf_save_counters": [_P, c_char_p],
+    "hanf_restore_counters": [_P, c_char_p, c_uint64],
     "hanf_sum_estimates": [_P, POINTER(c_double)],
     "hanf_step": [_P, POINTER(IterationReportC)],
     "hanf_run_to_stabilisation": [_P, POINTER(c_double), POINTER(c_uint64), c_uint64,

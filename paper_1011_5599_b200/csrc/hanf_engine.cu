@@ -990,6 +990,104 @@ hanf_status hanf_reset(hanf_engine* e) {
   return seed_all(e);
 }
 
+namespace {
+void put_le(std::string& out, uint64_t v, int bytes) {
+  for (int i = 0; i < bytes; ++i) out.push_back(static_cast<char>(v >> (8 * i)));
+}
+uint64_t get_le(const unsigned char* p, int bytes) {
+  uint64_t v = 0;
+  for (int i = 0; i < bytes; ++i) v |= static_cast<uint64_t>(p[i]) << (8 * i);
+  return v;
+}
+}  // namespace
+
+// hll.hpp:275-286: "HCA1", u32 b, u32 r, u64 n, u64 seed, n*W words (LE).
+hanf_status hanf_save_counters(hanf_engine* e, const char* path) {
+  if (!e || !path) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  std::vector<uint64_t> words(e->n * e->words);
+  if (e->n) {
+    const hanf_status st = hanf_read_counters(e, 0, e->n, words.data());
+    if (st != HANF_OK) return st;
+  }
+  std::string head("HCA1");
+  put_le(head, e->params.bucket_bits, 4);
+  put_le(head, e->params.register_bits, 4);
+  put_le(head, e->n, 8);
+  put_le(head, e->params.seed, 8);
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(HANF_IO_ERROR, std::string("cannot open for writing: ") + path);
+  bool ok = std::fwrite(head.data(), 1, head.size(), f) == head.size();
+  if (ok && !words.empty())  // little-endian host: raw words are the LE encoding
+    ok = std::fwrite(words.data(), sizeof(uint64_t), words.size(), f) == words.size();
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) return fail(HANF_IO_ERROR, std::string("write failed: ") + path);
+  return HANF_OK;
+}
+
+// hll.hpp:288-303 load_counters, into a running engine (resume).
+hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t iteration) {
+  if (!e || !path) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(HANF_IO_ERROR, std::string("cannot open: ") + path);
+  unsigned char h[28];
+  const size_t got = std::fread(h, 1, sizeof h, f);
+  if (got < 4 || std::memcmp(h, "HCA1", 4) != 0) {
+    std::fclose(f);
+    return fail(HANF_PARSE_ERROR, std::string(path) + ": bad counter snapshot magic");
+  }
+  if (got < sizeof h) {
+    std::fclose(f);
+    return fail(HANF_PARSE_ERROR, std::string(path) + ": truncated header");
+  }
+  const uint64_t b = get_le(h + 4, 4), r = get_le(h + 8, 4), n = get_le(h + 12, 8),
+                 seed = get_le(h + 20, 8);
+  if (b != e->params.bucket_bits || r != e->params.register_bits || n != e->n) {
+    std::fclose(f);
+    return fail(HANF_INVALID_ARGUMENT, "snapshot (b, r, n) does not match the engine");
+  }
+  std::vector<uint64_t> words(n * e->words);
+  const size_t rd = words.empty() ? 0 : std::fread(words.data(), sizeof(uint64_t), words.size(), f);
+  std::fclose(f);
+  if (rd != words.size())
+    return fail(HANF_PARSE_ERROR, std::string(path) + ": truncated counter data");
+  if (n == 0) {
+    e->t = iteration;
+    return HANF_OK;
+  }
+  HANF_CUDA(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  uint64_t* tmp = nullptr;
+  HANF_CUDA(palloc(&tmp, words.size(), s));
+  cudaError_t ce = cudaMemcpyAsync(tmp, words.data(), sizeof(uint64_t) * words.size(),
+                                   cudaMemcpyHostToDevice, s);
+  for (int g = 0; g < 2 && ce == cudaSuccess; ++g)  // both generations (next == cur)
+    ce = hanf::launch_scatter_rows(tmp, e->perm, n, static_cast<uint32_t>(e->pitch),
+                                   static_cast<uint32_t>(e->words), e->cnt[g], s, &e->launches);
+  cudaFreeAsync(tmp, s);
+  HANF_CUDA(ce);
+  // every counter counts as modified: the next step recomputes every node
+  HANF_CUDA(hanf::launch_seed_bitmap(e->mod[0], e->n, s));
+  HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, s));
+  if (e->relabel) {
+    HANF_CUDA(cudaMemcpyAsync(e->dirty[0], e->mod[0], sizeof(uint64_t) * e->blocks,
+                              cudaMemcpyDeviceToDevice, s));
+    HANF_CUDA(cudaMemsetAsync(e->dirty[1], 0, sizeof(uint64_t) * e->blocks, s));
+  }
+  e->cfg.seed = seed;
+  e->params.seed = seed;
+  e->cur = 0;
+  e->stale_valid = false;
+  e->systolic = false;
+  hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
+  if (st != HANF_OK) return st;
+  uint64_t count = 0;
+  st = finish(e, dirty_of(e, 0), false, 0, 0, &e->last_sum, &count);
+  if (st != HANF_OK) return st;
+  e->last_count = e->n;
+  e->t = iteration;
+  return HANF_OK;
+}
+
 hanf_status hanf_reseed(hanf_engine* e, uint64_t seed) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
   e->cfg.seed = seed;

@@ -89,6 +89,10 @@ cudaError_t relabel_arcs_device(const uint64_t* d_off, const uint32_t* d_succ, u
                                 uint32_t** succ_out, int* bad, uint64_t* launches);
 // rows perm[first + i] (or first + i) of `counters`, W words each, packed
 // densely into dst (device)
+cudaError_t launch_seed_bitmap(uint64_t* bits, uint64_t n, cudaStream_t s);
+cudaError_t launch_scatter_rows(const uint64_t* src, const uint32_t* perm, uint64_t count,
+                                uint32_t pitch, uint32_t words, uint64_t* counters,
+                                cudaStream_t s, uint64_t* launches);
 cudaError_t launch_gather_rows(const uint64_t* counters, const uint32_t* perm, uint64_t first,
                                uint64_t count, uint32_t pitch, uint32_t words, uint64_t* dst,
                                cudaStream_t s, uint64_t* launches);

@@ -892,6 +892,49 @@ __global__ void gather_rows_kernel(const uint64_t* __restrict__ counters,
   }
 }
 
+// bits [0, n) of a bitmap set, the rest of its words cleared
+__global__ void all_bits_kernel(uint64_t* __restrict__ bits, uint64_t n) {
+  const uint64_t words = (n + 63) / 64;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < words;
+       w += stride)
+    bits[w] = (w + 1) * 64 <= n ? ~0ull : (~0ull >> ((w + 1) * 64 - n));
+}
+
+cudaError_t launch_seed_bitmap(uint64_t* bits, uint64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint64_t blocks = ((n + 63) / 64 + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  all_bits_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(bits, n);
+  return cudaGetLastError();
+}
+
+// Snapshot restore: dense row i -> counter row perm[i] (or i), W words.
+__global__ void scatter_rows_kernel(const uint64_t* __restrict__ src,
+                                    const uint32_t* __restrict__ perm, uint64_t count,
+                                    uint32_t pitch, uint32_t words,
+                                    uint64_t* __restrict__ counters) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+       k < count * pitch; k += stride) {
+    const uint64_t i = k / pitch, w = k % pitch;
+    const uint64_t row = perm ? perm[i] : i;
+    counters[row * pitch + w] = w < words ? src[i * words + w] : 0ull;  // padding stays 0
+  }
+}
+
+cudaError_t launch_scatter_rows(const uint64_t* src, const uint32_t* perm, uint64_t count,
+                                uint32_t pitch, uint32_t words, uint64_t* counters,
+                                cudaStream_t s, uint64_t* launches) {
+  if (count == 0) return cudaSuccess;
+  uint64_t blocks = (count * pitch + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  scatter_rows_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(src, perm, count, pitch,
+                                                                    words, counters);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gather_rows(const uint64_t* counters, const uint32_t* perm, uint64_t first,
                                uint64_t count, uint32_t pitch, uint32_t words, uint64_t* dst,
                                cudaStream_t s, uint64_t* launches) {

@@ -233,6 +233,21 @@ class NfEngine:
         """Re-seed and rewind to iteration 0 (no graph re-upload)."""
         check(lib().hanf_reset(self._h))
 
+    def save_counters(self, path) -> None:
+        """hll.hpp:275-286: the current counters as an HCA1 snapshot, byte
+        for byte the reference's save_counters output."""
+        check(lib().hanf_save_counters(self._h, str(path).encode()))
+
+    def restore_counters(self, path, iteration: int = 0) -> None:
+        """Resume from an HCA1 snapshot (hll.hpp:288-303) taken at
+        `iteration`: both generations hold it, every counter counts as
+        modified, N(t) is re-summed; the snapshot's seed is adopted."""
+        check(lib().hanf_restore_counters(self._h, str(path).encode(), iteration))
+        p = _lib.SketchParamsC()
+        check(lib().hanf_params(self._h, ctypes.byref(p)))
+        self._params = SketchParams._from_c(p)
+        self._cfg.seed = self._params.seed
+
     def reseed(self, seed: int) -> None:
         """reset() under another HLL seed (hanf_reseed): the next run of a
         multi-seed experiment without re-uploading the graph."""

@@ -432,3 +432,46 @@ def test_multirun_reseed(hanf):
         assert r.values == ref.values and r.modified == ref.modified and r.seed == 100 + i
     rep = hanf.aggregate_runs(runs)
     assert rep is not None
+
+
+def test_hca1_snapshot_and_resume(hanf, ref, tmp_path, monkeypatch):
+    """HCA1 snapshots (hll.hpp:241-305): the engine's file is byte for byte
+    the reference's save_counters output after the same iterations, and an
+    engine restored from it continues exactly like the uninterrupted run."""
+    g = hanf.gen_rmat(11, 16, 0.57, 0.19, 0.19, 6, 2)
+    for relabel in ("0", "1"):
+        monkeypatch.setenv("HANF_RELABEL", relabel)
+        for b, r in [(6, 5), (5, 5), (8, 5), (6, 7)]:
+            re = ref.engine(ref.graph(g.num_nodes(), g.offsets(), g.arcs()), bucket_bits=b,
+                            register_bits=r, seed=11)
+            cfg = hanf.EngineConfig(bucket_bits=b, register_bits=r, seed=11)
+            with hanf.NfEngine(g, cfg) as e:
+                for _ in range(2):
+                    e.step()
+                    re.step()
+                ours, theirs = tmp_path / "ours.hca", tmp_path / "ref.hca"
+                e.save_counters(ours)
+                re.save_counters(theirs)
+                assert ours.read_bytes() == theirs.read_bytes()
+                at2 = e.sum_estimates()
+                rest = []
+                while True:  # the uninterrupted run from iteration 3 on
+                    rep = e.step()
+                    rest.append((rep.sum, rep.modified, e.counters()))
+                    if rep.modified == 0:
+                        break
+            with hanf.NfEngine(g, hanf.EngineConfig(bucket_bits=b, register_bits=r, seed=99)) as e:
+                e.restore_counters(ours, iteration=2)
+                assert e.iteration() == 2 and e.params().seed == 11
+                assert e.sum_estimates() == at2
+                for s_, m_, c_ in rest:
+                    rep = e.step()
+                    assert (rep.sum, rep.modified) == (s_, m_)
+                    assert np.array_equal(e.counters(), c_)
+    with hanf.NfEngine(g, hanf.EngineConfig(bucket_bits=7, seed=11)) as e:
+        with pytest.raises(ValueError):
+            e.restore_counters(ours)  # b mismatch
+        bad = tmp_path / "bad.hca"
+        bad.write_bytes(b"XXXX" + bytes(40))
+        with pytest.raises(Exception):
+            e.restore_counters(bad)
