@@ -117,6 +117,14 @@ hanf_status hanf_reset(hanf_engine* engine);
  * the uploaded graph, its task layout and its step graphs. */
 hanf_status hanf_reseed(hanf_engine* engine, uint64_t seed);
 
+/* Exact neighbourhood function (oracle.hpp:38-104): values[t] = ordered
+ * pairs at distance <= t, t = 0..diameter, computed on GPU `device` as
+ * bitset balls over batches of 2048 targets (hanf_exact.cu).  The same
+ * guard as the reference's OracleGuard (max_nodes, max_work = n * arcs)
+ * raises HANF_GUARD; HANF_CAPACITY when cap < the length (*len set). */
+hanf_status hanf_exact_nf(const hanf_graph_view* graph, int32_t device, uint64_t max_nodes,
+                          uint64_t max_work, uint64_t* values, uint64_t cap, uint64_t* len);
+
 /* HCA1 counter snapshots (hll.hpp:241-305): the current counters written
  * byte for byte as the reference's save_counters writes them.  restore
  * loads a snapshot with the engine's (b, r, n, seed) into both generations

@@ -9,7 +9,8 @@ Python mirror of that surface; there is no CPU fallback.
 from ._lib import (CapacityError, CudaError, GuardError, IoError, ParseError,  # noqa: F401
                    LIB_PATH, lib)
 from .engine import (EngineConfig, IterationReport, NfEngine, NfEstimate,  # noqa: F401
-                     SketchParams, Termination, estimate_nf, multirun)
+                     SketchParams, Termination, estimate_nf, multirun, ExactNf,
+                     exact_nf)
 from .graph import (Graph, gen_barabasi_albert, gen_clique_path, gen_copying,  # noqa: F401
                     gen_erdos_renyi, gen_rmat, gen_uniform_random, load_csr, save_csr,
                     transpose)
@@ -19,7 +20,7 @@ from .stats import (aggregate_runs, cdf_from_nf, diameter_interval,  # noqa: F40
 
 __all__ = [
     "EngineConfig", "IterationReport", "NfEngine", "NfEstimate", "SketchParams",
-    "Termination", "estimate_nf", "multirun", "Graph", "transpose", "gen_uniform_random",
+    "Termination", "estimate_nf", "multirun", "ExactNf", "exact_nf", "Graph", "transpose", "gen_uniform_random",
     "gen_clique_path", "gen_erdos_renyi", "gen_rmat", "gen_copying",
     "gen_barabasi_albert", "save_csr", "load_csr", "cdf_from_nf",
     "distribution_from_cdf", "distance_distribution", "effective_diameter",

@@ -60,6 +60,8 @@ _SIGNATURES = {
     "hanf_reset": [_P],
     "hanf_reseed": [_P, c_uint64],
     "hanf_save_counters": [_P, c_char_p],
+    "hanf_exact_nf": [POINTER(GraphView), c_int32, c_uint64, c_uint64, POINTER(c_uint64),
+                      c_uint64, POINTER(c_uint64)],
     "hanf_restore_counters": [_P, c_char_p, c_uint64],
     "hanf_sum_estimates": [_P, POINTER(c_double)],
     "hanf_step": [_P, POINTER(IterationReportC)],

@@ -298,6 +298,38 @@ def estimate_nf(g: Graph, cfg: EngineConfig = None) -> NfEstimate:
         return engine.run_to_stabilisation()
 
 
+@dataclass
+class ExactNf:
+    """oracle.hpp:24-35: values[t] = ordered pairs (x, y) with d(x, y) <= t."""
+    n: int = 0
+    values: List[int] = field(default_factory=list)
+
+    def diameter(self) -> int:
+        return 0 if not self.values else len(self.values) - 1
+
+    def as_doubles(self) -> List[float]:
+        return [float(v) for v in self.values]
+
+
+def exact_nf(g: Graph, device: int = 0, max_nodes: int = 1_000_000,
+             max_work: int = 100_000_000_000) -> ExactNf:
+    """oracle.hpp:38-104 (exact NF, same guard -> GuardError), computed on
+    the GPU as bitset balls (hanf_exact.cu) instead of all-pairs BFS."""
+    view = g.view()
+    cap = 64
+    while True:
+        vals = np.empty(cap, dtype=np.uint64)
+        length = c_uint64()
+        st = lib().hanf_exact_nf(ctypes.byref(view), device, max_nodes, max_work,
+                                 vals.ctypes.data_as(POINTER(c_uint64)), cap,
+                                 ctypes.byref(length))
+        if st == _lib.CAPACITY:
+            cap = length.value
+            continue
+        check(st)
+        return ExactNf(n=g.num_nodes(), values=[int(x) for x in vals[:length.value]])
+
+
 def multirun(g: Graph, cfg: EngineConfig = None, runs: int = 10, base_seed: int = None):
     """The reference's multirun (main.cpp:263-283): estimate_nf for seeds
     base_seed + i, i < runs (base_seed defaults to cfg.seed).  One engine:
