@@ -294,6 +294,49 @@ __device__ __forceinline__ void store_chunk(uint64_t* p, const uint32_t (&v)[Lay
   }
 }
 
+// Stores a whole counter (Lay::kWords words, 8-byte aligned) with 16-byte
+// stores where the address allows: NW = 5 costs 3 stores (one L1 wavefront
+// each) instead of 5.  The alignment is per lane (runtime).
+template <class Lay>
+__device__ __forceinline__ void store_counter(uint64_t* p, const uint32_t (&v)[Lay::kLimbs]) {
+  constexpr int NW = Lay::kWords;
+  constexpr int NL = Lay::kLimbs;
+  auto limb = [&](auto I) -> uint32_t {
+    constexpr int i = decltype(I)::value;
+    if constexpr (i < NL) return v[i]; else return 0u;
+  };
+  auto st16 = [&](auto K, int word) {  // limbs 2K .. 2K+3 at word `word`
+    constexpr int k = decltype(K)::value;
+    uint4 q;
+    q.x = limb(ic<2 * k + 0>{});
+    q.y = limb(ic<2 * k + 1>{});
+    q.z = limb(ic<2 * k + 2>{});
+    q.w = limb(ic<2 * k + 3>{});
+    *reinterpret_cast<uint4*>(p + word) = q;
+  };
+  auto st8 = [&](auto K, int word) {  // limbs 2K, 2K+1 at word `word`
+    constexpr int k = decltype(K)::value;
+    uint2 q;
+    q.x = limb(ic<2 * k + 0>{});
+    q.y = limb(ic<2 * k + 1>{});
+    *reinterpret_cast<uint2*>(p + word) = q;
+  };
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    sfor<0, NW / 2>([&](auto I) {
+      constexpr int k = decltype(I)::value;
+      st16(ic<2 * k>{}, 2 * k);
+    });
+    if constexpr (NW % 2) st8(ic<NW - 1>{}, NW - 1);
+  } else {
+    st8(ic<0>{}, 0);
+    sfor<0, (NW - 1) / 2>([&](auto I) {
+      constexpr int k = decltype(I)::value;
+      st16(ic<2 * k + 1>{}, 2 * k + 1);
+    });
+    if constexpr (NW % 2 == 0) st8(ic<NW - 1>{}, NW - 1);
+  }
+}
+
 template <class Lay>
 __device__ __forceinline__ bool limbs_differ(const uint32_t (&x)[Lay::kLimbs],
                                              const uint32_t (&y)[Lay::kLimbs]) {

@@ -285,8 +285,13 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
     own_load(own);
     const bool changed = lead && limbs_differ<Lay>(acc, own);
     any_changed |= changed;
-    if (changed || (lead && stale))
-      store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
+    if (changed || (lead && stale)) {
+      uint64_t* dst = args.next + static_cast<uint64_t>(v) * words + woff;
+      if (args.chunks == 1)
+        store_counter<Lay>(dst, acc);
+      else
+        store_chunk<Lay, kVec16>(dst, acc);
+    }
     if (changed && args.est) args.est[est_slot(args.orig_of, v)] = estimate_limbs<Lay>(acc, args.ep);
   }
 }
