@@ -248,7 +248,9 @@ struct hanf_engine {
   CUtensorMap tmap[2];        // descriptors of cnt[0], cnt[1]
 
   hanf::ReduceOut* h_reduce = nullptr;  // pinned (cache): total + count
-  double* h_block_sums = nullptr;       // pinned (cache): exact_sum mode
+  // pinned (cache), exact_sum mode: one per generation parity, so a step
+  // can be launched while the previous step's block sums are summed
+  double* h_block_sums[2] = {nullptr, nullptr};
 
   int cur = 0;               // index of the current generation
   uint64_t t = 0;            // iteration()
@@ -332,7 +334,8 @@ struct hanf_engine {
       phase("free");
     }
     pinned().put(h_reduce);
-    pinned().put(h_block_sums);
+    pinned().put(h_block_sums[0]);
+    pinned().put(h_block_sums[1]);
   }
 };
 
@@ -404,9 +407,18 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   HANF_CUDA(cudaMemcpyAsync(e->h_reduce, e->reduce, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                             e->stream));
   if (e->cfg.exact_sum)
-    HANF_CUDA(cudaMemcpyAsync(e->h_block_sums, e->block_sums, sizeof(double) * e->blocks,
+    HANF_CUDA(cudaMemcpyAsync(e->h_block_sums[e->cur], e->block_sums, sizeof(double) * e->blocks,
                               cudaMemcpyDeviceToHost, e->stream));
   return HANF_OK;
+}
+
+// The reference's summation order of the block sums (engine.hpp:115-117),
+// from the host copy made by the step launched at generation `parity`.
+double host_block_total(const hanf_engine* e, int parity) {
+  double s = 0.0;
+  const double* b = e->h_block_sums[parity];
+  for (uint64_t i = 0; i < e->blocks; ++i) s += b[i];
+  return s;
 }
 
 hanf_status finish_complete(hanf_engine* e, double* total, uint64_t* count, bool in_step) {
@@ -422,9 +434,7 @@ hanf_status finish_complete(hanf_engine* e, double* total, uint64_t* count, bool
     ++e->timed_steps;
   }
   if (e->cfg.exact_sum) {
-    double s = 0.0;
-    for (uint64_t b = 0; b < e->blocks; ++b) s += e->h_block_sums[b];
-    *total = s;
+    *total = host_block_total(e, e->cur);
   } else {
     *total = e->h_reduce->total;
   }
@@ -655,6 +665,18 @@ hanf_status commit_enqueue(hanf_engine* e) {
   return finish_enqueue(e, dirty_of(e, ng), commit_recomputes(e), 0, e->blocks, true);
 }
 
+// Generation swap and the per-step state after a step's modified count is
+// known (engine.hpp:198-216); N(t) is set by the caller.
+void advance_state(hanf_engine* e, uint64_t count) {
+  e->cur = 1 - e->cur;                             // std::swap, engine.hpp:198-200
+  e->stale_valid = true;
+  if (e->cfg.use_systolic && !e->systolic && count > 0 &&
+      static_cast<double>(count) < e->cfg.systolic_threshold * static_cast<double>(e->n))
+    e->systolic = true;                            // engine.hpp:211-216
+  ++e->t;
+  e->last_count = count;
+}
+
 hanf_status commit_complete(hanf_engine* e, hanf_iteration_report* rep) {
   double total = 0.0;
   uint64_t count = 0;
@@ -681,17 +703,25 @@ hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
 
 // One single-GPU step as a CUDA graph (memset + union + finish + read-back),
 // captured once per (generation parity, check_mod, stale_valid) and replayed.
-hanf_status step_graphed(hanf_engine* e, hanf_iteration_report* rep) {
+// Enqueues one whole single-GPU step (compute + finish + read-backs) on the
+// engine stream, graphed when allowed; the caller completes it.
+hanf_status step_enqueue(hanf_engine* e) {
+  note_step(e);
   const int mode = step_mode(e);
   if (mode == 2) {
     const hanf_status st = ensure_sparse(e);
     if (st != HANF_OK) return st;
   }
+  if (!e->use_graphs || e->timing) {
+    const hanf_status st = compute_local(e);
+    if (st != HANF_OK) return st;
+    return commit_enqueue(e);
+  }
   hanf_engine::StepGraph& G = e->graphs[e->cur][mode][e->stale_valid ? 1 : 0];
   if (!G.exec && ++G.uses < 3) {
     hanf_status st = compute_local(e);
     if (st != HANF_OK) return st;
-    return commit(e, rep);
+    return commit_enqueue(e);
   }
   if (!G.exec) {
     const uint64_t before = e->launches;
@@ -713,7 +743,7 @@ hanf_status step_graphed(hanf_engine* e, hanf_iteration_report* rep) {
   }
   HANF_CUDA(cudaGraphLaunch(G.exec, e->stream));
   e->launches += G.kernels;
-  return commit_complete(e, rep);
+  return HANF_OK;
 }
 
 }  // namespace
@@ -868,8 +898,10 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   e->h_reduce = static_cast<hanf::ReduceOut*>(pinned().get(sizeof(hanf::ReduceOut)));
   if (!e->h_reduce) return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
   if (cfg.exact_sum) {
-    e->h_block_sums = static_cast<double*>(pinned().get(sizeof(double) * (e->blocks ? e->blocks : 1)));
-    if (!e->h_block_sums) return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
+    for (auto& hb : e->h_block_sums) {
+      hb = static_cast<double*>(pinned().get(sizeof(double) * (e->blocks ? e->blocks : 1)));
+      if (!hb) return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
+    }
   }
   // linear-counting table m*log(m/z), same expression as hll.hpp:139
   {
@@ -1109,16 +1141,11 @@ hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
     return HANF_OK;
   }
   HANF_CUDA(cudaSetDevice(e->device));
-  note_step(e);
-  // phase timing needs events between the kernels: run ungraphed then
-  if (e->use_graphs && !e->timing) return step_graphed(e, rep);
-  if (step_mode(e) == 2) {
-    const hanf_status sst = ensure_sparse(e);
-    if (sst != HANF_OK) return sst;
-  }
-  hanf_status st = compute_local(e);
+  // (phase timing needs events between the kernels: step_enqueue runs
+  // ungraphed then)
+  const hanf_status st = step_enqueue(e);
   if (st != HANF_OK) return st;
-  return commit(e, rep);
+  return commit_complete(e, rep);
 }
 
 hanf_status hanf_shard_compute(hanf_engine* e) {
@@ -1163,7 +1190,35 @@ hanf_status hanf_run_to_stabilisation(hanf_engine* e, double* values, uint64_t* 
   std::vector<uint64_t> mods;
   vals.push_back(e->last_sum);
   mods.push_back(e->n);
-  for (;;) {
+  const bool sharded = e->lo != 0 || e->hi != e->n;
+  if (e->cfg.termination == 0 && !e->timing && !sharded) {
+    // Pipelined: once a step's modified count is known, the next step is
+    // launched before the host sums this step's block sums (exact_sum) -
+    // the next step reads only the count.  Same steps, same bits.
+    HANF_CUDA(cudaSetDevice(e->device));
+    hanf_status st = step_enqueue(e);
+    if (st != HANF_OK) return st;
+    for (;;) {
+      const int parity = e->cur;
+      HANF_CUDA(cudaStreamSynchronize(e->stream));
+      const uint64_t count = e->h_reduce->count;
+      const double dev_total = e->h_reduce->total;
+      advance_state(e, count);
+      if (count == 0) break;  // the stabilising step is not recorded
+      const bool capped = vals.size() >= e->cfg.max_iterations;  // no further step allowed
+      if (!capped) {
+        st = step_enqueue(e);
+        if (st != HANF_OK) return st;
+      }
+      const double total = e->cfg.exact_sum ? host_block_total(e, parity) : dev_total;
+      e->last_sum = total;
+      vals.push_back(total);
+      mods.push_back(count);
+      if (capped)
+        return fail(HANF_GUARD, "engine: iteration cap " + std::to_string(e->cfg.max_iterations) +
+                                    " exceeded; pathological input or bug");
+    }
+  } else for (;;) {
     if (vals.size() - 1 >= e->cfg.max_iterations)
       return fail(HANF_GUARD, "engine: iteration cap " + std::to_string(e->cfg.max_iterations) +
                                   " exceeded; pathological input or bug");

@@ -5,9 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1011_5599_b200 as h
 g = h.gen_rmat(20, 16, 0.57, 0.19, 0.19, 1, 7)
-off = torch.from_numpy(g.offsets().view("int64")).pin_memory()
-arc = torch.from_numpy(g.arcs().view("int32")).pin_memory()
-pg = h.Graph(g.num_nodes(), off.numpy().view("uint64"), arc.numpy().view("uint32"))
+pg = h.Graph(g.num_nodes(), g.offsets().copy(), g.arcs().copy()).pin()
 torch.cuda.init()
 cfg = h.EngineConfig(bucket_bits=6, seed=42, exact_sum=False)
 for k in range(4):
