@@ -109,6 +109,19 @@ hanf_status hanf_sketch_params_make(uint32_t bucket_bits, uint64_t seed,
 hanf_status hanf_create(const hanf_graph_view* graph, const hanf_config* cfg,
                         hanf_engine** out);
 void hanf_destroy(hanf_engine* engine);
+/* (new) `runs` independent runs in one engine, run k under
+ * seeds[k] (main.cpp:263-283 multirun): the graph is lifted to `runs`
+ * copies (row v*runs + k) so one gather serves a node's runs together.
+ * runs in {2, 4, 8} (1: hanf_create with seeds[0]); n * runs < 2^32; not
+ * sharded.  Drive it with hanf_run_batch (hanf_step and the single-run
+ * calls return HANF_INVALID_ARGUMENT). */
+hanf_status hanf_create_batch(const hanf_graph_view* graph, const hanf_config* cfg,
+                              const uint64_t* seeds, uint32_t runs, hanf_engine** out);
+/* run_to_stabilisation (engine.hpp:233-275) of every run: run k's N(t)
+ * and modified counts at values/modified[k*cap + t], t < lengths[k];
+ * HANF_CAPACITY (lengths set) when a run needs more than cap. */
+hanf_status hanf_run_batch(hanf_engine* engine, double* values, uint64_t* modified,
+                           uint64_t cap, uint64_t* lengths);
 /* Re-seeds the counters and rewinds to iteration 0 (a fresh NfEngine on
  * the same graph, without re-uploading it). */
 hanf_status hanf_reset(hanf_engine* engine);

@@ -59,6 +59,9 @@ _SIGNATURES = {
     "hanf_create": [POINTER(GraphView), POINTER(Config), POINTER(_P)],
     "hanf_reset": [_P],
     "hanf_reseed": [_P, c_uint64],
+    "hanf_create_batch": [POINTER(GraphView), POINTER(Config), POINTER(c_uint64), c_uint32,
+                          POINTER(_P)],
+    "hanf_run_batch": [_P, POINTER(c_double), POINTER(c_uint64), c_uint64, POINTER(c_uint64)],
     "hanf_save_counters": [_P, c_char_p],
     "hanf_exact_nf": [POINTER(GraphView), c_int32, c_uint64, c_uint64, POINTER(c_uint64),
                       c_uint64, POINTER(c_uint64)],

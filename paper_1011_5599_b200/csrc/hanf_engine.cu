@@ -30,6 +30,7 @@
 
 #include "../../include/hanf.h"
 #include "hanf_internal.h"
+#include "hanf_rng.h"
 
 namespace {
 
@@ -240,6 +241,18 @@ struct hanf_engine {
   // locality relabelling (hanf_relabel.cu): the device works on rows;
   // order[row] = original id, perm[id] = row; dirty[g] = original-id
   // bitmaps of changed counters for the block sums (mod[g] is in rows)
+  // batched runs (hanf_batch.cu): `batch` runs over the lifted graph, n =
+  // n_real * batch rows; run k's seed mix and per-run sums
+  uint32_t batch = 1;
+  uint64_t n_real = 0;
+  uint64_t blocks_real = 0;
+  std::vector<uint64_t> batch_seeds;
+  uint64_t* batch_mix = nullptr;                  // device [batch]
+  double* batch_sums = nullptr;                   // device [batch][blocks_real]
+  unsigned long long* batch_counts = nullptr;     // device [batch]
+  unsigned long long* h_batch_counts = nullptr;   // pinned [batch]
+  double* h_batch_sums[2] = {nullptr, nullptr};   // pinned [batch][blocks_real] per parity
+  std::vector<double> batch_last;                 // N(t) of every run
   bool relabel = false;
   uint32_t* order = nullptr;
   uint32_t* perm = nullptr;
@@ -320,6 +333,9 @@ struct hanf_engine {
       pfree(work, stream);
       pfree(hub_tasks, stream);
       pfree(hub_index, stream);
+      pfree(batch_mix, stream);
+      pfree(batch_sums, stream);
+      pfree(batch_counts, stream);
       pfree(order, stream);
       pfree(perm, stream);
       pfree(rl_off, stream);
@@ -336,6 +352,9 @@ struct hanf_engine {
     pinned().put(h_reduce);
     pinned().put(h_block_sums[0]);
     pinned().put(h_block_sums[1]);
+    pinned().put(h_batch_counts);
+    pinned().put(h_batch_sums[0]);
+    pinned().put(h_batch_sums[1]);
   }
 };
 
@@ -451,6 +470,32 @@ hanf_status finish(hanf_engine* e, const uint64_t* bits, bool recompute, uint64_
 
 // Seeds both generations (every engine seeds all n counters: seeding is a
 // pure function of (v, seed), so shards need no exchange) and computes N(0).
+// Batched runs: per-run dirty flags, counts and block sums of the generation
+// `bits` describes, read back into the pinned buffers of parity e->cur.
+hanf_status batch_enqueue(hanf_engine* e, const uint64_t* bits) {
+  HANF_CUDA(hanf::launch_finish_batch(e->est, bits, e->n_real, e->batch, true, e->batch_sums,
+                                      e->batch_counts, e->stream, &e->launches));
+  HANF_CUDA(cudaMemcpyAsync(e->h_batch_counts, e->batch_counts,
+                            sizeof(unsigned long long) * e->batch, cudaMemcpyDeviceToHost,
+                            e->stream));
+  HANF_CUDA(cudaMemcpyAsync(e->h_batch_sums[e->cur], e->batch_sums,
+                            sizeof(double) * e->batch * e->blocks_real, cudaMemcpyDeviceToHost,
+                            e->stream));
+  return HANF_OK;
+}
+// N(t) of every run from the block sums read back at `parity`, summed in
+// the reference's order (engine.hpp:115-117); counts[k] when non-null.
+void batch_totals(hanf_engine* e, int parity, uint64_t* counts) {
+  e->batch_last.assign(e->batch, 0.0);
+  for (uint32_t k = 0; k < e->batch; ++k) {
+    const double* b = e->h_batch_sums[parity] + static_cast<uint64_t>(k) * e->blocks_real;
+    double s = 0.0;
+    for (uint64_t i = 0; i < e->blocks_real; ++i) s += b[i];
+    e->batch_last[k] = s;
+    if (counts) counts[k] = e->h_batch_counts[k];
+  }
+}
+
 hanf_status seed_all(hanf_engine* e) {
   e->cur = 0;
   e->t = 0;
@@ -459,7 +504,7 @@ hanf_status seed_all(hanf_engine* e) {
   HANF_CUDA(hanf::launch_seed(e->cnt[0], e->cnt[1], e->mod[0], e->n, 0, e->n,
                               e->params.bucket_bits, e->params.register_bits,
                               e->params.words_per_counter, static_cast<uint32_t>(e->pitch),
-                              e->params.seed, e->order, e->stream,
+                              e->params.seed, e->order, e->batch, e->batch_mix, e->stream,
                               &e->launches));
   HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
   if (e->relabel) {  // every counter was seeded: all ones in both id spaces
@@ -471,6 +516,14 @@ hanf_status seed_all(hanf_engine* e) {
   if (st != HANF_OK) return st;
   uint64_t count = 0;
   e->last_count = e->n;
+  if (e->batch > 1) {  // N(0) of every run, in the reference's order
+    st = batch_enqueue(e, e->mod[0]);
+    if (st != HANF_OK) return st;
+    HANF_CUDA(cudaStreamSynchronize(e->stream));
+    batch_totals(e, e->cur, nullptr);
+    e->last_sum = e->batch_last[0];
+    return HANF_OK;
+  }
   return finish(e, dirty_of(e, 0), false, 0, 0, &e->last_sum, &count);
 }
 
@@ -662,6 +715,7 @@ bool commit_recomputes(const hanf_engine* e) {
 
 hanf_status commit_enqueue(hanf_engine* e) {
   const int ng = 1 - e->cur;
+  if (e->batch > 1) return batch_enqueue(e, e->mod[ng]);
   return finish_enqueue(e, dirty_of(e, ng), commit_recomputes(e), 0, e->blocks, true);
 }
 
@@ -779,24 +833,35 @@ hanf_status hanf_sketch_params_make(uint32_t b, uint64_t seed, uint32_t r, hanf_
   return make_params(b, seed, r, out);
 }
 
-hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, hanf_engine** out) {
+// One engine; K > 1 = K batched runs over the lifted graph (hanf_batch.cu).
+static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cfg_in,
+                                 const uint64_t* seeds, uint32_t K, hanf_engine** out) {
   if (!g || !cfg_in || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   const auto t_create0 = std::chrono::steady_clock::now();
   hanf_status st = validate_config(cfg_in);
   if (st != HANF_OK) return st;
-  const uint64_t n = g->n;
-  if (n > (1ull << 32) - 1)
+  const uint64_t n_real = g->n;
+  if (n_real > (1ull << 32) - 1)
     return fail(HANF_INVALID_ARGUMENT, "graph too large for 32-bit node ids");
-  if (n > 0 && !g->offsets) return fail(HANF_INVALID_ARGUMENT, "null offsets");
-  if (n > 0 && (g->offsets[0] != 0 || g->offsets[n] != g->num_arcs))
+  if (n_real > 0 && !g->offsets) return fail(HANF_INVALID_ARGUMENT, "null offsets");
+  if (n_real > 0 && (g->offsets[0] != 0 || g->offsets[n_real] != g->num_arcs))
     return fail(HANF_INVALID_ARGUMENT, "offsets must run from 0 to the arc count");
   if (g->num_arcs > 0 && !g->arcs) return fail(HANF_INVALID_ARGUMENT, "null arcs");
+  if (K > 1) {
+    if (K != 2 && K != 4 && K != 8)
+      return fail(HANF_INVALID_ARGUMENT, "batched runs: runs must be 2, 4 or 8");
+    if (n_real * K > (1ull << 32) - 1)
+      return fail(HANF_INVALID_ARGUMENT, "batched runs: n * runs must stay below 2^32");
+    if (cfg_in->shard_begin != 0 || cfg_in->shard_end != 0)
+      return fail(HANF_INVALID_ARGUMENT, "batched runs cannot be sharded");
+  }
+  const uint64_t n = n_real * K;  // rows (= nodes unless batched)
 
   hanf_config cfg = *cfg_in;
-  if (cfg.max_iterations == 0) cfg.max_iterations = n + 1;  // engine.hpp:78
+  if (cfg.max_iterations == 0) cfg.max_iterations = n_real + 1;  // engine.hpp:78
   uint32_t r = cfg.register_bits;
-  if (r == 0) r = n < (1ull << 32) ? 5 : 6;                  // engine.hpp:79-80
+  if (r == 0) r = n_real < (1ull << 32) ? 5 : 6;                 // engine.hpp:79-80
   hanf_sketch_params params;
   st = make_params(cfg.bucket_bits, cfg.seed, r, &params);
   if (st != HANF_OK) return st;
@@ -812,6 +877,10 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   e->cfg = cfg;
   e->params = params;
   e->n = n;
+  e->batch = K;
+  e->n_real = n_real;
+  e->blocks_real = (n_real + 63) / 64;
+  if (K > 1) e->batch_seeds.assign(seeds, seeds + K);
   e->lo = lo;
   e->hi = hi;
   e->blocks = (n + 63) / 64;
@@ -826,7 +895,7 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   // less than the worklist's launches); profiles/r01_sparse.md.
   e->sparse_ok = hanf::sparse_supported(params.register_bits, params.registers) &&
                  hanf::fused_estimates(params.register_bits, params.registers) &&
-                 n > 0 && g->offsets[hi] - g->offsets[lo] >= (1ull << 22);
+                 n > 0 && (K > 1 ? g->num_arcs * K : g->offsets[hi] - g->offsets[lo]) >= (1ull << 22);
   {
     const char* sp = std::getenv("HANF_SPARSE");
     if (sp && sp[0] == '0') e->sparse_ok = false;
@@ -841,7 +910,7 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   // HANF_RELABEL=1/0 forces it; by default graphs whose counters do not fit
   // in L2 (one generation > 64 MB) and whose ids show no locality (sampled
   // successors far from their source) are renumbered by degree.
-  if (lo == 0 && hi == n && n > 0) {
+  if (lo == 0 && hi == n && n > 0 && K == 1) {
     const char* rl = std::getenv("HANF_RELABEL");
     if (rl && (rl[0] == '0' || rl[0] == '1'))
       e->relabel = rl[0] == '1';
@@ -932,10 +1001,12 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   if (n > 0) {
     // the shard's CSR goes to the device to build the tasks (it is laid
     // out again in task order there) and stays for the worklist step
-    const uint64_t a0 = g->offsets[lo], a1 = g->offsets[hi];
+    // (batched runs upload the caller's graph and lift it on the device)
+    const uint64_t up_lo = K > 1 ? 0 : lo, up_hi = K > 1 ? n_real : hi;
+    uint64_t a0 = g->offsets[up_lo], a1 = g->offsets[up_hi];
     uint64_t* d_off = nullptr;
     uint32_t* d_succ = nullptr;
-    HANF_TRY(palloc(&d_off, hi - lo + 1, s));
+    HANF_TRY(palloc(&d_off, up_hi - up_lo + 1, s));
     HANF_TRY(palloc(&d_succ, a1 - a0, s));
     // offsets first on the engine stream; the arcs follow on a helper
     // stream while the engine stream seeds and sorts by degree (only the
@@ -960,7 +1031,7 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
     guard.a = ev_off;
     HANF_TRY(cudaEventCreateWithFlags(&ev_arcs, cudaEventDisableTiming));
     guard.b = ev_arcs;
-    HANF_TRY(cudaMemcpyAsync(d_off, g->offsets + lo, sizeof(uint64_t) * (hi - lo + 1),
+    HANF_TRY(cudaMemcpyAsync(d_off, g->offsets + up_lo, sizeof(uint64_t) * (up_hi - up_lo + 1),
                              cudaMemcpyHostToDevice, s));
     HANF_TRY(cudaEventRecord(ev_off, s));
     HANF_TRY(cudaStreamWaitEvent(s2, ev_off, 0));
@@ -969,6 +1040,38 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
                                cudaMemcpyHostToDevice, s2));
     HANF_TRY(cudaEventRecord(ev_arcs, s2));
     phase("offsets");
+    if (K > 1) {
+      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+      uint64_t* voff = nullptr;
+      uint32_t* vsucc = nullptr;
+      const cudaError_t le = hanf::lift_graph_device(d_off, d_succ, n_real, a1 - a0, K, s, &voff,
+                                                     &vsucc, &e->launches);
+      cudaFreeAsync(d_off, s);
+      cudaFreeAsync(d_succ, s);
+      d_off = voff;
+      d_succ = vsucc;
+      e->csr_off = d_off;  // owned by the engine from here on
+      e->csr_succ = d_succ;
+      HANF_TRY(le);
+      a1 = (a1 - a0) * K;
+      a0 = 0;
+      // run k's seed mix (item_hash, hash.hpp:20-22) and the per-run sums
+      std::vector<uint64_t> mix(K);
+      for (uint32_t k = 0; k < K; ++k) mix[k] = hanf_rng::mix64(seeds[k] ^ 0x9e3779b97f4a7c15ULL);
+      HANF_TRY(palloc(&e->batch_mix, K, s));
+      HANF_TRY(cudaMemcpyAsync(e->batch_mix, mix.data(), sizeof(uint64_t) * K,
+                               cudaMemcpyHostToDevice, s));
+      HANF_TRY(palloc(&e->batch_sums, static_cast<uint64_t>(K) * e->blocks_real, s));
+      HANF_TRY(palloc(&e->batch_counts, K, s));
+      HANF_TRY(cudaStreamSynchronize(s));  // `mix` is a stack object
+      e->h_batch_counts = static_cast<unsigned long long*>(
+          pinned().get(sizeof(unsigned long long) * K));
+      for (auto& hb : e->h_batch_sums)
+        hb = static_cast<double*>(pinned().get(sizeof(double) * K * (e->blocks_real + 1)));
+      if (!e->h_batch_counts || !e->h_batch_sums[0] || !e->h_batch_sums[1])
+        return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
+      phase("lift");
+    }
     if (e->relabel) {
       // renumber rows by out-degree (offsets only: overlaps the arcs upload)
       hanf::RelabelOut r;
@@ -1009,6 +1112,81 @@ hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg_in, han
   return HANF_OK;
 }
 
+hanf_status hanf_create(const hanf_graph_view* g, const hanf_config* cfg, hanf_engine** out) {
+  return create_engine(g, cfg, nullptr, 1, out);
+}
+
+hanf_status hanf_create_batch(const hanf_graph_view* g, const hanf_config* cfg,
+                              const uint64_t* seeds, uint32_t runs, hanf_engine** out) {
+  if (!seeds) return fail(HANF_INVALID_ARGUMENT, "null seeds");
+  if (runs == 1) {
+    if (!cfg) return fail(HANF_INVALID_ARGUMENT, "null argument");
+    hanf_config c = *cfg;
+    c.seed = seeds[0];
+    return create_engine(g, &c, nullptr, 1, out);
+  }
+  return create_engine(g, cfg, seeds, runs, out);
+}
+
+// run_to_stabilisation of every batched run (engine.hpp:233-275 per run):
+// pipelined like the single run; run k's series ends at its own
+// stabilisation (a run whose counters stopped changing never changes again).
+hanf_status hanf_run_batch(hanf_engine* e, double* values, uint64_t* modified, uint64_t cap,
+                           uint64_t* lengths) {
+  if (!e || !lengths) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->batch < 2) return fail(HANF_INVALID_ARGUMENT, "not a batched engine (hanf_create_batch)");
+  const uint32_t K = e->batch;
+  std::vector<std::vector<double>> vals(K);
+  std::vector<std::vector<uint64_t>> mods(K);
+  for (uint32_t k = 0; k < K; ++k) {
+    vals[k].push_back(e->batch_last.empty() ? 0.0 : e->batch_last[k]);
+    mods[k].push_back(e->n_real);
+  }
+  if (e->n > 0) {
+    HANF_CUDA(cudaSetDevice(e->device));
+    hanf_status st = step_enqueue(e);
+    if (st != HANF_OK) return st;
+    std::vector<uint64_t> counts(K);
+    uint64_t steps = 0;
+    for (;;) {
+      const int parity = e->cur;
+      HANF_CUDA(cudaStreamSynchronize(e->stream));
+      uint64_t total = 0;
+      for (uint32_t k = 0; k < K; ++k) total += (counts[k] = e->h_batch_counts[k]);
+      advance_state(e, total);
+      ++steps;
+      if (total == 0) break;
+      const bool capped = steps >= e->cfg.max_iterations;
+      if (!capped) {
+        st = step_enqueue(e);
+        if (st != HANF_OK) return st;
+      }
+      batch_totals(e, parity, nullptr);
+      for (uint32_t k = 0; k < K; ++k)
+        if (counts[k]) {
+          vals[k].push_back(e->batch_last[k]);
+          mods[k].push_back(counts[k]);
+        }
+      if (capped)
+        return fail(HANF_GUARD, "engine: iteration cap " + std::to_string(e->cfg.max_iterations) +
+                                    " exceeded; pathological input or bug");
+    }
+  }
+  bool fits = true;
+  for (uint32_t k = 0; k < K; ++k) {
+    auto& v = vals[k];
+    for (size_t t = 1; t < v.size(); ++t) v[t] = std::max(v[t], v[t - 1]);
+    lengths[k] = v.size();
+    fits = fits && v.size() <= cap;
+  }
+  if (!fits) return fail(HANF_CAPACITY, "output capacity too small for a batched run");
+  for (uint32_t k = 0; k < K; ++k) {
+    if (values) std::copy(vals[k].begin(), vals[k].end(), values + static_cast<uint64_t>(k) * cap);
+    if (modified) std::copy(mods[k].begin(), mods[k].end(), modified + static_cast<uint64_t>(k) * cap);
+  }
+  return HANF_OK;
+}
+
 void hanf_destroy(hanf_engine* e) { delete e; }
 
 
@@ -1036,6 +1214,7 @@ uint64_t get_le(const unsigned char* p, int bytes) {
 // hll.hpp:275-286: "HCA1", u32 b, u32 r, u64 n, u64 seed, n*W words (LE).
 hanf_status hanf_save_counters(hanf_engine* e, const char* path) {
   if (!e || !path) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: no single counter array");
   std::vector<uint64_t> words(e->n * e->words);
   if (e->n) {
     const hanf_status st = hanf_read_counters(e, 0, e->n, words.data());
@@ -1059,6 +1238,7 @@ hanf_status hanf_save_counters(hanf_engine* e, const char* path) {
 // hll.hpp:288-303 load_counters, into a running engine (resume).
 hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t iteration) {
   if (!e || !path) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: no single counter array");
   std::FILE* f = std::fopen(path, "rb");
   if (!f) return fail(HANF_IO_ERROR, std::string("cannot open: ") + path);
   unsigned char h[28];
@@ -1122,6 +1302,7 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
 
 hanf_status hanf_reseed(hanf_engine* e, uint64_t seed) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: seeds are fixed at creation");
   e->cfg.seed = seed;
   e->params.seed = seed;  // only the seeding hash reads it (engine.hpp:84-85)
   return hanf_reset(e);
@@ -1135,6 +1316,7 @@ hanf_status hanf_sum_estimates(hanf_engine* e, double* sum) {
 
 hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
   if (!e || !rep) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: use hanf_run_batch");
   if (e->n == 0) {                       // engine.hpp:124
     rep->sum = 0.0;
     rep->modified = 0;
@@ -1174,6 +1356,7 @@ hanf_status hanf_shard_commit(hanf_engine* e, hanf_iteration_report* rep) {
 hanf_status hanf_run_to_stabilisation(hanf_engine* e, double* values, uint64_t* modified,
                                       uint64_t capacity, uint64_t* length, double* wall) {
   if (!e || !length) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: use hanf_run_batch");
   const auto start = std::chrono::steady_clock::now();
   *length = 0;
   if (wall) *wall = 0.0;

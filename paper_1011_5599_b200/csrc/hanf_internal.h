@@ -189,7 +189,16 @@ struct EstimateArgs {
 cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
                         uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
-                        const uint32_t* orig_of, cudaStream_t s, uint64_t* launches);
+                        const uint32_t* orig_of, uint32_t batch, const uint64_t* batch_mix,
+                        cudaStream_t s, uint64_t* launches);
+// Batched runs (hanf_batch.cu): the K-fold lifted CSR (row v*K + k), and
+// the per-run block sums / modified counts of a generation.
+cudaError_t lift_graph_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n, uint64_t arcs,
+                              uint32_t K, cudaStream_t s, uint64_t** voff, uint32_t** vsucc,
+                              uint64_t* launches);
+cudaError_t launch_finish_batch(const double* est, const uint64_t* bits, uint64_t n_real, uint32_t K,
+                                bool recompute, double* block_sums, unsigned long long* counts,
+                                cudaStream_t s, uint64_t* launches);
 // map: TMA descriptor of args.cur for the gather4 kernel (nullptr: LDG
 // gathers; only single-chunk layouts with an even pitch take it)
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits,

@@ -36,13 +36,20 @@ __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
                             uint64_t* __restrict__ mod, uint64_t n, uint64_t node_begin,
                             uint64_t node_end, uint32_t bucket_bits, uint32_t register_bits,
                             uint32_t words, uint32_t pitch, uint64_t seed_mix,
-                            const uint32_t* __restrict__ orig_of) {
+                            const uint32_t* __restrict__ orig_of, uint32_t batch,
+                            const uint64_t* __restrict__ batch_mix) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = node_begin + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
        v < node_end; v += stride) {
-    // counter_add(v, v): the item is the node's original id (hash.hpp:20-22)
-    const uint64_t item = orig_of ? orig_of[v] : v;
-    const uint64_t h = mix64(item ^ seed_mix);
+    // counter_add(v, v): the item is the node's original id (hash.hpp:20-22);
+    // batched runs: row v is node v / batch of run v % batch
+    uint64_t item = orig_of ? orig_of[v] : v;
+    uint64_t mix = seed_mix;
+    if (batch > 1) {
+      item = v / batch;
+      mix = batch_mix[v % batch];
+    }
+    const uint64_t h = mix64(item ^ mix);
     const uint32_t bucket = static_cast<uint32_t>(h >> (64 - bucket_bits));
     const uint64_t rest = h << bucket_bits;
     uint32_t rho = rest == 0 ? (64 - bucket_bits) + 1 : __clzll(rest) + 1;
@@ -76,7 +83,8 @@ __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
 cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
                         uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
-                        const uint32_t* orig_of, cudaStream_t s, uint64_t* launches) {
+                        const uint32_t* orig_of, uint32_t batch, const uint64_t* batch_mix,
+                        cudaStream_t s, uint64_t* launches) {
   if (node_end <= node_begin) return cudaSuccess;
   const uint64_t items = node_end - node_begin;
   const uint32_t threads = 256;
@@ -84,7 +92,7 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
   if (blocks > 148ull * 64) blocks = 148ull * 64;
   seed_kernel<<<static_cast<uint32_t>(blocks), threads, 0, s>>>(
       a, b, mod, n, node_begin, node_end, bucket_bits, register_bits, words, pitch,
-      mix64(seed ^ 0x9e3779b97f4a7c15ULL), orig_of);
+      mix64(seed ^ 0x9e3779b97f4a7c15ULL), orig_of, batch, batch_mix);
   ++*launches;
   return cudaGetLastError();
 }

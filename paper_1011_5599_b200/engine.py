@@ -330,16 +330,67 @@ def exact_nf(g: Graph, device: int = 0, max_nodes: int = 1_000_000,
         return ExactNf(n=g.num_nodes(), values=[int(x) for x in vals[:length.value]])
 
 
-def multirun(g: Graph, cfg: EngineConfig = None, runs: int = 10, base_seed: int = None):
+def _run_batch(g: Graph, cfg: EngineConfig, seeds) -> List[NfEstimate]:
+    """len(seeds) in {2, 4, 8} runs in one batched engine (hanf_create_batch)."""
+    import time
+    k = len(seeds)
+    h = c_void_p()
+    view = g.view()
+    ccfg = cfg.to_c()
+    sarr = (c_uint64 * k)(*[s_ & 0xFFFFFFFFFFFFFFFF for s_ in seeds])
+    check(lib().hanf_create_batch(ctypes.byref(view), ctypes.byref(ccfg), sarr, k,
+                                  ctypes.byref(h)))
+    try:
+        p = _lib.SketchParamsC()
+        check(lib().hanf_params(h, ctypes.byref(p)))
+        cap = 64
+        while True:
+            vals = np.empty(k * cap, dtype=np.float64)
+            mods = np.empty(k * cap, dtype=np.uint64)
+            lens = (c_uint64 * k)()
+            t0 = time.perf_counter()
+            st = lib().hanf_run_batch(h, vals.ctypes.data_as(POINTER(c_double)),
+                                      mods.ctypes.data_as(POINTER(c_uint64)), cap, lens)
+            wall = time.perf_counter() - t0
+            if st == _lib.CAPACITY:
+                cap = max(lens)
+                check(lib().hanf_reset(h))
+                continue
+            check(st)
+            break
+        return [NfEstimate(n=g.num_nodes(), m=p.registers, seed=seeds[i],
+                           termination=cfg.termination,
+                           values=[float(x) for x in vals[i * cap:i * cap + lens[i]]],
+                           modified=[int(x) for x in mods[i * cap:i * cap + lens[i]]],
+                           wall_seconds=wall / k) for i in range(k)]
+    finally:
+        lib().hanf_destroy(h)
+
+
+def multirun(g: Graph, cfg: EngineConfig = None, runs: int = 10, base_seed: int = None,
+             batch: int = 1):
     """The reference's multirun (main.cpp:263-283): estimate_nf for seeds
-    base_seed + i, i < runs (base_seed defaults to cfg.seed).  One engine:
-    the graph is uploaded and laid out once, then re-seeded per run.
-    Aggregate with stats.aggregate_runs."""
+    base_seed + i, i < runs (base_seed defaults to cfg.seed).  batch = 1:
+    one engine re-seeded per run (the graph is uploaded and laid out once);
+    batch in {2, 4, 8}: that many runs at a time in one batched engine
+    (hanf_create_batch).  Bit-identical either way; aggregate with
+    stats.aggregate_runs."""
     import dataclasses
     cfg = dataclasses.replace(cfg) if cfg is not None else EngineConfig()
     base = cfg.seed if base_seed is None else base_seed
     out = []
     if runs <= 0:
+        return out
+    if batch > 1:
+        i = 0
+        while i < runs:
+            k = next(b for b in (8, 4, 2, 1) if b <= min(batch, runs - i))
+            seeds = [base + i + j for j in range(k)]
+            if k == 1:
+                out.append(estimate_nf(g, dataclasses.replace(cfg, seed=seeds[0])))
+            else:
+                out.extend(_run_batch(g, cfg, seeds))
+            i += k
         return out
     cfg.seed = base
     with NfEngine(g, cfg) as engine:

@@ -475,3 +475,39 @@ def test_hca1_snapshot_and_resume(hanf, ref, tmp_path, monkeypatch):
         bad.write_bytes(b"XXXX" + bytes(40))
         with pytest.raises(Exception):
             e.restore_counters(bad)
+
+
+@pytest.mark.parametrize("batch", [2, 4, 8])
+def test_batched_runs_equal_single_runs(hanf, monkeypatch, batch):
+    """Batched runs (hanf_create_batch: the graph lifted to K copies) give
+    every seed's estimate_nf bit for bit, over layouts, the worklist step and
+    a multi-chunk layout."""
+    for sparse in ("0", "1"):
+        monkeypatch.setenv("HANF_SPARSE", sparse)
+        for g, b, r in [(hanf.gen_rmat(11, 16, 0.57, 0.19, 0.19, 3, 8), 6, 5),
+                        (hanf.gen_clique_path(12, 30), 5, 5),
+                        (hanf.gen_uniform_random(1500, 3, 4), 8, 5),
+                        (hanf.gen_rmat(10, 8, 0.57, 0.19, 0.19, 5, 1), 5, 7)]:
+            cfg = hanf.EngineConfig(bucket_bits=b, register_bits=r, seed=1000)
+            runs = hanf.multirun(g, cfg, runs=batch + 1, batch=batch)
+            for i, est in enumerate(runs):
+                ref = hanf.estimate_nf(g, hanf.EngineConfig(bucket_bits=b, register_bits=r,
+                                                            seed=1000 + i))
+                assert est.values == ref.values and est.modified == ref.modified, (i, b, r)
+
+
+def test_batched_engine_rejects_single_run_calls(hanf):
+    import ctypes
+    from ctypes import c_uint64, c_void_p
+    g = hanf.gen_uniform_random(100, 2, 1)
+    view, cfg = g.view(), hanf.EngineConfig(bucket_bits=5).to_c()
+    seeds = (c_uint64 * 3)(1, 2, 3)
+    h = c_void_p()
+    assert hanf._lib.lib().hanf_create_batch(ctypes.byref(view), ctypes.byref(cfg), seeds, 3,
+                                             ctypes.byref(h)) != 0  # runs must be 2, 4, 8
+    seeds = (c_uint64 * 2)(1, 2)
+    hanf._lib.check(hanf._lib.lib().hanf_create_batch(ctypes.byref(view), ctypes.byref(cfg),
+                                                      seeds, 2, ctypes.byref(h)))
+    rep = hanf._lib.IterationReportC()
+    assert hanf._lib.lib().hanf_step(h, ctypes.byref(rep)) != 0
+    hanf._lib.lib().hanf_destroy(h)
