@@ -302,15 +302,19 @@ def test_config2_scale(hanf, port):
             assert np.array_equal(final[v], ball), v
 
 
-def test_sharded_engines_exchange(hanf, port):
+@pytest.mark.parametrize("b,env", [(6, {}), (6, {"HANF_SPARSE": "1"}), (5, {}), (8, {})])
+def test_sharded_engines_exchange(hanf, port, monkeypatch, b, env):
     """The shard ABI (hanf_shard_compute / device buffers / hanf_shard_commit)
     on one GPU: two node-range engines, exchange done by device copies in
-    sequence (no kernel waits on another), equal to one engine bit for bit."""
+    sequence (no kernel waits on another), equal to one engine bit for bit;
+    with the worklist step, the padded W = 3 rows and a multi-chunk layout."""
     import torch
     from paper_1011_5599_b200.sharded import LocalCudaShard, shard_ranges
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
     g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
     n = g.num_nodes()
-    cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
+    cfg = hanf.EngineConfig(bucket_bits=b, seed=42)
     dev = torch.device("cuda", 0)
     shards = [LocalCudaShard(g, cfg, lo, hi, dev) for lo, hi in shard_ranges(n, 2)]
     ranges = shard_ranges(n, 2)
