@@ -247,6 +247,22 @@ class NfEngine {
     return est;
   }
   void reset() { check(hanf_reset(h_)); }
+  // the next run of a multi-seed experiment on the uploaded graph (new)
+  void reseed(std::uint64_t seed) {
+    check(hanf_reseed(h_, seed));
+    cfg_.seed = seed;
+    params_.seed = seed;
+  }
+  // hll.hpp:275-286 save_counters of the current counters (same bytes)
+  void save_counters(const std::string& path) const { check(hanf_save_counters(h_, path.c_str())); }
+  // resume from an HCA1 snapshot taken at `iteration` (new; hll.hpp:288-303 format)
+  void restore_counters(const std::string& path, std::uint64_t iteration) {
+    check(hanf_restore_counters(h_, path.c_str(), iteration));
+    hanf_sketch_params p;
+    check(hanf_params(h_, &p));
+    params_ = SketchParams::from_c(p);
+    cfg_.seed = params_.seed;
+  }
   hanf_engine* handle() noexcept { return h_; }
 
  private:
@@ -260,6 +276,48 @@ template <class G>
 NfEstimate estimate_nf(const G& g, const EngineConfig& cfg) {
   NfEngine engine(g, cfg);
   return engine.run_to_stabilisation();
+}
+
+// main.cpp:263-283 multirun: estimate_nf for seeds base + i, on one engine
+template <class G>
+std::vector<NfEstimate> multirun(const G& g, EngineConfig cfg, std::uint64_t runs,
+                                 std::uint64_t base_seed) {
+  std::vector<NfEstimate> out;
+  if (runs == 0) return out;
+  cfg.seed = base_seed;
+  NfEngine engine(g, cfg);
+  for (std::uint64_t i = 0; i < runs; ++i) {
+    if (i) engine.reseed(base_seed + i);
+    out.push_back(engine.run_to_stabilisation());
+  }
+  return out;
+}
+
+// oracle.hpp:24-104: the exact neighbourhood function, on the GPU, with the
+// reference's guard (GuardError past max_nodes / max_work = n * arcs)
+struct ExactNf {
+  std::uint64_t n = 0;
+  std::vector<std::uint64_t> values;
+  std::uint64_t diameter() const noexcept { return values.empty() ? 0 : values.size() - 1; }
+  std::vector<double> as_doubles() const { return {values.begin(), values.end()}; }
+};
+template <class G>
+ExactNf exact_nf(const G& g, int device = 0, std::uint64_t max_nodes = 1'000'000,
+                 std::uint64_t max_work = 100'000'000'000ULL) {
+  const hanf_graph_view v = view_of(g);
+  ExactNf out;
+  out.n = v.n;
+  std::uint64_t len = 0;
+  std::vector<std::uint64_t> vals(64);
+  hanf_status st = hanf_exact_nf(&v, device, max_nodes, max_work, vals.data(), vals.size(), &len);
+  if (st == HANF_CAPACITY) {
+    vals.resize(len);
+    st = hanf_exact_nf(&v, device, max_nodes, max_work, vals.data(), vals.size(), &len);
+  }
+  check(st);
+  vals.resize(len);
+  out.values = std::move(vals);
+  return out;
 }
 
 // stats.hpp:44-77 on an N(t) vector

@@ -12,6 +12,8 @@
 
 #include "hyperanf/engine.hpp"
 #include "hyperanf/graph.hpp"
+#include "hyperanf/hll.hpp"
+#include "hyperanf/oracle.hpp"
 #include "hyperanf/stats.hpp"
 #include "hyperanf_b200/engine.hpp"
 
@@ -99,6 +101,53 @@ int main() {
                                hyperanf_b200::from_reference(capped));
     expect(false, "iteration cap not enforced");
   } catch (const hyperanf_b200::GuardError&) {
+  }
+  // exact NF (oracle.hpp) against the reference's all-pairs BFS
+  for (const auto& g : {hyperanf::gen_uniform_random(2000, 4, 3), hyperanf::gen_clique_path(20, 9)}) {
+    const auto want = hyperanf::exact_nf(g);
+    const auto got = hyperanf_b200::exact_nf(g);
+    expect(got.values == want.values, "exact_nf values");
+  }
+  try {
+    hyperanf_b200::exact_nf(hyperanf::gen_uniform_random(2000, 4, 3), 0, 100);
+    expect(false, "exact_nf guard not enforced");
+  } catch (const hyperanf_b200::GuardError&) {
+  }
+  // multirun: every seed equals its own estimate_nf; snapshots equal the
+  // reference's save_counters bytes
+  {
+    const hyperanf::Graph g = hyperanf::gen_uniform_random(3000, 6, 2);
+    hyperanf::EngineConfig cfg;
+    cfg.bucket_bits = 6;
+    const auto runs = hyperanf_b200::multirun(g, hyperanf_b200::from_reference(cfg), 3, 50);
+    for (std::uint64_t i = 0; i < runs.size(); ++i) {
+      hyperanf::EngineConfig c = cfg;
+      c.seed = 50 + i;
+      const auto ref_est = hyperanf::estimate_nf(g, c);
+      expect(runs[i].values == ref_est.values, "multirun seed " + std::to_string(50 + i));
+    }
+    hyperanf::EngineConfig c = cfg;
+    c.seed = 7;
+    hyperanf::NfEngine ref(g, c);
+    hyperanf_b200::NfEngine gpu(g, hyperanf_b200::from_reference(c));
+    ref.step();
+    gpu.step();
+    const std::string a = "/tmp/dropin_ref.hca", b = "/tmp/dropin_gpu.hca";
+    hyperanf::save_counters(ref.counters(), a);
+    gpu.save_counters(b);
+    auto slurp = [](const std::string& p) {
+      std::FILE* f = std::fopen(p.c_str(), "rb");
+      std::string d;
+      if (!f) return d;
+      char buf[4096];
+      size_t k;
+      while ((k = std::fread(buf, 1, sizeof buf, f)) > 0) d.append(buf, k);
+      std::fclose(f);
+      return d;
+    };
+    expect(!slurp(a).empty() && slurp(a) == slurp(b), "HCA1 snapshot bytes");
+    std::remove(a.c_str());
+    std::remove(b.c_str());
   }
   std::printf("dropin_test: %zu graphs, %d failures\n", cases.size(), failures);
   return failures == 0 ? 0 : 1;
