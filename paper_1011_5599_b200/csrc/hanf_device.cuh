@@ -338,6 +338,13 @@ __device__ __forceinline__ void store_counter(uint64_t* p, const uint32_t (&v)[L
 }
 
 template <class Lay>
+__device__ __forceinline__ bool limbs_nonzero(const uint32_t (&x)[Lay::kLimbs]) {
+  uint32_t any = 0;
+  sfor<0, Lay::kLimbs>([&](auto I) { any |= x[decltype(I)::value]; });
+  return any != 0;
+}
+
+template <class Lay>
 __device__ __forceinline__ bool limbs_differ(const uint32_t (&x)[Lay::kLimbs],
                                              const uint32_t (&y)[Lay::kLimbs]) {
   uint32_t diff = 0;

@@ -286,7 +286,10 @@ struct hanf_engine {
     uint32_t uses = 0;  // captured on the third use: capture + instantiate +
                         // destroy cost more than a one-shot run's few replays
   };
-  StepGraph graphs[2][3][2];
+  StepGraph graphs[2][4][2];
+  uint64_t* summ = nullptr;   // mode 3 summary bitmap (see create)
+  uint32_t summ_shift = 6;
+  uint64_t summ_bits = 0;
   bool use_graphs = true;
 
   ~hanf_engine() {
@@ -336,6 +339,7 @@ struct hanf_engine {
       pfree(batch_mix, stream);
       pfree(batch_sums, stream);
       pfree(batch_counts, stream);
+      pfree(summ, stream);
       pfree(order, stream);
       pfree(perm, stream);
       pfree(rl_off, stream);
@@ -550,7 +554,10 @@ int step_mode(const hanf_engine* e) {
   // (profiles/r01_sparse.md): build it (ski-rental style) only once that
   // many steps would have used it, so short runs never pay for it
   if (sparse_wanted(e) && (e->tr_off || e->sparse_wanted_steps >= e->sparse_after)) return 2;
-  return 2 * e->last_count < e->n ? 1 : 0;
+  if (2 * e->last_count >= e->n) return 0;
+  // few changed counters: filter the per-arc bitmap probes through the
+  // L1-resident summary first (most probes then never reach L2)
+  return 16 * e->last_count < e->summ_bits ? 3 : 1;
 }
 // Called once at the start of every step, before step_mode.
 void note_step(hanf_engine* e) {
@@ -688,7 +695,15 @@ hanf_status compute_local(hanf_engine* e) {
   hanf::UnionArgs a = union_args(e, g, ng);
   // skipping unmodified successors costs a bitmap probe per arc and saves
   // a counter gather per skipped arc: worth it once most counters settled
-  a.check_mod = step_mode(e) != 0 ? 1 : 0;
+  const int mode = step_mode(e);
+  a.check_mod = mode != 0 ? 1 : 0;
+  if (mode == 3) {
+    HANF_CUDA(hanf::launch_summary(e->mod[g], e->blocks + 1, e->summ_shift, e->summ_bits, e->summ,
+                                   e->stream, &e->launches));
+    a.summ = e->summ;
+    a.summ_shift = e->summ_shift;
+    a.summ_words = static_cast<uint32_t>((e->summ_bits + 63) / 64);
+  }
   const bool fused = a.est != nullptr;
   HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers,
                                e->gather_mode, e->tma ? &e->tmap[g] : nullptr, e->stream,
@@ -949,8 +964,20 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     HANF_TRY(encode_rows_map(&e->tmap[0], e->cnt[0], n + 1, e->pitch));
     HANF_TRY(encode_rows_map(&e->tmap[1], e->cnt[1], n + 1, e->pitch));
   }
-  HANF_TRY(palloc(&e->mod[0], e->blocks, s));
-  HANF_TRY(palloc(&e->mod[1], e->blocks, s));
+  // one extra word: the padding row n (TOS padding, skipped arcs) is probed
+  // like any successor and must read as unmodified
+  HANF_TRY(palloc(&e->mod[0], e->blocks + 1, s));
+  HANF_TRY(palloc(&e->mod[1], e->blocks + 1, s));
+  HANF_TRY(cudaMemsetAsync(e->mod[0] + e->blocks, 0, sizeof(uint64_t), s));
+  HANF_TRY(cudaMemsetAsync(e->mod[1] + e->blocks, 0, sizeof(uint64_t), s));
+  // summary of the modified bitmap for the skip sweep's tail (mode 3): one
+  // bit per 2^summ_shift rows, at most 32 KB; the mode-3 sweep runs as a
+  // persistent grid whose CTAs stage it in shared memory once (a random
+  // probe then costs a bank, not an L1 line)
+  e->summ_shift = 6;
+  while (((n + 1) >> e->summ_shift) >= (1ull << 18)) ++e->summ_shift;
+  e->summ_bits = ((n + 1) >> e->summ_shift) + 1;
+  HANF_TRY(palloc(&e->summ, (e->summ_bits + 63) / 64, s));
   HANF_TRY(palloc(&e->est, n, s));
   HANF_TRY(palloc(&e->block_sums, e->blocks, s));
   {

@@ -90,6 +90,8 @@ cudaError_t relabel_arcs_device(const uint64_t* d_off, const uint32_t* d_succ, u
 // rows perm[first + i] (or first + i) of `counters`, W words each, packed
 // densely into dst (device)
 cudaError_t launch_seed_bitmap(uint64_t* bits, uint64_t n, cudaStream_t s);
+cudaError_t launch_summary(const uint64_t* bits, uint64_t words, uint32_t shift, uint64_t summ_bits,
+                           uint64_t* summ, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_scatter_rows(const uint64_t* src, const uint32_t* perm, uint64_t count,
                                 uint32_t pitch, uint32_t words, uint64_t* counters,
                                 cudaStream_t s, uint64_t* launches);
@@ -163,6 +165,9 @@ struct UnionArgs {
   EstimateParams ep;
   const uint32_t* orig_of;         // row -> original id (for dirty_next)
   uint64_t* dirty_next;            // original-id bitmap of changed counters (nullptr: = mod_next)
+  const uint64_t* summ;            // mode 3: summary of mod_cur (nullptr: probe mod_cur only)
+  uint32_t summ_shift;             // one summary bit per 2^summ_shift rows
+  uint32_t summ_words;             // summary length (staged in shared memory)
   const uint32_t* task_list;       // non-null: run only these task indices
   const unsigned int* task_count;  // (device) length of task_list
 };

@@ -278,20 +278,31 @@ template <class Lay, bool kVec16, class OwnLoad>
 __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTask& task, bool hub,
                                             bool lead, uint32_t v, bool stale,
                                             uint32_t (&acc)[Lay::kLimbs], uint32_t woff,
-                                            uint32_t G, bool& any_changed, OwnLoad own_load) {
+                                            uint32_t G, bool live, bool& any_changed,
+                                            OwnLoad own_load) {
   constexpr int NL = Lay::kLimbs;
   const uint32_t words = args.pitch;
-  for (uint32_t off = G >> 1; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
+  if (live)  // (all-zero accumulators need no butterfly)
+    for (uint32_t off = G >> 1; off >= 1; off >>= 1) shfl_max<Lay>(acc, off);
   if (hub) {
     if ((threadIdx.x & 31) == 0)
       store_chunk<Lay, kVec16>(args.partials + static_cast<uint64_t>(task.item) * words + woff,
                                acc);
   } else {
-    // the old counter is re-read (L1/L2 hit) rather than kept live in
-    // registers across the loop
+    // The fold started from zero: the node's own counter is folded in only
+    // now, and only where it can matter.  An all-zero chunk maximum (no
+    // successor gathered - skipped or none - or only zero chunks) cannot
+    // change the counter, so unless the next slot is stale the own counter
+    // is not even read: the skip sweep's tail steps touch no counters of
+    // unaffected nodes, and dense steps read each own counter once.
+    const bool need = lead && (stale || limbs_nonzero<Lay>(acc));
     uint32_t own[NL];
-    own_load(own);
-    const bool changed = lead && limbs_differ<Lay>(acc, own);
+    own_load(own, need);
+    bool changed = false;
+    if (need) {
+      swar_max<Lay>(acc, own);
+      changed = limbs_differ<Lay>(acc, own);
+    }
     any_changed |= changed;
     if (changed || (lead && stale)) {
       uint64_t* dst = args.next + static_cast<uint64_t>(v) * words + woff;
@@ -327,7 +338,7 @@ __device__ __forceinline__ void task_finish(const UnionArgs& args, const WarpTas
 
 template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB, bool PF>
 __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_index,
-                                           uint32_t lane) {
+                                           uint32_t lane, const uint64_t* summ) {
   using Lay = Layout<R, NREG>;
   constexpr int NL = Lay::kLimbs;
   constexpr int NW = Lay::kWords;
@@ -359,11 +370,8 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
   for (uint32_t ch = 0; ch < args.chunks; ++ch) {
     const uint32_t woff = ch * NW;
     uint32_t acc[NL];
-    {
-      G_t g;
-      g.issue(cur, lead ? v : zero_row, words, woff);
-      g.extract(acc, lead ? v : zero_row);
-    }
+    zero_limbs<Lay>(acc);  // the own counter joins in node_commit
+    bool task_live = !args.check_mod;  // warp-uniform: some lane gathered something
     // PF: the ids of trip group i+U are requested before group i's gathers
     // so the id load latency overlaps the gathers instead of preceding them.
     uint32_t wn[U];
@@ -386,8 +394,22 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
       }
       if (args.check_mod) {
 #pragma unroll
-        for (int j = 0; j < U; ++j)
-          if (!((__ldg(args.mod_cur + (w[j] >> 6)) >> (w[j] & 63)) & 1)) w[j] = zero_row;
+        for (int j = 0; j < U; ++j) {
+          // mode 3: the L1-resident summary (one bit per 2^summ_shift rows)
+          // rules most successors out before the bitmap probe reaches L2
+          bool keep = true;
+          if (summ)  // shared memory: a random probe costs a bank, not an L1 line
+            keep = (summ[w[j] >> (args.summ_shift + 6)] >> ((w[j] >> args.summ_shift) & 63)) & 1;
+          if (keep) keep = (__ldg(args.mod_cur + (w[j] >> 6)) >> (w[j] & 63)) & 1;
+          if (!keep) w[j] = zero_row;
+        }
+        // a trip group with no live successor in any lane costs nothing
+        // more: late skip sweeps are mostly id loads and probes
+        bool live = false;
+#pragma unroll
+        for (int j = 0; j < U; ++j) live |= w[j] != zero_row;
+        if (!__any_sync(0xffffffffu, live)) continue;
+        task_live = true;
       }
       G_t g[U];
 #pragma unroll
@@ -399,11 +421,12 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
         swar_max<Lay>(acc, y);
       }
     }
-    node_commit<Lay, kVec16>(args, task, hub, lead, v, stale, acc, woff, G, any_changed,
-                             [&](uint32_t (&own)[NL]) {
+    node_commit<Lay, kVec16>(args, task, hub, lead, v, stale, acc, woff, G, task_live, any_changed,
+                             [&](uint32_t (&own)[NL], bool need) {
+                               const uint32_t r = need ? v : zero_row;
                                G_t g;
-                               g.issue(cur, lead ? v : zero_row, words, woff);
-                               g.extract(own, lead ? v : zero_row);
+                               g.issue(cur, r, words, woff);
+                               g.extract(own, r);
                              });
   }
   task_finish<Lay, kVec16>(args, task, hub, v, any_changed, lane);
@@ -413,17 +436,30 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
 // warps stride over the listed task indices instead.
 template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1, bool PF = false>
 __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) {
+  extern __shared__ uint64_t summ_smem[];
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  const uint64_t* summ = nullptr;
+  if (args.summ) {  // mode 3: the modified-bitmap summary, staged once per CTA
+    for (uint32_t i = threadIdx.x; i < args.summ_words; i += blockDim.x) summ_smem[i] = args.summ[i];
+    __syncthreads();
+    summ = summ_smem;
+  }
   if (args.task_list) {
     const uint32_t count = *args.task_count;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = gw; i < count; i += nw)
-      union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, args.task_list[i], lane);
+      union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, args.task_list[i], lane, summ);
+    return;
+  }
+  if (summ) {  // persistent grid (launch_union): the staging is paid once per CTA
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = gw; t < args.num_wtasks; t += nw)
+      union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, t, lane, summ);
     return;
   }
   if (gw >= args.num_wtasks) return;
-  union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, gw, lane);
+  union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, gw, lane, summ);
 }
 
 // ---------------------------------------------------------------------------
@@ -500,7 +536,7 @@ __global__ void __launch_bounds__(256, MINB)
   };
 
   uint32_t acc[NL];
-  load_row16<Lay>(acc, cur + static_cast<uint64_t>(lead ? v : zero_row) * pitch);
+  zero_limbs<Lay>(acc);  // the own counter joins in node_commit
   const uint32_t pre = trips < S - 1 ? trips : S - 1;
   for (uint32_t t = 0; t < pre; ++t) fill(t);
   uint32_t us = 0, ph = 0;
@@ -517,9 +553,9 @@ __global__ void __launch_bounds__(256, MINB)
     }
   }
   bool any_changed = false;
-  node_commit<Lay, false>(args, task, hub, lead, v, stale, acc, 0, G, any_changed,
-                          [&](uint32_t (&own)[NL]) {
-                            load_row16<Lay>(own, cur + static_cast<uint64_t>(lead ? v : zero_row) * pitch);
+  node_commit<Lay, false>(args, task, hub, lead, v, stale, acc, 0, G, true, any_changed,
+                          [&](uint32_t (&own)[NL], bool need) {
+                            load_row16<Lay>(own, cur + static_cast<uint64_t>(need ? v : zero_row) * pitch);
                           });
   task_finish<Lay, false>(args, task, hub, v, any_changed, lane);
 }
@@ -551,7 +587,9 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   if (a.num_wtasks == 0) return cudaSuccess;
   uint32_t blocks = (a.num_wtasks + 7) / 8;
   if (a.task_list && blocks > 148 * 4) blocks = 148 * 4;
-  union_kernel<R, NREG, U, GM, V, MINB, PF><<<blocks, 256, 0, s>>>(a);
+  if (a.summ && blocks > 148 * MINB) blocks = 148 * MINB;  // persistent (mode 3)
+  const size_t smem = a.summ ? sizeof(uint64_t) * a.summ_words : 0;
+  union_kernel<R, NREG, U, GM, V, MINB, PF><<<blocks, 256, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -912,6 +950,27 @@ __global__ void all_bits_kernel(uint64_t* __restrict__ bits, uint64_t n) {
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < words;
        w += stride)
     bits[w] = (w + 1) * 64 <= n ? ~0ull : (~0ull >> ((w + 1) * 64 - n));
+}
+
+// summ bit i = OR of the bitmap's rows [i << shift, (i + 1) << shift)
+__global__ void summary_kernel(const uint64_t* __restrict__ bits, uint64_t words, uint32_t shift,
+                               uint64_t summ_bits, uint32_t* __restrict__ summ32) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  uint64_t any = 0;
+  if (i < summ_bits) {
+    const uint64_t w0 = (i << shift) >> 6, w1 = ((i + 1) << shift) >> 6;
+    for (uint64_t w = w0; w < w1 && w < words; ++w) any |= bits[w];
+  }
+  const uint32_t b = __ballot_sync(0xffffffffu, any != 0);
+  if ((threadIdx.x & 31) == 0 && i < summ_bits) summ32[i >> 5] = b;
+}
+
+cudaError_t launch_summary(const uint64_t* bits, uint64_t words, uint32_t shift, uint64_t summ_bits,
+                           uint64_t* summ, cudaStream_t s, uint64_t* launches) {
+  summary_kernel<<<static_cast<uint32_t>((summ_bits + 255) / 256), 256, 0, s>>>(
+      bits, words, shift, summ_bits, reinterpret_cast<uint32_t*>(summ));
+  ++*launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_seed_bitmap(uint64_t* bits, uint64_t n, cudaStream_t s) {
