@@ -546,7 +546,7 @@ hanf_status validate_config(const hanf_config* cfg) {
 // produce the same bits; only the time differs.
 bool sparse_wanted(const hanf_engine* e) {
   return e->cfg.track_modified && e->t != 0 && e->sparse_ok && !e->tma && e->stale_valid &&
-         32 * e->last_count < e->n;
+         128 * e->last_count < e->n;
 }
 int step_mode(const hanf_engine* e) {
   if (!e->cfg.track_modified || e->t == 0) return 0;
@@ -904,7 +904,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
-  // Worklist step (HANF_SPARSE=0 disables): taken once fewer than n/32
+  // Worklist step (HANF_SPARSE=0 disables): taken once fewer than n/128
   // counters changed (the measured crossover on the long-diameter copying
   // graph) on graphs with >= 2^22 arcs (below that one dense launch costs
   // less than the worklist's launches); profiles/r01_sparse.md.
