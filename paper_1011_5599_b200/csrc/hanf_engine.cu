@@ -254,6 +254,10 @@ struct hanf_engine {
   double* h_batch_sums[2] = {nullptr, nullptr};   // pinned [batch][blocks_real] per parity
   std::vector<double> batch_last;                 // N(t) of every run
   bool relabel = false;
+  // relabelled engines keep estimates in row order (writes follow the task
+  // order); finish_kernel gathers them through perm for the original-id
+  // block sums.  HANF_EST_SCATTER=1: scatter to the original slot instead.
+  bool est_rows = false;
   uint32_t* order = nullptr;
   uint32_t* perm = nullptr;
   uint64_t* rl_off = nullptr;  // relabelled offsets until the worklist needs the CSR
@@ -404,7 +408,12 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
   a.register_bits = e->params.register_bits;
   a.pitch = static_cast<uint32_t>(e->pitch);
   a.log_table = e->log_table;
-  a.row_of = e->perm;  // blocks are original ids; counters are read from their rows
+  if (e->est_rows) {  // row order: plain row blocks, no block sums here
+    a.row_of = nullptr;
+    a.block_sums = nullptr;
+  } else {
+    a.row_of = e->perm;  // blocks are original ids; counters are read from their rows
+  }
   HANF_CUDA(hanf::launch_estimate(a, e->stream, &e->launches));
   return HANF_OK;
 }
@@ -424,6 +433,7 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   f.blocks = e->blocks;
   f.b0 = b0;
   f.b1 = b1;
+  f.perm = e->est_rows ? e->perm : nullptr;
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
@@ -528,7 +538,8 @@ hanf_status seed_all(hanf_engine* e) {
     e->last_sum = e->batch_last[0];
     return HANF_OK;
   }
-  return finish(e, dirty_of(e, 0), false, 0, 0, &e->last_sum, &count);
+  return finish(e, dirty_of(e, 0), e->est_rows, 0, e->est_rows ? e->blocks : 0, &e->last_sum,
+                &count);
 }
 
 hanf_status validate_config(const hanf_config* cfg) {
@@ -623,6 +634,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.pitch = static_cast<uint32_t>(e->pitch);
   a.stale_valid = e->stale_valid ? 1 : 0;
   a.orig_of = e->order;
+  a.est_index = e->est_rows ? nullptr : e->order;
   a.dirty_next = e->relabel ? e->dirty[ng] : nullptr;
   return a;
 }
@@ -653,6 +665,7 @@ hanf_status compute_sparse(hanf_engine* e) {
   a.lens = e->lens;
   a.hub_index = e->hub_index;
   a.orig_of = e->order;
+  a.est_index = e->est_rows ? nullptr : e->order;
   a.dirty_next = e->relabel ? e->dirty[ng] : nullptr;
   a.hub_first = e->tasks.hub_first;
   a.hub_count = e->tasks.hub_count;
@@ -711,7 +724,8 @@ hanf_status compute_local(hanf_engine* e) {
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
   const bool sharded = e->lo != 0 || e->hi != e->n;
   if (!fused) {
-    const hanf_status st = run_estimates(e, ng, dirty_of(e, ng), w0, w1);
+    // (row-order estimates: the row bitmap says which rows to redo)
+    const hanf_status st = run_estimates(e, ng, e->est_rows ? e->mod[ng] : dirty_of(e, ng), w0, w1);
     if (st != HANF_OK) return st;
   } else if (sharded) {
     // block sums of this shard now: they are exchanged before commit
@@ -725,7 +739,8 @@ bool commit_recomputes(const hanf_engine* e) {
   // single GPU with fused estimates: the block sums are recomputed in the
   // same launch as the totals
   const bool sharded = e->lo != 0 || e->hi != e->n;
-  return !sharded && hanf::fused_estimates(e->params.register_bits, e->params.registers);
+  return e->est_rows ||
+         (!sharded && hanf::fused_estimates(e->params.register_bits, e->params.registers));
 }
 
 hanf_status commit_enqueue(hanf_engine* e) {
@@ -931,6 +946,8 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       e->relabel = rl[0] == '1';
     else
       e->relabel = (n + 1) * e->pitch * 8 > (64ull << 20) && !ids_local(g);
+    const char* sc = std::getenv("HANF_EST_SCATTER");
+    e->est_rows = e->relabel && !(sc && sc[0] == '1');
   }
 
   auto bail = [&](hanf_status s) {
@@ -1320,7 +1337,8 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
   if (st != HANF_OK) return st;
   uint64_t count = 0;
-  st = finish(e, dirty_of(e, 0), false, 0, 0, &e->last_sum, &count);
+  st = finish(e, dirty_of(e, 0), e->est_rows, 0, e->est_rows ? e->blocks : 0, &e->last_sum,
+              &count);
   if (st != HANF_OK) return st;
   e->last_count = e->n;
   e->t = iteration;

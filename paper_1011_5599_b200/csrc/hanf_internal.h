@@ -121,6 +121,7 @@ struct SparseArgs {
   unsigned int* lens;         // [0] modified chunks, [1] worklist, [2] hub tasks
   const unsigned int* work_len;
   const uint32_t* orig_of;    // row -> original id (for dirty_next)
+  const uint32_t* est_index;  // est slot of a row (nullptr: the row itself)
   uint64_t* dirty_next;       // original-id bitmap of changed counters (nullptr: = mod_next)
   const uint32_t* hub_index;  // node -> hub (UINT32_MAX: not a hub)
   const uint32_t* hub_first;  // per hub: first chunk task, chunk count
@@ -164,6 +165,7 @@ struct UnionArgs {
   double* est;               // per-counter estimates (nullptr: not fused)
   EstimateParams ep;
   const uint32_t* orig_of;         // row -> original id (for dirty_next)
+  const uint32_t* est_index;       // est slot of a row (nullptr: the row itself)
   uint64_t* dirty_next;            // original-id bitmap of changed counters (nullptr: = mod_next)
   const uint64_t* summ;            // mode 3: summary of mod_cur (nullptr: probe mod_cur only)
   uint32_t summ_shift;             // one summary bit per 2^summ_shift rows
@@ -238,6 +240,7 @@ struct FinishArgs {
   uint64_t n;
   uint64_t blocks;        // totals over [0, blocks)
   uint64_t b0, b1;        // block sums recomputed over [b0, b1)
+  const uint32_t* perm = nullptr;  // estimates in row order: original id o is est[perm[o]]
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
 

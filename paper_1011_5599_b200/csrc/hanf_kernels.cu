@@ -265,7 +265,7 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
       any_changed |= changed;
       if (changed || stale)
         store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
-      if (changed && args.est) args.est[est_slot(args.orig_of, v)] = estimate_limbs<Lay>(acc, args.ep);
+      if (changed && args.est) args.est[est_slot(args.est_index, v)] = estimate_limbs<Lay>(acc, args.ep);
     }
   }
   if (lane == 0 && any_changed) mark_changed(args.mod_next, args.dirty_next, args.orig_of, v);
@@ -311,7 +311,7 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
       else
         store_chunk<Lay, kVec16>(dst, acc);
     }
-    if (changed && args.est) args.est[est_slot(args.orig_of, v)] = estimate_limbs<Lay>(acc, args.ep);
+    if (changed && args.est) args.est[est_slot(args.est_index, v)] = estimate_limbs<Lay>(acc, args.ep);
   }
 }
 
@@ -782,10 +782,11 @@ __global__ void __launch_bounds__(64) estimate_kernel(const EstimateArgs args) {
       else
         e = estimate_counter_generic(args.counters + row * args.pitch, p);
       args.est[v] = e;
-    } else {
+    } else if (args.block_sums) {
       e = args.est[v];
     }
   }
+  if (!args.block_sums) return;  // (the caller sums the blocks itself)
   sh[t] = e;
   __syncthreads();
   if (t == 0) {
@@ -874,7 +875,8 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
       const uint64_t e = bk * 64 + t;
       if (e < a.n) {
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tile[k * 65 + t]));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(a.est + e));
+        const uint64_t src = a.perm ? a.perm[e] : e;  // estimates in row order
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(a.est + src));
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");

@@ -9,17 +9,18 @@
 // (the copying model's windows) keep their labels: hanf_engine.cu decides
 // with a sampled locality test.
 //
-// The engine works on the relabelled CSR in "row" space (counters and the
-// modified bitmaps the skips and the worklist read); everything the caller
-// sees stays in the original id space:
-//   order[row] = original id   (seed hash input; a changed row writes its
-//                               estimate to est[order[row]] and sets its
-//                               bit in the original-id dirty bitmap)
-//   perm[id]   = row           (counter read-back; the estimate kernel of
-//                               multi-chunk layouts reads row perm[id])
+// The engine works on the relabelled CSR in "row" space (counters, the
+// modified bitmaps the skips and the worklist read, and by default the
+// estimates); everything the caller sees stays in the original id space:
+//   order[row] = original id   (seed hash input; a changed row sets its bit
+//                               in the original-id dirty bitmap)
+//   perm[id]   = row           (counter read-back; finish_kernel gathers
+//                               est[perm[o]] for the original-id blocks)
 // so N(t) is still summed over original-id blocks in the reference order.
-// Scattering the estimates at update time beat gathering them at sum time
-// (finish_kernel 13 -> 50 us on config 2 with the gather).
+// Estimates in row order cost the finish a random gather; scattered to the
+// original slots (HANF_EST_SCATTER=1) they cost the union sweep
+// partial-sector writes.  Measured per dense step: BA 2^25 13.38 ms
+// (rows) vs 13.89 ms (scatter), R-MAT 26 12.84 vs 12.73 ms.
 //
 // Relabelling pays where the counters do not fit in L2 (measured 2.4x on
 // R-MAT 26, 1.25x on BA 2^25).  On the L2-resident config 2 it gains 5% on

@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
       const bool stale = (a.mod_cur[v >> 6] >> (v & 63)) & 1;
       if (changed || stale) store_chunk<Lay, kVec16>(a.next + static_cast<uint64_t>(v) * words, acc);
       if (changed) {
-        a.est[a.orig_of ? a.orig_of[v] : v] = estimate_limbs<Lay>(acc, a.ep);
+        a.est[a.est_index ? a.est_index[v] : v] = estimate_limbs<Lay>(acc, a.ep);
         atomicOr(reinterpret_cast<unsigned long long*>(a.mod_next) + (v >> 6), 1ull << (v & 63));
         if (a.dirty_next) {
           const uint32_t o = a.orig_of[v];

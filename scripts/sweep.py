@@ -30,4 +30,6 @@ for l2 in l2s:
             e.reset(); flush.zero_(); torch.cuda.synchronize(); e.step()
         t = e.timing(); e.close()
         u = t["union_ms"] / t["steps"]
-        print(f"config{cfgno} variant {v:>3} l2fetch {l2:>4}: union {u:.3f} ms  {g.num_arcs()/u/1e6:.1f} G arcs/s", flush=True)
+        fin = t["reduce_ms"] / t["steps"]
+        print(f"config{cfgno} variant {v:>3} l2fetch {l2:>4}: union {u:.3f} ms  {g.num_arcs()/u/1e6:.1f} G arcs/s"
+              f"  (+ finish {fin:.3f} ms)", flush=True)
