@@ -210,6 +210,18 @@ hanf_status hanf_device_buffers(hanf_engine* engine, hanf_buffers* out);
 /* Sharded step, phase 1: compute this engine's node range into the next
  * generation (device-side; returns immediately, stream-ordered). */
 hanf_status hanf_shard_compute(hanf_engine* engine);
+/* (new) Changed-rows exchange for sharded steps: after hanf_shard_compute,
+ * pack writes to the device buffers ids[cap] / rows[cap * row_pitch] the
+ * rows of this engine's range that the step wrote (changed, or stale:
+ * changed by the previous step).  Those are exactly the rows in which the
+ * peers' copies of the next generation differ, so peers that unpack every
+ * other shard's packet (instead of receiving whole shards) hold the same
+ * next generation.  HANF_CAPACITY (count set) when more than cap rows.
+ * ids >= n in a packet are padding. */
+hanf_status hanf_shard_pack(hanf_engine* engine, uint32_t* ids, uint64_t* rows, uint64_t cap,
+                            uint64_t* count);
+hanf_status hanf_shard_unpack(hanf_engine* engine, const uint32_t* ids, const uint64_t* rows,
+                              uint64_t count);
 /* Sharded step, phase 2 (after the next-generation shards, modified bitmap
  * and block sums of every rank have been exchanged into this engine's
  * buffers): swap generations and produce the IterationReport. */

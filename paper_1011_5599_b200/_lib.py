@@ -86,6 +86,8 @@ _SIGNATURES = {
     "hanf_timing": [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                     POINTER(c_uint64)],
     "hanf_shard_compute": [_P],
+    "hanf_shard_pack": [_P, _P, _P, c_uint64, POINTER(c_uint64)],
+    "hanf_shard_unpack": [_P, _P, _P, c_uint64],
     "hanf_shard_commit": [_P, POINTER(IterationReportC)],
     "hanf_distance_distribution": [POINTER(c_double), c_uint64, POINTER(c_double),
                                    POINTER(c_double), POINTER(c_double)],

@@ -292,6 +292,7 @@ struct hanf_engine {
   };
   StepGraph graphs[2][4][2];
   uint64_t* summ = nullptr;   // mode 3 summary bitmap (see create)
+  unsigned long long* pack_count = nullptr;  // hanf_shard_pack scratch
   uint32_t summ_shift = 6;
   uint64_t summ_bits = 0;
   bool use_graphs = true;
@@ -344,6 +345,7 @@ struct hanf_engine {
       pfree(batch_sums, stream);
       pfree(batch_counts, stream);
       pfree(summ, stream);
+      pfree(pack_count, stream);
       pfree(order, stream);
       pfree(perm, stream);
       pfree(rl_off, stream);
@@ -1385,6 +1387,38 @@ hanf_status hanf_shard_compute(hanf_engine* e) {
     if (sst != HANF_OK) return sst;
   }
   return compute_local(e);
+}
+
+// Changed-rows exchange: the rows this shard's step wrote (changed now or
+// stale) - exactly the rows in which every peer's copy of the next
+// generation differs (peers hold generation t-1 there: the same stale-slot
+// invariant as the single engine).  ids/rows are device buffers.
+hanf_status hanf_shard_pack(hanf_engine* e, uint32_t* ids, uint64_t* rows, uint64_t cap,
+                            uint64_t* count) {
+  if (!e || !count || (cap && (!ids || !rows))) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *count = 0;
+  if (e->n == 0) return HANF_OK;
+  if (e->relabel || e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "not a shard engine");
+  HANF_CUDA(cudaSetDevice(e->device));
+  const int ng = 1 - e->cur;
+  if (!e->pack_count) HANF_CUDA(palloc(&e->pack_count, 1, e->stream));
+  HANF_CUDA(hanf::launch_pack_rows(e->mod[ng], e->stale_valid ? e->mod[e->cur] : e->mod[ng], e->lo,
+                                   e->hi, e->cnt[ng], static_cast<uint32_t>(e->pitch), ids, rows,
+                                   cap, e->pack_count, count, e->stream, &e->launches));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  if (*count > cap) return HANF_CAPACITY;  // (no error message: the caller falls back)
+  return HANF_OK;
+}
+
+hanf_status hanf_shard_unpack(hanf_engine* e, const uint32_t* ids, const uint64_t* rows,
+                              uint64_t count) {
+  if (!e || (count && (!ids || !rows))) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->n == 0 || count == 0) return HANF_OK;
+  HANF_CUDA(cudaSetDevice(e->device));
+  HANF_CUDA(hanf::launch_unpack_rows(ids, rows, count, e->n, static_cast<uint32_t>(e->pitch),
+                                     e->cnt[1 - e->cur], e->stream, &e->launches));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  return HANF_OK;
 }
 
 hanf_status hanf_shard_commit(hanf_engine* e, hanf_iteration_report* rep) {

@@ -128,6 +128,16 @@ struct SparseArgs {
   const uint32_t* hub_count;
   uint64_t n, blocks, hi;
 };
+// Changed-rows exchange of sharded steps (hanf_sparse.cu): the rows of
+// [lo, hi) the step wrote (mod_next | mod_cur) packed as (ids, rows), and
+// rows scattered back into a counter array (ids >= n are padding).
+cudaError_t launch_pack_rows(const uint64_t* mod_next, const uint64_t* mod_cur, uint64_t lo,
+                             uint64_t hi, const uint64_t* counters, uint32_t pitch, uint32_t* ids,
+                             uint64_t* rows, uint64_t cap, unsigned long long* d_count,
+                             uint64_t* count, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_unpack_rows(const uint32_t* ids, const uint64_t* rows, uint64_t count, uint64_t n,
+                               uint32_t pitch, uint64_t* counters, cudaStream_t s,
+                               uint64_t* launches);
 // predecessors signalled per warp task of the signal kernel
 constexpr uint32_t kSignalChunk = 256;
 // node -> hub index map for the worklist step (UINT32_MAX elsewhere)

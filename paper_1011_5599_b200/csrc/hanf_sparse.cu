@@ -301,6 +301,83 @@ cudaError_t launch_sparse_step(const SparseArgs& a, uint64_t w0, uint64_t w1, ui
   }
 }
 
+// ---- changed-rows exchange (hanf_shard_pack / hanf_shard_unpack) ----------
+// rows of [lo, hi) that the step wrote (changed now, or stale = changed by the
+// previous step): ids appended in any order
+__global__ void pack_ids_kernel(const uint64_t* __restrict__ mod_next,
+                                const uint64_t* __restrict__ mod_cur, uint64_t lo, uint64_t hi,
+                                uint32_t* __restrict__ ids, unsigned long long cap,
+                                unsigned long long* __restrict__ count) {
+  const uint64_t w0 = lo >> 6, w1 = (hi + 63) >> 6;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = w0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < w1;
+       w += stride) {
+    uint64_t word = mod_next[w] | mod_cur[w];
+    const uint64_t first = w << 6;
+    if (first < lo) word &= ~0ull << (lo - first);
+    if (first + 64 > hi) word &= hi > first ? (~0ull >> (first + 64 - hi)) : 0ull;
+    if (!word) continue;
+    unsigned long long pos = atomicAdd(count, static_cast<unsigned long long>(__popcll(word)));
+    for (; word; word &= word - 1, ++pos)
+      if (pos < cap) ids[pos] = static_cast<uint32_t>(first + __ffsll(static_cast<long long>(word)) - 1);
+  }
+}
+
+// rows[i] <-> counters[ids[i]] (pitch words each); ids past n are padding
+__global__ void move_rows_kernel(const uint32_t* __restrict__ ids, uint64_t count, uint64_t n,
+                                 uint32_t pitch, const uint64_t* __restrict__ src, bool gather,
+                                 uint64_t* __restrict__ dst) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+       k < count * pitch; k += stride) {
+    const uint64_t i = k / pitch, w = k % pitch;
+    const uint64_t id = ids[i];
+    if (id >= n) continue;
+    if (gather)
+      dst[k] = src[id * pitch + w];
+    else
+      dst[id * pitch + w] = src[k];
+  }
+}
+
+cudaError_t launch_pack_rows(const uint64_t* mod_next, const uint64_t* mod_cur, uint64_t lo,
+                             uint64_t hi, const uint64_t* counters, uint32_t pitch, uint32_t* ids,
+                             uint64_t* rows, uint64_t cap, unsigned long long* d_count,
+                             uint64_t* count, cudaStream_t s, uint64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  const uint64_t words = ((hi + 63) >> 6) - (lo >> 6);
+  if (words) {
+    pack_ids_kernel<<<static_cast<uint32_t>((words + 255) / 256), 256, 0, s>>>(
+        mod_next, mod_cur, lo, hi, ids, cap, d_count);
+    ++*launches;
+  }
+  unsigned long long h = 0;
+  e = cudaMemcpyAsync(&h, d_count, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  *count = h;
+  if (h == 0 || h > cap) return cudaGetLastError();
+  uint64_t blocks = (h * pitch + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  move_rows_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(ids, h, ~0ull, pitch, counters,
+                                                                 true, rows);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_rows(const uint32_t* ids, const uint64_t* rows, uint64_t count, uint64_t n,
+                               uint32_t pitch, uint64_t* counters, cudaStream_t s,
+                               uint64_t* launches) {
+  if (count == 0) return cudaSuccess;
+  uint64_t blocks = (count * pitch + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  move_rows_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(ids, count, n, pitch, rows, false,
+                                                                 counters);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t build_hub_index(const uint32_t* hub_nodes, uint32_t hubs, uint64_t n, cudaStream_t s,
                             uint32_t** out, uint64_t* launches) {
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(out), sizeof(uint32_t) * (n ? n : 1), s);

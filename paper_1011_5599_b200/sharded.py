@@ -10,9 +10,17 @@ ranks agree on the report without a separate all-reduce.  Exchange = an
 in-place all-gather when the shards are equal (n a multiple of 64*world),
 else one broadcast per owner.
 
+Late iterations change few counters, so once the previous step changed
+fewer than n/16 of them the counter shards travel as changed rows only
+(hanf_shard_pack / hanf_shard_unpack): each owner packs the rows its step
+wrote - the only rows in which the peers' copies differ - and every rank
+scatters the other ranks' packets.  Bitmaps and block sums still travel
+whole (they are 1/(8*40) of the counters).
+
 The local engine is anything with shard_compute() / exchange_buffers() /
-shard_commit() / before_exchange() / after_exchange(): the CUDA engine
-(`LocalCudaShard`) in production, a CPU emulation in the gloo tests.
+shard_commit() / before_exchange() / after_exchange() and optionally
+pack_rows() / unpack_rows(): the CUDA engine (`LocalCudaShard`) in
+production, a CPU emulation in the gloo tests.
 """
 from __future__ import annotations
 
@@ -79,6 +87,33 @@ class LocalCudaShard:
     def shard_commit(self) -> IterationReport:
         return self.engine.shard_commit()
 
+    def row_words(self) -> int:
+        return int(self.engine.device_buffers().row_pitch)
+
+    def pack_rows(self, ids: torch.Tensor, rows: torch.Tensor) -> int:
+        """Changed rows of this shard into ids (int32) / rows (int64); -1 when
+        more than ids.numel() rows changed."""
+        import ctypes
+        from ctypes import c_uint64, c_void_p
+        from ._lib import CAPACITY, check, lib
+        cnt = c_uint64()
+        st = lib().hanf_shard_pack(self.engine._h, c_void_p(ids.data_ptr()),
+                                   c_void_p(rows.data_ptr()), ids.numel(), ctypes.byref(cnt))
+        if st == CAPACITY:
+            return -1
+        check(st)
+        return int(cnt.value)
+
+    def unpack_rows(self, ids: torch.Tensor, rows: torch.Tensor, count: int) -> None:
+        from ctypes import c_void_p
+        from ._lib import check, lib
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))  # the gathered packets
+        check(lib().hanf_shard_unpack(self.engine._h, c_void_p(ids.data_ptr()),
+                                      c_void_p(rows.data_ptr()), count))
+
+    def new_buffer(self, count: int, dtype: torch.dtype) -> torch.Tensor:
+        return torch.empty(count, dtype=dtype, device=self.device)
+
     def sum_estimates(self) -> float:
         return self.engine.sum_estimates()
 
@@ -90,7 +125,7 @@ class ShardedNfEngine:
     """NfEngine across `world` ranks (engine.hpp:122-275 semantics)."""
 
     def __init__(self, graph, cfg: EngineConfig, rank: int, world: int, local=None,
-                 group=None):
+                 group=None, delta: bool = True, delta_ratio: int = 16, delta_cap: int = None):
         self.n = graph.num_nodes()
         self.cfg = cfg
         self.rank, self.world, self.group = rank, world, group
@@ -99,6 +134,17 @@ class ShardedNfEngine:
         if local is None:
             local = LocalCudaShard(graph, cfg, lo, hi, torch.device("cuda", torch.cuda.current_device()))
         self.local = local
+        # changed-rows exchange (see the module docstring); packets hold at
+        # most n/16 rows
+        self.delta = delta and hasattr(local, "pack_rows")
+        self.delta_ratio = delta_ratio  # changed rows once ratio * modified < n
+        self.last_modified = self.n
+        self.delta_steps = 0
+        if self.delta:
+            self.cap = delta_cap or max(64, self.n // 16)
+            self.words = local.row_words()
+            self.ids = local.new_buffer(self.cap, torch.int32)
+            self.rows = local.new_buffer(self.cap * self.words, torch.int64)
 
     def _exchange(self, tensor: torch.Tensor, unit: int, per_node):
         """Gives every rank the owners' slices of `tensor`.  unit = elements
@@ -119,15 +165,49 @@ class ShardedNfEngine:
                     view = tensor[b:e]
                     dist.broadcast(view, src=k, group=self.group)
 
+    def _exchange_changed_rows(self) -> bool:
+        """Changed-rows exchange of the counters; False when some shard had
+        more than `cap` rows (the caller then exchanges whole shards)."""
+        count = self.local.pack_rows(self.ids, self.rows)
+        counts = [torch.zeros(1, dtype=torch.int64) for _ in range(self.world)]
+        mine = torch.tensor([count], dtype=torch.int64)
+        if self.ids.is_cuda:
+            counts = [c.to(self.ids.device) for c in counts]
+            mine = mine.to(self.ids.device)
+        dist.all_gather(counts, mine, group=self.group)
+        counts = [int(c.item()) for c in counts]
+        if min(counts) < 0:
+            return False
+        m = max(counts)
+        if m == 0:
+            return True
+        self.ids[count:m] = -1  # padding: ids >= n are skipped by the unpack
+        ids_all = [torch.empty_like(self.ids[:m]) for _ in range(self.world)]
+        rows_all = [torch.empty_like(self.rows[:m * self.words]) for _ in range(self.world)]
+        dist.all_gather(ids_all, self.ids[:m].contiguous(), group=self.group)
+        dist.all_gather(rows_all, self.rows[:m * self.words].contiguous(), group=self.group)
+        for k in range(self.world):
+            if k != self.rank and counts[k]:
+                self.local.unpack_rows(ids_all[k], rows_all[k], counts[k])
+        return True
+
     def step(self) -> IterationReport:
         if self.n == 0:
             return IterationReport(0.0, 0)
         self.local.shard_compute()
         self.local.before_exchange()
+        rows_done = False
+        if self.delta and self.delta_ratio * self.last_modified < self.n:
+            rows_done = self._exchange_changed_rows()
+            self.delta_steps += rows_done
         for tensor, unit, per_node in self.local.exchange_buffers():
+            if per_node is not None and rows_done:
+                continue  # the counters went as changed rows
             self._exchange(tensor, unit, per_node)
         self.local.after_exchange()
-        return self.local.shard_commit()
+        rep = self.local.shard_commit()
+        self.last_modified = rep.modified
+        return rep
 
     def sum_estimates(self) -> float:
         return self.local.sum_estimates()

@@ -302,8 +302,10 @@ def test_config2_scale(hanf, port):
             assert np.array_equal(final[v], ball), v
 
 
-@pytest.mark.parametrize("b,env", [(6, {}), (6, {"HANF_SPARSE": "1"}), (5, {}), (8, {})])
-def test_sharded_engines_exchange(hanf, port, monkeypatch, b, env):
+@pytest.mark.parametrize("b,env,delta", [(6, {}, False), (6, {"HANF_SPARSE": "1"}, False),
+                                         (5, {}, False), (8, {}, False), (6, {}, True),
+                                         (5, {"HANF_SPARSE": "1"}, True), (8, {}, True)])
+def test_sharded_engines_exchange(hanf, port, monkeypatch, b, env, delta):
     """The shard ABI (hanf_shard_compute / device buffers / hanf_shard_commit)
     on one GPU: two node-range engines, exchange done by device copies in
     sequence (no kernel waits on another), equal to one engine bit for bit;
@@ -320,13 +322,26 @@ def test_sharded_engines_exchange(hanf, port, monkeypatch, b, env):
     ranges = shard_ranges(n, 2)
     values = [shards[0].sum_estimates()]
     mods = [n]
+    words = shards[0].row_words()
+    packets = [(torch.empty(n, dtype=torch.int32, device=dev),
+                torch.empty(n * words, dtype=torch.int64, device=dev)) for _ in shards]
+    rows_steps = 0
     while True:
         for sh in shards:
             sh.shard_compute()
         torch.cuda.synchronize()
+        # changed-rows exchange from the second step on (hanf_shard_pack/unpack)
+        use_rows = delta and len(values) > 1
+        if use_rows:
+            counts = [sh.pack_rows(*packets[k]) for k, sh in enumerate(shards)]
+            for k in range(2):
+                shards[1 - k].unpack_rows(packets[k][0], packets[k][1], counts[k])
+            rows_steps += 1
         bufs = [sh.exchange_buffers() for sh in shards]
         for k, (lo, hi) in enumerate(ranges):
             for b_idx, (t_own, unit, per_node) in enumerate(bufs[k]):
+                if per_node is not None and use_rows:
+                    continue
                 span = (lo * per_node, hi * per_node) if per_node else (lo // 64, -(-hi // 64))
                 for j in range(2):
                     if j != k:
@@ -340,6 +355,7 @@ def test_sharded_engines_exchange(hanf, port, monkeypatch, b, env):
         mods.append(reps[0].modified)
     single = hanf.estimate_nf(g, cfg)
     assert values == single.values and mods == single.modified
+    assert (rows_steps > 0) == delta
     a = shards[0].engine.counters()
     assert np.array_equal(a, shards[1].engine.counters())
     with hanf.NfEngine(g, cfg) as e:

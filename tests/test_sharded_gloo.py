@@ -89,6 +89,30 @@ class EmulatedShard:
         sums = torch.from_numpy(self.block_sums)
         return [(counters, 64 * self.W, self.W), (modified, 1, None), (sums, 1, None)]
 
+    # changed-rows exchange (LocalCudaShard.pack_rows / unpack_rows contract)
+    def row_words(self):
+        return self.W
+
+    def new_buffer(self, count, dtype):
+        return torch.zeros(count, dtype=dtype)
+
+    def pack_rows(self, ids, rows):
+        lo, hi = self.lo, self.hi
+        picked = [v for v in range(lo, hi)
+                  if (int(self.mod_next[v >> 6]) | int(self.mod_cur[v >> 6])) >> (v & 63) & 1]
+        if len(picked) > ids.numel():
+            return -1
+        for i, v in enumerate(picked):
+            ids[i] = v
+            rows[i * self.W:(i + 1) * self.W] = torch.from_numpy(self.next[v].view(np.int64))
+        return len(picked)
+
+    def unpack_rows(self, ids, rows, count):
+        for i in range(count):
+            v = int(ids[i]) & 0xFFFFFFFF
+            if v < self.n:
+                self.next[v] = rows[i * self.W:(i + 1) * self.W].numpy().view(np.uint64)
+
     def shard_commit(self):
         from paper_1011_5599_b200.engine import IterationReport
         count = int(sum(bin(int(w)).count("1") for w in self.mod_next))
@@ -120,16 +144,18 @@ def _worker(rank, world, port, spec, out):
     g = hanf.gen_uniform_random(*spec["graph"])
     cfg = hanf.EngineConfig(bucket_bits=spec["b"], seed=spec["seed"])
     lo, hi = shard_ranges(g.num_nodes(), world)[rank]
-    eng = ShardedNfEngine(g, cfg, rank, world, local=EmulatedShard(g, cfg, lo, hi))
+    eng = ShardedNfEngine(g, cfg, rank, world, local=EmulatedShard(g, cfg, lo, hi),
+                          delta=spec.get("delta", True), delta_ratio=2, delta_cap=g.num_nodes())
     est = eng.run_to_stabilisation()
-    out[rank] = (est.values, est.modified, eng.local.cur.copy())
+    out[rank] = (est.values, est.modified, eng.local.cur.copy(), eng.delta_steps)
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,graph", [(2, (256, 4, 5)), (3, (200, 3, 9)), (2, (130, 2, 1))])
-def test_sharded_run_matches_single_engine(port, world, graph):
-    spec = {"graph": graph, "b": 6, "seed": 42}
+@pytest.mark.parametrize("world,graph,delta", [(2, (256, 4, 5), True), (3, (200, 3, 9), True),
+                                               (2, (130, 2, 1), True), (2, (256, 4, 5), False)])
+def test_sharded_run_matches_single_engine(port, world, graph, delta):
+    spec = {"graph": graph, "b": 6, "seed": 42, "delta": delta}
     mgr = mp.Manager()
     out = mgr.dict()
     mp.start_processes(_worker, args=(world, _free_port(), spec, out), nprocs=world,
@@ -140,9 +166,10 @@ def test_sharded_run_matches_single_engine(port, world, graph):
     while final.step()[1]:
         pass
     for r in range(world):
-        v, m, cur = out[r]
+        v, m, cur, delta_steps = out[r]
         assert v == vals and m == mods
         assert np.array_equal(cur.reshape(-1), final.counters())
+        assert (delta_steps > 0) == delta  # the tail went as changed rows
 
 
 def test_shard_ranges():
