@@ -336,7 +336,9 @@ __device__ __forceinline__ void task_finish(const UnionArgs& args, const WarpTas
   }
 }
 
-template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB, bool PF>
+// SKIP: compiled for the skip sweeps (args.check_mod); the dense sweep's
+// instantiation carries no probe code (register pressure)
+template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB, bool PF, bool SKIP>
 __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_index,
                                            uint32_t lane, const uint64_t* summ) {
   using Lay = Layout<R, NREG>;
@@ -371,7 +373,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
     const uint32_t woff = ch * NW;
     uint32_t acc[NL];
     zero_limbs<Lay>(acc);  // the own counter joins in node_commit
-    bool task_live = !args.check_mod;  // warp-uniform: some lane gathered something
+    bool task_live = !SKIP;  // warp-uniform: some lane gathered something
     // PF: the ids of trip group i+U are requested before group i's gathers
     // so the id load latency overlaps the gathers instead of preceding them.
     uint32_t wn[U];
@@ -392,7 +394,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
         for (int j = 0; j < U; ++j)
           w[j] = (i + j < trips) ? ld_stream_u32(ids + 32 * (i + j)) : zero_row;
       }
-      if (args.check_mod) {
+      if constexpr (SKIP) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           // mode 3: the L1-resident summary (one bit per 2^summ_shift rows)
@@ -434,13 +436,14 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
 
 // One warp per task; with a task list (the worklist step's hub chunks) the
 // warps stride over the listed task indices instead.
-template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1, bool PF = false>
+template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1, bool PF = false,
+          bool SKIP = false>
 __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) {
   extern __shared__ uint64_t summ_smem[];
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t* summ = nullptr;
-  if (args.summ) {  // mode 3: the modified-bitmap summary, staged once per CTA
+  if (SKIP && args.summ) {  // mode 3: the modified-bitmap summary, staged once per CTA
     for (uint32_t i = threadIdx.x; i < args.summ_words; i += blockDim.x) summ_smem[i] = args.summ[i];
     __syncthreads();
     summ = summ_smem;
@@ -449,17 +452,17 @@ __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) 
     const uint32_t count = *args.task_count;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = gw; i < count; i += nw)
-      union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, args.task_list[i], lane, summ);
+      union_task<R, NREG, U, GMODE, kVec16, MINB, PF, SKIP>(args, args.task_list[i], lane, summ);
     return;
   }
-  if (summ) {  // persistent grid (launch_union): the staging is paid once per CTA
+  if (SKIP && summ) {  // persistent grid (launch_union): the staging is paid once per CTA
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t t = gw; t < args.num_wtasks; t += nw)
-      union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, t, lane, summ);
+      union_task<R, NREG, U, GMODE, kVec16, MINB, PF, SKIP>(args, t, lane, summ);
     return;
   }
   if (gw >= args.num_wtasks) return;
-  union_task<R, NREG, U, GMODE, kVec16, MINB, PF>(args, gw, lane, summ);
+  union_task<R, NREG, U, GMODE, kVec16, MINB, PF, SKIP>(args, gw, lane, summ);
 }
 
 // ---------------------------------------------------------------------------
@@ -589,7 +592,10 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   if (a.task_list && blocks > 148 * 4) blocks = 148 * 4;
   if (a.summ && blocks > 148 * MINB) blocks = 148 * MINB;  // persistent (mode 3)
   const size_t smem = a.summ ? sizeof(uint64_t) * a.summ_words : 0;
-  union_kernel<R, NREG, U, GM, V, MINB, PF><<<blocks, 256, smem, s>>>(a);
+  if (a.check_mod)
+    union_kernel<R, NREG, U, GM, V, MINB, PF, true><<<blocks, 256, smem, s>>>(a);
+  else
+    union_kernel<R, NREG, U, GM, V, MINB, PF, false><<<blocks, 256, smem, s>>>(a);
   return cudaGetLastError();
 }
 
