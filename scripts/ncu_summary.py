@@ -63,8 +63,11 @@ def launches(path, tag, command):
 
 
 def full(path, tag):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` exported on the GPU box
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out, per_kernel = [], {}
