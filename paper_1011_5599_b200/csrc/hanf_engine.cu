@@ -294,6 +294,7 @@ struct hanf_engine {
   uint64_t* summ = nullptr;   // mode 3 summary bitmap (see create)
   unsigned long long* pack_count = nullptr;  // hanf_shard_pack scratch
   uint32_t summ_shift = 6;
+  bool force_summary = false;  // HANF_SUMMARY=1 (tests): every skip sweep is mode 3
   uint64_t summ_bits = 0;
   bool use_graphs = true;
 
@@ -570,7 +571,7 @@ int step_mode(const hanf_engine* e) {
   if (2 * e->last_count >= e->n) return 0;
   // few changed counters: filter the per-arc bitmap probes through the
   // L1-resident summary first (most probes then never reach L2)
-  return 16 * e->last_count < e->summ_bits ? 3 : 1;
+  return e->force_summary || 16 * e->last_count < e->summ_bits ? 3 : 1;
 }
 // Called once at the start of every step, before step_mode.
 void note_step(hanf_engine* e) {
@@ -919,6 +920,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   e->words = params.words_per_counter;
   e->pitch = hanf::row_pitch(params.register_bits, params.registers, params.words_per_counter);
   if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
+  if (const char* fs = std::getenv("HANF_SUMMARY")) e->force_summary = fs[0] == '1';
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
   // Worklist step (HANF_SPARSE=0 disables): taken once fewer than n/128

@@ -590,10 +590,12 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   if (a.num_wtasks == 0) return cudaSuccess;
   uint32_t blocks = (a.num_wtasks + 7) / 8;
   if (a.task_list && blocks > 148 * 4) blocks = 148 * 4;
-  if (a.summ && blocks > 148 * MINB) blocks = 148 * MINB;  // persistent (mode 3)
+  if (a.summ && blocks > 148 * 4) blocks = 148 * 4;  // persistent (mode 3)
   const size_t smem = a.summ ? sizeof(uint64_t) * a.summ_words : 0;
+  // the skip sweep carries the probe code: one CTA/SM fewer keeps it spill-free
+  constexpr int SKIP_MINB = MINB > 4 ? 4 : MINB;
   if (a.check_mod)
-    union_kernel<R, NREG, U, GM, V, MINB, PF, true><<<blocks, 256, smem, s>>>(a);
+    union_kernel<R, NREG, U, GM, V, SKIP_MINB, PF, true><<<blocks, 256, smem, s>>>(a);
   else
     union_kernel<R, NREG, U, GM, V, MINB, PF, false><<<blocks, 256, smem, s>>>(a);
   return cudaGetLastError();

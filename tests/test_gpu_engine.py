@@ -389,7 +389,8 @@ def test_worklist_step_parity(hanf, port, monkeypatch):
                                  {"HANF_PITCH": "1", "HANF_GATHER": "30"},
                                  {"HANF_TMA": "1"}, {"HANF_TMA": "1", "HANF_GATHER": "40"},
                                  {"HANF_RELABEL": "1"}, {"HANF_RELABEL": "1", "HANF_SPARSE": "1"},
-                                 {"HANF_RELABEL": "1", "HANF_PITCH": "0"}])
+                                 {"HANF_RELABEL": "1", "HANF_PITCH": "0"},
+                                 {"HANF_SUMMARY": "1"}, {"HANF_SUMMARY": "1", "HANF_RELABEL": "1"}])
 def test_row_pitch_and_gather_variants(hanf, port, monkeypatch, env):
     """Padded rows (aligned 256-bit gathers), unpadded rows and the
     alternative gather kernels change time only: counters read back in the
