@@ -1002,7 +1002,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   HANF_TRY(palloc(&e->est, n, s));
   HANF_TRY(palloc(&e->block_sums, e->blocks, s));
   {
-    const uint64_t ctas = (e->blocks + hanf::kFinishThreads - 1) / hanf::kFinishThreads;
+    const uint64_t ctas = (e->blocks + hanf::kFinishBlocks - 1) / hanf::kFinishBlocks;
     HANF_TRY(palloc(&e->reduce, 1, s));
     HANF_TRY(palloc(&e->reduce_sums, ctas, s));
     HANF_TRY(palloc(&e->reduce_counts, ctas, s));

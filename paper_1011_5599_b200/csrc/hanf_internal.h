@@ -234,12 +234,13 @@ uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words);
 bool use_tma(uint32_t register_bits, uint32_t registers, uint32_t pitch);
 
 // Step epilogue (block sums + totals), see finish_kernel.
-constexpr int kFinishThreads = 64;
+constexpr int kFinishThreads = 256;  // threads per CTA
+constexpr int kFinishBlocks = 64;    // 64-counter blocks per CTA
 struct ReduceOut {
   double total;
   unsigned long long count;
   unsigned int ticket;
-  double* partial_sum;              // [ceil(blocks / kFinishThreads)]
+  double* partial_sum;              // [ceil(blocks / kFinishBlocks)]
   unsigned long long* partial_count;
 };
 struct FinishArgs {

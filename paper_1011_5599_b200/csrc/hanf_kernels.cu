@@ -835,6 +835,7 @@ cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* 
 // Every order is fixed, so N(t) is bit-identical across runs; the
 // reference's own sequential total is redone on the host under exact_sum.
 // ---------------------------------------------------------------------------
+// Fixed-order CTA reductions over kFinishThreads values (deterministic).
 __device__ __forceinline__ double cta_tree_sum(double v, double* sh) {
   const int t = threadIdx.x;
   sh[t] = v;
@@ -862,27 +863,31 @@ __device__ __forceinline__ unsigned long long cta_count_sum(unsigned long long v
   return r;
 }
 
+// CTA c owns the 64-counter blocks [64c, 64c + 64): all kFinishThreads
+// threads stage the dirty blocks' estimates (row k = block 64c + k, 64
+// doubles, row-major so consecutive threads copy consecutive addresses),
+// then thread k < 64 redoes block k's sum sequentially from shared memory.
 __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs a) {
   __shared__ double sh[kFinishThreads];
   __shared__ unsigned long long shc[kFinishThreads];
-  __shared__ double tile[kFinishThreads * (64 + 1)];  // row = one block's 64 estimates
+  __shared__ double tile[kFinishBlocks * (64 + 1)];  // row = one block's 64 estimates
+  __shared__ uint64_t dirty[kFinishBlocks];
   __shared__ bool is_last;
   const uint32_t t = threadIdx.x;
-  const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kFinishThreads;
-  const uint64_t b = b0 + t;
-  // stage the estimates of this CTA's dirty blocks with coalesced async
-  // copies (row k = block b0 + k, thread t copies column t of every row),
-  // so the sequential per-block sums below read shared memory only
-  __shared__ uint64_t dirty[kFinishThreads];
-  dirty[t] = (b < a.blocks && b >= a.b0 && b < a.b1) ? a.bits[b] : 0;
+  const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kFinishBlocks;
+  if (t < kFinishBlocks) {
+    const uint64_t b = b0 + t;
+    dirty[t] = (b < a.blocks && b >= a.b0 && b < a.b1) ? a.bits[b] : 0;
+  }
   __syncthreads();
   if (a.est) {
-    for (uint32_t k = 0; k < kFinishThreads; ++k) {
-      const uint64_t bk = b0 + k;
-      if (dirty[k] == 0) continue;
-      const uint64_t e = bk * 64 + t;
+    for (uint32_t k = t; k < kFinishBlocks * 64; k += kFinishThreads) {
+      const uint32_t row = k >> 6, col = k & 63;
+      if (dirty[row] == 0) continue;
+      const uint64_t e = (b0 + row) * 64 + col;
       if (e < a.n) {
-        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tile[k * 65 + t]));
+        const uint32_t dst =
+            static_cast<uint32_t>(__cvta_generic_to_shared(&tile[row * 65 + col]));
         const uint64_t src = a.perm ? a.perm[e] : e;  // estimates in row order
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(a.est + src));
       }
@@ -892,7 +897,8 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
   __syncthreads();
   double sum = 0.0;
   unsigned long long cnt = 0;
-  if (b < a.blocks) {
+  const uint64_t b = b0 + t;
+  if (t < kFinishBlocks && b < a.blocks) {
     const uint64_t word = a.bits[b];
     cnt = __popcll(word);
     if (a.est && word != 0 && b >= a.b0 && b < a.b1) {
@@ -933,7 +939,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
 
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches) {
   if (a.blocks == 0) return cudaSuccess;
-  const uint64_t ctas = (a.blocks + kFinishThreads - 1) / kFinishThreads;
+  const uint64_t ctas = (a.blocks + kFinishBlocks - 1) / kFinishBlocks;
   finish_kernel<<<static_cast<uint32_t>(ctas), kFinishThreads, 0, s>>>(a);
   ++*launches;
   return cudaGetLastError();
