@@ -149,6 +149,12 @@ hanf_status hanf_save_counters(hanf_engine* engine, const char* path);
 hanf_status hanf_restore_counters(hanf_engine* engine, const char* path, uint64_t iteration);
 
 /* ---- the hot path -------------------------------------------------------- */
+/* (new) hanf_step split at the device boundary: launch enqueues the whole
+ * step on the engine stream (hanf_stream) and returns at once; complete
+ * waits for it and fills the report.  Lets a caller bracket exactly the
+ * step's device work with its own stream events. */
+hanf_status hanf_step_launch(hanf_engine* engine);
+hanf_status hanf_step_complete(hanf_engine* engine, hanf_iteration_report* report);
 /* NfEngine::sum_estimates() (engine.hpp:100-118). */
 hanf_status hanf_sum_estimates(hanf_engine* engine, double* sum);
 /* NfEngine::step() (engine.hpp:122-228): one iteration; counters become

@@ -68,6 +68,8 @@ _SIGNATURES = {
     "hanf_restore_counters": [_P, c_char_p, c_uint64],
     "hanf_sum_estimates": [_P, POINTER(c_double)],
     "hanf_step": [_P, POINTER(IterationReportC)],
+    "hanf_step_launch": [_P],
+    "hanf_step_complete": [_P, POINTER(IterationReportC)],
     "hanf_run_to_stabilisation": [_P, POINTER(c_double), POINTER(c_uint64), c_uint64,
                                   POINTER(c_uint64), POINTER(c_double)],
     "hanf_last_result": [_P, POINTER(c_double), POINTER(c_uint64), c_uint64,

@@ -295,6 +295,7 @@ struct hanf_engine {
   unsigned long long* pack_count = nullptr;  // hanf_shard_pack scratch
   uint32_t summ_shift = 6;
   bool force_summary = false;  // HANF_SUMMARY=1 (tests): every skip sweep is mode 3
+  bool step_pending = false;   // hanf_step_launch done, hanf_step_complete not yet
   uint64_t summ_bits = 0;
   bool use_graphs = true;
 
@@ -1363,8 +1364,38 @@ hanf_status hanf_sum_estimates(hanf_engine* e, double* sum) {
   return HANF_OK;
 }
 
+// hanf_step split at the device boundary: launch enqueues the whole step on
+// the engine stream and returns; complete waits and reports.
+hanf_status hanf_step_launch(hanf_engine* e) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: use hanf_run_batch");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
+  if (e->n == 0) {
+    e->step_pending = true;
+    return HANF_OK;
+  }
+  HANF_CUDA(cudaSetDevice(e->device));
+  const hanf_status st = step_enqueue(e);
+  if (st == HANF_OK) e->step_pending = true;
+  return st;
+}
+
+hanf_status hanf_step_complete(hanf_engine* e, hanf_iteration_report* rep) {
+  if (!e || !rep) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (!e->step_pending) return fail(HANF_INVALID_ARGUMENT, "no launched step");
+  e->step_pending = false;
+  if (e->n == 0) {
+    rep->sum = 0.0;
+    rep->modified = 0;
+    return HANF_OK;
+  }
+  HANF_CUDA(cudaSetDevice(e->device));
+  return commit_complete(e, rep);
+}
+
 hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
   if (!e || !rep) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: use hanf_run_batch");
   if (e->n == 0) {                       // engine.hpp:124
     rep->sum = 0.0;

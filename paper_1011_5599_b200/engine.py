@@ -201,6 +201,16 @@ class NfEngine:
         check(lib().hanf_step(self._h, ctypes.byref(r)))
         return IterationReport(r.sum, r.modified)
 
+    def step_launch(self) -> None:
+        """hanf_step_launch: enqueue one step on stream() and return."""
+        check(lib().hanf_step_launch(self._h))
+
+    def step_complete(self) -> IterationReport:
+        """hanf_step_complete: wait for the launched step, report it."""
+        r = _lib.IterationReportC()
+        check(lib().hanf_step_complete(self._h, ctypes.byref(r)))
+        return IterationReport(r.sum, r.modified)
+
     def run_to_stabilisation(self) -> NfEstimate:
         """engine.hpp:233-275: N(0..T), clamped non-decreasing; the
         stabilising no-change iteration is not recorded."""

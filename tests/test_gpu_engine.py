@@ -532,3 +532,23 @@ def test_batched_engine_rejects_single_run_calls(hanf):
     rep = hanf._lib.IterationReportC()
     assert hanf._lib.lib().hanf_step(h, ctypes.byref(rep)) != 0
     hanf._lib.lib().hanf_destroy(h)
+
+
+def test_step_launch_complete(hanf):
+    """hanf_step_launch / hanf_step_complete = hanf_step, split at the device
+    boundary; misuse is an invalid argument."""
+    g = hanf.gen_rmat(11, 16, 0.57, 0.19, 0.19, 1, 2)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=9)
+    with hanf.NfEngine(g, cfg) as a, hanf.NfEngine(g, cfg) as b:
+        while True:
+            ra = a.step()
+            b.step_launch()
+            with pytest.raises(ValueError):
+                b.step()  # a launched step is pending
+            rb = b.step_complete()
+            assert (ra.sum, ra.modified) == (rb.sum, rb.modified)
+            assert np.array_equal(a.counters(), b.counters())
+            if ra.modified == 0:
+                break
+        with pytest.raises(ValueError):
+            b.step_complete()
