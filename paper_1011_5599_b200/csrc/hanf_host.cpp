@@ -477,7 +477,7 @@ hanf_status hanf_graph_load_csr(const char* path, hanf_graph** out) {
   for (uint64_t v = 0; v < n; ++v) {
     auto first = g->succ.begin() + g->offsets[v], last = g->succ.begin() + g->offsets[v + 1];
     if (!std::is_sorted(first, last) || std::adjacent_find(first, last) != last) {
-      std::vector<uint32_t> src(a), dst(g->succ);
+      std::vector<uint32_t> src(a), dst(g->succ.begin(), g->succ.end());
       for (uint64_t u = 0; u < n; ++u)
         for (uint64_t i = g->offsets[u]; i < g->offsets[u + 1]; ++i) src[i] = static_cast<uint32_t>(u);
       delete g;

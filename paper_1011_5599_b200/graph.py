@@ -15,6 +15,35 @@ from . import _lib
 from ._lib import check, lib
 
 
+class _GraphHandle:
+    """Owns a hanf_graph; freed when no array views it any more."""
+
+    def __init__(self, handle: c_void_p):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().hanf_graph_free(self.handle)
+        except Exception:
+            pass
+
+
+class _CsrBuffer:
+    """Buffer exporter (PEP 688) for one array of a library-built graph; the
+    arrays created from it keep the owning _GraphHandle alive."""
+
+    def __init__(self, owner: _GraphHandle, ptr, count: int, ctype):
+        self.owner = owner
+        self.carr = (ctype * count).from_address(ctypes.cast(ptr, ctypes.c_void_p).value)
+
+    def __buffer__(self, flags):
+        return memoryview(self.carr)
+
+    def __release_buffer__(self, view):
+        pass
+
+
 class Graph:
     """Immutable directed graph in CSR layout (graph.hpp:23-69)."""
 
@@ -35,15 +64,22 @@ class Graph:
     # -- construction -----------------------------------------------------
     @staticmethod
     def _adopt(handle: c_void_p) -> "Graph":
+        """Wraps a library-built graph without copying it: the numpy arrays
+        view the C++ CSR, which is freed when the last view is gone (a
+        config-5 graph is 19 GB)."""
         view = _lib.GraphView()
         try:
             check(lib().hanf_graph_view_of(handle, ctypes.byref(view)))
-            n = int(view.n)
-            offsets = np.ctypeslib.as_array(view.offsets, shape=(n + 1,)).copy()
-            arcs = (np.ctypeslib.as_array(view.arcs, shape=(int(view.num_arcs),)).copy()
-                    if view.num_arcs else np.zeros(0, dtype=np.uint32))
-        finally:
+        except Exception:
             lib().hanf_graph_free(handle)
+            raise
+        owner = _GraphHandle(handle)
+        n = int(view.n)
+        offsets = np.frombuffer(_CsrBuffer(owner, view.offsets, n + 1, ctypes.c_uint64),
+                                dtype=np.uint64)
+        arcs = (np.frombuffer(_CsrBuffer(owner, view.arcs, int(view.num_arcs), ctypes.c_uint32),
+                              dtype=np.uint32)
+                if view.num_arcs else np.zeros(0, dtype=np.uint32))
         return Graph(n, offsets, arcs)
 
     @staticmethod
