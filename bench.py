@@ -213,6 +213,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "collective"],
+                    help="N>1: peer-push rows over NVLink from the union kernels "
+                         "(hanf_shard_attach) or NCCL all-gathers")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -241,7 +244,7 @@ def main():
     n, a = g.num_nodes(), g.num_arcs()
     cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank, exact_sum=False)
     if world > 1:
-        sharded = ShardedNfEngine(g, cfg, rank, world)
+        sharded = ShardedNfEngine(g, cfg, rank, world, exchange=args.exchange)
         engine = sharded.local.engine
         do_step = sharded.step
     else:
@@ -315,6 +318,34 @@ def main():
     traffic = ncu_traffic(args.config)
 
     e2e = None
+    if not args.no_e2e and world > 1:
+        # whole sharded run through the public API: every rank page-locks
+        # its copy of the CSR, creates its shard engine (uploads its rows),
+        # attaches to the peers and iterates to stabilisation; wall time
+        # max over ranks
+        import torch.distributed as dist
+        pinned = hanf.Graph(n, g.offsets().copy(), g.arcs().copy()).pin()
+        e2e_cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank)
+        runs, iters, wall = min(args.steps, 3), 0, 0.0
+        for r in range(runs + 1):
+            barrier()
+            t0 = time.perf_counter()
+            sh = ShardedNfEngine(pinned, e2e_cfg, rank, world, exchange=args.exchange)
+            est = sh.run_to_stabilisation()
+            dt = time.perf_counter() - t0
+            sh.close()
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if r > 0:  # run 0 warms the context and allocator
+                wall += float(t.item())
+                iters += est.iterations() + 1
+        lo, hi = sharded.ranges[rank]
+        blocks = (n + 63) // 64
+        e2e = {"value": a * iters / wall, "unit": "arcs/s",
+               "h2d_bytes_per_step": 8 * (n + 1) + 4 * (int(g.offsets()[hi]) - int(g.offsets()[lo])),
+               "d2h_bytes_per_step": int(iters / runs * (16 + 8 * blocks)),
+               "step": "whole sharded estimate_nf() per rank (upload of the rank's rows, "
+                       "seed, every iteration, read-back), max over ranks; bytes per rank"}
     if not args.no_e2e and world == 1:
         # whole estimate_nf through the C-ABI from pinned host memory: the
         # caller's CSR (fresh numpy arrays) page-locked in place with
@@ -358,6 +389,9 @@ def main():
             "config": {"workload": name, "n": n, "arcs": a, "log2m": b, "register_bits": 5,
                        "words_per_counter": words, "hll_seed": HLL_SEED,
                        "parallelism": f"node-range shards x{world}" if world > 1 else "1 GPU",
+                       "exchange": (sharded.exchange + (f" (fallback: {sharded.fallback})"
+                                                        if sharded.fallback else ""))
+                                   if sharded is not None else None,
                        "step": "dense iteration 1 (all arcs) incl. estimates, N(t) total, "
                                "D2H report; re-seed + L2 flush outside the timed region; "
                                "events bracket the step's device work (launch enqueued "

@@ -232,6 +232,43 @@ hanf_status hanf_shard_unpack(hanf_engine* engine, const uint32_t* ids, const ui
  * and block sums of every rank have been exchanged into this engine's
  * buffers): swap generations and produce the IterationReport. */
 hanf_status hanf_shard_commit(hanf_engine* engine, hanf_iteration_report* report);
+/* (new) Peer-push exchange: the fused alternative to the collectives above
+ * (replaces the per-iteration all-gather of SURVEY 8(e); the reference has
+ * no distributed path).  Every shard engine keeps its two counter
+ * generations, both modified bitmaps and two block-sum inboxes in one
+ * IPC-exportable device arena of identical layout on every rank.  Once the
+ * engines are attached to each other, hanf_shard_compute's union and
+ * worklist kernels store every row they write (changed, or stale) into the
+ * peers' next generation as well - over NVLink peer memory, tile by tile
+ * as the rows are produced - and a last kernel publishes the shard's
+ * modified-bitmap words and block sums into the peers' arenas.  One step is
+ * then: hanf_shard_compute; wait for the engine stream; a barrier across
+ * the ranks; hanf_shard_commit.  No counter bytes pass through a
+ * collective; rows that did not change are never sent (the tail iterations
+ * move kilobytes).  Block sums are double-buffered by generation, so a
+ * rank may start step t+1 while a slower peer is still committing step t. */
+typedef struct {
+  uint8_t ipc_handle[64];  /* cudaIpcMemHandle_t of the exchange arena */
+  uint64_t arena_bytes;
+  uint64_t n, row_pitch;
+  uint64_t shard_begin, shard_end;
+  int32_t device;
+  int32_t reserved;
+} hanf_shard_peer;
+#define HANF_MAX_PEERS 7
+/* Describes this shard engine's arena for the other ranks. */
+hanf_status hanf_shard_export(hanf_engine* engine, hanf_shard_peer* out);
+/* Opens the other ranks' arenas (cudaIpcOpenMemHandle; peers[self] is this
+ * engine's own export and is not opened).  The ranges must tile [0, n) and
+ * the layouts must agree; at most HANF_MAX_PEERS peers. */
+hanf_status hanf_shard_attach(hanf_engine* engine, const hanf_shard_peer* peers, uint32_t count,
+                              uint32_t self);
+/* Same, for shard engines of one process (device pointers used directly:
+ * same device, or peer access enabled by the caller). */
+hanf_status hanf_shard_attach_local(hanf_engine* engine, hanf_engine* const* peers, uint32_t count,
+                                    uint32_t self);
+/* Back to the collective exchange (closes opened IPC mappings). */
+hanf_status hanf_shard_detach(hanf_engine* engine);
 
 /* ---- stats.hpp (host arithmetic on N(t)) ---------------------------------- */
 /* cdf_from_nf + distribution_from_cdf (stats.hpp:33-60). */

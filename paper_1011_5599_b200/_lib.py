@@ -48,6 +48,15 @@ class BuffersC(Structure):
                 ("shard_end", c_uint64), ("row_pitch", c_uint64)]
 
 
+class ShardPeerC(Structure):
+    """hanf_shard_peer: one rank's exchange arena (peer-push exchange)."""
+    _fields_ = [("ipc_handle", ctypes.c_uint8 * 64), ("arena_bytes", c_uint64),
+                ("n", c_uint64), ("row_pitch", c_uint64), ("shard_begin", c_uint64),
+                ("shard_end", c_uint64), ("device", c_int32), ("reserved", c_int32)]
+
+
+MAX_PEERS = 7
+
 # status codes (hanf.h)
 OK, INVALID_ARGUMENT, GUARD, OUT_OF_RANGE, CUDA_ERROR, OUT_OF_MEMORY, CAPACITY, \
     IO_ERROR, PARSE_ERROR = range(9)
@@ -91,6 +100,10 @@ _SIGNATURES = {
     "hanf_shard_pack": [_P, _P, _P, c_uint64, POINTER(c_uint64)],
     "hanf_shard_unpack": [_P, _P, _P, c_uint64],
     "hanf_shard_commit": [_P, POINTER(IterationReportC)],
+    "hanf_shard_export": [_P, POINTER(ShardPeerC)],
+    "hanf_shard_attach": [_P, POINTER(ShardPeerC), c_uint32, c_uint32],
+    "hanf_shard_attach_local": [_P, POINTER(_P), c_uint32, c_uint32],
+    "hanf_shard_detach": [_P],
     "hanf_distance_distribution": [POINTER(c_double), c_uint64, POINTER(c_double),
                                    POINTER(c_double), POINTER(c_double)],
     "hanf_effective_diameter": [POINTER(c_double), c_uint64, c_double, c_int32,

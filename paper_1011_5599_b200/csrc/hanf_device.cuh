@@ -377,6 +377,16 @@ __device__ __forceinline__ void shfl_max(uint32_t (&x)[Lay::kLimbs], int offset)
 // linear counting m*log(m/z) comes from a host table built with the same
 // libm call as the reference (log_table[z], z = 1..m).
 // ---------------------------------------------------------------------------
+// Peer-push exchange of sharded steps (hanf_shard_attach): generation t+1
+// of every peer rank, same row layout as the local one.  Each row a step
+// writes locally is stored there too (NVLink peer memory), so no counter
+// collective follows the sweep.
+constexpr int kMaxPeers = 7;
+struct PeerRows {
+  uint64_t* next[kMaxPeers];
+  uint32_t count;
+};
+
 struct EstimateParams {
   double alpha;
   double m;       // registers, as double

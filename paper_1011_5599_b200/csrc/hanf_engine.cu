@@ -298,6 +298,28 @@ struct hanf_engine {
   bool step_pending = false;   // hanf_step_launch done, hanf_step_complete not yet
   uint64_t summ_bits = 0;
   bool use_graphs = true;
+  // Sharded engines keep cnt[2], mod[2] and two block-sum inboxes in one
+  // IPC-exportable arena (cudaMalloc, not the pool), laid out identically
+  // on every rank; attached peers' arenas receive this shard's rows, bitmap
+  // words and block sums (peer-push exchange, hanf_shard_attach).
+  void* arena = nullptr;
+  uint64_t arena_bytes = 0;
+  uint64_t arena_off[6] = {};                // cnt0 cnt1 mod0 mod1 inbox0 inbox1
+  double* inbox[2] = {nullptr, nullptr};     // block sums of all shards, per generation
+  bool attached = false;
+  uint32_t npeers = 0;
+  uint8_t* peer_base[hanf::kMaxPeers] = {};
+  bool peer_ipc[hanf::kMaxPeers] = {};       // opened with cudaIpcOpenMemHandle
+
+  void detach_peers() {
+    for (uint32_t p = 0; p < npeers; ++p) {
+      if (peer_ipc[p] && peer_base[p]) cudaIpcCloseMemHandle(peer_base[p]);
+      peer_base[p] = nullptr;
+      peer_ipc[p] = false;
+    }
+    npeers = 0;
+    attached = false;
+  }
 
   ~hanf_engine() {
     static const bool prof = [] {
@@ -322,6 +344,15 @@ struct hanf_engine {
     phase("graphs");
     for (auto& x : ev)
       if (x) cudaEventDestroy(x);
+    if (stream) cudaStreamSynchronize(stream);
+    detach_peers();
+    if (arena) {  // (peers that mapped it were detached by their owners' ranks first)
+      cudaFree(arena);
+      arena = nullptr;
+      cnt[0] = cnt[1] = nullptr;
+      mod[0] = mod[1] = nullptr;
+      inbox[0] = inbox[1] = nullptr;
+    }
     if (stream) {
       for (int i = 0; i < 2; ++i) {
         pfree(cnt[i], stream);
@@ -431,7 +462,9 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   hanf::FinishArgs f{};
   f.est = recompute ? e->est : nullptr;
   f.bits = bits;
-  f.block_sums = e->block_sums;
+  // peer-push shards total the inbox the peers published into
+  double* sums = in_step && e->attached ? e->inbox[1 - e->cur] : e->block_sums;
+  f.block_sums = sums;
   f.out = e->reduce;
   f.n = e->n;
   f.blocks = e->blocks;
@@ -444,7 +477,7 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   HANF_CUDA(cudaMemcpyAsync(e->h_reduce, e->reduce, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                             e->stream));
   if (e->cfg.exact_sum)
-    HANF_CUDA(cudaMemcpyAsync(e->h_block_sums[e->cur], e->block_sums, sizeof(double) * e->blocks,
+    HANF_CUDA(cudaMemcpyAsync(e->h_block_sums[e->cur], sums, sizeof(double) * e->blocks,
                               cudaMemcpyDeviceToHost, e->stream));
   return HANF_OK;
 }
@@ -612,6 +645,15 @@ hanf_status ensure_sparse(hanf_engine* e) {
   return HANF_OK;
 }
 
+// Peer-push exchange: generation ng of every attached peer.
+hanf::PeerRows peer_rows(const hanf_engine* e, int ng) {
+  hanf::PeerRows p{};
+  p.count = e->attached ? e->npeers : 0;
+  for (uint32_t i = 0; i < p.count; ++i)
+    p.next[i] = reinterpret_cast<uint64_t*>(e->peer_base[i] + e->arena_off[ng]);
+  return p;
+}
+
 hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   hanf::UnionArgs a{};
   a.tos = e->tasks.tos;
@@ -640,6 +682,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.orig_of = e->order;
   a.est_index = e->est_rows ? nullptr : e->order;
   a.dirty_next = e->relabel ? e->dirty[ng] : nullptr;
+  a.peers = peer_rows(e, ng);
   return a;
 }
 
@@ -676,6 +719,7 @@ hanf_status compute_sparse(hanf_engine* e) {
   a.n = e->n;
   a.blocks = e->blocks;
   a.hi = e->hi;
+  a.peers = peer_rows(e, ng);
   HANF_CUDA(hanf::launch_sparse_step(a, w0, w1, e->params.register_bits, e->params.registers,
                                      e->stream, &e->launches));
   if (e->tasks.num_chunks) {
@@ -692,7 +736,30 @@ hanf_status compute_sparse(hanf_engine* e) {
   return HANF_OK;
 }
 
+hanf_status compute_shard(hanf_engine* e);
+
+// A sharded compute, then (peer-push exchange) the shard's bitmap words and
+// block sums into every peer's arena and the local inbox.
 hanf_status compute_local(hanf_engine* e) {
+  const hanf_status st = compute_shard(e);
+  if (st != HANF_OK || !e->attached) return st;
+  const int ng = 1 - e->cur;
+  hanf::PublishArgs p{};
+  p.mod_next = e->mod[ng];
+  p.block_sums = e->block_sums;
+  p.w0 = e->lo >> 6;
+  p.w1 = (e->hi + 63) >> 6;
+  p.count = e->npeers;
+  for (uint32_t i = 0; i < e->npeers; ++i) {
+    p.peer_mod[i] = reinterpret_cast<uint64_t*>(e->peer_base[i] + e->arena_off[2 + ng]);
+    p.peer_sums[i] = reinterpret_cast<double*>(e->peer_base[i] + e->arena_off[4 + ng]);
+  }
+  p.peer_sums[e->npeers] = e->inbox[ng];
+  HANF_CUDA(hanf::launch_publish(p, e->stream, &e->launches));
+  return HANF_OK;
+}
+
+hanf_status compute_shard(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
   HANF_CUDA(cudaMemsetAsync(e->mod[ng] + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
@@ -976,8 +1043,29 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   // row n is an all-zero counter (the union kernels' padding target); 8
   // extra words keep the 256-bit window loads of the last rows in bounds
   const uint64_t nw = (n + 1) * e->pitch + 8;
-  HANF_TRY(palloc(&e->cnt[0], nw, s));
-  HANF_TRY(palloc(&e->cnt[1], nw, s));
+  const bool sharded = lo != 0 || hi != n;
+  if (sharded) {
+    // the exchange arena (see hanf_engine::arena): same offsets on every rank
+    auto al = [](uint64_t bytes) { return (bytes + 255) & ~255ull; };
+    const uint64_t sizes[6] = {nw * 8, nw * 8, (e->blocks + 1) * 8, (e->blocks + 1) * 8,
+                               e->blocks * 8, e->blocks * 8};
+    uint64_t off = 0;
+    for (int i = 0; i < 6; ++i) {
+      e->arena_off[i] = off;
+      off += al(sizes[i] ? sizes[i] : 8);
+    }
+    e->arena_bytes = off;
+    HANF_TRY(cudaMalloc(&e->arena, off));
+    uint8_t* base = static_cast<uint8_t*>(e->arena);
+    for (int i = 0; i < 2; ++i) {
+      e->cnt[i] = reinterpret_cast<uint64_t*>(base + e->arena_off[i]);
+      e->mod[i] = reinterpret_cast<uint64_t*>(base + e->arena_off[2 + i]);
+      e->inbox[i] = reinterpret_cast<double*>(base + e->arena_off[4 + i]);
+    }
+  } else {
+    HANF_TRY(palloc(&e->cnt[0], nw, s));
+    HANF_TRY(palloc(&e->cnt[1], nw, s));
+  }
   HANF_TRY(cudaMemsetAsync(e->cnt[0] + n * e->pitch, 0, sizeof(uint64_t) * (e->pitch + 8), s));
   HANF_TRY(cudaMemsetAsync(e->cnt[1] + n * e->pitch, 0, sizeof(uint64_t) * (e->pitch + 8), s));
   e->tma = hanf::use_tma(params.register_bits, params.registers, static_cast<uint32_t>(e->pitch)) &&
@@ -988,8 +1076,10 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   }
   // one extra word: the padding row n (TOS padding, skipped arcs) is probed
   // like any successor and must read as unmodified
-  HANF_TRY(palloc(&e->mod[0], e->blocks + 1, s));
-  HANF_TRY(palloc(&e->mod[1], e->blocks + 1, s));
+  if (!sharded) {
+    HANF_TRY(palloc(&e->mod[0], e->blocks + 1, s));
+    HANF_TRY(palloc(&e->mod[1], e->blocks + 1, s));
+  }
   HANF_TRY(cudaMemsetAsync(e->mod[0] + e->blocks, 0, sizeof(uint64_t), s));
   HANF_TRY(cudaMemsetAsync(e->mod[1] + e->blocks, 0, sizeof(uint64_t), s));
   // summary of the modified bitmap for the skip sweep's tail (mode 3): one
@@ -1463,6 +1553,134 @@ hanf_status hanf_shard_commit(hanf_engine* e, hanf_iteration_report* rep) {
   }
   HANF_CUDA(cudaSetDevice(e->device));
   return commit(e, rep);
+}
+
+// ---- peer-push exchange ----------------------------------------------------
+hanf_status hanf_shard_export(hanf_engine* e, hanf_shard_peer* out) {
+  if (!e || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  std::memset(out, 0, sizeof(*out));
+  out->n = e->n;
+  out->row_pitch = e->pitch;
+  out->shard_begin = e->lo;
+  out->shard_end = e->hi;
+  out->device = e->device;
+  out->arena_bytes = e->arena_bytes;
+  if (!e->arena) return HANF_OK;  // a one-shard engine (all nodes): nothing to map
+  HANF_CUDA(cudaSetDevice(e->device));
+  cudaIpcMemHandle_t h;
+  HANF_CUDA(cudaIpcGetMemHandle(&h, e->arena));
+  static_assert(sizeof(h) == sizeof(out->ipc_handle), "cudaIpcMemHandle_t size");
+  std::memcpy(out->ipc_handle, &h, sizeof(h));
+  return HANF_OK;
+}
+
+namespace {
+
+// The shards must tile [0, n) with identical arenas; `self` describes e.
+hanf_status check_peers(const hanf_engine* e, const hanf_shard_peer* peers, uint32_t count,
+                        uint32_t self) {
+  if (count == 0 || self >= count) return fail(HANF_INVALID_ARGUMENT, "self outside the peer list");
+  if (count > hanf::kMaxPeers + 1)
+    return fail(HANF_INVALID_ARGUMENT, "peer-push exchange: at most 8 shards");
+  const hanf_shard_peer& me = peers[self];
+  if (me.n != e->n || me.shard_begin != e->lo || me.shard_end != e->hi ||
+      me.arena_bytes != e->arena_bytes)
+    return fail(HANF_INVALID_ARGUMENT, "peers[self] does not describe this engine");
+  std::vector<std::pair<uint64_t, uint64_t>> ranges;
+  for (uint32_t p = 0; p < count; ++p) {
+    if (peers[p].n != e->n || peers[p].row_pitch != e->pitch ||
+        peers[p].arena_bytes != e->arena_bytes)
+      return fail(HANF_INVALID_ARGUMENT, "peer engines differ in graph or counter layout");
+    if (peers[p].shard_end > peers[p].shard_begin)
+      ranges.emplace_back(peers[p].shard_begin, peers[p].shard_end);
+  }
+  std::sort(ranges.begin(), ranges.end());
+  uint64_t at = 0;
+  for (const auto& r : ranges) {
+    if (r.first != at) return fail(HANF_INVALID_ARGUMENT, "shard ranges do not tile [0, n)");
+    at = r.second;
+  }
+  if (at != e->n) return fail(HANF_INVALID_ARGUMENT, "shard ranges do not tile [0, n)");
+  return HANF_OK;
+}
+
+}  // namespace
+
+hanf_status hanf_shard_attach(hanf_engine* e, const hanf_shard_peer* peers, uint32_t count,
+                              uint32_t self) {
+  if (!e || !peers) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  hanf_status st = check_peers(e, peers, count, self);
+  if (st != HANF_OK) return st;
+  HANF_CUDA(cudaSetDevice(e->device));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  e->detach_peers();
+  if (!e->arena) return HANF_OK;  // one shard: nothing to exchange
+  for (uint32_t p = 0; p < count; ++p) {
+    if (p == self) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, peers[p].ipc_handle, sizeof(h));
+    void* ptr = nullptr;
+    const cudaError_t err = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (err != cudaSuccess) {
+      e->detach_peers();
+      return cuda_fail(err, "cudaIpcOpenMemHandle (peer shard arena)");
+    }
+    e->peer_base[e->npeers] = static_cast<uint8_t*>(ptr);
+    e->peer_ipc[e->npeers] = true;
+    ++e->npeers;
+  }
+  e->attached = true;
+  return HANF_OK;
+}
+
+hanf_status hanf_shard_attach_local(hanf_engine* e, hanf_engine* const* peers, uint32_t count,
+                                    uint32_t self) {
+  if (!e || !peers) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (self >= count || peers[self] != e)
+    return fail(HANF_INVALID_ARGUMENT, "peers[self] must be this engine");
+  std::vector<hanf_shard_peer> desc(count);
+  for (uint32_t p = 0; p < count; ++p) {
+    if (!peers[p]) return fail(HANF_INVALID_ARGUMENT, "null peer engine");
+    desc[p] = hanf_shard_peer{};
+    desc[p].n = peers[p]->n;
+    desc[p].row_pitch = peers[p]->pitch;
+    desc[p].shard_begin = peers[p]->lo;
+    desc[p].shard_end = peers[p]->hi;
+    desc[p].arena_bytes = peers[p]->arena_bytes;
+    desc[p].device = peers[p]->device;
+  }
+  hanf_status st = check_peers(e, desc.data(), count, self);
+  if (st != HANF_OK) return st;
+  HANF_CUDA(cudaSetDevice(e->device));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  e->detach_peers();
+  if (!e->arena) return HANF_OK;
+  for (uint32_t p = 0; p < count; ++p) {
+    if (p == self) continue;
+    if (peers[p]->device != e->device) {
+      int ok = 0;
+      HANF_CUDA(cudaDeviceCanAccessPeer(&ok, e->device, peers[p]->device));
+      if (!ok) return fail(HANF_INVALID_ARGUMENT, "no peer access between the shard devices");
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(peers[p]->device, 0);
+      if (pe == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else if (pe != cudaSuccess)
+        return cuda_fail(pe, "cudaDeviceEnablePeerAccess");
+    }
+    e->peer_base[e->npeers] = static_cast<uint8_t*>(peers[p]->arena);
+    e->peer_ipc[e->npeers] = false;
+    ++e->npeers;
+  }
+  e->attached = true;
+  return HANF_OK;
+}
+
+hanf_status hanf_shard_detach(hanf_engine* e) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  HANF_CUDA(cudaSetDevice(e->device));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  e->detach_peers();
+  return HANF_OK;
 }
 
 hanf_status hanf_run_to_stabilisation(hanf_engine* e, double* values, uint64_t* modified,

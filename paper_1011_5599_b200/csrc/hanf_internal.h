@@ -127,6 +127,7 @@ struct SparseArgs {
   const uint32_t* hub_first;  // per hub: first chunk task, chunk count
   const uint32_t* hub_count;
   uint64_t n, blocks, hi;
+  PeerRows peers;             // sharded peer-push: also store written rows there
 };
 // Changed-rows exchange of sharded steps (hanf_sparse.cu): the rows of
 // [lo, hi) the step wrote (mod_next | mod_cur) packed as (ids, rows), and
@@ -182,6 +183,7 @@ struct UnionArgs {
   uint32_t summ_words;             // summary length (staged in shared memory)
   const uint32_t* task_list;       // non-null: run only these task indices
   const unsigned int* task_count;  // (device) length of task_list
+  PeerRows peers;                  // sharded peer-push: also store written rows there
 };
 
 struct EstimateArgs {
@@ -254,5 +256,16 @@ struct FinishArgs {
   const uint32_t* perm = nullptr;  // estimates in row order: original id o is est[perm[o]]
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
+// Peer-push exchange: bitmap words and block sums [w0, w1) of this shard
+// into every peer's arena (and the block sums into the local inbox).
+struct PublishArgs {
+  const uint64_t* mod_next;
+  const double* block_sums;
+  uint64_t w0, w1;
+  uint64_t* peer_mod[kMaxPeers];
+  double* peer_sums[kMaxPeers + 1];  // [count] = the local inbox
+  uint32_t count;
+};
+cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s, uint64_t* launches);
 
 }  // namespace hanf

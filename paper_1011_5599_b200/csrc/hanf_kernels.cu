@@ -263,8 +263,12 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
       load_chunk<Lay, kVec16>(own, args.cur + static_cast<uint64_t>(v) * words + woff);
       const bool changed = limbs_differ<Lay>(acc, own);
       any_changed |= changed;
-      if (changed || stale)
-        store_chunk<Lay, kVec16>(args.next + static_cast<uint64_t>(v) * words + woff, acc);
+      if (changed || stale) {
+        const uint64_t off = static_cast<uint64_t>(v) * words + woff;
+        store_chunk<Lay, kVec16>(args.next + off, acc);
+        for (uint32_t p = 0; p < args.peers.count; ++p)
+          store_chunk<Lay, kVec16>(args.peers.next[p] + off, acc);
+      }
       if (changed && args.est) args.est[est_slot(args.est_index, v)] = estimate_limbs<Lay>(acc, args.ep);
     }
   }
@@ -305,11 +309,18 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
     }
     any_changed |= changed;
     if (changed || (lead && stale)) {
-      uint64_t* dst = args.next + static_cast<uint64_t>(v) * words + woff;
+      const uint64_t off = static_cast<uint64_t>(v) * words + woff;
       if (args.chunks == 1)
-        store_counter<Lay>(dst, acc);
+        store_counter<Lay>(args.next + off, acc);
       else
-        store_chunk<Lay, kVec16>(dst, acc);
+        store_chunk<Lay, kVec16>(args.next + off, acc);
+      // sharded peer-push: the same row into every peer's next generation
+      for (uint32_t p = 0; p < args.peers.count; ++p) {
+        if (args.chunks == 1)
+          store_counter<Lay>(args.peers.next[p] + off, acc);
+        else
+          store_chunk<Lay, kVec16>(args.peers.next[p] + off, acc);
+      }
     }
     if (changed && args.est) args.est[est_slot(args.est_index, v)] = estimate_limbs<Lay>(acc, args.ep);
   }
@@ -935,6 +946,34 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
     a.out->count = count;
     a.out->ticket = 0;
   }
+}
+
+// Peer-push exchange, end of a sharded compute: the shard's bitmap words
+// and block sums into every peer's arena, block sums into the local inbox
+// too (whole words: no clearing or atomics on the receiving side).
+__global__ void publish_kernel(const PublishArgs a) {
+  const uint64_t words = a.w1 - a.w0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < words;
+       i += stride) {
+    const uint64_t w = a.w0 + i;
+    const uint64_t bits = a.mod_next[w];
+    const double sum = a.block_sums[w];
+    for (uint32_t p = 0; p < a.count; ++p) {
+      a.peer_mod[p][w] = bits;
+      a.peer_sums[p][w] = sum;
+    }
+    a.peer_sums[a.count][w] = sum;
+  }
+}
+
+cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s, uint64_t* launches) {
+  if (a.w1 <= a.w0) return cudaSuccess;
+  uint64_t ctas = (a.w1 - a.w0 + 255) / 256;
+  if (ctas > 148ull * 8) ctas = 148ull * 8;
+  publish_kernel<<<static_cast<uint32_t>(ctas), 256, 0, s>>>(a);
+  ++*launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches) {

@@ -198,7 +198,12 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
       load_chunk<Lay, kVec16>(own, a.cur + static_cast<uint64_t>(v) * words);
       const bool changed = limbs_differ<Lay>(acc, own);
       const bool stale = (a.mod_cur[v >> 6] >> (v & 63)) & 1;
-      if (changed || stale) store_chunk<Lay, kVec16>(a.next + static_cast<uint64_t>(v) * words, acc);
+      if (changed || stale) {
+        const uint64_t off = static_cast<uint64_t>(v) * words;
+        store_chunk<Lay, kVec16>(a.next + off, acc);
+        for (uint32_t p = 0; p < a.peers.count; ++p)  // sharded peer-push
+          store_chunk<Lay, kVec16>(a.peers.next[p] + off, acc);
+      }
       if (changed) {
         a.est[a.est_index ? a.est_index[v] : v] = estimate_limbs<Lay>(acc, a.ep);
         atomicOr(reinterpret_cast<unsigned long long*>(a.mod_next) + (v >> 6), 1ull << (v & 63));

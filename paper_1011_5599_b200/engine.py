@@ -296,6 +296,28 @@ class NfEngine:
     def shard_compute(self) -> None:
         check(lib().hanf_shard_compute(self._h))
 
+    def shard_export(self) -> bytes:
+        """hanf_shard_export: this shard's exchange arena as bytes (to be
+        all-gathered and handed to every rank's shard_attach)."""
+        d = _lib.ShardPeerC()
+        check(lib().hanf_shard_export(self._h, ctypes.byref(d)))
+        return ctypes.string_at(ctypes.addressof(d), ctypes.sizeof(d))
+
+    def shard_attach(self, peers, self_index: int) -> None:
+        """hanf_shard_attach: peer-push exchange with the ranks' exports."""
+        arr = (_lib.ShardPeerC * len(peers))()
+        for i, raw in enumerate(peers):
+            ctypes.memmove(ctypes.addressof(arr[i]), bytes(raw), ctypes.sizeof(_lib.ShardPeerC))
+        check(lib().hanf_shard_attach(self._h, arr, len(peers), self_index))
+
+    def shard_attach_local(self, peers, self_index: int) -> None:
+        """hanf_shard_attach_local: peer-push between engines of this process."""
+        arr = (c_void_p * len(peers))(*[p._h.value for p in peers])
+        check(lib().hanf_shard_attach_local(self._h, arr, len(peers), self_index))
+
+    def shard_detach(self) -> None:
+        check(lib().hanf_shard_detach(self._h))
+
     def shard_commit(self) -> IterationReport:
         r = _lib.IterationReportC()
         check(lib().hanf_shard_commit(self._h, ctypes.byref(r)))

@@ -17,6 +17,16 @@ wrote - the only rows in which the peers' copies differ - and every rank
 scatters the other ranks' packets.  Bitmaps and block sums still travel
 whole (they are 1/(8*40) of the counters).
 
+Peer-push exchange (exchange="peer", hanf_shard_attach): the shard
+engines map each other's exchange arenas (CUDA IPC handles, all-gathered
+once) and the union / worklist kernels store every row they write straight
+into the peers' next generation over NVLink while the sweep runs; a last
+kernel publishes the shard's bitmap words and block sums.  A step is then
+compute -> wait for the engine stream -> barrier -> commit: no counter
+bytes go through a collective and unchanged rows are never sent.  Block
+sums land in a per-generation inbox, so one barrier per step suffices (a
+fast rank's step t+1 never overwrites what a slow rank's commit t reads).
+
 The local engine is anything with shard_compute() / exchange_buffers() /
 shard_commit() / before_exchange() / after_exchange() and optionally
 pack_rows() / unpack_rows(): the CUDA engine (`LocalCudaShard`) in
@@ -87,6 +97,19 @@ class LocalCudaShard:
     def shard_commit(self) -> IterationReport:
         return self.engine.shard_commit()
 
+    # peer-push exchange
+    def shard_export(self) -> bytes:
+        return self.engine.shard_export()
+
+    def shard_attach(self, exports, rank: int) -> None:
+        self.engine.shard_attach(exports, rank)
+
+    def shard_detach(self) -> None:
+        self.engine.shard_detach()
+
+    def wait_compute(self) -> None:
+        self.stream.synchronize()
+
     def row_words(self) -> int:
         return int(self.engine.device_buffers().row_pitch)
 
@@ -125,7 +148,8 @@ class ShardedNfEngine:
     """NfEngine across `world` ranks (engine.hpp:122-275 semantics)."""
 
     def __init__(self, graph, cfg: EngineConfig, rank: int, world: int, local=None,
-                 group=None, delta: bool = True, delta_ratio: int = 16, delta_cap: int = None):
+                 group=None, delta: bool = True, delta_ratio: int = 16, delta_cap: int = None,
+                 exchange: str = "collective"):
         self.n = graph.num_nodes()
         self.cfg = cfg
         self.rank, self.world, self.group = rank, world, group
@@ -134,6 +158,29 @@ class ShardedNfEngine:
         if local is None:
             local = LocalCudaShard(graph, cfg, lo, hi, torch.device("cuda", torch.cuda.current_device()))
         self.local = local
+        if exchange not in ("collective", "peer"):
+            raise ValueError(f"exchange must be 'collective' or 'peer', not {exchange!r}")
+        self.exchange = exchange
+        self.fallback = None
+        if exchange == "peer":
+            # every rank's arena description, then map the others' arenas;
+            # if any rank cannot map a peer (no IPC / peer access between
+            # the devices) all ranks fall back to the collective exchange
+            exports = [None] * world
+            dist.all_gather_object(exports, local.shard_export(), group=group)
+            error = None
+            try:
+                local.shard_attach(exports, rank)
+            except Exception as exc:  # noqa: BLE001 - reported through self.fallback
+                error = f"rank {rank}: {exc}"
+            errors = [None] * world
+            dist.all_gather_object(errors, error, group=group)
+            errors = [e for e in errors if e]
+            self.fallback = errors[0] if errors else None
+            if errors:
+                if error is None:
+                    local.shard_detach()
+                self.exchange = "collective"
         # changed-rows exchange (see the module docstring); packets hold at
         # most n/16 rows
         self.delta = delta and hasattr(local, "pack_rows")
@@ -195,6 +242,14 @@ class ShardedNfEngine:
         if self.n == 0:
             return IterationReport(0.0, 0)
         self.local.shard_compute()
+        if self.exchange == "peer":
+            # the kernels pushed rows, bitmap words and block sums into the
+            # peers' arenas: once every rank's compute is done, commit
+            self.local.wait_compute()
+            dist.barrier(group=self.group)
+            rep = self.local.shard_commit()
+            self.last_modified = rep.modified
+            return rep
         self.local.before_exchange()
         rows_done = False
         if self.delta and self.delta_ratio * self.last_modified < self.n:
@@ -239,4 +294,8 @@ class ShardedNfEngine:
         return est
 
     def close(self):
+        if self.exchange == "peer":
+            # unmap the peers' arenas before any owner frees its own
+            self.local.shard_detach()
+            dist.barrier(group=self.group)
         self.local.close()

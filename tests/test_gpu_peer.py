@@ -1,0 +1,165 @@
+"""Peer-push exchange of sharded steps (hanf_shard_export / hanf_shard_attach,
+include/hanf.h) on the one GPU a round has.
+
+* In one process: 2 and 3 shard engines on cuda:0 attached with
+  hanf_shard_attach_local.  Every union / worklist kernel stores its written
+  rows into the other engines' next generation and publishes bitmap words
+  and block sums; no exchange code runs on the host.  Computes run one after
+  another and each finishes before the next begins (no kernel waits on
+  another).  The schedule also lets a shard start step t+1 before another
+  has committed step t - the case the per-generation block-sum inbox is
+  for.  Equal to one engine bit for bit (N(t), modified, every counter).
+* Across processes: 2 ranks on the same GPU, arenas mapped with CUDA IPC
+  handles (hanf_shard_attach), ShardedNfEngine(exchange="peer") with a gloo
+  barrier between compute and commit.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_local(hanf, g, cfg, world, skew):
+    import torch
+    from paper_1011_5599_b200.sharded import LocalCudaShard, shard_ranges
+    dev = torch.device("cuda", 0)
+    shards = [LocalCudaShard(g, cfg, lo, hi, dev) for lo, hi in shard_ranges(g.num_nodes(), world)]
+    engines = [sh.engine for sh in shards]
+    for k, e in enumerate(engines):
+        e.shard_attach_local(engines, k)
+    values, mods = [shards[0].sum_estimates()], [g.num_nodes()]
+    pending = None  # skew: shard 0's commit of step t after shard 1's compute of t+1
+    while True:
+        for sh in shards:
+            sh.shard_compute()
+            sh.wait_compute()
+        reps = [sh.shard_commit() for sh in shards[:1]] if skew else []
+        if skew:
+            # shard 0 runs ahead into its next compute (writes the other
+            # generation of every peer's arena and block-sum inbox) before the
+            # others commit this step
+            if reps[0].modified:
+                shards[0].shard_compute()
+                shards[0].wait_compute()
+                pending = True
+            reps += [sh.shard_commit() for sh in shards[1:]]
+        else:
+            reps = [sh.shard_commit() for sh in shards]
+        assert all(r.sum == reps[0].sum and r.modified == reps[0].modified for r in reps)
+        if reps[0].modified == 0:
+            break
+        values.append(reps[0].sum)
+        mods.append(reps[0].modified)
+        if skew and pending:
+            # the others now compute step t+1; shard 0 already did
+            for sh in shards[1:]:
+                sh.shard_compute()
+                sh.wait_compute()
+            reps = [sh.shard_commit() for sh in shards]
+            assert all(r.sum == reps[0].sum and r.modified == reps[0].modified for r in reps)
+            pending = None
+            if reps[0].modified == 0:
+                break
+            values.append(reps[0].sum)
+            mods.append(reps[0].modified)
+    counters = [e.counters() for e in engines]
+    for sh in shards:
+        sh.shard_detach()
+    for sh in shards:
+        sh.close()
+    return values, mods, counters
+
+
+@pytest.mark.parametrize("b,env,world,skew", [
+    (6, {}, 2, False), (6, {}, 3, False), (6, {}, 2, True), (6, {"HANF_SPARSE": "1"}, 2, False),
+    (6, {"HANF_SPARSE": "1"}, 3, True), (5, {}, 2, True), (8, {}, 2, False), (7, {}, 3, False)])
+def test_peer_push_local(hanf, monkeypatch, b, env, world, skew):
+    """Attached shard engines of one process: bit-exact with one engine, with
+    the worklist step, the padded W = 3 rows, m = 128 and a multi-chunk layout."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
+    cfg = hanf.EngineConfig(bucket_bits=b, seed=42)
+    values, mods, counters = _run_local(hanf, g, cfg, world, skew)
+    with hanf.NfEngine(g, cfg) as e:
+        single = e.run_to_stabilisation()
+        ref = e.counters()
+    assert values == single.values and mods == single.modified
+    for c in counters:
+        assert np.array_equal(c, ref)
+
+
+def test_peer_attach_rejects_bad_peer_sets(hanf):
+    import torch
+    from paper_1011_5599_b200.sharded import LocalCudaShard, shard_ranges
+    dev = torch.device("cuda", 0)
+    g = hanf.gen_rmat(12, 8, 0.57, 0.19, 0.19, 1, 7)
+    n = g.num_nodes()
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=1)
+    a, b = [LocalCudaShard(g, cfg, lo, hi, dev) for lo, hi in shard_ranges(n, 2)]
+    other = LocalCudaShard(g, hanf.EngineConfig(bucket_bits=7, seed=1), 0, n // 2, dev)
+    try:
+        with pytest.raises(ValueError):        # ranges do not tile [0, n)
+            a.engine.shard_attach_local([a.engine, a.engine], 0)
+        with pytest.raises(ValueError):        # self is not this engine
+            a.engine.shard_attach_local([a.engine, b.engine], 1)
+        with pytest.raises(ValueError):        # different counter layout
+            other.engine.shard_attach_local([other.engine, b.engine], 0)
+        exports = [a.engine.shard_export(), b.engine.shard_export()]
+        with pytest.raises(ValueError):        # exports[self] must describe the engine
+            a.engine.shard_attach(exports, 1)
+    finally:
+        for sh in (a, b, other):
+            sh.close()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _ipc_worker(rank, world, port, out):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1011_5599_b200 as hanf
+    from paper_1011_5599_b200.sharded import ShardedNfEngine
+    torch.cuda.set_device(0)
+    g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
+    eng = ShardedNfEngine(g, cfg, rank, world, exchange="peer")
+    est = eng.run_to_stabilisation()
+    out[rank] = (est.values, est.modified, eng.local.engine.counters())
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_push_ipc_two_processes(hanf):
+    """Two ranks in two processes on one GPU, arenas mapped through CUDA IPC
+    handles, ShardedNfEngine(exchange="peer"): equal to one engine."""
+    import torch.multiprocessing as mp
+    g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
+    with hanf.NfEngine(g, cfg) as e:
+        single = e.run_to_stabilisation()
+        ref = e.counters()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_ipc_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    for r in range(2):
+        values, mods, counters = out[r]
+        assert values == single.values and mods == single.modified
+        assert np.array_equal(counters, ref)
