@@ -76,6 +76,12 @@ typedef struct {
                                  engine.hpp:115-117; 0: deterministic device tree */
   uint64_t shard_begin;       /* node range [shard_begin, shard_end) this engine */
   uint64_t shard_end;         /* updates; (0, 0) = all nodes (single GPU) */
+  uint32_t shard_count;       /* shards of the run (0: unknown).  With the peer-push
+                                 exchange, equal shards of a graph whose counters
+                                 exceed L2 and whose ids lack locality are
+                                 relabelled by degree, interleaved across the
+                                 shards (balanced arcs, hot rows first in each) */
+  uint32_t reserved;
 } hanf_config;
 
 /* IterationReport (engine.hpp:48-51) */
@@ -211,6 +217,9 @@ typedef struct {
   uint64_t blocks;         /* ceil(n/64) */
   uint64_t shard_begin, shard_end; /* node range updated by this engine */
   uint64_t row_pitch;      /* u64 words between consecutive counters (>= W) */
+  uint32_t relabelled;     /* rows are renumbered by degree (counters of row r are
+                              node order[r]'s; hanf_read_counters undoes it) */
+  uint32_t reserved;
 } hanf_buffers;
 hanf_status hanf_device_buffers(hanf_engine* engine, hanf_buffers* out);
 /* Sharded step, phase 1: compute this engine's node range into the next
@@ -253,7 +262,7 @@ typedef struct {
   uint64_t n, row_pitch;
   uint64_t shard_begin, shard_end;
   int32_t device;
-  int32_t reserved;
+  int32_t relabelled;      /* relabelled shards (hanf_config.shard_count): all or none */
 } hanf_shard_peer;
 #define HANF_MAX_PEERS 7
 /* Describes this shard engine's arena for the other ranks. */

@@ -78,6 +78,7 @@ struct EngineConfig {
   int device = 0;
   bool exact_sum = true;
   std::uint64_t shard_begin = 0, shard_end = 0;
+  std::uint32_t shard_count = 0;
 
   hanf_config to_c() const {
     hanf_config c;
@@ -98,6 +99,7 @@ struct EngineConfig {
     c.exact_sum = exact_sum;
     c.shard_begin = shard_begin;
     c.shard_end = shard_end;
+    c.shard_count = shard_count;
     return c;
   }
 };

@@ -28,7 +28,7 @@ class Config(Structure):
                 ("spill_to_disk", c_int32), ("track_modified", c_int32),
                 ("use_systolic", c_int32), ("device", c_int32),
                 ("exact_sum", c_int32), ("shard_begin", c_uint64),
-                ("shard_end", c_uint64)]
+                ("shard_end", c_uint64), ("shard_count", c_uint32), ("reserved", c_uint32)]
 
 
 class IterationReportC(Structure):
@@ -45,14 +45,15 @@ class BuffersC(Structure):
     _fields_ = [("next_counters", c_void_p), ("next_modified", c_void_p),
                 ("block_sums", c_void_p), ("words_per_counter", c_uint64),
                 ("blocks", c_uint64), ("shard_begin", c_uint64),
-                ("shard_end", c_uint64), ("row_pitch", c_uint64)]
+                ("shard_end", c_uint64), ("row_pitch", c_uint64),
+                ("relabelled", c_uint32), ("reserved", c_uint32)]
 
 
 class ShardPeerC(Structure):
     """hanf_shard_peer: one rank's exchange arena (peer-push exchange)."""
     _fields_ = [("ipc_handle", ctypes.c_uint8 * 64), ("arena_bytes", c_uint64),
                 ("n", c_uint64), ("row_pitch", c_uint64), ("shard_begin", c_uint64),
-                ("shard_end", c_uint64), ("device", c_int32), ("reserved", c_int32)]
+                ("shard_end", c_uint64), ("device", c_int32), ("relabelled", c_int32)]
 
 
 MAX_PEERS = 7

@@ -384,7 +384,9 @@ __device__ __forceinline__ void shfl_max(uint32_t (&x)[Lay::kLimbs], int offset)
 constexpr int kMaxPeers = 7;
 struct PeerRows {
   uint64_t* next[kMaxPeers];
+  double* est[kMaxPeers];  // relabelled shards: estimates of changed rows too
   uint32_t count;
+  uint32_t push_est;
 };
 
 struct EstimateParams {

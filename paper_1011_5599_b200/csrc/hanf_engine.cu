@@ -254,6 +254,10 @@ struct hanf_engine {
   double* h_batch_sums[2] = {nullptr, nullptr};   // pinned [batch][blocks_real] per parity
   std::vector<double> batch_last;                 // N(t) of every run
   bool relabel = false;
+  // relabelled shard of a peer-push run: rows interleaved across the
+  // shards by degree; estimates are pushed to the peers and every commit
+  // recomputes all original-id blocks from the full estimate array
+  bool shard_relabel = false;
   // relabelled engines keep estimates in row order (writes follow the task
   // order); finish_kernel gathers them through perm for the original-id
   // block sums.  HANF_EST_SCATTER=1: scatter to the original slot instead.
@@ -304,7 +308,10 @@ struct hanf_engine {
   // words and block sums (peer-push exchange, hanf_shard_attach).
   void* arena = nullptr;
   uint64_t arena_bytes = 0;
-  uint64_t arena_off[6] = {};                // cnt0 cnt1 mod0 mod1 inbox0 inbox1
+  uint64_t arena_off[8] = {};                // cnt0 cnt1 mod0 mod1 inbox0 inbox1 est0 est1
+  // relabelled shards: estimates per generation (a fast peer's step t+1
+  // must not overwrite what this rank's commit t re-sums); est = est_gen[cur]
+  double* est_gen[2] = {nullptr, nullptr};
   double* inbox[2] = {nullptr, nullptr};     // block sums of all shards, per generation
   bool attached = false;
   uint32_t npeers = 0;
@@ -352,6 +359,8 @@ struct hanf_engine {
       cnt[0] = cnt[1] = nullptr;
       mod[0] = mod[1] = nullptr;
       inbox[0] = inbox[1] = nullptr;
+      est = nullptr;
+      est_gen[0] = est_gen[1] = nullptr;
     }
     if (stream) {
       for (int i = 0; i < 2; ++i) {
@@ -424,7 +433,9 @@ bool ids_local(const hanf_graph_view* g) {
 
 // Bitmap of the counters changed into generation g, in original ids (what
 // the block sums and the modified count read).
-uint64_t* dirty_of(const hanf_engine* e, int g) { return e->relabel ? e->dirty[g] : e->mod[g]; }
+// (relabelled shard engines keep no original-id bitmap: their commit
+// recomputes every block, hanf_engine::shard_relabel)
+uint64_t* dirty_of(const hanf_engine* e, int g) { return e->dirty[g] ? e->dirty[g] : e->mod[g]; }
 
 // Recomputes estimates of the counters flagged in `dirty` (all when null)
 // for blocks [b0, b1) of generation g.
@@ -460,10 +471,10 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
 hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute, uint64_t b0,
                            uint64_t b1, bool in_step) {
   hanf::FinishArgs f{};
-  f.est = recompute ? e->est : nullptr;
+  f.est = recompute ? (in_step && e->shard_relabel ? e->est_gen[1 - e->cur] : e->est) : nullptr;
   f.bits = bits;
   // peer-push shards total the inbox the peers published into
-  double* sums = in_step && e->attached ? e->inbox[1 - e->cur] : e->block_sums;
+  double* sums = in_step && e->attached && !e->shard_relabel ? e->inbox[1 - e->cur] : e->block_sums;
   f.block_sums = sums;
   f.out = e->reduce;
   f.n = e->n;
@@ -471,6 +482,8 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   f.b0 = b0;
   f.b1 = b1;
   f.perm = e->est_rows ? e->perm : nullptr;
+  // relabelled shards: every block from the (peer-pushed) estimates
+  f.all_dirty = in_step && e->shard_relabel ? 1 : 0;
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
@@ -558,13 +571,17 @@ hanf_status seed_all(hanf_engine* e) {
                               e->params.seed, e->order, e->batch, e->batch_mix, e->stream,
                               &e->launches));
   HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
-  if (e->relabel) {  // every counter was seeded: all ones in both id spaces
+  if (e->dirty[0]) {  // every counter was seeded: all ones in both id spaces
     HANF_CUDA(cudaMemcpyAsync(e->dirty[0], e->mod[0], sizeof(uint64_t) * e->blocks,
                               cudaMemcpyDeviceToDevice, e->stream));
     HANF_CUDA(cudaMemsetAsync(e->dirty[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
   }
+  if (e->shard_relabel) e->est = e->est_gen[0];
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
   if (st != HANF_OK) return st;
+  if (e->shard_relabel)  // both generations hold the seeded estimates
+    HANF_CUDA(cudaMemcpyAsync(e->est_gen[1], e->est_gen[0], sizeof(double) * e->n,
+                              cudaMemcpyDeviceToDevice, e->stream));
   uint64_t count = 0;
   e->last_count = e->n;
   if (e->batch > 1) {  // N(0) of every run, in the reference's order
@@ -649,8 +666,11 @@ hanf_status ensure_sparse(hanf_engine* e) {
 hanf::PeerRows peer_rows(const hanf_engine* e, int ng) {
   hanf::PeerRows p{};
   p.count = e->attached ? e->npeers : 0;
-  for (uint32_t i = 0; i < p.count; ++i)
+  p.push_est = e->shard_relabel ? 1u : 0u;
+  for (uint32_t i = 0; i < p.count; ++i) {
     p.next[i] = reinterpret_cast<uint64_t*>(e->peer_base[i] + e->arena_off[ng]);
+    p.est[i] = reinterpret_cast<double*>(e->peer_base[i] + e->arena_off[6 + ng]);
+  }
   return p;
 }
 
@@ -661,7 +681,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.num_wtasks = e->tasks.num_wtasks;
   a.zero_row = static_cast<uint32_t>(e->n);
   const bool fused = hanf::fused_estimates(e->params.register_bits, e->params.registers);
-  a.est = fused ? e->est : nullptr;
+  a.est = fused ? (e->shard_relabel ? e->est_gen[ng] : e->est) : nullptr;
   a.ep = hanf::EstimateParams{e->params.alpha, static_cast<double>(e->params.registers),
                               e->params.registers, e->params.register_bits,
                               e->params.words_per_counter, e->log_table};
@@ -681,7 +701,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.stale_valid = e->stale_valid ? 1 : 0;
   a.orig_of = e->order;
   a.est_index = e->est_rows ? nullptr : e->order;
-  a.dirty_next = e->relabel ? e->dirty[ng] : nullptr;
+  a.dirty_next = e->dirty[ng];
   a.peers = peer_rows(e, ng);
   return a;
 }
@@ -713,7 +733,7 @@ hanf_status compute_sparse(hanf_engine* e) {
   a.hub_index = e->hub_index;
   a.orig_of = e->order;
   a.est_index = e->est_rows ? nullptr : e->order;
-  a.dirty_next = e->relabel ? e->dirty[ng] : nullptr;
+  a.dirty_next = e->dirty[ng];
   a.hub_first = e->tasks.hub_first;
   a.hub_count = e->tasks.hub_count;
   a.n = e->n;
@@ -746,7 +766,7 @@ hanf_status compute_local(hanf_engine* e) {
   const int ng = 1 - e->cur;
   hanf::PublishArgs p{};
   p.mod_next = e->mod[ng];
-  p.block_sums = e->block_sums;
+  p.block_sums = e->shard_relabel ? nullptr : e->block_sums;  // (commit redoes all blocks)
   p.w0 = e->lo >> 6;
   p.w1 = (e->hi + 63) >> 6;
   p.count = e->npeers;
@@ -761,9 +781,12 @@ hanf_status compute_local(hanf_engine* e) {
 
 hanf_status compute_shard(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
+  if (e->shard_relabel && !e->attached)
+    return fail(HANF_INVALID_ARGUMENT,
+                "relabelled shard engines exchange through hanf_shard_attach (peer-push)");
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
   HANF_CUDA(cudaMemsetAsync(e->mod[ng] + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
-  if (e->relabel)  // unsharded: the whole original-id bitmap
+  if (e->dirty[ng])  // unsharded relabelling: the whole original-id bitmap
     HANF_CUDA(cudaMemsetAsync(e->dirty[ng], 0, sizeof(uint64_t) * e->blocks, e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
   if (step_mode(e) == 2 && e->tr_off) {
@@ -798,7 +821,7 @@ hanf_status compute_shard(hanf_engine* e) {
     // (row-order estimates: the row bitmap says which rows to redo)
     const hanf_status st = run_estimates(e, ng, e->est_rows ? e->mod[ng] : dirty_of(e, ng), w0, w1);
     if (st != HANF_OK) return st;
-  } else if (sharded) {
+  } else if (sharded && !e->shard_relabel) {
     // block sums of this shard now: they are exchanged before commit
     hanf::FinishArgs f{e->est, e->mod[ng], e->block_sums, e->reduce, e->n, e->blocks, w0, w1};
     HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
@@ -810,7 +833,7 @@ bool commit_recomputes(const hanf_engine* e) {
   // single GPU with fused estimates: the block sums are recomputed in the
   // same launch as the totals
   const bool sharded = e->lo != 0 || e->hi != e->n;
-  return e->est_rows ||
+  return e->est_rows || e->shard_relabel ||
          (!sharded && hanf::fused_estimates(e->params.register_bits, e->params.registers));
 }
 
@@ -824,6 +847,7 @@ hanf_status commit_enqueue(hanf_engine* e) {
 // known (engine.hpp:198-216); N(t) is set by the caller.
 void advance_state(hanf_engine* e, uint64_t count) {
   e->cur = 1 - e->cur;                             // std::swap, engine.hpp:198-200
+  if (e->shard_relabel) e->est = e->est_gen[e->cur];
   e->stale_valid = true;
   if (e->cfg.use_systolic && !e->systolic && count > 0 &&
       static_cast<double>(count) < e->cfg.systolic_threshold * static_cast<double>(e->n))
@@ -838,6 +862,7 @@ hanf_status commit_complete(hanf_engine* e, hanf_iteration_report* rep) {
   const hanf_status st = finish_complete(e, &total, &count, true);
   if (st != HANF_OK) return st;
   e->cur = 1 - e->cur;                             // std::swap, engine.hpp:198-200
+  if (e->shard_relabel) e->est = e->est_gen[e->cur];
   e->stale_valid = true;
   if (e->cfg.use_systolic && !e->systolic && count > 0 &&
       static_cast<double>(count) < e->cfg.systolic_threshold * static_cast<double>(e->n))
@@ -926,6 +951,8 @@ hanf_status hanf_config_init(hanf_config* cfg) {
   cfg->exact_sum = 1;
   cfg->shard_begin = 0;
   cfg->shard_end = 0;
+  cfg->shard_count = 0;
+  cfg->reserved = 0;
   return HANF_OK;
 }
 
@@ -1012,7 +1039,15 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   // HANF_RELABEL=1/0 forces it; by default graphs whose counters do not fit
   // in L2 (one generation > 64 MB) and whose ids show no locality (sampled
   // successors far from their source) are renumbered by degree.
-  if (lo == 0 && hi == n && n > 0 && K == 1) {
+  // Shards relabel only for the peer-push exchange (cfg.shard_count), with
+  // equal shards and fused estimates: rows are interleaved across the
+  // shards in degree order (relabel_order_device `ways`).
+  const bool shard_cfg = lo != 0 || hi != n;
+  const bool shard_may_relabel =
+      shard_cfg && cfg.shard_count > 1 && n > 0 && n % (64ull * cfg.shard_count) == 0 &&
+      hi - lo == n / cfg.shard_count && lo % (n / cfg.shard_count) == 0 &&
+      hanf::fused_estimates(params.register_bits, params.registers);
+  if ((!shard_cfg || shard_may_relabel) && n > 0 && K == 1) {
     const char* rl = std::getenv("HANF_RELABEL");
     if (rl && (rl[0] == '0' || rl[0] == '1'))
       e->relabel = rl[0] == '1';
@@ -1020,6 +1055,14 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       e->relabel = (n + 1) * e->pitch * 8 > (64ull << 20) && !ids_local(g);
     const char* sc = std::getenv("HANF_EST_SCATTER");
     e->est_rows = e->relabel && !(sc && sc[0] == '1');
+    if (shard_cfg && e->relabel) {
+      // estimates stay in row order and are pushed to the peers with their
+      // rows; the commit gathers them through perm for every block
+      // (HANF_EST_SCATTER=1: original slots - random pushes, measured 1.36x
+      // slower per R-MAT 26 shard step, scripts/shard_relabel_time.py)
+      e->shard_relabel = true;
+      e->sparse_ok = false;  // (the worklist needs a row-space CSR of the shard)
+    }
   }
 
   auto bail = [&](hanf_status s) {
@@ -1047,10 +1090,11 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   if (sharded) {
     // the exchange arena (see hanf_engine::arena): same offsets on every rank
     auto al = [](uint64_t bytes) { return (bytes + 255) & ~255ull; };
-    const uint64_t sizes[6] = {nw * 8, nw * 8, (e->blocks + 1) * 8, (e->blocks + 1) * 8,
-                               e->blocks * 8, e->blocks * 8};
+    const uint64_t sizes[8] = {nw * 8, nw * 8, (e->blocks + 1) * 8, (e->blocks + 1) * 8,
+                               e->blocks * 8, e->blocks * 8, n * 8,
+                               e->shard_relabel ? n * 8 : 8};
     uint64_t off = 0;
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i < 8; ++i) {
       e->arena_off[i] = off;
       off += al(sizes[i] ? sizes[i] : 8);
     }
@@ -1061,6 +1105,11 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       e->cnt[i] = reinterpret_cast<uint64_t*>(base + e->arena_off[i]);
       e->mod[i] = reinterpret_cast<uint64_t*>(base + e->arena_off[2 + i]);
       e->inbox[i] = reinterpret_cast<double*>(base + e->arena_off[4 + i]);
+    }
+    e->est = reinterpret_cast<double*>(base + e->arena_off[6]);
+    if (e->shard_relabel) {
+      e->est_gen[0] = e->est;
+      e->est_gen[1] = reinterpret_cast<double*>(base + e->arena_off[7]);
     }
   } else {
     HANF_TRY(palloc(&e->cnt[0], nw, s));
@@ -1090,7 +1139,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   while (((n + 1) >> e->summ_shift) >= (1ull << 18)) ++e->summ_shift;
   e->summ_bits = ((n + 1) >> e->summ_shift) + 1;
   HANF_TRY(palloc(&e->summ, (e->summ_bits + 63) / 64, s));
-  HANF_TRY(palloc(&e->est, n, s));
+  if (!sharded) HANF_TRY(palloc(&e->est, n, s));
   HANF_TRY(palloc(&e->block_sums, e->blocks, s));
   {
     const uint64_t ctas = (e->blocks + hanf::kFinishBlocks - 1) / hanf::kFinishBlocks;
@@ -1141,7 +1190,9 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     // the shard's CSR goes to the device to build the tasks (it is laid
     // out again in task order there) and stays for the worklist step
     // (batched runs upload the caller's graph and lift it on the device)
-    const uint64_t up_lo = K > 1 ? 0 : lo, up_hi = K > 1 ? n_real : hi;
+    // (relabelled shards: the whole graph - their rows are spread over it)
+    const bool whole = K > 1 || e->shard_relabel;
+    const uint64_t up_lo = whole ? 0 : lo, up_hi = whole ? n_real : hi;
     uint64_t a0 = g->offsets[up_lo], a1 = g->offsets[up_hi];
     uint64_t* d_off = nullptr;
     uint32_t* d_succ = nullptr;
@@ -1214,13 +1265,17 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     if (e->relabel) {
       // renumber rows by out-degree (offsets only: overlaps the arcs upload)
       hanf::RelabelOut r;
-      const cudaError_t re = hanf::relabel_order_device(d_off, n, s, &r, &e->launches);
+      const cudaError_t re = hanf::relabel_order_device(
+          d_off, n, e->shard_relabel ? cfg.shard_count : 1, s, &r, &e->launches);
       e->order = r.order;
       e->perm = r.perm;
       e->rl_off = r.off;
       HANF_TRY(re);
-      HANF_TRY(palloc(&e->dirty[0], e->blocks, s));
-      HANF_TRY(palloc(&e->dirty[1], e->blocks, s));
+      if (e->shard_relabel) pfree(e->rl_off, s);  // (no worklist step: no relabelled CSR)
+      if (!e->shard_relabel) {
+        HANF_TRY(palloc(&e->dirty[0], e->blocks, s));
+        HANF_TRY(palloc(&e->dirty[1], e->blocks, s));
+      }
       phase("relabel");
     }
     st = seed_all(e);
@@ -1228,7 +1283,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     phase("seed");
     int bad = 0;
     // relabelled: row v's successors are the caller's arcs of order[v], through perm
-    const hanf::CsrView view{d_off, lo, d_succ, a0, e->order, e->perm, n};
+    const hanf::CsrView view{d_off, up_lo, d_succ, a0, e->order, e->perm, n};
     const cudaError_t be =
         hanf::build_tasks_device(view, lo, hi, n, s, ev_arcs, &e->tasks, &bad, &e->launches);
     // (also on the build's error paths) frees on `s` come after the upload
@@ -1243,6 +1298,10 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     if (bad)
       return bail(fail(HANF_INVALID_ARGUMENT,
                        "arc endpoint out of range or offsets not non-decreasing"));
+    if (e->shard_relabel) {  // the TOS holds the shard's rows; no worklist CSR is kept
+      pfree(e->csr_off, s);
+      pfree(e->csr_succ, s);
+    }
     phase("build");
     HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
   }
@@ -1419,7 +1478,7 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
   // every counter counts as modified: the next step recomputes every node
   HANF_CUDA(hanf::launch_seed_bitmap(e->mod[0], e->n, s));
   HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, s));
-  if (e->relabel) {
+  if (e->dirty[0]) {
     HANF_CUDA(cudaMemcpyAsync(e->dirty[0], e->mod[0], sizeof(uint64_t) * e->blocks,
                               cudaMemcpyDeviceToDevice, s));
     HANF_CUDA(cudaMemsetAsync(e->dirty[1], 0, sizeof(uint64_t) * e->blocks, s));
@@ -1429,8 +1488,12 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
   e->cur = 0;
   e->stale_valid = false;
   e->systolic = false;
+  if (e->shard_relabel) e->est = e->est_gen[0];
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
   if (st != HANF_OK) return st;
+  if (e->shard_relabel)
+    HANF_CUDA(cudaMemcpyAsync(e->est_gen[1], e->est_gen[0], sizeof(double) * e->n,
+                              cudaMemcpyDeviceToDevice, s));
   uint64_t count = 0;
   st = finish(e, dirty_of(e, 0), e->est_rows, 0, e->est_rows ? e->blocks : 0, &e->last_sum,
               &count);
@@ -1564,6 +1627,7 @@ hanf_status hanf_shard_export(hanf_engine* e, hanf_shard_peer* out) {
   out->shard_begin = e->lo;
   out->shard_end = e->hi;
   out->device = e->device;
+  out->relabelled = e->shard_relabel ? 1 : 0;
   out->arena_bytes = e->arena_bytes;
   if (!e->arena) return HANF_OK;  // a one-shard engine (all nodes): nothing to map
   HANF_CUDA(cudaSetDevice(e->device));
@@ -1584,12 +1648,12 @@ hanf_status check_peers(const hanf_engine* e, const hanf_shard_peer* peers, uint
     return fail(HANF_INVALID_ARGUMENT, "peer-push exchange: at most 8 shards");
   const hanf_shard_peer& me = peers[self];
   if (me.n != e->n || me.shard_begin != e->lo || me.shard_end != e->hi ||
-      me.arena_bytes != e->arena_bytes)
+      me.arena_bytes != e->arena_bytes || me.relabelled != (e->shard_relabel ? 1 : 0))
     return fail(HANF_INVALID_ARGUMENT, "peers[self] does not describe this engine");
   std::vector<std::pair<uint64_t, uint64_t>> ranges;
   for (uint32_t p = 0; p < count; ++p) {
     if (peers[p].n != e->n || peers[p].row_pitch != e->pitch ||
-        peers[p].arena_bytes != e->arena_bytes)
+        peers[p].arena_bytes != e->arena_bytes || peers[p].relabelled != me.relabelled)
       return fail(HANF_INVALID_ARGUMENT, "peer engines differ in graph or counter layout");
     if (peers[p].shard_end > peers[p].shard_begin)
       ranges.emplace_back(peers[p].shard_begin, peers[p].shard_end);
@@ -1648,6 +1712,7 @@ hanf_status hanf_shard_attach_local(hanf_engine* e, hanf_engine* const* peers, u
     desc[p].shard_end = peers[p]->hi;
     desc[p].arena_bytes = peers[p]->arena_bytes;
     desc[p].device = peers[p]->device;
+    desc[p].relabelled = peers[p]->shard_relabel ? 1 : 0;
   }
   hanf_status st = check_peers(e, desc.data(), count, self);
   if (st != HANF_OK) return st;
@@ -1898,6 +1963,8 @@ hanf_status hanf_device_buffers(hanf_engine* e, hanf_buffers* out) {
   out->blocks = e->blocks;
   out->shard_begin = e->lo;
   out->shard_end = e->hi;
+  out->relabelled = e->relabel ? 1u : 0u;
+  out->reserved = 0;
   return HANF_OK;
 }
 

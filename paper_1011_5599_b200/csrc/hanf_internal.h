@@ -80,8 +80,11 @@ struct RelabelOut {
   uint32_t* perm = nullptr;
   uint64_t* off = nullptr;
 };
-cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, cudaStream_t s, RelabelOut* out,
-                                 uint64_t* launches);
+// ways > 1 (relabelled shards, n a multiple of 64 * ways): degree rank i
+// goes to row (i mod ways) * n/ways + i / ways, so every shard's rows get
+// the same degree profile with its hot rows first.
+cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t ways, cudaStream_t s,
+                                 RelabelOut* out, uint64_t* launches);
 // The relabelled arcs (only the worklist step's transpose needs them; the
 // union sweep's TOS is filled through CsrView).  *bad = arc endpoint >= n.
 cudaError_t relabel_arcs_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n,
@@ -254,13 +257,14 @@ struct FinishArgs {
   uint64_t blocks;        // totals over [0, blocks)
   uint64_t b0, b1;        // block sums recomputed over [b0, b1)
   const uint32_t* perm = nullptr;  // estimates in row order: original id o is est[perm[o]]
+  int32_t all_dirty = 0;           // recompute every block of [b0, b1) (bits: count only)
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
 // Peer-push exchange: bitmap words and block sums [w0, w1) of this shard
 // into every peer's arena (and the block sums into the local inbox).
 struct PublishArgs {
   const uint64_t* mod_next;
-  const double* block_sums;
+  const double* block_sums;  // nullptr: bitmap words only
   uint64_t w0, w1;
   uint64_t* peer_mod[kMaxPeers];
   double* peer_sums[kMaxPeers + 1];  // [count] = the local inbox

@@ -231,6 +231,15 @@ __device__ __forceinline__ void mark_changed(uint64_t* mod_next, uint64_t* dirty
   }
 }
 
+// Estimate of a changed counter into its slot (and, for relabelled shards,
+// into every peer's estimate array: their commits re-sum all blocks).
+__device__ __forceinline__ void push_estimate(const UnionArgs& args, uint32_t v, double e) {
+  const uint32_t slot = est_slot(args.est_index, v);
+  args.est[slot] = e;
+  if (args.peers.push_est)
+    for (uint32_t p = 0; p < args.peers.count; ++p) args.peers.est[p][slot] = e;
+}
+
 // Max over a split node's chunk partials and its own counter (one warp),
 // then the usual commit.  Partials were written by other warps of the same
 // launch: read through L2 (ld.cg) after the ticket handshake.
@@ -269,7 +278,8 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
         for (uint32_t p = 0; p < args.peers.count; ++p)
           store_chunk<Lay, kVec16>(args.peers.next[p] + off, acc);
       }
-      if (changed && args.est) args.est[est_slot(args.est_index, v)] = estimate_limbs<Lay>(acc, args.ep);
+      if (args.est && (changed || (stale && args.peers.push_est)))
+        push_estimate(args, v, estimate_limbs<Lay>(acc, args.ep));
     }
   }
   if (lane == 0 && any_changed) mark_changed(args.mod_next, args.dirty_next, args.orig_of, v);
@@ -322,7 +332,10 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
           store_chunk<Lay, kVec16>(args.peers.next[p] + off, acc);
       }
     }
-    if (changed && args.est) args.est[est_slot(args.est_index, v)] = estimate_limbs<Lay>(acc, args.ep);
+    // (relabelled shards keep estimates per generation: a stale row's
+    // estimate is rewritten with its row)
+    if (args.est && (changed || (lead && stale && args.peers.push_est)))
+      push_estimate(args, v, estimate_limbs<Lay>(acc, args.ep));
   }
 }
 
@@ -888,7 +901,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
   const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kFinishBlocks;
   if (t < kFinishBlocks) {
     const uint64_t b = b0 + t;
-    dirty[t] = (b < a.blocks && b >= a.b0 && b < a.b1) ? a.bits[b] : 0;
+    dirty[t] = (b < a.blocks && b >= a.b0 && b < a.b1) ? (a.all_dirty ? ~0ull : a.bits[b]) : 0;
   }
   __syncthreads();
   if (a.est) {
@@ -912,7 +925,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
   if (t < kFinishBlocks && b < a.blocks) {
     const uint64_t word = a.bits[b];
     cnt = __popcll(word);
-    if (a.est && word != 0 && b >= a.b0 && b < a.b1) {
+    if (a.est && (word != 0 || a.all_dirty) && b >= a.b0 && b < a.b1) {
       const uint64_t first = b * 64;
       const uint32_t last = a.n - first < 64 ? static_cast<uint32_t>(a.n - first) : 64u;
       const double* row = tile + t * 65;
@@ -958,12 +971,12 @@ __global__ void publish_kernel(const PublishArgs a) {
        i += stride) {
     const uint64_t w = a.w0 + i;
     const uint64_t bits = a.mod_next[w];
-    const double sum = a.block_sums[w];
-    for (uint32_t p = 0; p < a.count; ++p) {
-      a.peer_mod[p][w] = bits;
-      a.peer_sums[p][w] = sum;
+    for (uint32_t p = 0; p < a.count; ++p) a.peer_mod[p][w] = bits;
+    if (a.block_sums) {
+      const double sum = a.block_sums[w];
+      for (uint32_t p = 0; p < a.count; ++p) a.peer_sums[p][w] = sum;
+      a.peer_sums[a.count][w] = sum;
     }
-    a.peer_sums[a.count][w] = sum;
   }
 }
 

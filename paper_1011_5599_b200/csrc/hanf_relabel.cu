@@ -62,6 +62,16 @@ __global__ void score_keys_kernel(const uint64_t* __restrict__ off, uint64_t n,
   }
 }
 
+// Relabelled shards: degree rank i -> row (i mod ways) * (n / ways) + i / ways
+__global__ void interleave_kernel(const uint32_t* __restrict__ sorted, uint64_t n, uint32_t ways,
+                                  uint32_t* __restrict__ order) {
+  const uint64_t per = n / ways;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += stride)
+    order[(i % ways) * per + i / ways] = sorted[i];
+}
+
 // perm[order[r]] = r; new degree of row r (for the offsets scan)
 __global__ void invert_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ order,
                               uint64_t n, uint32_t* __restrict__ perm, uint64_t* __restrict__ ndeg) {
@@ -164,8 +174,8 @@ struct Phases {  // HANF_PROFILE=1: synchronising phase times
 };
 }  // namespace
 
-cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, cudaStream_t s, RelabelOut* out,
-                                 uint64_t* launches) {
+cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t ways, cudaStream_t s,
+                                 RelabelOut* out, uint64_t* launches) {
   *out = RelabelOut{};
   if (n == 0) return cudaSuccess;
   Phases phase{s};
@@ -199,6 +209,15 @@ cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, cudaStream_t
   HANF_RELABEL_TRY(cudaFreeAsync(vals, s));
   HANF_RELABEL_TRY(cudaFreeAsync(skeys, s));
   HANF_RELABEL_TRY(cudaFreeAsync(d_bad, s));
+  if (ways > 1) {
+    if (n % (64ull * ways) != 0) return cudaErrorInvalidValue;
+    uint32_t* inter = nullptr;
+    HANF_RELABEL_TRY(pool_alloc(&inter, n, s));
+    interleave_kernel<<<grid(n), threads, 0, s>>>(out->order, n, ways, inter);
+    ++*launches;
+    HANF_RELABEL_TRY(cudaFreeAsync(out->order, s));
+    out->order = inter;
+  }
   phase("sort");
   HANF_RELABEL_TRY(pool_alloc(&out->perm, n, s));
   HANF_RELABEL_TRY(pool_alloc(&ndeg, n + 1, s));

@@ -50,6 +50,7 @@ class EngineConfig:
     exact_sum: bool = True          # N(t) total in the reference's summation order
     shard_begin: int = 0
     shard_end: int = 0
+    shard_count: int = 0            # peer-push shards: allows relabelled shards
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()
@@ -70,6 +71,7 @@ class EngineConfig:
         c.exact_sum = int(self.exact_sum)
         c.shard_begin = self.shard_begin
         c.shard_end = self.shard_end
+        c.shard_count = self.shard_count
         return c
 
 

@@ -155,8 +155,12 @@ class ShardedNfEngine:
         self.rank, self.world, self.group = rank, world, group
         self.ranges = shard_ranges(self.n, world)
         lo, hi = self.ranges[rank]
-        if local is None:
-            local = LocalCudaShard(graph, cfg, lo, hi, torch.device("cuda", torch.cuda.current_device()))
+        own_local = local is None
+        if own_local:
+            # peer-push shards may relabel (hanf_config.shard_count)
+            local = LocalCudaShard(graph, dataclasses.replace(
+                cfg, shard_count=world if exchange == "peer" else 0), lo, hi,
+                torch.device("cuda", torch.cuda.current_device()))
         self.local = local
         if exchange not in ("collective", "peer"):
             raise ValueError(f"exchange must be 'collective' or 'peer', not {exchange!r}")
@@ -180,7 +184,12 @@ class ShardedNfEngine:
             if errors:
                 if error is None:
                     local.shard_detach()
+                dist.barrier(group=group)  # no rank maps an arena that is freed next
                 self.exchange = "collective"
+                if own_local:  # (a relabelled shard needs the peer-push exchange)
+                    local.close()
+                    self.local = local = LocalCudaShard(
+                        graph, cfg, lo, hi, torch.device("cuda", torch.cuda.current_device()))
         # changed-rows exchange (see the module docstring); packets hold at
         # most n/16 rows
         self.delta = delta and hasattr(local, "pack_rows")

@@ -26,12 +26,13 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-def _run_local(hanf, g, cfg, world, skew):
+def _run_local(hanf, g, cfg, world, skew, relabelled=False):
     import torch
     from paper_1011_5599_b200.sharded import LocalCudaShard, shard_ranges
     dev = torch.device("cuda", 0)
     shards = [LocalCudaShard(g, cfg, lo, hi, dev) for lo, hi in shard_ranges(g.num_nodes(), world)]
     engines = [sh.engine for sh in shards]
+    assert all(bool(e.device_buffers().relabelled) == relabelled for e in engines)
     for k, e in enumerate(engines):
         e.shard_attach_local(engines, k)
     values, mods = [shards[0].sum_estimates()], [g.num_nodes()]
@@ -96,6 +97,51 @@ def test_peer_push_local(hanf, monkeypatch, b, env, world, skew):
         assert np.array_equal(c, ref)
 
 
+@pytest.mark.parametrize("b,world,skew,scatter", [(6, 2, False, "1"), (6, 4, True, "1"),
+                                                  (6, 4, True, "0"), (5, 2, True, "1"),
+                                                  (7, 4, False, "0")])
+def test_peer_push_relabelled_shards(hanf, monkeypatch, b, world, skew, scatter):
+    """Relabelled shards (hanf_config.shard_count, degree order interleaved
+    across the shards): rows live in another numbering on the device,
+    estimates are pushed to the peers and every commit re-sums all
+    original-id blocks.  N(t) and the counters equal one engine bit for bit."""
+    import dataclasses
+    monkeypatch.setenv("HANF_RELABEL", "1")
+    monkeypatch.setenv("HANF_EST_SCATTER", scatter)  # estimates in original ids / in rows
+    g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
+    cfg = hanf.EngineConfig(bucket_bits=b, seed=42)
+    values, mods, counters = _run_local(hanf, g, dataclasses.replace(cfg, shard_count=world),
+                                        world, skew, relabelled=True)
+    monkeypatch.setenv("HANF_RELABEL", "0")
+    with hanf.NfEngine(g, cfg) as e:
+        single = e.run_to_stabilisation()
+        ref = e.counters()
+    assert values == single.values and mods == single.modified
+    for c in counters:
+        assert np.array_equal(c, ref)
+
+
+def test_relabelled_shard_needs_peer_push(hanf, monkeypatch):
+    import dataclasses
+    import torch
+    from paper_1011_5599_b200.sharded import LocalCudaShard, shard_ranges
+    monkeypatch.setenv("HANF_RELABEL", "1")
+    g = hanf.gen_rmat(12, 8, 0.57, 0.19, 0.19, 1, 7)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=1, shard_count=2)
+    lo, hi = shard_ranges(g.num_nodes(), 2)[0]
+    sh = LocalCudaShard(g, cfg, lo, hi, torch.device("cuda", 0))
+    try:
+        assert sh.engine.device_buffers().relabelled
+        with pytest.raises(ValueError):
+            sh.shard_compute()
+    finally:
+        sh.close()
+    # unequal or unknown shards never relabel
+    sh = LocalCudaShard(g, dataclasses.replace(cfg, shard_count=0), lo, hi, torch.device("cuda", 0))
+    assert not sh.engine.device_buffers().relabelled
+    sh.close()
+
+
 def test_peer_attach_rejects_bad_peer_sets(hanf):
     import torch
     from paper_1011_5599_b200.sharded import LocalCudaShard, shard_ranges
@@ -126,7 +172,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _ipc_worker(rank, world, port, out):
+def _ipc_worker(rank, world, port, out, relabel=False):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -136,9 +182,13 @@ def _ipc_worker(rank, world, port, out):
     import paper_1011_5599_b200 as hanf
     from paper_1011_5599_b200.sharded import ShardedNfEngine
     torch.cuda.set_device(0)
+    if relabel:
+        os.environ["HANF_RELABEL"] = "1"
     g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
     cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
     eng = ShardedNfEngine(g, cfg, rank, world, exchange="peer")
+    assert eng.exchange == "peer", eng.fallback
+    assert bool(eng.local.engine.device_buffers().relabelled) == relabel
     est = eng.run_to_stabilisation()
     out[rank] = (est.values, est.modified, eng.local.engine.counters())
     eng.close()
@@ -146,9 +196,11 @@ def _ipc_worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_peer_push_ipc_two_processes(hanf):
+@pytest.mark.parametrize("relabel", [False, True])
+def test_peer_push_ipc_two_processes(hanf, relabel):
     """Two ranks in two processes on one GPU, arenas mapped through CUDA IPC
-    handles, ShardedNfEngine(exchange="peer"): equal to one engine."""
+    handles, ShardedNfEngine(exchange="peer"), plain and relabelled shards:
+    equal to one engine."""
     import torch.multiprocessing as mp
     g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
     cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
@@ -157,7 +209,7 @@ def test_peer_push_ipc_two_processes(hanf):
         ref = e.counters()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_ipc_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+    mp.start_processes(_ipc_worker, args=(2, _free_port(), out, relabel), nprocs=2, join=True,
                        start_method="spawn")
     for r in range(2):
         values, mods, counters = out[r]
