@@ -234,11 +234,18 @@ def main():
     import paper_1011_5599_b200 as hanf
     from paper_1011_5599_b200.sharded import ShardedNfEngine
 
+    # BENCH_DIST_BACKEND=gloo runs the N>1 path with several ranks per GPU
+    # (a functional check on a one-GPU box; NCCL needs distinct GPUs)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local_rank = local_rank % max(1, torch.cuda.device_count()) if backend != "nccl" else local_rank
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     g = make_graph()
     n, a = g.num_nodes(), g.num_arcs()
@@ -307,15 +314,22 @@ def main():
     engine.set_timing(False)
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64,
+                         device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = a * args.steps / (total_ms / 1e3)
     union_ms = timing["union_ms"] / max(1, timing["steps"])
     peak, peak_src = hbm_peak()
-    B = algorithmic_bytes(n, a, words)
+    if world > 1:
+        # the rank's own sweep: its rows and their arcs (rank 0 reports; the
+        # shards are arc-balanced by the id permutation / interleaving)
+        lo, hi = sharded.ranges[rank]
+        B = algorithmic_bytes(hi - lo, int(g.offsets()[hi]) - int(g.offsets()[lo]), words)
+    else:
+        B = algorithmic_bytes(n, a, words)
     achieved = B / (union_ms / 1e3) / 1e9 if union_ms > 0 else None
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(args.config) if world == 1 else None
 
     e2e = None
     if not args.no_e2e and world > 1:
@@ -334,7 +348,7 @@ def main():
             est = sh.run_to_stabilisation()
             dt = time.perf_counter() - t0
             sh.close()
-            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            t = torch.tensor([dt], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             if r > 0:  # run 0 warms the context and allocator
                 wall += float(t.item())
