@@ -325,7 +325,9 @@ def main():
         # the rank's own sweep: its rows and their arcs (rank 0 reports; the
         # shards are arc-balanced by the id permutation / interleaving)
         lo, hi = sharded.ranges[rank]
-        B = algorithmic_bytes(hi - lo, int(g.offsets()[hi]) - int(g.offsets()[lo]), words)
+        rank_arcs = (a // world if engine.device_buffers().relabelled  # rows interleaved by degree
+                     else int(g.offsets()[hi]) - int(g.offsets()[lo]))
+        B = algorithmic_bytes(hi - lo, rank_arcs, words)
     else:
         B = algorithmic_bytes(n, a, words)
     achieved = B / (union_ms / 1e3) / 1e9 if union_ms > 0 else None
