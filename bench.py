@@ -311,6 +311,25 @@ def main():
         torch.cuda.synchronize(dev)
         do_step()
     timing = engine.timing()
+    # the iterations after the dense ones, reported separately -
+    # one whole run to stabilisation, device time of each step's sweep
+    # (union / skip / worklist kernels) and of its finish, CUDA events
+    run_profile = []
+    if world == 1:
+        engine.reset()
+        prev = n
+        while True:
+            engine.set_timing(True)
+            rep = do_step()
+            t = engine.timing()
+            kind = ("dense" if 2 * prev >= n else
+                    "worklist or skip sweep (changed-successor probes)")
+            run_profile.append({"t": len(run_profile) + 1, "modified": rep.modified, "kind": kind,
+                                "sweep_ms": round(t["union_ms"], 4),
+                                "finish_ms": round(t["reduce_ms"] + t["estimate_ms"], 4)})
+            prev = rep.modified
+            if rep.modified == 0 or len(run_profile) >= 4 * n + 8:
+                break
     engine.set_timing(False)
     if world > 1:
         import torch.distributed as dist
@@ -424,6 +443,7 @@ def main():
                                        "finish": timing["reduce_ms"] / max(1, timing["steps"])}},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "run_profile": run_profile or None,
             "gpu_launches": step_launches,
             "clocks": clocks.summary(),
         }
