@@ -31,10 +31,12 @@ __host__ __device__ __forceinline__ uint32_t log2g_of(uint64_t d) {
   return g;
 }
 
-// keys = ~deg (descending degree), vals = node; degree-0 nodes get the
+// keys = (segment prefix << 32) | ~deg, vals = node: hubs (prefix 0) first
+// in descending degree, then light nodes by segment (prefix seg + 1, see
+// TaskBuild) and descending degree within it; degree-0 nodes get the
 // largest key and sort to the tail.  Counts hubs and degree-0 nodes.
-__global__ void degree_keys_kernel(const CsrView g, uint64_t lo, uint64_t count,
-                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+__global__ void degree_keys_kernel(const CsrView g, uint64_t lo, uint64_t count, uint32_t seg_shift,
+                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                    unsigned long long* __restrict__ counters, int* __restrict__ bad) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   unsigned long long hubs = 0, zeros = 0;
@@ -43,13 +45,15 @@ __global__ void degree_keys_kernel(const CsrView g, uint64_t lo, uint64_t count,
     const uint64_t a = g.begin(lo + i), b = g.end(lo + i);
     if (b < a) {
       *bad = 1;
-      keys[i] = 0xffffffffu;
+      keys[i] = ~0ull;
       vals[i] = static_cast<uint32_t>(lo + i);
       ++zeros;
       continue;
     }
     const uint64_t d = b - a;
-    keys[i] = d == 0 ? 0xffffffffu : ~static_cast<uint32_t>(d < 0xfffffffeull ? d : 0xfffffffeull);
+    const uint64_t dk = ~static_cast<uint32_t>(d < 0xfffffffeull ? d : 0xfffffffeull);
+    const uint64_t seg = seg_shift >= 32 ? 0 : ((lo + i) >> seg_shift);
+    keys[i] = d == 0 ? ~0ull : (d > kHubDegree ? dk : ((seg + 1) << 32) | dk);
     vals[i] = static_cast<uint32_t>(lo + i);
     hubs += d > kHubDegree;
     zeros += d == 0;
@@ -64,20 +68,80 @@ __global__ void degree_keys_kernel(const CsrView g, uint64_t lo, uint64_t count,
   }
 }
 
-// Boundaries of the light classes in the sorted order: first index whose
-// degree is <= 32 << (lg - 1), for lg = 5..1 (class lg = [start_lg, start_{lg-1})).
-__global__ void class_bounds_kernel(const uint32_t* __restrict__ sorted_keys, uint64_t begin,
-                                    uint64_t end, unsigned long long* __restrict__ bounds) {
-  const int lg = threadIdx.x;  // bounds[lg] = first index with log2g(deg) < lg, lg = 1..5
-  if (lg < 1 || lg > 5) return;
-  const uint64_t cap = 32ull << (lg - 1);
-  uint64_t a = begin, b = end;
-  while (a < b) {
-    const uint64_t mid = (a + b) / 2;
-    const uint64_t d = static_cast<uint32_t>(~sorted_keys[mid]);
-    if (d > cap) a = mid + 1; else b = mid;
+// Boundaries in the sorted light range [begin, end), per segment s < S:
+// bounds[6 s] = first index of segment s; bounds[6 s + lg], lg = 1..5 =
+// first index of segment s whose degree is <= 32 << (lg - 1) (class lg =
+// [start_lg, start_{lg-1})).  bounds[6 S] = end.
+__global__ void class_bounds_kernel(const uint64_t* __restrict__ sorted_keys, uint64_t begin,
+                                    uint64_t end, uint32_t segs,
+                                    unsigned long long* __restrict__ bounds) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i > 6ull * segs) return;
+  const uint64_t s = i / 6;
+  const int lg = static_cast<int>(i % 6);
+  auto first_ge = [&](uint64_t a, uint64_t b, uint64_t key) {  // first index with key >= `key`
+    while (a < b) {
+      const uint64_t mid = (a + b) / 2;
+      if (sorted_keys[mid] < key) a = mid + 1; else b = mid;
+    }
+    return a;
+  };
+  if (s == segs) {
+    if (lg == 0) bounds[i] = end;
+    return;
   }
-  bounds[lg] = a;
+  const uint64_t seg_begin = first_ge(begin, end, (s + 1) << 32);
+  if (lg == 0) {
+    bounds[i] = seg_begin;
+    return;
+  }
+  // within the segment keys grow as the degree falls: degree <= cap <=>
+  // key >= prefix | ~cap
+  const uint64_t seg_end = first_ge(seg_begin, end, (s + 2) << 32);
+  const uint64_t cap = 32ull << (lg - 1);
+  bounds[i] = first_ge(seg_begin, seg_end, ((s + 1) << 32) | static_cast<uint32_t>(~cap));
+}
+
+// Segment bounds: [seg_min, seg_max] covers every node of the segment and
+// every successor of those nodes (atomics, warp-reduced when a warp's nodes
+// share a segment).
+__global__ void segment_bounds_kernel(const CsrView g, uint64_t lo, uint64_t hi, uint32_t seg_shift,
+                                      uint32_t* __restrict__ seg_min,
+                                      uint32_t* __restrict__ seg_max) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t first = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  for (uint64_t base = first - (threadIdx.x & 31); base < hi - lo; base += stride) {
+    const uint64_t i = base + (threadIdx.x & 31);
+    uint32_t mn = 0xffffffffu, mx = 0;
+    uint32_t seg = 0xffffffffu;
+    if (i < hi - lo) {
+      const uint32_t v = static_cast<uint32_t>(lo + i);
+      seg = v >> seg_shift;
+      mn = mx = v;
+      const uint64_t a = g.begin(v), b = g.end(v);
+      for (uint64_t k = a; k < b; ++k) {
+        const uint32_t w = g.id(k);
+        mn = w < mn ? w : mn;
+        mx = w > mx ? w : mx;
+      }
+    }
+    const uint32_t seg0 = __shfl_sync(0xffffffffu, seg, 0);
+    if (__all_sync(0xffffffffu, seg == seg0 || seg == 0xffffffffu)) {
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t a = __shfl_down_sync(0xffffffffu, mn, o);
+        const uint32_t b = __shfl_down_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+      }
+      if ((threadIdx.x & 31) == 0 && seg0 != 0xffffffffu) {
+        atomicMin(seg_min + seg0, mn);
+        atomicMax(seg_max + seg0, mx);
+      }
+    } else if (seg != 0xffffffffu) {
+      atomicMin(seg_min + seg, mn);
+      atomicMax(seg_max + seg, mx);
+    }
+  }
 }
 
 // per-hub chunk counts
@@ -116,27 +180,35 @@ __global__ void hub_tasks_kernel(const CsrView g,
   }
 }
 
-// light warp tasks: slots [C, C + W); class table passed by value
-struct LightClasses {
-  uint64_t item_begin[6];   // index into order[] where class lg starts (lg = 0..5)
-  uint64_t item_end[6];
-  uint64_t warp_begin[6];   // task slots of class lg, relative to the first light slot;
-  uint64_t warp_end[6];     // heavier classes first
-  uint64_t total;
+// light warp tasks: slots [C, C + W).  Group k = one (segment, class)
+// pair in task order (segments ascending, heavier classes first); groups
+// are non-empty, warp_begin ascending.
+struct LightGroup {
+  uint64_t item_begin;  // index into order[] (light nodes only)
+  uint64_t item_end;
+  uint64_t warp_begin;  // task slots, relative to the first light slot
+  uint32_t lg;          // lanes per node = 2^lg
+  uint32_t pad;
 };
 
 __global__ void light_tasks_kernel(const CsrView g,
-                                   const uint32_t* __restrict__ order, LightClasses lc,
-                                   uint64_t first_slot, WarpTask* __restrict__ tasks,
-                                   uint64_t* __restrict__ trips) {
+                                   const uint32_t* __restrict__ order,
+                                   const LightGroup* __restrict__ groups, uint32_t num_groups,
+                                   uint64_t total, uint64_t first_slot,
+                                   WarpTask* __restrict__ tasks, uint64_t* __restrict__ trips) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < lc.total;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
        w += stride) {
-    int lg = 5;
-    while (lg > 0 && !(w >= lc.warp_begin[lg] && w < lc.warp_end[lg])) --lg;
+    uint32_t a = 0, b = num_groups - 1;  // last group with warp_begin <= w
+    while (a < b) {
+      const uint32_t mid = (a + b + 1) / 2;
+      if (groups[mid].warp_begin <= w) a = mid; else b = mid - 1;
+    }
+    const LightGroup gr = groups[a];
+    const uint32_t lg = gr.lg;
     const uint32_t per = 32u >> lg;
-    const uint64_t item = lc.item_begin[lg] + (w - lc.warp_begin[lg]) * per;
-    const uint64_t rem = lc.item_end[lg] - item;
+    const uint64_t item = gr.item_begin + (w - gr.warp_begin) * per;
+    const uint64_t rem = gr.item_end - item;
     const uint32_t nodes = static_cast<uint32_t>(rem < per ? rem : per);
     const uint32_t v = order[item];
     const uint64_t d = g.end(v) - g.begin(v);
@@ -213,9 +285,14 @@ cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
   } while (0)
 
 cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
-                               cudaStream_t s, cudaEvent_t succ_ready, TaskBuild* out,
-                               int* bad_input, uint64_t* launches) {
+                               uint32_t seg_shift, cudaStream_t s, cudaEvent_t succ_ready,
+                               TaskBuild* out, int* bad_input, uint64_t* launches) {
   *out = TaskBuild{};
+  if (seg_shift < 32 && hi > lo) {
+    out->seg_shift = seg_shift;
+    out->num_segs = static_cast<uint32_t>(((hi - 1) >> seg_shift) + 1);
+  }
+  const uint32_t segs = out->num_segs;
   *bad_input = 0;
   const uint64_t count = hi - lo;
   const uint32_t threads = 256;
@@ -224,7 +301,8 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
     if (b > 148ull * 32) b = 148ull * 32;
     return static_cast<uint32_t>(b ? b : 1);
   };
-  uint32_t *keys = nullptr, *vals = nullptr, *skeys = nullptr, *svals = nullptr;
+  uint64_t *keys = nullptr, *skeys = nullptr;
+  uint32_t *vals = nullptr, *svals = nullptr;
   unsigned long long* counters = nullptr;
   int* d_bad = nullptr;
   HANF_BUILD_TRY(pool_alloc(&keys, count, s));
@@ -235,16 +313,22 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   HANF_BUILD_TRY(pool_alloc(&d_bad, 1, s));
   HANF_BUILD_TRY(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), s));
   HANF_BUILD_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-  degree_keys_kernel<<<grid(count), threads, 0, s>>>(g, lo, count, keys, vals, counters, d_bad);
+  degree_keys_kernel<<<grid(count), threads, 0, s>>>(g, lo, count, out->seg_shift, keys, vals,
+                                                     counters, d_bad);
   ++*launches;
   HANF_BUILD_TRY(cudaGetLastError());
+  // key bits: 32 degree bits + the segment prefix (0 for hubs, 1..S for
+  // light nodes; degree-0 nodes are all ones, the largest in any width)
+  int prefix_bits = 1;
+  while ((1ull << prefix_bits) <= segs + 1) ++prefix_bits;
+  const int end_bit = 32 + prefix_bits;
   size_t temp_bytes = 0;
   HANF_BUILD_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, skeys, vals, svals,
-                                                 static_cast<int64_t>(count), 0, 32, s));
+                                                 static_cast<int64_t>(count), 0, end_bit, s));
   void* temp = nullptr;
   HANF_BUILD_TRY(cudaMallocAsync(&temp, temp_bytes ? temp_bytes : 1, s));
   HANF_BUILD_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, skeys, vals, svals,
-                                                 static_cast<int64_t>(count), 0, 32, s));
+                                                 static_cast<int64_t>(count), 0, end_bit, s));
   ++*launches;
   HANF_BUILD_TRY(cudaFreeAsync(temp, s));
   unsigned long long h_counts[8] = {};
@@ -254,32 +338,43 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   const uint64_t light = count - zeros - hubs;
   if (hubs > 0xffffffffull || light > 0xffffffffull) return cudaErrorInvalidValue;
 
-  // light class boundaries (sorted order: hubs, then light by desc degree)
-  unsigned long long* d_bounds = counters;  // reuse: bounds[1..5]
-  class_bounds_kernel<<<1, 32, 0, s>>>(skeys, hubs, hubs + light, d_bounds);
+  // segment and class boundaries (sorted order: hubs, then light nodes by
+  // segment, descending degree within each)
+  const uint64_t nb = 6ull * segs + 1;
+  unsigned long long* d_bounds = nullptr;
+  HANF_BUILD_TRY(pool_alloc(&d_bounds, nb, s));
+  class_bounds_kernel<<<static_cast<uint32_t>((nb + 255) / 256), 256, 0, s>>>(
+      skeys, hubs, hubs + light, segs, d_bounds);
   ++*launches;
   HANF_BUILD_TRY(cudaGetLastError());
-  unsigned long long b[8] = {};
-  HANF_BUILD_TRY(cudaMemcpyAsync(b, d_bounds, sizeof(b), cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> bnd(nb);
+  HANF_BUILD_TRY(cudaMemcpyAsync(bnd.data(), d_bounds, sizeof(unsigned long long) * nb,
+                                 cudaMemcpyDeviceToHost, s));
   HANF_BUILD_TRY(cudaStreamSynchronize(s));
-  // class lg (lanes 2^lg) = sorted positions [b[lg+1], b[lg]) with b[6] = hubs, b[0] = end
-  uint64_t start[7];
-  start[6] = hubs;
-  for (int lg = 5; lg >= 1; --lg) start[lg] = b[lg];
-  start[0] = hubs + light;
-  LightClasses lc{};
+  HANF_BUILD_TRY(cudaFreeAsync(d_bounds, s));
+  std::vector<LightGroup> groups;
   uint64_t warps = 0;
-  for (int lg = 5; lg >= 0; --lg) {
-    // class lg covers degrees (32 << (lg-1), 32 << lg]: positions [start[lg+1], start[lg])
-    const uint64_t a = start[lg + 1], e = start[lg];
-    lc.item_begin[lg] = a - hubs;  // index into order (light nodes only)
-    lc.item_end[lg] = e - hubs;
-    lc.warp_begin[lg] = warps;
-    const uint64_t per = 32u >> lg;
-    warps += (e - a + per - 1) / per;
-    lc.warp_end[lg] = warps;
+  for (uint32_t sg = 0; sg < segs; ++sg) {
+    // class lg (lanes 2^lg) = sorted positions [start[lg+1], start[lg]) with
+    // start[6] = the segment's first index, start[0] = the next segment's
+    uint64_t start[7];
+    start[6] = bnd[6ull * sg];
+    for (int lg = 5; lg >= 1; --lg) start[lg] = bnd[6ull * sg + lg];
+    start[0] = bnd[6ull * (sg + 1)];
+    for (int lg = 5; lg >= 0; --lg) {
+      // class lg covers degrees (32 << (lg-1), 32 << lg]
+      const uint64_t a = start[lg + 1], e = start[lg];
+      if (e <= a) continue;
+      const uint64_t per = 32u >> lg;
+      groups.push_back(LightGroup{a - hubs, e - hubs, warps, static_cast<uint32_t>(lg), 0});
+      warps += (e - a + per - 1) / per;
+    }
   }
-  lc.total = warps;
+  LightGroup* d_groups = nullptr;
+  HANF_BUILD_TRY(pool_alloc(&d_groups, groups.size(), s));
+  if (!groups.empty())
+    HANF_BUILD_TRY(cudaMemcpyAsync(d_groups, groups.data(), sizeof(LightGroup) * groups.size(),
+                                   cudaMemcpyHostToDevice, s));
 
   // hub tables
   TaskBuild& o = *out;
@@ -338,8 +433,9 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
     HANF_BUILD_TRY(cudaGetLastError());
   }
   if (warps) {
-    light_tasks_kernel<<<grid(warps), threads, 0, s>>>(g, o.order, lc, chunks, o.wtasks,
-                                                       trips);
+    light_tasks_kernel<<<grid(warps), threads, 0, s>>>(g, o.order, d_groups,
+                                                       static_cast<uint32_t>(groups.size()), warps,
+                                                       chunks, o.wtasks, trips);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
   }
@@ -373,6 +469,16 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
   }
+  if (o.seg_shift < 32) {
+    HANF_BUILD_TRY(pool_alloc(&o.seg_min, segs, s));
+    HANF_BUILD_TRY(pool_alloc(&o.seg_max, segs, s));
+    HANF_BUILD_TRY(cudaMemsetAsync(o.seg_min, 0xff, sizeof(uint32_t) * segs, s));
+    HANF_BUILD_TRY(cudaMemsetAsync(o.seg_max, 0, sizeof(uint32_t) * segs, s));
+    segment_bounds_kernel<<<grid(count), threads, 0, s>>>(g, lo, hi, o.seg_shift, o.seg_min,
+                                                          o.seg_max);
+    ++*launches;
+    HANF_BUILD_TRY(cudaGetLastError());
+  }
   int h_bad = 0;
   HANF_BUILD_TRY(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   HANF_BUILD_TRY(cudaFreeAsync(keys, s));
@@ -384,6 +490,7 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   HANF_BUILD_TRY(cudaFreeAsync(chunk_begin, s));
   HANF_BUILD_TRY(cudaFreeAsync(trips, s));
   HANF_BUILD_TRY(cudaFreeAsync(scan, s));
+  HANF_BUILD_TRY(cudaFreeAsync(d_groups, s));
   HANF_BUILD_TRY(cudaStreamSynchronize(s));
   *bad_input = h_bad;
   return cudaSuccess;
@@ -391,7 +498,8 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
 
 void free_tasks_device(TaskBuild* t, cudaStream_t s) {
   void* ptrs[] = {t->order, t->wtasks, t->tos, t->chunk_node, t->chunk_hub,
-                  t->hub_nodes, t->hub_first, t->hub_count, t->hub_ticket};
+                  t->hub_nodes, t->hub_first, t->hub_count, t->hub_ticket,
+                  t->seg_min, t->seg_max};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   *t = TaskBuild{};

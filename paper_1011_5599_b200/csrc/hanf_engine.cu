@@ -232,6 +232,7 @@ struct hanf_engine {
   unsigned int* lens = nullptr;
   bool sparse_ok = false;     // worklist step allowed (layout, graph size, HANF_SPARSE)
   uint32_t sparse_after = 8;  // eligible steps before the transpose is built
+  bool force_sparse = false;  // HANF_SPARSE=1 (tests)
   uint32_t sparse_wanted_steps = 0;
   hanf::ReduceOut* reduce = nullptr;
   double* reduce_sums = nullptr;
@@ -302,6 +303,7 @@ struct hanf_engine {
   bool step_pending = false;   // hanf_step_launch done, hanf_step_complete not yet
   uint64_t summ_bits = 0;
   bool use_graphs = true;
+  uint32_t* seg_live = nullptr;  // skip sweeps over segmented tasks (TaskBuild::seg_shift)
   // Sharded engines keep cnt[2], mod[2] and two block-sum inboxes in one
   // IPC-exportable arena (cudaMalloc, not the pool), laid out identically
   // on every rank; attached peers' arenas receive this shard's rows, bitmap
@@ -394,6 +396,7 @@ struct hanf_engine {
       pfree(dirty[0], stream);
       pfree(dirty[1], stream);
       pfree(lens, stream);
+      pfree(seg_live, stream);
       hanf::free_tasks_device(&tasks, stream);
       if (cudaStreamSynchronize(stream) == cudaSuccess)
         streams().put(device, stream);
@@ -610,8 +613,12 @@ hanf_status validate_config(const hanf_config* cfg) {
 // unmodified successors, 2 worklist step (engine.hpp:210-224).  All three
 // produce the same bits; only the time differs.
 bool sparse_wanted(const hanf_engine* e) {
+  // segmented engines' skip sweeps visit only the segments in reach of a
+  // changed counter: they beat the worklist down to ~n/4096 changed
+  // (config 3: 0.43 against 0.65 ms per step between n/4096 and n/128)
+  const uint64_t ratio = e->seg_live && !e->force_sparse ? 4096 : 128;
   return e->cfg.track_modified && e->t != 0 && e->sparse_ok && !e->tma && e->stale_valid &&
-         128 * e->last_count < e->n;
+         ratio * e->last_count < e->n;
 }
 int step_mode(const hanf_engine* e) {
   if (!e->cfg.track_modified || e->t == 0) return 0;
@@ -804,6 +811,12 @@ hanf_status compute_shard(hanf_engine* e) {
   // a counter gather per skipped arc: worth it once most counters settled
   const int mode = step_mode(e);
   a.check_mod = mode != 0 ? 1 : 0;
+  if (mode != 0 && e->seg_live) {
+    HANF_CUDA(hanf::launch_segment_live(e->mod[g], e->tasks.seg_min, e->tasks.seg_max,
+                                        e->tasks.num_segs, e->seg_live, e->stream, &e->launches));
+    a.seg_live = e->seg_live;
+    a.seg_shift = e->tasks.seg_shift;
+  }
   if (mode == 3) {
     HANF_CUDA(hanf::launch_summary(e->mod[g], e->blocks + 1, e->summ_shift, e->summ_bits, e->summ,
                                    e->stream, &e->launches));
@@ -1032,6 +1045,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       e->sparse_ok = hanf::sparse_supported(params.register_bits, params.registers) &&
                      hanf::fused_estimates(params.register_bits, params.registers);
       e->sparse_after = 1;
+      e->force_sparse = true;
     }
   }
 
@@ -1284,8 +1298,28 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     int bad = 0;
     // relabelled: row v's successors are the caller's arcs of order[v], through perm
     const hanf::CsrView view{d_off, up_lo, d_succ, a0, e->order, e->perm, n};
-    const cudaError_t be =
-        hanf::build_tasks_device(view, lo, hi, n, s, ev_arcs, &e->tasks, &bad, &e->launches);
+    // Segments (HANF_SEGMENTS=0/1 forces): graphs whose ids carry locality
+    // (the copying model's windows) group their tasks by node segment of
+    // n/256 nodes, so late skip sweeps visit only the segments near the
+    // changed counters; ids without locality would gain nothing
+    uint32_t seg_shift = 32;
+    {
+      const char* sg = std::getenv("HANF_SEGMENTS");
+      const bool want = sg && (sg[0] == '0' || sg[0] == '1')
+                            ? sg[0] == '1'
+                            : K == 1 && !e->relabel && n >= (1ull << 20) && ids_local(g);
+      if (want && K == 1 && !e->relabel && n > 1) {
+        uint32_t bits = 0;
+        while ((1ull << bits) < n) ++bits;
+        // 4096 segments (config 3: 2^12 nodes each; the +-2^12 windows make
+        // finer ones no better): profiles/r01_segments.md
+        seg_shift = bits > 18 ? bits - 12 : 6;
+        if (const char* sh = std::getenv("HANF_SEG_SHIFT")) seg_shift = std::atoi(sh);
+        if (seg_shift < 6) seg_shift = 6;
+      }
+    }
+    const cudaError_t be = hanf::build_tasks_device(view, lo, hi, n, seg_shift, s, ev_arcs,
+                                                    &e->tasks, &bad, &e->launches);
     // (also on the build's error paths) frees on `s` come after the upload
     HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
     e->csr_off = d_off;
@@ -1302,6 +1336,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       pfree(e->csr_off, s);
       pfree(e->csr_succ, s);
     }
+    if (e->tasks.seg_shift < 32) HANF_TRY(palloc(&e->seg_live, e->tasks.num_segs, s));
     phase("build");
     HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
   }

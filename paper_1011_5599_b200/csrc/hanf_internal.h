@@ -39,6 +39,16 @@ struct TaskBuild {
   uint32_t* hub_count = nullptr;
   uint32_t* hub_ticket = nullptr;
   uint32_t num_hubs = 0;
+  // Segments (graphs whose ids carry locality): light tasks are grouped by
+  // node segment v >> seg_shift (degree order within a segment), and
+  // [seg_min[s], seg_max[s]] bounds the successors and nodes of segment s,
+  // so a skip sweep drops every task of a segment with no modified row in
+  // that range (hanf_kernels.cu segment_live_kernel).  seg_shift = 32: one
+  // segment, no bounds.
+  uint32_t seg_shift = 32;
+  uint32_t num_segs = 1;
+  uint32_t* seg_min = nullptr;
+  uint32_t* seg_max = nullptr;
 };
 // The CSR as the task build reads it: node (row) v's successors are arcs
 // [begin(v), end(v)) of `succ` (from index succ_base), each mapped through
@@ -68,8 +78,8 @@ struct CsrView {
 // the final TOS fill reads the arcs: it waits for `succ_ready` (when
 // non-null), so the arcs upload overlaps the degree sort and task layout.
 cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
-                               cudaStream_t s, cudaEvent_t succ_ready, TaskBuild* out,
-                               int* bad_input, uint64_t* launches);
+                               uint32_t seg_shift, cudaStream_t s, cudaEvent_t succ_ready,
+                               TaskBuild* out, int* bad_input, uint64_t* launches);
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
 // Locality relabelling (hanf_relabel.cu): rows renumbered by descending
@@ -187,6 +197,8 @@ struct UnionArgs {
   const uint32_t* task_list;       // non-null: run only these task indices
   const unsigned int* task_count;  // (device) length of task_list
   PeerRows peers;                  // sharded peer-push: also store written rows there
+  const uint32_t* seg_live;        // skip sweeps over segmented tasks: segment s has work
+  uint32_t seg_shift;              // (TaskBuild::seg_shift)
 };
 
 struct EstimateArgs {
@@ -260,6 +272,11 @@ struct FinishArgs {
   int32_t all_dirty = 0;           // recompute every block of [b0, b1) (bits: count only)
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
+// live[s] = some row of [seg_min[s], seg_max[s]] is set in mod_cur (a
+// segment without one has no node that can change or is stale)
+cudaError_t launch_segment_live(const uint64_t* mod_cur, const uint32_t* seg_min,
+                                const uint32_t* seg_max, uint32_t segs, uint32_t* live,
+                                cudaStream_t s, uint64_t* launches);
 // Peer-push exchange: bitmap words and block sums [w0, w1) of this shard
 // into every peer's arena (and the block sums into the local inbox).
 struct PublishArgs {

@@ -371,6 +371,14 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
   using G_t = Gather<Lay, GMODE, kVec16>;
   const WarpTask task = args.wtasks[task_index];
   const bool hub = task.nodes == 0;
+  if constexpr (SKIP) {
+    // segmented tasks: a segment with no modified row among its nodes and
+    // their successors has nothing to gather and nothing stale to rewrite
+    if (args.seg_live) {
+      const uint32_t v0 = hub ? args.hub_node[task.item] : args.order[task.item];
+      if (!args.seg_live[v0 >> args.seg_shift]) return;
+    }
+  }
   const uint32_t lg = hub ? 5u : task.lg;
   const uint32_t G = 1u << lg;
   const uint32_t sub = lane & (G - 1);
@@ -959,6 +967,38 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
     a.out->count = count;
     a.out->ticket = 0;
   }
+}
+
+// One warp per segment: does mod_cur have a bit in [seg_min, seg_max]?
+__global__ void segment_live_kernel(const uint64_t* __restrict__ mod_cur,
+                                    const uint32_t* __restrict__ seg_min,
+                                    const uint32_t* __restrict__ seg_max, uint32_t segs,
+                                    uint32_t* __restrict__ live) {
+  const uint32_t sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (sg >= segs) return;
+  const uint32_t lo = seg_min[sg], hi = seg_max[sg];
+  bool any = false;
+  if (lo <= hi) {
+    const uint32_t w0 = lo >> 6, w1 = hi >> 6;
+    for (uint32_t w = w0 + lane; w <= w1; w += 32) {
+      uint64_t m = mod_cur[w];
+      if (w == w0) m &= ~0ull << (lo & 63);
+      if (w == w1) m &= ~0ull >> (63 - (hi & 63));
+      any |= m != 0;
+      if (__any_sync(__activemask(), any)) break;
+    }
+  }
+  any = __any_sync(0xffffffffu, any);
+  if (lane == 0) live[sg] = any ? 1u : 0u;
+}
+
+cudaError_t launch_segment_live(const uint64_t* mod_cur, const uint32_t* seg_min,
+                                const uint32_t* seg_max, uint32_t segs, uint32_t* live,
+                                cudaStream_t s, uint64_t* launches) {
+  segment_live_kernel<<<(segs + 7) / 8, 256, 0, s>>>(mod_cur, seg_min, seg_max, segs, live);
+  ++*launches;
+  return cudaGetLastError();
 }
 
 // Peer-push exchange, end of a sharded compute: the shard's bitmap words

@@ -390,7 +390,9 @@ def test_worklist_step_parity(hanf, port, monkeypatch):
                                  {"HANF_TMA": "1"}, {"HANF_TMA": "1", "HANF_GATHER": "40"},
                                  {"HANF_RELABEL": "1"}, {"HANF_RELABEL": "1", "HANF_SPARSE": "1"},
                                  {"HANF_RELABEL": "1", "HANF_PITCH": "0"},
-                                 {"HANF_SUMMARY": "1"}, {"HANF_SUMMARY": "1", "HANF_RELABEL": "1"}])
+                                 {"HANF_SUMMARY": "1"}, {"HANF_SUMMARY": "1", "HANF_RELABEL": "1"},
+                                 {"HANF_SEGMENTS": "1"}, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"},
+                                 {"HANF_SEGMENTS": "1", "HANF_SPARSE": "1"}])
 def test_row_pitch_and_gather_variants(hanf, port, monkeypatch, env):
     """Padded rows (aligned 256-bit gathers), unpadded rows and the
     alternative gather kernels change time only: counters read back in the
@@ -423,6 +425,27 @@ def test_golden_trace_relabelled(hanf, traces, idx, monkeypatch):
     on graphs the default heuristic leaves alone)."""
     monkeypatch.setenv("HANF_RELABEL", "1")
     test_golden_trace(hanf, traces, idx)
+
+
+@pytest.mark.parametrize("idx", range(28))
+def test_golden_trace_segmented(hanf, traces, idx, monkeypatch):
+    """Segmented tasks (light tasks grouped by node segment; skip sweeps drop
+    the segments with no modified row in reach) change time only: every
+    golden iteration bit-exact (HANF_SEGMENTS=1 forces them on)."""
+    monkeypatch.setenv("HANF_SEGMENTS", "1")
+    test_golden_trace(hanf, traces, idx)
+
+
+@pytest.mark.parametrize("env", [{}, {"HANF_SPARSE": "0"}, {"HANF_SUMMARY": "1"}])
+def test_segmented_copying_graph(hanf, port, monkeypatch, env):
+    """A config-3-shaped copying graph (local ids: segmented by default from
+    2^20 nodes, forced here at 2^15) run to stabilisation in lockstep with
+    the oracle: the long tail of skip sweeps visits a few segments only."""
+    monkeypatch.setenv("HANF_SEGMENTS", "1")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = hanf.gen_copying(1 << 15, 2.1, 8.0, 300, 0.6, 64, 3)
+    lockstep(hanf, port, g, bucket_bits=5, seed=42)
 
 
 def test_relabel_multichunk_and_readback(hanf, port, monkeypatch):
