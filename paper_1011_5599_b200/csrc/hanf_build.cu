@@ -18,6 +18,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <cstdint>
+#include <cstring>
 #include <vector>
 
 #include "hanf_internal.h"
@@ -31,11 +32,19 @@ __host__ __device__ __forceinline__ uint32_t log2g_of(uint64_t d) {
   return g;
 }
 
-// keys = (segment prefix << 32) | ~deg, vals = node: hubs (prefix 0) first
-// in descending degree, then light nodes by segment (prefix seg + 1, see
-// TaskBuild) and descending degree within it; degree-0 nodes get the
-// largest key and sort to the tail.  Counts hubs and degree-0 nodes.
+// keys = (group prefix << 32) | ~deg, vals = node: hubs (prefix 0) first
+// in descending degree, then light nodes by group - one (segment, class)
+// pair, prefix 1 + group_index(), see TaskBuild - and descending degree
+// within it; degree-0 nodes get the largest key and sort to the tail.
+// Counts hubs and degree-0 nodes.
+__host__ __device__ __forceinline__ uint64_t group_index(uint32_t seg, uint32_t lg, uint32_t segs,
+                                                         bool class_major) {
+  return class_major ? static_cast<uint64_t>(5 - lg) * segs + seg
+                     : static_cast<uint64_t>(seg) * 6 + (5 - lg);
+}
+
 __global__ void degree_keys_kernel(const CsrView g, uint64_t lo, uint64_t count, uint32_t seg_shift,
+                                   uint32_t segs, bool class_major,
                                    uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                    unsigned long long* __restrict__ counters, int* __restrict__ bad) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -52,8 +61,9 @@ __global__ void degree_keys_kernel(const CsrView g, uint64_t lo, uint64_t count,
     }
     const uint64_t d = b - a;
     const uint64_t dk = ~static_cast<uint32_t>(d < 0xfffffffeull ? d : 0xfffffffeull);
-    const uint64_t seg = seg_shift >= 32 ? 0 : ((lo + i) >> seg_shift);
-    keys[i] = d == 0 ? ~0ull : (d > kHubDegree ? dk : ((seg + 1) << 32) | dk);
+    const uint32_t seg = seg_shift >= 32 ? 0u : static_cast<uint32_t>((lo + i) >> seg_shift);
+    const uint64_t grp = 1 + group_index(seg, log2g_of(d), segs, class_major);
+    keys[i] = d == 0 ? ~0ull : (d > kHubDegree ? dk : (grp << 32) | dk);
     vals[i] = static_cast<uint32_t>(lo + i);
     hubs += d > kHubDegree;
     zeros += d == 0;
@@ -68,38 +78,74 @@ __global__ void degree_keys_kernel(const CsrView g, uint64_t lo, uint64_t count,
   }
 }
 
-// Boundaries in the sorted light range [begin, end), per segment s < S:
-// bounds[6 s] = first index of segment s; bounds[6 s + lg], lg = 1..5 =
-// first index of segment s whose degree is <= 32 << (lg - 1) (class lg =
-// [start_lg, start_{lg-1})).  bounds[6 S] = end.
-__global__ void class_bounds_kernel(const uint64_t* __restrict__ sorted_keys, uint64_t begin,
-                                    uint64_t end, uint32_t segs,
+// Group boundaries in the sorted light range [begin, end): bounds[i] =
+// first index whose key prefix is > i (group i = [bounds[i-1], bounds[i])
+// with bounds[-1] = begin), i < groups.
+__global__ void group_bounds_kernel(const uint64_t* __restrict__ sorted_keys, uint64_t begin,
+                                    uint64_t end, uint64_t groups,
                                     unsigned long long* __restrict__ bounds) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (i > 6ull * segs) return;
-  const uint64_t s = i / 6;
-  const int lg = static_cast<int>(i % 6);
-  auto first_ge = [&](uint64_t a, uint64_t b, uint64_t key) {  // first index with key >= `key`
-    while (a < b) {
-      const uint64_t mid = (a + b) / 2;
-      if (sorted_keys[mid] < key) a = mid + 1; else b = mid;
+  if (i >= groups) return;
+  const uint64_t key = (i + 2) << 32;  // first key of group i + 1
+  uint64_t a = begin, b = end;
+  while (a < b) {
+    const uint64_t mid = (a + b) / 2;
+    if (sorted_keys[mid] < key) a = mid + 1; else b = mid;
+  }
+  bounds[i] = a;
+}
+
+// light warp tasks: slots [C, C + W).  Group k = one (segment, class)
+// pair in task order (segments ascending, heavier classes first); groups
+// are non-empty, warp_begin ascending.
+struct LightGroup {
+  uint64_t item_begin;  // index into order[] (light nodes only)
+  uint64_t item_end;
+  uint64_t warp_begin;  // task slots, relative to the first light slot
+  uint32_t lg;          // lanes per node = 2^lg
+  uint32_t pad;
+};
+
+// Group table from the boundaries (one CTA): group i = sorted positions
+// [bounds[i-1], bounds[i]) (bounds[-1] = hubs), its class, and its first
+// light warp = exclusive scan of the groups' warp counts; wbeg[ng] = total.
+// Empty groups get warp_begin = the next group's (light_tasks_kernel's
+// binary search then skips them).
+__global__ void __launch_bounds__(1024)
+groups_kernel(const unsigned long long* __restrict__ bounds, uint64_t ng, uint64_t hubs,
+              uint32_t segs, bool class_major, LightGroup* __restrict__ groups,
+              unsigned long long* __restrict__ wbeg) {
+  __shared__ unsigned long long part[1024];
+  unsigned long long carry = 0;
+  for (uint64_t base = 0; base < ng; base += 1024) {
+    const uint64_t i = base + threadIdx.x;
+    unsigned long long w = 0;
+    uint32_t lg = 0;
+    uint64_t a = 0, e = 0;
+    if (i < ng) {
+      a = i ? bounds[i - 1] : hubs;
+      e = bounds[i];
+      lg = class_major ? 5 - static_cast<uint32_t>(i / segs) : 5 - static_cast<uint32_t>(i % 6);
+      const uint64_t per = 32u >> lg;
+      w = e > a ? (e - a + per - 1) / per : 0;
     }
-    return a;
-  };
-  if (s == segs) {
-    if (lg == 0) bounds[i] = end;
-    return;
+    part[threadIdx.x] = w;
+    __syncthreads();
+    for (uint32_t o = 1; o < 1024; o <<= 1) {  // inclusive scan (Hillis-Steele)
+      const unsigned long long x = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+      __syncthreads();
+      part[threadIdx.x] += x;
+      __syncthreads();
+    }
+    const unsigned long long incl = carry + part[threadIdx.x];
+    if (i < ng) {
+      groups[i] = LightGroup{a - hubs, (e > a ? e : a) - hubs, incl - w, lg, 0};
+      wbeg[i] = incl - w;
+    }
+    carry += part[1023];
+    __syncthreads();
   }
-  const uint64_t seg_begin = first_ge(begin, end, (s + 1) << 32);
-  if (lg == 0) {
-    bounds[i] = seg_begin;
-    return;
-  }
-  // within the segment keys grow as the degree falls: degree <= cap <=>
-  // key >= prefix | ~cap
-  const uint64_t seg_end = first_ge(seg_begin, end, (s + 2) << 32);
-  const uint64_t cap = 32ull << (lg - 1);
-  bounds[i] = first_ge(seg_begin, seg_end, ((s + 1) << 32) | static_cast<uint32_t>(~cap));
+  if (threadIdx.x == 0) wbeg[ng] = carry;
 }
 
 // Segment bounds: [seg_min, seg_max] covers every node of the segment and
@@ -180,17 +226,6 @@ __global__ void hub_tasks_kernel(const CsrView g,
   }
 }
 
-// light warp tasks: slots [C, C + W).  Group k = one (segment, class)
-// pair in task order (segments ascending, heavier classes first); groups
-// are non-empty, warp_begin ascending.
-struct LightGroup {
-  uint64_t item_begin;  // index into order[] (light nodes only)
-  uint64_t item_end;
-  uint64_t warp_begin;  // task slots, relative to the first light slot
-  uint32_t lg;          // lanes per node = 2^lg
-  uint32_t pad;
-};
-
 __global__ void light_tasks_kernel(const CsrView g,
                                    const uint32_t* __restrict__ order,
                                    const LightGroup* __restrict__ groups, uint32_t num_groups,
@@ -252,7 +287,7 @@ fill_tos_kernel(const CsrView g, const uint32_t* __restrict__ order,
       for (uint32_t k = lane; k < len; k += 32) {
         const uint32_t id = g.id(a + k);
         out_of_range |= id >= n;
-        dst[k] = id;
+        dst[k] = id < n ? id : n;  // (a pipelined sweep may run before the check)
       }
     } else {
       const uint32_t G = 1u << t.lg;
@@ -262,7 +297,7 @@ fill_tos_kernel(const CsrView g, const uint32_t* __restrict__ order,
         for (uint64_t k = lane; k < d; k += 32) {
           const uint32_t id = g.id(s + k);
           out_of_range |= id >= n;
-          dst[32 * (k >> t.lg) + j * G + (k & (G - 1))] = id;
+          dst[32 * (k >> t.lg) + j * G + (k & (G - 1))] = id < n ? id : n;
         }
       }
     }
@@ -276,6 +311,48 @@ cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
   return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), s);
 }
 
+// The build's small device->host reads go through page-locked memory: a
+// pageable read queues behind the arcs upload running on the helper stream
+// (measured: the whole build then waits for the upload), a pinned one uses
+// the other copy engine.  Synchronises `s`.
+cudaError_t read_back(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  thread_local void* buf = nullptr;  // (kept for the thread's lifetime)
+  thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    const size_t want = bytes < 4096 ? 4096 : bytes;
+    const cudaError_t e = cudaHostAlloc(&buf, want, cudaHostAllocDefault);
+    if (e != cudaSuccess) return e;
+    cap = want;
+  }
+  cudaError_t e = cudaMemcpyAsync(buf, src, bytes, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) std::memcpy(dst, buf, bytes);
+  return e;
+}
+
+// Host->device counterpart of read_back (a pageable copy would also wait
+// for the arcs upload).  Synchronises `s`.
+cudaError_t write_to_device(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  thread_local void* buf = nullptr;
+  thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    const size_t want = bytes < 4096 ? 4096 : bytes;
+    const cudaError_t e = cudaHostAlloc(&buf, want, cudaHostAllocDefault);
+    if (e != cudaSuccess) return e;
+    cap = want;
+  }
+  std::memcpy(buf, src, bytes);
+  cudaError_t e = cudaMemcpyAsync(dst, buf, bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return e;
+}
+
 }  // namespace
 
 #define HANF_BUILD_TRY(expr)                    \
@@ -286,7 +363,8 @@ cudaError_t pool_alloc(T** p, size_t count, cudaStream_t s) {
 
 cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
                                uint32_t seg_shift, cudaStream_t s, cudaEvent_t succ_ready,
-                               TaskBuild* out, int* bad_input, uint64_t* launches) {
+                               TaskBuild* out, int* bad_input, uint64_t* launches,
+                               bool defer_fill, bool seg_bounds, bool class_major) {
   *out = TaskBuild{};
   if (seg_shift < 32 && hi > lo) {
     out->seg_shift = seg_shift;
@@ -313,14 +391,14 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   HANF_BUILD_TRY(pool_alloc(&d_bad, 1, s));
   HANF_BUILD_TRY(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), s));
   HANF_BUILD_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-  degree_keys_kernel<<<grid(count), threads, 0, s>>>(g, lo, count, out->seg_shift, keys, vals,
-                                                     counters, d_bad);
+  degree_keys_kernel<<<grid(count), threads, 0, s>>>(g, lo, count, out->seg_shift, segs,
+                                                     class_major, keys, vals, counters, d_bad);
   ++*launches;
   HANF_BUILD_TRY(cudaGetLastError());
   // key bits: 32 degree bits + the segment prefix (0 for hubs, 1..S for
   // light nodes; degree-0 nodes are all ones, the largest in any width)
   int prefix_bits = 1;
-  while ((1ull << prefix_bits) <= segs + 1) ++prefix_bits;
+  while ((1ull << prefix_bits) <= 6ull * segs + 1) ++prefix_bits;
   const int end_bit = 32 + prefix_bits;
   size_t temp_bytes = 0;
   HANF_BUILD_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, skeys, vals, svals,
@@ -332,52 +410,45 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   ++*launches;
   HANF_BUILD_TRY(cudaFreeAsync(temp, s));
   unsigned long long h_counts[8] = {};
-  HANF_BUILD_TRY(cudaMemcpyAsync(h_counts, counters, sizeof(h_counts), cudaMemcpyDeviceToHost, s));
-  HANF_BUILD_TRY(cudaStreamSynchronize(s));
+  HANF_BUILD_TRY(read_back(h_counts, counters, sizeof(h_counts), s));
   const uint64_t hubs = h_counts[0], zeros = h_counts[1];
   const uint64_t light = count - zeros - hubs;
   if (hubs > 0xffffffffull || light > 0xffffffffull) return cudaErrorInvalidValue;
 
-  // segment and class boundaries (sorted order: hubs, then light nodes by
-  // segment, descending degree within each)
-  const uint64_t nb = 6ull * segs + 1;
+  // group boundaries (sorted order: hubs, then light nodes by group,
+  // descending degree within each)
+  const uint64_t ng = 6ull * segs;
   unsigned long long* d_bounds = nullptr;
-  HANF_BUILD_TRY(pool_alloc(&d_bounds, nb, s));
-  class_bounds_kernel<<<static_cast<uint32_t>((nb + 255) / 256), 256, 0, s>>>(
-      skeys, hubs, hubs + light, segs, d_bounds);
+  HANF_BUILD_TRY(pool_alloc(&d_bounds, ng, s));
+  group_bounds_kernel<<<static_cast<uint32_t>((ng + 255) / 256), 256, 0, s>>>(
+      skeys, hubs, hubs + light, ng, d_bounds);
   ++*launches;
   HANF_BUILD_TRY(cudaGetLastError());
-  std::vector<unsigned long long> bnd(nb);
-  HANF_BUILD_TRY(cudaMemcpyAsync(bnd.data(), d_bounds, sizeof(unsigned long long) * nb,
-                                 cudaMemcpyDeviceToHost, s));
-  HANF_BUILD_TRY(cudaStreamSynchronize(s));
-  HANF_BUILD_TRY(cudaFreeAsync(d_bounds, s));
-  std::vector<LightGroup> groups;
-  uint64_t warps = 0;
-  for (uint32_t sg = 0; sg < segs; ++sg) {
-    // class lg (lanes 2^lg) = sorted positions [start[lg+1], start[lg]) with
-    // start[6] = the segment's first index, start[0] = the next segment's
-    uint64_t start[7];
-    start[6] = bnd[6ull * sg];
-    for (int lg = 5; lg >= 1; --lg) start[lg] = bnd[6ull * sg + lg];
-    start[0] = bnd[6ull * (sg + 1)];
-    for (int lg = 5; lg >= 0; --lg) {
-      // class lg covers degrees (32 << (lg-1), 32 << lg]
-      const uint64_t a = start[lg + 1], e = start[lg];
-      if (e <= a) continue;
-      const uint64_t per = 32u >> lg;
-      groups.push_back(LightGroup{a - hubs, e - hubs, warps, static_cast<uint32_t>(lg), 0});
-      warps += (e - a + per - 1) / per;
-    }
-  }
+  // the group table is made on the device (a host->device copy would queue
+  // behind the arcs upload on the copy engine); the host reads back the
+  // warp offsets only
   LightGroup* d_groups = nullptr;
-  HANF_BUILD_TRY(pool_alloc(&d_groups, groups.size(), s));
-  if (!groups.empty())
-    HANF_BUILD_TRY(cudaMemcpyAsync(d_groups, groups.data(), sizeof(LightGroup) * groups.size(),
-                                   cudaMemcpyHostToDevice, s));
+  HANF_BUILD_TRY(pool_alloc(&d_groups, ng, s));
+  unsigned long long* d_wbeg = nullptr;
+  HANF_BUILD_TRY(pool_alloc(&d_wbeg, ng + 1, s));
+  groups_kernel<<<1, 1024, 0, s>>>(d_bounds, ng, hubs, segs, class_major, d_groups, d_wbeg);
+  ++*launches;
+  HANF_BUILD_TRY(cudaGetLastError());
+  std::vector<unsigned long long> wbeg(ng + 1);
+  HANF_BUILD_TRY(read_back(wbeg.data(), d_wbeg, sizeof(unsigned long long) * (ng + 1), s));
+  HANF_BUILD_TRY(cudaFreeAsync(d_bounds, s));
+  HANF_BUILD_TRY(cudaFreeAsync(d_wbeg, s));
+  TaskBuild& o = *out;
+  const uint64_t warps = wbeg[ng];
+  for (uint64_t i = 0; i < ng; ++i) {
+    if (wbeg[i + 1] == wbeg[i]) continue;  // empty group
+    o.group_seg.push_back(class_major ? static_cast<uint32_t>(i % segs)
+                                      : static_cast<uint32_t>(i / 6));
+    o.group_task_begin.push_back(wbeg[i]);
+  }
+  o.group_task_begin.push_back(warps);
 
   // hub tables
-  TaskBuild& o = *out;
   o.num_hubs = static_cast<uint32_t>(hubs);
   HANF_BUILD_TRY(pool_alloc(&o.hub_nodes, hubs, s));
   HANF_BUILD_TRY(pool_alloc(&o.hub_first, hubs, s));
@@ -404,15 +475,15 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
     ++*launches;
     HANF_BUILD_TRY(cudaFreeAsync(t2, s));
     uint32_t last_first = 0, last_count = 0;
-    HANF_BUILD_TRY(cudaMemcpyAsync(&last_first, o.hub_first + hubs - 1, 4, cudaMemcpyDeviceToHost, s));
-    HANF_BUILD_TRY(cudaMemcpyAsync(&last_count, o.hub_count + hubs - 1, 4, cudaMemcpyDeviceToHost, s));
-    HANF_BUILD_TRY(cudaStreamSynchronize(s));
+    HANF_BUILD_TRY(read_back(&last_first, o.hub_first + hubs - 1, 4, s));
+    HANF_BUILD_TRY(read_back(&last_count, o.hub_count + hubs - 1, 4, s));
     chunks = static_cast<uint64_t>(last_first) + last_count;
   }
   const uint64_t num_tasks = chunks + warps;
   if (num_tasks > 0x7fffffffull / 32) return cudaErrorInvalidValue;
   o.num_chunks = static_cast<uint32_t>(chunks);
   o.num_wtasks = static_cast<uint32_t>(num_tasks);
+  for (auto& t : o.group_task_begin) t += chunks;  // absolute task slots
   HANF_BUILD_TRY(pool_alloc(&o.chunk_node, chunks, s));
   HANF_BUILD_TRY(pool_alloc(&o.chunk_hub, chunks, s));
   uint64_t* chunk_begin = nullptr;
@@ -434,7 +505,7 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   }
   if (warps) {
     light_tasks_kernel<<<grid(warps), threads, 0, s>>>(g, o.order, d_groups,
-                                                       static_cast<uint32_t>(groups.size()), warps,
+                                                       static_cast<uint32_t>(ng), warps,
                                                        chunks, o.wtasks, trips);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
@@ -452,8 +523,7 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
     HANF_BUILD_TRY(cudaFreeAsync(t3, s));
   }
   uint64_t rows = 0;
-  HANF_BUILD_TRY(cudaMemcpyAsync(&rows, scan + num_tasks, 8, cudaMemcpyDeviceToHost, s));
-  HANF_BUILD_TRY(cudaStreamSynchronize(s));
+  HANF_BUILD_TRY(read_back(&rows, scan + num_tasks, 8, s));
   if (num_tasks) {
     set_tos_kernel<<<grid(num_tasks), threads, 0, s>>>(o.wtasks, scan, num_tasks);
     ++*launches;
@@ -461,15 +531,21 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   }
   o.tos_words = rows * 32;
   HANF_BUILD_TRY(pool_alloc(&o.tos, o.tos_words, s));
-  if (succ_ready) HANF_BUILD_TRY(cudaStreamWaitEvent(s, succ_ready, 0));
-  if (num_tasks) {
+  if (defer_fill) {
+    o.chunk_begin = chunk_begin;
+    chunk_begin = nullptr;
+    HANF_BUILD_TRY(pool_alloc(&o.fill_bad, 1, s));
+    HANF_BUILD_TRY(cudaMemsetAsync(o.fill_bad, 0, sizeof(int), s));
+  }
+  if (succ_ready && !defer_fill) HANF_BUILD_TRY(cudaStreamWaitEvent(s, succ_ready, 0));
+  if (num_tasks && !defer_fill) {
     fill_tos_kernel<<<grid(num_tasks * 32), threads, 0, s>>>(
         g, o.order, chunk_begin, o.chunk_node, o.wtasks, num_tasks,
         static_cast<uint32_t>(n), o.tos, d_bad);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
   }
-  if (o.seg_shift < 32) {
+  if (o.seg_shift < 32 && seg_bounds && !defer_fill) {
     HANF_BUILD_TRY(pool_alloc(&o.seg_min, segs, s));
     HANF_BUILD_TRY(pool_alloc(&o.seg_max, segs, s));
     HANF_BUILD_TRY(cudaMemsetAsync(o.seg_min, 0xff, sizeof(uint32_t) * segs, s));
@@ -480,14 +556,14 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
     HANF_BUILD_TRY(cudaGetLastError());
   }
   int h_bad = 0;
-  HANF_BUILD_TRY(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HANF_BUILD_TRY(read_back(&h_bad, d_bad, sizeof(int), s));
   HANF_BUILD_TRY(cudaFreeAsync(keys, s));
   HANF_BUILD_TRY(cudaFreeAsync(vals, s));
   HANF_BUILD_TRY(cudaFreeAsync(skeys, s));
   HANF_BUILD_TRY(cudaFreeAsync(svals, s));
   HANF_BUILD_TRY(cudaFreeAsync(counters, s));
   HANF_BUILD_TRY(cudaFreeAsync(d_bad, s));
-  HANF_BUILD_TRY(cudaFreeAsync(chunk_begin, s));
+  if (chunk_begin) HANF_BUILD_TRY(cudaFreeAsync(chunk_begin, s));
   HANF_BUILD_TRY(cudaFreeAsync(trips, s));
   HANF_BUILD_TRY(cudaFreeAsync(scan, s));
   HANF_BUILD_TRY(cudaFreeAsync(d_groups, s));
@@ -496,10 +572,53 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   return cudaSuccess;
 }
 
+cudaError_t fill_tos_range(const CsrView& g, const TaskBuild& t, uint64_t t0, uint64_t t1,
+                           uint64_t n, cudaStream_t s, uint64_t* launches) {
+  if (t1 <= t0) return cudaSuccess;
+  uint64_t blocks = ((t1 - t0) * 32 + 255) / 256;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  // (tasks are self-contained: a sub-array of them fills its own TOS rows)
+  fill_tos_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
+      g, t.order, t.chunk_begin, t.chunk_node, t.wtasks + t0, t1 - t0, static_cast<uint32_t>(n),
+      t.tos, t.fill_bad);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t finish_tasks_device(const CsrView& g, TaskBuild* t, uint64_t lo, uint64_t hi,
+                                bool seg_bounds, cudaStream_t s, int* bad_input,
+                                uint64_t* launches) {
+  if (t->seg_shift < 32 && seg_bounds) {
+    const uint32_t segs = t->num_segs;
+    HANF_BUILD_TRY(pool_alloc(&t->seg_min, segs, s));
+    HANF_BUILD_TRY(pool_alloc(&t->seg_max, segs, s));
+    HANF_BUILD_TRY(cudaMemsetAsync(t->seg_min, 0xff, sizeof(uint32_t) * segs, s));
+    HANF_BUILD_TRY(cudaMemsetAsync(t->seg_max, 0, sizeof(uint32_t) * segs, s));
+    uint64_t blocks = (hi - lo + 255) / 256;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    segment_bounds_kernel<<<static_cast<uint32_t>(blocks ? blocks : 1), 256, 0, s>>>(
+        g, lo, hi, t->seg_shift, t->seg_min, t->seg_max);
+    ++*launches;
+    HANF_BUILD_TRY(cudaGetLastError());
+  }
+  int h_bad = 0;
+  if (t->fill_bad) {
+    HANF_BUILD_TRY(read_back(&h_bad, t->fill_bad, sizeof(int), s));
+    HANF_BUILD_TRY(cudaFreeAsync(t->fill_bad, s));
+    t->fill_bad = nullptr;
+  }
+  if (t->chunk_begin) {
+    HANF_BUILD_TRY(cudaFreeAsync(t->chunk_begin, s));
+    t->chunk_begin = nullptr;
+  }
+  *bad_input = h_bad;
+  return cudaSuccess;
+}
+
 void free_tasks_device(TaskBuild* t, cudaStream_t s) {
   void* ptrs[] = {t->order, t->wtasks, t->tos, t->chunk_node, t->chunk_hub,
                   t->hub_nodes, t->hub_first, t->hub_count, t->hub_ticket,
-                  t->seg_min, t->seg_max};
+                  t->seg_min, t->seg_max, t->chunk_begin, t->fill_bad};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   *t = TaskBuild{};

@@ -304,6 +304,9 @@ struct hanf_engine {
   uint64_t summ_bits = 0;
   bool use_graphs = true;
   uint32_t* seg_live = nullptr;  // skip sweeps over segmented tasks (TaskBuild::seg_shift)
+  // create pipelined iteration 1 with the arcs upload: the next generation,
+  // its bitmap and estimates already hold step 1's sweep (hanf_create)
+  bool pre_step = false;
   // Sharded engines keep cnt[2], mod[2] and two block-sum inboxes in one
   // IPC-exportable arena (cudaMalloc, not the pool), laid out identically
   // on every rank; attached peers' arenas receive this shard's rows, bitmap
@@ -564,6 +567,7 @@ void batch_totals(hanf_engine* e, int parity, uint64_t* counts) {
 }
 
 hanf_status seed_all(hanf_engine* e) {
+  e->pre_step = false;
   e->cur = 0;
   e->t = 0;
   e->stale_valid = false;
@@ -788,6 +792,14 @@ hanf_status compute_local(hanf_engine* e) {
 
 hanf_status compute_shard(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
+  if (e->pre_step) {  // step 1's sweep ran during the upload (create)
+    e->pre_step = false;
+    if (e->timing) {
+      HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
+      HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
+    }
+    return HANF_OK;
+  }
   if (e->shard_relabel && !e->attached)
     return fail(HANF_INVALID_ARGUMENT,
                 "relabelled shard engines exchange through hanf_shard_attach (peer-push)");
@@ -905,7 +917,7 @@ hanf_status step_enqueue(hanf_engine* e) {
     const hanf_status st = ensure_sparse(e);
     if (st != HANF_OK) return st;
   }
-  if (!e->use_graphs || e->timing) {
+  if (!e->use_graphs || e->timing || e->pre_step) {
     const hanf_status st = compute_local(e);
     if (st != HANF_OK) return st;
     return commit_enqueue(e);
@@ -1207,6 +1219,42 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     // (relabelled shards: the whole graph - their rows are spread over it)
     const bool whole = K > 1 || e->shard_relabel;
     const uint64_t up_lo = whole ? 0 : lo, up_hi = whole ? n_real : hi;
+    // Segments (HANF_SEGMENTS=0/1 forces): graphs whose ids carry locality
+    // (the copying model's windows) group their tasks by node segment, so
+    // a warp's nodes are id-neighbours and late skip sweeps visit only the
+    // segments near the changed counters (profiles/r01_segments.md).
+    // Pipelined create (opt-in, HANF_PIPELINE=1; single-GPU engines with
+    // fused estimates): the arcs go up in node-range chunks, each chunk's
+    // TOS rows are filled and step 1's sweep of its light tasks runs as soon
+    // as it lands, the hubs after the last one.  Measured on config 2 it
+    // loses: the node-segmented task order it needs makes every dense step
+    // ~5% slower, and the chunk sweeps' small launches are latency-bound
+    // (profiles/r01_pipeline.md).
+    uint32_t seg_shift = 32;
+    bool seg_skip = false;
+    bool pipeline = false;
+    {
+      uint32_t bits = 0;
+      while ((1ull << bits) < n) ++bits;
+      const char* sg = std::getenv("HANF_SEGMENTS");
+      const bool want = sg && (sg[0] == '0' || sg[0] == '1')
+                            ? sg[0] == '1'
+                            : K == 1 && !e->relabel && n >= (1ull << 20) && ids_local(g);
+      if (want && K == 1 && !e->relabel && n > 1) {
+        // 4096 segments (config 3: 2^12 nodes each; the +-2^12 windows make
+        // finer ones no better)
+        seg_shift = bits > 18 ? bits - 12 : 6;
+        if (const char* sh = std::getenv("HANF_SEG_SHIFT")) seg_shift = std::atoi(sh);
+        if (seg_shift < 6) seg_shift = 6;
+        seg_skip = true;
+      }
+      const char* pp = std::getenv("HANF_PIPELINE");
+      const bool eligible = K == 1 && !e->relabel && lo == 0 && hi == n && n > 64 &&
+                            !e->tma && hanf::fused_estimates(params.register_bits,
+                                                             params.registers);
+      pipeline = eligible && pp && pp[0] == '1';
+      if (pipeline && seg_shift >= 32) seg_shift = bits > 9 ? bits - 3 : 6;  // 8 chunks
+    }
     uint64_t a0 = g->offsets[up_lo], a1 = g->offsets[up_hi];
     uint64_t* d_off = nullptr;
     uint32_t* d_succ = nullptr;
@@ -1222,6 +1270,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       int dev;
       cudaStream_t st;
       cudaEvent_t a, b;
+      std::vector<cudaEvent_t> chunks;
       ~UploadGuard() {
         if (cudaStreamSynchronize(st) == cudaSuccess)
           streams().put(dev, st);
@@ -1229,8 +1278,9 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
           cudaStreamDestroy(st);
         if (a) cudaEventDestroy(a);
         if (b) cudaEventDestroy(b);
+        for (cudaEvent_t c : chunks) cudaEventDestroy(c);
       }
-    } guard{cfg.device, s2, nullptr, nullptr};
+    } guard{cfg.device, s2, nullptr, nullptr, {}};
     HANF_TRY(cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming));
     guard.a = ev_off;
     HANF_TRY(cudaEventCreateWithFlags(&ev_arcs, cudaEventDisableTiming));
@@ -1239,9 +1289,42 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
                              cudaMemcpyHostToDevice, s));
     HANF_TRY(cudaEventRecord(ev_off, s));
     HANF_TRY(cudaStreamWaitEvent(s2, ev_off, 0));
-    if (a1 > a0)
+    // pipelined: chunk c = segments [c S / P, (c + 1) S / P), its arcs one copy
+    const uint32_t segs = seg_shift >= 32 ? 1u : static_cast<uint32_t>(((hi - 1) >> seg_shift) + 1);
+    const uint32_t pchunks = pipeline ? std::min<uint32_t>(8, segs) : 0;
+    std::vector<uint32_t> chunk_seg(pchunks + 1);
+    if (pipeline) {  // chunk arc ranges must be ordered (else: one copy; the build flags it)
+      uint64_t prev = a0;
+      for (uint32_t c = 1; c <= pchunks && pipeline; ++c) {
+        const uint64_t v = std::min<uint64_t>(
+            static_cast<uint64_t>(static_cast<uint64_t>(c) * segs / pchunks) << seg_shift, hi);
+        const uint64_t b = g->offsets[v];
+        if (b < prev || b > a1) pipeline = false;
+        prev = b;
+      }
+    }
+    if (pipeline) {
+      for (uint32_t c = 0; c <= pchunks; ++c) {
+        chunk_seg[c] = static_cast<uint32_t>(static_cast<uint64_t>(c) * segs / pchunks);
+        if (c < pchunks) {
+          cudaEvent_t ev = nullptr;
+          HANF_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          guard.chunks.push_back(ev);
+        }
+      }
+      for (uint32_t c = 0; c < pchunks; ++c) {
+        const uint64_t v0 = std::min<uint64_t>(static_cast<uint64_t>(chunk_seg[c]) << seg_shift, hi);
+        const uint64_t v1 = std::min<uint64_t>(static_cast<uint64_t>(chunk_seg[c + 1]) << seg_shift, hi);
+        const uint64_t b0 = g->offsets[v0], b1 = g->offsets[v1];
+        if (b1 > b0)
+          HANF_TRY(cudaMemcpyAsync(d_succ + (b0 - a0), g->arcs + b0, sizeof(uint32_t) * (b1 - b0),
+                                   cudaMemcpyHostToDevice, s2));
+        HANF_TRY(cudaEventRecord(guard.chunks[c], s2));
+      }
+    } else if (a1 > a0) {
       HANF_TRY(cudaMemcpyAsync(d_succ, g->arcs + a0, sizeof(uint32_t) * (a1 - a0),
                                cudaMemcpyHostToDevice, s2));
+    }
     HANF_TRY(cudaEventRecord(ev_arcs, s2));
     phase("offsets");
     if (K > 1) {
@@ -1298,30 +1381,12 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     int bad = 0;
     // relabelled: row v's successors are the caller's arcs of order[v], through perm
     const hanf::CsrView view{d_off, up_lo, d_succ, a0, e->order, e->perm, n};
-    // Segments (HANF_SEGMENTS=0/1 forces): graphs whose ids carry locality
-    // (the copying model's windows) group their tasks by node segment of
-    // n/256 nodes, so late skip sweeps visit only the segments near the
-    // changed counters; ids without locality would gain nothing
-    uint32_t seg_shift = 32;
-    {
-      const char* sg = std::getenv("HANF_SEGMENTS");
-      const bool want = sg && (sg[0] == '0' || sg[0] == '1')
-                            ? sg[0] == '1'
-                            : K == 1 && !e->relabel && n >= (1ull << 20) && ids_local(g);
-      if (want && K == 1 && !e->relabel && n > 1) {
-        uint32_t bits = 0;
-        while ((1ull << bits) < n) ++bits;
-        // 4096 segments (config 3: 2^12 nodes each; the +-2^12 windows make
-        // finer ones no better): profiles/r01_segments.md
-        seg_shift = bits > 18 ? bits - 12 : 6;
-        if (const char* sh = std::getenv("HANF_SEG_SHIFT")) seg_shift = std::atoi(sh);
-        if (seg_shift < 6) seg_shift = 6;
-      }
-    }
     const cudaError_t be = hanf::build_tasks_device(view, lo, hi, n, seg_shift, s, ev_arcs,
-                                                    &e->tasks, &bad, &e->launches);
-    // (also on the build's error paths) frees on `s` come after the upload
-    HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+                                                    &e->tasks, &bad, &e->launches, pipeline,
+                                                    seg_skip, !seg_skip);
+    // (also on the build's error paths) frees on `s` come after the upload;
+    // the pipelined sweep waits for each chunk itself
+    if (!pipeline || be != cudaSuccess || bad) HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
     e->csr_off = d_off;
     e->csr_succ = d_succ;
     e->succ_base = a0;
@@ -1336,9 +1401,54 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       pfree(e->csr_off, s);
       pfree(e->csr_succ, s);
     }
-    if (e->tasks.seg_shift < 32) HANF_TRY(palloc(&e->seg_live, e->tasks.num_segs, s));
+    if (seg_skip && e->tasks.seg_shift < 32)
+      HANF_TRY(palloc(&e->seg_live, e->tasks.num_segs, s));
+    if (pipeline) {
+      HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
+      // step 1's sweep (t = 0: dense, nothing stale) chunk by chunk
+      HANF_TRY(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, s));
+      hanf::UnionArgs u = union_args(e, 0, 1);
+      const hanf::WarpTask* all = e->tasks.wtasks;
+      auto sweep = [&](uint64_t t0, uint64_t t1) -> cudaError_t {
+        if (t1 <= t0) return cudaSuccess;
+        cudaError_t ce = hanf::fill_tos_range(view, e->tasks, t0, t1, n, s, &e->launches);
+        if (ce != cudaSuccess) return ce;
+        u.wtasks = all + t0;
+        u.num_wtasks = static_cast<uint32_t>(t1 - t0);
+        return hanf::launch_union(u, e->params.register_bits, e->params.registers, e->gather_mode,
+                                  nullptr, s, &e->launches);
+      };
+      const auto& gtb = e->tasks.group_task_begin;
+      const auto& gsg = e->tasks.group_seg;
+      phase("tasks");
+      for (uint32_t c = 0; c < pchunks; ++c) {
+        HANF_TRY(cudaStreamWaitEvent(s, guard.chunks[c], 0));
+        // the chunk's groups, adjacent ones merged into one launch
+        uint64_t t0 = 0, t1 = 0;
+        for (size_t k = 0; k < gsg.size(); ++k) {
+          if (gsg[k] < chunk_seg[c] || gsg[k] >= chunk_seg[c + 1]) continue;
+          if (gtb[k] != t1) {
+            HANF_TRY(sweep(t0, t1));
+            t0 = gtb[k];
+          }
+          t1 = gtb[k + 1];
+        }
+        HANF_TRY(sweep(t0, t1));
+        phase("chunk");
+      }
+      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+      HANF_TRY(sweep(0, e->tasks.num_chunks));  // hub chunks (their arcs span chunks)
+      phase("hubs");
+      int bad2 = 0;
+      HANF_TRY(hanf::finish_tasks_device(view, &e->tasks, lo, hi, seg_skip, s, &bad2,
+                                         &e->launches));
+      if (bad2)
+        return bail(fail(HANF_INVALID_ARGUMENT,
+                         "arc endpoint out of range or offsets not non-decreasing"));
+      e->pre_step = true;
+    }
     phase("build");
-    HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
+    if (!pipeline) HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
   }
 #undef HANF_TRY
   *out = e;
@@ -1523,6 +1633,7 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
   e->cur = 0;
   e->stale_valid = false;
   e->systolic = false;
+  e->pre_step = false;
   if (e->shard_relabel) e->est = e->est_gen[0];
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
   if (st != HANF_OK) return st;

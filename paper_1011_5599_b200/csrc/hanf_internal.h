@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "hanf_device.cuh"
 
@@ -49,6 +50,17 @@ struct TaskBuild {
   uint32_t num_segs = 1;
   uint32_t* seg_min = nullptr;
   uint32_t* seg_max = nullptr;
+  // light tasks in groups of one (segment, class) pair, segment-major (the
+  // locality order) or class-major (pipelined create: the heaviest tasks of
+  // every segment first); group k = task slots [group_task_begin[k],
+  // group_task_begin[k+1]) of segment group_seg[k] (hub chunk tasks are
+  // slots [0, num_chunks))
+  std::vector<uint64_t> group_task_begin;
+  std::vector<uint32_t> group_seg;
+  // deferred TOS fill (build_tasks_device(..., defer_fill)): kept until
+  // finish_tasks_device
+  uint64_t* chunk_begin = nullptr;
+  int* fill_bad = nullptr;
 };
 // The CSR as the task build reads it: node (row) v's successors are arcs
 // [begin(v), end(v)) of `succ` (from index succ_base), each mapped through
@@ -77,9 +89,19 @@ struct CsrView {
 // Sets *bad_input when offsets decrease or an arc endpoint is >= n.  Only
 // the final TOS fill reads the arcs: it waits for `succ_ready` (when
 // non-null), so the arcs upload overlaps the degree sort and task layout.
+// defer_fill: the TOS is allocated but not filled (nor the segment bounds
+// computed): the caller fills task ranges with fill_tos_range as their
+// arcs arrive, then calls finish_tasks_device.
 cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
                                uint32_t seg_shift, cudaStream_t s, cudaEvent_t succ_ready,
-                               TaskBuild* out, int* bad_input, uint64_t* launches);
+                               TaskBuild* out, int* bad_input, uint64_t* launches,
+                               bool defer_fill = false, bool seg_bounds = true,
+                               bool class_major = false);
+cudaError_t fill_tos_range(const CsrView& g, const TaskBuild& t, uint64_t t0, uint64_t t1,
+                           uint64_t n, cudaStream_t s, uint64_t* launches);
+cudaError_t finish_tasks_device(const CsrView& g, TaskBuild* t, uint64_t lo, uint64_t hi,
+                                bool seg_bounds, cudaStream_t s, int* bad_input,
+                                uint64_t* launches);
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
 // Locality relabelling (hanf_relabel.cu): rows renumbered by descending

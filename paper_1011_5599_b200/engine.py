@@ -14,6 +14,7 @@ error behaviour follow the reference:
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import enum
 from ctypes import POINTER, c_double, c_int32, c_uint64, c_void_p
 from dataclasses import dataclass, field
@@ -134,7 +135,7 @@ class NfEngine:
 
     def __init__(self, graph: Graph, cfg: EngineConfig = None):
         cfg = cfg or EngineConfig()
-        self._cfg = cfg
+        self._cfg = dataclasses.replace(cfg)  # (reseed / restore update the engine's copy only)
         self._graph = graph
         self._h = c_void_p()
         view = graph.view()

@@ -436,6 +436,48 @@ def test_golden_trace_segmented(hanf, traces, idx, monkeypatch):
     test_golden_trace(hanf, traces, idx)
 
 
+@pytest.mark.parametrize("idx", range(28))
+def test_golden_trace_pipelined(hanf, traces, idx, monkeypatch):
+    """Pipelined create (arcs uploaded in node-range chunks, iteration 1's
+    sweep run chunk by chunk as they land; on by default from 2^20 arcs,
+    forced here): every golden iteration bit-exact."""
+    monkeypatch.setenv("HANF_PIPELINE", "1")
+    test_golden_trace(hanf, traces, idx)
+
+
+@pytest.mark.parametrize("env", [{"HANF_PIPELINE": "1"}, {"HANF_PIPELINE": "1", "HANF_SEGMENTS": "1"},
+                                 {"HANF_PIPELINE": "0"}])
+def test_pipelined_create_lockstep_and_reset(hanf, port, monkeypatch, env):
+    """The precomputed iteration 1 is consumed by the first step only:
+    lockstep with the oracle, then reset / reseed re-run every step in full,
+    and bad arcs are still rejected (the pipelined sweep reads the zero row
+    for them before the check reports)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = hanf.gen_rmat(13, 16, 0.57, 0.19, 0.19, 2, 3)
+    for b in (5, 6, 7):
+        lockstep(hanf, port, g, bucket_bits=b, seed=21)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=21)
+    ref = hanf.estimate_nf(g, cfg)
+    with hanf.NfEngine(g, cfg) as e:
+        e.step()
+        e.reset()
+        assert e.run_to_stabilisation().values == ref.values
+        e.reseed(22)
+        other = e.run_to_stabilisation()
+    monkeypatch.setenv("HANF_PIPELINE", "0")
+    assert other.values == hanf.estimate_nf(g, hanf.EngineConfig(bucket_bits=6, seed=22)).values
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    arcs = g.arcs().copy()
+    arcs[len(arcs) // 2] = g.num_nodes() + 5
+    bad = hanf.Graph(g.num_nodes(), g.offsets().copy(), arcs)
+    with pytest.raises(ValueError):
+        hanf.NfEngine(bad, cfg)
+    with hanf.NfEngine(g, cfg) as e:  # the device is fine afterwards
+        assert e.run_to_stabilisation().values == ref.values
+
+
 @pytest.mark.parametrize("env", [{}, {"HANF_SPARSE": "0"}, {"HANF_SUMMARY": "1"}])
 def test_segmented_copying_graph(hanf, port, monkeypatch, env):
     """A config-3-shaped copying graph (local ids: segmented by default from
