@@ -304,7 +304,9 @@ def test_config2_scale(hanf, port):
 
 @pytest.mark.parametrize("b,env,delta", [(6, {}, False), (6, {"HANF_SPARSE": "1"}, False),
                                          (5, {}, False), (8, {}, False), (6, {}, True),
-                                         (5, {"HANF_SPARSE": "1"}, True), (8, {}, True)])
+                                         (5, {"HANF_SPARSE": "1"}, True), (8, {}, True),
+                                         (6, {"HANF_SEGMENTS": "1"}, True),
+                                         (7, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"}, False)])
 def test_sharded_engines_exchange(hanf, port, monkeypatch, b, env, delta):
     """The shard ABI (hanf_shard_compute / device buffers / hanf_shard_commit)
     on one GPU: two node-range engines, exchange done by device copies in
