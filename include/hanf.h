@@ -276,6 +276,9 @@ hanf_status hanf_shard_attach(hanf_engine* engine, const hanf_shard_peer* peers,
  * same device, or peer access enabled by the caller). */
 hanf_status hanf_shard_attach_local(hanf_engine* engine, hanf_engine* const* peers, uint32_t count,
                                     uint32_t self);
+/* Waits for this engine's enqueued device work (hanf_shard_compute's
+ * pushes included): the step's barrier across the ranks comes after it. */
+hanf_status hanf_shard_wait(hanf_engine* engine);
 /* Back to the collective exchange (closes opened IPC mappings). */
 hanf_status hanf_shard_detach(hanf_engine* engine);
 

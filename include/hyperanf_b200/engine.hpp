@@ -274,6 +274,77 @@ class NfEngine {
   hanf_engine* h_ = nullptr;
 };
 
+// One node range of a multi-GPU run (new; the reference has no distributed
+// engine).  Peer-push exchange (hanf.h): every rank exports its arena,
+// the caller's transport (MPI, sockets, torch.distributed) all-gathers the
+// descriptors, attach() maps the peers; a step is compute(), a barrier
+// across the ranks after compute() returned, then commit() - the same
+// IterationReport on every rank, equal to the single engine's bit for bit.
+class ShardEngine {
+ public:
+  template <class G>
+  ShardEngine(const G& graph, EngineConfig cfg, std::uint64_t begin, std::uint64_t end,
+              std::uint32_t shards)
+      : n_(graph.num_nodes()) {
+    const hanf_graph_view v = view_of(graph);
+    hanf_config c = cfg.to_c();
+    c.shard_begin = begin;
+    c.shard_end = end;
+    c.shard_count = shards;
+    check(hanf_create(&v, &c, &h_));
+  }
+  ShardEngine(const ShardEngine&) = delete;
+  ShardEngine& operator=(const ShardEngine&) = delete;
+  ~ShardEngine() {
+    hanf_shard_detach(h_);
+    hanf_destroy(h_);
+  }
+  hanf_shard_peer export_peer() const {
+    hanf_shard_peer p;
+    check(hanf_shard_export(h_, &p));
+    return p;
+  }
+  // peers = every rank's export_peer(), in rank order; self = this rank
+  void attach(const std::vector<hanf_shard_peer>& peers, std::uint32_t self) {
+    check(hanf_shard_attach(h_, peers.data(), static_cast<std::uint32_t>(peers.size()), self));
+  }
+  // shards of one process (same device, or peer access between them)
+  static void attach_local(const std::vector<ShardEngine*>& shards) {
+    std::vector<hanf_engine*> hs;
+    for (auto* s : shards) hs.push_back(s->h_);
+    for (std::uint32_t k = 0; k < hs.size(); ++k)
+      check(hanf_shard_attach_local(hs[k], hs.data(), static_cast<std::uint32_t>(hs.size()), k));
+  }
+  // enqueue this range's sweep (rows pushed to the peers) and wait for it
+  void compute() {
+    check(hanf_shard_compute(h_));
+    check(hanf_shard_wait(h_));
+  }
+  IterationReport commit() {
+    hanf_iteration_report r;
+    check(hanf_shard_commit(h_, &r));
+    return {r.sum, r.modified};
+  }
+  double sum_estimates() {
+    double s = 0.0;
+    check(hanf_sum_estimates(h_, &s));
+    return s;
+  }
+  std::vector<std::uint64_t> counters() const {
+    hanf_sketch_params p;
+    check(hanf_params(h_, &p));
+    std::vector<std::uint64_t> out(static_cast<size_t>(n_) * p.words_per_counter);
+    check(hanf_read_counters(h_, 0, n_, out.data()));
+    return out;
+  }
+  void detach() { check(hanf_shard_detach(h_)); }
+  hanf_engine* handle() noexcept { return h_; }
+
+ private:
+  std::uint64_t n_ = 0;
+  hanf_engine* h_ = nullptr;
+};
+
 template <class G>
 NfEstimate estimate_nf(const G& g, const EngineConfig& cfg) {
   NfEngine engine(g, cfg);

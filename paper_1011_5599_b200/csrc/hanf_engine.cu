@@ -1886,6 +1886,13 @@ hanf_status hanf_shard_attach_local(hanf_engine* e, hanf_engine* const* peers, u
   return HANF_OK;
 }
 
+hanf_status hanf_shard_wait(hanf_engine* e) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  HANF_CUDA(cudaSetDevice(e->device));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  return HANF_OK;
+}
+
 hanf_status hanf_shard_detach(hanf_engine* e) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
   HANF_CUDA(cudaSetDevice(e->device));

@@ -5,7 +5,9 @@
 // oracle/Makefile into oracle/_ref/ (it contains reference code), run by
 // tests/test_gpu_dropin.py on the GPU box.  Exit 0 = every check passed.
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -148,6 +150,39 @@ int main() {
     expect(!slurp(a).empty() && slurp(a) == slurp(b), "HCA1 snapshot bytes");
     std::remove(a.c_str());
     std::remove(b.c_str());
+  }
+  {  // multi-GPU path in C++: 2 and 3 peer-push shards of one process
+     // against the reference engine, every iteration
+    const auto g = hyperanf::gen_uniform_random(3000, 6.0, 17);
+    hyperanf::EngineConfig c;
+    c.bucket_bits = 6;
+    c.seed = 5;
+    for (std::uint32_t k : {2u, 3u}) {
+      const std::uint64_t n = g.num_nodes(), per = ((n + k - 1) / k + 63) / 64 * 64;
+      std::vector<std::unique_ptr<hyperanf_b200::ShardEngine>> own;
+      std::vector<hyperanf_b200::ShardEngine*> shards;
+      for (std::uint32_t r = 0; r < k; ++r) {
+        own.emplace_back(new hyperanf_b200::ShardEngine(
+            g, hyperanf_b200::from_reference(c), std::min(n, r * per), std::min(n, (r + 1) * per), k));
+        shards.push_back(own.back().get());
+      }
+      hyperanf_b200::ShardEngine::attach_local(shards);
+      hyperanf::NfEngine ref(g, c);
+      bool same = true;
+      for (std::uint64_t t = 1; t <= n + 1 && same; ++t) {
+        for (auto* s : shards) s->compute();
+        std::vector<hyperanf_b200::IterationReport> reps;
+        for (auto* s : shards) reps.push_back(s->commit());
+        const auto a = ref.step();
+        const auto& rc = ref.counters();
+        for (auto& r : reps) same = same && r.sum == a.sum && r.modified == a.modified;
+        same = same && std::vector<std::uint64_t>(rc.data(), rc.data() + rc.word_count()) ==
+                           shards.back()->counters();
+        if (a.modified == 0) break;
+      }
+      expect(same, "peer-push shards x" + std::to_string(k));
+      for (auto* s : shards) s->detach();
+    }
   }
   std::printf("dropin_test: %zu graphs, %d failures\n", cases.size(), failures);
   return failures == 0 ? 0 : 1;
