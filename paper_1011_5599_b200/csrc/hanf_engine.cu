@@ -1233,6 +1233,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     uint32_t seg_shift = 32;
     bool seg_skip = false;
     bool pipeline = false;
+    bool scatter = false;
     {
       uint32_t bits = 0;
       while ((1ull << bits) < n) ++bits;
@@ -1254,6 +1255,14 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
                                                              params.registers);
       pipeline = eligible && pp && pp[0] == '1';
       if (pipeline && seg_shift >= 32) seg_shift = bits > 9 ? bits - 3 : 6;  // 8 chunks
+      // Scatter fill (opt-in, HANF_SCATTER_FILL=1; unrelabelled engines):
+      // the arcs go up in 8 arc-balanced node-range chunks and each chunk's
+      // ids are scattered into the TOS as soon as it lands.  Measured on
+      // config 2 it loses: a node's ids land 32 rows apart, so the
+      // scattered 4-byte stores take ~0.25 ms per chunk against 0.09 ms for
+      // the whole task-ordered fill (profiles/r01_pipeline.md)
+      const char* sf = std::getenv("HANF_SCATTER_FILL");
+      scatter = !pipeline && K == 1 && !e->relabel && n > 64 && sf && sf[0] == '1';
     }
     uint64_t a0 = g->offsets[up_lo], a1 = g->offsets[up_hi];
     uint64_t* d_off = nullptr;
@@ -1321,10 +1330,40 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
                                    cudaMemcpyHostToDevice, s2));
         HANF_TRY(cudaEventRecord(guard.chunks[c], s2));
       }
-    } else if (a1 > a0) {
+    }
+    // scatter fill: chunk c = rows [scatter_v[c], scatter_v[c+1]), ~(a1-a0)/8 arcs each
+    std::vector<uint64_t> scatter_v;
+    if (scatter) {
+      const uint32_t P = 8;
+      scatter_v.push_back(lo);
+      for (uint32_t c = 1; c < P; ++c) {
+        const uint64_t target = a0 + (a1 - a0) * c / P;
+        uint64_t l = scatter_v.back(), h = hi;  // first v with offsets[v] >= target
+        while (l < h) {
+          const uint64_t mid = l + (h - l) / 2;
+          if (g->offsets[mid] < target) l = mid + 1; else h = mid;
+        }
+        scatter_v.push_back(l);
+      }
+      scatter_v.push_back(hi);
+      for (size_t c = 0; c + 1 < scatter_v.size() && scatter; ++c) {  // ordered and in range
+        const uint64_t b0 = g->offsets[scatter_v[c]], b1 = g->offsets[scatter_v[c + 1]];
+        if (b1 < b0 || b0 < a0 || b1 > a1) scatter = false;
+      }
+      for (size_t c = 0; c + 1 < scatter_v.size() && scatter; ++c) {
+        cudaEvent_t ev = nullptr;
+        HANF_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        guard.chunks.push_back(ev);
+        const uint64_t b0 = g->offsets[scatter_v[c]], b1 = g->offsets[scatter_v[c + 1]];
+        if (b1 > b0)
+          HANF_TRY(cudaMemcpyAsync(d_succ + (b0 - a0), g->arcs + b0, sizeof(uint32_t) * (b1 - b0),
+                                   cudaMemcpyHostToDevice, s2));
+        HANF_TRY(cudaEventRecord(ev, s2));
+      }
+    }
+    if (!pipeline && !scatter && a1 > a0)
       HANF_TRY(cudaMemcpyAsync(d_succ, g->arcs + a0, sizeof(uint32_t) * (a1 - a0),
                                cudaMemcpyHostToDevice, s2));
-    }
     HANF_TRY(cudaEventRecord(ev_arcs, s2));
     phase("offsets");
     if (K > 1) {
@@ -1382,11 +1421,12 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     // relabelled: row v's successors are the caller's arcs of order[v], through perm
     const hanf::CsrView view{d_off, up_lo, d_succ, a0, e->order, e->perm, n};
     const cudaError_t be = hanf::build_tasks_device(view, lo, hi, n, seg_shift, s, ev_arcs,
-                                                    &e->tasks, &bad, &e->launches, pipeline,
-                                                    seg_skip, !seg_skip);
+                                                    &e->tasks, &bad, &e->launches,
+                                                    pipeline || scatter, seg_skip, !seg_skip);
     // (also on the build's error paths) frees on `s` come after the upload;
     // the pipelined sweep waits for each chunk itself
-    if (!pipeline || be != cudaSuccess || bad) HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+    if (!(pipeline || scatter) || be != cudaSuccess || bad)
+      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
     e->csr_off = d_off;
     e->csr_succ = d_succ;
     e->succ_base = a0;
@@ -1403,6 +1443,24 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     }
     if (seg_skip && e->tasks.seg_shift < 32)
       HANF_TRY(palloc(&e->seg_live, e->tasks.num_segs, s));
+    if (scatter) {
+      phase("tasks");
+      HANF_TRY(hanf::scatter_fill_prepare(&e->tasks, lo, hi, n, s, &e->launches));
+      phase("prepare");
+      for (size_t c = 0; c + 1 < scatter_v.size(); ++c) {
+        HANF_TRY(cudaStreamWaitEvent(s, guard.chunks[c], 0));
+        HANF_TRY(hanf::scatter_fill_range(view, e->tasks, lo, scatter_v[c], scatter_v[c + 1], n, s,
+                                          &e->launches));
+        phase("scatter");
+      }
+      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+      int bad2 = 0;
+      HANF_TRY(hanf::finish_tasks_device(view, &e->tasks, lo, hi, seg_skip, s, &bad2,
+                                         &e->launches));
+      if (bad2)
+        return bail(fail(HANF_INVALID_ARGUMENT,
+                         "arc endpoint out of range or offsets not non-decreasing"));
+    }
     if (pipeline) {
       HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
       // step 1's sweep (t = 0: dense, nothing stale) chunk by chunk

@@ -61,6 +61,7 @@ struct TaskBuild {
   // finish_tasks_device
   uint64_t* chunk_begin = nullptr;
   int* fill_bad = nullptr;
+  uint64_t* row_slot = nullptr;  // scatter fill: per row (v - lo), TOS offset | lane info
 };
 // The CSR as the task build reads it: node (row) v's successors are arcs
 // [begin(v), end(v)) of `succ` (from index succ_base), each mapped through
@@ -99,6 +100,15 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
                                bool class_major = false);
 cudaError_t fill_tos_range(const CsrView& g, const TaskBuild& t, uint64_t t0, uint64_t t1,
                            uint64_t n, cudaStream_t s, uint64_t* launches);
+// Scatter fill (unrelabelled engines, default from 2^20 arcs): the TOS is
+// filled arc by arc as the upload's node-range chunks land, in the task
+// order of the global degree sort.  scatter_fill_prepare (after a deferred
+// build, before any arc has arrived): every row's TOS slot and the padding;
+// scatter_fill_range: rows [v0, v1) once their arcs are on the device.
+cudaError_t scatter_fill_prepare(TaskBuild* t, uint64_t lo, uint64_t hi, uint64_t n,
+                                 cudaStream_t s, uint64_t* launches);
+cudaError_t scatter_fill_range(const CsrView& g, const TaskBuild& t, uint64_t lo, uint64_t v0,
+                               uint64_t v1, uint64_t n, cudaStream_t s, uint64_t* launches);
 cudaError_t finish_tasks_device(const CsrView& g, TaskBuild* t, uint64_t lo, uint64_t hi,
                                 bool seg_bounds, cudaStream_t s, int* bad_input,
                                 uint64_t* launches);

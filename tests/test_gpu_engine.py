@@ -439,6 +439,15 @@ def test_golden_trace_segmented(hanf, traces, idx, monkeypatch):
 
 
 @pytest.mark.parametrize("idx", range(28))
+def test_golden_trace_scatter_fill(hanf, traces, idx, monkeypatch):
+    """Scatter fill (the TOS filled arc by arc as the upload's node-range
+    chunks land; on by default from 2^20 arcs, forced here): every golden
+    iteration bit-exact."""
+    monkeypatch.setenv("HANF_SCATTER_FILL", "1")
+    test_golden_trace(hanf, traces, idx)
+
+
+@pytest.mark.parametrize("idx", range(28))
 def test_golden_trace_pipelined(hanf, traces, idx, monkeypatch):
     """Pipelined create (arcs uploaded in node-range chunks, iteration 1's
     sweep run chunk by chunk as they land; on by default from 2^20 arcs,
@@ -448,7 +457,9 @@ def test_golden_trace_pipelined(hanf, traces, idx, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"HANF_PIPELINE": "1"}, {"HANF_PIPELINE": "1", "HANF_SEGMENTS": "1"},
-                                 {"HANF_PIPELINE": "0"}])
+                                 {"HANF_PIPELINE": "0"}, {"HANF_SCATTER_FILL": "1"},
+                                 {"HANF_SCATTER_FILL": "1", "HANF_SEGMENTS": "1"},
+                                 {"HANF_SCATTER_FILL": "0"}])
 def test_pipelined_create_lockstep_and_reset(hanf, port, monkeypatch, env):
     """The precomputed iteration 1 is consumed by the first step only:
     lockstep with the oracle, then reset / reseed re-run every step in full,
