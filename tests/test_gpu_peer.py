@@ -217,3 +217,23 @@ def test_peer_push_ipc_two_processes(hanf, relabel):
         values, mods, counters = out[r]
         assert values == single.values and mods == single.modified
         assert np.array_equal(counters, ref)
+
+
+@pytest.mark.parametrize("relabel,world", [("0", 2), ("1", 4)])
+def test_peer_push_config2_full_size(hanf, monkeypatch, relabel, world):
+    """BASELINE config 2 at full size (R-MAT 20, 16.1 M arcs) as 2 / 4
+    peer-push shards on one GPU, plain and relabelled: N(t), modified and
+    every counter equal to the single engine's."""
+    import dataclasses
+    monkeypatch.setenv("HANF_RELABEL", relabel)
+    g = hanf.gen_rmat(20, 16, 0.57, 0.19, 0.19, 1, 7, device=0)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
+    values, mods, counters = _run_local(hanf, g, dataclasses.replace(cfg, shard_count=world),
+                                        world, False, relabelled=relabel == "1")
+    monkeypatch.setenv("HANF_RELABEL", "0")
+    with hanf.NfEngine(g, cfg) as e:
+        single = e.run_to_stabilisation()
+        ref = e.counters()
+    assert values == single.values and mods == single.modified
+    for c in counters:
+        assert np.array_equal(c, ref)
