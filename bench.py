@@ -268,15 +268,16 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
+    reset = sharded.reset if sharded is not None else engine.reset  # (shards: + barrier)
     for _ in range(args.warmup):
-        engine.reset()
+        reset()
         do_step()
     step_launches = 0
     total_ms = 0.0
     barrier()
     with ClockSampler(local_rank) as clocks:
         for _ in range(args.steps):
-            engine.reset()                       # untimed: back to the seeded state
+            reset()                              # untimed: back to the seeded state
             torch.cuda.synchronize(dev)
             launches_before = engine.launch_count()
             start = torch.cuda.Event(enable_timing=True)
@@ -306,7 +307,7 @@ def main():
     # engine stream (ungraphed steps, same kernels), same flush protocol
     engine.set_timing(True)
     for _ in range(max(3, min(args.steps, 10))):
-        engine.reset()
+        reset()
         flush.zero_()
         torch.cuda.synchronize(dev)
         do_step()

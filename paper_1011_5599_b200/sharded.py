@@ -276,6 +276,15 @@ class ShardedNfEngine:
     def sum_estimates(self) -> float:
         return self.local.sum_estimates()
 
+    def reset(self) -> None:
+        """hanf_reset on every rank, then a barrier: with the peer-push
+        exchange a rank that started its next step could otherwise push rows
+        into a peer that is still re-seeding both generations."""
+        self.local.engine.reset()
+        self.local.wait_compute()
+        dist.barrier(group=self.group)
+        self.last_modified = self.n
+
     def run_to_stabilisation(self) -> NfEstimate:
         """engine.hpp:233-275 over the sharded step."""
         est = NfEstimate(n=self.n, m=1 << self.cfg.bucket_bits, seed=self.cfg.seed,
