@@ -259,6 +259,11 @@ struct hanf_engine {
   // shards by degree; estimates are pushed to the peers and every commit
   // recomputes all original-id blocks from the full estimate array
   bool shard_relabel = false;
+  // relabelled shards' commit after a step with few changes: the
+  // original-id blocks of the changed rows (derived from the published row
+  // bitmap) instead of every block; all_dirty_commit = recompute them all
+  uint64_t* dirty_derived = nullptr;
+  bool all_dirty_commit = true;
   // relabelled engines keep estimates in row order (writes follow the task
   // order); finish_kernel gathers them through perm for the original-id
   // block sums.  HANF_EST_SCATTER=1: scatter to the original slot instead.
@@ -400,6 +405,7 @@ struct hanf_engine {
       pfree(dirty[1], stream);
       pfree(lens, stream);
       pfree(seg_live, stream);
+      pfree(dirty_derived, stream);
       hanf::free_tasks_device(&tasks, stream);
       if (cudaStreamSynchronize(stream) == cudaSuccess)
         streams().put(device, stream);
@@ -488,8 +494,9 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   f.b0 = b0;
   f.b1 = b1;
   f.perm = e->est_rows ? e->perm : nullptr;
-  // relabelled shards: every block from the (peer-pushed) estimates
-  f.all_dirty = in_step && e->shard_relabel ? 1 : 0;
+  // relabelled shards: every block from the (peer-pushed) estimates, or
+  // the derived dirty blocks (commit_enqueue)
+  f.all_dirty = in_step && e->shard_relabel && e->all_dirty_commit ? 1 : 0;
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
@@ -865,6 +872,19 @@ bool commit_recomputes(const hanf_engine* e) {
 hanf_status commit_enqueue(hanf_engine* e) {
   const int ng = 1 - e->cur;
   if (e->batch > 1) return batch_enqueue(e, e->mod[ng]);
+  if (e->shard_relabel) {
+    // few changes in the previous step (the tail): mark the original-id
+    // blocks of this step's changed rows (a scatter over the row bitmap);
+    // dense steps recompute every block (n estimate gathers either way)
+    e->all_dirty_commit = 64 * e->last_count >= e->n;
+    if (!e->all_dirty_commit) {
+      if (!e->dirty_derived) HANF_CUDA(palloc(&e->dirty_derived, e->blocks, e->stream));
+      HANF_CUDA(cudaMemsetAsync(e->dirty_derived, 0, sizeof(uint64_t) * e->blocks, e->stream));
+      HANF_CUDA(hanf::launch_derive_dirty(e->mod[ng], e->order, e->blocks, e->n, e->dirty_derived,
+                                          e->stream, &e->launches));
+      return finish_enqueue(e, e->dirty_derived, true, 0, e->blocks, true);
+    }
+  }
   return finish_enqueue(e, dirty_of(e, ng), commit_recomputes(e), 0, e->blocks, true);
 }
 

@@ -304,6 +304,10 @@ struct FinishArgs {
   int32_t all_dirty = 0;           // recompute every block of [b0, b1) (bits: count only)
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
+// dirty[order[r] / 64] |= bit for every row r set in `rows` (pre-zeroed
+// dirty; relabelled shards' commit of a step with few changes)
+cudaError_t launch_derive_dirty(const uint64_t* rows, const uint32_t* order, uint64_t words,
+                                uint64_t n, uint64_t* dirty, cudaStream_t s, uint64_t* launches);
 // live[s] = some row of [seg_min[s], seg_max[s]] is set in mod_cur (a
 // segment without one has no node that can change or is stale)
 cudaError_t launch_segment_live(const uint64_t* mod_cur, const uint32_t* seg_min,

@@ -969,6 +969,35 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
   }
 }
 
+__global__ void derive_dirty_kernel(const uint64_t* __restrict__ rows,
+                                    const uint32_t* __restrict__ order, uint64_t words, uint64_t n,
+                                    unsigned long long* __restrict__ dirty) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < words;
+       w += stride) {
+    uint64_t bits = rows[w];
+    while (bits) {
+      const uint64_t r = w * 64 + __ffsll(static_cast<long long>(bits)) - 1;
+      bits &= bits - 1;
+      if (r < n) {
+        const uint32_t o = order[r];
+        atomicOr(dirty + (o >> 6), 1ull << (o & 63));
+      }
+    }
+  }
+}
+
+cudaError_t launch_derive_dirty(const uint64_t* rows, const uint32_t* order, uint64_t words,
+                                uint64_t n, uint64_t* dirty, cudaStream_t s, uint64_t* launches) {
+  if (words == 0) return cudaSuccess;
+  uint64_t blocks = (words + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  derive_dirty_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
+      rows, order, words, n, reinterpret_cast<unsigned long long*>(dirty));
+  ++*launches;
+  return cudaGetLastError();
+}
+
 // One warp per segment: does mod_cur have a bit in [seg_min, seg_max]?
 __global__ void segment_live_kernel(const uint64_t* __restrict__ mod_cur,
                                     const uint32_t* __restrict__ seg_min,
