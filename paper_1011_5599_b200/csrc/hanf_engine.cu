@@ -497,11 +497,12 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   // relabelled shards: every block from the (peer-pushed) estimates, or
   // the derived dirty blocks (commit_enqueue)
   f.all_dirty = in_step && e->shard_relabel && e->all_dirty_commit ? 1 : 0;
+  // the last CTA writes total + count into the page-locked report itself
+  // (no read-back copy node after the kernel)
+  f.host_out = e->h_reduce;
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
-  HANF_CUDA(cudaMemcpyAsync(e->h_reduce, e->reduce, 2 * sizeof(double), cudaMemcpyDeviceToHost,
-                            e->stream));
   if (e->cfg.exact_sum)
     HANF_CUDA(cudaMemcpyAsync(e->h_block_sums[e->cur], sums, sizeof(double) * e->blocks,
                               cudaMemcpyDeviceToHost, e->stream));

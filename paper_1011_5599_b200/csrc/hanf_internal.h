@@ -302,6 +302,8 @@ struct FinishArgs {
   uint64_t b0, b1;        // block sums recomputed over [b0, b1)
   const uint32_t* perm = nullptr;  // estimates in row order: original id o is est[perm[o]]
   int32_t all_dirty = 0;           // recompute every block of [b0, b1) (bits: count only)
+  ReduceOut* host_out = nullptr;   // page-locked: total + count written there too (zero-copy
+                                   // report, no read-back copy after the kernel)
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
 // dirty[order[r] / 64] |= bit for every row r set in `rows` (pre-zeroed

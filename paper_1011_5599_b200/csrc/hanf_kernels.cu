@@ -966,6 +966,10 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
     a.out->total = total;
     a.out->count = count;
     a.out->ticket = 0;
+    if (a.host_out) {  // visible to the host once the stream has synchronised
+      a.host_out->total = total;
+      a.host_out->count = count;
+    }
   }
 }
 
