@@ -312,6 +312,9 @@ struct hanf_engine {
   // create pipelined iteration 1 with the arcs upload: the next generation,
   // its bitmap and estimates already hold step 1's sweep (hanf_create)
   bool pre_step = false;
+  // mod[1 - cur] is known to be all zero (seeding, or the last commit's
+  // finish_kernel cleared it): the step's memset is skipped
+  bool next_bits_clear = false;
   // Sharded engines keep cnt[2], mod[2] and two block-sum inboxes in one
   // IPC-exportable arena (cudaMalloc, not the pool), laid out identically
   // on every rank; attached peers' arenas receive this shard's rows, bitmap
@@ -500,6 +503,11 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   // the last CTA writes total + count into the page-locked report itself
   // (no read-back copy node after the kernel)
   f.host_out = e->h_reduce;
+  // single-GPU steps: the bitmap the next step writes (this step's mod_cur,
+  // dead once the sweep has run) is cleared in the same pass.  Shards keep
+  // their memset: peers publish into those words during their next step.
+  const bool sharded = e->lo != 0 || e->hi != e->n;
+  if (in_step && !sharded && e->batch == 1) f.clear = e->mod[e->cur];
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
@@ -586,6 +594,7 @@ hanf_status seed_all(hanf_engine* e) {
                               e->params.seed, e->order, e->batch, e->batch_mix, e->stream,
                               &e->launches));
   HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
+  e->next_bits_clear = true;
   if (e->dirty[0]) {  // every counter was seeded: all ones in both id spaces
     HANF_CUDA(cudaMemcpyAsync(e->dirty[0], e->mod[0], sizeof(uint64_t) * e->blocks,
                               cudaMemcpyDeviceToDevice, e->stream));
@@ -812,7 +821,11 @@ hanf_status compute_shard(hanf_engine* e) {
     return fail(HANF_INVALID_ARGUMENT,
                 "relabelled shard engines exchange through hanf_shard_attach (peer-push)");
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
-  HANF_CUDA(cudaMemsetAsync(e->mod[ng] + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
+  // the next bitmap is zero already where the previous commit cleared it
+  // (single-GPU engines, finish_kernel `clear`); shards clear their words
+  if (!e->next_bits_clear)
+    HANF_CUDA(cudaMemsetAsync(e->mod[ng] + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
+  e->next_bits_clear = false;
   if (e->dirty[ng])  // unsharded relabelling: the whole original-id bitmap
     HANF_CUDA(cudaMemsetAsync(e->dirty[ng], 0, sizeof(uint64_t) * e->blocks, e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
@@ -886,7 +899,10 @@ hanf_status commit_enqueue(hanf_engine* e) {
       return finish_enqueue(e, e->dirty_derived, true, 0, e->blocks, true);
     }
   }
-  return finish_enqueue(e, dirty_of(e, ng), commit_recomputes(e), 0, e->blocks, true);
+  const hanf_status st = finish_enqueue(e, dirty_of(e, ng), commit_recomputes(e), 0, e->blocks, true);
+  // (finish_kernel cleared mod[cur], the next step's mod_next)
+  if (st == HANF_OK && e->lo == 0 && e->hi == e->n) e->next_bits_clear = true;
+  return st;
 }
 
 // Generation swap and the per-step state after a step's modified count is

@@ -304,6 +304,7 @@ struct FinishArgs {
   int32_t all_dirty = 0;           // recompute every block of [b0, b1) (bits: count only)
   ReduceOut* host_out = nullptr;   // page-locked: total + count written there too (zero-copy
                                    // report, no read-back copy after the kernel)
+  uint64_t* clear = nullptr;       // words [0, blocks) zeroed (the next step's mod_next)
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
 // dirty[order[r] / 64] |= bit for every row r set in `rows` (pre-zeroed

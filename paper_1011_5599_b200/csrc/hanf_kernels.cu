@@ -931,6 +931,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
   unsigned long long cnt = 0;
   const uint64_t b = b0 + t;
   if (t < kFinishBlocks && b < a.blocks) {
+    if (a.clear) a.clear[b] = 0;
     const uint64_t word = a.bits[b];
     cnt = __popcll(word);
     if (a.est && (word != 0 || a.all_dirty) && b >= a.b0 && b < a.b1) {
