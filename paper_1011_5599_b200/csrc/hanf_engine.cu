@@ -503,6 +503,9 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   // the last CTA writes total + count into the page-locked report itself
   // (no read-back copy node after the kernel)
   f.host_out = e->h_reduce;
+  // exact_sum: every block sum also goes straight to this parity's
+  // page-locked copy (the host sums them in the reference's order)
+  if (e->cfg.exact_sum) f.host_sums = e->h_block_sums[e->cur];
   // single-GPU steps: the bitmap the next step writes (this step's mod_cur,
   // dead once the sweep has run) is cleared in the same pass.  Shards keep
   // their memset: peers publish into those words during their next step.
@@ -511,9 +514,6 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[3], e->stream));
-  if (e->cfg.exact_sum)
-    HANF_CUDA(cudaMemcpyAsync(e->h_block_sums[e->cur], sums, sizeof(double) * e->blocks,
-                              cudaMemcpyDeviceToHost, e->stream));
   return HANF_OK;
 }
 

@@ -305,6 +305,8 @@ struct FinishArgs {
   ReduceOut* host_out = nullptr;   // page-locked: total + count written there too (zero-copy
                                    // report, no read-back copy after the kernel)
   uint64_t* clear = nullptr;       // words [0, blocks) zeroed (the next step's mod_next)
+  double* host_sums = nullptr;     // page-locked: every block sum [0, blocks) written there
+                                   // too (exact_sum: the host redoes the total in order)
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launches);
 // dirty[order[r] / 64] |= bit for every row r set in `rows` (pre-zeroed

@@ -943,6 +943,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const FinishArgs
     } else {
       sum = a.block_sums[b];
     }
+    if (a.host_sums) a.host_sums[b] = sum;
   }
   const double cta_sum = cta_tree_sum(sum, sh);
   const unsigned long long cta_cnt = cta_count_sum(cnt, shc);
