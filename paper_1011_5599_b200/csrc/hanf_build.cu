@@ -275,33 +275,37 @@ fill_tos_kernel(const CsrView g, const uint32_t* __restrict__ order,
   bool out_of_range = false;
   for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
        w < num_tasks; w += warps) {
+    // Row by row: lane l writes entry l of every row (coalesced 128-byte
+    // stores, padding included), reading successor i G + sub of its node
+    // (a node's G lanes read consecutive arcs; each lane walks its own list)
     const WarpTask t = tasks[w];
     uint32_t* dst = tos + t.tos;
-    for (uint32_t i = lane; i < 32u * t.trips; i += 32) dst[i] = n;
-    __syncwarp();
+    uint64_t s = 0, d = 0;  // this lane's arcs, and its stride / first index in them
+    uint32_t step = 32, first = lane;
     if (t.nodes == 0) {
-      const uint64_t a = chunk_begin[t.item];
-      const uint32_t v = chunk_node[t.item];
-      const uint64_t e = g.end(v);
-      const uint64_t len = e - a < kHubChunk ? e - a : kHubChunk;
-      for (uint32_t k = lane; k < len; k += 32) {
-        const uint32_t id = g.id(a + k);
-        out_of_range |= id >= n;
-        dst[k] = id < n ? id : n;  // (a pipelined sweep may run before the check)
-      }
+      s = chunk_begin[t.item];
+      const uint64_t e = g.end(chunk_node[t.item]);
+      d = e - s < kHubChunk ? e - s : kHubChunk;
     } else {
-      const uint32_t G = 1u << t.lg;
-      for (uint32_t j = 0; j < t.nodes; ++j) {
+      const uint32_t j = lane >> t.lg;
+      step = 1u << t.lg;
+      first = lane & (step - 1);
+      if (j < t.nodes) {
         const uint32_t v = order[t.item + j];
-        const uint64_t s = g.begin(v), d = g.end(v) - s;
-        for (uint64_t k = lane; k < d; k += 32) {
-          const uint32_t id = g.id(s + k);
-          out_of_range |= id >= n;
-          dst[32 * (k >> t.lg) + j * G + (k & (G - 1))] = id < n ? id : n;
-        }
+        s = g.begin(v);
+        d = g.end(v) - s;
       }
     }
-    __syncwarp();
+    for (uint32_t i = 0; i < t.trips; ++i) {
+      const uint64_t k = static_cast<uint64_t>(i) * step + first;
+      uint32_t id = n;
+      if (k < d) {
+        id = g.id(s + k);
+        out_of_range |= id >= n;
+        if (id >= n) id = n;  // (a pipelined sweep may run before the check)
+      }
+      dst[32 * i + lane] = id;
+    }
   }
   if (__any_sync(0xffffffffu, out_of_range) && lane == 0) *bad = 1;
 }
