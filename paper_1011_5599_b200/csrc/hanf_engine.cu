@@ -275,6 +275,7 @@ struct hanf_engine {
   CUtensorMap tmap[2];        // descriptors of cnt[0], cnt[1]
 
   hanf::ReduceOut* h_reduce = nullptr;  // pinned (cache): total + count
+  double* h_log_stage = nullptr;        // pinned (cache): the log table's upload source
   // pinned (cache), exact_sum mode: one per generation parity, so a step
   // can be launched while the previous step's block sums are summed
   double* h_block_sums[2] = {nullptr, nullptr};
@@ -417,6 +418,7 @@ struct hanf_engine {
       phase("free");
     }
     pinned().put(h_reduce);
+    pinned().put(h_log_stage);
     pinned().put(h_block_sums[0]);
     pinned().put(h_block_sums[1]);
     pinned().put(h_batch_counts);
@@ -1209,14 +1211,16 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     HANF_TRY(palloc(&e->reduce, 1, s));
     HANF_TRY(palloc(&e->reduce_sums, ctas, s));
     HANF_TRY(palloc(&e->reduce_counts, ctas, s));
+    // staged in the engine's page-locked report block: an async copy, no
+    // synchronisation (the first finish_kernel writes that block afterwards)
+    e->h_reduce = static_cast<hanf::ReduceOut*>(pinned().get(sizeof(hanf::ReduceOut)));
+    if (!e->h_reduce) return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
     hanf::ReduceOut init{};
     init.partial_sum = e->reduce_sums;
     init.partial_count = e->reduce_counts;
-    HANF_TRY(cudaMemcpyAsync(e->reduce, &init, sizeof(init), cudaMemcpyHostToDevice, s));
-    HANF_TRY(cudaStreamSynchronize(s));  // `init` is a stack object
+    *e->h_reduce = init;
+    HANF_TRY(cudaMemcpyAsync(e->reduce, e->h_reduce, sizeof(init), cudaMemcpyHostToDevice, s));
   }
-  e->h_reduce = static_cast<hanf::ReduceOut*>(pinned().get(sizeof(hanf::ReduceOut)));
-  if (!e->h_reduce) return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
   if (cfg.exact_sum) {
     for (auto& hb : e->h_block_sums) {
       hb = static_cast<double*>(pinned().get(sizeof(double) * (e->blocks ? e->blocks : 1)));
@@ -1226,13 +1230,15 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   // linear-counting table m*log(m/z), same expression as hll.hpp:139
   {
     const double m = static_cast<double>(params.registers);
-    std::vector<double> table(params.registers + 1, 0.0);
+    const size_t entries = params.registers + 1;
+    e->h_log_stage = static_cast<double*>(pinned().get(sizeof(double) * entries));
+    if (!e->h_log_stage) return bail(fail(HANF_OUT_OF_MEMORY, "pinned host allocation failed"));
+    e->h_log_stage[0] = 0.0;
     for (uint32_t z = 1; z <= params.registers; ++z)
-      table[z] = m * std::log(m / static_cast<double>(z));
-    HANF_TRY(palloc(&e->log_table, table.size(), s));
-    HANF_TRY(cudaMemcpyAsync(e->log_table, table.data(), sizeof(double) * table.size(),
-                             cudaMemcpyHostToDevice, s));
-    HANF_TRY(cudaStreamSynchronize(s));
+      e->h_log_stage[z] = m * std::log(m / static_cast<double>(z));
+    HANF_TRY(palloc(&e->log_table, entries, s));
+    HANF_TRY(cudaMemcpyAsync(e->log_table, e->h_log_stage, sizeof(double) * entries,
+                             cudaMemcpyHostToDevice, s));  // (staging kept while the engine lives)
   }
   // HANF_PROFILE=1: print the create phases (synchronising between them)
   static const bool prof = [] {
