@@ -156,7 +156,7 @@ StreamCache& streams() {
   return *c;
 }
 
-// Process-wide cache of pinned host blocks (cudaMallocHost / cudaFreeHost
+// Process-wide cache of pinned host blocks (cudaHostAlloc / cudaFreeHost
 // synchronise the device; engines borrow and return blocks instead).
 class PinnedCache {
  public:
@@ -172,7 +172,11 @@ class PinnedCache {
       }
     }
     void* p = nullptr;
-    if (cudaMallocHost(&p, bytes ? bytes : 1) != cudaSuccess) return nullptr;
+    // portable + mapped: finish_kernel writes its report here from any
+    // device of the process (blocks are shared by engines on all devices)
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped) !=
+        cudaSuccess)
+      return nullptr;
     std::lock_guard<std::mutex> lock(mu_);
     sizes_[p] = bytes;
     return p;
