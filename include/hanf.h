@@ -276,6 +276,14 @@ hanf_status hanf_shard_attach(hanf_engine* engine, const hanf_shard_peer* peers,
  * same device, or peer access enabled by the caller). */
 hanf_status hanf_shard_attach_local(hanf_engine* engine, hanf_engine* const* peers, uint32_t count,
                                     uint32_t self);
+/* Relabelled shards (hanf_config.shard_count) under the peer-push
+ * exchange, optional: after the compute barrier, re-sums this rank's
+ * 1/shard_count slice of the original-id blocks from the pushed estimates
+ * and publishes it to every rank; after a second barrier hanf_shard_commit
+ * only totals them.  Without it every rank re-sums every block in its
+ * commit (n estimate gathers per rank per dense step).  A no-op for other
+ * engines. */
+hanf_status hanf_shard_reduce(hanf_engine* engine);
 /* Waits for this engine's enqueued device work (hanf_shard_compute's
  * pushes included): the step's barrier across the ranks comes after it. */
 hanf_status hanf_shard_wait(hanf_engine* engine);

@@ -320,6 +320,12 @@ class ShardEngine {
     check(hanf_shard_compute(h_));
     check(hanf_shard_wait(h_));
   }
+  // relabelled shards, optional, between compute's barrier and a second
+  // one: re-sum this rank's slice of the block sums (hanf_shard_reduce)
+  void reduce() {
+    check(hanf_shard_reduce(h_));
+    check(hanf_shard_wait(h_));
+  }
   IterationReport commit() {
     hanf_iteration_report r;
     check(hanf_shard_commit(h_, &r));

@@ -106,6 +106,7 @@ _SIGNATURES = {
     "hanf_shard_attach_local": [_P, POINTER(_P), c_uint32, c_uint32],
     "hanf_shard_detach": [_P],
     "hanf_shard_wait": [_P],
+    "hanf_shard_reduce": [_P],
     "hanf_distance_distribution": [POINTER(c_double), c_uint64, POINTER(c_double),
                                    POINTER(c_double), POINTER(c_double)],
     "hanf_effective_diameter": [POINTER(c_double), c_uint64, c_double, c_int32,

@@ -268,6 +268,10 @@ struct hanf_engine {
   // bitmap) instead of every block; all_dirty_commit = recompute them all
   uint64_t* dirty_derived = nullptr;
   bool all_dirty_commit = true;
+  // hanf_shard_reduce ran for this step: the ranks re-summed one slice of
+  // the original-id blocks each and published them; commit sums the inbox
+  bool reduced = false;
+  bool ever_reduced = false;  // (then the local block sums are only current in the slice)
   // relabelled engines keep estimates in row order (writes follow the task
   // order); finish_kernel gathers them through perm for the original-id
   // block sums.  HANF_EST_SCATTER=1: scatter to the original slot instead.
@@ -490,12 +494,14 @@ hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t
 // stream.  exact_sum: the total is redone on the host in the reference's
 // order (engine.hpp:115-117).
 hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute, uint64_t b0,
-                           uint64_t b1, bool in_step) {
+                           uint64_t b1, bool in_step, bool from_inbox = false) {
   hanf::FinishArgs f{};
   f.est = recompute ? (in_step && e->shard_relabel ? e->est_gen[1 - e->cur] : e->est) : nullptr;
   f.bits = bits;
   // peer-push shards total the inbox the peers published into
-  double* sums = in_step && e->attached && !e->shard_relabel ? e->inbox[1 - e->cur] : e->block_sums;
+  double* sums = in_step && e->attached && (!e->shard_relabel || from_inbox)
+                     ? e->inbox[1 - e->cur]
+                     : e->block_sums;
   f.block_sums = sums;
   f.out = e->reduce;
   f.n = e->n;
@@ -889,21 +895,38 @@ bool commit_recomputes(const hanf_engine* e) {
          (!sharded && hanf::fused_estimates(e->params.register_bits, e->params.registers));
 }
 
+// Relabelled shards: the bitmap of original-id blocks to re-sum for the
+// step being committed.  Few changes in the previous step (the tail): the
+// blocks of this step's changed rows (a scatter over the row bitmap);
+// dense steps: every block (all_dirty_commit; n estimate gathers anyway).
+hanf_status relabel_dirty(hanf_engine* e, const uint64_t** bits) {
+  const int ng = 1 - e->cur;
+  e->all_dirty_commit = 64 * e->last_count >= e->n || (e->ever_reduced && !e->reduced);
+  *bits = e->mod[ng];  // (all_dirty: only the count is read from it)
+  if (!e->all_dirty_commit) {
+    if (!e->dirty_derived) HANF_CUDA(palloc(&e->dirty_derived, e->blocks, e->stream));
+    HANF_CUDA(cudaMemsetAsync(e->dirty_derived, 0, sizeof(uint64_t) * e->blocks, e->stream));
+    HANF_CUDA(hanf::launch_derive_dirty(e->mod[ng], e->order, e->blocks, e->n, e->dirty_derived,
+                                        e->stream, &e->launches));
+    *bits = e->dirty_derived;
+  }
+  return HANF_OK;
+}
+
 hanf_status commit_enqueue(hanf_engine* e) {
   const int ng = 1 - e->cur;
   if (e->batch > 1) return batch_enqueue(e, e->mod[ng]);
+  if (e->shard_relabel && e->reduced) {
+    // the block sums are in the inbox (hanf_shard_reduce): totals only
+    e->reduced = false;
+    e->all_dirty_commit = false;
+    return finish_enqueue(e, e->mod[ng], false, 0, e->blocks, true, true);
+  }
   if (e->shard_relabel) {
-    // few changes in the previous step (the tail): mark the original-id
-    // blocks of this step's changed rows (a scatter over the row bitmap);
-    // dense steps recompute every block (n estimate gathers either way)
-    e->all_dirty_commit = 64 * e->last_count >= e->n;
-    if (!e->all_dirty_commit) {
-      if (!e->dirty_derived) HANF_CUDA(palloc(&e->dirty_derived, e->blocks, e->stream));
-      HANF_CUDA(cudaMemsetAsync(e->dirty_derived, 0, sizeof(uint64_t) * e->blocks, e->stream));
-      HANF_CUDA(hanf::launch_derive_dirty(e->mod[ng], e->order, e->blocks, e->n, e->dirty_derived,
-                                          e->stream, &e->launches));
-      return finish_enqueue(e, e->dirty_derived, true, 0, e->blocks, true);
-    }
+    const uint64_t* bits = nullptr;
+    const hanf_status rs = relabel_dirty(e, &bits);
+    if (rs != HANF_OK) return rs;
+    return finish_enqueue(e, bits, true, 0, e->blocks, true);
   }
   const hanf_status st = finish_enqueue(e, dirty_of(e, ng), commit_recomputes(e), 0, e->blocks, true);
   // (finish_kernel cleared mod[cur], the next step's mod_next)
@@ -1988,6 +2011,49 @@ hanf_status hanf_shard_attach_local(hanf_engine* e, hanf_engine* const* peers, u
     ++e->npeers;
   }
   e->attached = true;
+  return HANF_OK;
+}
+
+hanf_status hanf_shard_reduce(hanf_engine* e) {
+  if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (!e->shard_relabel || !e->attached || e->n == 0) return HANF_OK;  // nothing to share
+  HANF_CUDA(cudaSetDevice(e->device));
+  const int ng = 1 - e->cur;
+  const uint32_t G = e->cfg.shard_count;
+  const uint64_t per = e->blocks / G;                   // (n is a multiple of 64 G)
+  const uint64_t k = e->lo / (e->n / G);                // this shard's index
+  const uint64_t b0 = k * per, b1 = b0 + per;
+  const uint64_t* bits = nullptr;
+  e->reduced = true;  // (relabel_dirty: the slice protocol is in use)
+  e->ever_reduced = true;
+  hanf_status st = relabel_dirty(e, &bits);
+  if (st != HANF_OK) return st;
+  // this rank's slice of the block sums (the totals this launch also makes
+  // are discarded: the commit redoes them from the inbox)
+  hanf::FinishArgs f{};
+  f.est = e->est_gen[ng];
+  f.bits = bits;
+  f.block_sums = e->block_sums;
+  f.out = e->reduce;
+  f.n = e->n;
+  f.blocks = e->blocks;
+  f.b0 = b0;
+  f.b1 = b1;
+  f.perm = e->est_rows ? e->perm : nullptr;
+  f.all_dirty = e->all_dirty_commit ? 1 : 0;
+  HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
+  hanf::PublishArgs p{};
+  p.mod_next = nullptr;  // (bitmap words went with the compute)
+  p.block_sums = e->block_sums;
+  p.w0 = b0;
+  p.w1 = b1;
+  p.count = e->npeers;
+  for (uint32_t i = 0; i < e->npeers; ++i) {
+    p.peer_mod[i] = nullptr;
+    p.peer_sums[i] = reinterpret_cast<double*>(e->peer_base[i] + e->arena_off[4 + ng]);
+  }
+  p.peer_sums[e->npeers] = e->inbox[ng];
+  HANF_CUDA(hanf::launch_publish(p, e->stream, &e->launches));
   return HANF_OK;
 }
 

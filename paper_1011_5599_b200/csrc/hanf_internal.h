@@ -321,7 +321,7 @@ cudaError_t launch_segment_live(const uint64_t* mod_cur, const uint32_t* seg_min
 // Peer-push exchange: bitmap words and block sums [w0, w1) of this shard
 // into every peer's arena (and the block sums into the local inbox).
 struct PublishArgs {
-  const uint64_t* mod_next;
+  const uint64_t* mod_next;  // nullptr: block sums only
   const double* block_sums;  // nullptr: bitmap words only
   uint64_t w0, w1;
   uint64_t* peer_mod[kMaxPeers];

@@ -1045,8 +1045,10 @@ __global__ void publish_kernel(const PublishArgs a) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < words;
        i += stride) {
     const uint64_t w = a.w0 + i;
-    const uint64_t bits = a.mod_next[w];
-    for (uint32_t p = 0; p < a.count; ++p) a.peer_mod[p][w] = bits;
+    if (a.mod_next) {
+      const uint64_t bits = a.mod_next[w];
+      for (uint32_t p = 0; p < a.count; ++p) a.peer_mod[p][w] = bits;
+    }
     if (a.block_sums) {
       const double sum = a.block_sums[w];
       for (uint32_t p = 0; p < a.count; ++p) a.peer_sums[p][w] = sum;

@@ -321,6 +321,11 @@ class NfEngine:
     def shard_detach(self) -> None:
         check(lib().hanf_shard_detach(self._h))
 
+    def shard_reduce(self) -> None:
+        """hanf_shard_reduce: relabelled peer-push shards re-sum one slice of
+        the block sums each (between two barriers); a no-op otherwise."""
+        check(lib().hanf_shard_reduce(self._h))
+
     def shard_commit(self) -> IterationReport:
         r = _lib.IterationReportC()
         check(lib().hanf_shard_commit(self._h, ctypes.byref(r)))

@@ -107,6 +107,12 @@ class LocalCudaShard:
     def shard_detach(self) -> None:
         self.engine.shard_detach()
 
+    def needs_reduce(self) -> bool:
+        return bool(self.engine.device_buffers().relabelled)
+
+    def shard_reduce(self) -> None:
+        self.engine.shard_reduce()
+
     def wait_compute(self) -> None:
         self.stream.synchronize()
 
@@ -166,6 +172,7 @@ class ShardedNfEngine:
             raise ValueError(f"exchange must be 'collective' or 'peer', not {exchange!r}")
         self.exchange = exchange
         self.fallback = None
+        self.sliced = False
         if exchange == "peer":
             # every rank's arena description, then map the others' arenas;
             # if any rank cannot map a peer (no IPC / peer access between
@@ -190,6 +197,8 @@ class ShardedNfEngine:
                     local.close()
                     self.local = local = LocalCudaShard(
                         graph, cfg, lo, hi, torch.device("cuda", torch.cuda.current_device()))
+        self.sliced = (self.exchange == "peer" and hasattr(local, "needs_reduce")
+                       and local.needs_reduce())
         # changed-rows exchange (see the module docstring); packets hold at
         # most n/16 rows
         self.delta = delta and hasattr(local, "pack_rows")
@@ -256,6 +265,12 @@ class ShardedNfEngine:
             # peers' arenas: once every rank's compute is done, commit
             self.local.wait_compute()
             dist.barrier(group=self.group)
+            if self.sliced:
+                # relabelled shards: each rank re-sums 1/world of the blocks
+                # and publishes them, instead of every rank re-summing all
+                self.local.shard_reduce()
+                self.local.wait_compute()
+                dist.barrier(group=self.group)
             rep = self.local.shard_commit()
             self.last_modified = rep.modified
             return rep

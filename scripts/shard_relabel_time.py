@@ -47,10 +47,18 @@ def sharded(relabel, scatter="1"):
         e.set_timing(True)
     rows = []
     steps = int(os.environ.get("STEPS", "2"))  # 0: to stabilisation
+    red = [0.0] * G
+    sliced = relabel and os.environ.get("SLICED", "1") == "1"
     while True:
         for s in shards:
             s.shard_compute()
             s.wait_compute()
+        if sliced:  # hanf_shard_reduce: each shard re-sums 1/G of the blocks
+            for k, s in enumerate(shards):
+                t0 = time.perf_counter()
+                s.shard_reduce()
+                s.wait_compute()
+                red[k] += 1e3 * (time.perf_counter() - t0)
         reps = [s.shard_commit() for s in shards]
         rows.append(reps[0])
         if reps[0].modified == 0 or (steps and len(rows) >= steps):
@@ -58,8 +66,8 @@ def sharded(relabel, scatter="1"):
     if not steps:
         t = [e.timing() for e in engines]
         print(f"   whole run: {len(rows)} steps, union per shard {max(x['union_ms'] for x in t):.2f} ms, "
-              f"finish per shard {max(x['reduce_ms'] for x in t):.2f} ms (sums over the steps)",
-              flush=True)
+              f"finish per shard {max(x['reduce_ms'] for x in t):.2f} ms + sliced reduce "
+              f"{max(red):.2f} ms host-timed (sums over the steps)", flush=True)
     union = [e.timing()["union_ms"] / e.timing()["steps"] for e in engines]
     fin = [e.timing()["reduce_ms"] / e.timing()["steps"] for e in engines]
     arcs = [int(g.offsets()[hi]) - int(g.offsets()[lo]) for lo, hi in shard_ranges(g.num_nodes(), G)]

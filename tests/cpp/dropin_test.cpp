@@ -171,6 +171,7 @@ int main() {
       bool same = true;
       for (std::uint64_t t = 1; t <= n + 1 && same; ++t) {
         for (auto* s : shards) s->compute();
+        for (auto* s : shards) s->reduce();  // (a no-op: these shards are not relabelled)
         std::vector<hyperanf_b200::IterationReport> reps;
         for (auto* s : shards) reps.push_back(s->commit());
         const auto a = ref.step();

@@ -26,7 +26,7 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-def _run_local(hanf, g, cfg, world, skew, relabelled=False):
+def _run_local(hanf, g, cfg, world, skew, relabelled=False, reduce=False):
     import torch
     from paper_1011_5599_b200.sharded import LocalCudaShard, shard_ranges
     dev = torch.device("cuda", 0)
@@ -37,10 +37,17 @@ def _run_local(hanf, g, cfg, world, skew, relabelled=False):
         e.shard_attach_local(engines, k)
     values, mods = [shards[0].sum_estimates()], [g.num_nodes()]
     pending = None  # skew: shard 0's commit of step t after shard 1's compute of t+1
-    while True:
-        for sh in shards:
+    def computes(group):
+        for sh in group:
             sh.shard_compute()
             sh.wait_compute()
+        if reduce:  # (all computes of the step are done: the sliced block sums)
+            for sh in shards:
+                sh.shard_reduce()
+                sh.wait_compute()
+
+    while True:
+        computes(shards)
         reps = [sh.shard_commit() for sh in shards[:1]] if skew else []
         if skew:
             # shard 0 runs ahead into its next compute (writes the other
@@ -60,9 +67,7 @@ def _run_local(hanf, g, cfg, world, skew, relabelled=False):
         mods.append(reps[0].modified)
         if skew and pending:
             # the others now compute step t+1; shard 0 already did
-            for sh in shards[1:]:
-                sh.shard_compute()
-                sh.wait_compute()
+            computes(shards[1:])
             reps = [sh.shard_commit() for sh in shards]
             assert all(r.sum == reps[0].sum and r.modified == reps[0].modified for r in reps)
             pending = None
@@ -99,10 +104,11 @@ def test_peer_push_local(hanf, monkeypatch, b, env, world, skew):
         assert np.array_equal(c, ref)
 
 
-@pytest.mark.parametrize("b,world,skew,scatter", [(6, 2, False, "1"), (6, 4, True, "1"),
-                                                  (6, 4, True, "0"), (5, 2, True, "1"),
-                                                  (7, 4, False, "0")])
-def test_peer_push_relabelled_shards(hanf, monkeypatch, b, world, skew, scatter):
+@pytest.mark.parametrize("b,world,skew,scatter,reduce", [
+    (6, 2, False, "1", False), (6, 4, True, "1", False), (6, 4, True, "0", False),
+    (5, 2, True, "1", False), (7, 4, False, "0", False), (6, 4, False, "0", True),
+    (6, 4, True, "0", True), (5, 2, True, "1", True), (7, 4, False, "0", True)])
+def test_peer_push_relabelled_shards(hanf, monkeypatch, b, world, skew, scatter, reduce):
     """Relabelled shards (hanf_config.shard_count, degree order interleaved
     across the shards): rows live in another numbering on the device,
     estimates are pushed to the peers and every commit re-sums all
@@ -113,7 +119,7 @@ def test_peer_push_relabelled_shards(hanf, monkeypatch, b, world, skew, scatter)
     g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
     cfg = hanf.EngineConfig(bucket_bits=b, seed=42)
     values, mods, counters = _run_local(hanf, g, dataclasses.replace(cfg, shard_count=world),
-                                        world, skew, relabelled=True)
+                                        world, skew, relabelled=True, reduce=reduce)
     monkeypatch.setenv("HANF_RELABEL", "0")
     with hanf.NfEngine(g, cfg) as e:
         single = e.run_to_stabilisation()
@@ -229,7 +235,8 @@ def test_peer_push_config2_full_size(hanf, monkeypatch, relabel, world):
     g = hanf.gen_rmat(20, 16, 0.57, 0.19, 0.19, 1, 7, device=0)
     cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
     values, mods, counters = _run_local(hanf, g, dataclasses.replace(cfg, shard_count=world),
-                                        world, False, relabelled=relabel == "1")
+                                        world, False, relabelled=relabel == "1",
+                                        reduce=relabel == "1")
     monkeypatch.setenv("HANF_RELABEL", "0")
     with hanf.NfEngine(g, cfg) as e:
         single = e.run_to_stabilisation()
