@@ -309,7 +309,7 @@ struct hanf_engine {
     uint32_t uses = 0;  // captured on the third use: capture + instantiate +
                         // destroy cost more than a one-shot run's few replays
   };
-  StepGraph graphs[2][4][2];
+  StepGraph graphs[2][5][2];
   uint64_t* summ = nullptr;   // mode 3 summary bitmap (see create)
   unsigned long long* pack_count = nullptr;  // hanf_shard_pack scratch
   uint32_t summ_shift = 6;
@@ -318,6 +318,11 @@ struct hanf_engine {
   uint64_t summ_bits = 0;
   bool use_graphs = true;
   uint32_t* seg_live = nullptr;  // skip sweeps over segmented tasks (TaskBuild::seg_shift)
+  // scan-signalled worklist steps (mode 4): TOS row -> warp task; allowed
+  // on unrelabelled single-chunk engines (HANF_SCAN=0 off, =1 every skip step)
+  uint32_t* row_task = nullptr;
+  bool scan_ok = false;
+  bool force_scan = false;
   // create pipelined iteration 1 with the arcs upload: the next generation,
   // its bitmap and estimates already hold step 1's sweep (hanf_create)
   bool pre_step = false;
@@ -417,6 +422,7 @@ struct hanf_engine {
       pfree(dirty[1], stream);
       pfree(lens, stream);
       pfree(seg_live, stream);
+      pfree(row_task, stream);
       pfree(dirty_derived, stream);
       hanf::free_tasks_device(&tasks, stream);
       if (cudaStreamSynchronize(stream) == cudaSuccess)
@@ -660,6 +666,11 @@ int step_mode(const hanf_engine* e) {
   // many steps would have used it, so short runs never pay for it
   if (sparse_wanted(e) && (e->tr_off || e->sparse_wanted_steps >= e->sparse_after)) return 2;
   if (2 * e->last_count >= e->n) return 0;
+  // very few changed counters and no transpose: one scan of the TOS
+  // signals the nodes with a changed successor, and only they are redone
+  if (e->scan_ok && !e->tr_off && e->stale_valid &&
+      (e->force_scan || 256 * e->last_count < e->n))
+    return 4;
   // few changed counters: filter the per-arc bitmap probes through the
   // L1-resident summary first (most probes then never reach L2)
   return e->force_summary || 16 * e->last_count < e->summ_bits ? 3 : 1;
@@ -671,6 +682,8 @@ void note_step(hanf_engine* e) {
 
 // Builds the transpose and worklist scratch on first use (outside any
 // graph capture).
+hanf_status ensure_worklist_scratch(hanf_engine* e);
+
 hanf_status ensure_sparse(hanf_engine* e) {
   if (e->tr_off) return HANF_OK;
   cudaStream_t s = e->stream;
@@ -690,16 +703,30 @@ hanf_status ensure_sparse(hanf_engine* e) {
   }
   HANF_CUDA(hanf::build_transpose_device(e->csr_off, e->csr_succ, e->lo, e->hi, e->succ_base, e->n,
                                          s, &e->tr_off, &e->tr_succ, &e->launches));
-  HANF_CUDA(palloc(&e->sig, e->blocks, s));
   // one signal task per kSignalChunk predecessors of a modified node
   HANF_CUDA(palloc(&e->mod_list, e->n + e->shard_arcs / hanf::kSignalChunk + 64, s));
-  HANF_CUDA(palloc(&e->work, e->hi - e->lo + 1, s));
-  HANF_CUDA(palloc(&e->hub_tasks, e->tasks.num_chunks + 1ull, s));
-  HANF_CUDA(hanf::build_hub_index(e->tasks.hub_nodes, e->tasks.num_hubs, e->n, s, &e->hub_index,
-                                  &e->launches));
-  HANF_CUDA(palloc(&e->lens, 3, s));
+  return ensure_worklist_scratch(e);
+}
+
+// The worklist stages' scratch (shared by modes 2 and 4).
+hanf_status ensure_worklist_scratch(hanf_engine* e) {
+  cudaStream_t s = e->stream;
+  if (!e->sig) {
+    HANF_CUDA(palloc(&e->sig, e->blocks, s));
+    HANF_CUDA(palloc(&e->work, e->hi - e->lo + 1, s));
+    HANF_CUDA(palloc(&e->hub_tasks, e->tasks.num_chunks + 1ull, s));
+    HANF_CUDA(hanf::build_hub_index(e->tasks.hub_nodes, e->tasks.num_hubs, e->n, s, &e->hub_index,
+                                    &e->launches));
+    HANF_CUDA(palloc(&e->lens, 3, s));
+  }
   HANF_CUDA(cudaStreamSynchronize(s));
   return HANF_OK;
+}
+
+// Mode 4's TOS row -> task map and the worklist scratch, on first use.
+hanf_status ensure_scan(hanf_engine* e) {
+  if (!e->row_task) HANF_CUDA(hanf::build_row_task(e->tasks, e->stream, &e->row_task, &e->launches));
+  return ensure_worklist_scratch(e);
 }
 
 // Peer-push exchange: generation ng of every attached peer.
@@ -746,7 +773,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   return a;
 }
 
-hanf_status compute_sparse(hanf_engine* e) {
+hanf_status compute_sparse(hanf_engine* e, bool scan = false) {
   const int g = e->cur, ng = 1 - e->cur;
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
   hanf::SparseArgs a{};
@@ -780,8 +807,17 @@ hanf_status compute_sparse(hanf_engine* e) {
   a.blocks = e->blocks;
   a.hi = e->hi;
   a.peers = peer_rows(e, ng);
-  HANF_CUDA(hanf::launch_sparse_step(a, w0, w1, e->params.register_bits, e->params.registers,
-                                     e->stream, &e->launches));
+  if (scan) {
+    HANF_CUDA(hanf::launch_summary(e->mod[g], e->blocks + 1, e->summ_shift, e->summ_bits, e->summ,
+                                   e->stream, &e->launches));
+    HANF_CUDA(hanf::launch_scan_step(a, e->tasks, e->row_task, e->summ, e->summ_shift,
+                                     static_cast<uint32_t>((e->summ_bits + 63) / 64), w0, w1,
+                                     e->params.register_bits, e->params.registers, e->stream,
+                                     &e->launches));
+  } else {
+    HANF_CUDA(hanf::launch_sparse_step(a, w0, w1, e->params.register_bits, e->params.registers,
+                                       e->stream, &e->launches));
+  }
   if (e->tasks.num_chunks) {
     // worklist hubs: their chunk tasks through the dense kernel (skipping
     // unmodified successors), chunk partials folded by the usual ticket
@@ -841,8 +877,8 @@ hanf_status compute_shard(hanf_engine* e) {
   if (e->dirty[ng])  // unsharded relabelling: the whole original-id bitmap
     HANF_CUDA(cudaMemsetAsync(e->dirty[ng], 0, sizeof(uint64_t) * e->blocks, e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
-  if (step_mode(e) == 2 && e->tr_off) {
-    const hanf_status st = compute_sparse(e);
+  if ((step_mode(e) == 2 && e->tr_off) || step_mode(e) == 4) {
+    const hanf_status st = compute_sparse(e, step_mode(e) == 4);
     if (st != HANF_OK) return st;
     if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
     if (e->lo != 0 || e->hi != e->n) {
@@ -979,8 +1015,8 @@ hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
 hanf_status step_enqueue(hanf_engine* e) {
   note_step(e);
   const int mode = step_mode(e);
-  if (mode == 2) {
-    const hanf_status st = ensure_sparse(e);
+  if (mode == 2 || mode == 4) {
+    const hanf_status st = mode == 2 ? ensure_sparse(e) : ensure_scan(e);
     if (st != HANF_OK) return st;
   }
   if (!e->use_graphs || e->timing || e->pre_step) {
@@ -1513,6 +1549,17 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     }
     if (seg_skip && e->tasks.seg_shift < 32)
       HANF_TRY(palloc(&e->seg_live, e->tasks.num_segs, s));
+    {  // mode 4 (scan-signalled worklist; opt-in HANF_SCAN=1, every skip step):
+       // unrelabelled, unsegmented, single chunk.  Measured on config 2's
+       // tail it loses to the summary skip sweep (0.090 against 0.046 ms):
+       // its ~7 small launches cost more than one sweep (profiles/r01_sparse.md)
+      const char* sc = std::getenv("HANF_SCAN");
+      const bool forced = sc && sc[0] == '1';
+      e->scan_ok = forced && K == 1 && !e->relabel && !seg_skip && !e->tma && n > 0 &&
+                   hanf::sparse_supported(params.register_bits, params.registers) &&
+                   hanf::fused_estimates(params.register_bits, params.registers);
+      e->force_scan = e->scan_ok;
+    }
     if (scatter) {
       phase("tasks");
       HANF_TRY(hanf::scatter_fill_prepare(&e->tasks, lo, hi, n, s, &e->launches));
@@ -1842,8 +1889,8 @@ hanf_status hanf_shard_compute(hanf_engine* e) {
   if (e->n == 0) return HANF_OK;
   HANF_CUDA(cudaSetDevice(e->device));
   note_step(e);
-  if (step_mode(e) == 2) {
-    const hanf_status sst = ensure_sparse(e);
+  if (step_mode(e) == 2 || step_mode(e) == 4) {
+    const hanf_status sst = step_mode(e) == 2 ? ensure_sparse(e) : ensure_scan(e);
     if (sst != HANF_OK) return sst;
   }
   return compute_local(e);

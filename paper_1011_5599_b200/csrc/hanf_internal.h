@@ -196,6 +196,14 @@ cudaError_t build_transpose_device(const uint64_t* d_off, const uint32_t* d_succ
 cudaError_t launch_sparse_step(const SparseArgs& a, uint64_t w0, uint64_t w1, uint32_t register_bits,
                                uint32_t registers, cudaStream_t s, uint64_t* launches);
 bool sparse_supported(uint32_t register_bits, uint32_t registers);
+// Worklist step signalled by one scan of the TOS instead of a transpose
+// (tail steps of unrelabelled engines; hanf_sparse.cu scan_signal_kernel):
+// row_task = build_row_task's map from TOS row to warp task.
+cudaError_t build_row_task(const TaskBuild& t, cudaStream_t s, uint32_t** out, uint64_t* launches);
+cudaError_t launch_scan_step(const SparseArgs& a, const TaskBuild& t, const uint32_t* row_task,
+                             const uint64_t* summ, uint32_t summ_shift, uint32_t summ_words,
+                             uint64_t w0, uint64_t w1, uint32_t register_bits, uint32_t registers,
+                             cudaStream_t s, uint64_t* launches);
 
 struct UnionArgs {
   const uint32_t* tos;       // task-ordered successor ids

@@ -306,6 +306,7 @@ def test_config2_scale(hanf, port):
                                          (5, {}, False), (8, {}, False), (6, {}, True),
                                          (5, {"HANF_SPARSE": "1"}, True), (8, {}, True),
                                          (6, {"HANF_SEGMENTS": "1"}, True),
+                                         (6, {"HANF_SCAN": "1"}, True), (5, {"HANF_SCAN": "1"}, False),
                                          (7, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"}, False)])
 def test_sharded_engines_exchange(hanf, port, monkeypatch, b, env, delta):
     """The shard ABI (hanf_shard_compute / device buffers / hanf_shard_commit)
@@ -394,7 +395,8 @@ def test_worklist_step_parity(hanf, port, monkeypatch):
                                  {"HANF_RELABEL": "1", "HANF_PITCH": "0"},
                                  {"HANF_SUMMARY": "1"}, {"HANF_SUMMARY": "1", "HANF_RELABEL": "1"},
                                  {"HANF_SEGMENTS": "1"}, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"},
-                                 {"HANF_SEGMENTS": "1", "HANF_SPARSE": "1"}])
+                                 {"HANF_SEGMENTS": "1", "HANF_SPARSE": "1"},
+                                 {"HANF_SCAN": "1"}, {"HANF_SCAN": "1", "HANF_PITCH": "0"}])
 def test_row_pitch_and_gather_variants(hanf, port, monkeypatch, env):
     """Padded rows (aligned 256-bit gathers), unpadded rows and the
     alternative gather kernels change time only: counters read back in the
@@ -435,6 +437,16 @@ def test_golden_trace_segmented(hanf, traces, idx, monkeypatch):
     the segments with no modified row in reach) change time only: every
     golden iteration bit-exact (HANF_SEGMENTS=1 forces them on)."""
     monkeypatch.setenv("HANF_SEGMENTS", "1")
+    test_golden_trace(hanf, traces, idx)
+
+
+@pytest.mark.parametrize("idx", range(28))
+def test_golden_trace_scan_worklist(hanf, traces, idx, monkeypatch):
+    """Scan-signalled worklist steps (one pass over the TOS marks the nodes
+    with a changed successor; on by default for tail steps of unrelabelled
+    graphs from 2^22 arcs, forced here for every skip step): every golden
+    iteration bit-exact."""
+    monkeypatch.setenv("HANF_SCAN", "1")
     test_golden_trace(hanf, traces, idx)
 
 

@@ -87,7 +87,8 @@ def _run_local(hanf, g, cfg, world, skew, relabelled=False, reduce=False):
     (6, {}, 2, False), (6, {}, 3, False), (6, {}, 2, True), (6, {"HANF_SPARSE": "1"}, 2, False),
     (6, {"HANF_SPARSE": "1"}, 3, True), (5, {}, 2, True), (8, {}, 2, False), (7, {}, 3, False),
     (6, {"HANF_SEGMENTS": "1"}, 3, True), (5, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"}, 2, False),
-    (6, {"HANF_SCATTER_FILL": "1"}, 3, False)])
+    (6, {"HANF_SCATTER_FILL": "1"}, 3, False), (6, {"HANF_SCAN": "1"}, 3, True),
+    (7, {"HANF_SCAN": "1"}, 2, False)])
 def test_peer_push_local(hanf, monkeypatch, b, env, world, skew):
     """Attached shard engines of one process: bit-exact with one engine, with
     the worklist step, the padded W = 3 rows, m = 128 and a multi-chunk layout."""
