@@ -163,10 +163,13 @@ class PinnedCache {
   void* get(size_t bytes) {
     {
       std::lock_guard<std::mutex> lock(mu_);
+      // best fit, but only among blocks at most 2x the request: a 16-byte
+      // report must not pin down a 32 MB block
       auto it = free_.lower_bound(bytes);
-      if (it != free_.end()) {
+      if (it != free_.end() && it->first <= 2 * std::max<size_t>(bytes, 4096)) {
         void* p = it->second;
         sizes_[p] = it->first;
+        cached_ -= it->first;
         free_.erase(it);
         return p;
       }
@@ -181,16 +184,31 @@ class PinnedCache {
     sizes_[p] = bytes;
     return p;
   }
+  // Returns a block.  Cached page-locked memory is capped: beyond kCap the
+  // block is freed (cudaFreeHost synchronises, so only large, rare blocks
+  // take that path; small report blocks stay cached).
   void put(void* p) {
     if (!p) return;
-    std::lock_guard<std::mutex> lock(mu_);
-    free_.emplace(sizes_[p], p);
+    size_t bytes;
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      bytes = sizes_[p];
+      if (cached_ + bytes <= kCap) {
+        free_.emplace(bytes, p);
+        cached_ += bytes;
+        return;
+      }
+      sizes_.erase(p);
+    }
+    cudaFreeHost(p);
   }
 
  private:
   std::mutex mu_;
+  static constexpr size_t kCap = size_t(256) << 20;
   std::multimap<size_t, void*> free_;
   std::map<void*, size_t> sizes_;
+  size_t cached_ = 0;
 };
 PinnedCache& pinned() {
   static PinnedCache* c = new PinnedCache();  // never destroyed: outlives engines
@@ -1193,8 +1211,10 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     }
   }
 
+  cudaStream_t helper = nullptr;  // upload stream: idle before any buffer is freed
   auto bail = [&](hanf_status s) {
     const std::string msg = g_last_error;
+    if (helper) cudaStreamSynchronize(helper);
     delete e;
     g_last_error = msg;
     return s;
@@ -1374,12 +1394,15 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     uint64_t* d_off = nullptr;
     uint32_t* d_succ = nullptr;
     HANF_TRY(palloc(&d_off, up_hi - up_lo + 1, s));
+    e->csr_off = d_off;  // owned by the engine at once: error paths free them
     HANF_TRY(palloc(&d_succ, a1 - a0, s));
+    e->csr_succ = d_succ;
     // offsets first on the engine stream; the arcs follow on a helper
     // stream while the engine stream seeds and sorts by degree (only the
     // TOS fill waits for them)
     cudaStream_t s2 = nullptr;
     HANF_TRY(streams().get(cfg.device, &s2));
+    helper = s2;
     cudaEvent_t ev_off = nullptr, ev_arcs = nullptr;
     struct UploadGuard {  // the helper stream is idle again before anything is freed
       int dev;
@@ -1710,6 +1733,7 @@ void hanf_destroy(hanf_engine* e) { delete e; }
 
 hanf_status hanf_reset(hanf_engine* e) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (e->n == 0) {
     e->t = 0;
     return HANF_OK;
@@ -1732,6 +1756,7 @@ uint64_t get_le(const unsigned char* p, int bytes) {
 // hll.hpp:275-286: "HCA1", u32 b, u32 r, u64 n, u64 seed, n*W words (LE).
 hanf_status hanf_save_counters(hanf_engine* e, const char* path) {
   if (!e || !path) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: no single counter array");
   std::vector<uint64_t> words(e->n * e->words);
   if (e->n) {
@@ -1756,6 +1781,7 @@ hanf_status hanf_save_counters(hanf_engine* e, const char* path) {
 // hll.hpp:288-303 load_counters, into a running engine (resume).
 hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t iteration) {
   if (!e || !path) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: no single counter array");
   std::FILE* f = std::fopen(path, "rb");
   if (!f) return fail(HANF_IO_ERROR, std::string("cannot open: ") + path);
@@ -1886,6 +1912,7 @@ hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
 
 hanf_status hanf_shard_compute(hanf_engine* e) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (e->n == 0) return HANF_OK;
   HANF_CUDA(cudaSetDevice(e->device));
   note_step(e);
@@ -1930,6 +1957,7 @@ hanf_status hanf_shard_unpack(hanf_engine* e, const uint32_t* ids, const uint64_
 
 hanf_status hanf_shard_commit(hanf_engine* e, hanf_iteration_report* rep) {
   if (!e || !rep) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (e->n == 0) {
     rep->sum = 0.0;
     rep->modified = 0;
@@ -2122,6 +2150,7 @@ hanf_status hanf_shard_detach(hanf_engine* e) {
 hanf_status hanf_run_to_stabilisation(hanf_engine* e, double* values, uint64_t* modified,
                                       uint64_t capacity, uint64_t* length, double* wall) {
   if (!e || !length) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: use hanf_run_batch");
   const auto start = std::chrono::steady_clock::now();
   *length = 0;
@@ -2224,6 +2253,7 @@ hanf_status hanf_estimate_nf(const hanf_graph_view* g, const hanf_config* cfg, d
 
 hanf_status hanf_read_counters(hanf_engine* e, uint64_t first, uint64_t count, uint64_t* dst) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (first > e->n || count > e->n - first)
     return fail(HANF_OUT_OF_RANGE, "counter index out of range");
   if (count == 0) return HANF_OK;
