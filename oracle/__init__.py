@@ -114,6 +114,12 @@ class Port:
                                                POINTER(c_double), POINTER(c_double)]
         L.or_effective_diameter.argtypes = [POINTER(c_double), c_uint64, c_double, c_int,
                                             POINTER(c_double)]
+        L.or_gen_rmat.argtypes = [c_uint32, c_uint32, c_double, c_double, c_double, c_uint64,
+                                  c_uint64, ctypes.c_uint, POINTER(_Graph)]
+        L.or_counter_digest.restype = c_uint64
+        L.or_counter_digest.argtypes = [POINTER(c_uint64), c_uint64, ctypes.c_uint, ctypes.c_uint]
+        L.or_csr_digest.restype = c_uint64
+        L.or_csr_digest.argtypes = [POINTER(c_uint64), POINTER(c_uint32), c_uint64]
         self.L = L
 
     # sketch primitives ------------------------------------------------------
@@ -169,6 +175,29 @@ class Port:
             raise ValueError("bad generator arguments")
         return self._take(g)
 
+    def gen_rmat(self, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, permute_seed=7,
+                 threads=None):
+        """BASELINE configs 2/5 R-MAT (hanf_oracle_gen.c), multi-threaded.
+        Returns (n, offsets, succ); the arrays own the C buffers (no copy)."""
+        g = _Graph()
+        rc = self.L.or_gen_rmat(scale, edge_factor, a, b, c, seed, permute_seed,
+                                threads or os.cpu_count() or 1, ctypes.byref(g))
+        if rc:
+            raise (MemoryError if rc == -2 else ValueError)("or_gen_rmat failed")
+        return g.n, _owned(self, g, g.offsets, g.n + 1), _owned(self, g, g.succ, g.arcs)
+
+    def counter_digest(self, words, n, W, threads=None):
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        assert w.size >= n * W
+        return int(self.L.or_counter_digest(_u64p(w), n, W, threads or os.cpu_count() or 1))
+
+    def csr_digest(self, n, offsets, succ):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        succ = np.ascontiguousarray(succ, dtype=np.uint32)
+        if succ.size == 0:
+            succ = np.zeros(1, dtype=np.uint32)
+        return int(self.L.or_csr_digest(_u64p(offsets), _u32p(succ), n))
+
     def from_edges(self, n, src, dst):
         src = np.ascontiguousarray(src, dtype=np.uint32)
         dst = np.ascontiguousarray(dst, dtype=np.uint32)
@@ -217,6 +246,43 @@ class Port:
                                         ctypes.byref(out)):
             raise ValueError("bad input")
         return out.value
+
+
+class _CBuffers:
+    """Frees an or_graph's malloc'd arrays when the last view goes."""
+
+    def __init__(self, port, g):
+        self.port, self.g = port, g
+        self.refs = 0
+
+    def release(self):
+        self.refs -= 1
+        if self.refs == 0:
+            self.port.L.or_graph_free(ctypes.byref(self.g))
+
+
+class _OwnedArray(np.ndarray):
+    def __del__(self):
+        owner = getattr(self, "_owner", None)
+        if owner is not None:
+            self._owner = None
+            owner.release()
+
+
+_owners = {}
+
+
+def _owned(port, g, ptr, count):
+    key = ctypes.addressof(g)
+    owner = _owners.get(key)
+    if owner is None or owner.g is not g:
+        owner = _owners[key] = _CBuffers(port, g)
+    if count == 0:
+        return np.zeros(0, dtype=np.uint32 if ptr._type_ is c_uint32 else np.uint64)
+    arr = np.ctypeslib.as_array(ptr, shape=(int(count),)).view(_OwnedArray)
+    arr._owner = owner
+    owner.refs += 1
+    return arr
 
 
 class PortEngine:
@@ -326,12 +392,32 @@ class Ref:
                                              POINTER(c_double)]
         L.ref_exact_nf.argtypes = [vp, POINTER(c_uint64), c_uint64, POINTER(c_uint64)]
         L.ref_hardware_threads.restype = ctypes.c_uint
+        L.ref_graph_from_sorted_csr.restype = vp
+        L.ref_graph_from_sorted_csr.argtypes = [c_uint64, POINTER(c_uint64), POINTER(c_uint32)]
+        L.ref_engine_step_sample.restype = c_double
+        L.ref_engine_step_sample.argtypes = [vp, c_uint64, c_uint64, ctypes.c_uint,
+                                             POINTER(c_uint64), POINTER(c_double),
+                                             POINTER(c_uint64)]
+        L.ref_engine_next_counters.restype = POINTER(c_uint64)
+        L.ref_engine_next_counters.argtypes = [vp, POINTER(c_uint64)]
         self.L = L
 
     def graph(self, n, offsets, succ):
         offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
         succ = np.ascontiguousarray(succ, dtype=np.uint32)
         return RefGraph(self, self.L.ref_graph_from_csr(n, _u64p(offsets), _u32p(succ)))
+
+    def graph_sorted(self, n, offsets, succ):
+        """hyperanf::Graph from a sorted, deduplicated CSR in O(a): the same
+        object Graph::from_edges builds, without its std::sort."""
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        succ = np.ascontiguousarray(succ, dtype=np.uint32)
+        if succ.size == 0:
+            succ = np.zeros(1, dtype=np.uint32)
+        h = self.L.ref_graph_from_sorted_csr(n, _u64p(offsets), _u32p(succ))
+        if not h:
+            raise ValueError("CSR rows are not sorted / deduplicated / in range")
+        return RefGraph(self, h)
 
     def gen_uniform_random(self, n, d, seed):
         return RefGraph(self, self.L.ref_gen_uniform_random(n, d, seed))
@@ -434,6 +520,21 @@ class RefEngine:
 
     def iteration(self):
         return self.L.ref_engine_iteration(self.h)
+
+    def step_sample(self, lo, hi, threads):
+        """NfEngine::step's per-node body over [lo, hi) plus the block
+        re-sum (ref_shim.cpp ref_engine_step_sample); no swap.
+        Returns (seconds, arcs, block sum, changed)."""
+        arcs, s, ch = c_uint64(), c_double(), c_uint64()
+        secs = self.L.ref_engine_step_sample(self.h, lo, hi, threads, ctypes.byref(arcs),
+                                             ctypes.byref(s), ctypes.byref(ch))
+        return secs, arcs.value, s.value, ch.value
+
+    def next_counters(self):
+        wc = c_uint64()
+        p = self.L.ref_engine_next_counters(self.h, ctypes.byref(wc))
+        return np.ctypeslib.as_array(p, shape=(wc.value,)).copy() if wc.value else \
+            np.zeros(0, dtype=np.uint64)
 
     def save_counters(self, path):
         """The reference's own HCA1 writer (hll.hpp:275-286)."""

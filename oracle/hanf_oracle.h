@@ -125,6 +125,17 @@ int or_distance_distribution(const double* nf, uint64_t len, double* mean,
 int or_effective_diameter(const double* nf, uint64_t len, double alpha,
                           int interpolated, double* out);
 
+/* ---- hanf_oracle_gen.c (multi-threaded; results thread-independent) -- */
+/* BASELINE configs 2/5 R-MAT as the B200 package defines it (hanf_rng.h):
+ * 2^scale nodes, edge_factor*2^scale draws, Feistel-permuted ids,
+ * self-loops dropped, rows sorted + deduplicated.  -1 bad args, -2 OOM. */
+int or_gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                uint64_t seed, uint64_t permute_seed, unsigned threads, or_graph* out);
+/* order-independent digest of n counters of W words (reference packing) */
+uint64_t or_counter_digest(const uint64_t* words, uint64_t n, unsigned W, unsigned threads);
+/* digest of a CSR (n+1 offsets, offsets[n] successors) */
+uint64_t or_csr_digest(const uint64_t* offsets, const uint32_t* succ, uint64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,36 @@
 using namespace hyperanf;
 
 namespace {
+// Access to the reference's private members without editing its headers:
+// an explicit template instantiation may name private members (C++
+// [temp.spec]), and the friend it defines hands the member pointer out.
+// Used for two things only: building a hyperanf::Graph from an already
+// sorted, deduplicated CSR in O(a) (from_edges' std::sort of 4.3 B pairs
+// takes minutes at config 5), and running NfEngine::step's per-node body
+// over a node range (ref_engine_step_sample).
+template <typename Tag, typename Tag::type M>
+struct Rob {
+  friend typename Tag::type get(Tag) { return M; }
+};
+#define HANF_ROB(Name, Class, Type, Member)                   \
+  struct Name {                                               \
+    using type = Type Class::*;                               \
+    friend type get(Name);                                    \
+  };                                                          \
+  template struct Rob<Name, &Class::Member>;
+HANF_ROB(GraphN, Graph, std::uint64_t, n_)
+HANF_ROB(GraphOff, Graph, std::vector<std::uint64_t>, offsets_)
+HANF_ROB(GraphSucc, Graph, std::vector<std::uint32_t>, succ_)
+HANF_ROB(EngGraph, NfEngine, const Graph*, graph_)
+HANF_ROB(EngCfg, NfEngine, EngineConfig, cfg_)
+HANF_ROB(EngKernel, NfEngine, PackedMax, kernel_)
+HANF_ROB(EngCur, NfEngine, CounterArray, current_)
+HANF_ROB(EngNext, NfEngine, CounterArray, next_)
+HANF_ROB(EngParams, NfEngine, SketchParams, params_)
+HANF_ROB(EngMod, NfEngine, std::vector<std::uint8_t>, modified_)
+HANF_ROB(EngNextMod, NfEngine, std::vector<std::uint8_t>, next_modified_)
+#undef HANF_ROB
+
 int status_of(const std::exception_ptr& ep) {
   try {
     std::rethrow_exception(ep);
@@ -66,6 +96,27 @@ void* ref_graph_from_csr(uint64_t n, const uint64_t* offsets, const uint32_t* su
     for (uint64_t i = offsets[v]; i < offsets[v + 1]; ++i)
       edges.emplace_back(static_cast<uint32_t>(v), succ[i]);
   return new Graph(Graph::from_edges(n, std::move(edges)));
+}
+// The same Graph as from_edges would build from this CSR, without the
+// sort: the caller guarantees rows sorted and deduplicated with ids < n
+// (checked here in O(a)).  nullptr if the CSR is not in that form.
+void* ref_graph_from_sorted_csr(uint64_t n, const uint64_t* offsets, const uint32_t* succ) {
+  try {
+    if (offsets[0] != 0) return nullptr;
+    const uint64_t a = offsets[n];
+    for (uint64_t v = 0; v < n; ++v) {
+      if (offsets[v + 1] < offsets[v]) return nullptr;
+      for (uint64_t i = offsets[v]; i < offsets[v + 1]; ++i)
+        if (succ[i] >= n || (i > offsets[v] && succ[i] <= succ[i - 1])) return nullptr;
+    }
+    Graph* g = new Graph();
+    g->*get(GraphN{}) = n;
+    (g->*get(GraphOff{})).assign(offsets, offsets + n + 1);
+    (g->*get(GraphSucc{})).assign(succ, succ + a);
+    return g;
+  } catch (...) {
+    return nullptr;
+  }
 }
 void* ref_gen_uniform_random(uint64_t n, double d, uint64_t seed) {
   try { return new Graph(gen_uniform_random(n, d, seed)); } catch (...) { return nullptr; }
@@ -150,6 +201,84 @@ double ref_engine_timed_step(void* e, double* sum, uint64_t* modified) {
   *sum = rep.sum;
   *modified = rep.modified;
   return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// A bounded sample of one dense iteration of the reference engine: the
+// per-node body of NfEngine::step (engine.hpp:157-184, non-systolic,
+// in-memory) over nodes [lo, hi) only, dealt to `threads` workers by the
+// reference's own parallel_chunks (parallel.hpp:16-48, chunk task_size),
+// followed by the per-block re-sum of sum_estimates (engine.hpp:100-112)
+// over the blocks of [lo, hi) on the freshly written counters.  It writes
+// next_ / next_modified_ of those nodes and never swaps, so repeated
+// samples all start from the same generation (the bench samples iteration
+// 1 from the seeded state).  Returns the seconds (steady_clock, as
+// tests/acceptance.cpp:438-443), and the sampled arcs and block sum.
+double ref_engine_step_sample(void* ep, uint64_t lo, uint64_t hi, unsigned threads,
+                              uint64_t* arcs_out, double* sum_out, uint64_t* changed_out) {
+  NfEngine* e = static_cast<NfEngine*>(ep);
+  const Graph& g = *(e->*get(EngGraph{}));
+  const EngineConfig& cfg = e->*get(EngCfg{});
+  const PackedMax& kernel = e->*get(EngKernel{});
+  CounterArray& cur = e->*get(EngCur{});
+  CounterArray& next = e->*get(EngNext{});
+  const SketchParams& params = e->*get(EngParams{});
+  const std::vector<std::uint8_t>& modified = e->*get(EngMod{});
+  std::vector<std::uint8_t>& next_modified = e->*get(EngNextMod{});
+  const uint64_t n = g.num_nodes();
+  if (hi > n) hi = n;
+  if (lo >= hi) {
+    *arcs_out = 0;
+    *sum_out = 0.0;
+    *changed_out = 0;
+    return 0.0;
+  }
+  const unsigned words = params.words_per_counter();
+  if (next.size() != n) next = CounterArray(params, n);      // engine.hpp:126
+  if (next_modified.size() != n) next_modified.assign(n, 0);  // engine.hpp:127
+  if (threads == 0) threads = 1;
+  std::vector<std::vector<std::uint64_t>> scratch(threads, std::vector<std::uint64_t>(words));
+  constexpr uint64_t kBlock = 64;
+  const uint64_t b0 = lo / kBlock, b1 = (hi + kBlock - 1) / kBlock;
+  std::vector<double> block_sums(b1 - b0, 0.0);
+  const auto t0 = std::chrono::steady_clock::now();
+  parallel_chunks(hi - lo, threads, cfg.task_size,
+                  [&](std::uint64_t clo, std::uint64_t chi, unsigned id) {
+    for (std::uint64_t v = lo + clo; v < lo + chi; ++v) {
+      std::uint64_t* dst = next.counter(v).data();
+      std::memcpy(dst, cur.counter(v).data(), words * sizeof(std::uint64_t));
+      bool changed = false;
+      for (std::uint32_t succ : g.successors(v)) {
+        if (cfg.track_modified && !modified[succ]) continue;
+        changed |= kernel.max_into(dst, cur.counter(succ).data(), scratch[id].data());
+      }
+      next_modified[v] = changed ? 1 : 0;
+    }
+  });
+  parallel_chunks(b1 - b0, threads, 16, [&](std::uint64_t blo, std::uint64_t bhi, unsigned) {
+    for (std::uint64_t b = b0 + blo; b < b0 + bhi; ++b) {
+      const std::uint64_t first = std::max<std::uint64_t>(b * kBlock, lo);
+      const std::uint64_t last = std::min<std::uint64_t>((b + 1) * kBlock, hi);
+      double sum = 0.0;
+      for (std::uint64_t i = first; i < last; ++i) sum += next.estimate(i);
+      block_sums[b - b0] = sum;
+    }
+  });
+  const auto t1 = std::chrono::steady_clock::now();
+  double total = 0.0;
+  for (double s : block_sums) total += s;
+  uint64_t changed = 0;
+  for (uint64_t v = lo; v < hi; ++v) changed += next_modified[v];
+  *arcs_out = g.offsets()[hi] - g.offsets()[lo];
+  *sum_out = total;
+  *changed_out = changed;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+// next_ after samples (the sampled rows are the step's rows)
+const uint64_t* ref_engine_next_counters(const void* ep, uint64_t* word_count) {
+  const NfEngine* e = static_cast<const NfEngine*>(ep);
+  const CounterArray& c = const_cast<NfEngine*>(e)->*get(EngNext{});
+  *word_count = c.word_count();
+  return c.data();
 }
 
 // ---- sketch primitives (hll.hpp) ------------------------------------------
