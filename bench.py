@@ -1,28 +1,39 @@
 #!/usr/bin/env python
 """Benchmark of the B200 HyperANF iteration (BASELINE.json metric: arcs/s per
-HyperANF iteration, and % of HBM roofline).
+HyperANF iteration, and % of HBM roofline, at 1/2/4/8 B200).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
 
-A "step" is one dense HyperANF iteration (iteration 1 from the seeded state:
-every arc scanned, every counter read and written, estimates and N(1)
-reduced) over the synthetic graph of BASELINE config C (default 2: R-MAT
-scale 20).  The state is re-seeded and L2 flushed (256 MiB write) before
-each timed step, outside the timed region; each step is timed with CUDA
-events on the engine's stream.  One JSON line on rank 0.
+Workload: BASELINE config C, default 5 -- R-MAT scale 28 (2^28 nodes, 4.26 B
+arcs after dedup), log2m = 6, the largest configuration and the only one
+BASELINE quotes at 1/2/4/8 GPUs.  The graph is generated on the GPU
+(hanf_gen_rmat_gpu, bit-identical to the host generator and to the
+oracle's restatement).  Synthetic data: there is no public dataset.
+
+A "step" is one dense HyperANF iteration: iteration 1 from the seeded
+state, every arc scanned, every counter gathered / compared / written,
+estimates and N(1) reduced, report read back to the host.  The state is
+re-seeded and L2 flushed (256 MiB write > 126 MB L2) before each timed step,
+outside the timed region; each step is timed with CUDA events on the
+engine's stream.  One JSON line on rank 0.
 
   value     arcs/s, graph resident in HBM (device-timed dense iterations)
   e2e       arcs/s per iteration of a whole estimate_nf() through the C-ABI
-            from pinned host CSR to N(t) on the host: upload, seeding, every
-            iteration to stabilisation, read-back (wall clock)
+            from the caller's page-locked host CSR to N(t) on the host:
+            upload, seeding, every iteration to stabilisation, read-back
   roofline  union sweep: SURVEY 8(d) algorithmic bytes per launch / the
             sweep's CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline  the reference engine (oracle/_ref) on this host's cores, on
-            dense iterations of the same graph
+  cpu_baseline  the reference engine (oracle/_ref, built from the reference's
+            own headers) on this host's cores, same graph, same unit:
+            bounded node-range samples of dense iteration 1 (NfEngine::step's
+            per-node body + block re-sum, ref_shim.cpp), all threads and 1
+  config2   the same device-timed measurement on config 2 (R-MAT scale 20)
 
---impl reference times the reference's own CPU engine (oracle/_ref, built
-from /root/reference's headers) on e2e's metric: whole estimate_nf() runs,
-all host threads.
+--impl reference times the reference's own CPU engine (oracle/_ref) on the
+same metric and unit: node-range samples of dense iteration 1 of the same
+config-5 graph, all host threads.  Its process never loads libhanf.so: the
+graph comes from the oracle's R-MAT restatement (oracle/hanf_oracle_gen.c,
+pinned to the package's generators by tests/test_oracle_gen.py).
 """
 from __future__ import annotations
 
@@ -30,6 +41,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -39,28 +51,35 @@ sys.path.insert(0, ROOT)
 
 HLL_SEED = 42
 METRIC = "arcs/s per HyperANF iteration"
+STEP_DESC = ("dense iteration 1 from the seeded state (every arc scanned, every counter "
+             "gathered/compared/written, estimates + N(1) reduced)")
+
+CONFIGS = {
+    1: dict(b=6, kind="er", name="config1: directed G(n,p) n=65536, mean out-degree 8, "
+            "no self-loops, seed 1; log2m=6"),
+    2: dict(b=6, kind="rmat", scale=20, name="config2: R-MAT scale 20, edge factor 16, "
+            "a=.57 b=.19 c=.19, self-loops/dups removed, ids permuted (seed 7); log2m=6"),
+    3: dict(b=7, kind="copying", name="config3: copying model n=2^24, power-law out-degree "
+            "(2.1, mean 20, max 5000), copy prob 0.6, window +-2^12; log2m=7"),
+    4: dict(b=5, kind="ba", name="config4: Barabasi-Albert n=2^25, m=10, symmetric, ids "
+            "permuted (seed 11); log2m=5"),
+    5: dict(b=6, kind="rmat", scale=28, name="config5: R-MAT scale 28, edge factor 16, "
+            "a=.57 b=.19 c=.19, self-loops/dups removed, 32-bit ids randomly permuted "
+            "(seed 7); log2m=6"),
+}
 
 
-def workload(config: int):
+def make_graph(config: int, device=None):
+    """The package's generators (B200 arm only)."""
     import paper_1011_5599_b200 as hanf
-    if config == 1:
-        return ("config1: directed G(n,p) n=65536, mean out-degree 8, no self-loops, seed 1; "
-                "log2m=6", lambda: hanf.gen_erdos_renyi(65536, 8.0, 1), 6)
-    if config == 2:
-        return ("config2: R-MAT scale 20, edge factor 16, a=.57 b=.19 c=.19, self-loops/dups "
-                "removed, ids permuted (seed 7); log2m=6",
-                lambda: hanf.gen_rmat(20, 16, 0.57, 0.19, 0.19, 1, 7), 6)
-    if config == 3:
-        return ("config3: copying model n=2^24, power-law out-degree (2.1, mean 20, max 5000), "
-                "copy prob 0.6, window +-2^12; log2m=7",
-                lambda: hanf.gen_copying(1 << 24, 2.1, 20.0, 5000, 0.6, 1 << 12, 3), 7)
-    if config == 4:
-        return ("config4: Barabasi-Albert n=2^25, m=10, symmetric, ids permuted (seed 11); "
-                "log2m=5", lambda: hanf.gen_barabasi_albert(1 << 25, 10, 4, 11), 5)
-    if config == 5:
-        return ("config5: R-MAT scale 28, edge factor 16, a=.57 b=.19 c=.19, ids permuted; "
-                "log2m=6", lambda: hanf.gen_rmat(28, 16, 0.57, 0.19, 0.19, 1, 7), 6)
-    raise SystemExit(f"unknown config {config}")
+    c = CONFIGS[config]
+    if c["kind"] == "er":
+        return hanf.gen_erdos_renyi(65536, 8.0, 1)
+    if c["kind"] == "rmat":
+        return hanf.gen_rmat(c["scale"], 16, 0.57, 0.19, 0.19, 1, 7, device=device)
+    if c["kind"] == "copying":
+        return hanf.gen_copying(1 << 24, 2.1, 20.0, 5000, 0.6, 1 << 12, 3)
+    return hanf.gen_barabasi_albert(1 << 25, 10, 4, 11)
 
 
 def algorithmic_bytes(n: int, a: int, words: int) -> int:
@@ -76,6 +95,23 @@ def hbm_peak():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_cpu():
+    """lscpu sockets x cores x threads, and the threads this process may use."""
+    info = {"nproc": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        keys = {"Socket(s)": "sockets", "Core(s) per socket": "cores_per_socket",
+                "Thread(s) per core": "threads_per_core", "Model name": "model"}
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in keys:
+                v = v.strip()
+                info[keys[k.strip()]] = int(v) if v.isdigit() else v
+    except Exception:
+        pass
+    return info
 
 
 class ClockSampler:
@@ -109,7 +145,7 @@ class ClockSampler:
                 self.reasons |= self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
             except Exception:
                 pass
-            self._stop.wait(0.002)  # the timed loop is only tens of ms long
+            self._stop.wait(0.002)
 
     def __enter__(self):
         if self._nv:
@@ -130,8 +166,8 @@ class ClockSampler:
 
 
 def ncu_traffic(config: int):
-    """dram bytes per union-kernel launch from the committed ncu --set full
-    summary (profiles/), or None."""
+    """DRAM bytes (read + write) per union-kernel launch from the committed
+    ncu --set full summary (profiles/union_kernel_ncu.json), or None."""
     path = os.path.join(ROOT, "profiles", "union_kernel_ncu.json")
     try:
         with open(path) as f:
@@ -142,92 +178,271 @@ def ncu_traffic(config: int):
 
 
 # ---------------------------------------------------------------------------
-# reference arm / cpu baseline (oracle/_ref: the reference engine itself)
+# the reference engine on the host cores (reference arm and cpu_baseline)
 # ---------------------------------------------------------------------------
-def reference_arm(args, g, workload_name, b):
+def reference_graph(config: int):
+    """(n, offsets, succ) without loading libhanf.so: R-MAT configs from the
+    oracle's restatement of the generator; the others from a child process
+    that writes the package generator's CSR to /dev/shm."""
+    import numpy as np
     import oracle
-    ref = oracle.ref()
-    threads = os.cpu_count() or 1
-    rg = ref.graph(g.num_nodes(), g.offsets(), g.arcs())
-    a = g.num_arcs()
-    times, iters = [], []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()  # estimate_nf = ctor (seeding) + run
-        eng = ref.engine(rg, bucket_bits=b, seed=HLL_SEED, threads=threads)
-        vals, mods, wall = eng.run()
-        dt = time.perf_counter() - t0
-        del eng
-        if i >= args.warmup:
-            times.append(dt)
-            iters.append(len(vals))  # T recorded + the stabilising iteration
-    value = a * sum(iters) / sum(times)
+    c = CONFIGS[config]
+    if c["kind"] == "rmat":
+        return oracle.port().gen_rmat(c["scale"], 16, 0.57, 0.19, 0.19, 1, 7)
+    d = f"/dev/shm/hanf_bench_graph_{os.getpid()}"
+    os.makedirs(d, exist_ok=True)
+    subprocess.run([sys.executable, os.path.abspath(__file__), "--write-graph", d,
+                    "--config", str(config)], check=True)
+    off = np.load(os.path.join(d, "offsets.npy"))
+    succ = np.load(os.path.join(d, "succ.npy"))
+    for f in ("offsets.npy", "succ.npy"):
+        os.unlink(os.path.join(d, f))
+    os.rmdir(d)
+    return len(off) - 1, off, succ
+
+
+def reference_samples(eng, n, arcs, threads, steps, warmup, budget_s):
+    """Bounded samples of dense iteration 1 of the reference engine: node
+    slices [lo, lo + size), rotating through the (randomly permuted) id
+    space, each timed with steady_clock inside ref_shim.  The slice size is
+    calibrated on the first warm-up sample so all steps take about
+    budget_s.  Returns (arcs/s over the timed samples, per-sample seconds,
+    sampled arcs, slice size)."""
+    probe = max(64, min(n, (n // 4096) // 64 * 64 or 64))
+    while True:  # calibration (warm-up): grow the slice until it takes >= 0.25 s
+        secs, a, _, _ = eng.step_sample(0, probe, threads)
+        if secs >= 0.25 or probe >= n or secs * (n / probe) >= 0.25 * budget_s:
+            break
+        probe = min(n, probe * 4)
+    rate = a / secs if secs > 0 and a else 1e7
+    per_step = budget_s / max(1, steps + warmup)
+    size = int(per_step * rate / max(1.0, arcs / n))
+    size = max(64, min(n, size // 64 * 64))
+    lo, times, sampled = probe % n, [], []
+    for i in range(warmup - 1 + steps):
+        if lo + size > n:
+            lo = 0
+        s, a, _, _ = eng.step_sample(lo, lo + size, threads)
+        lo += size
+        if i >= warmup - 1:
+            times.append(s)
+            sampled.append(a)
+    return sum(sampled) / sum(times), times, sampled, size
+
+
+def reference_arm(args):
+    """--impl reference: the reference's own CPU engine (oracle/_ref) on all
+    host threads, same config, metric and unit as the B200 arm."""
+    import oracle
+    cfg = CONFIGS[args.config]
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    n, off, succ = reference_graph(args.config)
+    a = int(off[-1])
+    R = oracle.ref()
+    rg = R.graph_sorted(n, off, succ)
+    del off, succ
+    gen_s = time.perf_counter() - t0
+    eng = R.engine(rg, bucket_bits=cfg["b"], seed=HLL_SEED, threads=threads)
+    value, times, sampled, size = reference_samples(eng, n, a, threads, args.steps,
+                                                    max(1, args.warmup), args.ref_budget)
+    cpu = host_cpu()
+    sample = (f"{len(times)} timed samples (+{max(1, args.warmup)} warm-up) of dense iteration "
+              f"1 of the same graph: NfEngine::step's per-node body (engine.hpp:157-184) + "
+              f"block re-sum (engine.hpp:100-112) over node slices of {size} of {n} nodes "
+              f"({sum(sampled) / len(sampled) / a:.2%} of the arcs each), threads={threads}, "
+              f"parallel_chunks(task_size=n/4096), oracle/_ref (reference headers)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "arcs/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": workload_name, "n": g.num_nodes(), "arcs": a, "log2m": b,
-                   "hll_seed": HLL_SEED, "step": "one whole estimate_nf() run to "
-                   "stabilisation (engine.hpp:233-275), arcs x iterations / wall time"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "n": n, "arcs": a, "log2m": cfg["b"],
+                   "hll_seed": HLL_SEED, "step": STEP_DESC + "; a bounded node-slice sample "
+                   "per step (see cpu_baseline.sample)",
+                   "graph_source": "oracle R-MAT restatement (hanf_oracle_gen.c)"
+                   if cfg["kind"] == "rmat" else "package generator in a child process",
+                   "setup_s": round(gen_s, 1)},
         "cpu_baseline": {"value": value, "unit": "arcs/s", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{args.steps} estimate_nf runs of {workload_name}, "
-                                   f"threads={threads}, oracle/_ref (reference headers)"},
+                         "kind": "reference", "host": cpu, "sample": sample},
         "e2e": {"value": value, "unit": "arcs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(g, b, budget_s=12.0):
-    """Reference engine, dense iteration 1 (same unit of work as `value`)."""
+def cpu_baseline(g, b, budget_all=14.0, budget_one=7.0):
+    """Reference engine on this host, same graph and unit as `value`."""
     import oracle
     if not oracle.have_ref():
         return None
-    ref = oracle.ref()
-    threads = os.cpu_count() or 1
-    rg = ref.graph(g.num_nodes(), g.offsets(), g.arcs())
-    steps, total = 0, 0.0
-    start = time.perf_counter()
-    while steps < 1 or (time.perf_counter() - start < budget_s and steps < 20):
-        eng = ref.engine(rg, bucket_bits=b, seed=HLL_SEED, threads=threads)
-        secs, _, _ = eng.timed_step()
-        del eng
-        total += secs
-        steps += 1
-    return {"value": g.num_arcs() * steps / total, "unit": "arcs/s", "cores": threads,
-            "kind": "reference",
-            "sample": f"{steps} dense iterations (iteration 1 from the seeded state) of the "
-                      f"same graph, NfEngine::step() timed with steady_clock, threads={threads}"}
+    R = oracle.ref()
+    n, a = g.num_nodes(), g.num_arcs()
+    rg = R.graph_sorted(n, g.offsets(), g.arcs())
+    threads = len(os.sched_getaffinity(0))
+    out = {"unit": "arcs/s", "kind": "reference", "host": host_cpu()}
+    eng = R.engine(rg, bucket_bits=b, seed=HLL_SEED, threads=threads)
+    v_all, t_all, s_all, size_all = reference_samples(eng, n, a, threads, 8, 2, budget_all)
+    v_one, t_one, s_one, size_one = reference_samples(eng, n, a, 1, 3, 1, budget_one)
+    del eng, rg
+    out.update(value=v_all, cores=threads, threads_1={"value": v_one, "samples": len(t_one),
+                                                       "slice_nodes": size_one},
+               sample=f"{len(t_all)} samples of dense iteration 1 (NfEngine::step per-node "
+                      f"body + block re-sum over node slices of {size_all} of {n} nodes, "
+                      f"{sum(s_all) / len(s_all) / max(1, a):.2%} of the arcs each), "
+                      f"threads={threads}; threads=1 leg: {len(t_one)} slices of {size_one} "
+                      f"nodes; oracle/_ref on the same CSR")
+    return out
 
 
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+def dense_step_timing(engine, dev, steps, warmup, flush, sharded=None, world=1):
+    """Device time of `steps` dense iterations 1 (re-seed + L2 flush before
+    each, outside the timed region).  Returns (total ms, launches, clocks)."""
+    import torch
+    stream = torch.cuda.ExternalStream(engine.stream(), device=dev)
+    reset = sharded.reset if sharded is not None else engine.reset
+    do_step = sharded.step if sharded is not None else engine.step
+    for _ in range(warmup):
+        reset()
+        do_step()
+    launches = 0
+    total_ms = 0.0
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clocks:
+        for _ in range(steps):
+            reset()
+            torch.cuda.synchronize(dev)
+            before = engine.launch_count()
+            start = torch.cuda.Event(enable_timing=True)
+            end = torch.cuda.Event(enable_timing=True)
+            if world == 1:
+                # the untimed L2 flush keeps the GPU busy while the host
+                # enqueues the step: the events bracket the step's device
+                # work only
+                flush.zero_()
+                stream.wait_stream(torch.cuda.current_stream(dev))
+                start.record(stream)
+                engine.step_launch()
+                end.record(stream)
+                end.synchronize()
+                engine.step_complete()
+            else:
+                flush.zero_()
+                torch.cuda.synchronize(dev)
+                start.record(stream)
+                do_step()
+                end.record(stream)
+                end.synchronize()
+            total_ms += start.elapsed_time(end)
+            launches += engine.launch_count() - before
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    return total_ms, launches, clocks.summary()
+
+
+def phase_timing(engine, dev, flush, reps, sharded=None):
+    """CUDA events between the step's kernels (ungraphed steps, same kernels)."""
+    import torch
+    reset = sharded.reset if sharded is not None else engine.reset
+    do_step = sharded.step if sharded is not None else engine.step
+    engine.set_timing(True)
+    for _ in range(reps):
+        reset()
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        do_step()
+    t = engine.timing()
+    engine.set_timing(False)
+    k = max(1, t["steps"])
+    return {"union": t["union_ms"] / k, "estimate": t["estimate_ms"] / k,
+            "finish": t["reduce_ms"] / k}
+
+
+def run_profile(engine, n):
+    """every iteration of one whole run, device time of each
+    step's sweep and finish (the dense ones and the tail, separately)."""
+    engine.reset()
+    engine.run_to_stabilisation()  # untimed: first launches of the tail kernels
+    engine.reset()
+    prof, prev = [], n
+    while True:
+        engine.set_timing(True)
+        rep = engine.step()
+        t = engine.timing()
+        kind = "dense" if 2 * prev >= n else "tail (worklist or skip sweep)"
+        prof.append({"t": len(prof) + 1, "modified": rep.modified, "kind": kind,
+                     "sweep_ms": round(t["union_ms"], 4),
+                     "finish_ms": round(t["reduce_ms"] + t["estimate_ms"], 4)})
+        prev = rep.modified
+        if rep.modified == 0 or len(prof) >= 4 * n + 8:
+            break
+    engine.set_timing(False)
+    return prof
+
+
+def single_gpu_config2(dev, steps, warmup, flush, peak):
+    """Config 2 (R-MAT scale 20, L2-resident counters), same protocol."""
+    import paper_1011_5599_b200 as hanf
+    g = make_graph(2, device=dev.index)
+    n, a = g.num_nodes(), g.num_arcs()
+    eng = hanf.NfEngine(g, hanf.EngineConfig(bucket_bits=6, seed=HLL_SEED, device=dev.index,
+                                             exact_sum=False))
+    total_ms, _, _ = dense_step_timing(eng, dev, steps, warmup, flush)
+    ph = phase_timing(eng, dev, flush, max(3, min(steps, 10)))
+    B = algorithmic_bytes(n, a, eng.params().words)
+    eng.close()
+    ach = B / (ph["union"] / 1e3) / 1e9
+    return {"workload": CONFIGS[2]["name"], "value": a * steps / (total_ms / 1e3),
+            "unit": "arcs/s", "ms_per_step": total_ms / steps,
+            "roofline": {"achieved": ach, "frac": ach / peak, "kernel_ms": ph["union"],
+                         "algorithmic_bytes": B,
+                         "note": "42 MB counter array: L2-resident, bound by L1 wavefronts"}}
+
+
+def write_graph(args):
+    """--write-graph DIR: the package generator's CSR as .npy (the reference
+    arm's child process for configs without an oracle generator)."""
+    import numpy as np
+    g = make_graph(args.config)
+    np.save(os.path.join(args.write_graph, "offsets.npy"), g.offsets())
+    np.save(os.path.join(args.write_graph, "succ.npy"), g.arcs())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-config2", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=80.0,
+                    help="seconds of reference CPU work across all reference-arm steps")
     ap.add_argument("--exchange", default="peer", choices=["peer", "collective"],
                     help="N>1: peer-push rows over NVLink from the union kernels "
                          "(hanf_shard_attach) or NCCL all-gathers")
+    ap.add_argument("--write-graph", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    args.warmup = max(3, args.warmup) if args.impl == "b200" else args.warmup
 
+    if args.write_graph:
+        write_graph(args)
+        return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    name, make_graph, b = workload(args.config)
-
     if args.impl == "reference":
-        if rank != 0:
-            return
-        g = make_graph()
-        reference_arm(args, g, name, b)
+        if rank == 0:
+            reference_arm(args)
         return
 
     import torch
@@ -247,93 +462,26 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    g = make_graph()
+    cfgd = CONFIGS[args.config]
+    b = cfgd["b"]
+    t_gen = time.perf_counter()
+    g = make_graph(args.config, device=local_rank if cfgd["kind"] == "rmat" else None)
+    t_gen = time.perf_counter() - t_gen
     n, a = g.num_nodes(), g.num_arcs()
     cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank, exact_sum=False)
     if world > 1:
         sharded = ShardedNfEngine(g, cfg, rank, world, exchange=args.exchange)
         engine = sharded.local.engine
-        do_step = sharded.step
     else:
         sharded = None
         engine = hanf.NfEngine(g, cfg)
-        do_step = engine.step
     words = engine.params().words
-    stream = torch.cuda.ExternalStream(engine.stream(), device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def barrier():
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize(dev)
-
-    reset = sharded.reset if sharded is not None else engine.reset  # (shards: + barrier)
-    for _ in range(args.warmup):
-        reset()
-        do_step()
-    step_launches = 0
-    total_ms = 0.0
-    barrier()
-    with ClockSampler(local_rank) as clocks:
-        for _ in range(args.steps):
-            reset()                              # untimed: back to the seeded state
-            torch.cuda.synchronize(dev)
-            launches_before = engine.launch_count()
-            start = torch.cuda.Event(enable_timing=True)
-            end = torch.cuda.Event(enable_timing=True)
-            if world == 1:
-                # the L2 flush (untimed) keeps the GPU busy while the host
-                # enqueues the step, so the events bracket the step's device
-                # work only - no host launch latency inside the timed span
-                flush.zero_()
-                stream.wait_stream(torch.cuda.current_stream(dev))
-                start.record(stream)
-                engine.step_launch()
-                end.record(stream)
-                end.synchronize()
-                rep = engine.step_complete()
-            else:
-                flush.zero_()                    # untimed: evict L2 (256 MiB > 126 MB)
-                torch.cuda.synchronize(dev)
-                start.record(stream)
-                rep = do_step()
-                end.record(stream)
-                end.synchronize()
-            total_ms += start.elapsed_time(end)
-            step_launches += engine.launch_count() - launches_before  # the step's kernels only
-    barrier()
-    # kernel phases for the roofline: CUDA events between the kernels on the
-    # engine stream (ungraphed steps, same kernels), same flush protocol
-    engine.set_timing(True)
-    for _ in range(max(3, min(args.steps, 10))):
-        reset()
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        do_step()
-    timing = engine.timing()
-    # the iterations after the dense ones, reported separately -
-    # one whole run to stabilisation, device time of each step's sweep
-    # (union / skip / worklist kernels) and of its finish, CUDA events
-    run_profile = []
-    if world == 1:
-        engine.reset()
-        engine.run_to_stabilisation()  # untimed: first launches of the tail kernels (lazy loading)
-        engine.reset()
-        prev = n
-        while True:
-            engine.set_timing(True)
-            rep = do_step()
-            t = engine.timing()
-            kind = ("dense" if 2 * prev >= n else
-                    "worklist or skip sweep (changed-successor probes)")
-            run_profile.append({"t": len(run_profile) + 1, "modified": rep.modified, "kind": kind,
-                                "sweep_ms": round(t["union_ms"], 4),
-                                "finish_ms": round(t["reduce_ms"] + t["estimate_ms"], 4)})
-            prev = rep.modified
-            if rep.modified == 0 or len(run_profile) >= 4 * n + 8:
-                break
-    engine.set_timing(False)
+    total_ms, step_launches, clocks = dense_step_timing(engine, dev, args.steps, args.warmup,
+                                                        flush, sharded, world)
+    phases = phase_timing(engine, dev, flush, max(3, min(args.steps, 10)), sharded)
+    profile = run_profile(engine, n) if world == 1 else None
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], dtype=torch.float64,
@@ -341,75 +489,72 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = a * args.steps / (total_ms / 1e3)
-    union_ms = timing["union_ms"] / max(1, timing["steps"])
+    union_ms = phases["union"]
     peak, peak_src = hbm_peak()
     if world > 1:
         # the rank's own sweep: its rows and their arcs (rank 0 reports; the
         # shards are arc-balanced by the id permutation / interleaving)
         lo, hi = sharded.ranges[rank]
-        rank_arcs = (a // world if engine.device_buffers().relabelled  # rows interleaved by degree
+        rank_arcs = (a // world if engine.device_buffers().relabelled
                      else int(g.offsets()[hi]) - int(g.offsets()[lo]))
         B = algorithmic_bytes(hi - lo, rank_arcs, words)
     else:
         B = algorithmic_bytes(n, a, words)
     achieved = B / (union_ms / 1e3) / 1e9 if union_ms > 0 else None
     traffic = ncu_traffic(args.config) if world == 1 else None
+    if sharded is not None:
+        sharded.close()
+    else:
+        engine.close()
 
+    # whole estimate_nf through the public API from the caller's page-locked
+    # host CSR (pinned in place with Graph.pin(), hanf_pin_host)
     e2e = None
-    if not args.no_e2e and world > 1:
-        # whole sharded run through the public API: every rank page-locks
-        # its copy of the CSR, creates its shard engine (uploads its rows),
-        # attaches to the peers and iterates to stabilisation; wall time
-        # max over ranks
-        import torch.distributed as dist
-        pinned = hanf.Graph(n, g.offsets().copy(), g.arcs().copy()).pin()
+    if not args.no_e2e:
+        g.pin()
         e2e_cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank)
-        runs, iters, wall = min(args.steps, 3), 0, 0.0
-        for r in range(runs + 1):
-            barrier()
-            t0 = time.perf_counter()
-            sh = ShardedNfEngine(pinned, e2e_cfg, rank, world, exchange=args.exchange)
-            est = sh.run_to_stabilisation()
-            dt = time.perf_counter() - t0
-            sh.close()
-            t = torch.tensor([dt], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            if r > 0:  # run 0 warms the context and allocator
-                wall += float(t.item())
-                iters += est.iterations() + 1
-        lo, hi = sharded.ranges[rank]
+        runs = max(1, min(args.steps, 3 if n > (1 << 24) else 5))
+        iters, wall = 0, 0.0
         blocks = (n + 63) // 64
-        e2e = {"value": a * iters / wall, "unit": "arcs/s",
-               "h2d_bytes_per_step": 8 * (n + 1) + 4 * (int(g.offsets()[hi]) - int(g.offsets()[lo])),
-               "d2h_bytes_per_step": int(iters / runs * (16 + 8 * blocks)),
-               "step": "whole sharded estimate_nf() per rank (upload of the rank's rows, "
-                       "seed, every iteration, read-back), max over ranks; bytes per rank"}
-    if not args.no_e2e and world == 1:
-        # whole estimate_nf through the C-ABI from pinned host memory: the
-        # caller's CSR (fresh numpy arrays) page-locked in place with
-        # Graph.pin() (hanf_pin_host).  torch.pin_memory() buffers are not
-        # used: on these VMs their H2D rate varies 21-55 GB/s from buffer to
-        # buffer, registered huge-page memory holds 55 (profiles/r01_h2d.md)
-        pinned = hanf.Graph(n, g.offsets().copy(), g.arcs().copy()).pin()
-        e2e_cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank)
-        hanf.estimate_nf(pinned, e2e_cfg)     # warm (context, allocator)
-        runs, iters, wall = min(args.steps, 5), 0, 0.0
-        for _ in range(runs):
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            est = hanf.estimate_nf(pinned, e2e_cfg)
-            wall += time.perf_counter() - t0
-            if os.environ.get("BENCH_DEBUG"):
-                print(f"e2e run {1e3 * (time.perf_counter() - t0):.3f} ms", file=sys.stderr)
-            iters += est.iterations() + 1       # + the stabilising iteration
-        blocks = (n + 63) // 64
-        per_run_iters = iters / runs
-        e2e = {"value": a * iters / wall, "unit": "arcs/s",
-               "h2d_bytes_per_step": 8 * (n + 1) + 4 * a,
-               "d2h_bytes_per_step": int(per_run_iters * (16 + 8 * blocks)
-                                         + 16 * (est.iterations() + 1)),
-               "step": "whole estimate_nf() (upload, seed, %d iterations, read-back) per step"
-                       % round(per_run_iters)}
+        if world == 1:
+            hanf.estimate_nf(g, e2e_cfg)  # warm (context, allocator)
+            for _ in range(runs):
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                est = hanf.estimate_nf(g, e2e_cfg)
+                wall += time.perf_counter() - t0
+                iters += est.iterations() + 1       # + the stabilising iteration
+            h2d = 8 * (n + 1) + 4 * a
+            desc = "whole estimate_nf() (upload, seed, %d iterations, read-back) per step"
+        else:
+            import torch.distributed as dist
+            for r in range(runs + 1):
+                torch.cuda.synchronize(dev)
+                dist.barrier()
+                t0 = time.perf_counter()
+                sh = ShardedNfEngine(g, e2e_cfg, rank, world, exchange=args.exchange)
+                est = sh.run_to_stabilisation()
+                dt = time.perf_counter() - t0
+                sh.close()
+                t = torch.tensor([dt], dtype=torch.float64,
+                                 device=dev if backend == "nccl" else "cpu")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                if r > 0:  # run 0 warms the context and allocator
+                    wall += float(t.item())
+                    iters += est.iterations() + 1
+            lo, hi = sharded.ranges[rank]
+            h2d = 8 * (n + 1) + 4 * (int(g.offsets()[hi]) - int(g.offsets()[lo]))
+            desc = ("whole sharded estimate_nf() per rank (upload of the rank's rows, seed, "
+                    "%d iterations, read-back), max over ranks; bytes per rank")
+        per_run = iters / runs
+        e2e = {"value": a * iters / wall, "unit": "arcs/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(per_run * (16 + 8 * blocks)),
+               "ms_per_run": 1e3 * wall / runs, "step": desc % round(per_run)}
+        g.unpin()
+
+    extra2 = None
+    if not args.no_config2 and world == 1 and args.config != 2:
+        extra2 = single_gpu_config2(dev, args.steps, args.warmup, flush, peak)
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
@@ -424,37 +569,32 @@ def main():
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": name, "n": n, "arcs": a, "log2m": b, "register_bits": 5,
-                       "words_per_counter": words, "hll_seed": HLL_SEED,
+            "config": {"workload": cfgd["name"], "n": n, "arcs": a, "log2m": b,
+                       "register_bits": 5, "words_per_counter": words, "hll_seed": HLL_SEED,
                        "parallelism": f"node-range shards x{world}" if world > 1 else "1 GPU",
-                       "exchange": (sharded.exchange + (f" (fallback: {sharded.fallback})"
-                                                        if sharded.fallback else ""))
-                                   if sharded is not None else None,
-                       "step": "dense iteration 1 (all arcs) incl. estimates, N(t) total, "
-                               "D2H report; re-seed + L2 flush outside the timed region; "
-                               "events bracket the step's device work (launch enqueued "
-                               "during the flush)",
-                       "l2": "flushed before every timed step (256 MiB write)",
+                       "graph": "generated on the GPU (hanf_gen_rmat_gpu) in %.1f s" % t_gen
+                                if cfgd["kind"] == "rmat" else "host generator",
+                       "exchange": args.exchange if world > 1 else None,
+                       "step": STEP_DESC + "; re-seed + L2 flush outside the timed region; "
+                               "events bracket the step's device work",
+                       "l2": "flushed before every timed step (256 MiB write); inputs "
+                             "(counters %.1f GB, arcs %.1f GB) exceed the 126 MB L2"
+                             % (2 * 8 * words * n / 1e9, 4 * a / 1e9),
                        "sum_mode": "device (deterministic tree)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "union_kernel (successor gather + broadword max + fused estimator)",
+                         "kernel": "union_kernel (successor gather + broadword max + fused "
+                                   "estimator)",
                          "kernel_ms": union_ms, "algorithmic_bytes": B,
-                         "peak_source": peak_src,
-                         "phases_ms": {"union": timing["union_ms"] / max(1, timing["steps"]),
-                                       "estimate": timing["estimate_ms"] / max(1, timing["steps"]),
-                                       "finish": timing["reduce_ms"] / max(1, timing["steps"])}},
+                         "peak_source": peak_src, "phases_ms": phases},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "run_profile": run_profile or None,
+            "config2": extra2,
+            "run_profile": profile,
             "gpu_launches": step_launches,
-            "clocks": clocks.summary(),
+            "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    if sharded is not None:
-        sharded.close()
-    else:
-        engine.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 

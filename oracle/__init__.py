@@ -187,9 +187,12 @@ class Port:
         return g.n, _owned(self, g, g.offsets, g.n + 1), _owned(self, g, g.succ, g.arcs)
 
     def counter_digest(self, words, n, W, threads=None):
-        w = np.ascontiguousarray(words, dtype=np.uint64)
-        assert w.size >= n * W
-        return int(self.L.or_counter_digest(_u64p(w), n, W, threads or os.cpu_count() or 1))
+        """words: a uint64 array, or a ctypes POINTER(c_uint64)."""
+        if isinstance(words, np.ndarray):
+            w = np.ascontiguousarray(words, dtype=np.uint64)
+            assert w.size >= n * W
+            words = _u64p(w)
+        return int(self.L.or_counter_digest(words, n, W, threads or os.cpu_count() or 1))
 
     def csr_digest(self, n, offsets, succ):
         offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
@@ -529,6 +532,12 @@ class RefEngine:
         secs = self.L.ref_engine_step_sample(self.h, lo, hi, threads, ctypes.byref(arcs),
                                              ctypes.byref(s), ctypes.byref(ch))
         return secs, arcs.value, s.value, ch.value
+
+    def counters_ptr(self):
+        """(pointer, word count) of the engine's current counters, no copy."""
+        wc = c_uint64()
+        p = self.L.ref_engine_counters(self.h, ctypes.byref(wc))
+        return p, wc.value
 
     def next_counters(self):
         wc = c_uint64()
