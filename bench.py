@@ -205,17 +205,17 @@ def reference_samples(eng, n, arcs, threads, steps, warmup, budget_s):
     """Bounded samples of dense iteration 1 of the reference engine: node
     slices [lo, lo + size), rotating through the (randomly permuted) id
     space, each timed with steady_clock inside ref_shim.  The slice size is
-    calibrated on the first warm-up sample so all steps take about
-    budget_s.  Returns (arcs/s over the timed samples, per-sample seconds,
+    calibrated by warm-up samples so all steps take about budget_s.  Returns (arcs/s over the timed samples, per-sample seconds,
     sampled arcs, slice size)."""
+    eng.prefault(threads)  # next_ allocated and touched: steady-state samples
+    per_step = budget_s / max(1, steps + warmup)
     probe = max(64, min(n, (n // 4096) // 64 * 64 or 64))
-    while True:  # calibration (warm-up): grow the slice until it takes >= 0.25 s
-        secs, a, _, _ = eng.step_sample(0, probe, threads)
-        if secs >= 0.25 or probe >= n or secs * (n / probe) >= 0.25 * budget_s:
+    while True:  # calibration (warm-up): grow the slice until it takes long
+        secs, a, _, _ = eng.step_sample(0, probe, threads)  # enough to time
+        if secs >= min(0.25, 0.2 * per_step) or probe >= n:
             break
         probe = min(n, probe * 4)
     rate = a / secs if secs > 0 and a else 1e7
-    per_step = budget_s / max(1, steps + warmup)
     size = int(per_step * rate / max(1.0, arcs / n))
     size = max(64, min(n, size // 64 * 64))
     lo, times, sampled = probe % n, [], []

@@ -401,6 +401,7 @@ class Ref:
         L.ref_engine_step_sample.argtypes = [vp, c_uint64, c_uint64, ctypes.c_uint,
                                              POINTER(c_uint64), POINTER(c_double),
                                              POINTER(c_uint64)]
+        L.ref_engine_prefault.argtypes = [vp, ctypes.c_uint]
         L.ref_engine_next_counters.restype = POINTER(c_uint64)
         L.ref_engine_next_counters.argtypes = [vp, POINTER(c_uint64)]
         self.L = L
@@ -538,6 +539,10 @@ class RefEngine:
         wc = c_uint64()
         p = self.L.ref_engine_counters(self.h, ctypes.byref(wc))
         return p, wc.value
+
+    def prefault(self, threads):
+        """Allocate and touch next_ (ref_shim.cpp ref_engine_prefault)."""
+        self.L.ref_engine_prefault(self.h, threads)
 
     def next_counters(self):
         wc = c_uint64()

@@ -273,6 +273,23 @@ double ref_engine_step_sample(void* ep, uint64_t lo, uint64_t hi, unsigned threa
   *changed_out = changed;
   return std::chrono::duration<double>(t1 - t0).count();
 }
+// Allocates next_ / next_modified_ as step() would (engine.hpp:126-127) and
+// touches every page with `threads` workers, so step samples measure the
+// steady state rather than first-touch page faults of iteration 1.
+void ref_engine_prefault(void* ep, unsigned threads) {
+  NfEngine* e = static_cast<NfEngine*>(ep);
+  const uint64_t n = (e->*get(EngGraph{}))->num_nodes();
+  const SketchParams& params = e->*get(EngParams{});
+  CounterArray& next = e->*get(EngNext{});
+  std::vector<std::uint8_t>& next_modified = e->*get(EngNextMod{});
+  if (next.size() != n) next = CounterArray(params, n);
+  if (next_modified.size() != n) next_modified.assign(n, 0);
+  const unsigned words = params.words_per_counter();
+  parallel_chunks(n, threads ? threads : 1, 1 << 16,
+                  [&](std::uint64_t lo, std::uint64_t hi, unsigned) {
+    std::memset(next.counter(lo).data(), 0, (hi - lo) * words * sizeof(std::uint64_t));
+  });
+}
 // next_ after samples (the sampled rows are the step's rows)
 const uint64_t* ref_engine_next_counters(const void* ep, uint64_t* word_count) {
   const NfEngine* e = static_cast<const NfEngine*>(ep);

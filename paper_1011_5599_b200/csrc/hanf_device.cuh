@@ -213,6 +213,39 @@ __device__ __forceinline__ uint4 ld16(const uint4* p) {
   }
   return v;
 }
+// L2 eviction-priority policies (createpolicy): the gathers of hot rows
+// (the first rows after degree relabelling, most in-arcs) are kept with
+// evict_last, everything streamed once (cold rows, successor ids) is
+// evict_first, so the streams do not wash the hot set out of L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld16_pol(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld4_pol(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void ldg256_pol(uint32_t (&v)[8], const uint64_t* p, uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "l"(p), "l"(pol));
+}
+
 template <int kPol>
 __device__ __forceinline__ uint2 ld8(const uint2* p) {
   uint2 v;
@@ -320,6 +353,45 @@ __device__ __forceinline__ void store_counter(uint64_t* p, const uint32_t (&v)[L
     q.x = limb(ic<2 * k + 0>{});
     q.y = limb(ic<2 * k + 1>{});
     *reinterpret_cast<uint2*>(p + word) = q;
+  };
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    sfor<0, NW / 2>([&](auto I) {
+      constexpr int k = decltype(I)::value;
+      st16(ic<2 * k>{}, 2 * k);
+    });
+    if constexpr (NW % 2) st8(ic<NW - 1>{}, NW - 1);
+  } else {
+    st8(ic<0>{}, 0);
+    sfor<0, (NW - 1) / 2>([&](auto I) {
+      constexpr int k = decltype(I)::value;
+      st16(ic<2 * k + 1>{}, 2 * k + 1);
+    });
+    if constexpr (NW % 2 == 0) st8(ic<NW - 1>{}, NW - 1);
+  }
+}
+
+// store_counter with an L2 eviction-priority policy (evict_first for the
+// next generation: written once, read back only next step)
+template <class Lay>
+__device__ __forceinline__ void store_counter_pol(uint64_t* p, const uint32_t (&v)[Lay::kLimbs],
+                                                  uint64_t pol) {
+  constexpr int NW = Lay::kWords;
+  constexpr int NL = Lay::kLimbs;
+  auto limb = [&](auto I) -> uint32_t {
+    constexpr int i = decltype(I)::value;
+    if constexpr (i < NL) return v[i]; else return 0u;
+  };
+  auto st16 = [&](auto K, int word) {
+    constexpr int k = decltype(K)::value;
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(p + word), "r"(limb(ic<2 * k + 0>{})), "r"(limb(ic<2 * k + 1>{})),
+                    "r"(limb(ic<2 * k + 2>{})), "r"(limb(ic<2 * k + 3>{})), "l"(pol) : "memory");
+  };
+  auto st8 = [&](auto K, int word) {
+    constexpr int k = decltype(K)::value;
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;"
+                 :: "l"(p + word), "r"(limb(ic<2 * k + 0>{})), "r"(limb(ic<2 * k + 1>{})),
+                    "l"(pol) : "memory");
   };
   if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
     sfor<0, NW / 2>([&](auto I) {
@@ -550,6 +622,18 @@ __device__ __forceinline__ void window128_load(uint4 (&raw)[Window128<NW>::kLoad
   sfor<0, Window128<NW>::kLoads>([&](auto I) {
     constexpr int k = decltype(I)::value;
     raw[k] = ld16<kPol>(p + k);
+  });
+}
+
+template <int NW>
+__device__ __forceinline__ void window128_load_pol(uint4 (&raw)[Window128<NW>::kLoads],
+                                                   const uint64_t* base, uint32_t w,
+                                                   uint64_t pol) {
+  const uint64_t word = static_cast<uint64_t>(w) * NW;
+  const uint4* p = reinterpret_cast<const uint4*>(base + (word & ~1ull));
+  sfor<0, Window128<NW>::kLoads>([&](auto I) {
+    constexpr int k = decltype(I)::value;
+    raw[k] = ld16_pol(p + k, pol);
   });
 }
 

@@ -260,6 +260,7 @@ struct hanf_engine {
   double* reduce_sums = nullptr;
   unsigned long long* reduce_counts = nullptr;
   int gather_mode = -1;       // union kernel variant (-1: per-layout default)
+  uint32_t hot_rows = 0;      // relabelled rows kept in L2 by gather policy 3
   bool tma = false;           // gather successor rows with TMA gather4
   // locality relabelling (hanf_relabel.cu): the device works on rows;
   // order[row] = original id, perm[id] = row; dirty[g] = original-id
@@ -788,6 +789,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.est_index = e->est_rows ? nullptr : e->order;
   a.dirty_next = e->dirty[ng];
   a.peers = peer_rows(e, ng);
+  a.hot_rows = e->hot_rows;
   return a;
 }
 
@@ -1209,6 +1211,13 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       e->shard_relabel = true;
       e->sparse_ok = false;  // (the worklist needs a row-space CSR of the shard)
     }
+  }
+  if (e->relabel && !e->shard_relabel) {
+    // the first rows after degree relabelling take most gathers: the
+    // policy-3 sweep keeps this many bytes of them in L2 (evict_last)
+    uint64_t mb = 64;
+    if (const char* hm = std::getenv("HANF_HOT_MB")) mb = std::strtoull(hm, nullptr, 10);
+    e->hot_rows = static_cast<uint32_t>(std::min<uint64_t>(n, (mb << 20) / (e->pitch * 8)));
   }
 
   cudaStream_t helper = nullptr;  // upload stream: idle before any buffer is freed

@@ -239,6 +239,7 @@ struct UnionArgs {
   PeerRows peers;                  // sharded peer-push: also store written rows there
   const uint32_t* seg_live;        // skip sweeps over segmented tasks: segment s has work
   uint32_t seg_shift;              // (TaskBuild::seg_shift)
+  uint32_t hot_rows;               // gather policy 3: rows below are kept in L2 (evict_last)
 };
 
 struct EstimateArgs {

@@ -131,7 +131,7 @@ template <class Lay, bool kVec16>
 struct Gather<Lay, 0, kVec16> {
   uint32_t v[Lay::kLimbs];
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
-                                        uint32_t woff) {
+                                        uint32_t woff, uint64_t = 0) {
     load_chunk<Lay, kVec16>(v, cur + static_cast<uint64_t>(w) * words + woff);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
@@ -143,7 +143,7 @@ template <class Lay, bool kVec16>
 struct Gather<Lay, 10, kVec16> {
   uint32_t v[Lay::kLimbs];
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
-                                        uint32_t woff) {
+                                        uint32_t woff, uint64_t = 0) {
     load_chunk<Lay, kVec16, 1>(v, cur + static_cast<uint64_t>(w) * words + woff);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
@@ -155,7 +155,7 @@ template <class Lay, bool kVec16>
 struct Gather<Lay, 20, kVec16> {
   uint32_t v[Lay::kLimbs];
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
-                                        uint32_t woff) {
+                                        uint32_t woff, uint64_t = 0) {
     load_chunk<Lay, kVec16, 2>(v, cur + static_cast<uint64_t>(w) * words + woff);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
@@ -166,13 +166,29 @@ struct Gather<Lay, 20, kVec16> {
 template <class Lay, int POL>
 struct Gather128 {
   uint4 raw[Window128<Lay::kWords>::kLoads];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t) {
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t,
+                                        uint64_t = 0) {
     window128_load<Lay::kWords, POL>(raw, cur, w);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
     window128_extract<Lay, Lay::kWords>(x, raw, w);
   }
 };
+// policy 3: 16-byte windows with the L2 policy the caller picks per row
+// (hot rows evict_last, cold rows evict_first; UnionArgs::hot_rows)
+template <class Lay>
+struct Gather128Pol {
+  uint4 raw[Window128<Lay::kWords>::kLoads];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t,
+                                        uint64_t pol) {
+    window128_load_pol<Lay::kWords>(raw, cur, w, pol);
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
+    window128_extract<Lay, Lay::kWords>(x, raw, w);
+  }
+};
+template <class Lay, bool kVec16>
+struct Gather<Lay, 31, kVec16> : Gather128Pol<Lay> {};
 template <class Lay, bool kVec16>
 struct Gather<Lay, 1, kVec16> : Gather128<Lay, 0> {};
 template <class Lay, bool kVec16>
@@ -183,11 +199,30 @@ struct Gather<Lay, 21, kVec16> : Gather128<Lay, 2> {};
 template <class Lay, bool kVec16>
 struct Gather<Lay, 2, kVec16> {
   uint32_t raw[Window<Lay::kWords>::kLoads][8];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t) {
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t,
+                                        uint64_t = 0) {
     window_load<Lay::kWords>(raw, cur, w);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
     window_extract<Lay, Lay::kWords>(x, raw, w);
+  }
+};
+
+// GMODE 33: GMODE 3 with the per-row L2 policy of GMODE 31.
+template <class Lay, bool kVec16>
+struct Gather<Lay, 33, kVec16> {
+  static constexpr int K = (Lay::kWords + 3) / 4;
+  uint32_t raw[K][8];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t pitch,
+                                        uint32_t woff, uint64_t pol) {
+    const uint64_t* p = cur + static_cast<uint64_t>(w) * pitch + woff;
+    sfor<0, K>([&](auto I) { ldg256_pol(raw[decltype(I)::value], p + 4 * decltype(I)::value, pol); });
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
+    sfor<0, Lay::kLimbs>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      x[i] = raw[i / 8][i % 8];
+    });
   }
 };
 
@@ -198,7 +233,7 @@ struct Gather<Lay, 3, kVec16> {
   static constexpr int K = (Lay::kWords + 3) / 4;
   uint32_t raw[K][8];
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t pitch,
-                                        uint32_t woff) {
+                                        uint32_t woff, uint64_t = 0) {
     const uint64_t* p = cur + static_cast<uint64_t>(w) * pitch + woff;
     sfor<0, K>([&](auto I) { ldg256(raw[decltype(I)::value], p + 4 * decltype(I)::value); });
   }
@@ -293,7 +328,7 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
                                             bool lead, uint32_t v, bool stale,
                                             uint32_t (&acc)[Lay::kLimbs], uint32_t woff,
                                             uint32_t G, bool live, bool& any_changed,
-                                            OwnLoad own_load) {
+                                            OwnLoad own_load, uint64_t st_pol = 0) {
   constexpr int NL = Lay::kLimbs;
   const uint32_t words = args.pitch;
   if (live)  // (all-zero accumulators need no butterfly)
@@ -320,10 +355,14 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
     any_changed |= changed;
     if (changed || (lead && stale)) {
       const uint64_t off = static_cast<uint64_t>(v) * words + woff;
-      if (args.chunks == 1)
-        store_counter<Lay>(args.next + off, acc);
-      else
+      if (args.chunks == 1) {
+        if (st_pol)
+          store_counter_pol<Lay>(args.next + off, acc, st_pol);
+        else
+          store_counter<Lay>(args.next + off, acc);
+      } else {
         store_chunk<Lay, kVec16>(args.next + off, acc);
+      }
       // sharded peer-push: the same row into every peer's next generation
       for (uint32_t p = 0; p < args.peers.count; ++p) {
         if (args.chunks == 1)
@@ -399,6 +438,16 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
   const uint32_t* __restrict__ ids = args.tos + task.tos + lane;
   const uint32_t words = args.pitch;
   const uint32_t trips = task.trips;
+  constexpr bool kPol = GMODE / 10 == 3;
+  uint64_t pol_hot = 0, pol_cold = 0;
+  if constexpr (kPol) {
+    pol_hot = l2_policy_evict_last();
+    pol_cold = l2_policy_evict_first();
+  }
+  const uint32_t hot_rows = args.hot_rows;
+  auto ld_id = [&](const uint32_t* p) -> uint32_t {
+    if constexpr (kPol) return ld4_pol(p, pol_cold); else return ld_stream_u32(p);
+  };
 
   bool any_changed = false;
   for (uint32_t ch = 0; ch < args.chunks; ++ch) {
@@ -411,7 +460,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
     uint32_t wn[U];
     if (PF) {
 #pragma unroll
-      for (int j = 0; j < U; ++j) wn[j] = (j < trips) ? ld_stream_u32(ids + 32 * j) : zero_row;
+      for (int j = 0; j < U; ++j) wn[j] = (j < trips) ? ld_id(ids + 32 * j) : zero_row;
     }
     for (uint32_t i = 0; i < trips; i += U) {
       uint32_t w[U];
@@ -419,12 +468,12 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           w[j] = wn[j];
-          wn[j] = (i + U + j < trips) ? ld_stream_u32(ids + 32 * (i + U + j)) : zero_row;
+          wn[j] = (i + U + j < trips) ? ld_id(ids + 32 * (i + U + j)) : zero_row;
         }
       } else {
 #pragma unroll
         for (int j = 0; j < U; ++j)
-          w[j] = (i + j < trips) ? ld_stream_u32(ids + 32 * (i + j)) : zero_row;
+          w[j] = (i + j < trips) ? ld_id(ids + 32 * (i + j)) : zero_row;
       }
       if constexpr (SKIP) {
 #pragma unroll
@@ -447,7 +496,8 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
       }
       G_t g[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) g[j].issue(cur, w[j], words, woff);
+      for (int j = 0; j < U; ++j)
+        g[j].issue(cur, w[j], words, woff, w[j] < hot_rows ? pol_hot : pol_cold);
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         uint32_t y[NL];
@@ -459,9 +509,9 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
                              [&](uint32_t (&own)[NL], bool need) {
                                const uint32_t r = need ? v : zero_row;
                                G_t g;
-                               g.issue(cur, r, words, woff);
+                               g.issue(cur, r, words, woff, pol_cold);
                                g.extract(own, r);
-                             });
+                             }, pol_cold);
   }
   task_finish<Lay, kVec16>(args, task, hub, v, any_changed, lane);
 }
@@ -712,6 +762,8 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
   if (single && args.pitch % 4 == 0) switch (k.r * 1000 + k.nreg) {
       case 5032:
         if (variant == 30) return union_launch<5, 32, 4, 3, false, 4, true>(args, ch, s);
+        if (variant == 50) return union_launch<5, 32, 4, 33, false, 1, true>(args, ch, s);
+        if (variant == 51) return union_launch<5, 32, 4, 33, false, 4, true>(args, ch, s);
         return union_launch<5, 32, 4, 3, false, 1, true>(args, ch, s);
       case 5064:
         switch (variant) {
@@ -769,6 +821,8 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
           case 26: return union_launch<5, 64, 1, 1, false, 6, true>(args, ch, s);
           case 27: return union_launch<5, 64, 1, 1, false, 8, true>(args, ch, s);
           case 22: return union_launch<5, 64, 3, 1, false, 4>(args, ch, s);
+          case 50: return union_launch<5, 64, 3, 31, false, 5, true>(args, ch, s);
+          case 51: return union_launch<5, 64, 4, 31, false, 4, true>(args, ch, s);
           // U = 3, <= 48 registers (5 CTAs/SM), next-trip id prefetch: +2%
           // on config 2 and +1% on R-MAT 26 over 64 registers
           default: return union_launch<5, 64, 3, 1, false, 5, true>(args, ch, s);
