@@ -227,10 +227,15 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+template <bool kL1 = true>
 __device__ __forceinline__ uint4 ld16_pol(const uint4* p, uint64_t pol) {
   uint4 v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  if constexpr (kL1)
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  else
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ uint32_t ld4_pol(const uint32_t* p, uint64_t pol) {
@@ -240,7 +245,7 @@ __device__ __forceinline__ uint32_t ld4_pol(const uint32_t* p, uint64_t pol) {
   return v;
 }
 __device__ __forceinline__ void ldg256_pol(uint32_t (&v)[8], const uint64_t* p, uint64_t pol) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+  asm volatile("ld.global.nc.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
                  "=r"(v[6]), "=r"(v[7])
                : "l"(p), "l"(pol));
@@ -625,7 +630,7 @@ __device__ __forceinline__ void window128_load(uint4 (&raw)[Window128<NW>::kLoad
   });
 }
 
-template <int NW>
+template <int NW, bool kL1 = true>
 __device__ __forceinline__ void window128_load_pol(uint4 (&raw)[Window128<NW>::kLoads],
                                                    const uint64_t* base, uint32_t w,
                                                    uint64_t pol) {
@@ -633,7 +638,7 @@ __device__ __forceinline__ void window128_load_pol(uint4 (&raw)[Window128<NW>::k
   const uint4* p = reinterpret_cast<const uint4*>(base + (word & ~1ull));
   sfor<0, Window128<NW>::kLoads>([&](auto I) {
     constexpr int k = decltype(I)::value;
-    raw[k] = ld16_pol(p + k, pol);
+    raw[k] = ld16_pol<kL1>(p + k, pol);
   });
 }
 

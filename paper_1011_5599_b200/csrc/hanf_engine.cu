@@ -1236,6 +1236,17 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
 
   HANF_TRY(cudaSetDevice(cfg.device));
   configure_pool(cfg.device);
+  if (const char* pm = std::getenv("HANF_L2_PERSIST_MB")) {
+    // L2 set-aside for evict_last (persisting) lines: without it the
+    // policy-3 sweep's evict_last is an ordinary priority
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, cfg.device);
+    const size_t want = std::min<size_t>(static_cast<size_t>(maxp),
+                                         std::strtoull(pm, nullptr, 10) << 20);
+    HANF_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    if (std::getenv("HANF_PROFILE"))
+      std::fprintf(stderr, "[hanf] L2 persisting set-aside %zu of max %d bytes\n", want, maxp);
+  }
   if (const char* l2 = std::getenv("HANF_L2_FETCH"))
     HANF_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::atoi(l2)));
   HANF_TRY(streams().get(cfg.device, &e->stream));

@@ -176,19 +176,39 @@ struct Gather128 {
 };
 // policy 3: 16-byte windows with the L2 policy the caller picks per row
 // (hot rows evict_last, cold rows evict_first; UnionArgs::hot_rows)
-template <class Lay>
+template <class Lay, bool kL1>
 struct Gather128Pol {
   uint4 raw[Window128<Lay::kWords>::kLoads];
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t,
                                         uint64_t pol) {
-    window128_load_pol<Lay::kWords>(raw, cur, w, pol);
+    window128_load_pol<Lay::kWords, kL1>(raw, cur, w, pol);
+  }
+  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
+    window128_extract<Lay, Lay::kWords>(x, raw, w);
+  }
+};
+// policy 5: hot rows L1-allocating + evict_last, cold rows sector-granular
+// (L1::no_allocate) + evict_first
+template <class Lay>
+struct Gather128Split {
+  uint4 raw[Window128<Lay::kWords>::kLoads];
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t hot, uint32_t,
+                                        uint64_t pol) {
+    if (w < hot)
+      window128_load_pol<Lay::kWords, true>(raw, cur, w, pol);
+    else
+      window128_load_pol<Lay::kWords, false>(raw, cur, w, pol);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
     window128_extract<Lay, Lay::kWords>(x, raw, w);
   }
 };
 template <class Lay, bool kVec16>
-struct Gather<Lay, 31, kVec16> : Gather128Pol<Lay> {};
+struct Gather<Lay, 51, kVec16> : Gather128Split<Lay> {};
+template <class Lay, bool kVec16>
+struct Gather<Lay, 31, kVec16> : Gather128Pol<Lay, true> {};
+template <class Lay, bool kVec16>
+struct Gather<Lay, 41, kVec16> : Gather128Pol<Lay, false> {};
 template <class Lay, bool kVec16>
 struct Gather<Lay, 1, kVec16> : Gather128<Lay, 0> {};
 template <class Lay, bool kVec16>
@@ -438,7 +458,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
   const uint32_t* __restrict__ ids = args.tos + task.tos + lane;
   const uint32_t words = args.pitch;
   const uint32_t trips = task.trips;
-  constexpr bool kPol = GMODE / 10 == 3;
+  constexpr bool kPol = GMODE / 10 == 3 || GMODE / 10 == 4 || GMODE / 10 == 5;
   uint64_t pol_hot = 0, pol_cold = 0;
   if constexpr (kPol) {
     pol_hot = l2_policy_evict_last();
@@ -497,7 +517,8 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
       G_t g[U];
 #pragma unroll
       for (int j = 0; j < U; ++j)
-        g[j].issue(cur, w[j], words, woff, w[j] < hot_rows ? pol_hot : pol_cold);
+        g[j].issue(cur, w[j], GMODE / 10 == 5 ? hot_rows : words, woff,
+                   w[j] < hot_rows ? pol_hot : pol_cold);
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         uint32_t y[NL];
@@ -823,6 +844,8 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
           case 22: return union_launch<5, 64, 3, 1, false, 4>(args, ch, s);
           case 50: return union_launch<5, 64, 3, 31, false, 5, true>(args, ch, s);
           case 51: return union_launch<5, 64, 4, 31, false, 4, true>(args, ch, s);
+          case 52: return union_launch<5, 64, 3, 41, false, 5, true>(args, ch, s);
+          case 53: return union_launch<5, 64, 3, 51, false, 5, true>(args, ch, s);
           // U = 3, <= 48 registers (5 CTAs/SM), next-trip id prefetch: +2%
           // on config 2 and +1% on R-MAT 26 over 64 registers
           default: return union_launch<5, 64, 3, 1, false, 5, true>(args, ch, s);
