@@ -480,6 +480,8 @@ def main():
 
     total_ms, step_launches, clocks = dense_step_timing(engine, dev, args.steps, args.warmup,
                                                         flush, sharded, world)
+    (sharded.reset if sharded is not None else engine.reset)()
+    step_modified = (sharded.step() if sharded is not None else engine.step()).modified
     phases = phase_timing(engine, dev, flush, max(3, min(args.steps, 10)), sharded)
     profile = run_profile(engine, n) if world == 1 else None
     if world > 1:
@@ -502,6 +504,22 @@ def main():
         B = algorithmic_bytes(n, a, words)
     achieved = B / (union_ms / 1e3) / 1e9 if union_ms > 0 else None
     traffic = ncu_traffic(args.config) if world == 1 else None
+    nvlink = None
+    if world > 1:
+        # peer-push bytes a rank sends per dense step: every row its sweep
+        # writes (the changed rows of its range; iteration 1 has no stale
+        # rows) to each of the G-1 peers, plus the estimates of relabelled
+        # rows and the published bitmap words and block sums
+        lo, hi = sharded.ranges[rank]
+        bufs = engine.device_buffers()
+        changed = step_modified * (hi - lo) / n
+        row = 8 * int(bufs.row_pitch) + (8 if bufs.relabelled else 0)
+        per_peer = changed * row + 2 * 8 * -(-(hi - lo) // 64)
+        sent = (world - 1) * per_peer
+        nvlink = {"bytes_per_gpu_per_step": sent, "achieved": sent / (total_ms / args.steps / 1e3) / 1e9,
+                  "peak": 900.0, "unit": "GB/s", "frac": sent / (total_ms / args.steps / 1e3) / 900e9,
+                  "note": "NVLink 5 per-direction peak; bytes from the step's modified count "
+                          "(rows changed in this rank's range x row bytes x (G-1) peers)"}
     if sharded is not None:
         sharded.close()
     else:
@@ -587,6 +605,7 @@ def main():
                                    "estimator)",
                          "kernel_ms": union_ms, "algorithmic_bytes": B,
                          "peak_source": peak_src, "phases_ms": phases},
+            "nvlink": nvlink,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "config2": extra2,

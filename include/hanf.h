@@ -115,6 +115,23 @@ hanf_status hanf_sketch_params_make(uint32_t bucket_bits, uint64_t seed,
 hanf_status hanf_create(const hanf_graph_view* graph, const hanf_config* cfg,
                         hanf_engine** out);
 void hanf_destroy(hanf_engine* engine);
+/* (new) One engine over several GPUs of this process,
+ * driven by one host thread - the reference keeps its parallelism inside
+ * NfEngine::step (engine.hpp:157, parallel.hpp:16-48) and so does this
+ * handle.  Nodes are split into `count` contiguous ranges (multiples of 64),
+ * one shard engine per devices[k] (repeats allowed), attached to each other
+ * for the peer-push exchange (peer access enabled between distinct
+ * devices): each step, every shard's union kernels store the rows they
+ * write into all peers' next generation over NVLink, the shards' streams
+ * wait on each other's compute events (a device-side barrier, no host
+ * round trip), and each shard commits the full arrays.  The handle accepts
+ * hanf_step, hanf_step_launch / _complete, hanf_run_to_stabilisation,
+ * hanf_sum_estimates, hanf_read_counters, hanf_save_counters, hanf_reset,
+ * hanf_reseed, the accessors and hanf_destroy; results are bit-identical
+ * to hanf_create's.  count in [1, HANF_MAX_PEERS + 1]; graphs with fewer
+ * than 64 * count nodes get one shard. */
+hanf_status hanf_create_multi(const hanf_graph_view* graph, const hanf_config* cfg,
+                              const int32_t* devices, uint32_t count, hanf_engine** out);
 /* (new) `runs` independent runs in one engine, run k under
  * seeds[k] (main.cpp:263-283 multirun): the graph is lifted to `runs`
  * copies (row v*runs + k) so one gather serves a node's runs together.

@@ -26,8 +26,23 @@
 
 #include "../hanf.h"
 
+// With the reference's headers on the include path, its exception types
+// are used directly (errors.hpp:8-20): a caller catching
+// hyperanf::GuardError catches this engine's iteration-cap error too.
+#if defined(__has_include)
+#if __has_include(<hyperanf/errors.hpp>)
+#include <hyperanf/errors.hpp>
+#define HANF_HAVE_REFERENCE_ERRORS 1
+#endif
+#endif
+
 namespace hyperanf_b200 {
 
+#ifdef HANF_HAVE_REFERENCE_ERRORS
+using ParseError = hyperanf::ParseError;
+using IoError = hyperanf::IoError;
+using GuardError = hyperanf::GuardError;
+#else
 struct ParseError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -37,6 +52,7 @@ struct IoError : std::runtime_error {
 struct GuardError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+#endif
 struct DeviceError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -79,6 +95,10 @@ struct EngineConfig {
   bool exact_sum = true;
   std::uint64_t shard_begin = 0, shard_end = 0;
   std::uint32_t shard_count = 0;
+  // several GPUs of this process, one node-range shard each (repeats
+  // allowed): NfEngine then drives them all (hanf_create_multi), as the
+  // reference's NfEngine keeps its threads internal (engine.hpp:157)
+  std::vector<int> devices;
 
   hanf_config to_c() const {
     hanf_config c;
@@ -182,7 +202,11 @@ class NfEngine {
   NfEngine(const G& graph, EngineConfig cfg) : cfg_(cfg), n_(graph.num_nodes()) {
     const hanf_graph_view v = view_of(graph);
     const hanf_config c = cfg_.to_c();
-    check(hanf_create(&v, &c, &h_));
+    if (cfg_.devices.empty())
+      check(hanf_create(&v, &c, &h_));
+    else
+      check(hanf_create_multi(&v, &c, cfg_.devices.data(),
+                              static_cast<std::uint32_t>(cfg_.devices.size()), &h_));
     hanf_sketch_params p;
     check(hanf_params(h_, &p));
     params_ = SketchParams::from_c(p);
@@ -193,11 +217,17 @@ class NfEngine {
 
   const SketchParams& params() const noexcept { return params_; }
   const EngineConfig& config() const noexcept { return cfg_; }
-  // CounterArray::data() of the current generation, reference packing
-  std::vector<std::uint64_t> counters() const {
-    std::vector<std::uint64_t> out(static_cast<size_t>(n_) * params_.words);
-    check(hanf_read_counters(h_, 0, n_, out.data()));
-    return out;
+  // NfEngine::counters() (engine.hpp:94): the current generation in the
+  // reference packing (CounterArray::data(), hll.hpp:224), as a stable
+  // reference to a host mirror that is refreshed from HBM only after the
+  // counters changed (step, reset, reseed, restore)
+  const std::vector<std::uint64_t>& counters() const {
+    if (mirror_version_ != version_) {
+      mirror_.resize(static_cast<size_t>(n_) * params_.words);
+      check(hanf_read_counters(h_, 0, n_, mirror_.data()));
+      mirror_version_ = version_;
+    }
+    return mirror_;
   }
   std::vector<std::uint64_t> counter(std::uint64_t i) const {
     std::vector<std::uint64_t> out(params_.words);
@@ -221,10 +251,12 @@ class NfEngine {
   }
   IterationReport step() {
     hanf_iteration_report r;
+    ++version_;
     check(hanf_step(h_, &r));
     return {r.sum, r.modified};
   }
   NfEstimate run_to_stabilisation() {
+    ++version_;
     NfEstimate est;
     est.n = n_;
     est.m = params_.registers;
@@ -248,9 +280,13 @@ class NfEngine {
     est.wall_seconds = wall;
     return est;
   }
-  void reset() { check(hanf_reset(h_)); }
+  void reset() {
+    ++version_;
+    check(hanf_reset(h_));
+  }
   // the next run of a multi-seed experiment on the uploaded graph (new)
   void reseed(std::uint64_t seed) {
+    ++version_;
     check(hanf_reseed(h_, seed));
     cfg_.seed = seed;
     params_.seed = seed;
@@ -259,6 +295,7 @@ class NfEngine {
   void save_counters(const std::string& path) const { check(hanf_save_counters(h_, path.c_str())); }
   // resume from an HCA1 snapshot taken at `iteration` (new; hll.hpp:288-303 format)
   void restore_counters(const std::string& path, std::uint64_t iteration) {
+    ++version_;
     check(hanf_restore_counters(h_, path.c_str(), iteration));
     hanf_sketch_params p;
     check(hanf_params(h_, &p));
@@ -272,6 +309,9 @@ class NfEngine {
   std::uint64_t n_ = 0;
   SketchParams params_;
   hanf_engine* h_ = nullptr;
+  std::uint64_t version_ = 0;                      // bumped by every mutating call
+  mutable std::uint64_t mirror_version_ = ~0ull;
+  mutable std::vector<std::uint64_t> mirror_;
 };
 
 // One node range of a multi-GPU run (new; the reference has no distributed

@@ -67,6 +67,8 @@ _SIGNATURES = {
     "hanf_config_init": [POINTER(Config)],
     "hanf_sketch_params_make": [c_uint32, c_uint64, c_uint32, POINTER(SketchParamsC)],
     "hanf_create": [POINTER(GraphView), POINTER(Config), POINTER(_P)],
+    "hanf_create_multi": [POINTER(GraphView), POINTER(Config), POINTER(c_int32), c_uint32,
+                          POINTER(_P)],
     "hanf_reset": [_P],
     "hanf_reseed": [_P, c_uint64],
     "hanf_create_batch": [POINTER(GraphView), POINTER(Config), POINTER(c_uint64), c_uint32,

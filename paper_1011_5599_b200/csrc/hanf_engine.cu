@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <iostream>
@@ -360,6 +361,10 @@ struct hanf_engine {
   double* est_gen[2] = {nullptr, nullptr};
   double* inbox[2] = {nullptr, nullptr};     // block sums of all shards, per generation
   bool attached = false;
+  // hanf_create_multi: this handle owns one attached shard engine per
+  // device entry and drives them from one host thread (no kernels of its own)
+  std::vector<hanf_engine*> parts;
+  std::vector<cudaEvent_t> part_ev;  // per part: its compute (then reduce) is done
   uint32_t npeers = 0;
   uint8_t* peer_base[hanf::kMaxPeers] = {};
   bool peer_ipc[hanf::kMaxPeers] = {};       // opened with cudaIpcOpenMemHandle
@@ -387,6 +392,21 @@ struct hanf_engine {
                    std::chrono::duration<double, std::milli>(now - t0).count());
       t0 = now;
     };
+    if (!parts.empty()) {
+      // unmap every peer arena before any part frees its own
+      for (hanf_engine* p : parts) {
+        cudaSetDevice(p->device);
+        cudaStreamSynchronize(p->stream);
+        p->detach_peers();
+      }
+      for (size_t i = 0; i < parts.size(); ++i) {
+        cudaSetDevice(parts[i]->device);
+        if (part_ev[i]) cudaEventDestroy(part_ev[i]);
+        delete parts[i];
+      }
+      parts.clear();
+      return;
+    }
     if (device >= 0) cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     phase("sync");
@@ -546,7 +566,7 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   // single-GPU steps: the bitmap the next step writes (this step's mod_cur,
   // dead once the sweep has run) is cleared in the same pass.  Shards keep
   // their memset: peers publish into those words during their next step.
-  const bool sharded = e->lo != 0 || e->hi != e->n;
+  const bool sharded = e->lo != 0 || e->hi != e->n || !e->parts.empty();
   if (in_step && !sharded && e->batch == 1) f.clear = e->mod[e->cur];
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
@@ -1073,6 +1093,12 @@ hanf_status step_enqueue(hanf_engine* e) {
   return HANF_OK;
 }
 
+}  // namespace
+
+namespace {  // hanf_create_multi's step (defined with it, below)
+hanf_status multi_step_enqueue(hanf_engine* e);
+hanf_status multi_step_complete(hanf_engine* e, hanf_iteration_report* rep);
+hanf_status multi_reset(hanf_engine* e, const uint64_t* seed);
 }  // namespace
 
 extern "C" {
@@ -1754,6 +1780,7 @@ void hanf_destroy(hanf_engine* e) { delete e; }
 hanf_status hanf_reset(hanf_engine* e) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
   if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
+  if (!e->parts.empty()) return multi_reset(e, nullptr);
   if (e->n == 0) {
     e->t = 0;
     return HANF_OK;
@@ -1802,6 +1829,8 @@ hanf_status hanf_save_counters(hanf_engine* e, const char* path) {
 hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t iteration) {
   if (!e || !path) return fail(HANF_INVALID_ARGUMENT, "null argument");
   if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
+  if (!e->parts.empty())
+    return fail(HANF_INVALID_ARGUMENT, "restore into a multi-device engine is not supported");
   if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: no single counter array");
   std::FILE* f = std::fopen(path, "rb");
   if (!f) return fail(HANF_IO_ERROR, std::string("cannot open: ") + path);
@@ -1872,6 +1901,10 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
 
 hanf_status hanf_reseed(hanf_engine* e, uint64_t seed) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (!e->parts.empty()) {
+    if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
+    return multi_reset(e, &seed);
+  }
   if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: seeds are fixed at creation");
   e->cfg.seed = seed;
   e->params.seed = seed;  // only the seeding hash reads it (engine.hpp:84-85)
@@ -1890,6 +1923,11 @@ hanf_status hanf_step_launch(hanf_engine* e) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
   if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: use hanf_run_batch");
   if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
+  if (!e->parts.empty()) {
+    const hanf_status st = multi_step_enqueue(e);
+    if (st == HANF_OK) e->step_pending = true;
+    return st;
+  }
   if (e->n == 0) {
     e->step_pending = true;
     return HANF_OK;
@@ -1904,6 +1942,7 @@ hanf_status hanf_step_complete(hanf_engine* e, hanf_iteration_report* rep) {
   if (!e || !rep) return fail(HANF_INVALID_ARGUMENT, "null argument");
   if (!e->step_pending) return fail(HANF_INVALID_ARGUMENT, "no launched step");
   e->step_pending = false;
+  if (!e->parts.empty()) return multi_step_complete(e, rep);
   if (e->n == 0) {
     rep->sum = 0.0;
     rep->modified = 0;
@@ -1916,6 +1955,11 @@ hanf_status hanf_step_complete(hanf_engine* e, hanf_iteration_report* rep) {
 hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
   if (!e || !rep) return fail(HANF_INVALID_ARGUMENT, "null argument");
   if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
+  if (!e->parts.empty()) {
+    hanf_status st = multi_step_enqueue(e);
+    if (st != HANF_OK) return st;
+    return multi_step_complete(e, rep);
+  }
   if (e->batch > 1) return fail(HANF_INVALID_ARGUMENT, "batched engine: use hanf_run_batch");
   if (e->n == 0) {                       // engine.hpp:124
     rep->sum = 0.0;
@@ -1931,6 +1975,7 @@ hanf_status hanf_step(hanf_engine* e, hanf_iteration_report* rep) {
 }
 
 hanf_status hanf_shard_compute(hanf_engine* e) {
+  if (e && !e->parts.empty()) return fail(HANF_INVALID_ARGUMENT, "not a shard engine");
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
   if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
   if (e->n == 0) return HANF_OK;
@@ -1989,6 +2034,7 @@ hanf_status hanf_shard_commit(hanf_engine* e, hanf_iteration_report* rep) {
 
 // ---- peer-push exchange ----------------------------------------------------
 hanf_status hanf_shard_export(hanf_engine* e, hanf_shard_peer* out) {
+  if (e && !e->parts.empty()) return fail(HANF_INVALID_ARGUMENT, "not a shard engine");
   if (!e || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
   std::memset(out, 0, sizeof(*out));
   out->n = e->n;
@@ -2167,6 +2213,160 @@ hanf_status hanf_shard_detach(hanf_engine* e) {
   return HANF_OK;
 }
 
+// ---- one handle over several GPUs (hanf_create_multi) ---------------------
+}  // extern "C"
+namespace {
+hanf_status multi_cross_wait(hanf_engine* e) {
+  const size_t G = e->parts.size();
+  for (size_t k = 0; k < G; ++k) {
+    HANF_CUDA(cudaSetDevice(e->parts[k]->device));
+    for (size_t j = 0; j < G; ++j)
+      if (j != k) HANF_CUDA(cudaStreamWaitEvent(e->parts[k]->stream, e->part_ev[j], 0));
+  }
+  return HANF_OK;
+}
+
+// Every part computes its node range on its own stream (its union kernels
+// push the rows they write into the peers' arenas over NVLink peer memory,
+// then publish bitmap words and block sums); each stream then waits on the
+// other parts' compute events - a device-side barrier, no host round trip -
+// relabelled parts re-sum their slice of the blocks behind a second such
+// barrier, and every part enqueues its commit.
+hanf_status multi_step_enqueue(hanf_engine* e) {
+  const size_t G = e->parts.size();
+  for (size_t k = 0; k < G; ++k) {
+    hanf_status st = hanf_shard_compute(e->parts[k]);
+    if (st != HANF_OK) return st;
+    HANF_CUDA(cudaSetDevice(e->parts[k]->device));
+    HANF_CUDA(cudaEventRecord(e->part_ev[k], e->parts[k]->stream));
+  }
+  hanf_status st = multi_cross_wait(e);
+  if (st != HANF_OK) return st;
+  if (e->parts[0]->shard_relabel) {
+    for (size_t k = 0; k < G; ++k) {
+      st = hanf_shard_reduce(e->parts[k]);
+      if (st != HANF_OK) return st;
+      HANF_CUDA(cudaSetDevice(e->parts[k]->device));
+      HANF_CUDA(cudaEventRecord(e->part_ev[k], e->parts[k]->stream));
+    }
+    st = multi_cross_wait(e);
+    if (st != HANF_OK) return st;
+  }
+  for (size_t k = 0; k < G; ++k) {
+    HANF_CUDA(cudaSetDevice(e->parts[k]->device));
+    st = commit_enqueue(e->parts[k]);
+    if (st != HANF_OK) return st;
+  }
+  return HANF_OK;
+}
+
+// Every part's commit reduces the same full arrays: the reports agree.
+hanf_status multi_step_complete(hanf_engine* e, hanf_iteration_report* rep) {
+  hanf_iteration_report first{};
+  for (size_t k = 0; k < e->parts.size(); ++k) {
+    HANF_CUDA(cudaSetDevice(e->parts[k]->device));
+    hanf_iteration_report r{};
+    const hanf_status st = commit_complete(e->parts[k], &r);
+    if (st != HANF_OK) return st;
+    if (k == 0)
+      first = r;
+    else if (r.modified != first.modified)
+      return fail(HANF_CUDA_ERROR, "shard engines disagree on the modified count");
+  }
+  e->t = e->parts[0]->t;
+  e->last_sum = e->parts[0]->last_sum;
+  e->last_count = e->parts[0]->last_count;
+  *rep = first;
+  return HANF_OK;
+}
+
+hanf_status multi_sync(hanf_engine* e) {
+  for (hanf_engine* p : e->parts) {
+    HANF_CUDA(cudaSetDevice(p->device));
+    HANF_CUDA(cudaStreamSynchronize(p->stream));
+  }
+  return HANF_OK;
+}
+
+hanf_status multi_reset(hanf_engine* e, const uint64_t* seed) {
+  hanf_status st = multi_sync(e);  // no part may still push into a peer being re-seeded
+  if (st != HANF_OK) return st;
+  for (hanf_engine* p : e->parts) {
+    st = seed ? hanf_reseed(p, *seed) : hanf_reset(p);
+    if (st != HANF_OK) return st;
+  }
+  st = multi_sync(e);
+  if (st != HANF_OK) return st;
+  if (seed) {
+    e->cfg.seed = *seed;
+    e->params.seed = *seed;
+  }
+  e->t = 0;
+  e->last_sum = e->parts[0]->last_sum;
+  e->last_count = e->n;
+  return HANF_OK;
+}
+}  // namespace
+extern "C" {
+
+hanf_status hanf_create_multi(const hanf_graph_view* g, const hanf_config* cfg,
+                              const int32_t* devices, uint32_t count, hanf_engine** out) {
+  if (!g || !cfg || !devices || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (count < 1 || count > HANF_MAX_PEERS + 1)
+    return fail(HANF_INVALID_ARGUMENT, "hanf_create_multi takes 1.." +
+                                           std::to_string(HANF_MAX_PEERS + 1) + " devices");
+  if (cfg->shard_begin || cfg->shard_end)
+    return fail(HANF_INVALID_ARGUMENT, "hanf_create_multi makes the shards itself");
+  const uint64_t n = g->n;
+  if (count == 1 || n < 64ull * count) {  // one shard (tiny graphs: no empty shards)
+    hanf_config c = *cfg;
+    c.device = devices[0];
+    return hanf_create(g, &c, out);
+  }
+  // contiguous ranges of ceil(n / count) nodes rounded up to 64 (whole
+  // bitmap words and blocks); n % (64 count) == 0 gives equal shards, which
+  // may relabel (interleaved by degree)
+  uint64_t per = (n + count - 1) / count;
+  per = (per + 63) / 64 * 64;
+  std::unique_ptr<hanf_engine> m(new (std::nothrow) hanf_engine());
+  if (!m) return fail(HANF_OUT_OF_MEMORY, "engine allocation failed");
+  m->device = -1;
+  for (uint32_t k = 0; k < count; ++k) {
+    hanf_config c = *cfg;
+    c.device = devices[k];
+    c.shard_begin = std::min<uint64_t>(n, k * per);
+    c.shard_end = std::min<uint64_t>(n, (k + 1) * per);
+    c.shard_count = count;
+    hanf_engine* part = nullptr;
+    hanf_status st = hanf_create(g, &c, &part);
+    if (st != HANF_OK) return st;  // (m's destructor frees the parts made so far)
+    m->parts.push_back(part);
+    m->part_ev.push_back(nullptr);
+    HANF_CUDA(cudaSetDevice(devices[k]));
+    HANF_CUDA(cudaEventCreateWithFlags(&m->part_ev.back(), cudaEventDisableTiming));
+  }
+  for (uint32_t k = 1; k < count; ++k)
+    if (m->parts[k]->shard_relabel != m->parts[0]->shard_relabel)
+      return fail(HANF_INVALID_ARGUMENT, "shards disagree on relabelling");
+  for (uint32_t k = 0; k < count; ++k) {
+    const hanf_status st = hanf_shard_attach_local(m->parts[k], m->parts.data(), count, k);
+    if (st != HANF_OK) return st;
+  }
+  m->cfg = *cfg;
+  m->params = m->parts[0]->params;
+  m->n = n;
+  m->lo = 0;
+  m->hi = n;
+  m->blocks = m->parts[0]->blocks;
+  m->words = m->parts[0]->words;
+  m->pitch = m->parts[0]->pitch;
+  m->last_sum = m->parts[0]->last_sum;
+  m->last_count = n;
+  *out = m.release();
+  return HANF_OK;
+}
+
 hanf_status hanf_run_to_stabilisation(hanf_engine* e, double* values, uint64_t* modified,
                                       uint64_t capacity, uint64_t* length, double* wall) {
   if (!e || !length) return fail(HANF_INVALID_ARGUMENT, "null argument");
@@ -2274,6 +2474,7 @@ hanf_status hanf_estimate_nf(const hanf_graph_view* g, const hanf_config* cfg, d
 hanf_status hanf_read_counters(hanf_engine* e, uint64_t first, uint64_t count, uint64_t* dst) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
   if (e->step_pending) return fail(HANF_INVALID_ARGUMENT, "a launched step is not complete");
+  if (!e->parts.empty()) return hanf_read_counters(e->parts[0], first, count, dst);
   if (first > e->n || count > e->n - first)
     return fail(HANF_OUT_OF_RANGE, "counter index out of range");
   if (count == 0) return HANF_OK;
@@ -2318,7 +2519,7 @@ hanf_status hanf_iteration(const hanf_engine* e, uint64_t* t) {
 
 hanf_status hanf_systolic_active(const hanf_engine* e, int32_t* active) {
   if (!e || !active) return fail(HANF_INVALID_ARGUMENT, "null argument");
-  *active = e->systolic ? 1 : 0;
+  *active = (e->parts.empty() ? e : e->parts[0])->systolic ? 1 : 0;
   return HANF_OK;
 }
 
@@ -2330,18 +2531,25 @@ hanf_status hanf_num_nodes(const hanf_engine* e, uint64_t* n) {
 
 hanf_status hanf_stream(const hanf_engine* e, void** stream) {
   if (!e || !stream) return fail(HANF_INVALID_ARGUMENT, "null argument");
-  *stream = static_cast<void*>(e->stream);
+  // (multi-device handles: the first part's stream)
+  *stream = static_cast<void*>(e->parts.empty() ? e->stream : e->parts[0]->stream);
   return HANF_OK;
 }
 
 hanf_status hanf_launch_count(const hanf_engine* e, uint64_t* launches) {
   if (!e || !launches) return fail(HANF_INVALID_ARGUMENT, "null argument");
   *launches = e->launches;
+  for (const hanf_engine* p : e->parts) *launches += p->launches;
   return HANF_OK;
 }
 
 hanf_status hanf_set_timing(hanf_engine* e, int32_t enable) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  for (hanf_engine* p : e->parts) {  // multi-device: per part (hanf_timing reports the first)
+    const hanf_status st = hanf_set_timing(p, enable);
+    if (st != HANF_OK) return st;
+  }
+  if (!e->parts.empty()) return HANF_OK;
   HANF_CUDA(cudaSetDevice(e->device));
   for (auto& x : e->ev)
     if (!x) HANF_CUDA(cudaEventCreate(&x));
@@ -2354,6 +2562,7 @@ hanf_status hanf_set_timing(hanf_engine* e, int32_t enable) {
 hanf_status hanf_timing(const hanf_engine* e, double* union_ms, double* estimate_ms,
                         double* reduce_ms, uint64_t* steps) {
   if (!e) return fail(HANF_INVALID_ARGUMENT, "null engine");
+  if (!e->parts.empty()) e = e->parts[0];
   if (union_ms) *union_ms = e->union_ms;
   if (estimate_ms) *estimate_ms = e->estimate_ms;
   if (reduce_ms) *reduce_ms = e->reduce_ms;
@@ -2375,6 +2584,7 @@ hanf_status hanf_unpin_host(const void* p) {
 
 hanf_status hanf_device_buffers(hanf_engine* e, hanf_buffers* out) {
   if (!e || !out) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (!e->parts.empty()) return fail(HANF_INVALID_ARGUMENT, "multi-device engine: no single buffer set");
   const int ng = 1 - e->cur;
   out->next_counters = e->cnt[ng];
   out->next_modified = e->mod[ng];

@@ -52,6 +52,9 @@ class EngineConfig:
     shard_begin: int = 0
     shard_end: int = 0
     shard_count: int = 0            # peer-push shards: allows relabelled shards
+    # several GPUs of this process, one node-range shard each (repeats
+    # allowed): the engine drives them all (hanf_create_multi)
+    devices: tuple = ()
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()
@@ -140,7 +143,13 @@ class NfEngine:
         self._h = c_void_p()
         view = graph.view()
         ccfg = cfg.to_c()
-        check(lib().hanf_create(ctypes.byref(view), ctypes.byref(ccfg), ctypes.byref(self._h)))
+        if cfg.devices:
+            devs = (c_int32 * len(cfg.devices))(*cfg.devices)
+            check(lib().hanf_create_multi(ctypes.byref(view), ctypes.byref(ccfg), devs,
+                                          len(cfg.devices), ctypes.byref(self._h)))
+        else:
+            check(lib().hanf_create(ctypes.byref(view), ctypes.byref(ccfg),
+                                    ctypes.byref(self._h)))
         p = _lib.SketchParamsC()
         check(lib().hanf_params(self._h, ctypes.byref(p)))
         self._params = SketchParams._from_c(p)

@@ -59,6 +59,36 @@ void lockstep(const hyperanf::Graph& g, const hyperanf::EngineConfig& cfg, const
            std::string(name) + " interpolated effective diameter");
   }
 }
+// hanf_create_multi through the drop-in: EngineConfig::devices lists one
+// device per shard (here repeats of device 0: one GPU on the test box)
+void lockstep_multi(const hyperanf::Graph& g, const hyperanf::EngineConfig& cfg,
+                    std::vector<int> devices, const std::string& name) {
+  hyperanf::NfEngine ref(g, cfg);
+  hyperanf_b200::EngineConfig bc = hyperanf_b200::from_reference(cfg);
+  bc.devices = devices;
+  hyperanf_b200::NfEngine gpu(g, bc);
+  const auto& rc0 = ref.counters();
+  expect(ref.sum_estimates() == gpu.sum_estimates(), name + " N(0)");
+  expect(std::vector<std::uint64_t>(rc0.data(), rc0.data() + rc0.word_count()) == gpu.counters(),
+         name + " seeded counters");
+  for (std::uint64_t t = 1; t <= g.num_nodes() + 1; ++t) {
+    const auto a = ref.step();
+    const auto b = gpu.step();
+    const auto& c = ref.counters();
+    const bool same = a.sum == b.sum && a.modified == b.modified &&
+                      std::vector<std::uint64_t>(c.data(), c.data() + c.word_count()) ==
+                          gpu.counters() &&
+                      ref.iteration() == gpu.iteration();
+    expect(same, name + " step " + std::to_string(t));
+    if (!same || a.modified == 0) break;
+  }
+  const auto ea = hyperanf::estimate_nf(g, cfg);
+  gpu.reset();
+  const auto eb = gpu.run_to_stabilisation();
+  expect(ea.values == eb.values && ea.modified == eb.modified, name + " reset + run");
+  const auto ec = hyperanf_b200::estimate_nf(g, bc);
+  expect(ea.values == ec.values, name + " estimate_nf");
+}
 }  // namespace
 
 int main() {
@@ -102,7 +132,7 @@ int main() {
     hyperanf_b200::estimate_nf(hyperanf::gen_clique_path(4, 8),
                                hyperanf_b200::from_reference(capped));
     expect(false, "iteration cap not enforced");
-  } catch (const hyperanf_b200::GuardError&) {
+  } catch (const hyperanf::GuardError&) {  // the reference's own type (aliased)
   }
   // exact NF (oracle.hpp) against the reference's all-pairs BFS
   for (const auto& g : {hyperanf::gen_uniform_random(2000, 4, 3), hyperanf::gen_clique_path(20, 9)}) {
@@ -184,6 +214,19 @@ int main() {
       expect(same, "peer-push shards x" + std::to_string(k));
       for (auto* s : shards) s->detach();
     }
+  }
+  {  // one engine over several devices (hanf_create_multi), plain and
+     // relabelled (interleaved) shards
+    hyperanf::EngineConfig c;
+    c.bucket_bits = 6;
+    c.seed = 9;
+    const auto g = hyperanf::gen_uniform_random(4096, 7.0, 23);
+    lockstep_multi(g, c, {0, 0}, "multi x2");
+    lockstep_multi(g, c, {0, 0, 0}, "multi x3");
+    setenv("HANF_RELABEL", "1", 1);
+    lockstep_multi(g, c, {0, 0, 0, 0}, "multi x4 relabelled");
+    unsetenv("HANF_RELABEL");
+    lockstep_multi(hyperanf::gen_uniform_random(100, 3.0, 2), c, {0, 0}, "multi tiny (one shard)");
   }
   std::printf("dropin_test: %zu graphs, %d failures\n", cases.size(), failures);
   return failures == 0 ? 0 : 1;

@@ -214,3 +214,18 @@ def test_diameter_interval_and_aggregate(hanf):
     assert len(rep.per_run) == 2 and rep.stddev.spid >= 0.0
     with pytest.raises(ValueError):
         hanf.aggregate_runs(runs[:1])
+
+
+def test_create_multi_validates_before_device_work(hanf):
+    """hanf_create_multi: device count in [1, 8] and no caller-made shard
+    range; rejected with HANF_INVALID_ARGUMENT before any device call."""
+    from paper_1011_5599_b200 import _lib
+    g = hanf.gen_uniform_random(100, 3, 1)
+    view = g.view()
+    for count, shard in [(0, 0), (9, 0), (2, 64)]:
+        cfg = hanf.EngineConfig(bucket_bits=6, shard_begin=shard, shard_end=2 * shard).to_c()
+        devs = (ctypes.c_int32 * 9)(*([0] * 9))
+        h = ctypes.c_void_p()
+        st = hanf.lib().hanf_create_multi(ctypes.byref(view), ctypes.byref(cfg), devs, count,
+                                          ctypes.byref(h))
+        assert st == _lib.INVALID_ARGUMENT and not h.value
