@@ -368,7 +368,7 @@ cudaError_t write_to_device(void* dst, const void* src, size_t bytes, cudaStream
 cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
                                uint32_t seg_shift, cudaStream_t s, cudaEvent_t succ_ready,
                                TaskBuild* out, int* bad_input, uint64_t* launches,
-                               bool defer_fill, bool seg_bounds, bool class_major) {
+                               bool seg_bounds, bool class_major) {
   *out = TaskBuild{};
   if (seg_shift < 32 && hi > lo) {
     out->seg_shift = seg_shift;
@@ -535,21 +535,15 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   }
   o.tos_words = rows * 32;
   HANF_BUILD_TRY(pool_alloc(&o.tos, o.tos_words, s));
-  if (defer_fill) {
-    o.chunk_begin = chunk_begin;
-    chunk_begin = nullptr;
-    HANF_BUILD_TRY(pool_alloc(&o.fill_bad, 1, s));
-    HANF_BUILD_TRY(cudaMemsetAsync(o.fill_bad, 0, sizeof(int), s));
-  }
-  if (succ_ready && !defer_fill) HANF_BUILD_TRY(cudaStreamWaitEvent(s, succ_ready, 0));
-  if (num_tasks && !defer_fill) {
+  if (succ_ready) HANF_BUILD_TRY(cudaStreamWaitEvent(s, succ_ready, 0));
+  if (num_tasks) {
     fill_tos_kernel<<<grid(num_tasks * 32), threads, 0, s>>>(
         g, o.order, chunk_begin, o.chunk_node, o.wtasks, num_tasks,
         static_cast<uint32_t>(n), o.tos, d_bad);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
   }
-  if (o.seg_shift < 32 && seg_bounds && !defer_fill) {
+  if (o.seg_shift < 32 && seg_bounds) {
     HANF_BUILD_TRY(pool_alloc(&o.seg_min, segs, s));
     HANF_BUILD_TRY(pool_alloc(&o.seg_max, segs, s));
     HANF_BUILD_TRY(cudaMemsetAsync(o.seg_min, 0xff, sizeof(uint32_t) * segs, s));
@@ -572,148 +566,6 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   HANF_BUILD_TRY(cudaFreeAsync(scan, s));
   HANF_BUILD_TRY(cudaFreeAsync(d_groups, s));
   HANF_BUILD_TRY(cudaStreamSynchronize(s));
-  *bad_input = h_bad;
-  return cudaSuccess;
-}
-
-namespace {
-
-// row_slot[v - lo] = (TOS offset of v's first id) << 16 | hub << 15 | lg << 8 | j:
-// light row v is node slot j of its task (2^lg lanes each), so its arc k
-// goes to offset + 32 (k >> lg) + j 2^lg + (k & (2^lg - 1)); a hub's
-// chunks are consecutive 1024-id runs, so its arc k goes to offset + k.
-__global__ void row_slots_kernel(const WarpTask* __restrict__ tasks, uint64_t num_tasks,
-                                 const uint32_t* __restrict__ order,
-                                 const uint32_t* __restrict__ chunk_node,
-                                 const uint32_t* __restrict__ chunk_hub,
-                                 const uint32_t* __restrict__ hub_first, uint64_t lo,
-                                 uint64_t* __restrict__ slot) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < num_tasks;
-       w += stride) {
-    const WarpTask t = tasks[w];
-    if (t.nodes == 0) {
-      if (hub_first[chunk_hub[t.item]] == t.item)  // the hub's first chunk
-        slot[chunk_node[t.item] - lo] = (t.tos << 16) | (1u << 15);
-    } else {
-      for (uint32_t j = 0; j < t.nodes; ++j)
-        slot[order[t.item + j] - lo] = (t.tos << 16) | (static_cast<uint64_t>(t.lg) << 8) | j;
-    }
-  }
-}
-
-__global__ void tos_pad_kernel(uint32_t* __restrict__ tos, uint64_t words, uint32_t n) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  uint4 v = make_uint4(n, n, n, n);
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < words / 4;
-       i += stride)
-    reinterpret_cast<uint4*>(tos)[i] = v;
-}
-
-// One warp per row of [v0, v1): its ids into their TOS slots (ids >= n are
-// flagged and replaced by the zero row).
-__global__ void __launch_bounds__(256)
-scatter_tos_kernel(const CsrView g, const uint64_t* __restrict__ slot, uint64_t lo, uint64_t v0,
-                   uint64_t v1, uint32_t n, uint32_t* __restrict__ tos, int* __restrict__ bad) {
-  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  bool out_of_range = false;
-  for (uint64_t v = v0 + ((blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5);
-       v < v1; v += warps) {
-    const uint64_t s = g.begin(v), e = g.end(v);
-    if (e <= s) continue;
-    const uint64_t sl = slot[v - lo];
-    const uint64_t base = sl >> 16;
-    const bool hub = (sl >> 15) & 1;
-    const uint32_t lg = (sl >> 8) & 0x7f, j = sl & 0xff;
-    for (uint64_t k = lane; k < e - s; k += 32) {
-      const uint32_t id = g.id(s + k);
-      out_of_range |= id >= n;
-      const uint64_t at = hub ? base + k
-                              : base + 32 * (k >> lg) + (static_cast<uint64_t>(j) << lg) +
-                                    (k & ((1u << lg) - 1));
-      tos[at] = id < n ? id : n;
-    }
-  }
-  if (__any_sync(0xffffffffu, out_of_range) && lane == 0) *bad = 1;
-}
-
-}  // namespace
-
-cudaError_t scatter_fill_prepare(TaskBuild* t, uint64_t lo, uint64_t hi, uint64_t n,
-                                 cudaStream_t s, uint64_t* launches) {
-  HANF_BUILD_TRY(pool_alloc(&t->row_slot, hi - lo, s));
-  if (t->num_wtasks) {
-    uint64_t blocks = (t->num_wtasks + 255) / 256;
-    if (blocks > 148ull * 32) blocks = 148ull * 32;
-    row_slots_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
-        t->wtasks, t->num_wtasks, t->order, t->chunk_node, t->chunk_hub, t->hub_first, lo,
-        t->row_slot);
-    ++*launches;
-    HANF_BUILD_TRY(cudaGetLastError());
-  }
-  if (t->tos_words) {  // (the TOS is a multiple of 32 ids)
-    tos_pad_kernel<<<148 * 8, 256, 0, s>>>(t->tos, t->tos_words, static_cast<uint32_t>(n));
-    ++*launches;
-    HANF_BUILD_TRY(cudaGetLastError());
-  }
-  return cudaSuccess;
-}
-
-cudaError_t scatter_fill_range(const CsrView& g, const TaskBuild& t, uint64_t lo, uint64_t v0,
-                               uint64_t v1, uint64_t n, cudaStream_t s, uint64_t* launches) {
-  if (v1 <= v0) return cudaSuccess;
-  uint64_t blocks = ((v1 - v0) * 32 + 255) / 256;
-  if (blocks > 148ull * 32) blocks = 148ull * 32;
-  scatter_tos_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
-      g, t.row_slot, lo, v0, v1, static_cast<uint32_t>(n), t.tos, t.fill_bad);
-  ++*launches;
-  return cudaGetLastError();
-}
-
-cudaError_t fill_tos_range(const CsrView& g, const TaskBuild& t, uint64_t t0, uint64_t t1,
-                           uint64_t n, cudaStream_t s, uint64_t* launches) {
-  if (t1 <= t0) return cudaSuccess;
-  uint64_t blocks = ((t1 - t0) * 32 + 255) / 256;
-  if (blocks > 148ull * 32) blocks = 148ull * 32;
-  // (tasks are self-contained: a sub-array of them fills its own TOS rows)
-  fill_tos_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
-      g, t.order, t.chunk_begin, t.chunk_node, t.wtasks + t0, t1 - t0, static_cast<uint32_t>(n),
-      t.tos, t.fill_bad);
-  ++*launches;
-  return cudaGetLastError();
-}
-
-cudaError_t finish_tasks_device(const CsrView& g, TaskBuild* t, uint64_t lo, uint64_t hi,
-                                bool seg_bounds, cudaStream_t s, int* bad_input,
-                                uint64_t* launches) {
-  if (t->seg_shift < 32 && seg_bounds) {
-    const uint32_t segs = t->num_segs;
-    HANF_BUILD_TRY(pool_alloc(&t->seg_min, segs, s));
-    HANF_BUILD_TRY(pool_alloc(&t->seg_max, segs, s));
-    HANF_BUILD_TRY(cudaMemsetAsync(t->seg_min, 0xff, sizeof(uint32_t) * segs, s));
-    HANF_BUILD_TRY(cudaMemsetAsync(t->seg_max, 0, sizeof(uint32_t) * segs, s));
-    uint64_t blocks = (hi - lo + 255) / 256;
-    if (blocks > 148ull * 32) blocks = 148ull * 32;
-    segment_bounds_kernel<<<static_cast<uint32_t>(blocks ? blocks : 1), 256, 0, s>>>(
-        g, lo, hi, t->seg_shift, t->seg_min, t->seg_max);
-    ++*launches;
-    HANF_BUILD_TRY(cudaGetLastError());
-  }
-  int h_bad = 0;
-  if (t->fill_bad) {
-    HANF_BUILD_TRY(read_back(&h_bad, t->fill_bad, sizeof(int), s));
-    HANF_BUILD_TRY(cudaFreeAsync(t->fill_bad, s));
-    t->fill_bad = nullptr;
-  }
-  if (t->chunk_begin) {
-    HANF_BUILD_TRY(cudaFreeAsync(t->chunk_begin, s));
-    t->chunk_begin = nullptr;
-  }
-  if (t->row_slot) {
-    HANF_BUILD_TRY(cudaFreeAsync(t->row_slot, s));
-    t->row_slot = nullptr;
-  }
   *bad_input = h_bad;
   return cudaSuccess;
 }

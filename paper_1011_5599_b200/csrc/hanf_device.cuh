@@ -213,44 +213,6 @@ __device__ __forceinline__ uint4 ld16(const uint4* p) {
   }
   return v;
 }
-// L2 eviction-priority policies (createpolicy): the gathers of hot rows
-// (the first rows after degree relabelling, most in-arcs) are kept with
-// evict_last, everything streamed once (cold rows, successor ids) is
-// evict_first, so the streams do not wash the hot set out of L2.
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-template <bool kL1 = true>
-__device__ __forceinline__ uint4 ld16_pol(const uint4* p, uint64_t pol) {
-  uint4 v;
-  if constexpr (kL1)
-    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
-  else
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ uint32_t ld4_pol(const uint32_t* p, uint64_t pol) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
-               : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void ldg256_pol(uint32_t (&v)[8], const uint64_t* p, uint64_t pol) {
-  asm volatile("ld.global.nc.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                 "=r"(v[6]), "=r"(v[7])
-               : "l"(p), "l"(pol));
-}
-
 template <int kPol>
 __device__ __forceinline__ uint2 ld8(const uint2* p) {
   uint2 v;
@@ -358,45 +320,6 @@ __device__ __forceinline__ void store_counter(uint64_t* p, const uint32_t (&v)[L
     q.x = limb(ic<2 * k + 0>{});
     q.y = limb(ic<2 * k + 1>{});
     *reinterpret_cast<uint2*>(p + word) = q;
-  };
-  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-    sfor<0, NW / 2>([&](auto I) {
-      constexpr int k = decltype(I)::value;
-      st16(ic<2 * k>{}, 2 * k);
-    });
-    if constexpr (NW % 2) st8(ic<NW - 1>{}, NW - 1);
-  } else {
-    st8(ic<0>{}, 0);
-    sfor<0, (NW - 1) / 2>([&](auto I) {
-      constexpr int k = decltype(I)::value;
-      st16(ic<2 * k + 1>{}, 2 * k + 1);
-    });
-    if constexpr (NW % 2 == 0) st8(ic<NW - 1>{}, NW - 1);
-  }
-}
-
-// store_counter with an L2 eviction-priority policy (evict_first for the
-// next generation: written once, read back only next step)
-template <class Lay>
-__device__ __forceinline__ void store_counter_pol(uint64_t* p, const uint32_t (&v)[Lay::kLimbs],
-                                                  uint64_t pol) {
-  constexpr int NW = Lay::kWords;
-  constexpr int NL = Lay::kLimbs;
-  auto limb = [&](auto I) -> uint32_t {
-    constexpr int i = decltype(I)::value;
-    if constexpr (i < NL) return v[i]; else return 0u;
-  };
-  auto st16 = [&](auto K, int word) {
-    constexpr int k = decltype(K)::value;
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
-                 :: "l"(p + word), "r"(limb(ic<2 * k + 0>{})), "r"(limb(ic<2 * k + 1>{})),
-                    "r"(limb(ic<2 * k + 2>{})), "r"(limb(ic<2 * k + 3>{})), "l"(pol) : "memory");
-  };
-  auto st8 = [&](auto K, int word) {
-    constexpr int k = decltype(K)::value;
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;"
-                 :: "l"(p + word), "r"(limb(ic<2 * k + 0>{})), "r"(limb(ic<2 * k + 1>{})),
-                    "l"(pol) : "memory");
   };
   if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
     sfor<0, NW / 2>([&](auto I) {
@@ -556,61 +479,6 @@ __device__ __forceinline__ void ldg256(uint32_t (&v)[8], const uint64_t* p) {
                : "l"(p));
 }
 
-template <int NW>
-struct Window {
-  // worst-case word offset inside the 32-byte block, over all counters
-  static constexpr int kMaxQ = (NW % 4 == 0) ? 0 : ((NW % 2 == 0) ? 2 : 3);
-  static constexpr int kLoads = (kMaxQ + NW + 3) / 4;
-  static constexpr int kLimbs = 8 * kLoads;
-};
-
-// Issues the window loads of counter w (row stride NW words).
-template <int NW>
-__device__ __forceinline__ void window_load(uint32_t (&raw)[Window<NW>::kLoads][8],
-                                            const uint64_t* base, uint32_t w) {
-  const uint64_t word = static_cast<uint64_t>(w) * NW;
-  const uint64_t* p = base + (word & ~3ull);
-  sfor<0, Window<NW>::kLoads>([&](auto I) {
-    constexpr int k = decltype(I)::value;
-    ldg256(raw[k], p + 4 * k);
-  });
-}
-
-// Extracts the counter's limbs from its window: limb i = raw limb 2q + i.
-template <class Lay, int NW>
-__device__ __forceinline__ void window_extract(uint32_t (&x)[Lay::kLimbs],
-                                               const uint32_t (&raw)[Window<NW>::kLoads][8],
-                                               uint32_t w) {
-  constexpr int NL = Lay::kLimbs;
-  constexpr int WL = Window<NW>::kLimbs;
-  const uint32_t q = (w * NW) & 3u;
-  auto at = [&](int i) -> uint32_t { return raw[i / 8][i % 8]; };
-  if constexpr (Window<NW>::kMaxQ == 0) {
-    sfor<0, NL>([&](auto I) { x[decltype(I)::value] = at(decltype(I)::value); });
-  } else if constexpr (Window<NW>::kMaxQ == 2) {
-    const bool s2 = q & 2u;
-    sfor<0, NL>([&](auto I) {
-      constexpr int i = decltype(I)::value;
-      x[i] = s2 ? at(i + 4) : at(i);
-    });
-  } else {
-    const bool s2 = q & 2u, s1 = q & 1u;
-    constexpr int TL = NL + 2 < WL - 4 ? NL + 2 : WL - 4;  // limbs kept after the 2-word step
-    uint32_t t[TL];
-    sfor<0, TL>([&](auto I) {
-      constexpr int i = decltype(I)::value;
-      t[i] = s2 ? at(i + 4) : at(i);
-    });
-    sfor<0, NL>([&](auto I) {
-      constexpr int i = decltype(I)::value;
-      if constexpr (i + 2 < TL)
-        x[i] = s1 ? t[i + 2] : t[i];
-      else
-        x[i] = t[i];  // unreachable limb pairing (q=1 never needs it)
-    });
-  }
-}
-
 // 128-bit windows: counter w (W words, W odd) starts q = (W*w) mod 2 words
 // into its 16-byte block; ceil((W+1)/2) aligned 16-byte loads, one select.
 template <int NW>
@@ -627,18 +495,6 @@ __device__ __forceinline__ void window128_load(uint4 (&raw)[Window128<NW>::kLoad
   sfor<0, Window128<NW>::kLoads>([&](auto I) {
     constexpr int k = decltype(I)::value;
     raw[k] = ld16<kPol>(p + k);
-  });
-}
-
-template <int NW, bool kL1 = true>
-__device__ __forceinline__ void window128_load_pol(uint4 (&raw)[Window128<NW>::kLoads],
-                                                   const uint64_t* base, uint32_t w,
-                                                   uint64_t pol) {
-  const uint64_t word = static_cast<uint64_t>(w) * NW;
-  const uint4* p = reinterpret_cast<const uint4*>(base + (word & ~1ull));
-  sfor<0, Window128<NW>::kLoads>([&](auto I) {
-    constexpr int k = decltype(I)::value;
-    raw[k] = ld16_pol<kL1>(p + k, pol);
   });
 }
 
@@ -697,63 +553,6 @@ __device__ __forceinline__ double estimate_limbs(const uint32_t (&x)[Lay::kLimbs
     });
     return finish_estimate(p, harmonic, zeros);
   }
-}
-
-// ---------------------------------------------------------------------------
-// TMA row gathers (sm_100 cp.async.bulk.tensor ... tile::gather4).  The
-// counter array is described to the TMA unit as a 2-D tensor of `pitch`
-// u64 columns x (n + 1) rows; one gather4 copies 4 whole rows (given by
-// index) into shared memory and signals an mbarrier with the byte count.
-// Gathers then bypass the LSU/L1 data pipe: the rows reach the SM as bulk
-// transfers and are read back with LDS.128.  Opt-in: on the BASELINE
-// graphs it is slower than LDG windows (profiles/r01_tma_gather.md).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_init_fence() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "HANF_MBAR_WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra HANF_MBAR_WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_gather4(void* dst, const void* map, uint64_t* bar, uint32_t r0,
-                                            uint32_t r1, uint32_t r2, uint32_t r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(0), "r"(r0), "r"(r1),
-      "r"(r2), "r"(r3)
-      : "memory");
-}
-
-// Loads a counter row (16-byte aligned, pitch >= 2*ceil(kWords/2) words)
-// with 128-bit loads; works on shared and global addresses.
-template <class Lay>
-__device__ __forceinline__ void load_row16(uint32_t (&v)[Lay::kLimbs], const void* p) {
-  constexpr int NL = Lay::kLimbs;
-  constexpr int NQ = (Lay::kWords + 1) / 2;
-  sfor<0, NQ>([&](auto I) {
-    constexpr int k = decltype(I)::value;
-    const uint4 q = reinterpret_cast<const uint4*>(p)[k];
-    if constexpr (4 * k + 0 < NL) v[4 * k + 0] = q.x;
-    if constexpr (4 * k + 1 < NL) v[4 * k + 1] = q.y;
-    if constexpr (4 * k + 2 < NL) v[4 * k + 2] = q.z;
-    if constexpr (4 * k + 3 < NL) v[4 * k + 3] = q.w;
-  });
 }
 
 }  // namespace hanf

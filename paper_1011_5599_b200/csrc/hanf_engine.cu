@@ -87,31 +87,6 @@ void pfree(T*& p, cudaStream_t s) {
   p = nullptr;
 }
 
-// TMA descriptor of a counter generation: a 2-D tensor of `pitch` u64
-// columns x (n + 1) rows, box = one whole row (gather4 takes 4 row indices).
-// The encoder is a driver entry point (no libcuda link dependency).
-cudaError_t encode_rows_map(CUtensorMap* map, const uint64_t* base, uint64_t rows, uint64_t pitch) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
-                                cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      encode = nullptr;
-  });
-  if (!encode) return cudaErrorNotSupported;
-  cuuint64_t gdim[2] = {pitch, rows};
-  cuuint64_t gstride[1] = {pitch * 8};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(pitch), 1};
-  cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(base),
-                            gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
 // Keep freed device memory in the pool (no release at synchronisation).
 void configure_pool(int device) {
   static std::mutex mu;
@@ -260,9 +235,6 @@ struct hanf_engine {
   hanf::ReduceOut* reduce = nullptr;
   double* reduce_sums = nullptr;
   unsigned long long* reduce_counts = nullptr;
-  int gather_mode = -1;       // union kernel variant (-1: per-layout default)
-  uint32_t hot_rows = 0;      // relabelled rows kept in L2 by gather policy 3
-  bool tma = false;           // gather successor rows with TMA gather4
   // locality relabelling (hanf_relabel.cu): the device works on rows;
   // order[row] = original id, perm[id] = row; dirty[g] = original-id
   // bitmaps of changed counters for the block sums (mod[g] is in rows)
@@ -294,13 +266,13 @@ struct hanf_engine {
   bool ever_reduced = false;  // (then the local block sums are only current in the slice)
   // relabelled engines keep estimates in row order (writes follow the task
   // order); finish_kernel gathers them through perm for the original-id
-  // block sums.  HANF_EST_SCATTER=1: scatter to the original slot instead.
+  // block sums (scattering them to the original slots instead measured
+  // 1.36x slower per R-MAT 26 shard step)
   bool est_rows = false;
   uint32_t* order = nullptr;
   uint32_t* perm = nullptr;
   uint64_t* rl_off = nullptr;  // relabelled offsets until the worklist needs the CSR
   uint64_t* dirty[2] = {nullptr, nullptr};
-  CUtensorMap tmap[2];        // descriptors of cnt[0], cnt[1]
 
   hanf::ReduceOut* h_reduce = nullptr;  // pinned (cache): total + count
   double* h_log_stage = nullptr;        // pinned (cache): the log table's upload source
@@ -338,14 +310,6 @@ struct hanf_engine {
   uint64_t summ_bits = 0;
   bool use_graphs = true;
   uint32_t* seg_live = nullptr;  // skip sweeps over segmented tasks (TaskBuild::seg_shift)
-  // scan-signalled worklist steps (mode 4): TOS row -> warp task; allowed
-  // on unrelabelled single-chunk engines (HANF_SCAN=0 off, =1 every skip step)
-  uint32_t* row_task = nullptr;
-  bool scan_ok = false;
-  bool force_scan = false;
-  // create pipelined iteration 1 with the arcs upload: the next generation,
-  // its bitmap and estimates already hold step 1's sweep (hanf_create)
-  bool pre_step = false;
   // mod[1 - cur] is known to be all zero (seeding, or the last commit's
   // finish_kernel cleared it): the step's memset is skipped
   bool next_bits_clear = false;
@@ -461,7 +425,6 @@ struct hanf_engine {
       pfree(dirty[1], stream);
       pfree(lens, stream);
       pfree(seg_live, stream);
-      pfree(row_task, stream);
       pfree(dirty_derived, stream);
       hanf::free_tasks_device(&tasks, stream);
       if (cudaStreamSynchronize(stream) == cudaSuccess)
@@ -640,7 +603,6 @@ void batch_totals(hanf_engine* e, int parity, uint64_t* counts) {
 }
 
 hanf_status seed_all(hanf_engine* e) {
-  e->pre_step = false;
   e->cur = 0;
   e->t = 0;
   e->stale_valid = false;
@@ -695,7 +657,7 @@ bool sparse_wanted(const hanf_engine* e) {
   // changed counter: they beat the worklist down to ~n/4096 changed
   // (config 3: 0.43 against 0.65 ms per step between n/4096 and n/128)
   const uint64_t ratio = e->seg_live && !e->force_sparse ? 4096 : 128;
-  return e->cfg.track_modified && e->t != 0 && e->sparse_ok && !e->tma && e->stale_valid &&
+  return e->cfg.track_modified && e->t != 0 && e->sparse_ok && e->stale_valid &&
          ratio * e->last_count < e->n;
 }
 int step_mode(const hanf_engine* e) {
@@ -705,11 +667,6 @@ int step_mode(const hanf_engine* e) {
   // many steps would have used it, so short runs never pay for it
   if (sparse_wanted(e) && (e->tr_off || e->sparse_wanted_steps >= e->sparse_after)) return 2;
   if (2 * e->last_count >= e->n) return 0;
-  // very few changed counters and no transpose: one scan of the TOS
-  // signals the nodes with a changed successor, and only they are redone
-  if (e->scan_ok && !e->tr_off && e->stale_valid &&
-      (e->force_scan || 256 * e->last_count < e->n))
-    return 4;
   // few changed counters: filter the per-arc bitmap probes through the
   // L1-resident summary first (most probes then never reach L2)
   return e->force_summary || 16 * e->last_count < e->summ_bits ? 3 : 1;
@@ -762,12 +719,6 @@ hanf_status ensure_worklist_scratch(hanf_engine* e) {
   return HANF_OK;
 }
 
-// Mode 4's TOS row -> task map and the worklist scratch, on first use.
-hanf_status ensure_scan(hanf_engine* e) {
-  if (!e->row_task) HANF_CUDA(hanf::build_row_task(e->tasks, e->stream, &e->row_task, &e->launches));
-  return ensure_worklist_scratch(e);
-}
-
 // Peer-push exchange: generation ng of every attached peer.
 hanf::PeerRows peer_rows(const hanf_engine* e, int ng) {
   hanf::PeerRows p{};
@@ -809,11 +760,10 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.est_index = e->est_rows ? nullptr : e->order;
   a.dirty_next = e->dirty[ng];
   a.peers = peer_rows(e, ng);
-  a.hot_rows = e->hot_rows;
   return a;
 }
 
-hanf_status compute_sparse(hanf_engine* e, bool scan = false) {
+hanf_status compute_sparse(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
   const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
   hanf::SparseArgs a{};
@@ -847,17 +797,8 @@ hanf_status compute_sparse(hanf_engine* e, bool scan = false) {
   a.blocks = e->blocks;
   a.hi = e->hi;
   a.peers = peer_rows(e, ng);
-  if (scan) {
-    HANF_CUDA(hanf::launch_summary(e->mod[g], e->blocks + 1, e->summ_shift, e->summ_bits, e->summ,
-                                   e->stream, &e->launches));
-    HANF_CUDA(hanf::launch_scan_step(a, e->tasks, e->row_task, e->summ, e->summ_shift,
-                                     static_cast<uint32_t>((e->summ_bits + 63) / 64), w0, w1,
-                                     e->params.register_bits, e->params.registers, e->stream,
-                                     &e->launches));
-  } else {
-    HANF_CUDA(hanf::launch_sparse_step(a, w0, w1, e->params.register_bits, e->params.registers,
-                                       e->stream, &e->launches));
-  }
+  HANF_CUDA(hanf::launch_sparse_step(a, w0, w1, e->params.register_bits, e->params.registers,
+                                     e->stream, &e->launches));
   if (e->tasks.num_chunks) {
     // worklist hubs: their chunk tasks through the dense kernel (skipping
     // unmodified successors), chunk partials folded by the usual ticket
@@ -866,8 +807,8 @@ hanf_status compute_sparse(hanf_engine* e, bool scan = false) {
     u.task_list = e->hub_tasks;
     u.task_count = e->lens + 2;
     u.num_wtasks = e->tasks.num_chunks;
-    HANF_CUDA(hanf::launch_union(u, e->params.register_bits, e->params.registers, e->gather_mode,
-                                 nullptr, e->stream, &e->launches));
+    HANF_CUDA(hanf::launch_union(u, e->params.register_bits, e->params.registers, e->stream,
+                                 &e->launches));
   }
   return HANF_OK;
 }
@@ -897,14 +838,6 @@ hanf_status compute_local(hanf_engine* e) {
 
 hanf_status compute_shard(hanf_engine* e) {
   const int g = e->cur, ng = 1 - e->cur;
-  if (e->pre_step) {  // step 1's sweep ran during the upload (create)
-    e->pre_step = false;
-    if (e->timing) {
-      HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
-      HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
-    }
-    return HANF_OK;
-  }
   if (e->shard_relabel && !e->attached)
     return fail(HANF_INVALID_ARGUMENT,
                 "relabelled shard engines exchange through hanf_shard_attach (peer-push)");
@@ -917,8 +850,8 @@ hanf_status compute_shard(hanf_engine* e) {
   if (e->dirty[ng])  // unsharded relabelling: the whole original-id bitmap
     HANF_CUDA(cudaMemsetAsync(e->dirty[ng], 0, sizeof(uint64_t) * e->blocks, e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
-  if ((step_mode(e) == 2 && e->tr_off) || step_mode(e) == 4) {
-    const hanf_status st = compute_sparse(e, step_mode(e) == 4);
+  if (step_mode(e) == 2 && e->tr_off) {
+    const hanf_status st = compute_sparse(e);
     if (st != HANF_OK) return st;
     if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
     if (e->lo != 0 || e->hi != e->n) {
@@ -946,8 +879,7 @@ hanf_status compute_shard(hanf_engine* e) {
     a.summ_words = static_cast<uint32_t>((e->summ_bits + 63) / 64);
   }
   const bool fused = a.est != nullptr;
-  HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers,
-                               e->gather_mode, e->tma ? &e->tmap[g] : nullptr, e->stream,
+  HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers, e->stream,
                                &e->launches));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
   const bool sharded = e->lo != 0 || e->hi != e->n;
@@ -1055,11 +987,11 @@ hanf_status commit(hanf_engine* e, hanf_iteration_report* rep) {
 hanf_status step_enqueue(hanf_engine* e) {
   note_step(e);
   const int mode = step_mode(e);
-  if (mode == 2 || mode == 4) {
-    const hanf_status st = mode == 2 ? ensure_sparse(e) : ensure_scan(e);
+  if (mode == 2) {
+    const hanf_status st = ensure_sparse(e);
     if (st != HANF_OK) return st;
   }
-  if (!e->use_graphs || e->timing || e->pre_step) {
+  if (!e->use_graphs || e->timing) {
     const hanf_status st = compute_local(e);
     if (st != HANF_OK) return st;
     return commit_enqueue(e);
@@ -1187,7 +1119,6 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   e->blocks = (n + 63) / 64;
   e->words = params.words_per_counter;
   e->pitch = hanf::row_pitch(params.register_bits, params.registers, params.words_per_counter);
-  if (const char* gm = std::getenv("HANF_GATHER")) e->gather_mode = std::atoi(gm);
   if (const char* fs = std::getenv("HANF_SUMMARY")) e->force_summary = fs[0] == '1';
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
@@ -1227,25 +1158,14 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       e->relabel = rl[0] == '1';
     else
       e->relabel = (n + 1) * e->pitch * 8 > (64ull << 20) && !ids_local(g);
-    const char* sc = std::getenv("HANF_EST_SCATTER");
-    e->est_rows = e->relabel && !(sc && sc[0] == '1');
+    e->est_rows = e->relabel;
     if (shard_cfg && e->relabel) {
       // estimates stay in row order and are pushed to the peers with their
       // rows; the commit gathers them through perm for every block
-      // (HANF_EST_SCATTER=1: original slots - random pushes, measured 1.36x
-      // slower per R-MAT 26 shard step, scripts/shard_relabel_time.py)
       e->shard_relabel = true;
       e->sparse_ok = false;  // (the worklist needs a row-space CSR of the shard)
     }
   }
-  if (e->relabel && !e->shard_relabel) {
-    // the first rows after degree relabelling take most gathers: the
-    // policy-3 sweep keeps this many bytes of them in L2 (evict_last)
-    uint64_t mb = 64;
-    if (const char* hm = std::getenv("HANF_HOT_MB")) mb = std::strtoull(hm, nullptr, 10);
-    e->hot_rows = static_cast<uint32_t>(std::min<uint64_t>(n, (mb << 20) / (e->pitch * 8)));
-  }
-
   cudaStream_t helper = nullptr;  // upload stream: idle before any buffer is freed
   auto bail = [&](hanf_status s) {
     const std::string msg = g_last_error;
@@ -1262,19 +1182,6 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
 
   HANF_TRY(cudaSetDevice(cfg.device));
   configure_pool(cfg.device);
-  if (const char* pm = std::getenv("HANF_L2_PERSIST_MB")) {
-    // L2 set-aside for evict_last (persisting) lines: without it the
-    // policy-3 sweep's evict_last is an ordinary priority
-    int maxp = 0;
-    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, cfg.device);
-    const size_t want = std::min<size_t>(static_cast<size_t>(maxp),
-                                         std::strtoull(pm, nullptr, 10) << 20);
-    HANF_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-    if (std::getenv("HANF_PROFILE"))
-      std::fprintf(stderr, "[hanf] L2 persisting set-aside %zu of max %d bytes\n", want, maxp);
-  }
-  if (const char* l2 = std::getenv("HANF_L2_FETCH"))
-    HANF_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::atoi(l2)));
   HANF_TRY(streams().get(cfg.device, &e->stream));
   cudaStream_t s = e->stream;
   // row n is an all-zero counter (the union kernels' padding target); 8
@@ -1311,12 +1218,6 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   }
   HANF_TRY(cudaMemsetAsync(e->cnt[0] + n * e->pitch, 0, sizeof(uint64_t) * (e->pitch + 8), s));
   HANF_TRY(cudaMemsetAsync(e->cnt[1] + n * e->pitch, 0, sizeof(uint64_t) * (e->pitch + 8), s));
-  e->tma = hanf::use_tma(params.register_bits, params.registers, static_cast<uint32_t>(e->pitch)) &&
-           n + 1 <= 0xffffffffull;
-  if (e->tma) {
-    HANF_TRY(encode_rows_map(&e->tmap[0], e->cnt[0], n + 1, e->pitch));
-    HANF_TRY(encode_rows_map(&e->tmap[1], e->cnt[1], n + 1, e->pitch));
-  }
   // one extra word: the padding row n (TOS padding, skipped arcs) is probed
   // like any successor and must read as unmodified
   if (!sharded) {
@@ -1395,17 +1296,10 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     // (the copying model's windows) group their tasks by node segment, so
     // a warp's nodes are id-neighbours and late skip sweeps visit only the
     // segments near the changed counters (profiles/r01_segments.md).
-    // Pipelined create (opt-in, HANF_PIPELINE=1; single-GPU engines with
-    // fused estimates): the arcs go up in node-range chunks, each chunk's
-    // TOS rows are filled and step 1's sweep of its light tasks runs as soon
-    // as it lands, the hubs after the last one.  Measured on config 2 it
-    // loses: the node-segmented task order it needs makes every dense step
-    // ~5% slower, and the chunk sweeps' small launches are latency-bound
-    // (profiles/r01_pipeline.md).
+    // (Two ways to hide step 1 or the TOS fill under the arcs upload were
+    // measured and removed: profiles/r01_pipeline.md.)
     uint32_t seg_shift = 32;
     bool seg_skip = false;
-    bool pipeline = false;
-    bool scatter = false;
     {
       uint32_t bits = 0;
       while ((1ull << bits) < n) ++bits;
@@ -1421,20 +1315,6 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
         if (seg_shift < 6) seg_shift = 6;
         seg_skip = true;
       }
-      const char* pp = std::getenv("HANF_PIPELINE");
-      const bool eligible = K == 1 && !e->relabel && lo == 0 && hi == n && n > 64 &&
-                            !e->tma && hanf::fused_estimates(params.register_bits,
-                                                             params.registers);
-      pipeline = eligible && pp && pp[0] == '1';
-      if (pipeline && seg_shift >= 32) seg_shift = bits > 9 ? bits - 3 : 6;  // 8 chunks
-      // Scatter fill (opt-in, HANF_SCATTER_FILL=1; unrelabelled engines):
-      // the arcs go up in 8 arc-balanced node-range chunks and each chunk's
-      // ids are scattered into the TOS as soon as it lands.  Measured on
-      // config 2 it loses: a node's ids land 32 rows apart, so the
-      // scattered 4-byte stores take ~0.25 ms per chunk against 0.09 ms for
-      // the whole task-ordered fill (profiles/r01_pipeline.md)
-      const char* sf = std::getenv("HANF_SCATTER_FILL");
-      scatter = !pipeline && K == 1 && !e->relabel && n > 64 && sf && sf[0] == '1';
     }
     uint64_t a0 = g->offsets[up_lo], a1 = g->offsets[up_hi];
     uint64_t* d_off = nullptr;
@@ -1473,70 +1353,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
                              cudaMemcpyHostToDevice, s));
     HANF_TRY(cudaEventRecord(ev_off, s));
     HANF_TRY(cudaStreamWaitEvent(s2, ev_off, 0));
-    // pipelined: chunk c = segments [c S / P, (c + 1) S / P), its arcs one copy
-    const uint32_t segs = seg_shift >= 32 ? 1u : static_cast<uint32_t>(((hi - 1) >> seg_shift) + 1);
-    const uint32_t pchunks = pipeline ? std::min<uint32_t>(8, segs) : 0;
-    std::vector<uint32_t> chunk_seg(pchunks + 1);
-    if (pipeline) {  // chunk arc ranges must be ordered (else: one copy; the build flags it)
-      uint64_t prev = a0;
-      for (uint32_t c = 1; c <= pchunks && pipeline; ++c) {
-        const uint64_t v = std::min<uint64_t>(
-            static_cast<uint64_t>(static_cast<uint64_t>(c) * segs / pchunks) << seg_shift, hi);
-        const uint64_t b = g->offsets[v];
-        if (b < prev || b > a1) pipeline = false;
-        prev = b;
-      }
-    }
-    if (pipeline) {
-      for (uint32_t c = 0; c <= pchunks; ++c) {
-        chunk_seg[c] = static_cast<uint32_t>(static_cast<uint64_t>(c) * segs / pchunks);
-        if (c < pchunks) {
-          cudaEvent_t ev = nullptr;
-          HANF_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-          guard.chunks.push_back(ev);
-        }
-      }
-      for (uint32_t c = 0; c < pchunks; ++c) {
-        const uint64_t v0 = std::min<uint64_t>(static_cast<uint64_t>(chunk_seg[c]) << seg_shift, hi);
-        const uint64_t v1 = std::min<uint64_t>(static_cast<uint64_t>(chunk_seg[c + 1]) << seg_shift, hi);
-        const uint64_t b0 = g->offsets[v0], b1 = g->offsets[v1];
-        if (b1 > b0)
-          HANF_TRY(cudaMemcpyAsync(d_succ + (b0 - a0), g->arcs + b0, sizeof(uint32_t) * (b1 - b0),
-                                   cudaMemcpyHostToDevice, s2));
-        HANF_TRY(cudaEventRecord(guard.chunks[c], s2));
-      }
-    }
-    // scatter fill: chunk c = rows [scatter_v[c], scatter_v[c+1]), ~(a1-a0)/8 arcs each
-    std::vector<uint64_t> scatter_v;
-    if (scatter) {
-      const uint32_t P = 8;
-      scatter_v.push_back(lo);
-      for (uint32_t c = 1; c < P; ++c) {
-        const uint64_t target = a0 + (a1 - a0) * c / P;
-        uint64_t l = scatter_v.back(), h = hi;  // first v with offsets[v] >= target
-        while (l < h) {
-          const uint64_t mid = l + (h - l) / 2;
-          if (g->offsets[mid] < target) l = mid + 1; else h = mid;
-        }
-        scatter_v.push_back(l);
-      }
-      scatter_v.push_back(hi);
-      for (size_t c = 0; c + 1 < scatter_v.size() && scatter; ++c) {  // ordered and in range
-        const uint64_t b0 = g->offsets[scatter_v[c]], b1 = g->offsets[scatter_v[c + 1]];
-        if (b1 < b0 || b0 < a0 || b1 > a1) scatter = false;
-      }
-      for (size_t c = 0; c + 1 < scatter_v.size() && scatter; ++c) {
-        cudaEvent_t ev = nullptr;
-        HANF_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        guard.chunks.push_back(ev);
-        const uint64_t b0 = g->offsets[scatter_v[c]], b1 = g->offsets[scatter_v[c + 1]];
-        if (b1 > b0)
-          HANF_TRY(cudaMemcpyAsync(d_succ + (b0 - a0), g->arcs + b0, sizeof(uint32_t) * (b1 - b0),
-                                   cudaMemcpyHostToDevice, s2));
-        HANF_TRY(cudaEventRecord(ev, s2));
-      }
-    }
-    if (!pipeline && !scatter && a1 > a0)
+    if (a1 > a0)
       HANF_TRY(cudaMemcpyAsync(d_succ, g->arcs + a0, sizeof(uint32_t) * (a1 - a0),
                                cudaMemcpyHostToDevice, s2));
     HANF_TRY(cudaEventRecord(ev_arcs, s2));
@@ -1596,12 +1413,10 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     // relabelled: row v's successors are the caller's arcs of order[v], through perm
     const hanf::CsrView view{d_off, up_lo, d_succ, a0, e->order, e->perm, n};
     const cudaError_t be = hanf::build_tasks_device(view, lo, hi, n, seg_shift, s, ev_arcs,
-                                                    &e->tasks, &bad, &e->launches,
-                                                    pipeline || scatter, seg_skip, !seg_skip);
-    // (also on the build's error paths) frees on `s` come after the upload;
-    // the pipelined sweep waits for each chunk itself
-    if (!(pipeline || scatter) || be != cudaSuccess || bad)
-      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+                                                    &e->tasks, &bad, &e->launches, seg_skip,
+                                                    !seg_skip);
+    // (also on the build's error paths) frees on `s` come after the upload
+    HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
     e->csr_off = d_off;
     e->csr_succ = d_succ;
     e->succ_base = a0;
@@ -1618,81 +1433,8 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     }
     if (seg_skip && e->tasks.seg_shift < 32)
       HANF_TRY(palloc(&e->seg_live, e->tasks.num_segs, s));
-    {  // mode 4 (scan-signalled worklist; opt-in HANF_SCAN=1, every skip step):
-       // unrelabelled, unsegmented, single chunk.  Measured on config 2's
-       // tail it loses to the summary skip sweep (0.090 against 0.046 ms):
-       // its ~7 small launches cost more than one sweep (profiles/r01_sparse.md)
-      const char* sc = std::getenv("HANF_SCAN");
-      const bool forced = sc && sc[0] == '1';
-      e->scan_ok = forced && K == 1 && !e->relabel && !seg_skip && !e->tma && n > 0 &&
-                   hanf::sparse_supported(params.register_bits, params.registers) &&
-                   hanf::fused_estimates(params.register_bits, params.registers);
-      e->force_scan = e->scan_ok;
-    }
-    if (scatter) {
-      phase("tasks");
-      HANF_TRY(hanf::scatter_fill_prepare(&e->tasks, lo, hi, n, s, &e->launches));
-      phase("prepare");
-      for (size_t c = 0; c + 1 < scatter_v.size(); ++c) {
-        HANF_TRY(cudaStreamWaitEvent(s, guard.chunks[c], 0));
-        HANF_TRY(hanf::scatter_fill_range(view, e->tasks, lo, scatter_v[c], scatter_v[c + 1], n, s,
-                                          &e->launches));
-        phase("scatter");
-      }
-      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
-      int bad2 = 0;
-      HANF_TRY(hanf::finish_tasks_device(view, &e->tasks, lo, hi, seg_skip, s, &bad2,
-                                         &e->launches));
-      if (bad2)
-        return bail(fail(HANF_INVALID_ARGUMENT,
-                         "arc endpoint out of range or offsets not non-decreasing"));
-    }
-    if (pipeline) {
-      HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
-      // step 1's sweep (t = 0: dense, nothing stale) chunk by chunk
-      HANF_TRY(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, s));
-      hanf::UnionArgs u = union_args(e, 0, 1);
-      const hanf::WarpTask* all = e->tasks.wtasks;
-      auto sweep = [&](uint64_t t0, uint64_t t1) -> cudaError_t {
-        if (t1 <= t0) return cudaSuccess;
-        cudaError_t ce = hanf::fill_tos_range(view, e->tasks, t0, t1, n, s, &e->launches);
-        if (ce != cudaSuccess) return ce;
-        u.wtasks = all + t0;
-        u.num_wtasks = static_cast<uint32_t>(t1 - t0);
-        return hanf::launch_union(u, e->params.register_bits, e->params.registers, e->gather_mode,
-                                  nullptr, s, &e->launches);
-      };
-      const auto& gtb = e->tasks.group_task_begin;
-      const auto& gsg = e->tasks.group_seg;
-      phase("tasks");
-      for (uint32_t c = 0; c < pchunks; ++c) {
-        HANF_TRY(cudaStreamWaitEvent(s, guard.chunks[c], 0));
-        // the chunk's groups, adjacent ones merged into one launch
-        uint64_t t0 = 0, t1 = 0;
-        for (size_t k = 0; k < gsg.size(); ++k) {
-          if (gsg[k] < chunk_seg[c] || gsg[k] >= chunk_seg[c + 1]) continue;
-          if (gtb[k] != t1) {
-            HANF_TRY(sweep(t0, t1));
-            t0 = gtb[k];
-          }
-          t1 = gtb[k + 1];
-        }
-        HANF_TRY(sweep(t0, t1));
-        phase("chunk");
-      }
-      HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
-      HANF_TRY(sweep(0, e->tasks.num_chunks));  // hub chunks (their arcs span chunks)
-      phase("hubs");
-      int bad2 = 0;
-      HANF_TRY(hanf::finish_tasks_device(view, &e->tasks, lo, hi, seg_skip, s, &bad2,
-                                         &e->launches));
-      if (bad2)
-        return bail(fail(HANF_INVALID_ARGUMENT,
-                         "arc endpoint out of range or offsets not non-decreasing"));
-      e->pre_step = true;
-    }
     phase("build");
-    if (!pipeline) HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
+    HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
   }
 #undef HANF_TRY
   *out = e;
@@ -1883,7 +1625,6 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
   e->cur = 0;
   e->stale_valid = false;
   e->systolic = false;
-  e->pre_step = false;
   if (e->shard_relabel) e->est = e->est_gen[0];
   hanf_status st = run_estimates(e, 0, nullptr, 0, e->blocks);
   if (st != HANF_OK) return st;
@@ -1981,8 +1722,8 @@ hanf_status hanf_shard_compute(hanf_engine* e) {
   if (e->n == 0) return HANF_OK;
   HANF_CUDA(cudaSetDevice(e->device));
   note_step(e);
-  if (step_mode(e) == 2 || step_mode(e) == 4) {
-    const hanf_status sst = step_mode(e) == 2 ? ensure_sparse(e) : ensure_scan(e);
+  if (step_mode(e) == 2) {
+    const hanf_status sst = ensure_sparse(e);
     if (sst != HANF_OK) return sst;
   }
   return compute_local(e);

@@ -90,28 +90,10 @@ struct CsrView {
 // Sets *bad_input when offsets decrease or an arc endpoint is >= n.  Only
 // the final TOS fill reads the arcs: it waits for `succ_ready` (when
 // non-null), so the arcs upload overlaps the degree sort and task layout.
-// defer_fill: the TOS is allocated but not filled (nor the segment bounds
-// computed): the caller fills task ranges with fill_tos_range as their
-// arcs arrive, then calls finish_tasks_device.
 cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
                                uint32_t seg_shift, cudaStream_t s, cudaEvent_t succ_ready,
                                TaskBuild* out, int* bad_input, uint64_t* launches,
-                               bool defer_fill = false, bool seg_bounds = true,
-                               bool class_major = false);
-cudaError_t fill_tos_range(const CsrView& g, const TaskBuild& t, uint64_t t0, uint64_t t1,
-                           uint64_t n, cudaStream_t s, uint64_t* launches);
-// Scatter fill (unrelabelled engines, default from 2^20 arcs): the TOS is
-// filled arc by arc as the upload's node-range chunks land, in the task
-// order of the global degree sort.  scatter_fill_prepare (after a deferred
-// build, before any arc has arrived): every row's TOS slot and the padding;
-// scatter_fill_range: rows [v0, v1) once their arcs are on the device.
-cudaError_t scatter_fill_prepare(TaskBuild* t, uint64_t lo, uint64_t hi, uint64_t n,
-                                 cudaStream_t s, uint64_t* launches);
-cudaError_t scatter_fill_range(const CsrView& g, const TaskBuild& t, uint64_t lo, uint64_t v0,
-                               uint64_t v1, uint64_t n, cudaStream_t s, uint64_t* launches);
-cudaError_t finish_tasks_device(const CsrView& g, TaskBuild* t, uint64_t lo, uint64_t hi,
-                                bool seg_bounds, cudaStream_t s, int* bad_input,
-                                uint64_t* launches);
+                               bool seg_bounds = true, bool class_major = false);
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
 // Locality relabelling (hanf_relabel.cu): rows renumbered by descending
@@ -196,14 +178,6 @@ cudaError_t build_transpose_device(const uint64_t* d_off, const uint32_t* d_succ
 cudaError_t launch_sparse_step(const SparseArgs& a, uint64_t w0, uint64_t w1, uint32_t register_bits,
                                uint32_t registers, cudaStream_t s, uint64_t* launches);
 bool sparse_supported(uint32_t register_bits, uint32_t registers);
-// Worklist step signalled by one scan of the TOS instead of a transpose
-// (tail steps of unrelabelled engines; hanf_sparse.cu scan_signal_kernel):
-// row_task = build_row_task's map from TOS row to warp task.
-cudaError_t build_row_task(const TaskBuild& t, cudaStream_t s, uint32_t** out, uint64_t* launches);
-cudaError_t launch_scan_step(const SparseArgs& a, const TaskBuild& t, const uint32_t* row_task,
-                             const uint64_t* summ, uint32_t summ_shift, uint32_t summ_words,
-                             uint64_t w0, uint64_t w1, uint32_t register_bits, uint32_t registers,
-                             cudaStream_t s, uint64_t* launches);
 
 struct UnionArgs {
   const uint32_t* tos;       // task-ordered successor ids
@@ -239,7 +213,6 @@ struct UnionArgs {
   PeerRows peers;                  // sharded peer-push: also store written rows there
   const uint32_t* seg_live;        // skip sweeps over segmented tasks: segment s has work
   uint32_t seg_shift;              // (TaskBuild::seg_shift)
-  uint32_t hot_rows;               // gather policy 3: rows below are kept in L2 (evict_last)
 };
 
 struct EstimateArgs {
@@ -274,22 +247,15 @@ cudaError_t lift_graph_device(const uint64_t* d_off, const uint32_t* d_succ, uin
 cudaError_t launch_finish_batch(const double* est, const uint64_t* bits, uint64_t n_real, uint32_t K,
                                 bool recompute, double* block_sums, unsigned long long* counts,
                                 cudaStream_t s, uint64_t* launches);
-// map: TMA descriptor of args.cur for the gather4 kernel (nullptr: LDG
-// gathers; only single-chunk layouts with an even pitch take it)
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits,
-                         uint32_t registers, int variant, const CUtensorMap* map,
-                         cudaStream_t s, uint64_t* launches);
+                         uint32_t registers, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* launches);
 // true when the union kernels compute estimates themselves (single-chunk layouts)
 bool fused_estimates(uint32_t register_bits, uint32_t registers);
 // Row pitch of the counter arrays (u64 words between counters): W, except
 // W = 3 which is padded to one aligned 32-byte sector
-// (profiles/r01_row_pitch.md).  With TMA gathers (opt-in HANF_TMA=1,
-// single-chunk layouts) rows are padded to an even word count: gather4
-// moves whole 16-byte-multiple rows.
+// (profiles/r01_row_pitch.md).
 uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words);
-// true when the engine should build TMA descriptors and gather with them
-bool use_tma(uint32_t register_bits, uint32_t registers, uint32_t pitch);
 
 // Step epilogue (block sums + totals), see finish_kernel.
 constexpr int kFinishThreads = 256;  // threads per CTA

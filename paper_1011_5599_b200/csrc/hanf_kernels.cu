@@ -123,7 +123,7 @@ __device__ __forceinline__ void zero_limbs(uint32_t (&x)[Lay::kLimbs]) {
   sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = 0u; });
 }
 
-// GMODE = gather kind + 10 * cache policy (ld16/ld8).
+// GMODE = gather kind (0 per-word loads, 1 16-byte windows, 3 aligned 256-bit rows).
 template <class Lay, int GMODE, bool kVec16>
 struct Gather;
 
@@ -131,32 +131,8 @@ template <class Lay, bool kVec16>
 struct Gather<Lay, 0, kVec16> {
   uint32_t v[Lay::kLimbs];
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
-                                        uint32_t woff, uint64_t = 0) {
+                                        uint32_t woff) {
     load_chunk<Lay, kVec16>(v, cur + static_cast<uint64_t>(w) * words + woff);
-  }
-  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
-    sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = v[decltype(I)::value]; });
-  }
-};
-
-template <class Lay, bool kVec16>
-struct Gather<Lay, 10, kVec16> {
-  uint32_t v[Lay::kLimbs];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
-                                        uint32_t woff, uint64_t = 0) {
-    load_chunk<Lay, kVec16, 1>(v, cur + static_cast<uint64_t>(w) * words + woff);
-  }
-  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
-    sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = v[decltype(I)::value]; });
-  }
-};
-
-template <class Lay, bool kVec16>
-struct Gather<Lay, 20, kVec16> {
-  uint32_t v[Lay::kLimbs];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t words,
-                                        uint32_t woff, uint64_t = 0) {
-    load_chunk<Lay, kVec16, 2>(v, cur + static_cast<uint64_t>(w) * words + woff);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
     sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = v[decltype(I)::value]; });
@@ -166,85 +142,15 @@ struct Gather<Lay, 20, kVec16> {
 template <class Lay, int POL>
 struct Gather128 {
   uint4 raw[Window128<Lay::kWords>::kLoads];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t,
-                                        uint64_t = 0) {
+  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t) {
     window128_load<Lay::kWords, POL>(raw, cur, w);
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
     window128_extract<Lay, Lay::kWords>(x, raw, w);
   }
 };
-// policy 3: 16-byte windows with the L2 policy the caller picks per row
-// (hot rows evict_last, cold rows evict_first; UnionArgs::hot_rows)
-template <class Lay, bool kL1>
-struct Gather128Pol {
-  uint4 raw[Window128<Lay::kWords>::kLoads];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t,
-                                        uint64_t pol) {
-    window128_load_pol<Lay::kWords, kL1>(raw, cur, w, pol);
-  }
-  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
-    window128_extract<Lay, Lay::kWords>(x, raw, w);
-  }
-};
-// policy 5: hot rows L1-allocating + evict_last, cold rows sector-granular
-// (L1::no_allocate) + evict_first
-template <class Lay>
-struct Gather128Split {
-  uint4 raw[Window128<Lay::kWords>::kLoads];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t hot, uint32_t,
-                                        uint64_t pol) {
-    if (w < hot)
-      window128_load_pol<Lay::kWords, true>(raw, cur, w, pol);
-    else
-      window128_load_pol<Lay::kWords, false>(raw, cur, w, pol);
-  }
-  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
-    window128_extract<Lay, Lay::kWords>(x, raw, w);
-  }
-};
-template <class Lay, bool kVec16>
-struct Gather<Lay, 51, kVec16> : Gather128Split<Lay> {};
-template <class Lay, bool kVec16>
-struct Gather<Lay, 31, kVec16> : Gather128Pol<Lay, true> {};
-template <class Lay, bool kVec16>
-struct Gather<Lay, 41, kVec16> : Gather128Pol<Lay, false> {};
 template <class Lay, bool kVec16>
 struct Gather<Lay, 1, kVec16> : Gather128<Lay, 0> {};
-template <class Lay, bool kVec16>
-struct Gather<Lay, 11, kVec16> : Gather128<Lay, 1> {};
-template <class Lay, bool kVec16>
-struct Gather<Lay, 21, kVec16> : Gather128<Lay, 2> {};
-
-template <class Lay, bool kVec16>
-struct Gather<Lay, 2, kVec16> {
-  uint32_t raw[Window<Lay::kWords>::kLoads][8];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t, uint32_t,
-                                        uint64_t = 0) {
-    window_load<Lay::kWords>(raw, cur, w);
-  }
-  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t w) const {
-    window_extract<Lay, Lay::kWords>(x, raw, w);
-  }
-};
-
-// GMODE 33: GMODE 3 with the per-row L2 policy of GMODE 31.
-template <class Lay, bool kVec16>
-struct Gather<Lay, 33, kVec16> {
-  static constexpr int K = (Lay::kWords + 3) / 4;
-  uint32_t raw[K][8];
-  __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t pitch,
-                                        uint32_t woff, uint64_t pol) {
-    const uint64_t* p = cur + static_cast<uint64_t>(w) * pitch + woff;
-    sfor<0, K>([&](auto I) { ldg256_pol(raw[decltype(I)::value], p + 4 * decltype(I)::value, pol); });
-  }
-  __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
-    sfor<0, Lay::kLimbs>([&](auto I) {
-      constexpr int i = decltype(I)::value;
-      x[i] = raw[i / 8][i % 8];
-    });
-  }
-};
 
 // GMODE 3: rows padded to a multiple of 4 words (row_pitch): counter w
 // starts a 32-byte block, ceil(W/4) aligned 256-bit loads, no shifts.
@@ -253,7 +159,7 @@ struct Gather<Lay, 3, kVec16> {
   static constexpr int K = (Lay::kWords + 3) / 4;
   uint32_t raw[K][8];
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t pitch,
-                                        uint32_t woff, uint64_t = 0) {
+                                        uint32_t woff) {
     const uint64_t* p = cur + static_cast<uint64_t>(w) * pitch + woff;
     sfor<0, K>([&](auto I) { ldg256(raw[decltype(I)::value], p + 4 * decltype(I)::value); });
   }
@@ -348,7 +254,7 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
                                             bool lead, uint32_t v, bool stale,
                                             uint32_t (&acc)[Lay::kLimbs], uint32_t woff,
                                             uint32_t G, bool live, bool& any_changed,
-                                            OwnLoad own_load, uint64_t st_pol = 0) {
+                                            OwnLoad own_load) {
   constexpr int NL = Lay::kLimbs;
   const uint32_t words = args.pitch;
   if (live)  // (all-zero accumulators need no butterfly)
@@ -375,14 +281,10 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
     any_changed |= changed;
     if (changed || (lead && stale)) {
       const uint64_t off = static_cast<uint64_t>(v) * words + woff;
-      if (args.chunks == 1) {
-        if (st_pol)
-          store_counter_pol<Lay>(args.next + off, acc, st_pol);
-        else
-          store_counter<Lay>(args.next + off, acc);
-      } else {
+      if (args.chunks == 1)
+        store_counter<Lay>(args.next + off, acc);
+      else
         store_chunk<Lay, kVec16>(args.next + off, acc);
-      }
       // sharded peer-push: the same row into every peer's next generation
       for (uint32_t p = 0; p < args.peers.count; ++p) {
         if (args.chunks == 1)
@@ -458,16 +360,6 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
   const uint32_t* __restrict__ ids = args.tos + task.tos + lane;
   const uint32_t words = args.pitch;
   const uint32_t trips = task.trips;
-  constexpr bool kPol = GMODE / 10 == 3 || GMODE / 10 == 4 || GMODE / 10 == 5;
-  uint64_t pol_hot = 0, pol_cold = 0;
-  if constexpr (kPol) {
-    pol_hot = l2_policy_evict_last();
-    pol_cold = l2_policy_evict_first();
-  }
-  const uint32_t hot_rows = args.hot_rows;
-  auto ld_id = [&](const uint32_t* p) -> uint32_t {
-    if constexpr (kPol) return ld4_pol(p, pol_cold); else return ld_stream_u32(p);
-  };
 
   bool any_changed = false;
   for (uint32_t ch = 0; ch < args.chunks; ++ch) {
@@ -480,7 +372,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
     uint32_t wn[U];
     if (PF) {
 #pragma unroll
-      for (int j = 0; j < U; ++j) wn[j] = (j < trips) ? ld_id(ids + 32 * j) : zero_row;
+      for (int j = 0; j < U; ++j) wn[j] = (j < trips) ? ld_stream_u32(ids + 32 * j) : zero_row;
     }
     for (uint32_t i = 0; i < trips; i += U) {
       uint32_t w[U];
@@ -488,12 +380,12 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           w[j] = wn[j];
-          wn[j] = (i + U + j < trips) ? ld_id(ids + 32 * (i + U + j)) : zero_row;
+          wn[j] = (i + U + j < trips) ? ld_stream_u32(ids + 32 * (i + U + j)) : zero_row;
         }
       } else {
 #pragma unroll
         for (int j = 0; j < U; ++j)
-          w[j] = (i + j < trips) ? ld_id(ids + 32 * (i + j)) : zero_row;
+          w[j] = (i + j < trips) ? ld_stream_u32(ids + 32 * (i + j)) : zero_row;
       }
       if constexpr (SKIP) {
 #pragma unroll
@@ -516,9 +408,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
       }
       G_t g[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j)
-        g[j].issue(cur, w[j], GMODE / 10 == 5 ? hot_rows : words, woff,
-                   w[j] < hot_rows ? pol_hot : pol_cold);
+      for (int j = 0; j < U; ++j) g[j].issue(cur, w[j], words, woff);
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         uint32_t y[NL];
@@ -530,9 +420,9 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
                              [&](uint32_t (&own)[NL], bool need) {
                                const uint32_t r = need ? v : zero_row;
                                G_t g;
-                               g.issue(cur, r, words, woff, pol_cold);
+                               g.issue(cur, r, words, woff);
                                g.extract(own, r);
-                             }, pol_cold);
+                             });
   }
   task_finish<Lay, kVec16>(args, task, hub, v, any_changed, lane);
 }
@@ -566,104 +456,6 @@ __global__ void __launch_bounds__(256, MINB) union_kernel(const UnionArgs args) 
   }
   if (gw >= args.num_wtasks) return;
   union_task<R, NREG, U, GMODE, kVec16, MINB, PF, SKIP>(args, gw, lane, summ);
-}
-
-// ---------------------------------------------------------------------------
-// Union sweep with TMA row gathers (single-chunk layouts, even pitch).  Same
-// tasks, TOS rows and commit as union_kernel; the successor counters of
-// trip t land in stage t mod S of the warp's shared-memory ring: lane 0
-// arms the stage's mbarrier with the byte count, lanes 0-7 each issue one
-// gather4 for the rows of lanes 4k..4k+3, and every lane reads its own row
-// back once the barrier's phase completes.  S - 1 trips are in flight
-// while one is folded; the loads never touch the LSU data pipe, which
-// bounds the LDG gather (profiles/r01_tma_gather.md).
-// ---------------------------------------------------------------------------
-__host__ __device__ constexpr uint32_t tma_slot_bytes(uint32_t pitch) {
-  return (4 * pitch * 8 + 127) & ~127u;  // gather4 destinations are 128-byte aligned
-}
-__host__ __device__ constexpr uint32_t tma_smem_bytes(uint32_t pitch, int S) {
-  return 1024 + 8 * S * 8 * tma_slot_bytes(pitch);
-}
-
-template <int R, int NREG, int S, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-    union_tma_kernel(const UnionArgs args, const __grid_constant__ CUtensorMap map) {
-  using Lay = Layout<R, NREG>;
-  constexpr int NL = Lay::kLimbs;
-  static_assert(8 * S * 8 <= 1024, "barrier area");
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t gw = blockIdx.x * 8 + warp;
-  if (gw >= args.num_wtasks) return;
-  const uint32_t pitch = args.pitch;
-  const uint32_t row_bytes = pitch * 8;
-  const uint32_t slot = tma_slot_bytes(pitch);
-  const uint32_t stage_bytes = 8 * slot;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * S;
-  uint8_t* ring = smem + 1024 + warp * S * stage_bytes;
-  const uint32_t my_off = (lane >> 2) * slot + (lane & 3) * row_bytes;
-  if (lane < S) mbar_init(bars + lane, 1);
-  mbar_init_fence();
-  __syncwarp();
-
-  const WarpTask task = args.wtasks[gw];
-  const bool hub = task.nodes == 0;
-  const uint32_t lg = hub ? 5u : task.lg;
-  const uint32_t G = 1u << lg;
-  const uint32_t sub = lane & (G - 1);
-  const uint32_t zero_row = args.zero_row;
-  uint32_t v = zero_row;
-  bool active = true;
-  if (hub) {
-    v = args.hub_node[task.item];
-  } else {
-    const uint32_t j = lane >> lg;
-    active = j < task.nodes;
-    if (active) v = args.order[task.item + j];
-  }
-  const bool lead = active && sub == 0 && !hub;
-  bool stale = false;
-  if (lead && args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
-  const uint64_t* __restrict__ cur = args.cur;
-  const uint32_t* __restrict__ ids = args.tos + task.tos + lane;
-  const uint32_t trips = task.trips;
-
-  uint32_t fs = 0;  // next stage to fill
-  auto fill = [&](uint32_t t) {
-    uint32_t w = ld_stream_u32(ids + 32 * t);
-    if (args.check_mod && !((__ldg(args.mod_cur + (w >> 6)) >> (w & 63)) & 1)) w = zero_row;
-    if (lane == 0) mbar_expect_tx(bars + fs, 32 * row_bytes);
-    const uint32_t r0 = __shfl_sync(0xffffffffu, w, (4 * lane + 0) & 31);
-    const uint32_t r1 = __shfl_sync(0xffffffffu, w, (4 * lane + 1) & 31);
-    const uint32_t r2 = __shfl_sync(0xffffffffu, w, (4 * lane + 2) & 31);
-    const uint32_t r3 = __shfl_sync(0xffffffffu, w, (4 * lane + 3) & 31);
-    if (lane < 8) tma_gather4(ring + fs * stage_bytes + lane * slot, &map, bars + fs, r0, r1, r2, r3);
-    fs = fs + 1 == S ? 0 : fs + 1;
-  };
-
-  uint32_t acc[NL];
-  zero_limbs<Lay>(acc);  // the own counter joins in node_commit
-  const uint32_t pre = trips < S - 1 ? trips : S - 1;
-  for (uint32_t t = 0; t < pre; ++t) fill(t);
-  uint32_t us = 0, ph = 0;
-  for (uint32_t t = 0; t < trips; ++t) {
-    __syncwarp();  // every lane is done with the stage refilled next
-    if (t + S - 1 < trips) fill(t + S - 1);
-    mbar_wait(bars + us, ph);
-    uint32_t y[NL];
-    load_row16<Lay>(y, ring + us * stage_bytes + my_off);
-    swar_max<Lay>(acc, y);
-    if (++us == S) {
-      us = 0;
-      ph ^= 1;
-    }
-  }
-  bool any_changed = false;
-  node_commit<Lay, false>(args, task, hub, lead, v, stale, acc, 0, G, true, any_changed,
-                          [&](uint32_t (&own)[NL], bool need) {
-                            load_row16<Lay>(own, cur + static_cast<uint64_t>(need ? v : zero_row) * pitch);
-                          });
-  task_finish<Lay, false>(args, task, hub, v, any_changed, lane);
 }
 
 namespace {
@@ -704,165 +496,48 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int R, int NREG, int S, int MINB>
-cudaError_t union_tma_launch(UnionArgs a, const CUtensorMap* map, cudaStream_t s) {
-  a.chunks = 1;
-  if (a.num_wtasks == 0) return cudaSuccess;
-  const uint32_t smem = tma_smem_bytes(a.pitch, S);
-  static bool attr_set = false;  // per instantiation; first call is outside capture
-  if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(union_tma_kernel<R, NREG, S, MINB>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const uint32_t blocks = (a.num_wtasks + 7) / 8;
-  union_tma_kernel<R, NREG, S, MINB><<<blocks, 256, smem, s>>>(a, *map);
-  return cudaGetLastError();
-}
-
 }  // namespace
 
 bool fused_estimates(uint32_t register_bits, uint32_t registers) {
   return choose(register_bits, registers).chunks == 1;
 }
 
-namespace {
-// Opt-in (HANF_TMA=1): measured slower than the LDG window gathers on the
-// BASELINE graphs (profiles/r01_tma_gather.md).
-bool tma_env_enabled() {
-  const char* env = std::getenv("HANF_TMA");
-  return env && env[0] == '1';
-}
-}  // namespace
-
+// Rows of W = 3 words are padded to 4 (one aligned 32-byte sector per
+// counter: +5% on the DRAM-bound BA graph, profiles/r01_row_pitch.md);
+// every other layout keeps the reference's dense packing.
 uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words) {
   if (choose(register_bits, registers).chunks != 1) return words;
-  if (const char* env = std::getenv("HANF_PITCH")) {
-    if (env[0] == '0') return words;
-    if (env[0] == '1') return (words + 3) & ~3u;  // experiments: pad every layout
-  }
-  if (tma_env_enabled()) return (words + 1) & ~1u;
   return words == 3 ? 4 : words;
 }
 
-bool use_tma(uint32_t register_bits, uint32_t registers, uint32_t pitch) {
-  return choose(register_bits, registers).chunks == 1 && pitch % 2 == 0 && tma_env_enabled();
-}
-
-// variant < 0 picks the measured best gather for the layout (profiles/);
-// variants >= 0 select alternatives for experiments (HANF_GATHER).
+// The measured best gather per layout (profiles/r01_*): 16-byte windows
+// for m = 64 (3 x LDG.128 per 40-byte counter, U = 3 in flight, <= 48
+// registers), aligned 256-bit loads for padded W = 3 rows, 16-byte vector
+// loads where rows are 16-byte aligned, per-word loads otherwise.
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t registers,
-                         int variant, const CUtensorMap* map, cudaStream_t s,
-                         uint64_t* launches) {
+                         cudaStream_t s, uint64_t* launches) {
   const KernelChoice k = choose(register_bits, registers);
   if (args.num_wtasks == 0) return cudaSuccess;
   ++*launches;
   const uint32_t ch = static_cast<uint32_t>(k.chunks);
   const bool single = ch == 1;
-  if (map && single) switch (k.r * 1000 + k.nreg) {
-      case 5016: return union_tma_launch<5, 16, 4, 4>(args, map, s);
-      case 5032: return union_tma_launch<5, 32, 4, 4>(args, map, s);
-      case 5064:
-        switch (variant) {
-          case 40: return union_tma_launch<5, 64, 2, 4>(args, map, s);
-          case 41: return union_tma_launch<5, 64, 4, 3>(args, map, s);
-          case 42: return union_tma_launch<5, 64, 3, 3>(args, map, s);
-          default: return union_tma_launch<5, 64, 3, 4>(args, map, s);
-        }
-      case 5128: return union_tma_launch<5, 128, 3, 3>(args, map, s);
-      case 6016: return union_tma_launch<6, 16, 4, 4>(args, map, s);
-      case 6032: return union_tma_launch<6, 32, 4, 4>(args, map, s);
-      case 7016: return union_tma_launch<7, 16, 4, 4>(args, map, s);
-      case 7032: return union_tma_launch<7, 32, 4, 4>(args, map, s);
-      case 7064: return union_tma_launch<7, 64, 3, 3>(args, map, s);
-      case 8016: return union_tma_launch<8, 16, 4, 4>(args, map, s);
-      default: break;
-    }
   if (single && args.pitch % 4 == 0) switch (k.r * 1000 + k.nreg) {
-      case 5032:
-        if (variant == 30) return union_launch<5, 32, 4, 3, false, 4, true>(args, ch, s);
-        if (variant == 50) return union_launch<5, 32, 4, 33, false, 1, true>(args, ch, s);
-        if (variant == 51) return union_launch<5, 32, 4, 33, false, 4, true>(args, ch, s);
-        return union_launch<5, 32, 4, 3, false, 1, true>(args, ch, s);
-      case 5064:
-        switch (variant) {
-          case 30: return union_launch<5, 64, 2, 3, false, 4, true>(args, ch, s);
-          case 31: return union_launch<5, 64, 4, 3, false, 3, true>(args, ch, s);
-          case 32: return union_launch<5, 64, 3, 3, false, 3, true>(args, ch, s);
-          case 33: return union_launch<5, 64, 3, 3, false, 4, false>(args, ch, s);
-          default: return union_launch<5, 64, 3, 3, false, 4, true>(args, ch, s);
-        }
-      case 5128:
-        if (variant == 30) return union_launch<5, 128, 1, 3, false, 4, true>(args, ch, s);
-        return union_launch<5, 128, 2, 3, false, 3, true>(args, ch, s);
+      case 5032: return union_launch<5, 32, 4, 3, false, 1, true>(args, ch, s);
       case 6032: return union_launch<6, 32, 4, 3, false, 1, true>(args, ch, s);
       case 7032: return union_launch<7, 32, 4, 3, false, 1, true>(args, ch, s);
-      case 7064: return union_launch<7, 64, 2, 3, false, 1, true>(args, ch, s);
       default: break;
     }
   switch (k.r * 1000 + k.nreg) {
     case 5016: return union_launch<5, 16, 4, 0, true>(args, ch, s);
     case 5032:
-      if (single) switch (variant) {
-          case 0: return union_launch<5, 32, 4, 0, false>(args, ch, s);
-          case 2: return union_launch<5, 32, 4, 2, false>(args, ch, s);
-          case 3: return union_launch<5, 32, 2, 1, false>(args, ch, s);
-          case 7: return union_launch<5, 32, 4, 1, false, 4>(args, ch, s);
-          case 8: return union_launch<5, 32, 4, 0, false, 4>(args, ch, s);
-          case 9: return union_launch<5, 32, 8, 1, false, 3>(args, ch, s);
-          case 11: return union_launch<5, 32, 4, 11, false>(args, ch, s);
-          case 12: return union_launch<5, 32, 4, 21, false>(args, ch, s);
-          case 13: return union_launch<5, 32, 4, 10, false>(args, ch, s);
-          case 14: return union_launch<5, 32, 8, 11, false, 3>(args, ch, s);
-          case 20: return union_launch<5, 32, 4, 1, false, 1, true>(args, ch, s);
-          default: return union_launch<5, 32, 4, 1, false, 1, true>(args, ch, s);
-        }
+      if (single) return union_launch<5, 32, 4, 1, false, 1, true>(args, ch, s);
       return union_launch<5, 32, 4, 0, false>(args, ch, s);
     case 5064:
-      if (single) switch (variant) {
-          case 0: return union_launch<5, 64, 4, 0, false>(args, ch, s);
-          case 1: return union_launch<5, 64, 4, 1, false>(args, ch, s);
-          case 2: return union_launch<5, 64, 4, 2, false>(args, ch, s);
-          case 3: return union_launch<5, 64, 2, 2, false>(args, ch, s);
-          case 5: return union_launch<5, 64, 2, 2, false, 6>(args, ch, s);
-          case 6: return union_launch<5, 64, 4, 1, false, 5>(args, ch, s);
-          case 7: return union_launch<5, 64, 2, 1, false, 4>(args, ch, s);
-          case 10: return union_launch<5, 64, 2, 1, false>(args, ch, s);
-          case 11: return union_launch<5, 64, 3, 11, false, 4>(args, ch, s);
-          case 12: return union_launch<5, 64, 3, 21, false, 4>(args, ch, s);
-          case 13: return union_launch<5, 64, 4, 10, false>(args, ch, s);
-          case 9: return union_launch<5, 64, 2, 2, false, 4>(args, ch, s);
-          case 20: return union_launch<5, 64, 3, 1, false, 4, true>(args, ch, s);
-          case 21: return union_launch<5, 64, 2, 1, false, 4, true>(args, ch, s);
-          case 23: return union_launch<5, 64, 2, 1, false, 5, true>(args, ch, s);
-          case 24: return union_launch<5, 64, 2, 1, false, 6, true>(args, ch, s);
-          case 25: return union_launch<5, 64, 3, 1, false, 4, true>(args, ch, s);  // r01 default
-          case 26: return union_launch<5, 64, 1, 1, false, 6, true>(args, ch, s);
-          case 27: return union_launch<5, 64, 1, 1, false, 8, true>(args, ch, s);
-          case 22: return union_launch<5, 64, 3, 1, false, 4>(args, ch, s);
-          case 50: return union_launch<5, 64, 3, 31, false, 5, true>(args, ch, s);
-          case 51: return union_launch<5, 64, 4, 31, false, 4, true>(args, ch, s);
-          case 52: return union_launch<5, 64, 3, 41, false, 5, true>(args, ch, s);
-          case 53: return union_launch<5, 64, 3, 51, false, 5, true>(args, ch, s);
-          // U = 3, <= 48 registers (5 CTAs/SM), next-trip id prefetch: +2%
-          // on config 2 and +1% on R-MAT 26 over 64 registers
-          default: return union_launch<5, 64, 3, 1, false, 5, true>(args, ch, s);
-        }
+      // U = 3, <= 48 registers (5 CTAs/SM), next-trip id prefetch: +2%
+      // on config 2 and +1% on R-MAT 26 over 64 registers
+      if (single) return union_launch<5, 64, 3, 1, false, 5, true>(args, ch, s);
       return union_launch<5, 64, 4, 0, false>(args, ch, s);
-    case 5128:
-      switch (variant) {
-        case 2: return union_launch<5, 128, 2, 2, true>(args, ch, s);
-        case 7: return union_launch<5, 128, 2, 0, true, 3>(args, ch, s);
-        case 8: return union_launch<5, 128, 1, 0, true, 4>(args, ch, s);
-        case 9: return union_launch<5, 128, 1, 2, true, 4>(args, ch, s);
-        case 11: return union_launch<5, 128, 2, 10, true, 3>(args, ch, s);
-        case 12: return union_launch<5, 128, 2, 20, true, 3>(args, ch, s);
-        case 20: return union_launch<5, 128, 2, 0, true, 3, true>(args, ch, s);
-        case 22: return union_launch<5, 128, 2, 0, true, 3>(args, ch, s);
-        default: return union_launch<5, 128, 2, 0, true, 3, true>(args, ch, s);
-      }
+    case 5128: return union_launch<5, 128, 2, 0, true, 3, true>(args, ch, s);
     case 6016: return union_launch<6, 16, 4, 0, true>(args, ch, s);
     case 6032: return union_launch<6, 32, 4, 0, false>(args, ch, s);
     case 7016: return union_launch<7, 16, 4, 0, true>(args, ch, s);

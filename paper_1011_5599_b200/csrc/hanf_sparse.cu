@@ -272,101 +272,11 @@ cudaError_t build_transpose_device(const uint64_t* d_off, const uint32_t* d_succ
   return cudaGetLastError();
 }
 
-// ---- scan signalling (no transpose) ----------------------------------------
-// row_task[r] = the warp task owning TOS row r (a row = 32 ids)
-__global__ void row_task_kernel(const WarpTask* __restrict__ tasks, uint64_t num_tasks,
-                                uint32_t* __restrict__ row_task) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < num_tasks;
-       t += stride) {
-    const WarpTask w = tasks[t];
-    for (uint32_t i = 0; i < w.trips; ++i) row_task[(w.tos >> 5) + i] = static_cast<uint32_t>(t);
-  }
-}
-
-// One pass over the whole TOS, 4 ids per thread per load (coalesced): an id
-// whose counter changed in the last step signals the node owning its slot
-// (the systolic "signal the predecessors" of engine.hpp:210-224, without a
-// transpose).  The modified-bitmap summary (one bit per 2^shift rows) is
-// staged in shared memory; the bitmap is probed only where it is set.
-__global__ void __launch_bounds__(256)
-scan_signal_kernel(const uint4* __restrict__ tos, uint64_t quads, const uint32_t* __restrict__ row_task,
-                   const WarpTask* __restrict__ tasks, const uint32_t* __restrict__ order,
-                   const uint32_t* __restrict__ chunk_node, const uint64_t* __restrict__ mod_cur,
-                   const uint64_t* __restrict__ summ, uint32_t summ_shift, uint32_t summ_words,
-                   uint64_t* __restrict__ sig) {
-  extern __shared__ uint64_t sm[];
-  for (uint32_t i = threadIdx.x; i < summ_words; i += blockDim.x) sm[i] = summ[i];
-  __syncthreads();
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < quads;
-       q += stride) {
-    const uint4 ids = tos[q];
-    const uint32_t w4[4] = {ids.x, ids.y, ids.z, ids.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t w = w4[k];
-      if (!((sm[w >> (summ_shift + 6)] >> ((w >> summ_shift) & 63)) & 1)) continue;
-      if (!((mod_cur[w >> 6] >> (w & 63)) & 1)) continue;  // (padding: row n is never set)
-      const uint64_t pos = 4 * q + k;  // id slot in the TOS
-      const WarpTask t = tasks[row_task[pos >> 5]];
-      const uint32_t lane = static_cast<uint32_t>(pos & 31);
-      uint32_t v;
-      if (t.nodes == 0) {
-        v = chunk_node[t.item];
-      } else {
-        const uint32_t j = lane >> t.lg;
-        if (j >= t.nodes) continue;
-        v = order[t.item + j];
-      }
-      atomicOr(reinterpret_cast<unsigned long long*>(sig) + (v >> 6), 1ull << (v & 63));
-    }
-  }
-}
-
-cudaError_t build_row_task(const TaskBuild& t, cudaStream_t s, uint32_t** out, uint64_t* launches) {
-  *out = nullptr;
-  const uint64_t rows = t.tos_words / 32;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(out), sizeof(uint32_t) * (rows ? rows : 1), s);
-  if (e != cudaSuccess || t.num_wtasks == 0) return e;
-  uint64_t blocks = (t.num_wtasks + 255) / 256;
-  if (blocks > 148ull * 32) blocks = 148ull * 32;
-  row_task_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(t.wtasks, t.num_wtasks, *out);
-  ++*launches;
-  return cudaGetLastError();
-}
-
 // Stages 3-4 of the worklist step: the worklist from sig | stale, then the
 // sparse union (hubs go to the dense kernel through hub_tasks, by the caller)
 cudaError_t sparse_tail_stages(const SparseArgs& a, uint64_t w0, uint64_t w1,
                                uint32_t register_bits, uint32_t registers, cudaStream_t s,
                                uint64_t* launches);
-
-cudaError_t launch_scan_step(const SparseArgs& a, const TaskBuild& t, const uint32_t* row_task,
-                             const uint64_t* summ, uint32_t summ_shift, uint32_t summ_words,
-                             uint64_t w0, uint64_t w1, uint32_t register_bits, uint32_t registers,
-                             cudaStream_t s, uint64_t* launches) {
-  cudaError_t e = cudaMemsetAsync(a.lens, 0, 3 * sizeof(unsigned int), s);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(a.sig + w0, 0, sizeof(uint64_t) * (w1 - w0), s);
-  if (e != cudaSuccess) return e;
-  const uint64_t quads = t.tos_words / 4;
-  if (quads) {
-    const size_t smem = sizeof(uint64_t) * summ_words;
-    if (smem > 48 * 1024) {
-      e = cudaFuncSetAttribute(scan_signal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-    }
-    scan_signal_kernel<<<148 * 4, 256, smem, s>>>(reinterpret_cast<const uint4*>(t.tos), quads,
-                                                  row_task, t.wtasks, t.order, t.chunk_node,
-                                                  a.mod_cur, summ, summ_shift, summ_words, a.sig);
-    ++*launches;
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return sparse_tail_stages(a, w0, w1, register_bits, registers, s, launches);
-}
 
 cudaError_t launch_sparse_step(const SparseArgs& a, uint64_t w0, uint64_t w1, uint32_t register_bits,
                                uint32_t registers, cudaStream_t s, uint64_t* launches) {

@@ -38,7 +38,6 @@ def single(relabel):
 
 def sharded(relabel, scatter="1"):
     os.environ["HANF_RELABEL"] = "1" if relabel else "0"
-    os.environ["HANF_EST_SCATTER"] = scatter
     c = dataclasses.replace(cfg, shard_count=G)
     shards = [LocalCudaShard(g, c, lo, hi, dev) for lo, hi in shard_ranges(g.num_nodes(), G)]
     engines = [s.engine for s in shards]

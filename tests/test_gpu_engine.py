@@ -306,7 +306,6 @@ def test_config2_scale(hanf, port):
                                          (5, {}, False), (8, {}, False), (6, {}, True),
                                          (5, {"HANF_SPARSE": "1"}, True), (8, {}, True),
                                          (6, {"HANF_SEGMENTS": "1"}, True),
-                                         (6, {"HANF_SCAN": "1"}, True), (5, {"HANF_SCAN": "1"}, False),
                                          (7, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"}, False)])
 def test_sharded_engines_exchange(hanf, port, monkeypatch, b, env, delta):
     """The shard ABI (hanf_shard_compute / device buffers / hanf_shard_commit)
@@ -377,8 +376,9 @@ def test_launch_accounting(hanf):
 
 
 def test_worklist_step_parity(hanf, port, monkeypatch):
-    """The opt-in worklist step (HANF_SPARSE=1, engine.hpp:210-224 systolic
-    mode) changes time only: lockstep bit-exact with the oracle."""
+    """The worklist step (engine.hpp:210-224 systolic mode; on by default
+    below n/128 changed counters on graphs from 2^22 arcs, forced here with
+    HANF_SPARSE=1) changes time only: lockstep bit-exact with the oracle."""
     monkeypatch.setenv("HANF_SPARSE", "1")
     for g in (hanf.gen_rmat(12, 16, 0.57, 0.19, 0.19, 2, 3),
               hanf.Graph.from_edges(300, [(v, v + 1) for v in range(299)]),
@@ -387,20 +387,15 @@ def test_worklist_step_parity(hanf, port, monkeypatch):
             lockstep(hanf, port, g, bucket_bits=b, seed=9)
 
 
-@pytest.mark.parametrize("env", [{"HANF_PITCH": "1"}, {"HANF_PITCH": "0"},
-                                 {"HANF_GATHER": "22"}, {"HANF_GATHER": "2"},
-                                 {"HANF_PITCH": "1", "HANF_GATHER": "30"},
-                                 {"HANF_TMA": "1"}, {"HANF_TMA": "1", "HANF_GATHER": "40"},
-                                 {"HANF_RELABEL": "1"}, {"HANF_RELABEL": "1", "HANF_SPARSE": "1"},
-                                 {"HANF_RELABEL": "1", "HANF_PITCH": "0"},
+@pytest.mark.parametrize("env", [{}, {"HANF_RELABEL": "1"}, {"HANF_RELABEL": "1", "HANF_SPARSE": "1"},
                                  {"HANF_SUMMARY": "1"}, {"HANF_SUMMARY": "1", "HANF_RELABEL": "1"},
                                  {"HANF_SEGMENTS": "1"}, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"},
-                                 {"HANF_SEGMENTS": "1", "HANF_SPARSE": "1"},
-                                 {"HANF_SCAN": "1"}, {"HANF_SCAN": "1", "HANF_PITCH": "0"}])
+                                 {"HANF_SEGMENTS": "1", "HANF_SPARSE": "1"}])
 def test_row_pitch_and_gather_variants(hanf, port, monkeypatch, env):
-    """Padded rows (aligned 256-bit gathers), unpadded rows and the
-    alternative gather kernels change time only: counters read back in the
-    reference packing and bit-exact in lockstep with the oracle."""
+    """Every layout's gather (padded W = 3 rows with aligned 256-bit loads,
+    16-byte windows, per-word loads, multi-chunk counters) under each
+    schedule change time only: counters read back in the reference packing
+    and bit-exact in lockstep with the oracle."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for g in (hanf.gen_rmat(11, 16, 0.57, 0.19, 0.19, 4, 6), hanf.gen_clique_path(20, 9)):
@@ -440,43 +435,10 @@ def test_golden_trace_segmented(hanf, traces, idx, monkeypatch):
     test_golden_trace(hanf, traces, idx)
 
 
-@pytest.mark.parametrize("idx", range(28))
-def test_golden_trace_scan_worklist(hanf, traces, idx, monkeypatch):
-    """Scan-signalled worklist steps (one pass over the TOS marks the nodes
-    with a changed successor; on by default for tail steps of unrelabelled
-    graphs from 2^22 arcs, forced here for every skip step): every golden
-    iteration bit-exact."""
-    monkeypatch.setenv("HANF_SCAN", "1")
-    test_golden_trace(hanf, traces, idx)
-
-
-@pytest.mark.parametrize("idx", range(28))
-def test_golden_trace_scatter_fill(hanf, traces, idx, monkeypatch):
-    """Scatter fill (the TOS filled arc by arc as the upload's node-range
-    chunks land; on by default from 2^20 arcs, forced here): every golden
-    iteration bit-exact."""
-    monkeypatch.setenv("HANF_SCATTER_FILL", "1")
-    test_golden_trace(hanf, traces, idx)
-
-
-@pytest.mark.parametrize("idx", range(28))
-def test_golden_trace_pipelined(hanf, traces, idx, monkeypatch):
-    """Pipelined create (arcs uploaded in node-range chunks, iteration 1's
-    sweep run chunk by chunk as they land; on by default from 2^20 arcs,
-    forced here): every golden iteration bit-exact."""
-    monkeypatch.setenv("HANF_PIPELINE", "1")
-    test_golden_trace(hanf, traces, idx)
-
-
-@pytest.mark.parametrize("env", [{"HANF_PIPELINE": "1"}, {"HANF_PIPELINE": "1", "HANF_SEGMENTS": "1"},
-                                 {"HANF_PIPELINE": "0"}, {"HANF_SCATTER_FILL": "1"},
-                                 {"HANF_SCATTER_FILL": "1", "HANF_SEGMENTS": "1"},
-                                 {"HANF_SCATTER_FILL": "0"}])
-def test_pipelined_create_lockstep_and_reset(hanf, port, monkeypatch, env):
-    """The precomputed iteration 1 is consumed by the first step only:
-    lockstep with the oracle, then reset / reseed re-run every step in full,
-    and bad arcs are still rejected (the pipelined sweep reads the zero row
-    for them before the check reports)."""
+@pytest.mark.parametrize("env", [{}, {"HANF_SEGMENTS": "1"}])
+def test_create_lockstep_and_reset(hanf, port, monkeypatch, env):
+    """Lockstep with the oracle, then reset / reseed re-run every step in
+    full, and bad arcs are rejected at create."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = hanf.gen_rmat(13, 16, 0.57, 0.19, 0.19, 2, 3)
@@ -490,7 +452,6 @@ def test_pipelined_create_lockstep_and_reset(hanf, port, monkeypatch, env):
         assert e.run_to_stabilisation().values == ref.values
         e.reseed(22)
         other = e.run_to_stabilisation()
-    monkeypatch.setenv("HANF_PIPELINE", "0")
     assert other.values == hanf.estimate_nf(g, hanf.EngineConfig(bucket_bits=6, seed=22)).values
     for k, v in env.items():
         monkeypatch.setenv(k, v)

@@ -86,9 +86,7 @@ def _run_local(hanf, g, cfg, world, skew, relabelled=False, reduce=False):
 @pytest.mark.parametrize("b,env,world,skew", [
     (6, {}, 2, False), (6, {}, 3, False), (6, {}, 2, True), (6, {"HANF_SPARSE": "1"}, 2, False),
     (6, {"HANF_SPARSE": "1"}, 3, True), (5, {}, 2, True), (8, {}, 2, False), (7, {}, 3, False),
-    (6, {"HANF_SEGMENTS": "1"}, 3, True), (5, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"}, 2, False),
-    (6, {"HANF_SCATTER_FILL": "1"}, 3, False), (6, {"HANF_SCAN": "1"}, 3, True),
-    (7, {"HANF_SCAN": "1"}, 2, False)])
+    (6, {"HANF_SEGMENTS": "1"}, 3, True), (5, {"HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"}, 2, False)])
 def test_peer_push_local(hanf, monkeypatch, b, env, world, skew):
     """Attached shard engines of one process: bit-exact with one engine, with
     the worklist step, the padded W = 3 rows, m = 128 and a multi-chunk layout."""
@@ -105,18 +103,16 @@ def test_peer_push_local(hanf, monkeypatch, b, env, world, skew):
         assert np.array_equal(c, ref)
 
 
-@pytest.mark.parametrize("b,world,skew,scatter,reduce", [
-    (6, 2, False, "1", False), (6, 4, True, "1", False), (6, 4, True, "0", False),
-    (5, 2, True, "1", False), (7, 4, False, "0", False), (6, 4, False, "0", True),
-    (6, 4, True, "0", True), (5, 2, True, "1", True), (7, 4, False, "0", True)])
-def test_peer_push_relabelled_shards(hanf, monkeypatch, b, world, skew, scatter, reduce):
+@pytest.mark.parametrize("b,world,skew,reduce", [
+    (6, 2, False, False), (6, 4, True, False), (5, 2, True, False), (7, 4, False, False),
+    (6, 4, False, True), (6, 4, True, True), (5, 2, True, True), (7, 4, False, True)])
+def test_peer_push_relabelled_shards(hanf, monkeypatch, b, world, skew, reduce):
     """Relabelled shards (hanf_config.shard_count, degree order interleaved
     across the shards): rows live in another numbering on the device,
     estimates are pushed to the peers and every commit re-sums all
     original-id blocks.  N(t) and the counters equal one engine bit for bit."""
     import dataclasses
     monkeypatch.setenv("HANF_RELABEL", "1")
-    monkeypatch.setenv("HANF_EST_SCATTER", scatter)  # estimates in original ids / in rows
     g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
     cfg = hanf.EngineConfig(bucket_bits=b, seed=42)
     values, mods, counters = _run_local(hanf, g, dataclasses.replace(cfg, shard_count=world),
