@@ -443,6 +443,7 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   HANF_BUILD_TRY(cudaFreeAsync(d_bounds, s));
   HANF_BUILD_TRY(cudaFreeAsync(d_wbeg, s));
   TaskBuild& o = *out;
+  o.active_nodes = hubs + light;
   const uint64_t warps = wbeg[ng];
   for (uint64_t i = 0; i < ng; ++i) {
     if (wbeg[i + 1] == wbeg[i]) continue;  // empty group
@@ -573,7 +574,7 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
 void free_tasks_device(TaskBuild* t, cudaStream_t s) {
   void* ptrs[] = {t->order, t->wtasks, t->tos, t->chunk_node, t->chunk_hub,
                   t->hub_nodes, t->hub_first, t->hub_count, t->hub_ticket,
-                  t->seg_min, t->seg_max, t->chunk_begin, t->fill_bad, t->row_slot};
+                  t->seg_min, t->seg_max, t->chunk_begin, t->fill_bad};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   *t = TaskBuild{};

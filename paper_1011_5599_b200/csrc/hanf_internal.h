@@ -40,6 +40,7 @@ struct TaskBuild {
   uint32_t* hub_count = nullptr;
   uint32_t* hub_ticket = nullptr;
   uint32_t num_hubs = 0;
+  uint64_t active_nodes = 0;       // nodes of the range with out-degree >= 1
   // Segments (graphs whose ids carry locality): light tasks are grouped by
   // node segment v >> seg_shift (degree order within a segment), and
   // [seg_min[s], seg_max[s]] bounds the successors and nodes of segment s,
@@ -57,11 +58,8 @@ struct TaskBuild {
   // slots [0, num_chunks))
   std::vector<uint64_t> group_task_begin;
   std::vector<uint32_t> group_seg;
-  // deferred TOS fill (build_tasks_device(..., defer_fill)): kept until
-  // finish_tasks_device
-  uint64_t* chunk_begin = nullptr;
+  uint64_t* chunk_begin = nullptr;  // (build scratch)
   int* fill_bad = nullptr;
-  uint64_t* row_slot = nullptr;  // scatter fill: per row (v - lo), TOS offset | lane info
 };
 // The CSR as the task build reads it: node (row) v's successors are arcs
 // [begin(v), end(v)) of `succ` (from index succ_base), each mapped through
