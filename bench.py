@@ -406,6 +406,33 @@ def single_gpu_config2(dev, steps, warmup, flush, peak):
                          "note": "42 MB counter array: L2-resident, bound by L1 wavefronts"}}
 
 
+def shared_graph(config: int, local_rank: int, backend: str):
+    """N>1: the node's local rank 0 generates the graph once (on its GPU
+    for R-MAT) and writes the CSR to /dev/shm; every rank of the node maps
+    the same pages (one copy of the 19 GB config-5 CSR in host RAM instead
+    of one per rank)."""
+    import numpy as np
+    import torch.distributed as dist
+    import paper_1011_5599_b200 as hanf
+    tag = os.environ.get("TORCHELASTIC_RUN_ID", os.environ.get("MASTER_PORT", "0"))
+    base = f"/dev/shm/hanf_bench_{tag}_c{config}"
+    if local_rank == 0:
+        g = make_graph(config, device=0 if CONFIGS[config]["kind"] == "rmat" and backend == "nccl"
+                       else None)
+        np.save(base + "_off.npy", g.offsets())
+        np.save(base + "_succ.npy", g.arcs())
+        del g
+    dist.barrier()
+    off = np.load(base + "_off.npy", mmap_mode="r+")
+    succ = np.load(base + "_succ.npy", mmap_mode="r+")
+    g = hanf.Graph(len(off) - 1, off, succ)
+    dist.barrier()
+    if local_rank == 0:  # (the mappings stay valid)
+        for f in (base + "_off.npy", base + "_succ.npy"):
+            os.unlink(f)
+    return g
+
+
 def write_graph(args):
     """--write-graph DIR: the package generator's CSR as .npy (the reference
     arm's child process for configs without an oracle generator)."""
@@ -465,7 +492,10 @@ def main():
     cfgd = CONFIGS[args.config]
     b = cfgd["b"]
     t_gen = time.perf_counter()
-    g = make_graph(args.config, device=local_rank if cfgd["kind"] == "rmat" else None)
+    if world > 1:
+        g = shared_graph(args.config, local_rank, backend)
+    else:
+        g = make_graph(args.config, device=local_rank if cfgd["kind"] == "rmat" else None)
     t_gen = time.perf_counter() - t_gen
     n, a = g.num_nodes(), g.num_arcs()
     cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank, exact_sum=False)
@@ -529,7 +559,10 @@ def main():
     # host CSR (pinned in place with Graph.pin(), hanf_pin_host)
     e2e = None
     if not args.no_e2e:
-        g.pin()
+        try:
+            g.pin()
+        except Exception:  # (shared mappings may refuse page-locking: pageable upload)
+            pass
         e2e_cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank)
         runs = max(1, min(args.steps, 3 if n > (1 << 24) else 5))
         iters, wall = 0, 0.0
