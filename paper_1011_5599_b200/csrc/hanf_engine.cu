@@ -529,7 +529,7 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   // single-GPU steps: the bitmap the next step writes (this step's mod_cur,
   // dead once the sweep has run) is cleared in the same pass.  Shards keep
   // their memset: peers publish into those words during their next step.
-  const bool sharded = e->lo != 0 || e->hi != e->n || !e->parts.empty();
+  const bool sharded = e->lo != 0 || e->hi != e->n;
   if (in_step && !sharded && e->batch == 1) f.clear = e->mod[e->cur];
   if (in_step && e->timing) HANF_CUDA(cudaEventRecord(e->ev[2], e->stream));
   HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
@@ -2134,7 +2134,7 @@ hanf_status hanf_run_to_stabilisation(hanf_engine* e, double* values, uint64_t* 
   std::vector<uint64_t> mods;
   vals.push_back(e->last_sum);
   mods.push_back(e->n);
-  const bool sharded = e->lo != 0 || e->hi != e->n;
+  const bool sharded = e->lo != 0 || e->hi != e->n || !e->parts.empty();
   if (e->cfg.termination == 0 && !e->timing && !sharded) {
     // Pipelined: once a step's modified count is known, the next step is
     // launched before the host sums this step's block sums (exact_sum) -
