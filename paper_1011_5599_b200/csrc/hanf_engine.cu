@@ -2099,7 +2099,10 @@ hanf_status hanf_create_multi(const hanf_graph_view* g, const hanf_config* cfg,
     const hanf_status st = hanf_shard_attach_local(m->parts[k], m->parts.data(), count, k);
     if (st != HANF_OK) return st;
   }
-  m->cfg = *cfg;
+  m->cfg = m->parts[0]->cfg;  // (normalised: max_iterations 0 -> n + 1, ...)
+  m->cfg.device = devices[0];
+  m->cfg.shard_begin = m->cfg.shard_end = 0;
+  m->cfg.shard_count = 0;
   m->params = m->parts[0]->params;
   m->n = n;
   m->lo = 0;
