@@ -279,7 +279,8 @@ typedef struct {
   uint64_t n, row_pitch;
   uint64_t shard_begin, shard_end;
   int32_t device;
-  int32_t relabelled;      /* relabelled shards (hanf_config.shard_count): all or none */
+  int32_t relabelled;      /* bit 0: relabelled shards (hanf_config.shard_count), all or
+                              none; bit 1: byte-layout counter rows (all or none) */
 } hanf_shard_peer;
 #define HANF_MAX_PEERS 7
 /* Describes this shard engine's arena for the other ranks. */

@@ -40,6 +40,7 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
 // Register layout of one chunk: NREG registers of R bits.
 template <int R, int NREG>
 struct Layout {
+  static constexpr bool kBytes = false;
   static constexpr int kR = R;
   static constexpr int kNReg = NREG;
   static constexpr int kBits = NREG * R;
@@ -70,6 +71,54 @@ struct Layout {
     return e;
   }
 };
+
+// Byte layout (the engine's default counter store for r = 5): register j of
+// a counter is byte j of its row, value in the low 5 bits.  A row of M
+// registers is M bytes, 16-byte aligned (M >= 16), so a quad of lanes reads
+// a 64-register counter as one coalesced 64-byte access and the register-
+// wise max is three instructions per four registers (byte_max).  Every
+// exchange with the caller (read-back, snapshots, restore) converts to or
+// from the reference packing (hll.hpp:183-240), so the bits a caller sees
+// are the reference's.
+template <int M>
+struct ByteLayout {
+  static constexpr bool kBytes = true;
+  static constexpr int kR = 5;
+  static constexpr int kNReg = M;
+  static constexpr int kLimbs = M / 4;  // four registers per 32-bit limb
+  static constexpr int kWords = M / 8;
+};
+
+// Byte-wise max of four registers (each < 128): bit 7 of byte k of
+// x + 0x80 - y is set iff x_k >= y_k (no borrow leaves a byte), PRMT's
+// sign-replicate selector turns it into a whole-byte mask, one LOP3
+// selects.  This is PackedMax::max_into (broadword.hpp:94-130) on
+// byte-aligned lanes, where no register straddles a limb.
+__device__ __forceinline__ uint32_t byte_max(uint32_t x, uint32_t y) {
+  const uint32_t d = x + 0x80808080u - y;
+  uint32_t m;  // 0xff where x_k >= y_k (PRMT selector nibble 8 + k: byte k, sign-replicated)
+  asm("prmt.b32 %0, %1, 0, 0xba98;" : "=r"(m) : "r"(d));
+  return lop3<0xE4>(x, y, m);  // m ? x : y
+}
+
+__device__ __forceinline__ uint4 byte_max4(const uint4& x, const uint4& y) {
+  return make_uint4(byte_max(x.x, y.x), byte_max(x.y, y.y), byte_max(x.z, y.z),
+                    byte_max(x.w, y.w));
+}
+
+// sum of 2^(31 - M_j) over the 16 byte registers of v (M_j <= 31) and the
+// number of zero registers: the r = 5 estimator's exact integer terms
+__device__ __forceinline__ void byte_terms(const uint4& v, uint64_t& s, uint32_t& zeros) {
+  const uint32_t l[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t term = 0x80000000u >> ((l[i] >> (8 * b)) & 31u);
+      s += term;
+      zeros += term >> 31;
+    }
+}
 
 // d[S..S+N) = a[S..S+N) - b[S..S+N) as one multi-precision number (borrow
 // chain in the carry flag).  One asm statement per chain so nothing can
@@ -193,7 +242,14 @@ __device__ __forceinline__ void swar_chain(uint32_t (&x)[Lay::kLimbs],
 template <class Lay>
 __device__ __forceinline__ void swar_max(uint32_t (&x)[Lay::kLimbs],
                                          const uint32_t (&y)[Lay::kLimbs]) {
-  swar_chain<Lay, 0>(x, y);
+  if constexpr (Lay::kBytes) {
+    sfor<0, Lay::kLimbs>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      x[i] = byte_max(x[i], y[i]);
+    });
+  } else {
+    swar_chain<Lay, 0>(x, y);
+  }
 }
 
 // Counter loads with a cache policy: 0 = read-only path (L1 allocating, a
@@ -435,6 +491,16 @@ __device__ inline double estimate_counter_generic(const uint64_t* c, const Estim
   return finish_estimate(p, harmonic, zeros);
 }
 
+// Byte layout: M registers as M bytes at c (16-byte aligned).
+template <int M>
+__device__ __forceinline__ double estimate_counter_bytes(const uint64_t* c, const EstimateParams& p) {
+  uint64_t s = 0;
+  uint32_t zeros = 0;
+  const uint4* q = reinterpret_cast<const uint4*>(c);
+  sfor<0, M / 16>([&](auto I) { byte_terms(q[decltype(I)::value], s, zeros); });
+  return finish_estimate(p, __dmul_rn(static_cast<double>(s), 0x1p-31), zeros);
+}
+
 // Fast path for r = 5 with a compile-time register count: the counter is
 // read as 32-bit limbs and every register is extracted with one funnel
 // shift; 2^(31-M) is one wrapping funnel shift of 0x80000000.
@@ -525,6 +591,15 @@ __device__ __forceinline__ void window128_extract(uint32_t (&x)[Lay::kLimbs],
 template <class Lay>
 __device__ __forceinline__ double estimate_limbs(const uint32_t (&x)[Lay::kLimbs],
                                                  const EstimateParams& p) {
+  if constexpr (Lay::kBytes) {
+    uint64_t s = 0;
+    uint32_t zeros = 0;
+    sfor<0, Lay::kLimbs / 4>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      byte_terms(make_uint4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]), s, zeros);
+    });
+    return finish_estimate(p, __dmul_rn(static_cast<double>(s), 0x1p-31), zeros);
+  }
   constexpr int R = Lay::kR;
   constexpr int NL = Lay::kLimbs;
   auto limb = [&](int i) -> uint32_t { return i < NL ? x[i] : 0u; };

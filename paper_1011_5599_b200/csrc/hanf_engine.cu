@@ -205,6 +205,7 @@ struct hanf_engine {
   uint64_t blocks = 0;       // ceil(n / 64)
   uint64_t words = 0;        // W
   uint64_t pitch = 0;        // row pitch in words (hanf::row_pitch)
+  bool bytes = false;        // byte-layout counter store (hanf_device.cuh ByteLayout)
   int device = 0;
   cudaStream_t stream = nullptr;
 
@@ -475,6 +476,7 @@ uint64_t* dirty_of(const hanf_engine* e, int g) { return e->dirty[g] ? e->dirty[
 hanf_status run_estimates(hanf_engine* e, int g, const uint64_t* dirty, uint64_t b0, uint64_t b1) {
   hanf::EstimateArgs a{};
   a.counters = e->cnt[g];
+  a.bytes = e->bytes ? 1 : 0;
   a.dirty = dirty;
   a.est = e->est;
   a.block_sums = e->block_sums;
@@ -610,8 +612,8 @@ hanf_status seed_all(hanf_engine* e) {
   HANF_CUDA(hanf::launch_seed(e->cnt[0], e->cnt[1], e->mod[0], e->n, 0, e->n,
                               e->params.bucket_bits, e->params.register_bits,
                               e->params.words_per_counter, static_cast<uint32_t>(e->pitch),
-                              e->params.seed, e->order, e->batch, e->batch_mix, e->stream,
-                              &e->launches));
+                              e->params.seed, e->order, e->batch, e->batch_mix, e->bytes,
+                              e->stream, &e->launches));
   HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, e->stream));
   e->next_bits_clear = true;
   if (e->dirty[0]) {  // every counter was seeded: all ones in both id spaces
@@ -765,6 +767,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.est_index = e->est_rows ? nullptr : e->order;
   a.dirty_next = e->dirty[ng];
   a.peers = peer_rows(e, ng);
+  a.bytes = e->bytes ? 1 : 0;
   return a;
 }
 
@@ -802,6 +805,7 @@ hanf_status compute_sparse(hanf_engine* e) {
   a.blocks = e->blocks;
   a.hi = e->hi;
   a.peers = peer_rows(e, ng);
+  a.bytes = e->bytes ? 1 : 0;
   HANF_CUDA(hanf::launch_sparse_step(a, w0, w1, e->params.register_bits, e->params.registers,
                                      e->stream, &e->launches));
   if (e->tasks.num_chunks) {
@@ -1123,7 +1127,21 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   e->hi = hi;
   e->blocks = (n + 63) / 64;
   e->words = params.words_per_counter;
-  e->pitch = hanf::row_pitch(params.register_bits, params.registers, params.words_per_counter);
+  // Counter store.  Byte registers (hanf_device.cuh ByteLayout: one coalesced
+  // access and 3 instructions per 4 registers per gathered counter) when a
+  // generation of byte rows stays L2-resident; DRAM-resident arrays keep
+  // the reference packing, whose 1.6x smaller footprint wins there (config
+  // 2: 0.139 vs 0.177 ms per union sweep; configs 3/4/5: 7.08/13.5/66.5 vs
+  // 5.92/12.97/58.8 ms, profiles/r02_byte_layout.md).  HANF_LAYOUT=bytes or
+  // packed forces either; both give the same bits.
+  const bool bytes_ok = hanf::byte_layout_supported(params.register_bits, params.registers);
+  e->bytes = bytes_ok && (n + 1) * params.registers <= (96ull << 20);
+  if (const char* ly = std::getenv("HANF_LAYOUT")) {
+    if (std::strcmp(ly, "packed") == 0) e->bytes = false;
+    if (std::strcmp(ly, "bytes") == 0) e->bytes = bytes_ok;
+  }
+  e->pitch = hanf::row_pitch(params.register_bits, params.registers, params.words_per_counter,
+                             e->bytes);
   if (const char* fs = std::getenv("HANF_SUMMARY")) e->force_summary = fs[0] == '1';
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
@@ -1162,7 +1180,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     if (rl && (rl[0] == '0' || rl[0] == '1'))
       e->relabel = rl[0] == '1';
     else
-      e->relabel = (n + 1) * e->pitch * 8 > (64ull << 20) && !ids_local(g);
+      e->relabel = (n + 1) * e->words * 8 > (64ull << 20) && !ids_local(g);
     e->est_rows = e->relabel;
     if (shard_cfg && e->relabel) {
       // estimates stay in row order and are pushed to the peers with their
@@ -1399,7 +1417,8 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       // renumber rows by out-degree (offsets only: overlaps the arcs upload)
       hanf::RelabelOut r;
       const cudaError_t re = hanf::relabel_order_device(
-          d_off, n, e->shard_relabel ? cfg.shard_count : 1, s, &r, &e->launches);
+          d_off, n, e->shard_relabel ? cfg.shard_count : 1, static_cast<uint32_t>(e->pitch), s, &r,
+          &e->launches);
       e->order = r.order;
       e->perm = r.perm;
       e->rl_off = r.off;
@@ -1614,7 +1633,8 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
                                    cudaMemcpyHostToDevice, s);
   for (int g = 0; g < 2 && ce == cudaSuccess; ++g)  // both generations (next == cur)
     ce = hanf::launch_scatter_rows(tmp, e->perm, n, static_cast<uint32_t>(e->pitch),
-                                   static_cast<uint32_t>(e->words), e->cnt[g], s, &e->launches);
+                                   static_cast<uint32_t>(e->words), e->cnt[g], e->bytes,
+                                   e->params.registers, s, &e->launches);
   cudaFreeAsync(tmp, s);
   HANF_CUDA(ce);
   // every counter counts as modified: the next step recomputes every node
@@ -1788,7 +1808,7 @@ hanf_status hanf_shard_export(hanf_engine* e, hanf_shard_peer* out) {
   out->shard_begin = e->lo;
   out->shard_end = e->hi;
   out->device = e->device;
-  out->relabelled = e->shard_relabel ? 1 : 0;
+  out->relabelled = (e->shard_relabel ? 1 : 0) | (e->bytes ? 2 : 0);
   out->arena_bytes = e->arena_bytes;
   if (!e->arena) return HANF_OK;  // a one-shard engine (all nodes): nothing to map
   HANF_CUDA(cudaSetDevice(e->device));
@@ -1809,7 +1829,8 @@ hanf_status check_peers(const hanf_engine* e, const hanf_shard_peer* peers, uint
     return fail(HANF_INVALID_ARGUMENT, "peer-push exchange: at most 8 shards");
   const hanf_shard_peer& me = peers[self];
   if (me.n != e->n || me.shard_begin != e->lo || me.shard_end != e->hi ||
-      me.arena_bytes != e->arena_bytes || me.relabelled != (e->shard_relabel ? 1 : 0))
+      me.arena_bytes != e->arena_bytes ||
+      me.relabelled != ((e->shard_relabel ? 1 : 0) | (e->bytes ? 2 : 0)))
     return fail(HANF_INVALID_ARGUMENT, "peers[self] does not describe this engine");
   std::vector<std::pair<uint64_t, uint64_t>> ranges;
   for (uint32_t p = 0; p < count; ++p) {
@@ -1873,7 +1894,7 @@ hanf_status hanf_shard_attach_local(hanf_engine* e, hanf_engine* const* peers, u
     desc[p].shard_end = peers[p]->hi;
     desc[p].arena_bytes = peers[p]->arena_bytes;
     desc[p].device = peers[p]->device;
-    desc[p].relabelled = peers[p]->shard_relabel ? 1 : 0;
+    desc[p].relabelled = (peers[p]->shard_relabel ? 1 : 0) | (peers[p]->bytes ? 2 : 0);
   }
   hanf_status st = check_peers(e, desc.data(), count, self);
   if (st != HANF_OK) return st;
@@ -2229,14 +2250,15 @@ hanf_status hanf_read_counters(hanf_engine* e, uint64_t first, uint64_t count, u
   if (count == 0) return HANF_OK;
   if (!dst) return fail(HANF_INVALID_ARGUMENT, "null destination");
   HANF_CUDA(cudaSetDevice(e->device));
-  if (e->relabel) {
-    // counter of original id first + i lives in row perm[first + i]
+  if (e->relabel || e->bytes) {
+    // counter of original id first + i lives in row perm[first + i]; byte
+    // rows are packed into the reference layout on the way
     uint64_t* tmp = nullptr;
     HANF_CUDA(palloc(&tmp, count * e->words, e->stream));
     cudaError_t ce = hanf::launch_gather_rows(e->cnt[e->cur], e->perm, first, count,
                                               static_cast<uint32_t>(e->pitch),
-                                              static_cast<uint32_t>(e->words), tmp, e->stream,
-                                              &e->launches);
+                                              static_cast<uint32_t>(e->words), tmp, e->bytes,
+                                              e->params.registers, e->stream, &e->launches);
     if (ce == cudaSuccess)
       ce = cudaMemcpyAsync(dst, tmp, sizeof(uint64_t) * count * e->words, cudaMemcpyDeviceToHost,
                            e->stream);

@@ -104,9 +104,11 @@ struct RelabelOut {
 };
 // ways > 1 (relabelled shards, n a multiple of 64 * ways): degree rank i
 // goes to row (i mod ways) * n/ways + i / ways, so every shard's rows get
-// the same degree profile with its hot rows first.
-cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t ways, cudaStream_t s,
-                                 RelabelOut* out, uint64_t* launches);
+// the same degree profile with its hot rows first.  Rows of an odd pitch
+// (< 16 words) past a hot prefix are assigned line-aligned slots first
+// (the coldest ranks take the rows that straddle a 128-byte line).
+cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t ways, uint32_t pitch,
+                                 cudaStream_t s, RelabelOut* out, uint64_t* launches);
 // The relabelled arcs (only the worklist step's transpose needs them; the
 // union sweep's TOS is filled through CsrView).  *bad = arc endpoint >= n.
 cudaError_t relabel_arcs_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n,
@@ -117,12 +119,14 @@ cudaError_t relabel_arcs_device(const uint64_t* d_off, const uint32_t* d_succ, u
 cudaError_t launch_seed_bitmap(uint64_t* bits, uint64_t n, cudaStream_t s);
 cudaError_t launch_summary(const uint64_t* bits, uint64_t words, uint32_t shift, uint64_t summ_bits,
                            uint64_t* summ, cudaStream_t s, uint64_t* launches);
+// (bytes: the device rows are byte registers, `registers` of them; the
+// dense rows on the other side keep the reference packing, r = 5)
 cudaError_t launch_scatter_rows(const uint64_t* src, const uint32_t* perm, uint64_t count,
-                                uint32_t pitch, uint32_t words, uint64_t* counters,
-                                cudaStream_t s, uint64_t* launches);
+                                uint32_t pitch, uint32_t words, uint64_t* counters, bool bytes,
+                                uint32_t registers, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_gather_rows(const uint64_t* counters, const uint32_t* perm, uint64_t first,
                                uint64_t count, uint32_t pitch, uint32_t words, uint64_t* dst,
-                               cudaStream_t s, uint64_t* launches);
+                               bool bytes, uint32_t registers, cudaStream_t s, uint64_t* launches);
 
 // Worklist ("systolic") step, hanf_sparse.cu.
 struct SparseArgs {
@@ -153,6 +157,7 @@ struct SparseArgs {
   const uint32_t* hub_count;
   uint64_t n, blocks, hi;
   PeerRows peers;             // sharded peer-push: also store written rows there
+  uint32_t bytes;             // byte-layout counter store
 };
 // Changed-rows exchange of sharded steps (hanf_sparse.cu): the rows of
 // [lo, hi) the step wrote (mod_next | mod_cur) packed as (ids, rows), and
@@ -211,6 +216,7 @@ struct UnionArgs {
   PeerRows peers;                  // sharded peer-push: also store written rows there
   const uint32_t* seg_live;        // skip sweeps over segmented tasks: segment s has work
   uint32_t seg_shift;              // (TaskBuild::seg_shift)
+  uint32_t bytes;                  // byte-layout counter store (ByteLayout)
 };
 
 struct EstimateArgs {
@@ -229,6 +235,7 @@ struct EstimateArgs {
   uint32_t pitch;            // row pitch in u64 words
   const double* log_table;
   const uint32_t* row_of;    // original id -> row (nullptr: identity labels)
+  uint32_t bytes;            // byte-layout counter store
 };
 
 // Launchers (hanf_kernels.cu).  All are stream-ordered and asynchronous.
@@ -236,7 +243,7 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
                         uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
                         const uint32_t* orig_of, uint32_t batch, const uint64_t* batch_mix,
-                        cudaStream_t s, uint64_t* launches);
+                        bool bytes, cudaStream_t s, uint64_t* launches);
 // Batched runs (hanf_batch.cu): the K-fold lifted CSR (row v*K + k), and
 // the per-run block sums / modified counts of a generation.
 cudaError_t lift_graph_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n, uint64_t arcs,
@@ -252,8 +259,11 @@ cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* 
 bool fused_estimates(uint32_t register_bits, uint32_t registers);
 // Row pitch of the counter arrays (u64 words between counters): W, except
 // W = 3 which is padded to one aligned 32-byte sector
-// (profiles/r01_row_pitch.md).
-uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words);
+// (profiles/r01_row_pitch.md); m / 8 in the byte layout.
+uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words, bool bytes);
+// The byte layout serves r = 5 with 16 <= m <= 128 (one to eight lanes per
+// row); other layouts keep the reference packing on the device too.
+bool byte_layout_supported(uint32_t register_bits, uint32_t registers);
 
 // Step epilogue (block sums + totals), see finish_kernel.
 constexpr int kFinishThreads = 256;  // threads per CTA

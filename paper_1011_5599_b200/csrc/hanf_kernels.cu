@@ -37,7 +37,7 @@ __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
                             uint64_t node_end, uint32_t bucket_bits, uint32_t register_bits,
                             uint32_t words, uint32_t pitch, uint64_t seed_mix,
                             const uint32_t* __restrict__ orig_of, uint32_t batch,
-                            const uint64_t* __restrict__ batch_mix) {
+                            const uint64_t* __restrict__ batch_mix, bool bytes) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = node_begin + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
        v < node_end; v += stride) {
@@ -60,6 +60,14 @@ __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
     const uint32_t off = bit & 63;
     uint64_t* ca = a + v * pitch;
     uint64_t* cb = b + v * pitch;
+    if (bytes) {  // byte layout: register `bucket` is byte `bucket` of the row
+      for (uint32_t k = 0; k < pitch; ++k) {
+        const uint64_t word = k == bucket / 8 ? static_cast<uint64_t>(rho) << (8 * (bucket % 8)) : 0;
+        ca[k] = word;
+        cb[k] = word;
+      }
+      continue;
+    }
     for (uint32_t k = 0; k < pitch; ++k) {  // padding words beyond W stay 0
       uint64_t word = 0;
       if (k == wi) word |= static_cast<uint64_t>(rho) << off;
@@ -84,7 +92,7 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,
                         uint32_t register_bits, uint32_t words, uint32_t pitch, uint64_t seed,
                         const uint32_t* orig_of, uint32_t batch, const uint64_t* batch_mix,
-                        cudaStream_t s, uint64_t* launches) {
+                        bool bytes, cudaStream_t s, uint64_t* launches) {
   if (node_end <= node_begin) return cudaSuccess;
   const uint64_t items = node_end - node_begin;
   const uint32_t threads = 256;
@@ -92,7 +100,7 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
   if (blocks > 148ull * 64) blocks = 148ull * 64;
   seed_kernel<<<static_cast<uint32_t>(blocks), threads, 0, s>>>(
       a, b, mod, n, node_begin, node_end, bucket_bits, register_bits, words, pitch,
-      mix64(seed ^ 0x9e3779b97f4a7c15ULL), orig_of, batch, batch_mix);
+      mix64(seed ^ 0x9e3779b97f4a7c15ULL), orig_of, batch, batch_mix, bytes);
   ++*launches;
   return cudaGetLastError();
 }
@@ -427,6 +435,184 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
   task_finish<Lay, kVec16>(args, task, hub, v, any_changed, lane);
 }
 
+// ---------------------------------------------------------------------------
+// Union sweep over the byte layout (ByteLayout<M>).  Same tasks and TOS as
+// union_task: TOS row i holds the ids of trip i of the warp's 32 streams
+// (stream l: node slot l >> lg, sub-stream l & (G-1)).  A counter row is M
+// bytes, read by a group of Q = M/16 lanes (16 registers each, one 16-byte
+// load), so a gathered counter costs one coalesced M-byte access and three
+// instructions per four registers per lane.  Group g walks the streams
+// [gQ, gQ + Q) one after the other with a single accumulator: streams of a
+// node are consecutive, so a node of G < Q streams is committed every G
+// streams, and a node of G >= Q streams is combined across its G/Q groups
+// by a butterfly at the end.  The node's group then compares with the old
+// counter, writes a changed or stale row (one coalesced store), sums the
+// estimator's integer terms of its registers and sets the modified bit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 shfl_xor4(const uint4& v, int off) {
+  return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, off), __shfl_xor_sync(0xffffffffu, v.y, off),
+                    __shfl_xor_sync(0xffffffffu, v.z, off), __shfl_xor_sync(0xffffffffu, v.w, off));
+}
+
+template <int Q>
+__device__ __forceinline__ uint32_t group_or(uint32_t x) {
+#pragma unroll
+  for (int off = 1; off < Q; off <<= 1) x |= __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
+}
+
+// Group commit of light node slot j (warp-synchronous: every lane calls it;
+// `act` is uniform within a group).
+template <int Q>
+__device__ __forceinline__ void commit_bytes(const UnionArgs& args, const WarpTask& task, uint32_t j,
+                                             bool act, bool live, const uint4& acc, uint32_t k) {
+  const uint4* __restrict__ cur = reinterpret_cast<const uint4*>(args.cur);
+  act = act && j < task.nodes;
+  uint32_t v = args.zero_row;
+  bool st = false;
+  if (act) {
+    v = args.order[task.item + j];
+    if (args.stale_valid) st = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
+  }
+  const bool nz = group_or<Q>(live && (acc.x | acc.y | acc.z | acc.w) != 0);
+  const bool need = act && (st || nz);
+  uint4 own = make_uint4(0, 0, 0, 0);
+  if (need) own = __ldg(cur + static_cast<uint64_t>(v) * Q + k);
+  const uint4 nx = byte_max4(acc, own);
+  const bool changed =
+      group_or<Q>(need && ((nx.x ^ own.x) | (nx.y ^ own.y) | (nx.z ^ own.z) | (nx.w ^ own.w)));
+  if (changed || (act && st)) {
+    const uint64_t off = static_cast<uint64_t>(v) * Q + k;
+    reinterpret_cast<uint4*>(args.next)[off] = nx;
+    for (uint32_t p = 0; p < args.peers.count; ++p)
+      reinterpret_cast<uint4*>(args.peers.next[p])[off] = nx;
+  }
+  if (args.est) {
+    const bool want = changed || (act && st && args.peers.push_est);
+    if (__any_sync(0xffffffffu, want)) {
+      uint64_t sum = 0;
+      uint32_t zeros = 0;
+      byte_terms(nx, sum, zeros);
+#pragma unroll
+      for (int o = 1; o < Q; o <<= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
+      }
+      if (want && k == 0)
+        push_estimate(args, v,
+                      finish_estimate(args.ep, __dmul_rn(static_cast<double>(sum), 0x1p-31), zeros));
+    }
+  }
+  if (changed && k == 0) mark_changed(args.mod_next, args.dirty_next, args.orig_of, v);
+}
+
+template <int M, int U, bool SKIP>
+__device__ __forceinline__ void union_task_bytes(const UnionArgs& args, uint32_t task_index,
+                                                 uint32_t lane, const uint64_t* summ) {
+  using Lay = ByteLayout<M>;
+  constexpr int Q = M / 16;  // lanes per counter row
+  const WarpTask task = args.wtasks[task_index];
+  const bool hub = task.nodes == 0;
+  if constexpr (SKIP) {
+    if (args.seg_live) {
+      const uint32_t v0 = hub ? args.hub_node[task.item] : args.order[task.item];
+      if (!args.seg_live[v0 >> args.seg_shift]) return;
+    }
+  }
+  const uint32_t lg = hub ? 5u : task.lg;
+  const uint32_t G = 1u << lg;
+  const uint32_t zero_row = args.zero_row;
+  const uint32_t grp = lane / Q, k = lane % Q;
+  const uint4* __restrict__ cur = reinterpret_cast<const uint4*>(args.cur);
+  const uint32_t trips = task.trips;
+  bool task_live = !SKIP;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+  for (uint32_t s = 0; s < static_cast<uint32_t>(Q); ++s) {
+    const uint32_t* __restrict__ ids = args.tos + task.tos + grp * Q + s;
+#pragma unroll 1
+    for (uint32_t i = 0; i < trips; i += U) {
+      uint32_t w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = i + u < trips ? __ldg(ids + 32 * (i + u)) : zero_row;
+      if constexpr (SKIP) {
+        bool live = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          bool keep = true;
+          if (summ)
+            keep = (summ[w[u] >> (args.summ_shift + 6)] >> ((w[u] >> args.summ_shift) & 63)) & 1;
+          if (keep) keep = (__ldg(args.mod_cur + (w[u] >> 6)) >> (w[u] & 63)) & 1;
+          if (!keep) w[u] = zero_row;
+          live |= w[u] != zero_row;
+        }
+        if (!__any_sync(0xffffffffu, live)) continue;
+        task_live = true;
+      }
+      uint4 y[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) y[u] = __ldg(cur + static_cast<uint64_t>(w[u]) * Q + k);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = byte_max4(acc, y[u]);
+    }
+    // a node of G < Q streams ends with stream grp*Q + s
+    if (G < static_cast<uint32_t>(Q) && ((s + 1) & (G - 1)) == 0) {
+      const uint32_t first = grp * Q + s + 1 - G;
+      commit_bytes<Q>(args, task, first >> lg, true, task_live, acc, k);
+      acc = make_uint4(0, 0, 0, 0);
+    }
+  }
+  if (G < static_cast<uint32_t>(Q)) return;
+  // nodes of G >= Q streams: combine the G/Q groups of each node
+  if (task_live)
+    for (uint32_t off = 1; off < G / Q; off <<= 1) acc = byte_max4(acc, shfl_xor4(acc, off * Q));
+  if (!hub) {
+    commit_bytes<Q>(args, task, (grp * Q) >> lg, ((grp * Q) & (G - 1)) == 0, task_live, acc, k);
+    return;
+  }
+  // hub chunk: the partial maximum (every group holds it), then the ticket
+  if (grp == 0)
+    reinterpret_cast<uint4*>(args.partials)[static_cast<uint64_t>(task.item) * Q + k] = acc;
+  const uint32_t h = args.chunk_hub[task.item];
+  uint32_t last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(args.hub_ticket + h, 1u) == args.hub_count[h] - 1;
+  }
+  if (__shfl_sync(0xffffffffu, last, 0)) {
+    __threadfence();
+    finalize_hub<Lay, true>(args, h, lane);
+    if (lane == 0) args.hub_ticket[h] = 0;
+  }
+}
+
+template <int M, int MINB, bool SKIP>
+__global__ void __launch_bounds__(256, MINB) union_kernel_bytes(const UnionArgs args) {
+  extern __shared__ uint64_t summ_smem[];
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t* summ = nullptr;
+  if (SKIP && args.summ) {
+    for (uint32_t i = threadIdx.x; i < args.summ_words; i += blockDim.x) summ_smem[i] = args.summ[i];
+    __syncthreads();
+    summ = summ_smem;
+  }
+  if (args.task_list) {
+    const uint32_t count = *args.task_count;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = gw; i < count; i += nw)
+      union_task_bytes<M, 4, SKIP>(args, args.task_list[i], lane, summ);
+    return;
+  }
+  if (SKIP && summ) {
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = gw; t < args.num_wtasks; t += nw) union_task_bytes<M, 4, SKIP>(args, t, lane, summ);
+    return;
+  }
+  if (gw >= args.num_wtasks) return;
+  union_task_bytes<M, 4, SKIP>(args, gw, lane, summ);
+}
+
 // One warp per task; with a task list (the worklist step's hub chunks) the
 // warps stride over the listed task indices instead.
 template <int R, int NREG, int U, int GMODE, bool kVec16, int MINB = 1, bool PF = false,
@@ -478,6 +664,21 @@ KernelChoice choose(uint32_t r, uint32_t m) {
   }
 }
 
+template <int M, int MINB>
+cudaError_t union_launch_bytes(UnionArgs a, cudaStream_t s) {
+  a.chunks = 1;
+  if (a.num_wtasks == 0) return cudaSuccess;
+  uint32_t blocks = (a.num_wtasks + 7) / 8;
+  if (a.task_list && blocks > 148 * 4) blocks = 148 * 4;
+  if (a.summ && blocks > 148 * 4) blocks = 148 * 4;  // persistent (mode 3)
+  const size_t smem = a.summ ? sizeof(uint64_t) * a.summ_words : 0;
+  if (a.check_mod)
+    union_kernel_bytes<M, (MINB > 4 ? 4 : MINB), true><<<blocks, 256, smem, s>>>(a);
+  else
+    union_kernel_bytes<M, MINB, false><<<blocks, 256, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <int R, int NREG, int U, int GM, bool V, int MINB = 1, bool PF = false>
 cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   a.chunks = chunks;
@@ -502,10 +703,15 @@ bool fused_estimates(uint32_t register_bits, uint32_t registers) {
   return choose(register_bits, registers).chunks == 1;
 }
 
+bool byte_layout_supported(uint32_t register_bits, uint32_t registers) {
+  return register_bits == 5 && registers >= 16 && registers <= 128;
+}
+
 // Rows of W = 3 words are padded to 4 (one aligned 32-byte sector per
 // counter: +5% on the DRAM-bound BA graph, profiles/r01_row_pitch.md);
 // every other layout keeps the reference's dense packing.
-uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words) {
+uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words, bool bytes) {
+  if (bytes) return registers / 8;
   if (choose(register_bits, registers).chunks != 1) return words;
   return words == 3 ? 4 : words;
 }
@@ -519,6 +725,13 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
   const KernelChoice k = choose(register_bits, registers);
   if (args.num_wtasks == 0) return cudaSuccess;
   ++*launches;
+  if (args.bytes) switch (registers) {
+      case 16: return union_launch_bytes<16, 5>(args, s);
+      case 32: return union_launch_bytes<32, 5>(args, s);
+      case 64: return union_launch_bytes<64, 5>(args, s);
+      case 128: return union_launch_bytes<128, 3>(args, s);
+      default: return cudaErrorInvalidValue;
+    }
   const uint32_t ch = static_cast<uint32_t>(k.chunks);
   const bool single = ch == 1;
   if (single && args.pitch % 4 == 0) switch (k.r * 1000 + k.nreg) {
@@ -569,7 +782,9 @@ __global__ void __launch_bounds__(64) estimate_kernel(const EstimateArgs args) {
   if (v < args.n) {
     if ((word >> t) & 1) {
       const uint64_t row = args.row_of ? args.row_of[v] : v;  // v is an original id
-      if constexpr (M > 0)
+      if constexpr (M < 0)
+        e = estimate_counter_bytes<-M>(args.counters + row * args.pitch, p);
+      else if constexpr (M > 0)
         e = estimate_counter_r5<M>(args.counters + row * args.pitch, p);
       else
         e = estimate_counter_generic(args.counters + row * args.pitch, p);
@@ -594,6 +809,15 @@ cudaError_t launch_estimate(const EstimateArgs& args, cudaStream_t s, uint64_t* 
   if (args.block_end <= args.block_begin) return cudaSuccess;
   const uint64_t blocks = args.block_end - args.block_begin;
   ++*launches;
+  if (args.bytes) {
+    switch (args.registers) {
+      case 16: estimate_kernel<-16><<<static_cast<uint32_t>(blocks), 64, 0, s>>>(args); break;
+      case 32: estimate_kernel<-32><<<static_cast<uint32_t>(blocks), 64, 0, s>>>(args); break;
+      case 64: estimate_kernel<-64><<<static_cast<uint32_t>(blocks), 64, 0, s>>>(args); break;
+      default: estimate_kernel<-128><<<static_cast<uint32_t>(blocks), 64, 0, s>>>(args); break;
+    }
+    return cudaGetLastError();
+  }
   if (args.register_bits == 5 && args.registers == 32)
     estimate_kernel<32><<<static_cast<uint32_t>(blocks), 64, 0, s>>>(args);
   else if (args.register_bits == 5 && args.registers == 64)
@@ -826,6 +1050,59 @@ cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s, uint64_t* launche
   return cudaGetLastError();
 }
 
+// Reference packing of a byte-layout row: word w of the dense W-word row
+// holds bits [64w, 64w + 64) of register j at bit 5j (hll.hpp:183-240).
+__device__ __forceinline__ uint64_t pack_word(const uint8_t* row, uint32_t registers, uint64_t w) {
+  uint64_t word = 0;
+  const uint32_t j0 = static_cast<uint32_t>(64 * w / 5);
+  const uint32_t j1 = static_cast<uint32_t>((64 * w + 63) / 5);
+  for (uint32_t j = j0; j <= j1 && j < registers; ++j) {
+    const int64_t sh = static_cast<int64_t>(5 * j) - static_cast<int64_t>(64 * w);
+    const uint64_t r = row[j] & 31u;
+    word |= sh >= 0 ? r << sh : r >> -sh;
+  }
+  return word;
+}
+
+__global__ void gather_rows_bytes_kernel(const uint64_t* __restrict__ counters,
+                                         const uint32_t* __restrict__ perm, uint64_t first,
+                                         uint64_t count, uint32_t pitch, uint32_t words,
+                                         uint32_t registers, uint64_t* __restrict__ dst) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+       k < count * words; k += stride) {
+    const uint64_t i = k / words, w = k % words;
+    const uint64_t row = perm ? perm[first + i] : first + i;
+    dst[k] = pack_word(reinterpret_cast<const uint8_t*>(counters + row * pitch), registers, w);
+  }
+}
+
+// Restore into the byte layout: limb q (registers 4q..4q+3) of a row from
+// the reference packing.
+__global__ void scatter_rows_bytes_kernel(const uint64_t* __restrict__ src,
+                                          const uint32_t* __restrict__ perm, uint64_t count,
+                                          uint32_t pitch, uint32_t words, uint32_t registers,
+                                          uint64_t* __restrict__ counters) {
+  const uint64_t limbs = 2ull * pitch;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+       k < count * limbs; k += stride) {
+    const uint64_t i = k / limbs, q = k % limbs;
+    const uint64_t row = perm ? perm[i] : i;
+    const uint64_t* in = src + i * words;
+    uint32_t limb = 0;
+    for (uint32_t b = 0; b < 4; ++b) {
+      const uint32_t j = static_cast<uint32_t>(4 * q + b);
+      if (j >= registers) break;
+      const uint32_t bit = 5 * j, wi = bit >> 6, off = bit & 63;
+      uint64_t v = in[wi] >> off;
+      if (off + 5 > 64 && wi + 1 < words) v |= in[wi + 1] << (64 - off);
+      limb |= static_cast<uint32_t>(v & 31u) << (8 * b);
+    }
+    reinterpret_cast<uint32_t*>(counters + row * pitch)[q] = limb;
+  }
+}
+
 // Counter read-back under relabelling: row perm[first + i] -> dst row i.
 __global__ void gather_rows_kernel(const uint64_t* __restrict__ counters,
                                    const uint32_t* __restrict__ perm, uint64_t first,
@@ -893,9 +1170,17 @@ __global__ void scatter_rows_kernel(const uint64_t* __restrict__ src,
 }
 
 cudaError_t launch_scatter_rows(const uint64_t* src, const uint32_t* perm, uint64_t count,
-                                uint32_t pitch, uint32_t words, uint64_t* counters,
-                                cudaStream_t s, uint64_t* launches) {
+                                uint32_t pitch, uint32_t words, uint64_t* counters, bool bytes,
+                                uint32_t registers, cudaStream_t s, uint64_t* launches) {
   if (count == 0) return cudaSuccess;
+  if (bytes) {
+    uint64_t blocks = (count * 2 * pitch + 255) / 256;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    scatter_rows_bytes_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
+        src, perm, count, pitch, words, registers, counters);
+    ++*launches;
+    return cudaGetLastError();
+  }
   uint64_t blocks = (count * pitch + 255) / 256;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   scatter_rows_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(src, perm, count, pitch,
@@ -906,10 +1191,16 @@ cudaError_t launch_scatter_rows(const uint64_t* src, const uint32_t* perm, uint6
 
 cudaError_t launch_gather_rows(const uint64_t* counters, const uint32_t* perm, uint64_t first,
                                uint64_t count, uint32_t pitch, uint32_t words, uint64_t* dst,
-                               cudaStream_t s, uint64_t* launches) {
+                               bool bytes, uint32_t registers, cudaStream_t s, uint64_t* launches) {
   if (count == 0) return cudaSuccess;
   uint64_t blocks = (count * words + 255) / 256;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
+  if (bytes) {
+    gather_rows_bytes_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
+        counters, perm, first, count, pitch, words, registers, dst);
+    ++*launches;
+    return cudaGetLastError();
+  }
   gather_rows_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(counters, perm, first, count,
                                                                    pitch, words, dst);
   ++*launches;

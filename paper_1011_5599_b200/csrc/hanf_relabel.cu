@@ -62,14 +62,63 @@ __global__ void score_keys_kernel(const uint64_t* __restrict__ off, uint64_t n,
   }
 }
 
-// Relabelled shards: degree rank i -> row (i mod ways) * (n / ways) + i / ways
+// Line-aligned slots.  A W-word row with W odd (40 bytes for m = 64)
+// straddles a 128-byte line at 4 of every 16 row offsets; a random gather
+// of such a row costs two DRAM line fetches instead of one.  Past a hot
+// prefix (rows that live in L2 anyway, kept dense), degree ranks fill the
+// rows that sit inside one line first and the straddling rows last, so the
+// coldest nodes - the ones almost never gathered - take the straddling
+// slots.
+struct Slots {
+  uint64_t hot;    // rows [0, hot) of a range keep rank order (multiple of 16)
+  uint32_t n_in;   // offsets (mod 16) whose row lies inside one line
+  uint32_t n_st;   // offsets whose row straddles a line
+  uint8_t in[16];  // ascending
+  uint8_t st[16];  // ascending
+};
+
+// Local rank j of a range of `per` rows (per - hot arbitrary) -> local row.
+__device__ __forceinline__ uint64_t slot_of(const Slots& sl, uint64_t per, uint64_t j) {
+  if (sl.n_st == 0 || j < sl.hot) return j;
+  const uint64_t len = per - sl.hot, full = len / 16, rem = len % 16;
+  uint64_t in_total = full * sl.n_in;
+  for (uint32_t k = 0; k < sl.n_in; ++k) in_total += sl.in[k] < rem;
+  uint64_t k = j - sl.hot;
+  if (k < in_total) return sl.hot + 16 * (k / sl.n_in) + sl.in[k % sl.n_in];
+  k -= in_total;
+  return sl.hot + 16 * (k / sl.n_st) + sl.st[k % sl.n_st];
+}
+
+// Degree rank i -> row (i mod ways) * (n / ways) + slot(i / ways): relabelled
+// shards (ways > 1) get the same degree profile with their hot rows first.
 __global__ void interleave_kernel(const uint32_t* __restrict__ sorted, uint64_t n, uint32_t ways,
-                                  uint32_t* __restrict__ order) {
+                                  const Slots sl, uint32_t* __restrict__ order) {
   const uint64_t per = n / ways;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += stride)
-    order[(i % ways) * per + i / ways] = sorted[i];
+    order[(i % ways) * per + slot_of(sl, per, i / ways)] = sorted[i];
+}
+
+Slots make_slots(uint32_t pitch, uint64_t per, uint32_t ways) {
+  Slots sl{};
+  // HANF_SLOTS=0: plain rank order.  HANF_SLOTS_HOT: dense hot prefix (rows
+  // per range), default 2^22 rows (measured best on config 5, profiles/r02_union_probes.md)
+  const char* e = std::getenv("HANF_SLOTS");
+  if ((e && e[0] == '0') || pitch % 2 == 0 || pitch >= 16) return sl;
+  uint64_t hot = 1ull << 22;
+  if (const char* h = std::getenv("HANF_SLOTS_HOT")) hot = std::strtoull(h, nullptr, 10);
+  hot = (hot / ways) & ~15ull;  // the hot rows spread over the shards
+  if (hot >= per) return sl;
+  sl.hot = hot;
+  for (uint32_t o = 0; o < 16; ++o) {
+    const uint32_t start = (8 * pitch * o) % 128;
+    if (start + 8 * pitch > 128)
+      sl.st[sl.n_st++] = static_cast<uint8_t>(o);
+    else
+      sl.in[sl.n_in++] = static_cast<uint8_t>(o);
+  }
+  return sl;
 }
 
 // perm[order[r]] = r; new degree of row r (for the offsets scan)
@@ -174,8 +223,8 @@ struct Phases {  // HANF_PROFILE=1: synchronising phase times
 };
 }  // namespace
 
-cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t ways, cudaStream_t s,
-                                 RelabelOut* out, uint64_t* launches) {
+cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t ways, uint32_t pitch,
+                                 cudaStream_t s, RelabelOut* out, uint64_t* launches) {
   *out = RelabelOut{};
   if (n == 0) return cudaSuccess;
   Phases phase{s};
@@ -209,11 +258,13 @@ cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t way
   HANF_RELABEL_TRY(cudaFreeAsync(vals, s));
   HANF_RELABEL_TRY(cudaFreeAsync(skeys, s));
   HANF_RELABEL_TRY(cudaFreeAsync(d_bad, s));
-  if (ways > 1) {
-    if (n % (64ull * ways) != 0) return cudaErrorInvalidValue;
+  if (ways > 1 && n % (64ull * ways) != 0) return cudaErrorInvalidValue;
+  if (ways == 0) ways = 1;
+  const Slots sl = make_slots(pitch, n / ways, ways);
+  if (ways > 1 || sl.n_st) {
     uint32_t* inter = nullptr;
     HANF_RELABEL_TRY(pool_alloc(&inter, n, s));
-    interleave_kernel<<<grid(n), threads, 0, s>>>(out->order, n, ways, inter);
+    interleave_kernel<<<grid(n), threads, 0, s>>>(out->order, n, ways, sl, inter);
     ++*launches;
     HANF_RELABEL_TRY(cudaFreeAsync(out->order, s));
     out->order = inter;

@@ -153,9 +153,8 @@ __global__ void hub_index_kernel(const uint32_t* __restrict__ hub_nodes, uint32_
 }
 
 // ---- sparse union: one warp per worklist node -----------------------------
-template <int R, int NREG, bool kVec16>
+template <class Lay, bool kVec16>
 __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
-  using Lay = Layout<R, NREG>;
   constexpr int NL = Lay::kLimbs;
   const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -218,7 +217,12 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
 
 template <int R, int NREG, bool V>
 cudaError_t sparse_launch(const SparseArgs& a, uint32_t blocks, cudaStream_t s) {
-  sparse_union_kernel<R, NREG, V><<<blocks, 256, 0, s>>>(a);
+  sparse_union_kernel<Layout<R, NREG>, V><<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+template <int M>
+cudaError_t sparse_launch_bytes(const SparseArgs& a, uint32_t blocks, cudaStream_t s) {
+  sparse_union_kernel<ByteLayout<M>, true><<<blocks, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -304,6 +308,13 @@ cudaError_t sparse_tail_stages(const SparseArgs& a, uint64_t w0, uint64_t w1,
   SparseArgs b = a;
   b.work_len = a.lens + 1;
   ++*launches;
+  if (b.bytes) switch (registers) {
+      case 16: return sparse_launch_bytes<16>(b, blocks, s);
+      case 32: return sparse_launch_bytes<32>(b, blocks, s);
+      case 64: return sparse_launch_bytes<64>(b, blocks, s);
+      case 128: return sparse_launch_bytes<128>(b, blocks, s);
+      default: return cudaErrorInvalidValue;
+    }
   switch (register_bits * 1000 + registers) {
     case 5032: return sparse_launch<5, 32, false>(b, blocks, s);
     case 5064: return sparse_launch<5, 64, false>(b, blocks, s);

@@ -603,3 +603,60 @@ def test_step_launch_complete(hanf):
                 break
         with pytest.raises(ValueError):
             b.step_complete()
+
+
+@pytest.mark.parametrize("layout", ["packed", "bytes"])
+def test_golden_traces_each_counter_layout(hanf, traces, monkeypatch, layout):
+    """Both device counter stores (byte registers, the default for
+    L2-resident arrays, and the reference packing) reproduce every golden
+    trace bit for bit: the layout changes time only."""
+    monkeypatch.setenv("HANF_LAYOUT", layout)
+    for case in traces:
+        g = graph_of(hanf, case["graph"])
+        with hanf.NfEngine(g, hanf.EngineConfig(**case["cfg"])) as e:
+            assert sha(e.counters()) == case["counters0_sha256"]
+            for step in case["steps"]:
+                r = e.step()
+                assert (float.hex(r.sum), r.modified) == (step["sum"], step["modified"]), step["t"]
+                assert sha(e.counters()) == step["counters_sha256"], step["t"]
+            e.reset()
+            est = e.run_to_stabilisation()
+            assert [float.hex(v) for v in est.values] == case["run_values"]
+
+
+@pytest.mark.parametrize("env", [{"HANF_LAYOUT": "bytes", "HANF_RELABEL": "1"},
+                                 {"HANF_LAYOUT": "bytes", "HANF_SPARSE": "1"},
+                                 {"HANF_LAYOUT": "bytes", "HANF_SEGMENTS": "1", "HANF_SUMMARY": "1"},
+                                 {"HANF_LAYOUT": "bytes", "HANF_RELABEL": "1", "HANF_SPARSE": "1"},
+                                 {"HANF_LAYOUT": "packed", "HANF_SPARSE": "1"}])
+def test_byte_layout_paths(hanf, port, monkeypatch, env):
+    """Byte-layout rows through every path that touches them: relabelled
+    rows, the worklist step, segmented skip sweeps with the summary probe,
+    hub chunks (clique-path hubs) and m = 16..128; lockstep with the
+    oracle, counters read back in the reference packing."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for g in (hanf.gen_rmat(12, 16, 0.57, 0.19, 0.19, 3, 5), hanf.gen_clique_path(1500, 3)):
+        for b in (4, 5, 6, 7):
+            lockstep(hanf, port, g, bucket_bits=b, seed=1234 + b)
+
+
+def test_byte_layout_snapshot_restore(hanf, monkeypatch, tmp_path):
+    """HCA1 snapshots written from byte rows are the reference packing, and
+    restoring them into either layout resumes bit for bit."""
+    g = hanf.gen_rmat(11, 8, 0.57, 0.19, 0.19, 2, 9)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=5)
+    monkeypatch.setenv("HANF_LAYOUT", "packed")
+    with hanf.NfEngine(g, cfg) as ref:
+        ref.step(), ref.step()
+        want = ref.counters()
+        ref.save_counters(str(tmp_path / "p.hca"))
+    monkeypatch.setenv("HANF_LAYOUT", "bytes")
+    with hanf.NfEngine(g, cfg) as e:
+        e.step(), e.step()
+        assert np.array_equal(e.counters(), want)
+        e.save_counters(str(tmp_path / "b.hca"))
+        assert (tmp_path / "b.hca").read_bytes() == (tmp_path / "p.hca").read_bytes()
+        e.reset()
+        e.restore_counters(str(tmp_path / "p.hca"))
+        assert np.array_equal(e.counters(), want)
