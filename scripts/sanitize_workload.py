@@ -2,7 +2,7 @@
 initcheck): the engine paths on small graphs, each checked against the
 oracle so a run also proves the results.
     compute-sanitizer --tool T python scripts/sanitize_workload.py PATH
-PATH: dense | worklist | summary | segments | peer | multi | relabel | hubs"""
+PATH: dense | packed | worklist | summary | segments | peer | multi | relabel | hubs"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -10,7 +10,7 @@ import oracle
 import paper_1011_5599_b200 as h
 
 path = sys.argv[1]
-env = {"worklist": {"HANF_SPARSE": "1"}, "summary": {"HANF_SUMMARY": "1"},
+env = {"packed": {"HANF_LAYOUT": "packed"}, "worklist": {"HANF_SPARSE": "1"}, "summary": {"HANF_SUMMARY": "1"},
        "segments": {"HANF_SEGMENTS": "1"}, "relabel": {"HANF_RELABEL": "1"},
        "multi": {}, "peer": {"HANF_RELABEL": "1"}}.get(path, {})
 os.environ.update(env)
