@@ -12,7 +12,9 @@ from ctypes import (POINTER, Structure, c_char_p, c_double, c_int32, c_uint32,
                     c_uint64, c_void_p)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhanf.so")
+# HANF_LIB=checked loads the bounds-checked build (csrc/Makefile `checked`)
+LIB_PATH = os.path.join(_HERE, "libhanf_checked.so" if os.environ.get("HANF_LIB") == "checked"
+                        else "libhanf.so")
 
 
 class GraphView(Structure):

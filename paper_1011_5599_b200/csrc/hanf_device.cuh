@@ -12,7 +12,26 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <type_traits>
+
+// Checked builds (make checked -> libhanf_checked.so, HANF_LIB=checked):
+// every row, bitmap word and task index a kernel derives from device data
+// is bounds-checked and a violation traps with its source line.  The
+// default build compiles the checks out.
+#ifdef HANF_CHECKED
+#define HANF_DCHECK(c)                                                            \
+  do {                                                                            \
+    if (!(c)) {                                                                   \
+      printf("hanf check failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);          \
+      __trap();                                                                   \
+    }                                                                             \
+  } while (0)
+#else
+#define HANF_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
 
 namespace hanf {
 

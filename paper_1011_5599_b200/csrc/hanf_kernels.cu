@@ -193,6 +193,7 @@ __device__ __forceinline__ uint32_t est_slot(const uint32_t* orig_of, uint32_t v
 }
 __device__ __forceinline__ void mark_changed(uint64_t* mod_next, uint64_t* dirty_next,
                                              const uint32_t* orig_of, uint32_t v) {
+  HANF_DCHECK(!dirty_next || orig_of);
   atomicOr(reinterpret_cast<unsigned long long*>(mod_next) + (v >> 6), 1ull << (v & 63));
   if (dirty_next) {
     const uint32_t o = orig_of[v];
@@ -219,6 +220,7 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
   const uint32_t v = args.hub_nodes[h];
   const uint32_t first = args.hub_first[h];
   const uint32_t count = args.hub_count[h];
+  HANF_DCHECK(v < args.zero_row && count >= 1);
   const uint32_t words = args.pitch;
   bool stale = false;
   if (args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
@@ -338,6 +340,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
   constexpr int NL = Lay::kLimbs;
   constexpr int NW = Lay::kWords;
   using G_t = Gather<Lay, GMODE, kVec16>;
+  HANF_DCHECK(task_index < args.num_wtasks);
   const WarpTask task = args.wtasks[task_index];
   const bool hub = task.nodes == 0;
   if constexpr (SKIP) {
@@ -361,6 +364,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
     active = j < task.nodes;
     if (active) v = args.order[task.item + j];
   }
+  HANF_DCHECK(v <= zero_row && (!active || v < zero_row));
   const bool lead = active && sub == 0 && !hub;
   bool stale = false;
   if (lead && args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
@@ -416,7 +420,10 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
       }
       G_t g[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) g[j].issue(cur, w[j], words, woff);
+      for (int j = 0; j < U; ++j) {
+        HANF_DCHECK(w[j] <= zero_row);
+        g[j].issue(cur, w[j], words, woff);
+      }
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         uint32_t y[NL];
@@ -472,6 +479,7 @@ __device__ __forceinline__ void commit_bytes(const UnionArgs& args, const WarpTa
   bool st = false;
   if (act) {
     v = args.order[task.item + j];
+    HANF_DCHECK(v < args.zero_row);
     if (args.stale_valid) st = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
   }
   const bool nz = group_or<Q>(live && (acc.x | acc.y | acc.z | acc.w) != 0);
@@ -511,6 +519,7 @@ __device__ __forceinline__ void union_task_bytes(const UnionArgs& args, uint32_t
                                                  uint32_t lane, const uint64_t* summ) {
   using Lay = ByteLayout<M>;
   constexpr int Q = M / 16;  // lanes per counter row
+  HANF_DCHECK(task_index < args.num_wtasks);
   const WarpTask task = args.wtasks[task_index];
   const bool hub = task.nodes == 0;
   if constexpr (SKIP) {
@@ -551,7 +560,10 @@ __device__ __forceinline__ void union_task_bytes(const UnionArgs& args, uint32_t
       }
       uint4 y[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) y[u] = __ldg(cur + static_cast<uint64_t>(w[u]) * Q + k);
+      for (int u = 0; u < U; ++u) {
+        HANF_DCHECK(w[u] <= zero_row);
+        y[u] = __ldg(cur + static_cast<uint64_t>(w[u]) * Q + k);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) acc = byte_max4(acc, y[u]);
     }

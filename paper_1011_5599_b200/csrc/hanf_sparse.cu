@@ -164,7 +164,9 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
   for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
        i += warps) {
     const uint32_t v = a.work[i];
+    HANF_DCHECK(v >= a.node_base && v < a.hi);
     const uint64_t s = a.off[v - a.node_base], e = a.off[v - a.node_base + 1];
+    HANF_DCHECK(s <= e && e - s <= kHubDegree);
     uint32_t acc[NL];
     if (lane == 0)
       load_chunk<Lay, kVec16>(acc, a.cur + static_cast<uint64_t>(v) * words);
@@ -180,8 +182,10 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
         w[j] = k < e ? a.succ[k - a.succ_base] : zero_row;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 4; ++j) {
+        HANF_DCHECK(w[j] <= zero_row);
         if (!((__ldg(a.mod_cur + (w[j] >> 6)) >> (w[j] & 63)) & 1)) w[j] = zero_row;
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (w[j] != zero_row) {
