@@ -469,49 +469,61 @@ __device__ __forceinline__ uint32_t group_or(uint32_t x) {
 }
 
 // Group commit of light node slot j (warp-synchronous: every lane calls it;
-// `act` is uniform within a group).
+// `act` is uniform within a group): the row store happens here; the
+// estimate's integer terms come back summed over the group so that the
+// caller can finish estimates and set modified bits for a whole warp of
+// nodes at once (one double division per lane instead of one per group).
+struct ByteCommit {
+  uint64_t sum;   // sum of 2^(31 - M_j) over the node's registers
+  uint32_t zeros;
+  uint32_t v;
+  bool want;      // the estimate must be written
+  bool changed;
+};
+
 template <int Q>
-__device__ __forceinline__ void commit_bytes(const UnionArgs& args, const WarpTask& task, uint32_t j,
-                                             bool act, bool live, const uint4& acc, uint32_t k) {
+__device__ __forceinline__ ByteCommit commit_bytes(const UnionArgs& args, const WarpTask& task,
+                                                   uint32_t j, bool act, bool live, const uint4& acc,
+                                                   uint32_t k) {
   const uint4* __restrict__ cur = reinterpret_cast<const uint4*>(args.cur);
   act = act && j < task.nodes;
-  uint32_t v = args.zero_row;
+  ByteCommit o{0, 0, args.zero_row, false, false};
   bool st = false;
   if (act) {
-    v = args.order[task.item + j];
-    HANF_DCHECK(v < args.zero_row);
-    if (args.stale_valid) st = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
+    o.v = args.order[task.item + j];
+    HANF_DCHECK(o.v < args.zero_row);
+    if (args.stale_valid) st = (args.mod_cur[o.v >> 6] >> (o.v & 63)) & 1;
   }
   const bool nz = group_or<Q>(live && (acc.x | acc.y | acc.z | acc.w) != 0);
   const bool need = act && (st || nz);
   uint4 own = make_uint4(0, 0, 0, 0);
-  if (need) own = __ldg(cur + static_cast<uint64_t>(v) * Q + k);
+  if (need) own = __ldg(cur + static_cast<uint64_t>(o.v) * Q + k);
   const uint4 nx = byte_max4(acc, own);
-  const bool changed =
+  o.changed =
       group_or<Q>(need && ((nx.x ^ own.x) | (nx.y ^ own.y) | (nx.z ^ own.z) | (nx.w ^ own.w)));
-  if (changed || (act && st)) {
-    const uint64_t off = static_cast<uint64_t>(v) * Q + k;
+  if (o.changed || (act && st)) {
+    const uint64_t off = static_cast<uint64_t>(o.v) * Q + k;
     reinterpret_cast<uint4*>(args.next)[off] = nx;
     for (uint32_t p = 0; p < args.peers.count; ++p)
       reinterpret_cast<uint4*>(args.peers.next[p])[off] = nx;
   }
-  if (args.est) {
-    const bool want = changed || (act && st && args.peers.push_est);
-    if (__any_sync(0xffffffffu, want)) {
-      uint64_t sum = 0;
-      uint32_t zeros = 0;
-      byte_terms(nx, sum, zeros);
+  o.want = args.est && (o.changed || (act && st && args.peers.push_est));
+  if (__any_sync(0xffffffffu, o.want)) {
+    byte_terms(nx, o.sum, o.zeros);
 #pragma unroll
-      for (int o = 1; o < Q; o <<= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
-      }
-      if (want && k == 0)
-        push_estimate(args, v,
-                      finish_estimate(args.ep, __dmul_rn(static_cast<double>(sum), 0x1p-31), zeros));
+    for (int off = 1; off < Q; off <<= 1) {
+      o.sum += __shfl_xor_sync(0xffffffffu, o.sum, off);
+      o.zeros += __shfl_xor_sync(0xffffffffu, o.zeros, off);
     }
   }
-  if (changed && k == 0) mark_changed(args.mod_next, args.dirty_next, args.orig_of, v);
+  return o;
+}
+
+__device__ __forceinline__ void finish_commit(const UnionArgs& args, const ByteCommit& o) {
+  if (o.want)
+    push_estimate(args, o.v,
+                  finish_estimate(args.ep, __dmul_rn(static_cast<double>(o.sum), 0x1p-31), o.zeros));
+  if (o.changed) mark_changed(args.mod_next, args.dirty_next, args.orig_of, o.v);
 }
 
 template <int M, int U, bool SKIP>
@@ -536,14 +548,27 @@ __device__ __forceinline__ void union_task_bytes(const UnionArgs& args, uint32_t
   const uint32_t trips = task.trips;
   bool task_live = !SKIP;
   uint4 acc = make_uint4(0, 0, 0, 0);
+  ByteCommit mine{0, 0, zero_row, false, false};  // G < Q: this lane's node of the warp
+  // ids of the next trip group are requested before the current group's
+  // gathers (across the stream passes too)
+  const uint32_t* __restrict__ base = args.tos + task.tos + grp * Q;
+  uint32_t wn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) wn[u] = u < static_cast<int>(trips) ? __ldg(base + 32 * u) : zero_row;
 #pragma unroll 1
   for (uint32_t s = 0; s < static_cast<uint32_t>(Q); ++s) {
-    const uint32_t* __restrict__ ids = args.tos + task.tos + grp * Q + s;
 #pragma unroll 1
     for (uint32_t i = 0; i < trips; i += U) {
       uint32_t w[U];
+      // next group: trips i+U.. of this stream, or the first of the next
+      const bool wrap = i + U >= trips;
+      const uint32_t ns = wrap ? s + 1 : s, ni = wrap ? 0 : i + U;
 #pragma unroll
-      for (int u = 0; u < U; ++u) w[u] = i + u < trips ? __ldg(ids + 32 * (i + u)) : zero_row;
+      for (int u = 0; u < U; ++u) {
+        w[u] = wn[u];
+        wn[u] = ns < static_cast<uint32_t>(Q) && ni + u < trips ? __ldg(base + ns + 32 * (ni + u))
+                                                                : zero_row;
+      }
       if constexpr (SKIP) {
         bool live = false;
 #pragma unroll
@@ -567,19 +592,26 @@ __device__ __forceinline__ void union_task_bytes(const UnionArgs& args, uint32_t
 #pragma unroll
       for (int u = 0; u < U; ++u) acc = byte_max4(acc, y[u]);
     }
-    // a node of G < Q streams ends with stream grp*Q + s
+    // a node of G < Q streams ends with stream grp*Q + s; lane s / G of
+    // the group keeps its commit for the warp-wide finish
     if (G < static_cast<uint32_t>(Q) && ((s + 1) & (G - 1)) == 0) {
       const uint32_t first = grp * Q + s + 1 - G;
-      commit_bytes<Q>(args, task, first >> lg, true, task_live, acc, k);
+      const ByteCommit o = commit_bytes<Q>(args, task, first >> lg, true, task_live, acc, k);
+      if (k == s >> lg) mine = o;
       acc = make_uint4(0, 0, 0, 0);
     }
   }
-  if (G < static_cast<uint32_t>(Q)) return;
+  if (G < static_cast<uint32_t>(Q)) {
+    finish_commit(args, mine);
+    return;
+  }
   // nodes of G >= Q streams: combine the G/Q groups of each node
   if (task_live)
     for (uint32_t off = 1; off < G / Q; off <<= 1) acc = byte_max4(acc, shfl_xor4(acc, off * Q));
   if (!hub) {
-    commit_bytes<Q>(args, task, (grp * Q) >> lg, ((grp * Q) & (G - 1)) == 0, task_live, acc, k);
+    const ByteCommit o =
+        commit_bytes<Q>(args, task, (grp * Q) >> lg, ((grp * Q) & (G - 1)) == 0, task_live, acc, k);
+    if (k == 0) finish_commit(args, o);
     return;
   }
   // hub chunk: the partial maximum (every group holds it), then the ticket
