@@ -261,6 +261,9 @@ struct hanf_engine {
   // bitmap) instead of every block; all_dirty_commit = recompute them all
   uint64_t* dirty_derived = nullptr;
   bool all_dirty_commit = true;
+  // unsharded relabelled engines, dense sweeps: no original-id dirty bits
+  // (one random atomic per changed row); the commit re-sums every block
+  bool skip_dirty = false;
   // hanf_shard_reduce ran for this step: the ranks re-summed one slice of
   // the original-id blocks each and published them; commit sums the inbox
   bool reduced = false;
@@ -521,7 +524,7 @@ hanf_status finish_enqueue(hanf_engine* e, const uint64_t* bits, bool recompute,
   f.perm = e->est_rows ? e->perm : nullptr;
   // relabelled shards: every block from the (peer-pushed) estimates, or
   // the derived dirty blocks (commit_enqueue)
-  f.all_dirty = in_step && e->shard_relabel && e->all_dirty_commit ? 1 : 0;
+  f.all_dirty = in_step && ((e->shard_relabel && e->all_dirty_commit) || e->skip_dirty) ? 1 : 0;
   // the last CTA writes total + count into the page-locked report itself
   // (no read-back copy node after the kernel)
   f.host_out = e->h_reduce;
@@ -765,7 +768,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.stale_valid = e->stale_valid ? 1 : 0;
   a.orig_of = e->order;
   a.est_index = e->est_rows ? nullptr : e->order;
-  a.dirty_next = e->dirty[ng];
+  a.dirty_next = e->skip_dirty ? nullptr : e->dirty[ng];
   a.peers = peer_rows(e, ng);
   a.bytes = e->bytes ? 1 : 0;
   return a;
@@ -856,7 +859,13 @@ hanf_status compute_shard(hanf_engine* e) {
   if (!e->next_bits_clear)
     HANF_CUDA(cudaMemsetAsync(e->mod[ng] + w0, 0, sizeof(uint64_t) * (w1 - w0), e->stream));
   e->next_bits_clear = false;
-  if (e->dirty[ng])  // unsharded relabelling: the whole original-id bitmap
+  // Dense sweeps of unsharded relabelled engines change nearly every block:
+  // rather than an original-id dirty bit per changed row (a random atomic
+  // each), the commit re-sums every block through perm (same sums, same
+  // order).  The count comes from the row bitmap (popcount is permutation-
+  // invariant).
+  e->skip_dirty = e->dirty[ng] && e->est_rows && e->lo == 0 && e->hi == e->n && step_mode(e) == 0;
+  if (e->dirty[ng] && !e->skip_dirty)  // unsharded relabelling: the whole original-id bitmap
     HANF_CUDA(cudaMemsetAsync(e->dirty[ng], 0, sizeof(uint64_t) * e->blocks, e->stream));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[0], e->stream));
   if (step_mode(e) == 2 && e->tr_off) {
@@ -945,7 +954,8 @@ hanf_status commit_enqueue(hanf_engine* e) {
     if (rs != HANF_OK) return rs;
     return finish_enqueue(e, bits, true, 0, e->blocks, true);
   }
-  const hanf_status st = finish_enqueue(e, dirty_of(e, ng), commit_recomputes(e), 0, e->blocks, true);
+  const hanf_status st = finish_enqueue(e, e->skip_dirty ? e->mod[ng] : dirty_of(e, ng),
+                                        commit_recomputes(e), 0, e->blocks, true);
   // (finish_kernel cleared mod[cur], the next step's mod_next)
   if (st == HANF_OK && e->lo == 0 && e->hi == e->n) e->next_bits_clear = true;
   return st;
