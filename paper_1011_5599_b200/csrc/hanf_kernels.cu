@@ -191,6 +191,28 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
 __device__ __forceinline__ uint32_t est_slot(const uint32_t* orig_of, uint32_t v) {
   return orig_of ? orig_of[v] : v;
 }
+// Warp-aggregated form for the packed sweep (every lane calls it): lanes
+// whose rows share a bitmap word (a warp's light nodes are consecutive
+// rows in degree order) set their bits with one atomic (config 5: 56.4 ->
+// 55.6 ms; the byte-layout sweep keeps one atomic per node, which measured
+// faster there).
+__device__ __forceinline__ void mark_changed_warp(uint64_t* mod_next, uint64_t* dirty_next,
+                                                  const uint32_t* orig_of, uint32_t v,
+                                                  bool changed) {
+  const uint32_t word = changed ? v >> 6 : 0xffffffffu;
+  const uint32_t peers = __match_any_sync(0xffffffffu, word);
+  const uint64_t bit = changed ? 1ull << (v & 63) : 0ull;
+  const uint32_t lo = __reduce_or_sync(peers, static_cast<uint32_t>(bit));
+  const uint32_t hi = __reduce_or_sync(peers, static_cast<uint32_t>(bit >> 32));
+  if (changed && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
+    atomicOr(reinterpret_cast<unsigned long long*>(mod_next) + word,
+             (static_cast<uint64_t>(hi) << 32) | lo);
+  if (changed && dirty_next) {
+    const uint32_t o = orig_of[v];
+    atomicOr(reinterpret_cast<unsigned long long*>(dirty_next) + (o >> 6), 1ull << (o & 63));
+  }
+}
+
 __device__ __forceinline__ void mark_changed(uint64_t* mod_next, uint64_t* dirty_next,
                                              const uint32_t* orig_of, uint32_t v) {
   HANF_DCHECK(!dirty_next || orig_of);
@@ -315,7 +337,7 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
 template <class Lay, bool kVec16>
 __device__ __forceinline__ void task_finish(const UnionArgs& args, const WarpTask& task, bool hub,
                                             uint32_t v, bool any_changed, uint32_t lane) {
-  if (any_changed) mark_changed(args.mod_next, args.dirty_next, args.orig_of, v);
+  mark_changed_warp(args.mod_next, args.dirty_next, args.orig_of, v, any_changed);
   if (hub) {
     const uint32_t h = args.chunk_hub[task.item];
     uint32_t last = 0;
