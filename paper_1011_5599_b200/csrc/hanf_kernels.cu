@@ -812,9 +812,10 @@ cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t
       if (single) return union_launch<5, 32, 4, 1, false, 1, true>(args, ch, s);
       return union_launch<5, 32, 4, 0, false>(args, ch, s);
     case 5064:
-      // U = 3, <= 48 registers (5 CTAs/SM), next-trip id prefetch: +2%
-      // on config 2 and +1% on R-MAT 26 over 64 registers
-      if (single) return union_launch<5, 64, 3, 1, false, 5, true>(args, ch, s);
+      // U = 2, <= 48 registers (5 CTAs/SM), next-trip id prefetch: config 5
+      // 54.5 ms against 55.6 (U = 3), 57.8 (U = 2, 6 CTAs/SM), 59.9 (U = 4)
+      // and 67.7 (U = 3, 6 CTAs/SM); config 2 packed 0.181 vs 0.184 ms
+      if (single) return union_launch<5, 64, 2, 1, false, 5, true>(args, ch, s);
       return union_launch<5, 64, 4, 0, false>(args, ch, s);
     case 5128: return union_launch<5, 128, 2, 0, true, 3, true>(args, ch, s);
     case 6016: return union_launch<6, 16, 4, 0, true>(args, ch, s);

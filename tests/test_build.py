@@ -9,7 +9,7 @@ LOG = os.path.join(ROOT, "paper_1011_5599_b200", "csrc", "build", "hanf_kernels.
 
 # mangled template arguments of the default dense variants: R, NREG, U, GMODE,
 # kVec16, MINB, PF, SKIP=false (hanf_kernels.cu launch_union)
-DEFAULTS = ["ILi5ELi64ELi3ELi1ELb0ELi5ELb1ELb0E",   # m = 64 (configs 1, 2, 5)
+DEFAULTS = ["ILi5ELi64ELi2ELi1ELb0ELi5ELb1ELb0E",   # m = 64 (configs 5; 1, 2 under HANF_LAYOUT=packed)
             "ILi5ELi32ELi4ELi3ELb0ELi1ELb1ELb0E",   # m = 32, padded rows (config 4)
             "ILi5ELi128ELi2ELi0ELb1ELi3ELb1ELb0E"]  # m = 128 (config 3)
 
