@@ -403,7 +403,8 @@ def single_gpu_config2(dev, steps, warmup, flush, peak):
             "unit": "arcs/s", "ms_per_step": total_ms / steps,
             "roofline": {"achieved": ach, "frac": ach / peak, "kernel_ms": ph["union"],
                          "algorithmic_bytes": B,
-                         "note": "42 MB counter array: L2-resident, bound by L1 wavefronts"}}
+                         "note": "L2-resident counter array (byte-register store, 67 MB): "
+                                 "bound by the SM side (L1 wavefronts, ALU), not DRAM"}}
 
 
 def shared_graph(config: int, local_rank: int, backend: str):
@@ -416,7 +417,10 @@ def shared_graph(config: int, local_rank: int, backend: str):
     import paper_1011_5599_b200 as hanf
     tag = os.environ.get("TORCHELASTIC_RUN_ID", os.environ.get("MASTER_PORT", "0"))
     base = f"/dev/shm/hanf_bench_{tag}_c{config}"
-    if local_rank == 0:
+    # (the node's first process by launch order: with gloo several ranks may
+    # share a GPU and so a remapped local_rank)
+    leader = int(os.environ.get("LOCAL_RANK", "0")) == 0
+    if leader:
         g = make_graph(config, device=0 if CONFIGS[config]["kind"] == "rmat" and backend == "nccl"
                        else None)
         np.save(base + "_off.npy", g.offsets())
@@ -427,7 +431,7 @@ def shared_graph(config: int, local_rank: int, backend: str):
     succ = np.load(base + "_succ.npy", mmap_mode="r+")
     g = hanf.Graph(len(off) - 1, off, succ)
     dist.barrier()
-    if local_rank == 0:  # (the mappings stay valid)
+    if leader:  # (the mappings stay valid)
         for f in (base + "_off.npy", base + "_succ.npy"):
             os.unlink(f)
     return g
