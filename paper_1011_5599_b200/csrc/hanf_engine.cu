@@ -310,6 +310,11 @@ struct hanf_engine {
   unsigned long long* pack_count = nullptr;  // hanf_shard_pack scratch
   uint32_t summ_shift = 6;
   bool force_summary = false;  // HANF_SUMMARY=1 (tests): every skip sweep is mode 3
+  // task-scan step (mode 4): flat TOS scan lists the tasks to sweep
+  int task_scan = -1;             // HANF_TASKSCAN: -1 by size, 0 off, 1 forced
+  unsigned int* scan_flags = nullptr;
+  uint32_t* scan_list = nullptr;
+  unsigned int* scan_count = nullptr;
   bool step_pending = false;   // hanf_step_launch done, hanf_step_complete not yet
   uint64_t summ_bits = 0;
   bool use_graphs = true;
@@ -416,6 +421,9 @@ struct hanf_engine {
       pfree(mod_list, stream);
       pfree(work, stream);
       pfree(hub_tasks, stream);
+      pfree(scan_flags, stream);
+      pfree(scan_list, stream);
+      pfree(scan_count, stream);
       pfree(hub_index, stream);
       pfree(batch_mix, stream);
       pfree(batch_sums, stream);
@@ -665,6 +673,13 @@ bool sparse_wanted(const hanf_engine* e) {
   return e->cfg.track_modified && e->t != 0 && e->sparse_ok && e->stale_valid &&
          ratio * e->last_count < e->n;
 }
+bool task_scan_wanted(const hanf_engine* e) {
+  if (e->task_scan == 0 || e->lo != 0 || e->hi != e->n || e->batch != 1 || e->seg_live ||
+      !hanf::fused_estimates(e->params.register_bits, e->params.registers))
+    return false;
+  if (e->task_scan == 1) return true;
+  return e->tasks.tos_words >= (1ull << 28) && 64 * e->last_count < e->n;
+}
 int step_mode(const hanf_engine* e) {
   if (!e->cfg.track_modified || e->t == 0) return 0;
   // the transpose costs about as much as 8 skip sweeps of the same arcs
@@ -677,6 +692,10 @@ int step_mode(const hanf_engine* e) {
   const uint64_t span = e->hi - e->lo;
   const uint64_t active = span ? e->tasks.active_nodes * (e->n / span) : e->n;
   if (2 * e->last_count >= active) return 0;
+  // few changed counters on a large unsegmented single engine: list the
+  // tasks in reach of a change with one flat TOS scan (mode 4); skip sweeps
+  // otherwise walk every task (config 5's tail: ~10 ms for one counter)
+  if (task_scan_wanted(e)) return 4;
   // few changed counters: filter the per-arc bitmap probes through the
   // L1-resident summary first (most probes then never reach L2)
   return e->force_summary || 16 * e->last_count < e->summ_bits ? 3 : 1;
@@ -889,16 +908,43 @@ hanf_status compute_shard(hanf_engine* e) {
     a.seg_live = e->seg_live;
     a.seg_shift = e->tasks.seg_shift;
   }
-  if (mode == 3) {
+  if (mode == 3 || mode == 4) {
     HANF_CUDA(hanf::launch_summary(e->mod[g], e->blocks + 1, e->summ_shift, e->summ_bits, e->summ,
                                    e->stream, &e->launches));
     a.summ = e->summ;
     a.summ_shift = e->summ_shift;
     a.summ_words = static_cast<uint32_t>((e->summ_bits + 63) / 64);
   }
+  if (mode == 4) {
+    // the tasks in reach of a change, from one pass over the TOS
+    HANF_CUDA(cudaMemsetAsync(e->scan_flags, 0, sizeof(unsigned int) * e->tasks.num_wtasks, e->stream));
+    HANF_CUDA(cudaMemsetAsync(e->scan_count, 0, sizeof(unsigned int), e->stream));
+    hanf::TaskScanArgs ts{};
+    ts.tos = e->tasks.tos;
+    ts.tos_words = e->tasks.tos_words;
+    ts.wtasks = e->tasks.wtasks;
+    ts.num_wtasks = e->tasks.num_wtasks;
+    ts.zero_row = static_cast<uint32_t>(e->n);
+    ts.mod_cur = e->mod[g];
+    ts.summ = e->summ;
+    ts.summ_shift = e->summ_shift;
+    ts.summ_words = a.summ_words;
+    ts.chunk_hub = e->tasks.chunk_hub;
+    ts.hub_first = e->tasks.hub_first;
+    ts.hub_count = e->tasks.hub_count;
+    ts.flags = e->scan_flags;
+    ts.list = e->scan_list;
+    ts.count = e->scan_count;
+    HANF_CUDA(hanf::launch_task_scan(ts, e->stream, &e->launches));
+    a.task_list = e->scan_list;
+    a.task_count = e->scan_count;
+  }
   const bool fused = a.est != nullptr;
   HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers, e->stream,
                                &e->launches));
+  if (mode == 4)  // rows changed last step that no listed task rewrote
+    HANF_CUDA(hanf::launch_stale_fixup(e->mod[g], e->mod[ng], e->n, static_cast<uint32_t>(e->pitch),
+                                       e->cnt[g], e->cnt[ng], e->stream, &e->launches));
   if (e->timing) HANF_CUDA(cudaEventRecord(e->ev[1], e->stream));
   const bool sharded = e->lo != 0 || e->hi != e->n;
   if (!fused) {
@@ -1009,6 +1055,11 @@ hanf_status step_enqueue(hanf_engine* e) {
   if (mode == 2) {
     const hanf_status st = ensure_sparse(e);
     if (st != HANF_OK) return st;
+  }
+  if (mode == 4 && !e->scan_list) {  // (allocated outside any graph capture)
+    HANF_CUDA(palloc(&e->scan_flags, e->tasks.num_wtasks, e->stream));
+    HANF_CUDA(palloc(&e->scan_list, e->tasks.num_wtasks, e->stream));
+    HANF_CUDA(palloc(&e->scan_count, 1, e->stream));
   }
   if (!e->use_graphs || e->timing) {
     const hanf_status st = compute_local(e);
@@ -1153,6 +1204,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   e->pitch = hanf::row_pitch(params.register_bits, params.registers, params.words_per_counter,
                              e->bytes);
   if (const char* fs = std::getenv("HANF_SUMMARY")) e->force_summary = fs[0] == '1';
+  if (const char* ts = std::getenv("HANF_TASKSCAN")) e->task_scan = ts[0] == '1' ? 1 : (ts[0] == '0' ? 0 : -1);
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
   // Worklist step (HANF_SPARSE=0 disables): taken once fewer than n/128

@@ -238,6 +238,30 @@ struct EstimateArgs {
   uint32_t bytes;            // byte-layout counter store
 };
 
+// Task-scan step (hanf_kernels.cu, step mode 4): tasks with a successor
+// modified by the previous step, listed from one flat pass over the TOS.
+struct TaskScanArgs {
+  const uint32_t* tos;
+  uint64_t tos_words;
+  const WarpTask* wtasks;
+  uint32_t num_wtasks;
+  uint32_t zero_row;
+  const uint64_t* mod_cur;
+  const uint64_t* summ;     // summary of mod_cur (one bit per 2^summ_shift rows)
+  uint32_t summ_shift;
+  uint32_t summ_words;
+  const uint32_t* chunk_hub;
+  const uint32_t* hub_first;
+  const uint32_t* hub_count;
+  unsigned int* flags;      // per task, zeroed before the scan
+  uint32_t* list;           // listed task indices
+  unsigned int* count;      // (device) list length, zeroed before the scan
+};
+cudaError_t launch_task_scan(const TaskScanArgs& a, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_stale_fixup(const uint64_t* mod_cur, const uint64_t* mod_next, uint64_t n,
+                               uint32_t pitch, const uint64_t* cur, uint64_t* next, cudaStream_t s,
+                               uint64_t* launches);
+
 // Launchers (hanf_kernels.cu).  All are stream-ordered and asynchronous.
 cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
                         uint64_t node_begin, uint64_t node_end, uint32_t bucket_bits,

@@ -1079,6 +1079,125 @@ cudaError_t launch_segment_live(const uint64_t* mod_cur, const uint32_t* seg_min
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Task-scan step (late iterations of large graphs, step mode 4).  Instead of
+// walking every task, one flat, coalesced pass over the TOS finds the id
+// rows holding a successor modified by the previous step (summary bit in
+// shared memory, then the bitmap) and lists their tasks (every chunk of a
+// hub, so the hub ticket completes); the skip sweep then runs on that list
+// only (union_kernel task_list).  Nodes changed by the previous step whose
+// task is not listed cannot change now, but their next slot is stale:
+// stale_fixup copies their row (cur -> next) afterwards.  Same bits as the
+// full skip sweep (engine.hpp:173: an unmodified successor adds nothing).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_stream_u4(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+// Lists the task holding TOS row `row` (and every chunk of its hub).
+__device__ __noinline__ void list_task_of_row(const TaskScanArgs& a, uint64_t row) {
+  const uint64_t pos = row * 32;
+  uint32_t lo = 0, hi = a.num_wtasks - 1;  // last t with wtasks[t].tos <= pos
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo + 1) / 2;
+    if (a.wtasks[mid].tos <= pos) lo = mid; else hi = mid - 1;
+  }
+  HANF_DCHECK(a.wtasks[lo].tos <= pos && pos < a.wtasks[lo].tos + 32ull * a.wtasks[lo].trips);
+  uint32_t first = lo, count = 1;
+  if (a.wtasks[lo].nodes == 0) {  // hub chunk: every chunk of its hub
+    const uint32_t h = a.chunk_hub[a.wtasks[lo].item];
+    first = a.hub_first[h];
+    count = a.hub_count[h];
+  }
+  for (uint32_t t = first; t < first + count; ++t)
+    if (atomicExch(a.flags + t, 1u) == 0u) a.list[atomicAdd(a.count, 1u)] = t;
+}
+
+// Each warp streams 512-byte pieces (four TOS rows; lane l holds ids
+// 4l..4l+3, so eight lanes share a row), four pieces in flight.
+__global__ void __launch_bounds__(512) task_scan_kernel(const TaskScanArgs a) {
+  extern __shared__ uint64_t summ_sm[];
+  for (uint32_t i = threadIdx.x; i < a.summ_words; i += blockDim.x) summ_sm[i] = a.summ[i];
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t pieces = a.tos_words / 128;  // (tos_words is a multiple of 32)
+  const uint64_t tail_rows = (a.tos_words % 128) / 32;
+  constexpr uint32_t R = 4;
+  auto probe = [&](uint32_t w) -> bool {
+    bool hit = (summ_sm[w >> (a.summ_shift + 6)] >> ((w >> a.summ_shift) & 63)) & 1;
+    if (hit) hit = (__ldg(a.mod_cur + (w >> 6)) >> (w & 63)) & 1;
+    return hit;
+  };
+  for (uint64_t p0 = ((blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5) * R;
+       p0 < pieces; p0 += warps * R) {
+    uint4 q[R];
+#pragma unroll
+    for (uint32_t k = 0; k < R; ++k)
+      q[k] = p0 + k < pieces ? ld_stream_u4(a.tos + (p0 + k) * 128 + 4 * lane)
+                             : make_uint4(a.zero_row, a.zero_row, a.zero_row, a.zero_row);
+#pragma unroll
+    for (uint32_t k = 0; k < R; ++k) {
+      const bool hit = probe(q[k].x) | probe(q[k].y) | probe(q[k].z) | probe(q[k].w);
+      uint32_t rows = __ballot_sync(0xffffffffu, hit);  // lane group l / 8 = row
+      while (rows) {
+        const uint32_t l = __ffs(rows) - 1;
+        rows &= ~(0xffu << (l & ~7u));
+        if (lane == 0) list_task_of_row(a, (p0 + k) * 4 + l / 8);
+      }
+    }
+  }
+  // the last < 4 rows: warp 0
+  if (blockIdx.x == 0 && threadIdx.x < 32)
+    for (uint64_t r = pieces * 4; r < pieces * 4 + tail_rows; ++r) {
+      const bool hit = probe(a.tos[r * 32 + lane]);
+      if (__any_sync(0xffffffffu, hit) && lane == 0) list_task_of_row(a, r);
+    }
+}
+
+cudaError_t launch_task_scan(const TaskScanArgs& a, cudaStream_t s, uint64_t* launches) {
+  if (a.num_wtasks == 0) return cudaSuccess;
+  const size_t smem = sizeof(uint64_t) * a.summ_words;
+  task_scan_kernel<<<148 * 3, 512, smem, s>>>(a);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// next[v] = cur[v] for every row changed by the previous step (mod_cur)
+// that did not change now (mod_next): their next slot held generation t-2.
+__global__ void stale_fixup_kernel(const uint64_t* __restrict__ mod_cur,
+                                   const uint64_t* __restrict__ mod_next, uint64_t words,
+                                   uint64_t n, uint32_t pitch, const uint64_t* __restrict__ cur,
+                                   uint64_t* __restrict__ next) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < words;
+       w += stride) {
+    uint64_t bits = mod_cur[w] & ~mod_next[w];
+    while (bits) {
+      const uint64_t v = w * 64 + __ffsll(static_cast<long long>(bits)) - 1;
+      bits &= bits - 1;
+      if (v >= n) break;
+      for (uint32_t k = 0; k < pitch; ++k) next[v * pitch + k] = cur[v * pitch + k];
+    }
+  }
+}
+
+cudaError_t launch_stale_fixup(const uint64_t* mod_cur, const uint64_t* mod_next, uint64_t n,
+                               uint32_t pitch, const uint64_t* cur, uint64_t* next, cudaStream_t s,
+                               uint64_t* launches) {
+  const uint64_t words = (n + 63) / 64;
+  if (words == 0) return cudaSuccess;
+  uint64_t blocks = (words + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  stale_fixup_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(mod_cur, mod_next, words, n,
+                                                                    pitch, cur, next);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 // Peer-push exchange, end of a sharded compute: the shard's bitmap words
 // and block sums into every peer's arena, block sums into the local inbox
 // too (whole words: no clearing or atomics on the receiving side).

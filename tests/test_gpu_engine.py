@@ -660,3 +660,29 @@ def test_byte_layout_snapshot_restore(hanf, monkeypatch, tmp_path):
         e.reset()
         e.restore_counters(str(tmp_path / "p.hca"))
         assert np.array_equal(e.counters(), want)
+
+
+@pytest.mark.parametrize("env", [{"HANF_TASKSCAN": "1"},
+                                 {"HANF_TASKSCAN": "1", "HANF_LAYOUT": "packed"},
+                                 {"HANF_TASKSCAN": "1", "HANF_RELABEL": "1"},
+                                 {"HANF_TASKSCAN": "1", "HANF_RELABEL": "1", "HANF_LAYOUT": "packed"}])
+def test_task_scan_step(hanf, port, traces, monkeypatch, env):
+    """Mode 4 (one flat TOS scan lists the tasks in reach of a change, the
+    skip sweep runs on that list, stale rows outside it are copied) forced
+    on every skip step: every golden trace and lockstep runs with hubs,
+    relabelled rows and both counter stores stay bit-exact."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for case in traces:
+        g = graph_of(hanf, case["graph"])
+        with hanf.NfEngine(g, hanf.EngineConfig(**case["cfg"])) as e:
+            for step in case["steps"]:
+                r = e.step()
+                assert (float.hex(r.sum), r.modified) == (step["sum"], step["modified"]), step["t"]
+                assert sha(e.counters()) == step["counters_sha256"], step["t"]
+            e.reset()
+            est = e.run_to_stabilisation()
+            assert [float.hex(v) for v in est.values] == case["run_values"]
+    for g in (hanf.gen_rmat(13, 16, 0.57, 0.19, 0.19, 3, 5), hanf.gen_clique_path(2000, 3),
+              hanf.gen_uniform_random(5000, 3, 4)):
+        lockstep(hanf, port, g, bucket_bits=6, seed=99)
