@@ -663,8 +663,10 @@ hanf_status validate_config(const hanf_config* cfg) {
 }
 
 // Step kind for the current state: 0 dense sweep, 1 dense sweep skipping
-// unmodified successors, 2 worklist step (engine.hpp:210-224).  All three
-// produce the same bits; only the time differs.
+// unmodified successors, 2 worklist step (engine.hpp:210-224), 3 skip sweep
+// probing the modified-bitmap summary first, 4 task-scan step (the skip
+// sweep over the tasks a flat TOS scan lists).  All produce the same bits;
+// only the time differs.
 bool sparse_wanted(const hanf_engine* e) {
   // segmented engines' skip sweeps visit only the segments in reach of a
   // changed counter: they beat the worklist down to ~n/4096 changed
@@ -733,7 +735,7 @@ hanf_status ensure_sparse(hanf_engine* e) {
   return ensure_worklist_scratch(e);
 }
 
-// The worklist stages' scratch (shared by modes 2 and 4).
+// The worklist stages' scratch (step mode 2).
 hanf_status ensure_worklist_scratch(hanf_engine* e) {
   cudaStream_t s = e->stream;
   if (!e->sig) {

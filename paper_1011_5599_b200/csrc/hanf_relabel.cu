@@ -18,7 +18,7 @@
 //                               est[perm[o]] for the original-id blocks)
 // so N(t) is still summed over original-id blocks in the reference order.
 // Estimates in row order cost the finish a random gather; scattered to the
-// original slots (HANF_EST_SCATTER=1) they cost the union sweep
+// original slots (a round-1 variant, removed) they cost the union sweep
 // partial-sector writes.  Measured per dense step: BA 2^25 13.38 ms
 // (rows) vs 13.89 ms (scatter), R-MAT 26 12.84 vs 12.73 ms.
 //

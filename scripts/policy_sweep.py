@@ -1,5 +1,5 @@
 """Dev aid: union-sweep time of a dense iteration 1 under engine env
-variants (HANF_GATHER / HANF_HOT_MB ...), one graph.
+variants (HANF_LAYOUT / HANF_SLOTS_HOT ...), one graph.
     python scripts/policy_sweep.py CONFIG "ENV1;ENV2;..."   (ENV = K=V,K=V)"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
