@@ -686,3 +686,18 @@ def test_task_scan_step(hanf, port, traces, monkeypatch, env):
     for g in (hanf.gen_rmat(13, 16, 0.57, 0.19, 0.19, 3, 5), hanf.gen_clique_path(2000, 3),
               hanf.gen_uniform_random(5000, 3, 4)):
         lockstep(hanf, port, g, bucket_bits=6, seed=99)
+
+
+@pytest.mark.parametrize("hot", ["0", "16", "1040"])
+def test_relabel_line_slots(hanf, port, monkeypatch, hot):
+    """Relabelled rows of an odd pitch past a hot prefix take line-aligned
+    slots first (hanf_relabel.cu make_slots; on by default only past 2^22
+    rows, forced small here): every counter read back, N(t) and the
+    modified counts stay the reference's, for W = 5 and W = 7 rows."""
+    monkeypatch.setenv("HANF_LAYOUT", "packed")
+    monkeypatch.setenv("HANF_RELABEL", "1")
+    monkeypatch.setenv("HANF_SLOTS_HOT", hot)
+    for g in (hanf.gen_rmat(12, 16, 0.57, 0.19, 0.19, 3, 5), hanf.gen_clique_path(700, 4),
+              hanf.gen_uniform_random(3001, 4, 8)):
+        lockstep(hanf, port, g, bucket_bits=6, seed=17)
+        lockstep(hanf, port, g, bucket_bits=6, register_bits=7, seed=18)
