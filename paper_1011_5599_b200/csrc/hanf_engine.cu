@@ -197,6 +197,11 @@ namespace hanf_host_detail {
 void set_error(const std::string& s) { g_last_error = s; }
 }  // namespace hanf_host_detail
 
+namespace l2win {
+std::mutex mu;
+std::map<int, int> users;
+}  // namespace l2win
+
 struct hanf_engine {
   hanf_config cfg{};
   hanf_sketch_params params{};
@@ -264,6 +269,11 @@ struct hanf_engine {
   // unsharded relabelled engines, dense sweeps: no original-id dirty bits
   // (one random atomic per changed row); the commit re-sums every block
   bool skip_dirty = false;
+  // Relabelled engines: the hot row prefix of the generation a dense sweep
+  // gathers is an L2 access-policy window of persisting lines (0: none)
+  size_t l2_window = 0;
+  size_t l2_setaside = 0;  // the device's maximum persisting set-aside
+  bool l2_active = false;  // this engine holds the raised set-aside
   // hanf_shard_reduce ran for this step: the ranks re-summed one slice of
   // the original-id blocks each and published them; commit sums the inbox
   bool reduced = false;
@@ -383,6 +393,15 @@ struct hanf_engine {
     if (device >= 0) cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     phase("sync");
+    if (l2_active) {  // the persisting set-aside goes with the last windowed engine
+      std::lock_guard<std::mutex> lock(l2win::mu);
+      if (--l2win::users[device] == 0) {
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+      }
+      l2_active = false;
+      phase("l2");
+    }
     for (auto& a : graphs)
       for (auto& b : a)
         for (auto& c : b)
@@ -615,7 +634,46 @@ void batch_totals(hanf_engine* e, int parity, uint64_t* counts) {
   }
 }
 
+// L2 access-policy window of the dense sweeps (UnionArgs::l2_window_bytes)
+// for relabelled (DRAM-resident) engines: the hot row prefix, about 1.5x
+// the persisting set-aside (config 5: 54.5 -> 53.7 ms; windows near 128 MiB
+// fall off a cliff, 64 ms at 134 MB, so at most 120 MiB).  The set-aside
+// itself shrinks the L2 left to everything else (config 2's byte rows in
+// the same process: 0.135 -> 0.154 ms), so it is raised while a windowed
+// engine lives and dropped with the last one (refcounted per device, at
+// create before any upload and at destroy after the final sync, when the
+// device is idle).  HANF_L2_WINDOW_MB sets the size, 0 turns windows off.
+void choose_l2_window(hanf_engine* e) {
+  int maxp = 0, maxw = 0;
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, e->device);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, e->device);
+  if (maxp <= 0 || maxw <= 0 || !e->relabel || e->bytes) return;
+  size_t cap = std::min<size_t>({static_cast<size_t>(maxp) * 3 / 2, static_cast<size_t>(maxw),
+                                 120ull << 20});
+  if (const char* w = std::getenv("HANF_L2_WINDOW_MB"))
+    cap = std::min<size_t>(std::strtoull(w, nullptr, 10) << 20, static_cast<size_t>(maxw));
+  e->l2_window = std::min<size_t>(cap, sizeof(uint64_t) * (e->n + 1) * e->pitch);
+  e->l2_setaside = static_cast<size_t>(maxp);
+}
+
+// Raises the set-aside before the engine's first dense sweep, once its
+// create work has drained (the build's random perm lookups lose L2 to the
+// set-aside: +65 ms of config 5's create when raised there).  Outside any
+// graph capture.
+hanf_status activate_l2_window(hanf_engine* e) {
+  if (!e->l2_window || e->l2_active) return HANF_OK;
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  std::lock_guard<std::mutex> lock(l2win::mu);
+  if (l2win::users[e->device]++ == 0)
+    HANF_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, e->l2_setaside));
+  e->l2_active = true;
+  return HANF_OK;
+}
+
 hanf_status seed_all(hanf_engine* e) {
+  // a run starts with no persisting lines from an earlier one (the L2
+  // window of §5.1 marks lines of the generation a dense sweep gathers)
+  if (e->l2_active) HANF_CUDA(cudaCtxResetPersistingL2Cache());
   e->cur = 0;
   e->t = 0;
   e->stale_valid = false;
@@ -790,6 +848,7 @@ hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   a.orig_of = e->order;
   a.est_index = e->est_rows ? nullptr : e->order;
   a.dirty_next = e->skip_dirty ? nullptr : e->dirty[ng];
+  a.l2_window_bytes = 0;
   a.peers = peer_rows(e, ng);
   a.bytes = e->bytes ? 1 : 0;
   return a;
@@ -904,6 +963,7 @@ hanf_status compute_shard(hanf_engine* e) {
   // a counter gather per skipped arc: worth it once most counters settled
   const int mode = step_mode(e);
   a.check_mod = mode != 0 ? 1 : 0;
+  if (mode == 0 && e->l2_active) a.l2_window_bytes = e->l2_window;
   if (mode != 0 && e->seg_live) {
     HANF_CUDA(hanf::launch_segment_live(e->mod[g], e->tasks.seg_min, e->tasks.seg_max,
                                         e->tasks.num_segs, e->seg_live, e->stream, &e->launches));
@@ -1056,6 +1116,10 @@ hanf_status step_enqueue(hanf_engine* e) {
   const int mode = step_mode(e);
   if (mode == 2) {
     const hanf_status st = ensure_sparse(e);
+    if (st != HANF_OK) return st;
+  }
+  if (mode == 0) {
+    const hanf_status st = activate_l2_window(e);
     if (st != HANF_OK) return st;
   }
   if (mode == 4 && !e->scan_list) {  // (allocated outside any graph capture)
@@ -1269,6 +1333,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
 
   HANF_TRY(cudaSetDevice(cfg.device));
   configure_pool(cfg.device);
+  if (!(lo != 0 || hi != n) && K == 1) choose_l2_window(e);
   HANF_TRY(streams().get(cfg.device, &e->stream));
   cudaStream_t s = e->stream;
   // row n is an all-zero counter (the union kernels' padding target); 8

@@ -217,6 +217,7 @@ struct UnionArgs {
   const uint32_t* seg_live;        // skip sweeps over segmented tasks: segment s has work
   uint32_t seg_shift;              // (TaskBuild::seg_shift)
   uint32_t bytes;                  // byte-layout counter store (ByteLayout)
+  size_t l2_window_bytes;          // dense sweeps: hot prefix of cur kept in persisting L2
 };
 
 struct EstimateArgs {

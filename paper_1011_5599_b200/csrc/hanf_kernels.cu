@@ -738,10 +738,27 @@ cudaError_t union_launch_bytes(UnionArgs a, cudaStream_t s) {
   if (a.task_list && blocks > 148 * 4) blocks = 148 * 4;
   if (a.summ && blocks > 148 * 4) blocks = 148 * 4;  // persistent (mode 3)
   const size_t smem = a.summ ? sizeof(uint64_t) * a.summ_words : 0;
-  if (a.check_mod)
+  if (a.check_mod) {
     union_kernel_bytes<M, (MINB > 4 ? 4 : MINB), true><<<blocks, 256, smem, s>>>(a);
-  else
+  } else if (a.l2_window_bytes) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(blocks);
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = const_cast<uint64_t*>(a.cur);
+    at[0].val.accessPolicyWindow.num_bytes = a.l2_window_bytes;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, union_kernel_bytes<M, MINB, false>, a);
+  } else {
     union_kernel_bytes<M, MINB, false><<<blocks, 256, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -756,10 +773,30 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   const size_t smem = a.summ ? sizeof(uint64_t) * a.summ_words : 0;
   // the skip sweep carries the probe code: one CTA/SM fewer keeps it spill-free
   constexpr int SKIP_MINB = MINB > 4 ? 4 : MINB;
-  if (a.check_mod)
+  if (a.check_mod) {
     union_kernel<R, NREG, U, GM, V, SKIP_MINB, PF, true><<<blocks, 256, smem, s>>>(a);
-  else
+  } else if (a.l2_window_bytes) {
+    // the hot prefix of the generation being gathered as an L2 access
+    // policy window (persisting lines): a launch attribute, so CUDA graph
+    // captures keep it per node
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(blocks);
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = const_cast<uint64_t*>(a.cur);
+    at[0].val.accessPolicyWindow.num_bytes = a.l2_window_bytes;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, union_kernel<R, NREG, U, GM, V, MINB, PF, false>, a);
+  } else {
     union_kernel<R, NREG, U, GM, V, MINB, PF, false><<<blocks, 256, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

@@ -6,7 +6,7 @@ g = h.gen_rmat(28, 16, 0.57, 0.19, 0.19, 1, 7, device=0)
 g.pin()
 cfg = h.EngineConfig(bucket_bits=6, seed=42)
 h.estimate_nf(g, cfg)
-os.environ["HANF_PROFILE"] = "1"
+os.environ.setdefault("HANF_PROFILE", "0")
 for _ in range(2):
     t0 = time.perf_counter()
     e = h.NfEngine(g, cfg)
