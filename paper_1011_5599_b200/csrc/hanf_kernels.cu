@@ -730,6 +730,29 @@ KernelChoice choose(uint32_t r, uint32_t m) {
   }
 }
 
+// A dense sweep launched with the generation's hot row prefix as an L2
+// access-policy window (persisting hits, streaming misses; hanf_engine.cu
+// choose_l2_window): a launch attribute, so CUDA graph captures keep it.
+template <class K>
+cudaError_t launch_windowed(K kernel, uint32_t blocks, size_t smem, cudaStream_t s,
+                            const UnionArgs& a) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(blocks);
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow.base_ptr = const_cast<uint64_t*>(a.cur);
+  at[0].val.accessPolicyWindow.num_bytes = a.l2_window_bytes;
+  at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kernel, a);
+}
+
 template <int M, int MINB>
 cudaError_t union_launch_bytes(UnionArgs a, cudaStream_t s) {
   a.chunks = 1;
@@ -741,21 +764,7 @@ cudaError_t union_launch_bytes(UnionArgs a, cudaStream_t s) {
   if (a.check_mod) {
     union_kernel_bytes<M, (MINB > 4 ? 4 : MINB), true><<<blocks, 256, smem, s>>>(a);
   } else if (a.l2_window_bytes) {
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(blocks);
-    lc.blockDim = dim3(256);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow.base_ptr = const_cast<uint64_t*>(a.cur);
-    at[0].val.accessPolicyWindow.num_bytes = a.l2_window_bytes;
-    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    return cudaLaunchKernelEx(&lc, union_kernel_bytes<M, MINB, false>, a);
+    return launch_windowed(union_kernel_bytes<M, MINB, false>, blocks, smem, s, a);
   } else {
     union_kernel_bytes<M, MINB, false><<<blocks, 256, smem, s>>>(a);
   }
@@ -776,24 +785,7 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   if (a.check_mod) {
     union_kernel<R, NREG, U, GM, V, SKIP_MINB, PF, true><<<blocks, 256, smem, s>>>(a);
   } else if (a.l2_window_bytes) {
-    // the hot prefix of the generation being gathered as an L2 access
-    // policy window (persisting lines): a launch attribute, so CUDA graph
-    // captures keep it per node
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(blocks);
-    lc.blockDim = dim3(256);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow.base_ptr = const_cast<uint64_t*>(a.cur);
-    at[0].val.accessPolicyWindow.num_bytes = a.l2_window_bytes;
-    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    return cudaLaunchKernelEx(&lc, union_kernel<R, NREG, U, GM, V, MINB, PF, false>, a);
+    return launch_windowed(union_kernel<R, NREG, U, GM, V, MINB, PF, false>, blocks, smem, s, a);
   } else {
     union_kernel<R, NREG, U, GM, V, MINB, PF, false><<<blocks, 256, smem, s>>>(a);
   }
