@@ -963,7 +963,7 @@ hanf_status compute_shard(hanf_engine* e) {
   // a counter gather per skipped arc: worth it once most counters settled
   const int mode = step_mode(e);
   a.check_mod = mode != 0 ? 1 : 0;
-  if (mode == 0 && e->l2_active) a.l2_window_bytes = e->l2_window;
+  if (mode != 4 && e->l2_active) a.l2_window_bytes = e->l2_window;  // (skip sweeps too: -2%)
   if (mode != 0 && e->seg_live) {
     HANF_CUDA(hanf::launch_segment_live(e->mod[g], e->tasks.seg_min, e->tasks.seg_max,
                                         e->tasks.num_segs, e->seg_live, e->stream, &e->launches));

@@ -782,7 +782,9 @@ cudaError_t union_launch(UnionArgs a, uint32_t chunks, cudaStream_t s) {
   const size_t smem = a.summ ? sizeof(uint64_t) * a.summ_words : 0;
   // the skip sweep carries the probe code: one CTA/SM fewer keeps it spill-free
   constexpr int SKIP_MINB = MINB > 4 ? 4 : MINB;
-  if (a.check_mod) {
+  if (a.check_mod && a.l2_window_bytes) {
+    return launch_windowed(union_kernel<R, NREG, U, GM, V, SKIP_MINB, PF, true>, blocks, smem, s, a);
+  } else if (a.check_mod) {
     union_kernel<R, NREG, U, GM, V, SKIP_MINB, PF, true><<<blocks, 256, smem, s>>>(a);
   } else if (a.l2_window_bytes) {
     return launch_windowed(union_kernel<R, NREG, U, GM, V, MINB, PF, false>, blocks, smem, s, a);
