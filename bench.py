@@ -256,7 +256,7 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "arcs/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": cfg["name"], "n": n, "arcs": a, "log2m": cfg["b"],
                    "hll_seed": HLL_SEED, "step": STEP_DESC + "; a bounded node-slice sample "
                    "per step (see cpu_baseline.sample)",
