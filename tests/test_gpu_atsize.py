@@ -112,6 +112,21 @@ def test_config5_schedule_never_changes_a_bit(hanf, monkeypatch, relabel):
     _whole_run(hanf, g, fx, hanf.EngineConfig(bucket_bits=6, seed=42))
 
 
+def test_config5_device_sum_within_tolerance(hanf):
+    """Config 5 in the bench's mode (exact_sum=False: the deterministic
+    device tree; default schedule: relabelling, L2 window, task-scan tail):
+    N(t) within 1e-9 relative of the reference engine's, modified counts
+    identical, every iteration."""
+    fx = _fixture(5)
+    g = _cached_graph(hanf, 5)
+    est = hanf.estimate_nf(g, hanf.EngineConfig(bucket_bits=6, seed=42, exact_sum=False))
+    ref_vals = [float.fromhex(v) for v in fx["values"]]
+    mods = [rec["modified"] for rec in fx["iterations"]]
+    assert len(est.values) == len(ref_vals) and len(est.modified) >= len(ref_vals)
+    assert est.modified == mods[:len(est.modified)]
+    np.testing.assert_allclose(est.values, ref_vals, rtol=1e-9, atol=0)
+
+
 def test_config2_device_sum_within_tolerance(hanf):
     """exact_sum=False (the bench's deterministic device tree) against the
     reference's sequential N(t): within 1e-9 relative (north_star), with the
