@@ -241,3 +241,25 @@ def test_peer_push_config2_full_size(hanf, monkeypatch, relabel, world):
     assert values == single.values and mods == single.modified
     for c in counters:
         assert np.array_equal(c, ref)
+
+
+@pytest.mark.parametrize("world,hot", [(2, "0"), (4, "64")])
+def test_peer_push_relabelled_shards_line_slots(hanf, monkeypatch, world, hot):
+    """Relabelled shards with the reference packing (W = 5 rows) and the
+    line-aligned slot assignment inside every shard range forced small
+    (by default only past 2^22 / G rows): bit for bit against one engine."""
+    import dataclasses
+    monkeypatch.setenv("HANF_LAYOUT", "packed")
+    monkeypatch.setenv("HANF_RELABEL", "1")
+    monkeypatch.setenv("HANF_SLOTS_HOT", hot)
+    g = hanf.gen_rmat(14, 16, 0.57, 0.19, 0.19, 1, 7)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
+    values, mods, counters = _run_local(hanf, g, dataclasses.replace(cfg, shard_count=world),
+                                        world, True, relabelled=True, reduce=True)
+    monkeypatch.setenv("HANF_RELABEL", "0")
+    with hanf.NfEngine(g, cfg) as e:
+        single = e.run_to_stabilisation()
+        ref = e.counters()
+    assert values == single.values and mods == single.modified
+    for c in counters:
+        assert np.array_equal(c, ref)
