@@ -2,12 +2,19 @@
 //
 //   seed_kernel        NfEngine ctor seeding (engine.hpp:84-85, hll.hpp:104-117)
 //   union_kernel       the union sweep of NfEngine::step (engine.hpp:157-185,
-//                      PackedMax::max_into broadword.hpp:94-130), degree-binned
-//   hub_finalize       combines the partial maxima of split high-degree nodes
+//                      PackedMax::max_into broadword.hpp:94-130) over the
+//                      reference packing, degree-binned warp tasks
+//   union_kernel_bytes the same sweep over byte-register rows (ByteLayout),
+//                      a group of lanes per gathered counter
+//   finalize_hub       combines the partial maxima of split high-degree nodes
+//                      (the last chunk to finish, by ticket)
 //   estimate_kernel    counter_estimate + per-64-counter block sums
 //                      (hll.hpp:122-141, engine.hpp:100-113), dirty blocks only
-//   reduce kernels     deterministic total of the block sums and the modified
-//                      count (engine.hpp:115-117, 202-208)
+//   finish_kernel      block sums, deterministic total and modified count
+//                      (engine.hpp:109-117, 202-208), report to the host
+//   task_scan_kernel,  step mode 4: tasks in reach of a change from one TOS
+//   stale_fixup_kernel pass, stale rows outside them copied
+//   gather/scatter_rows read-back and restore (packing byte rows)
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -123,8 +130,9 @@ cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,
 // with the old counter, writes the next generation where it changed or
 // where next[v] is stale, estimates a changed counter from its registers
 // (single-chunk layouts) and sets the node's bit in mod_next.
-// Successor gathers: GMODE 0 = per-word loads, 1 = 16-byte windows,
-// 2 = 32-byte windows (fewer L1 wavefronts, more selects).
+// Successor gathers: GMODE 0 = per-word (or 16-byte vector) loads, 1 =
+// aligned 16-byte windows and a select on the word offset (odd W), 3 = one
+// aligned 256-bit load per 4-word row (W = 3 padded to 4).
 // ---------------------------------------------------------------------------
 template <class Lay>
 __device__ __forceinline__ void zero_limbs(uint32_t (&x)[Lay::kLimbs]) {
