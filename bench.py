@@ -632,8 +632,10 @@ def main():
                        "exchange": args.exchange if world > 1 else None,
                        "step": STEP_DESC + "; re-seed + L2 flush outside the timed region; "
                                "events bracket the step's device work",
-                       "l2": "flushed before every timed step (256 MiB write); inputs "
-                             "(counters %.1f GB, arcs %.1f GB) exceed the 126 MB L2"
+                       "l2": "flushed before every timed step (256 MiB write; persisting "
+                             "lines reset by the re-seed); inputs (counters %.1f GB, arcs "
+                             "%.1f GB) exceed the 126 MB L2; the sweep runs with its L2 "
+                             "access-policy window over the hot rows (DESIGN 5.1)"
                              % (2 * 8 * words * n / 1e9, 4 * a / 1e9),
                        "sum_mode": "device (deterministic tree)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
