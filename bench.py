@@ -516,6 +516,8 @@ def main():
                                                         flush, sharded, world)
     (sharded.reset if sharded is not None else engine.reset)()
     step_modified = (sharded.step() if sharded is not None else engine.step()).modified
+    # (rank's changed rows, row stores pushed to peers) of that dense step
+    push_stats = engine.shard_push_stats() if world > 1 else None
     phases = phase_timing(engine, dev, flush, max(3, min(args.steps, 10)), sharded)
     profile = run_profile(engine, n) if world == 1 else None
     if world > 1:
@@ -540,20 +542,28 @@ def main():
     traffic = ncu_traffic(args.config) if world == 1 else None
     nvlink = None
     if world > 1:
-        # peer-push bytes a rank sends per dense step: every row its sweep
-        # writes (the changed rows of its range; iteration 1 has no stale
-        # rows) to each of the G-1 peers, plus the estimates of relabelled
-        # rows and the published bitmap words and block sums
+        # peer-push bytes a rank sends per dense step, counted on the device
+        # after one more dense step (hanf_shard_push_stats): each changed row
+        # of its range goes to the peers that gather it (needed-rows filter;
+        # iteration 1 has no stale rows), relabelled shards add the row's
+        # estimate to every peer, and the publish kernel sends the bitmap
+        # words and block sums of the range
         lo, hi = sharded.ranges[rank]
         bufs = engine.device_buffers()
-        changed = step_modified * (hi - lo) / n
-        row = 8 * int(bufs.row_pitch) + (8 if bufs.relabelled else 0)
-        per_peer = changed * row + 2 * 8 * -(-(hi - lo) // 64)
-        sent = (world - 1) * per_peer
-        nvlink = {"bytes_per_gpu_per_step": sent, "achieved": sent / (total_ms / args.steps / 1e3) / 1e9,
-                  "peak": 900.0, "unit": "GB/s", "frac": sent / (total_ms / args.steps / 1e3) / 900e9,
-                  "note": "NVLink 5 per-direction peak; bytes from the step's modified count "
-                          "(rows changed in this rank's range x row bytes x (G-1) peers)"}
+        changed, pushed = push_stats
+        row = 8 * int(bufs.row_pitch)
+        est = 8 if bufs.relabelled else 0
+        publish = (world - 1) * 2 * 8 * -(-(hi - lo) // 64)
+        sent = pushed * row + changed * (world - 1) * est + publish
+        unfiltered = changed * (world - 1) * (row + est) + publish
+        step_s = total_ms / args.steps / 1e3
+        nvlink = {"bytes_per_gpu_per_step": sent, "achieved": sent / step_s / 1e9,
+                  "peak": 900.0, "unit": "GB/s", "frac": sent / step_s / 900e9,
+                  "rows_changed": changed, "row_stores_pushed": pushed,
+                  "bytes_without_filter": unfiltered,
+                  "note": "NVLink 5 per-direction peak; rank 0's pushes of the dense step "
+                          "counted on the device (changed rows x the peers that gather them "
+                          "x row bytes, + estimates and published bitmap/block sums)"}
     if sharded is not None:
         sharded.close()
     else:

@@ -272,7 +272,15 @@ hanf_status hanf_shard_commit(hanf_engine* engine, hanf_iteration_report* report
  * the ranks; hanf_shard_commit.  No counter bytes pass through a
  * collective; rows that did not change are never sent (the tail iterations
  * move kilobytes).  Block sums are double-buffered by generation, so a
- * rank may start step t+1 while a slower peer is still committing step t. */
+ * rank may start step t+1 while a slower peer is still committing step t.
+ * Needed-rows filter: each engine derives from its task-ordered successor
+ * array the rows its nodes can ever gather (n bits, in the arena); attach
+ * copies every peer's bits over this shard's range, and a written row is
+ * pushed only to the peers that gather it (about 44% of the pushes of a
+ * relabelled R-MAT at 8 shards).  A peer's copies of rows it never
+ * gathers go stale; hanf_read_counters / hanf_save_counters first copy
+ * every peer's own range of the current generation back (peer memory).
+ * HANF_PEER_NEED=0 (environment, read at create) pushes every row. */
 typedef struct {
   uint8_t ipc_handle[64];  /* cudaIpcMemHandle_t of the exchange arena */
   uint64_t arena_bytes;
@@ -305,6 +313,12 @@ hanf_status hanf_shard_reduce(hanf_engine* engine);
 /* Waits for this engine's enqueued device work (hanf_shard_compute's
  * pushes included): the step's barrier across the ranks comes after it. */
 hanf_status hanf_shard_wait(hanf_engine* engine);
+/* (new) Peer-push traffic of the last committed step, for reporting:
+ * *changed = rows of this shard's range the step changed, *pushed = the
+ * row stores those changes sent to peers (sum over peers of the changed
+ * rows each peer gathers; changed * peers without the needed-rows filter).
+ * Stale rows rewritten with them are pushed under the same filter. */
+hanf_status hanf_shard_push_stats(hanf_engine* engine, uint64_t* changed, uint64_t* pushed);
 /* Back to the collective exchange (closes opened IPC mappings). */
 hanf_status hanf_shard_detach(hanf_engine* engine);
 

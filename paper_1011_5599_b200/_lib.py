@@ -111,6 +111,7 @@ _SIGNATURES = {
     "hanf_shard_detach": [_P],
     "hanf_shard_wait": [_P],
     "hanf_shard_reduce": [_P],
+    "hanf_shard_push_stats": [_P, POINTER(c_uint64), POINTER(c_uint64)],
     "hanf_distance_distribution": [POINTER(c_double), c_uint64, POINTER(c_double),
                                    POINTER(c_double), POINTER(c_double)],
     "hanf_effective_diameter": [POINTER(c_double), c_uint64, c_double, c_int32,

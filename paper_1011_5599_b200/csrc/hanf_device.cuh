@@ -460,9 +460,21 @@ constexpr int kMaxPeers = 7;
 struct PeerRows {
   uint64_t* next[kMaxPeers];
   double* est[kMaxPeers];  // relabelled shards: estimates of changed rows too
+  // needed-rows filter: bit v of need[p] (word (v >> 6) - need_base) is set
+  // iff some node of peer p's range has row v as a successor, i.e. peer p
+  // can ever gather it; rows a peer never gathers are not pushed to it.
+  // null = push every written row (filter off)
+  const uint64_t* need[kMaxPeers];
+  uint32_t need_base;  // first bitmap word of this shard's range (lo >> 6)
   uint32_t count;
   uint32_t push_est;
 };
+
+// Does peer p gather row v (a row of this shard's range)?
+__device__ __forceinline__ bool peer_wants(const PeerRows& p, uint32_t i, uint32_t v) {
+  const uint64_t* nd = p.need[i];
+  return !nd || ((nd[(v >> 6) - p.need_base] >> (v & 63)) & 1);
+}
 
 struct EstimateParams {
   double alpha;

@@ -338,7 +338,17 @@ struct hanf_engine {
   // words and block sums (peer-push exchange, hanf_shard_attach).
   void* arena = nullptr;
   uint64_t arena_bytes = 0;
-  uint64_t arena_off[8] = {};                // cnt0 cnt1 mod0 mod1 inbox0 inbox1 est0 est1
+  uint64_t arena_off[9] = {};  // cnt0 cnt1 mod0 mod1 inbox0 inbox1 est0 est1 need
+  // peer-push needed-rows filter: arena region 8 is this shard's needed-rows
+  // bitmap (n bits, from its TOS); need_of holds, peer after peer, the
+  // peers' bits over this shard's range (need_words words each), copied at
+  // attach.  HANF_PEER_NEED=0 pushes every written row instead.
+  uint64_t* need = nullptr;
+  uint64_t* need_of = nullptr;
+  uint64_t need_words = 0;
+  bool need_filter = true;
+  uint64_t peer_lo[hanf::kMaxPeers] = {};
+  uint64_t peer_hi[hanf::kMaxPeers] = {};
   // relabelled shards: estimates per generation (a fast peer's step t+1
   // must not overwrite what this rank's commit t re-sums); est = est_gen[cur]
   double* est_gen[2] = {nullptr, nullptr};
@@ -358,6 +368,8 @@ struct hanf_engine {
       peer_base[p] = nullptr;
       peer_ipc[p] = false;
     }
+    if (need_of) cudaFree(need_of);
+    need_of = nullptr;
     npeers = 0;
     attached = false;
   }
@@ -816,7 +828,9 @@ hanf::PeerRows peer_rows(const hanf_engine* e, int ng) {
   for (uint32_t i = 0; i < p.count; ++i) {
     p.next[i] = reinterpret_cast<uint64_t*>(e->peer_base[i] + e->arena_off[ng]);
     p.est[i] = reinterpret_cast<double*>(e->peer_base[i] + e->arena_off[6 + ng]);
+    p.need[i] = e->need_of ? e->need_of + i * e->need_words : nullptr;
   }
+  p.need_base = static_cast<uint32_t>(e->lo >> 6);
   return p;
 }
 
@@ -1270,6 +1284,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   e->pitch = hanf::row_pitch(params.register_bits, params.registers, params.words_per_counter,
                              e->bytes);
   if (const char* fs = std::getenv("HANF_SUMMARY")) e->force_summary = fs[0] == '1';
+  if (const char* pn = std::getenv("HANF_PEER_NEED")) e->need_filter = pn[0] != '0';
   if (const char* ts = std::getenv("HANF_TASKSCAN")) e->task_scan = ts[0] == '1' ? 1 : (ts[0] == '0' ? 0 : -1);
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
   if (lo != 0 || hi != n) e->use_graphs = false;  // sharded steps are split around the exchange
@@ -1343,11 +1358,11 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   if (sharded) {
     // the exchange arena (see hanf_engine::arena): same offsets on every rank
     auto al = [](uint64_t bytes) { return (bytes + 255) & ~255ull; };
-    const uint64_t sizes[8] = {nw * 8, nw * 8, (e->blocks + 1) * 8, (e->blocks + 1) * 8,
+    const uint64_t sizes[9] = {nw * 8, nw * 8, (e->blocks + 1) * 8, (e->blocks + 1) * 8,
                                e->blocks * 8, e->blocks * 8, n * 8,
-                               e->shard_relabel ? n * 8 : 8};
+                               e->shard_relabel ? n * 8 : 8, (e->blocks + 1) * 8};
     uint64_t off = 0;
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 9; ++i) {
       e->arena_off[i] = off;
       off += al(sizes[i] ? sizes[i] : 8);
     }
@@ -1360,6 +1375,7 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       e->inbox[i] = reinterpret_cast<double*>(base + e->arena_off[4 + i]);
     }
     e->est = reinterpret_cast<double*>(base + e->arena_off[6]);
+    e->need = reinterpret_cast<uint64_t*>(base + e->arena_off[8]);
     if (e->shard_relabel) {
       e->est_gen[0] = e->est;
       e->est_gen[1] = reinterpret_cast<double*>(base + e->arena_off[7]);
@@ -1588,6 +1604,9 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       HANF_TRY(palloc(&e->seg_live, e->tasks.num_segs, s));
     phase("build");
     HANF_TRY(palloc(&e->partials, static_cast<size_t>(e->tasks.num_chunks) * e->pitch, s));
+    if (e->need)  // peer-push filter: the rows this shard gathers (read at the peers' attach)
+      HANF_TRY(hanf::launch_need_rows(e->tasks.tos, e->tasks.tos_words, n, e->need, s,
+                                      &e->launches));
   }
 #undef HANF_TRY
   *out = e;
@@ -1941,6 +1960,8 @@ hanf_status hanf_shard_export(hanf_engine* e, hanf_shard_peer* out) {
   out->arena_bytes = e->arena_bytes;
   if (!e->arena) return HANF_OK;  // a one-shard engine (all nodes): nothing to map
   HANF_CUDA(cudaSetDevice(e->device));
+  // the needed-rows bitmap the peers copy at attach is complete
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
   cudaIpcMemHandle_t h;
   HANF_CUDA(cudaIpcGetMemHandle(&h, e->arena));
   static_assert(sizeof(h) == sizeof(out->ipc_handle), "cudaIpcMemHandle_t size");
@@ -1981,6 +2002,45 @@ hanf_status check_peers(const hanf_engine* e, const hanf_shard_peer* peers, uint
 
 }  // namespace
 
+namespace {
+
+// Peer-push filter, at attach: copies every peer's needed-rows bits over
+// this shard's range (words [lo/64, ceil(hi/64)) of the peer's arena
+// region 8) into need_of.  The peers' bitmaps are complete: export and
+// attach_local synchronise the peer's stream first.
+hanf_status load_peer_need(hanf_engine* e) {
+  if (!e->need_filter || e->npeers == 0 || e->hi <= e->lo) return HANF_OK;
+  const uint64_t w0 = e->lo >> 6, w1 = (e->hi + 63) >> 6;
+  e->need_words = w1 - w0;
+  HANF_CUDA(cudaMalloc(&e->need_of, sizeof(uint64_t) * e->npeers * e->need_words));
+  for (uint32_t i = 0; i < e->npeers; ++i)
+    HANF_CUDA(cudaMemcpyAsync(e->need_of + i * e->need_words,
+                              e->peer_base[i] + e->arena_off[8] + sizeof(uint64_t) * w0,
+                              sizeof(uint64_t) * e->need_words, cudaMemcpyDefault, e->stream));
+  HANF_CUDA(cudaStreamSynchronize(e->stream));
+  return HANF_OK;
+}
+
+}  // namespace
+
+// Filtered peer-push leaves this shard's copies of peer rows it never
+// gathers stale; a read-back first copies every peer's own range of the
+// current generation from the peer's arena (peer memory, stream-ordered).
+// Rows this shard gathers are equal on both sides already.
+static hanf_status pull_peer_rows(hanf_engine* e) {
+  if (!e->attached || !e->need_of) return HANF_OK;
+  const int g = e->cur;
+  for (uint32_t i = 0; i < e->npeers; ++i) {
+    const uint64_t lo = e->peer_lo[i], hi = e->peer_hi[i];
+    if (hi <= lo) continue;
+    HANF_CUDA(cudaMemcpyAsync(e->cnt[g] + lo * e->pitch,
+                              e->peer_base[i] + e->arena_off[g] + sizeof(uint64_t) * lo * e->pitch,
+                              sizeof(uint64_t) * (hi - lo) * e->pitch, cudaMemcpyDefault,
+                              e->stream));
+  }
+  return HANF_OK;
+}
+
 hanf_status hanf_shard_attach(hanf_engine* e, const hanf_shard_peer* peers, uint32_t count,
                               uint32_t self) {
   if (!e || !peers) return fail(HANF_INVALID_ARGUMENT, "null argument");
@@ -2002,7 +2062,14 @@ hanf_status hanf_shard_attach(hanf_engine* e, const hanf_shard_peer* peers, uint
     }
     e->peer_base[e->npeers] = static_cast<uint8_t*>(ptr);
     e->peer_ipc[e->npeers] = true;
+    e->peer_lo[e->npeers] = peers[p].shard_begin;
+    e->peer_hi[e->npeers] = peers[p].shard_end;
     ++e->npeers;
+  }
+  st = load_peer_need(e);
+  if (st != HANF_OK) {
+    e->detach_peers();
+    return st;
   }
   e->attached = true;
   return HANF_OK;
@@ -2045,7 +2112,18 @@ hanf_status hanf_shard_attach_local(hanf_engine* e, hanf_engine* const* peers, u
     }
     e->peer_base[e->npeers] = static_cast<uint8_t*>(peers[p]->arena);
     e->peer_ipc[e->npeers] = false;
+    e->peer_lo[e->npeers] = peers[p]->lo;
+    e->peer_hi[e->npeers] = peers[p]->hi;
     ++e->npeers;
+    // the needed-rows bitmap load_peer_need copies is complete
+    HANF_CUDA(cudaSetDevice(peers[p]->device));
+    HANF_CUDA(cudaStreamSynchronize(peers[p]->stream));
+    HANF_CUDA(cudaSetDevice(e->device));
+  }
+  st = load_peer_need(e);
+  if (st != HANF_OK) {
+    e->detach_peers();
+    return st;
   }
   e->attached = true;
   return HANF_OK;
@@ -2091,6 +2169,35 @@ hanf_status hanf_shard_reduce(hanf_engine* e) {
   }
   p.peer_sums[e->npeers] = e->inbox[ng];
   HANF_CUDA(hanf::launch_publish(p, e->stream, &e->launches));
+  return HANF_OK;
+}
+
+hanf_status hanf_shard_push_stats(hanf_engine* e, uint64_t* changed, uint64_t* pushed) {
+  if (!e || !changed || !pushed) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  if (!e->parts.empty()) return fail(HANF_INVALID_ARGUMENT, "not a shard engine");
+  *changed = *pushed = 0;
+  if (e->hi <= e->lo) return HANF_OK;
+  HANF_CUDA(cudaSetDevice(e->device));
+  const uint64_t w0 = e->lo >> 6, words = ((e->hi + 63) >> 6) - w0;
+  const uint64_t* rows = e->mod[e->cur] + w0;  // the last step's modified bits
+  uint64_t* d = nullptr;  // [0] pushed, [1] changed
+  uint64_t* d_ones = nullptr;
+  HANF_CUDA(palloc(&d, 2, e->stream));
+  cudaError_t ce = palloc(&d_ones, words, e->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(d_ones, 0xff, sizeof(uint64_t) * words, e->stream);
+  if (ce == cudaSuccess)  // changed rows: popcount against one all-ones "peer"
+    ce = hanf::launch_count_pushes(rows, d_ones, words, 1, d + 1, e->stream, &e->launches);
+  if (ce == cudaSuccess && e->need_of)
+    ce = hanf::launch_count_pushes(rows, e->need_of, words, e->npeers, d, e->stream, &e->launches);
+  uint64_t h[2] = {0, 0};
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, e->stream);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->stream);
+  pfree(d, e->stream);
+  if (d_ones) pfree(d_ones, e->stream);
+  HANF_CUDA(ce);
+  *changed = h[1];
+  *pushed = e->need_of ? h[0] : h[1] * (e->attached ? e->npeers : 0);
   return HANF_OK;
 }
 
@@ -2379,6 +2486,10 @@ hanf_status hanf_read_counters(hanf_engine* e, uint64_t first, uint64_t count, u
   if (count == 0) return HANF_OK;
   if (!dst) return fail(HANF_INVALID_ARGUMENT, "null destination");
   HANF_CUDA(cudaSetDevice(e->device));
+  {
+    const hanf_status ps = pull_peer_rows(e);
+    if (ps != HANF_OK) return ps;
+  }
   if (e->relabel || e->bytes) {
     // counter of original id first + i lives in row perm[first + i]; byte
     // rows are packed into the reference layout on the way

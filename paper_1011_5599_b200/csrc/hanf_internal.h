@@ -262,6 +262,12 @@ cudaError_t launch_task_scan(const TaskScanArgs& a, cudaStream_t s, uint64_t* la
 cudaError_t launch_stale_fixup(const uint64_t* mod_cur, const uint64_t* mod_next, uint64_t n,
                                uint32_t pitch, const uint64_t* cur, uint64_t* next, cudaStream_t s,
                                uint64_t* launches);
+// Peer-push needed-rows filter: the shard's needed-rows bitmap from its TOS
+// (zeroed first), and sum over peers of popcount(rows & need[p]).
+cudaError_t launch_need_rows(const uint32_t* tos, uint64_t count, uint64_t n, uint64_t* need,
+                             cudaStream_t s, uint64_t* launches);
+cudaError_t launch_count_pushes(const uint64_t* rows, const uint64_t* need, uint64_t words,
+                                uint32_t peers, uint64_t* out, cudaStream_t s, uint64_t* launches);
 
 // Launchers (hanf_kernels.cu).  All are stream-ordered and asynchronous.
 cudaError_t launch_seed(uint64_t* a, uint64_t* b, uint64_t* mod, uint64_t n,

@@ -277,7 +277,7 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
         const uint64_t off = static_cast<uint64_t>(v) * words + woff;
         store_chunk<Lay, kVec16>(args.next + off, acc);
         for (uint32_t p = 0; p < args.peers.count; ++p)
-          store_chunk<Lay, kVec16>(args.peers.next[p] + off, acc);
+          if (peer_wants(args.peers, p, v)) store_chunk<Lay, kVec16>(args.peers.next[p] + off, acc);
       }
       if (args.est && (changed || (stale && args.peers.push_est)))
         push_estimate(args, v, estimate_limbs<Lay>(acc, args.ep));
@@ -327,6 +327,7 @@ __device__ __forceinline__ void node_commit(const UnionArgs& args, const WarpTas
         store_chunk<Lay, kVec16>(args.next + off, acc);
       // sharded peer-push: the same row into every peer's next generation
       for (uint32_t p = 0; p < args.peers.count; ++p) {
+        if (!peer_wants(args.peers, p, v)) continue;
         if (args.chunks == 1)
           store_counter<Lay>(args.peers.next[p] + off, acc);
         else
@@ -535,7 +536,7 @@ __device__ __forceinline__ ByteCommit commit_bytes(const UnionArgs& args, const 
     const uint64_t off = static_cast<uint64_t>(o.v) * Q + k;
     reinterpret_cast<uint4*>(args.next)[off] = nx;
     for (uint32_t p = 0; p < args.peers.count; ++p)
-      reinterpret_cast<uint4*>(args.peers.next[p])[off] = nx;
+      if (peer_wants(args.peers, p, o.v)) reinterpret_cast<uint4*>(args.peers.next[p])[off] = nx;
   }
   o.want = args.est && (o.changed || (act && st && args.peers.push_est));
   if (__any_sync(0xffffffffu, o.want)) {
@@ -1233,6 +1234,64 @@ cudaError_t launch_stale_fixup(const uint64_t* mod_cur, const uint64_t* mod_next
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   stale_fixup_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(mod_cur, mod_next, words, n,
                                                                     pitch, cur, next);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// Needed-rows bitmap of a shard (peer-push filter): bit v is set iff row v
+// is a successor id in the shard's TOS, i.e. one of its nodes can gather
+// row v (hub chunks and the worklist step read the same successors).
+// Padding ids (>= n) are skipped; a bit already set costs a read, not an
+// atomic.
+__global__ void need_rows_kernel(const uint32_t* __restrict__ tos, uint64_t count, uint32_t n,
+                                 unsigned long long* __restrict__ need) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += stride) {
+    const uint32_t v = tos[i];
+    if (v >= n) continue;
+    const unsigned long long bit = 1ull << (v & 63);
+    if (!(need[v >> 6] & bit)) atomicOr(need + (v >> 6), bit);
+  }
+}
+
+cudaError_t launch_need_rows(const uint32_t* tos, uint64_t count, uint64_t n, uint64_t* need,
+                             cudaStream_t s, uint64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(need, 0, sizeof(uint64_t) * ((n + 63) / 64), s);
+  if (e != cudaSuccess || count == 0) return e;
+  uint64_t blocks = (count + 255) / 256;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  need_rows_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
+      tos, count, static_cast<uint32_t>(n), reinterpret_cast<unsigned long long*>(need));
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// Rows of bitmap `rows` (words [0, words)) that peer p needs, summed over
+// the peers: need[p] holds `words` words, peer after peer (the peer-push
+// filter's copies); the total goes to *out (zeroed by the caller).
+__global__ void count_pushes_kernel(const uint64_t* __restrict__ rows,
+                                    const uint64_t* __restrict__ need, uint64_t words,
+                                    uint32_t peers, unsigned long long* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  unsigned long long c = 0;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < words;
+       w += stride) {
+    const uint64_t r = rows[w];
+    for (uint32_t p = 0; p < peers; ++p) c += __popcll(r & need[p * words + w]);
+  }
+  for (int off = 16; off >= 1; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+cudaError_t launch_count_pushes(const uint64_t* rows, const uint64_t* need, uint64_t words,
+                                uint32_t peers, uint64_t* out, cudaStream_t s, uint64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
+  if (e != cudaSuccess || words == 0) return e;
+  uint64_t blocks = (words + 255) / 256;
+  if (blocks > 148ull * 8) blocks = 148ull * 8;
+  count_pushes_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(
+      rows, need, words, peers, reinterpret_cast<unsigned long long*>(out));
   ++*launches;
   return cudaGetLastError();
 }

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256) sparse_union_kernel(const SparseArgs a) {
         const uint64_t off = static_cast<uint64_t>(v) * words;
         store_chunk<Lay, kVec16>(a.next + off, acc);
         for (uint32_t p = 0; p < a.peers.count; ++p)  // sharded peer-push
-          store_chunk<Lay, kVec16>(a.peers.next[p] + off, acc);
+          if (peer_wants(a.peers, p, v)) store_chunk<Lay, kVec16>(a.peers.next[p] + off, acc);
       }
       if (changed) {
         a.est[a.est_index ? a.est_index[v] : v] = estimate_limbs<Lay>(acc, a.ep);

@@ -335,6 +335,13 @@ class NfEngine:
         the block sums each (between two barriers); a no-op otherwise."""
         check(lib().hanf_shard_reduce(self._h))
 
+    def shard_push_stats(self):
+        """hanf_shard_push_stats: (rows of this shard the last committed step
+        changed, row stores those changes pushed to peers)."""
+        changed, pushed = c_uint64(), c_uint64()
+        check(lib().hanf_shard_push_stats(self._h, ctypes.byref(changed), ctypes.byref(pushed)))
+        return int(changed.value), int(pushed.value)
+
     def shard_commit(self) -> IterationReport:
         r = _lib.IterationReportC()
         check(lib().hanf_shard_commit(self._h, ctypes.byref(r)))

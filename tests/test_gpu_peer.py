@@ -126,6 +126,64 @@ def test_peer_push_relabelled_shards(hanf, monkeypatch, b, world, skew, reduce):
         assert np.array_equal(c, ref)
 
 
+@pytest.mark.parametrize("need", ["1", "0"])
+def test_peer_push_needed_rows_filter(hanf, monkeypatch, need):
+    """Needed-rows filter of the peer push (hanf_shard_push_stats): after
+    every step, each shard's pushed row stores equal the host count of its
+    changed rows that each peer gathers (successors of the peer's nodes),
+    and changed * peers with HANF_PEER_NEED=0.  The shards' changed rows
+    are exactly the rows the single engine changed, and read-back (which
+    pulls the peers' ranges) stays bit-exact."""
+    import torch
+    from paper_1011_5599_b200.sharded import LocalCudaShard, shard_ranges
+    monkeypatch.setenv("HANF_PEER_NEED", need)
+    g = hanf.gen_rmat(13, 8, 0.57, 0.19, 0.19, 1, 7)
+    n, off, arcs = g.num_nodes(), g.offsets().astype(np.int64), g.arcs()
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
+    world = 3
+    ranges = shard_ranges(n, world)
+    needs = []
+    for lo, hi in ranges:
+        m = np.zeros(n, bool)
+        m[arcs[off[lo]:off[hi]]] = True
+        needs.append(m)
+    dev = torch.device("cuda", 0)
+    shards = [LocalCudaShard(g, cfg, lo, hi, dev) for lo, hi in ranges]
+    engines = [sh.engine for sh in shards]
+    for k, e in enumerate(engines):
+        e.shard_attach_local(engines, k)
+    total_pushed = total_all = 0
+    with hanf.NfEngine(g, cfg) as single:
+        prev = single.counters().reshape(n, -1)
+        while True:
+            for sh in shards:
+                sh.shard_compute()
+                sh.wait_compute()
+            reps = [sh.shard_commit() for sh in shards]
+            rep = single.step()
+            assert all(r.sum == rep.sum and r.modified == rep.modified for r in reps)
+            cur = single.counters().reshape(n, -1)
+            changed = np.any(cur != prev, axis=1)
+            prev = cur
+            for k, ((lo, hi), e) in enumerate(zip(ranges, engines)):
+                c, pushed = e.shard_push_stats()
+                mine = changed[lo:hi]
+                assert c == int(mine.sum())
+                want = sum(int((mine & needs[p][lo:hi]).sum()) for p in range(world) if p != k)
+                assert pushed == (want if need == "1" else c * (world - 1))
+                total_pushed += want
+                total_all += c * (world - 1)
+            for e in engines:
+                assert np.array_equal(e.counters().reshape(n, -1), cur)
+            if rep.modified == 0:
+                break
+    assert total_pushed < total_all  # the filter has something to drop on R-MAT
+    for sh in shards:
+        sh.shard_detach()
+    for sh in shards:
+        sh.close()
+
+
 def test_relabelled_shard_needs_peer_push(hanf, monkeypatch):
     import dataclasses
     import torch
