@@ -371,12 +371,16 @@ def run_profile(engine, n):
     engine.reset()
     engine.run_to_stabilisation()  # untimed: first launches of the tail kernels
     engine.reset()
-    prof, prev = [], n
+    prof, prev, first = [], None, None
     while True:
         engine.set_timing(True)
         rep = engine.step()
         t = engine.timing()
-        kind = "dense" if 2 * prev >= n else "tail (worklist or skip sweep)"
+        # step 1 changes every node with a successor; a step is dense while
+        # the previous one changed at least a quarter as many counters
+        first = rep.modified if first is None else first
+        kind = ("dense" if prev is None or 4 * prev >= first
+                else "tail (skip sweep, task scan or worklist)")
         prof.append({"t": len(prof) + 1, "modified": rep.modified, "kind": kind,
                      "sweep_ms": round(t["union_ms"], 4),
                      "finish_ms": round(t["reduce_ms"] + t["estimate_ms"], 4)})

@@ -219,6 +219,13 @@ const char* hanf_last_error(void);
 hanf_status hanf_stream(const hanf_engine* engine, void** stream);
 /* Kernels launched by this engine since creation. */
 hanf_status hanf_launch_count(const hanf_engine* engine, uint64_t* launches);
+/* Source-blocked dense sweeps (an engine-internal schedule of
+ * NfEngine::step's union loop, engine.hpp:157-185; results are unchanged):
+ * the number of (successor segment, source) items and the arcs they cover,
+ * 0 / 0 while the engine sweeps every arc from its own node's list.  Built
+ * at the first hanf_reset / hanf_reseed of a large relabelled engine
+ * (HANF_BLOCK=1: at create, 2: at the first reset whatever the size, 0: never). */
+hanf_status hanf_block_stats(const hanf_engine* engine, uint64_t* items, uint64_t* arcs);
 /* Phase timing with CUDA events on the engine stream (off by default):
  * union sweep (union + hub kernels), estimates + block sums, totals.
  * Accumulated over the steps since the last hanf_set_timing(e, 1). */

@@ -97,6 +97,7 @@ _SIGNATURES = {
     "hanf_num_nodes": [_P, POINTER(c_uint64)],
     "hanf_stream": [_P, POINTER(_P)],
     "hanf_launch_count": [_P, POINTER(c_uint64)],
+    "hanf_block_stats": [_P, POINTER(c_uint64), POINTER(c_uint64)],
     "hanf_device_buffers": [_P, POINTER(BuffersC)],
     "hanf_set_timing": [_P, c_int32],
     "hanf_timing": [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double),

@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256)
 fill_tos_kernel(const CsrView g, const uint32_t* __restrict__ order,
                 const uint64_t* __restrict__ chunk_begin, const uint32_t* __restrict__ chunk_node,
                 const WarpTask* __restrict__ tasks, uint64_t num_tasks, uint32_t n,
-                uint32_t* __restrict__ tos, int* __restrict__ bad) {
+                uint32_t limit, uint32_t* __restrict__ tos, int* __restrict__ bad) {
   const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   bool out_of_range = false;
@@ -301,8 +301,8 @@ fill_tos_kernel(const CsrView g, const uint32_t* __restrict__ order,
       uint32_t id = n;
       if (k < d) {
         id = g.id(s + k);
-        out_of_range |= id >= n;
-        if (id >= n) id = n;  // (a pipelined sweep may run before the check)
+        out_of_range |= id >= limit;
+        if (id >= limit) id = n;  // (a pipelined sweep may run before the check)
       }
       dst[32 * i + lane] = id;
     }
@@ -368,8 +368,9 @@ cudaError_t write_to_device(void* dst, const void* src, size_t bytes, cudaStream
 cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
                                uint32_t seg_shift, cudaStream_t s, cudaEvent_t succ_ready,
                                TaskBuild* out, int* bad_input, uint64_t* launches,
-                               bool seg_bounds, bool class_major) {
+                               bool seg_bounds, bool class_major, uint64_t id_limit) {
   *out = TaskBuild{};
+  if (id_limit == 0) id_limit = n;
   if (seg_shift < 32 && hi > lo) {
     out->seg_shift = seg_shift;
     out->num_segs = static_cast<uint32_t>(((hi - 1) >> seg_shift) + 1);
@@ -540,7 +541,7 @@ cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint6
   if (num_tasks) {
     fill_tos_kernel<<<grid(num_tasks * 32), threads, 0, s>>>(
         g, o.order, chunk_begin, o.chunk_node, o.wtasks, num_tasks,
-        static_cast<uint32_t>(n), o.tos, d_bad);
+        static_cast<uint32_t>(n), static_cast<uint32_t>(id_limit), o.tos, d_bad);
     ++*launches;
     HANF_BUILD_TRY(cudaGetLastError());
   }

@@ -329,6 +329,21 @@ struct hanf_engine {
   uint64_t summ_bits = 0;
   bool use_graphs = true;
   uint32_t* seg_live = nullptr;  // skip sweeps over segmented tasks (TaskBuild::seg_shift)
+  // Source-blocked dense sweeps (hanf_block.cu; unsharded relabelled engines
+  // with the packed store).  block_mode: 1 = built at create (HANF_BLOCK=1),
+  // 0 = never, -1 = built at the first re-seed of a large engine (multi-run
+  // use amortises the build; a one-shot run never pays for it).  Item k is
+  // row n + 1 + k of both counter generations.
+  int block_mode = -1;
+  bool block_ready = false;
+  bool block_tried = false;
+  uint64_t block_items = 0;
+  uint64_t block_arcs = 0;
+  hanf::TaskBuild item_tasks;     // first sweep of a dense step: the items
+  hanf::TaskBuild block_tasks;    // main sweep: the sources' lists name item rows
+  uint64_t* item_partials = nullptr;
+  uint64_t* block_partials = nullptr;
+  uint64_t* item_bits = nullptr;  // the item sweep's changed-row bitmap (never read)
   // mod[1 - cur] is known to be all zero (seeding, or the last commit's
   // finish_kernel cleared it): the step's memset is skipped
   bool next_bits_clear = false;
@@ -469,6 +484,11 @@ struct hanf_engine {
       pfree(lens, stream);
       pfree(seg_live, stream);
       pfree(dirty_derived, stream);
+      pfree(item_partials, stream);
+      pfree(block_partials, stream);
+      pfree(item_bits, stream);
+      hanf::free_tasks_device(&item_tasks, stream);
+      hanf::free_tasks_device(&block_tasks, stream);
       hanf::free_tasks_device(&tasks, stream);
       if (cudaStreamSynchronize(stream) == cudaSuccess)
         streams().put(device, stream);
@@ -682,6 +702,16 @@ hanf_status activate_l2_window(hanf_engine* e) {
   return HANF_OK;
 }
 
+// Item rows (source-blocked dense sweeps) hold maxima of the running
+// counters: a new run, or restored counters, start them from zero.
+hanf_status clear_item_rows(hanf_engine* e) {
+  if (!e->block_ready) return HANF_OK;
+  for (int i = 0; i < 2; ++i)
+    HANF_CUDA(cudaMemsetAsync(e->cnt[i] + (e->n + 1) * e->pitch, 0,
+                              sizeof(uint64_t) * (e->block_items * e->pitch + 8), e->stream));
+  return HANF_OK;
+}
+
 hanf_status seed_all(hanf_engine* e) {
   // a run starts with no persisting lines from an earlier one (the L2
   // window of §5.1 marks lines of the generation a dense sweep gathers)
@@ -690,6 +720,10 @@ hanf_status seed_all(hanf_engine* e) {
   e->t = 0;
   e->stale_valid = false;
   e->systolic = false;
+  {
+    const hanf_status bs = clear_item_rows(e);
+    if (bs != HANF_OK) return bs;
+  }
   HANF_CUDA(hanf::launch_seed(e->cnt[0], e->cnt[1], e->mod[0], e->n, 0, e->n,
                               e->params.bucket_bits, e->params.register_bits,
                               e->params.words_per_counter, static_cast<uint32_t>(e->pitch),
@@ -834,12 +868,28 @@ hanf::PeerRows peer_rows(const hanf_engine* e, int ng) {
   return p;
 }
 
+// The sweep's work arrays from another task build (source-blocked sweeps).
+void use_tasks(hanf::UnionArgs* a, const hanf::TaskBuild& t, uint64_t* partials) {
+  a->tos = t.tos;
+  a->wtasks = t.wtasks;
+  a->num_wtasks = t.num_wtasks;
+  a->order = t.order;
+  a->hub_node = t.chunk_node;
+  a->partials = partials;
+  a->chunk_hub = t.chunk_hub;
+  a->hub_nodes = t.hub_nodes;
+  a->hub_first = t.hub_first;
+  a->hub_count = t.hub_count;
+  a->hub_ticket = t.hub_ticket;
+}
+
 hanf::UnionArgs union_args(const hanf_engine* e, int g, int ng) {
   hanf::UnionArgs a{};
   a.tos = e->tasks.tos;
   a.wtasks = e->tasks.wtasks;
   a.num_wtasks = e->tasks.num_wtasks;
   a.zero_row = static_cast<uint32_t>(e->n);
+  a.row_limit = static_cast<uint32_t>(e->n + 1 + e->block_items);
   const bool fused = hanf::fused_estimates(e->params.register_bits, e->params.registers);
   a.est = fused ? (e->shard_relabel ? e->est_gen[ng] : e->est) : nullptr;
   a.ep = hanf::EstimateParams{e->params.alpha, static_cast<double>(e->params.registers),
@@ -1016,6 +1066,26 @@ hanf_status compute_shard(hanf_engine* e) {
     a.task_count = e->scan_count;
   }
   const bool fused = a.est != nullptr;
+  if (mode == 0 && e->block_ready) {
+    // Source-blocked dense sweep (hanf_block.cu).  First the items: their
+    // rows n + 1 + k of the current generation take the maximum of the
+    // item's cold successors (counters only grow, so the row's value of two
+    // steps ago folds in harmlessly: the sweep's own-row rule applies to it
+    // unchanged).  Then the main sweep over the lists that name the items.
+    hanf::UnionArgs v = a;
+    use_tasks(&v, e->item_tasks, e->item_partials);
+    v.next = e->cnt[g];
+    v.mod_next = e->item_bits;
+    v.est = nullptr;
+    v.dirty_next = nullptr;
+    v.orig_of = nullptr;
+    v.est_index = nullptr;
+    v.stale_valid = 0;
+    v.l2_window_bytes = 0;
+    HANF_CUDA(hanf::launch_union(v, e->params.register_bits, e->params.registers, e->stream,
+                                 &e->launches));
+    use_tasks(&a, e->block_tasks, e->block_partials);
+  }
   HANF_CUDA(hanf::launch_union(a, e->params.register_bits, e->params.registers, e->stream,
                                &e->launches));
   if (mode == 4)  // rows changed last step that no listed task rewrote
@@ -1032,6 +1102,123 @@ hanf_status compute_shard(hanf_engine* e) {
     hanf::FinishArgs f{e->est, e->mod[ng], e->block_sums, e->reduce, e->n, e->blocks, w0, w1};
     HANF_CUDA(hanf::launch_finish(f, e->stream, &e->launches));
   }
+  return HANF_OK;
+}
+
+// Source-blocked dense sweeps (hanf_block.cu): which engines, and with
+// which shape.  Config 5 (measured, profiles/r02_block.md): the 2^20 rows of
+// highest out-degree as sources, rows past the first 2^21 (84 MB, what L2
+// keeps anyway) as cold, segments of 2^20 rows (42 MB), item tasks grouped
+// 2^18 items at a time.  HANF_BLOCK_S / _T / _SEG / _GROUP give the log2 of
+// each (tests force small ones).
+bool block_eligible(const hanf_engine* e) {
+  return e->relabel && !e->shard_relabel && e->lo == 0 && e->hi == e->n && e->batch == 1 &&
+         !e->bytes && !e->seg_live && !e->arena && e->parts.empty() && e->n >= 64 &&
+         e->csr_off && e->csr_succ &&
+         hanf::fused_estimates(e->params.register_bits, e->params.registers);
+}
+bool block_wanted_by_size(const hanf_engine* e) {
+  // counters far beyond L2 and enough arcs that the hot sources' lists
+  // split into items of several arcs (config 5; config 4's BA graph has no
+  // such sources)
+  return e->tasks.tos_words >= (1ull << 31) && (e->n + 1) * e->pitch * 8 >= (4ull << 30);
+}
+
+hanf_status build_block(hanf_engine* e) {
+  e->block_tried = true;
+  if (!block_eligible(e)) return HANF_OK;
+  cudaStream_t s = e->stream;
+  const uint64_t n = e->n;
+  auto env_log2 = [](const char* name, uint32_t dflt) {
+    const char* v = std::getenv(name);
+    return v && v[0] ? static_cast<uint32_t>(std::atoi(v)) : dflt;
+  };
+  // rows of ~84 MB stay in L2 on their own; half of that per segment
+  uint32_t cold_log2 = 0;
+  while ((2ull << cold_log2) * e->pitch * 8 <= (84ull << 20)) ++cold_log2;
+  cold_log2 = env_log2("HANF_BLOCK_T", cold_log2);
+  const uint32_t src_log2 = env_log2("HANF_BLOCK_S", cold_log2 ? cold_log2 - 1 : 0);
+  const uint32_t seg_log2 = env_log2("HANF_BLOCK_SEG", cold_log2 ? cold_log2 - 1 : 0);
+  const uint32_t group_log2 = env_log2("HANF_BLOCK_GROUP", 18);
+  if (cold_log2 > 31 || src_log2 > 31 || seg_log2 > 31 || group_log2 < 6 || group_log2 > 31)
+    return fail(HANF_INVALID_ARGUMENT, "HANF_BLOCK_* out of range");
+  const uint64_t cold = std::min<uint64_t>(1ull << cold_log2, n);
+  const uint64_t sources = std::min<uint64_t>(1ull << src_log2, n);
+  if (cold >= n || ((n - cold - 1) >> seg_log2) + 1 > 4096) return HANF_OK;  // nothing to block
+  HANF_CUDA(cudaStreamSynchronize(s));
+  // the engine's CSR: the caller's arcs through perm, or (once the worklist
+  // step relabelled them) rows already
+  const bool caller_ids = e->rl_off != nullptr;
+  const hanf::CsrView base{e->csr_off, 0, e->csr_succ, e->succ_base,
+                           caller_ids ? e->order : nullptr, caller_ids ? e->perm : nullptr, n};
+  hanf::BlockSplit b;
+  cudaError_t ce = hanf::build_block_split(base, n, sources, cold, seg_log2, s, &b, &e->launches);
+  if (ce == cudaErrorInvalidValue) return HANF_OK;  // (too many rows for 32-bit ids)
+  HANF_CUDA(ce);
+  // items of one arc save nothing (forced modes keep them: tests)
+  if (b.items == 0 || (e->block_mode == -1 && b.blocked_arcs < 2 * b.items)) {
+    hanf::free_block_split(&b, s);
+    return HANF_OK;
+  }
+  auto drop = [&](hanf_status st) {
+    hanf::free_block_split(&b, s);
+    hanf::free_tasks_device(&e->item_tasks, s);
+    hanf::free_tasks_device(&e->block_tasks, s);
+    pfree(e->item_partials, s);
+    pfree(e->block_partials, s);
+    pfree(e->item_bits, s);
+    return st;
+  };
+  int bad = 0;
+  const hanf::CsrView items{b.item_off, n + 1, b.item_succ, 0, nullptr, nullptr, n};
+  ce = hanf::build_tasks_device(items, n + 1, n + 1 + b.items, n, group_log2, s, nullptr,
+                                &e->item_tasks, &bad, &e->launches, false, false);
+  if (ce != cudaSuccess || bad) return drop(ce == cudaSuccess || ce == cudaErrorInvalidValue
+                                                ? HANF_OK : cuda_fail(ce, "item task build"));
+  hanf::CsrView main = base;
+  main.ovr_off = b.src_off;
+  main.ovr_succ = b.src_succ;
+  main.ovr_rows = sources;
+  ce = hanf::build_tasks_device(main, 0, n, n, 32, s, nullptr, &e->block_tasks, &bad, &e->launches,
+                                false, true, n + 1 + b.items);
+  if (ce != cudaSuccess || bad) return drop(ce == cudaSuccess || ce == cudaErrorInvalidValue
+                                                ? HANF_OK : cuda_fail(ce, "blocked task build"));
+  const uint64_t items_n = b.items;
+  e->block_arcs = b.blocked_arcs;
+  hanf::free_block_split(&b, s);
+  cudaError_t ae = palloc(&e->item_partials, static_cast<size_t>(e->item_tasks.num_chunks) * e->pitch, s);
+  if (ae == cudaSuccess)
+    ae = palloc(&e->block_partials, static_cast<size_t>(e->block_tasks.num_chunks) * e->pitch, s);
+  if (ae == cudaSuccess) ae = palloc(&e->item_bits, (n + 1 + items_n + 63) / 64 + 1, s);
+  if (ae == cudaSuccess)
+    ae = cudaMemsetAsync(e->item_bits, 0, sizeof(uint64_t) * ((n + 1 + items_n + 63) / 64 + 1), s);
+  // both generations grow by the item rows (the caller re-seeds next)
+  uint64_t* grown[2] = {nullptr, nullptr};
+  const uint64_t nw = (n + 1 + items_n) * e->pitch + 8;
+  HANF_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < 2 && ae == cudaSuccess; ++i) {
+    pfree(e->cnt[i], s);  // (freed first: two grown generations may not fit beside the old ones)
+    ae = palloc(&grown[i], nw, s);
+    if (ae == cudaSuccess) {
+      e->cnt[i] = grown[i];
+      ae = cudaMemsetAsync(e->cnt[i] + n * e->pitch, 0,
+                           sizeof(uint64_t) * ((1 + items_n) * e->pitch + 8), s);
+    }
+  }
+  if (ae != cudaSuccess) {
+    // without counter arrays the engine cannot go on
+    drop(HANF_OK);
+    return cuda_fail(ae, "source-blocked sweep allocation");
+  }
+  for (auto& x : e->graphs)  // captured steps hold the old arrays
+    for (auto& y : x)
+      for (auto& z : y) {
+        if (z.exec) cudaGraphExecDestroy(z.exec);
+        z = hanf_engine::StepGraph{};
+      }
+  e->block_items = items_n;
+  e->block_ready = true;
+  HANF_CUDA(cudaStreamSynchronize(s));
   return HANF_OK;
 }
 
@@ -1284,6 +1471,8 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
   e->pitch = hanf::row_pitch(params.register_bits, params.registers, params.words_per_counter,
                              e->bytes);
   if (const char* fs = std::getenv("HANF_SUMMARY")) e->force_summary = fs[0] == '1';
+  if (const char* bl = std::getenv("HANF_BLOCK"))
+    e->block_mode = bl[0] == '1' ? 1 : (bl[0] == '0' ? 0 : (bl[0] == '2' ? 2 : -1));
   if (const char* pn = std::getenv("HANF_PEER_NEED")) e->need_filter = pn[0] != '0';
   if (const char* ts = std::getenv("HANF_TASKSCAN")) e->task_scan = ts[0] == '1' ? 1 : (ts[0] == '0' ? 0 : -1);
   if (const char* ng = std::getenv("HANF_NO_GRAPHS")) e->use_graphs = std::atoi(ng) == 0;
@@ -1607,6 +1796,11 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     if (e->need)  // peer-push filter: the rows this shard gathers (read at the peers' attach)
       HANF_TRY(hanf::launch_need_rows(e->tasks.tos, e->tasks.tos_words, n, e->need, s,
                                       &e->launches));
+    if (e->block_mode == 1) {  // HANF_BLOCK=1: blocked dense sweeps from the first run on
+      st = build_block(e);
+      if (st == HANF_OK && e->block_ready) st = seed_all(e);  // (the counter arrays moved)
+      if (st != HANF_OK) return bail(st);
+    }
   }
 #undef HANF_TRY
   *out = e;
@@ -1700,6 +1894,11 @@ hanf_status hanf_reset(hanf_engine* e) {
     return HANF_OK;
   }
   HANF_CUDA(cudaSetDevice(e->device));
+  if (!e->block_tried && (e->block_mode == 2 || (e->block_mode == -1 && block_wanted_by_size(e)))) {
+    // a second run on this engine: the blocked dense sweeps pay for their build
+    const hanf_status bs = build_block(e);
+    if (bs != HANF_OK) return bs;
+  }
   return seed_all(e);
 }
 
@@ -1785,6 +1984,10 @@ hanf_status hanf_restore_counters(hanf_engine* e, const char* path, uint64_t ite
                                    e->params.registers, s, &e->launches);
   cudaFreeAsync(tmp, s);
   HANF_CUDA(ce);
+  {
+    const hanf_status bs = clear_item_rows(e);
+    if (bs != HANF_OK) return bs;
+  }
   // every counter counts as modified: the next step recomputes every node
   HANF_CUDA(hanf::launch_seed_bitmap(e->mod[0], e->n, s));
   HANF_CUDA(cudaMemsetAsync(e->mod[1], 0, sizeof(uint64_t) * e->blocks, s));
@@ -2551,6 +2754,13 @@ hanf_status hanf_launch_count(const hanf_engine* e, uint64_t* launches) {
   if (!e || !launches) return fail(HANF_INVALID_ARGUMENT, "null argument");
   *launches = e->launches;
   for (const hanf_engine* p : e->parts) *launches += p->launches;
+  return HANF_OK;
+}
+
+hanf_status hanf_block_stats(const hanf_engine* e, uint64_t* items, uint64_t* arcs) {
+  if (!e || !items || !arcs) return fail(HANF_INVALID_ARGUMENT, "null argument");
+  *items = e->block_ready ? e->block_items : 0;
+  *arcs = e->block_ready ? e->block_arcs : 0;
   return HANF_OK;
 }
 

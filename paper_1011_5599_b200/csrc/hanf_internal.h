@@ -73,13 +73,24 @@ struct CsrView {
   const uint32_t* orig_of;  // nullptr: identity labels (off indexed by v - lo)
   const uint32_t* perm;
   uint64_t n;
+  // Source-blocked dense sweeps (hanf_block.cu): rows [0, ovr_rows) take
+  // their successor lists from a second CSR already in row space (arc
+  // indices of that CSR carry kOvr, so begin/end/id stay the whole
+  // interface and end - begin is still the degree).
+  const uint64_t* ovr_off = nullptr;
+  const uint32_t* ovr_succ = nullptr;
+  uint64_t ovr_rows = 0;
+  static constexpr uint64_t kOvr = 1ull << 63;
   __device__ __forceinline__ uint64_t begin(uint64_t v) const {
+    if (v < ovr_rows) return kOvr | ovr_off[v];
     return orig_of ? off[orig_of[v]] : off[v - lo];
   }
   __device__ __forceinline__ uint64_t end(uint64_t v) const {
+    if (v < ovr_rows) return kOvr | ovr_off[v + 1];
     return orig_of ? off[orig_of[v] + 1] : off[v - lo + 1];
   }
   __device__ __forceinline__ uint32_t id(uint64_t k) const {
+    if (k & kOvr) return ovr_succ[k & ~kOvr];
     const uint32_t w = succ[k - succ_base];
     return perm && w < n ? perm[w] : w;  // out-of-range ids stay out of range (flagged)
   }
@@ -88,10 +99,34 @@ struct CsrView {
 // Sets *bad_input when offsets decrease or an arc endpoint is >= n.  Only
 // the final TOS fill reads the arcs: it waits for `succ_ready` (when
 // non-null), so the arcs upload overlaps the degree sort and task layout.
+// Successor ids must be < id_limit (0: n); TOS padding is always row n.
 cudaError_t build_tasks_device(const CsrView& g, uint64_t lo, uint64_t hi, uint64_t n,
                                uint32_t seg_shift, cudaStream_t s, cudaEvent_t succ_ready,
                                TaskBuild* out, int* bad_input, uint64_t* launches,
-                               bool seg_bounds = true, bool class_major = false);
+                               bool seg_bounds = true, bool class_major = false,
+                               uint64_t id_limit = 0);
+// Source-blocked dense sweeps (hanf_block.cu).  The arcs from the `sources`
+// first rows (the highest out-degrees of a relabelled engine) to rows >=
+// `cold` are cut out of those rows' lists and regrouped into items: one per
+// (segment of 2^seg_shift successor rows, source) pair with at least one
+// such arc, numbered segment-major.  Item k becomes row n + 1 + k of the
+// counter arrays: a first sweep over the items (successors = the cold rows,
+// all tasks of a segment together, so the segment stays in L2) leaves the
+// item's maximum in that row, and the main sweep gathers it through the
+// one id that replaced the item's arcs in its source's list.
+struct BlockSplit {
+  uint64_t* item_off = nullptr;  // [items + 1] into item_succ
+  uint32_t* item_succ = nullptr; // cold successor rows, item after item
+  uint64_t items = 0;
+  uint64_t blocked_arcs = 0;
+  uint64_t* src_off = nullptr;   // [sources + 1] into src_succ
+  uint32_t* src_succ = nullptr;  // per source: its rows < cold, then n + 1 + k per item
+  uint64_t src_arcs = 0;
+};
+cudaError_t build_block_split(const CsrView& g, uint64_t n, uint64_t sources, uint64_t cold,
+                              uint32_t seg_shift, cudaStream_t s, BlockSplit* out,
+                              uint64_t* launches);
+void free_block_split(BlockSplit* b, cudaStream_t s);
 void free_tasks_device(TaskBuild* t, cudaStream_t s);
 
 // Locality relabelling (hanf_relabel.cu): rows renumbered by descending
@@ -201,6 +236,7 @@ struct UnionArgs {
   uint32_t pitch;            // row pitch in u64 words (>= W, see row_pitch)
   uint32_t chunks;           // chunks per counter
   uint32_t zero_row;         // index of the all-zero counter row (= n)
+  uint32_t row_limit;        // rows of cur / next (n + 1, or more with item rows: hanf_block.cu)
   int32_t check_mod;         // skip successors whose bit is clear in mod_cur
   int32_t stale_valid;       // next[v] may be stale where mod_cur[v] is set
   double* est;               // per-counter estimates (nullptr: not fused)

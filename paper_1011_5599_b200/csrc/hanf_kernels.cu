@@ -250,7 +250,7 @@ __device__ __forceinline__ void finalize_hub(const UnionArgs& args, uint32_t h, 
   const uint32_t v = args.hub_nodes[h];
   const uint32_t first = args.hub_first[h];
   const uint32_t count = args.hub_count[h];
-  HANF_DCHECK(v < args.zero_row && count >= 1);
+  HANF_DCHECK(v < args.row_limit && v != args.zero_row && count >= 1);
   const uint32_t words = args.pitch;
   bool stale = false;
   if (args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
@@ -395,7 +395,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
     active = j < task.nodes;
     if (active) v = args.order[task.item + j];
   }
-  HANF_DCHECK(v <= zero_row && (!active || v < zero_row));
+  HANF_DCHECK(v < args.row_limit && (!active || v != zero_row));
   const bool lead = active && sub == 0 && !hub;
   bool stale = false;
   if (lead && args.stale_valid) stale = (args.mod_cur[v >> 6] >> (v & 63)) & 1;
@@ -452,7 +452,7 @@ __device__ __forceinline__ void union_task(const UnionArgs& args, uint32_t task_
       G_t g[U];
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        HANF_DCHECK(w[j] <= zero_row);
+        HANF_DCHECK(w[j] < args.row_limit);
         g[j].issue(cur, w[j], words, woff);
       }
 #pragma unroll

@@ -289,6 +289,13 @@ class NfEngine:
         check(lib().hanf_launch_count(self._h, ctypes.byref(c)))
         return c.value
 
+    def block_stats(self):
+        """hanf_block_stats: (items, arcs they cover) of the source-blocked
+        dense sweeps, (0, 0) when the engine does not use them."""
+        items, arcs = c_uint64(), c_uint64()
+        check(lib().hanf_block_stats(self._h, ctypes.byref(items), ctypes.byref(arcs)))
+        return int(items.value), int(arcs.value)
+
     def set_timing(self, enable: bool = True) -> None:
         """CUDA-event phase timing on the engine stream (resets the totals)."""
         check(lib().hanf_set_timing(self._h, int(enable)))
