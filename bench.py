@@ -377,9 +377,9 @@ def run_profile(engine, n):
         rep = engine.step()
         t = engine.timing()
         # step 1 changes every node with a successor; a step is dense while
-        # the previous one changed at least a quarter as many counters
+        # the previous one changed at least half as many counters (step_mode)
         first = rep.modified if first is None else first
-        kind = ("dense" if prev is None or 4 * prev >= first
+        kind = ("dense" if prev is None or 2 * prev >= first
                 else "tail (skip sweep, task scan or worklist)")
         prof.append({"t": len(prof) + 1, "modified": rep.modified, "kind": kind,
                      "sweep_ms": round(t["union_ms"], 4),
@@ -515,6 +515,19 @@ def main():
         engine = hanf.NfEngine(g, cfg)
     words = engine.params().words
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # Large relabelled engines switch to source-blocked dense sweeps at their
+    # first re-seed (hanf_block.cu; a one-shot estimate_nf never builds
+    # them): built here, timed, before the warm-up steps.
+    block = None
+    if world == 1:
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        engine.reset()
+        torch.cuda.synchronize(dev)
+        items, blocked_arcs = engine.block_stats()
+        if items:
+            block = {"items": items, "arcs": blocked_arcs,
+                     "build_s": round(time.perf_counter() - t0, 3)}
 
     total_ms, step_launches, clocks = dense_step_timing(engine, dev, args.steps, args.warmup,
                                                         flush, sharded, world)
@@ -572,6 +585,23 @@ def main():
         sharded.close()
     else:
         engine.close()
+    if block is not None:
+        # the same dense step the way a one-shot run sweeps it (every arc from
+        # its own node's list, no item rows): HANF_BLOCK=0
+        os.environ["HANF_BLOCK"] = "0"
+        try:
+            plain = hanf.NfEngine(g, cfg)
+        finally:
+            del os.environ["HANF_BLOCK"]
+        k = max(3, min(args.steps, 5))
+        ms, _, _ = dense_step_timing(plain, dev, k, args.warmup, flush)
+        ph = phase_timing(plain, dev, flush, 3)
+        plain.close()
+        block["one_shot_engine"] = {
+            "ms_per_step": ms / k, "value": a * k / (ms / 1e3), "union_ms": ph["union"],
+            "roofline_frac": B / (ph["union"] / 1e3) / 1e9 / peak,
+            "note": "first run of an engine (no re-seed yet): plain dense sweep with the L2 "
+                    "window, as every step of the e2e leg"}
 
     # whole estimate_nf through the public API from the caller's page-locked
     # host CSR (pinned in place with Graph.pin(), hanf_pin_host)
@@ -648,14 +678,23 @@ def main():
                                "events bracket the step's device work",
                        "l2": "flushed before every timed step (256 MiB write; persisting "
                              "lines reset by the re-seed); inputs (counters %.1f GB, arcs "
-                             "%.1f GB) exceed the 126 MB L2; the sweep runs with its L2 "
-                             "access-policy window over the hot rows (DESIGN 5.1)"
+                             "%.1f GB) exceed the 126 MB L2; plain dense sweeps run with an L2 "
+                             "access-policy window over the hot rows (DESIGN 5.1), "
+                             "source-blocked ones without"
                              % (2 * 8 * words * n / 1e9, 4 * a / 1e9),
-                       "sum_mode": "device (deterministic tree)"},
+                       "sum_mode": "device (deterministic tree)",
+                       "schedule": ("source-blocked dense sweep (DESIGN 5.1b): the engine was "
+                                    "re-seeded, as between the runs of a multi-run estimate; "
+                                    "an item sweep over %d (segment, source) items covering "
+                                    "%d arcs, then the main sweep; both launches are in "
+                                    "kernel_ms" % (block["items"], block["arcs"]))
+                                   if block else "plain dense sweep",
+                       "block": block},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "union_kernel (successor gather + broadword max + fused "
-                                   "estimator)",
+                                   "estimator)" + (": item sweep + main sweep, two launches "
+                                                   "per step" if block else ""),
                          "kernel_ms": union_ms, "algorithmic_bytes": B,
                          "peak_source": peak_src, "phases_ms": phases},
             "nvlink": nvlink,

@@ -98,6 +98,9 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--command", default="python bench.py --steps 2 --warmup 1")
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--sum-launches", action="store_true",
+                    help="the captured launches are one step (item sweep + main sweep of a "
+                         "source-blocked dense step): record their summed DRAM bytes")
     a = ap.parse_args()
     os.makedirs(PROFILES, exist_ok=True)
     if a.launches:
@@ -116,11 +119,16 @@ def main():
                 v = float(v.replace(",", ""))
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
-            traffic = sum(num(m, "DRAM read") + num(m, "DRAM write") for m in ms) / len(ms)
+            traffic = sum(num(m, "DRAM read") + num(m, "DRAM write") for m in ms)
+            if not a.sum_launches:
+                traffic /= len(ms)
             path = os.path.join(PROFILES, "union_kernel_ncu.json")
             doc = json.load(open(path)) if os.path.exists(path) else {}
             doc[f"config{a.config}"] = {"dram_bytes_per_launch": traffic, "source": f"{a.tag}_ncu_full.md",
                                         "kernel": union[0]}
+            if a.sum_launches:
+                doc[f"config{a.config}"]["note"] = (f"sum of the {len(ms)} launches of one "
+                                                    "source-blocked dense step")
             json.dump(doc, open(path, "w"), indent=1)
 
 

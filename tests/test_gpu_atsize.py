@@ -112,6 +112,29 @@ def test_config5_schedule_never_changes_a_bit(hanf, monkeypatch, relabel):
     _whole_run(hanf, g, fx, hanf.EngineConfig(bucket_bits=6, seed=42))
 
 
+def test_config5_source_blocked_sweeps(hanf, monkeypatch):
+    """Config 5 the way a re-seeded engine sweeps it (hanf_block.cu: on by
+    size from the first reset; HANF_BLOCK=1 builds it at create): the
+    reference's modified counts, N(t) bit for bit and counter digests at
+    every recorded iteration, and a second, re-seeded run of the same engine
+    equal to the first."""
+    fx = _fixture(5)
+    g = _cached_graph(hanf, 5)
+    cfg = hanf.EngineConfig(bucket_bits=6, seed=42)
+    monkeypatch.setenv("HANF_BLOCK", "1")
+    _lockstep(hanf, g, fx, cfg)
+    monkeypatch.delenv("HANF_BLOCK")
+    with hanf.NfEngine(g, cfg) as e:
+        assert e.block_stats() == (0, 0)
+        first = e.run_to_stabilisation()
+        assert [v.hex() for v in first.values] == fx["values"]
+        e.reset()
+        items, arcs = e.block_stats()
+        assert items > 0 and arcs > 2 * items
+        again = e.run_to_stabilisation()
+        assert again.values == first.values and again.modified == first.modified
+
+
 def test_config5_device_sum_within_tolerance(hanf):
     """Config 5 in the bench's mode (exact_sum=False: the deterministic
     device tree; default schedule: relabelling, L2 window, task-scan tail):
