@@ -1106,11 +1106,12 @@ hanf_status compute_shard(hanf_engine* e) {
 }
 
 // Source-blocked dense sweeps (hanf_block.cu): which engines, and with
-// which shape.  Config 5 (measured, profiles/r02_block.md): the 2^20 rows of
+// which shape.  Config 5 (measured, profiles/r02_block.md): the 2^21 rows of
 // highest out-degree as sources, rows past the first 2^21 (84 MB, what L2
-// keeps anyway) as cold, segments of 2^20 rows (42 MB), item tasks grouped
-// 2^18 items at a time.  HANF_BLOCK_S / _T / _SEG / _GROUP give the log2 of
-// each (tests force small ones).
+// keeps anyway) as cold, segments of 2^21 rows, item tasks grouped 2^18
+// items at a time (a flat optimum: 48.7 ms; 49.2-50.2 with 2^20 sources or
+// 2^20-row segments, 52 with 2^19- or 2^23-row segments).  HANF_BLOCK_S /
+// _T / _SEG / _GROUP give the log2 of each (tests force small ones).
 bool block_eligible(const hanf_engine* e) {
   return e->relabel && !e->shard_relabel && e->lo == 0 && e->hi == e->n && e->batch == 1 &&
          !e->bytes && !e->seg_live && !e->arena && e->parts.empty() && e->n >= 64 &&
@@ -1133,12 +1134,12 @@ hanf_status build_block(hanf_engine* e) {
     const char* v = std::getenv(name);
     return v && v[0] ? static_cast<uint32_t>(std::atoi(v)) : dflt;
   };
-  // rows of ~84 MB stay in L2 on their own; half of that per segment
+  // rows of ~84 MB stay in L2 on their own; as many per segment
   uint32_t cold_log2 = 0;
   while ((2ull << cold_log2) * e->pitch * 8 <= (84ull << 20)) ++cold_log2;
   cold_log2 = env_log2("HANF_BLOCK_T", cold_log2);
-  const uint32_t src_log2 = env_log2("HANF_BLOCK_S", cold_log2 ? cold_log2 - 1 : 0);
-  const uint32_t seg_log2 = env_log2("HANF_BLOCK_SEG", cold_log2 ? cold_log2 - 1 : 0);
+  const uint32_t src_log2 = env_log2("HANF_BLOCK_S", cold_log2);
+  const uint32_t seg_log2 = env_log2("HANF_BLOCK_SEG", cold_log2);
   const uint32_t group_log2 = env_log2("HANF_BLOCK_GROUP", 18);
   if (cold_log2 > 31 || src_log2 > 31 || seg_log2 > 31 || group_log2 < 6 || group_log2 > 31)
     return fail(HANF_INVALID_ARGUMENT, "HANF_BLOCK_* out of range");
