@@ -569,13 +569,6 @@ __device__ __forceinline__ double estimate_counter_r5(const uint64_t* c, const E
 // L1 wavefront each; the 8-byte loads they replace cost one per word) and
 // shifted down by q words with selects.
 // ---------------------------------------------------------------------------
-// sector-granular variants (probe): no L1 allocation / L2 only
-__device__ __forceinline__ void ldg256_na(uint32_t (&v)[8], const uint64_t* p) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                 "=r"(v[6]), "=r"(v[7])
-               : "l"(p));
-}
 __device__ __forceinline__ void ldg256(uint32_t (&v)[8], const uint64_t* p) {
   asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),

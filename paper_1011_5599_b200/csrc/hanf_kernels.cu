@@ -139,7 +139,6 @@ __device__ __forceinline__ void zero_limbs(uint32_t (&x)[Lay::kLimbs]) {
   sfor<0, Lay::kLimbs>([&](auto I) { x[decltype(I)::value] = 0u; });
 }
 
-__constant__ uint32_t g3_cold_from = 0;  // (probe) HANF_G3_COLD: rows from here gather sector-granular
 // GMODE = gather kind (0 per-word loads, 1 16-byte windows, 3 aligned 256-bit rows).
 template <class Lay, int GMODE, bool kVec16>
 struct Gather;
@@ -178,10 +177,7 @@ struct Gather<Lay, 3, kVec16> {
   __device__ __forceinline__ void issue(const uint64_t* cur, uint32_t w, uint32_t pitch,
                                         uint32_t woff) {
     const uint64_t* p = cur + static_cast<uint64_t>(w) * pitch + woff;
-    if (g3_cold_from && w >= g3_cold_from)  // (probe) cold rows: one sector, no L1 line
-      sfor<0, K>([&](auto I) { ldg256_na(raw[decltype(I)::value], p + 4 * decltype(I)::value); });
-    else
-      sfor<0, K>([&](auto I) { ldg256(raw[decltype(I)::value], p + 4 * decltype(I)::value); });
+    sfor<0, K>([&](auto I) { ldg256(raw[decltype(I)::value], p + 4 * decltype(I)::value); });
   }
   __device__ __forceinline__ void extract(uint32_t (&x)[Lay::kLimbs], uint32_t) const {
     sfor<0, Lay::kLimbs>([&](auto I) {
@@ -832,14 +828,6 @@ uint32_t row_pitch(uint32_t register_bits, uint32_t registers, uint32_t words, b
 // loads where rows are 16-byte aligned, per-word loads otherwise.
 cudaError_t launch_union(const UnionArgs& args, uint32_t register_bits, uint32_t registers,
                          cudaStream_t s, uint64_t* launches) {
-  static const bool probe = [] {
-    if (const char* c = std::getenv("HANF_G3_COLD")) {
-      const uint32_t from = static_cast<uint32_t>(std::strtoul(c, nullptr, 10));
-      cudaMemcpyToSymbol(g3_cold_from, &from, sizeof(from));
-    }
-    return true;
-  }();
-  (void)probe;
   const KernelChoice k = choose(register_bits, registers);
   if (args.num_wtasks == 0) return cudaSuccess;
   ++*launches;
