@@ -1154,7 +1154,14 @@ hanf_status build_block(hanf_engine* e) {
                            caller_ids ? e->order : nullptr, caller_ids ? e->perm : nullptr, n};
   hanf::BlockSplit b;
   cudaError_t ce = hanf::build_block_split(base, n, sources, cold, seg_log2, s, &b, &e->launches);
-  if (ce == cudaErrorInvalidValue) return HANF_OK;  // (too many rows for 32-bit ids)
+  // (too many rows for 32-bit ids, or no room for the build's scratch: the
+  // plain sweep stays)
+  auto soft = [](cudaError_t x) {
+    if (x != cudaErrorInvalidValue && x != cudaErrorMemoryAllocation) return false;
+    cudaGetLastError();
+    return true;
+  };
+  if (soft(ce)) return HANF_OK;
   HANF_CUDA(ce);
   // items of one arc save nothing (forced modes keep them: tests)
   if (b.items == 0 || (e->block_mode == -1 && b.blocked_arcs < 2 * b.items)) {
@@ -1174,16 +1181,16 @@ hanf_status build_block(hanf_engine* e) {
   const hanf::CsrView items{b.item_off, n + 1, b.item_succ, 0, nullptr, nullptr, n};
   ce = hanf::build_tasks_device(items, n + 1, n + 1 + b.items, n, group_log2, s, nullptr,
                                 &e->item_tasks, &bad, &e->launches, false, false);
-  if (ce != cudaSuccess || bad) return drop(ce == cudaSuccess || ce == cudaErrorInvalidValue
-                                                ? HANF_OK : cuda_fail(ce, "item task build"));
+  if (ce != cudaSuccess || bad)
+    return drop(ce == cudaSuccess || soft(ce) ? HANF_OK : cuda_fail(ce, "item task build"));
   hanf::CsrView main = base;
   main.ovr_off = b.src_off;
   main.ovr_succ = b.src_succ;
   main.ovr_rows = sources;
   ce = hanf::build_tasks_device(main, 0, n, n, 32, s, nullptr, &e->block_tasks, &bad, &e->launches,
                                 false, true, n + 1 + b.items);
-  if (ce != cudaSuccess || bad) return drop(ce == cudaSuccess || ce == cudaErrorInvalidValue
-                                                ? HANF_OK : cuda_fail(ce, "blocked task build"));
+  if (ce != cudaSuccess || bad)
+    return drop(ce == cudaSuccess || soft(ce) ? HANF_OK : cuda_fail(ce, "blocked task build"));
   const uint64_t items_n = b.items;
   e->block_arcs = b.blocked_arcs;
   hanf::free_block_split(&b, s);
@@ -1193,10 +1200,17 @@ hanf_status build_block(hanf_engine* e) {
   if (ae == cudaSuccess) ae = palloc(&e->item_bits, (n + 1 + items_n + 63) / 64 + 1, s);
   if (ae == cudaSuccess)
     ae = cudaMemsetAsync(e->item_bits, 0, sizeof(uint64_t) * ((n + 1 + items_n + 63) / 64 + 1), s);
+  if (ae != cudaSuccess) return drop(soft(ae) ? HANF_OK : cuda_fail(ae, "blocked sweep scratch"));
   // both generations grow by the item rows (the caller re-seeds next)
   uint64_t* grown[2] = {nullptr, nullptr};
   const uint64_t nw = (n + 1 + items_n) * e->pitch + 8;
   HANF_CUDA(cudaStreamSynchronize(s));
+  {
+    size_t free_b = 0, total_b = 0;  // room for both grown generations once the old ones are freed?
+    HANF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t extra = 2 * 8 * items_n * e->pitch;
+    if (free_b < extra + (1ull << 30)) return drop(HANF_OK);
+  }
   for (int i = 0; i < 2 && ae == cudaSuccess; ++i) {
     pfree(e->cnt[i], s);  // (freed first: two grown generations may not fit beside the old ones)
     ae = palloc(&grown[i], nw, s);
