@@ -257,6 +257,9 @@ struct hanf_engine {
   double* h_batch_sums[2] = {nullptr, nullptr};   // pinned [batch][blocks_real] per parity
   std::vector<double> batch_last;                 // N(t) of every run
   bool relabel = false;
+  // csr_succ holds rows already (mapped through perm chunk by chunk under the
+  // upload), still grouped by the caller's node order
+  bool succ_rows = false;
   // relabelled shard of a peer-push run: rows interleaved across the
   // shards by degree; estimates are pushed to the peers and every commit
   // recomputes all original-id blocks from the full estimate array
@@ -823,7 +826,7 @@ hanf_status ensure_sparse(hanf_engine* e) {
     // copy is not needed after that
     uint32_t* succ = nullptr;
     int bad = 0;
-    const hanf::RelabelOut r{e->order, e->perm, e->rl_off};
+    const hanf::RelabelOut r{e->order, e->succ_rows ? nullptr : e->perm, e->rl_off};
     HANF_CUDA(hanf::relabel_arcs_device(e->csr_off, e->csr_succ, e->n, e->shard_arcs, r, s, &succ,
                                         &bad, &e->launches));
     pfree(e->csr_off, s);
@@ -1151,7 +1154,8 @@ hanf_status build_block(hanf_engine* e) {
   // step relabelled them) rows already
   const bool caller_ids = e->rl_off != nullptr;
   const hanf::CsrView base{e->csr_off, 0, e->csr_succ, e->succ_base,
-                           caller_ids ? e->order : nullptr, caller_ids ? e->perm : nullptr, n};
+                           caller_ids ? e->order : nullptr,
+                           caller_ids && !e->succ_rows ? e->perm : nullptr, n};
   hanf::BlockSplit b;
   cudaError_t ce = hanf::build_block_split(base, n, sources, cold, seg_log2, s, &b, &e->launches);
   // (too many rows for 32-bit ids, or no room for the build's scratch: the
@@ -1713,16 +1717,20 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     HANF_TRY(streams().get(cfg.device, &s2));
     helper = s2;
     cudaEvent_t ev_off = nullptr, ev_arcs = nullptr;
-    struct UploadGuard {  // the helper stream is idle again before anything is freed
+    struct UploadGuard {  // the helper streams are idle again before anything is freed
       int dev;
       cudaStream_t st;
       cudaEvent_t a, b;
       std::vector<cudaEvent_t> chunks;
+      cudaStream_t st3 = nullptr;  // maps uploaded arc chunks to rows (relabelled engines)
       ~UploadGuard() {
-        if (cudaStreamSynchronize(st) == cudaSuccess)
-          streams().put(dev, st);
-        else
-          cudaStreamDestroy(st);
+        for (cudaStream_t x : {st, st3}) {
+          if (!x) continue;
+          if (cudaStreamSynchronize(x) == cudaSuccess)
+            streams().put(dev, x);
+          else
+            cudaStreamDestroy(x);
+        }
         if (a) cudaEventDestroy(a);
         if (b) cudaEventDestroy(b);
         for (cudaEvent_t c : chunks) cudaEventDestroy(c);
@@ -1736,9 +1744,32 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
                              cudaMemcpyHostToDevice, s));
     HANF_TRY(cudaEventRecord(ev_off, s));
     HANF_TRY(cudaStreamWaitEvent(s2, ev_off, 0));
-    if (a1 > a0)
-      HANF_TRY(cudaMemcpyAsync(d_succ, g->arcs + a0, sizeof(uint32_t) * (a1 - a0),
+    // Large relabelled engines upload the arcs in chunks: each chunk's ids
+    // are mapped to rows through perm as soon as it has landed (on a third
+    // stream, under the rest of the upload), so the TOS fill that follows the
+    // upload streams row ids instead of gathering perm for every arc
+    // (config 5: ~4.3 G random 4-byte gathers off the critical path).
+    const uint64_t up_arcs = a1 - a0;
+    // (HANF_MAP_CHUNK=arcs forces it with that chunk size, 0 turns it off: tests)
+    bool map_chunks = e->relabel && K == 1 && up_arcs >= (1ull << 26);
+    uint64_t chunk_arcs = std::max<uint64_t>(up_arcs / 32 + 1, 1ull << 24);
+    if (const char* mc = std::getenv("HANF_MAP_CHUNK")) {
+      const uint64_t forced = std::strtoull(mc, nullptr, 10);
+      map_chunks = e->relabel && K == 1 && forced > 0 && up_arcs > 0;
+      chunk_arcs = std::max<uint64_t>(forced, up_arcs / 1024 + 1);
+    }
+    if (!map_chunks) chunk_arcs = up_arcs;
+    for (uint64_t c0 = 0; c0 < up_arcs; c0 += chunk_arcs) {
+      const uint64_t len = std::min(chunk_arcs, up_arcs - c0);
+      HANF_TRY(cudaMemcpyAsync(d_succ + c0, g->arcs + a0 + c0, sizeof(uint32_t) * len,
                                cudaMemcpyHostToDevice, s2));
+      if (map_chunks) {
+        cudaEvent_t ce = nullptr;
+        HANF_TRY(cudaEventCreateWithFlags(&ce, cudaEventDisableTiming));
+        guard.chunks.push_back(ce);
+        HANF_TRY(cudaEventRecord(ce, s2));
+      }
+    }
     HANF_TRY(cudaEventRecord(ev_arcs, s2));
     phase("offsets");
     if (K > 1) {
@@ -1790,17 +1821,43 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
       }
       phase("relabel");
     }
+    cudaEvent_t succ_ready = ev_arcs;
+    if (map_chunks) {
+      // perm is complete on `s` here; chunk c is mapped once it has landed
+      cudaStream_t s3 = nullptr;
+      HANF_TRY(streams().get(cfg.device, &s3));
+      guard.st3 = s3;
+      cudaEvent_t ev_perm = nullptr, ev_mapped = nullptr;
+      HANF_TRY(cudaEventCreateWithFlags(&ev_perm, cudaEventDisableTiming));
+      guard.chunks.push_back(ev_perm);
+      HANF_TRY(cudaEventCreateWithFlags(&ev_mapped, cudaEventDisableTiming));
+      guard.chunks.push_back(ev_mapped);
+      const size_t nchunks = guard.chunks.size() - 2;
+      HANF_TRY(cudaEventRecord(ev_perm, s));
+      HANF_TRY(cudaStreamWaitEvent(s3, ev_perm, 0));
+      for (size_t c = 0; c < nchunks; ++c) {
+        const uint64_t c0 = c * chunk_arcs;
+        HANF_TRY(cudaStreamWaitEvent(s3, guard.chunks[c], 0));
+        HANF_TRY(hanf::launch_map_ids(d_succ + c0, std::min(chunk_arcs, up_arcs - c0), e->perm, n,
+                                      s3, &e->launches));
+      }
+      HANF_TRY(cudaEventRecord(ev_mapped, s3));
+      succ_ready = ev_mapped;
+      e->succ_rows = true;
+    }
     st = seed_all(e);
     if (st != HANF_OK) return bail(st);
     phase("seed");
     int bad = 0;
-    // relabelled: row v's successors are the caller's arcs of order[v], through perm
-    const hanf::CsrView view{d_off, up_lo, d_succ, a0, e->order, e->perm, n};
-    const cudaError_t be = hanf::build_tasks_device(view, lo, hi, n, seg_shift, s, ev_arcs,
+    // relabelled: row v's successors are the caller's arcs of order[v],
+    // through perm unless the upload mapped them already
+    const hanf::CsrView view{d_off, up_lo, d_succ, a0, e->order, e->succ_rows ? nullptr : e->perm, n};
+    const cudaError_t be = hanf::build_tasks_device(view, lo, hi, n, seg_shift, s, succ_ready,
                                                     &e->tasks, &bad, &e->launches, seg_skip,
                                                     !seg_skip);
     // (also on the build's error paths) frees on `s` come after the upload
     HANF_TRY(cudaStreamWaitEvent(s, ev_arcs, 0));
+    HANF_TRY(cudaStreamWaitEvent(s, succ_ready, 0));
     e->csr_off = d_off;
     e->csr_succ = d_succ;
     e->succ_base = a0;

@@ -146,6 +146,10 @@ cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t way
                                  cudaStream_t s, RelabelOut* out, uint64_t* launches);
 // The relabelled arcs (only the worklist step's transpose needs them; the
 // union sweep's TOS is filled through CsrView).  *bad = arc endpoint >= n.
+// ids[i] = perm[ids[i]] in place for ids < n (arc chunks mapped to rows as
+// they land, under the rest of the upload).
+cudaError_t launch_map_ids(uint32_t* ids, uint64_t count, const uint32_t* perm, uint64_t n,
+                           cudaStream_t s, uint64_t* launches);
 cudaError_t relabel_arcs_device(const uint64_t* d_off, const uint32_t* d_succ, uint64_t n,
                                 uint64_t arcs, const RelabelOut& r, cudaStream_t s,
                                 uint32_t** succ_out, int* bad, uint64_t* launches);

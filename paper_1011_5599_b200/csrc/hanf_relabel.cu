@@ -178,7 +178,7 @@ __global__ void rewrite_arcs_kernel(const uint64_t* __restrict__ off, const uint
           const uint64_t src = off[order[r]] + (i - noff[r]);
           const uint32_t w = src < arcs ? succ[src] : 0xffffffffu;
           if (w < n)
-            val = perm[w];
+            val = perm ? perm[w] : w;  // (null: the upload mapped the ids already)
           else
             oob = true;
         }
@@ -288,6 +288,27 @@ cudaError_t relabel_order_device(const uint64_t* d_off, uint64_t n, uint32_t way
   }
   HANF_RELABEL_TRY(cudaFreeAsync(ndeg, s));
   phase("offsets");
+  return cudaGetLastError();
+}
+
+// ids[i] = perm[ids[i]] in place (ids >= n stay: the TOS fill flags them)
+__global__ void map_ids_kernel(uint32_t* __restrict__ ids, uint64_t count,
+                               const uint32_t* __restrict__ perm, uint64_t n) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += stride) {
+    const uint32_t w = ids[i];
+    if (w < n) ids[i] = perm[w];
+  }
+}
+
+cudaError_t launch_map_ids(uint32_t* ids, uint64_t count, const uint32_t* perm, uint64_t n,
+                           cudaStream_t s, uint64_t* launches) {
+  if (count == 0) return cudaSuccess;
+  uint64_t blocks = (count + 1023) / 1024;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  map_ids_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(ids, count, perm, n);
+  ++*launches;
   return cudaGetLastError();
 }
 

@@ -127,3 +127,42 @@ def test_blocked_restore_and_worklist(hanf, port, monkeypatch, tmp_path):
         again = e.run_to_stabilisation()
         assert again.values == first.values and again.modified == first.modified
     lockstep(hanf, port, g, bucket_bits=6, seed=3)
+
+
+@pytest.mark.parametrize("chunk", ["1", "1000", "65536"])
+def test_upload_maps_arc_chunks(hanf, port, monkeypatch, chunk):
+    """Large relabelled engines upload the arcs in chunks and map each
+    chunk's ids to rows under the rest of the upload (hanf_engine.cu
+    create_engine; on by size from 2^26 arcs, forced here with tiny chunks):
+    the plain sweeps, the worklist step (whose CSR rewrite then must not map
+    again), the source-blocked sweeps and relabelled peer-push shards all
+    read row ids and stay bit-exact; bad arc endpoints are still refused."""
+    monkeypatch.setenv("HANF_RELABEL", "1")
+    monkeypatch.setenv("HANF_MAP_CHUNK", chunk)
+    for g in _graphs(hanf):
+        lockstep(hanf, port, g, bucket_bits=6, seed=21)
+    monkeypatch.setenv("HANF_SPARSE", "1")
+    lockstep(hanf, port, hanf.gen_clique_path(600, 40), bucket_bits=6, seed=3)
+    lockstep(hanf, port, hanf.gen_rmat(12, 16, 0.57, 0.19, 0.19, 6, 2), bucket_bits=7, seed=4)
+    monkeypatch.delenv("HANF_SPARSE")
+    _force(monkeypatch, SHAPES[0])
+    for g in _graphs(hanf):
+        lockstep(hanf, port, g, bucket_bits=6, seed=22)
+    _force(monkeypatch, SHAPES[1], mode="2")
+    monkeypatch.setenv("HANF_SPARSE", "1")
+    g = hanf.gen_clique_path(600, 40)
+    with hanf.NfEngine(g, hanf.EngineConfig(bucket_bits=6, seed=3)) as e:
+        first = e.run_to_stabilisation()
+        e.reset()
+        assert e.block_stats()[0] > 0
+        again = e.run_to_stabilisation()
+        assert again.values == first.values and again.modified == first.modified
+    monkeypatch.delenv("HANF_SPARSE")
+    monkeypatch.setenv("HANF_BLOCK", "0")
+    bad = hanf.Graph(3, np.array([0, 1, 2, 2], dtype=np.uint64), np.array([1, 7], dtype=np.uint32))
+    with pytest.raises(ValueError):
+        hanf.NfEngine(bad, hanf.EngineConfig(bucket_bits=6, seed=1))
+    import test_gpu_peer
+    test_gpu_peer.test_peer_push_relabelled_shards(hanf, monkeypatch, 6, 4, True, False)
+    monkeypatch.setenv("HANF_MAP_CHUNK", chunk)
+    test_gpu_peer.test_peer_push_relabelled_shards(hanf, monkeypatch, 5, 2, True, True)
