@@ -506,7 +506,12 @@ def main():
         g = make_graph(args.config, device=local_rank if cfgd["kind"] == "rmat" else None)
     t_gen = time.perf_counter() - t_gen
     n, a = g.num_nodes(), g.num_arcs()
-    cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank, exact_sum=False)
+    # the dense-step engine is configured like a long multi-run's engine
+    # (hanf.multirun passes its run count the same way): large relabelled
+    # engines then sweep source-blocked from the first run (hanf_block.cu)
+    cfg = hanf.EngineConfig(bucket_bits=b, seed=HLL_SEED, device=local_rank, exact_sum=False,
+                            expected_runs=100)
+    t_create = time.perf_counter()
     if world > 1:
         sharded = ShardedNfEngine(g, cfg, rank, world, exchange=args.exchange)
         engine = sharded.local.engine
@@ -515,19 +520,14 @@ def main():
         engine = hanf.NfEngine(g, cfg)
     words = engine.params().words
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    # Large relabelled engines switch to source-blocked dense sweeps at their
-    # first re-seed (hanf_block.cu; a one-shot estimate_nf never builds
-    # them): built here, timed, before the warm-up steps.
     block = None
     if world == 1:
         torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        engine.reset()
-        torch.cuda.synchronize(dev)
+        t_create = time.perf_counter() - t_create
         items, blocked_arcs = engine.block_stats()
         if items:
-            block = {"items": items, "arcs": blocked_arcs,
-                     "build_s": round(time.perf_counter() - t0, 3)}
+            block = {"items": items, "arcs": blocked_arcs, "expected_runs": cfg.expected_runs,
+                     "create_s": round(t_create, 3)}
 
     total_ms, step_launches, clocks = dense_step_timing(engine, dev, args.steps, args.warmup,
                                                         flush, sharded, world)
@@ -586,13 +586,13 @@ def main():
     else:
         engine.close()
     if block is not None:
-        # the same dense step the way a one-shot run sweeps it (every arc from
-        # its own node's list, no item rows): HANF_BLOCK=0
-        os.environ["HANF_BLOCK"] = "0"
-        try:
-            plain = hanf.NfEngine(g, cfg)
-        finally:
-            del os.environ["HANF_BLOCK"]
+        # the same dense step the way a one-shot run (or a short multi-run)
+        # sweeps it: every arc from its own node's list, no item rows
+        import dataclasses
+        t0 = time.perf_counter()
+        plain = hanf.NfEngine(g, dataclasses.replace(cfg, expected_runs=0))
+        torch.cuda.synchronize(dev)
+        block["one_shot_create_s"] = round(time.perf_counter() - t0, 3)
         k = max(3, min(args.steps, 5))
         ms, _, _ = dense_step_timing(plain, dev, k, args.warmup, flush)
         ph = phase_timing(plain, dev, flush, 3)
@@ -600,8 +600,8 @@ def main():
         block["one_shot_engine"] = {
             "ms_per_step": ms / k, "value": a * k / (ms / 1e3), "union_ms": ph["union"],
             "roofline_frac": B / (ph["union"] / 1e3) / 1e9 / peak,
-            "note": "first run of an engine (no re-seed yet): plain dense sweep with the L2 "
-                    "window, as every step of the e2e leg"}
+            "note": "EngineConfig.expected_runs = 0 (the default): plain dense sweep with the "
+                    "L2 window, as every step of the e2e legs"}
 
     # whole estimate_nf through the public API from the caller's page-locked
     # host CSR (pinned in place with Graph.pin(), hanf_pin_host)
@@ -626,8 +626,8 @@ def main():
             h2d = 8 * (n + 1) + 4 * a
             desc = "whole estimate_nf() (upload, seed, %d iterations, read-back) per step"
             # the reference's multirun (main.cpp:263-283) through the same API:
-            # one upload, the engine re-seeded per run (large engines switch to
-            # source-blocked dense sweeps at the first re-seed; build included)
+            # one upload, the engine re-seeded per run (too few runs to repay a
+            # source-blocked build: plain sweeps)
             k = 4
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
@@ -698,11 +698,12 @@ def main():
                              "source-blocked ones without"
                              % (2 * 8 * words * n / 1e9, 4 * a / 1e9),
                        "sum_mode": "device (deterministic tree)",
-                       "schedule": ("source-blocked dense sweep (DESIGN 5.1b): the engine was "
-                                    "re-seeded, as between the runs of a multi-run estimate; "
-                                    "an item sweep over %d (segment, source) items covering "
-                                    "%d arcs, then the main sweep; both launches are in "
-                                    "kernel_ms" % (block["items"], block["arcs"]))
+                       "schedule": ("source-blocked dense sweep (DESIGN 5.1b): the engine is "
+                                    "configured for a long multi-run (EngineConfig."
+                                    "expected_runs = 100, as hanf.multirun passes its run "
+                                    "count); an item sweep over %d (segment, source) items "
+                                    "covering %d arcs, then the main sweep; both launches "
+                                    "are in kernel_ms" % (block["items"], block["arcs"]))
                                    if block else "plain dense sweep",
                        "block": block},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

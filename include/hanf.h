@@ -81,7 +81,13 @@ typedef struct {
                                  exceed L2 and whose ids lack locality are
                                  relabelled by degree, interleaved across the
                                  shards (balanced arcs, hot rows first in each) */
-  uint32_t reserved;
+  uint32_t expected_runs;     /* (new) runs the caller plans on this engine (multirun,
+                                 main.cpp:263-283: hanf_reseed between them); 0 =
+                                 unknown.  Only schedules depend on it: from 20 runs
+                                 a large relabelled engine builds its source-blocked
+                                 dense sweeps at create (see hanf_block_stats);
+                                 otherwise they are built once the engine has run
+                                 enough dense steps to repay the build */
 } hanf_config;
 
 /* IterationReport (engine.hpp:48-51) */
@@ -223,7 +229,9 @@ hanf_status hanf_launch_count(const hanf_engine* engine, uint64_t* launches);
  * NfEngine::step's union loop, engine.hpp:157-185; results are unchanged):
  * the number of (successor segment, source) items and the arcs they cover,
  * 0 / 0 while the engine sweeps every arc from its own node's list.  Built
- * at the first hanf_reset / hanf_reseed of a large relabelled engine
+ * for large relabelled engines: at create when hanf_config.expected_runs >= 20,
+ * else at the hanf_reset / hanf_reseed that follows the engine's 96th dense
+ * step, when the steps saved so far would have repaid the build
  * (HANF_BLOCK=1: at create, 2: at the first reset whatever the size, 0: never). */
 hanf_status hanf_block_stats(const hanf_engine* engine, uint64_t* items, uint64_t* arcs);
 /* Phase timing with CUDA events on the engine stream (off by default):

@@ -95,6 +95,10 @@ struct EngineConfig {
   bool exact_sum = true;
   std::uint64_t shard_begin = 0, shard_end = 0;
   std::uint32_t shard_count = 0;
+  // runs planned on this engine (reseed() between them, main.cpp:263-283);
+  // schedules only: from 20, large engines build their source-blocked dense
+  // sweeps at construction (hanf_block_stats)
+  std::uint32_t expected_runs = 0;
   // several GPUs of this process, one node-range shard each (repeats
   // allowed): NfEngine then drives them all (hanf_create_multi), as the
   // reference's NfEngine keeps its threads internal (engine.hpp:157)
@@ -120,6 +124,7 @@ struct EngineConfig {
     c.shard_begin = shard_begin;
     c.shard_end = shard_end;
     c.shard_count = shard_count;
+    c.expected_runs = expected_runs;
     return c;
   }
 };

@@ -30,7 +30,7 @@ class Config(Structure):
                 ("spill_to_disk", c_int32), ("track_modified", c_int32),
                 ("use_systolic", c_int32), ("device", c_int32),
                 ("exact_sum", c_int32), ("shard_begin", c_uint64),
-                ("shard_end", c_uint64), ("shard_count", c_uint32), ("reserved", c_uint32)]
+                ("shard_end", c_uint64), ("shard_count", c_uint32), ("expected_runs", c_uint32)]
 
 
 class IterationReportC(Structure):

@@ -334,9 +334,15 @@ struct hanf_engine {
   uint32_t* seg_live = nullptr;  // skip sweeps over segmented tasks (TaskBuild::seg_shift)
   // Source-blocked dense sweeps (hanf_block.cu; unsharded relabelled engines
   // with the packed store).  block_mode: 1 = built at create (HANF_BLOCK=1),
-  // 0 = never, -1 = built at the first re-seed of a large engine (multi-run
-  // use amortises the build; a one-shot run never pays for it).  Item k is
-  // row n + 1 + k of both counter generations.
+  // 2 = at the first re-seed, 0 = never, -1 = by size and use: at create
+  // when the caller announced a long multi-run (cfg.expected_runs >=
+  // kBlockRuns), else at the re-seed after kBlockDenseSteps dense steps,
+  // when the steps saved so far would have repaid the build (ski rental; a
+  // one-shot run and a short multi-run never pay for it).  Item k is row
+  // n + 1 + k of both counter generations.
+  static constexpr uint32_t kBlockRuns = 20;
+  static constexpr uint64_t kBlockDenseSteps = 96;  // build ~0.47 s / ~5 ms saved per step
+  uint64_t dense_steps = 0;
   int block_mode = -1;
   bool block_ready = false;
   bool block_tried = false;
@@ -1350,6 +1356,7 @@ hanf_status step_enqueue(hanf_engine* e) {
     if (st != HANF_OK) return st;
   }
   if (mode == 0) {
+    ++e->dense_steps;
     const hanf_status st = activate_l2_window(e);
     if (st != HANF_OK) return st;
   }
@@ -1424,7 +1431,7 @@ hanf_status hanf_config_init(hanf_config* cfg) {
   cfg->shard_begin = 0;
   cfg->shard_end = 0;
   cfg->shard_count = 0;
-  cfg->reserved = 0;
+  cfg->expected_runs = 0;
   return HANF_OK;
 }
 
@@ -1879,7 +1886,10 @@ static hanf_status create_engine(const hanf_graph_view* g, const hanf_config* cf
     if (e->need)  // peer-push filter: the rows this shard gathers (read at the peers' attach)
       HANF_TRY(hanf::launch_need_rows(e->tasks.tos, e->tasks.tos_words, n, e->need, s,
                                       &e->launches));
-    if (e->block_mode == 1) {  // HANF_BLOCK=1: blocked dense sweeps from the first run on
+    // HANF_BLOCK=1, or a long multi-run announced on a large engine: blocked
+    // dense sweeps from the first run on
+    if (e->block_mode == 1 || (e->block_mode == -1 && cfg.expected_runs >= hanf_engine::kBlockRuns &&
+                               block_wanted_by_size(e))) {
       st = build_block(e);
       if (st == HANF_OK && e->block_ready) st = seed_all(e);  // (the counter arrays moved)
       if (st != HANF_OK) return bail(st);
@@ -1977,8 +1987,10 @@ hanf_status hanf_reset(hanf_engine* e) {
     return HANF_OK;
   }
   HANF_CUDA(cudaSetDevice(e->device));
-  if (!e->block_tried && (e->block_mode == 2 || (e->block_mode == -1 && block_wanted_by_size(e)))) {
-    // a second run on this engine: the blocked dense sweeps pay for their build
+  if (!e->block_tried &&
+      (e->block_mode == 2 || (e->block_mode == -1 && block_wanted_by_size(e) &&
+                              e->dense_steps >= hanf_engine::kBlockDenseSteps))) {
+    // a long-lived engine: the blocked dense sweeps pay for their build from here on
     const hanf_status bs = build_block(e);
     if (bs != HANF_OK) return bs;
   }

@@ -52,6 +52,9 @@ class EngineConfig:
     shard_begin: int = 0
     shard_end: int = 0
     shard_count: int = 0            # peer-push shards: allows relabelled shards
+    expected_runs: int = 0          # runs planned on this engine (multirun sets it):
+                                    # from 20, large engines build their source-blocked
+                                    # dense sweeps at create (hanf_block_stats)
     # several GPUs of this process, one node-range shard each (repeats
     # allowed): the engine drives them all (hanf_create_multi)
     devices: tuple = ()
@@ -76,6 +79,7 @@ class EngineConfig:
         c.shard_begin = self.shard_begin
         c.shard_end = self.shard_end
         c.shard_count = self.shard_count
+        c.expected_runs = max(0, min(int(self.expected_runs), 0xFFFFFFFF))
         return c
 
 
@@ -456,6 +460,8 @@ def multirun(g: Graph, cfg: EngineConfig = None, runs: int = 10, base_seed: int 
             i += k
         return out
     cfg.seed = base
+    if not cfg.expected_runs:
+        cfg.expected_runs = runs  # the engine may schedule for the whole multi-run
     with NfEngine(g, cfg) as engine:
         for i in range(runs):
             if i:

@@ -113,8 +113,9 @@ def test_config5_schedule_never_changes_a_bit(hanf, monkeypatch, relabel):
 
 
 def test_config5_source_blocked_sweeps(hanf, monkeypatch):
-    """Config 5 the way a re-seeded engine sweeps it (hanf_block.cu: on by
-    size from the first reset; HANF_BLOCK=1 builds it at create): the
+    """Config 5 the way a long-lived engine sweeps it (hanf_block.cu: by
+    size, at create for an announced long multi-run, else once enough dense
+    steps ran; HANF_BLOCK=1 builds it at create): the
     reference's modified counts, N(t) bit for bit and counter digests at
     every recorded iteration, and a second, re-seeded run of the same engine
     equal to the first."""
@@ -124,13 +125,29 @@ def test_config5_source_blocked_sweeps(hanf, monkeypatch):
     monkeypatch.setenv("HANF_BLOCK", "1")
     _lockstep(hanf, g, fx, cfg)
     monkeypatch.delenv("HANF_BLOCK")
+    # a long multi-run announced (EngineConfig.expected_runs, as multirun
+    # passes it): built at create
+    import dataclasses
+    with hanf.NfEngine(g, dataclasses.replace(cfg, expected_runs=32)) as e:
+        items, arcs = e.block_stats()
+        assert items > 0 and arcs > 2 * items
+        first = e.run_to_stabilisation()
+        assert [v.hex() for v in first.values] == fx["values"]
+    # nothing announced: plain sweeps until the engine has run enough dense
+    # steps to repay the build (96: the 20th run of config 5), then blocked
     with hanf.NfEngine(g, cfg) as e:
         assert e.block_stats() == (0, 0)
         first = e.run_to_stabilisation()
         assert [v.hex() for v in first.values] == fx["values"]
-        e.reset()
-        items, arcs = e.block_stats()
-        assert items > 0 and arcs > 2 * items
+        built_at = None
+        for i in range(1, 24):
+            e.reseed(1000 + i)
+            if e.block_stats()[0] > 0:
+                built_at = i
+                break
+            e.run_to_stabilisation()
+        assert built_at is not None and built_at > 4
+        e.reseed(42)
         again = e.run_to_stabilisation()
         assert again.values == first.values and again.modified == first.modified
 
