@@ -795,12 +795,25 @@ bool task_scan_wanted(const hanf_engine* e) {
   if (e->task_scan == 1) return true;
   return e->tasks.tos_words >= (1ull << 28) && 64 * e->last_count < e->n;
 }
+// Eligible steps before the worklist's transpose is built (ski rental).  It
+// costs about as much as 8 skip sweeps of the same arcs
+// (profiles/r01_sparse.md) - but where the task-scan step (mode 4) serves
+// the tail, an eligible step costs a fraction of a sweep: config 5's three
+// tail steps take 20 ms per run by task scan against a 1.03 s transpose
+// (profiles/r02_block.md), so such engines wait for 192 eligible steps
+// (a 4-seed multirun went from 0.69 to ~0.43 s per run).
+uint32_t sparse_after(const hanf_engine* e) {
+  if (e->force_sparse || e->sparse_after != 8) return e->sparse_after;
+  const bool scan = e->task_scan != 0 && e->lo == 0 && e->hi == e->n && e->batch == 1 &&
+                    !e->seg_live && e->tasks.tos_words >= (1ull << 28) &&
+                    hanf::fused_estimates(e->params.register_bits, e->params.registers);
+  return scan ? 192 : e->sparse_after;
+}
 int step_mode(const hanf_engine* e) {
   if (!e->cfg.track_modified || e->t == 0) return 0;
-  // the transpose costs about as much as 8 skip sweeps of the same arcs
-  // (profiles/r01_sparse.md): build it (ski-rental style) only once that
-  // many steps would have used it, so short runs never pay for it
-  if (sparse_wanted(e) && (e->tr_off || e->sparse_wanted_steps >= e->sparse_after)) return 2;
+  // build the transpose only once that many steps would have used it, so
+  // short runs never pay for it
+  if (sparse_wanted(e) && (e->tr_off || e->sparse_wanted_steps >= sparse_after(e))) return 2;
   // dense while at least half of the nodes that can change did (nodes of
   // out-degree 0 never do: 60% of config 5's, whose steps 2-4 change 99% of
   // the rest and ran 20% slower as skip sweeps)
