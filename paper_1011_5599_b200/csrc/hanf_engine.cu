@@ -386,6 +386,17 @@ struct hanf_engine {
   uint8_t* peer_base[hanf::kMaxPeers] = {};
   bool peer_ipc[hanf::kMaxPeers] = {};       // opened with cudaIpcOpenMemHandle
 
+  // the persisting set-aside goes with the last windowed engine of the device
+  void release_l2() {
+    if (!l2_active) return;
+    std::lock_guard<std::mutex> lock(l2win::mu);
+    if (--l2win::users[device] == 0) {
+      cudaCtxResetPersistingL2Cache();
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    }
+    l2_active = false;
+  }
+
   void detach_peers() {
     for (uint32_t p = 0; p < npeers; ++p) {
       if (peer_ipc[p] && peer_base[p]) cudaIpcCloseMemHandle(peer_base[p]);
@@ -429,13 +440,8 @@ struct hanf_engine {
     if (device >= 0) cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     phase("sync");
-    if (l2_active) {  // the persisting set-aside goes with the last windowed engine
-      std::lock_guard<std::mutex> lock(l2win::mu);
-      if (--l2win::users[device] == 0) {
-        cudaCtxResetPersistingL2Cache();
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-      }
-      l2_active = false;
+    if (l2_active) {
+      release_l2();
       phase("l2");
     }
     for (auto& a : graphs)
@@ -1256,14 +1262,7 @@ hanf_status build_block(hanf_engine* e) {
       }
   // the item sweep wants the whole L2 for its segment: no persisting
   // set-aside for the hot prefix (config 5: 49.2 ms without, 50.4 with)
-  if (e->l2_active) {
-    std::lock_guard<std::mutex> lock(l2win::mu);
-    if (--l2win::users[e->device] == 0) {
-      cudaCtxResetPersistingL2Cache();
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-    }
-    e->l2_active = false;
-  }
+  e->release_l2();
   e->l2_window = 0;
   e->block_items = items_n;
   e->block_ready = true;
