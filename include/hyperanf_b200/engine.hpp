@@ -22,6 +22,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../hanf.h"
@@ -295,6 +296,13 @@ class NfEngine {
     check(hanf_reseed(h_, seed));
     cfg_.seed = seed;
     params_.seed = seed;
+  }
+  // (new) items and arcs of the engine's source-blocked dense sweeps, {0, 0}
+  // on the plain schedule (hanf_block_stats; results never depend on it)
+  std::pair<std::uint64_t, std::uint64_t> block_stats() const {
+    std::uint64_t items = 0, arcs = 0;
+    check(hanf_block_stats(h_, &items, &arcs));
+    return {items, arcs};
   }
   // hll.hpp:275-286 save_counters of the current counters (same bytes)
   void save_counters(const std::string& path) const { check(hanf_save_counters(h_, path.c_str())); }

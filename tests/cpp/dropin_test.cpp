@@ -228,6 +228,31 @@ int main() {
     unsetenv("HANF_RELABEL");
     lockstep_multi(hyperanf::gen_uniform_random(100, 3.0, 2), c, {0, 0}, "multi tiny (one shard)");
   }
+  {  // source-blocked dense sweeps (hanf_block.cu) forced on small shapes,
+     // mapped arc chunks at upload: the reference's bits through the drop-in
+    hyperanf::EngineConfig c;
+    c.bucket_bits = 6;
+    c.seed = 31;
+    const auto g = hyperanf::gen_uniform_random(5000, 12.0, 4);
+    setenv("HANF_RELABEL", "1", 1);
+    setenv("HANF_LAYOUT", "packed", 1);
+    setenv("HANF_BLOCK", "1", 1);
+    setenv("HANF_BLOCK_S", "6", 1);
+    setenv("HANF_BLOCK_T", "7", 1);
+    setenv("HANF_BLOCK_SEG", "6", 1);
+    setenv("HANF_BLOCK_GROUP", "6", 1);
+    setenv("HANF_MAP_CHUNK", "1000", 1);
+    {
+      auto bc = hyperanf_b200::from_reference(c);
+      bc.expected_runs = 32;
+      hyperanf_b200::NfEngine probe(g, bc);
+      expect(probe.block_stats().first > 0, "blocked engine has items");
+    }
+    lockstep(g, c, "source-blocked sweeps");
+    for (const char* k : {"HANF_RELABEL", "HANF_LAYOUT", "HANF_BLOCK", "HANF_BLOCK_S", "HANF_BLOCK_T",
+                          "HANF_BLOCK_SEG", "HANF_BLOCK_GROUP", "HANF_MAP_CHUNK"})
+      unsetenv(k);
+  }
   std::printf("dropin_test: %zu graphs, %d failures\n", cases.size(), failures);
   return failures == 0 ? 0 : 1;
 }
