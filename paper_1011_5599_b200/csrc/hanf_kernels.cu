@@ -46,41 +46,54 @@ __global__ void seed_kernel(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
                             const uint32_t* __restrict__ orig_of, uint32_t batch,
                             const uint64_t* __restrict__ batch_mix, bool bytes) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t v = node_begin + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-       v < node_end; v += stride) {
+  // One warp per 32 consecutive rows: lane l hashes row v0 + l, then the
+  // warp writes the rows' 32 * pitch words with lane-contiguous 8-byte
+  // stores (word j of the block belongs to row j / pitch: its one or two
+  // non-zero words come from that row's lane by shuffle).  Per-thread rows
+  // wrote 8 bytes every `pitch` words: 1.2 TB/s on config 5's 21.5 GB.
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t v0 = node_begin + (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x - lane);
+       v0 < node_end; v0 += stride) {
+    const uint64_t v = v0 + lane;
     // counter_add(v, v): the item is the node's original id (hash.hpp:20-22);
     // batched runs: row v is node v / batch of run v % batch
-    uint64_t item = orig_of ? orig_of[v] : v;
-    uint64_t mix = seed_mix;
-    if (batch > 1) {
-      item = v / batch;
-      mix = batch_mix[v % batch];
-    }
-    const uint64_t h = mix64(item ^ mix);
-    const uint32_t bucket = static_cast<uint32_t>(h >> (64 - bucket_bits));
-    const uint64_t rest = h << bucket_bits;
-    uint32_t rho = rest == 0 ? (64 - bucket_bits) + 1 : __clzll(rest) + 1;
-    const uint32_t maxv = (1u << register_bits) - 1;
-    rho = rho < maxv ? rho : maxv;
-    const uint64_t bit = static_cast<uint64_t>(bucket) * register_bits;
-    const uint64_t wi = bit >> 6;
-    const uint32_t off = bit & 63;
-    uint64_t* ca = a + v * pitch;
-    uint64_t* cb = b + v * pitch;
-    if (bytes) {  // byte layout: register `bucket` is byte `bucket` of the row
-      for (uint32_t k = 0; k < pitch; ++k) {
-        const uint64_t word = k == bucket / 8 ? static_cast<uint64_t>(rho) << (8 * (bucket % 8)) : 0;
-        ca[k] = word;
-        cb[k] = word;
+    uint32_t wi = 0xffffffffu;  // (rows past the range write nothing)
+    uint64_t lo = 0, hi = 0;
+    if (v < node_end) {
+      uint64_t item = orig_of ? orig_of[v] : v;
+      uint64_t mix = seed_mix;
+      if (batch > 1) {
+        item = v / batch;
+        mix = batch_mix[v % batch];
       }
-      continue;
+      const uint64_t h = mix64(item ^ mix);
+      const uint32_t bucket = static_cast<uint32_t>(h >> (64 - bucket_bits));
+      const uint64_t rest = h << bucket_bits;
+      uint32_t rho = rest == 0 ? (64 - bucket_bits) + 1 : __clzll(rest) + 1;
+      const uint32_t maxv = (1u << register_bits) - 1;
+      rho = rho < maxv ? rho : maxv;
+      if (bytes) {  // byte layout: register `bucket` is byte `bucket` of the row
+        wi = bucket / 8;
+        lo = static_cast<uint64_t>(rho) << (8 * (bucket % 8));
+      } else {
+        const uint64_t bit = static_cast<uint64_t>(bucket) * register_bits;
+        const uint32_t off = bit & 63;
+        wi = static_cast<uint32_t>(bit >> 6);
+        lo = static_cast<uint64_t>(rho) << off;
+        if (off + register_bits > 64) hi = static_cast<uint64_t>(rho) >> (64 - off);
+      }
     }
-    for (uint32_t k = 0; k < pitch; ++k) {  // padding words beyond W stay 0
-      uint64_t word = 0;
-      if (k == wi) word |= static_cast<uint64_t>(rho) << off;
-      if (k == wi + 1 && off + register_bits > 64) word |= static_cast<uint64_t>(rho) >> (64 - off);
-      ca[k] = word;
-      cb[k] = word;
+    uint64_t* ca = a + v0 * pitch;
+    uint64_t* cb = b + v0 * pitch;
+    for (uint32_t j = lane; j < 32 * pitch; j += 32) {  // padding words beyond W stay 0
+      const uint32_t r = j / pitch, k = j - r * pitch;
+      const uint32_t rwi = __shfl_sync(0xffffffffu, wi, r);
+      const uint64_t rlo = __shfl_sync(0xffffffffu, lo, r);
+      const uint64_t rhi = __shfl_sync(0xffffffffu, hi, r);
+      if (rwi == 0xffffffffu) continue;
+      const uint64_t word = k == rwi ? rlo : (k == rwi + 1 ? rhi : 0);
+      ca[j] = word;
+      cb[j] = word;
     }
   }
   // every seeded counter counts as modified (engine.hpp:86)
