@@ -68,9 +68,10 @@ def test_blocked_golden_traces(hanf, traces, monkeypatch):
 
 
 def test_blocked_from_the_first_reseed(hanf, monkeypatch):
-    """The default for large engines, forced here whatever the size: the
-    first run sweeps plainly, the build happens at the first reset / reseed,
-    and every later run equals a fresh engine's."""
+    """HANF_BLOCK=2: the build at the first reset / reseed whatever the size
+    (by default a large engine builds at the reset that follows its 96th
+    dense step, tests/test_gpu_atsize.py).  The first run sweeps plainly,
+    every later run equals a fresh engine's."""
     _force(monkeypatch, SHAPES[1], mode="2")
     g = hanf.gen_rmat(13, 16, 0.57, 0.19, 0.19, 3, 5)
     with hanf.NfEngine(g, hanf.EngineConfig(bucket_bits=6, seed=7)) as e:
