@@ -134,11 +134,28 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _drop_rendezvous(tag):
+    try:
+        os.unlink(f"/tmp/hanf_gloo_{os.getpid()}_{tag}")
+    except FileNotFoundError:
+        pass
+
+
+def _fresh_tag():
+    """A tag unique to this run (also names the emulated peers' shared
+    memory), with no rendezvous file left over from an earlier run."""
+    tag = _free_port()
+    _drop_rendezvous(tag)
+    return tag
+
+
 def _worker(rank, world, port, spec, out):
     import sys
     sys.path.insert(0, ROOT)
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: a TCP port picked by the parent can be taken again
+    # before the workers bind it (`port` stays the run's unique tag)
+    dist.init_process_group("gloo", init_method=f"file:///tmp/hanf_gloo_{os.getppid()}_{port}",
+                            rank=rank, world_size=world)
     import paper_1011_5599_b200 as hanf
     from paper_1011_5599_b200.sharded import ShardedNfEngine, shard_ranges
     g = hanf.gen_uniform_random(*spec["graph"])
@@ -158,8 +175,10 @@ def test_sharded_run_matches_single_engine(port, world, graph, delta):
     spec = {"graph": graph, "b": 6, "seed": 42, "delta": delta}
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), spec, out), nprocs=world,
+    tag = _fresh_tag()
+    mp.start_processes(_worker, args=(world, tag, spec, out), nprocs=world,
                        join=True, start_method="spawn")
+    _drop_rendezvous(tag)
     n, off, succ = port.gen_uniform_random(*graph)
     vals, mods = port.engine(n, off, succ, bucket_bits=6, seed=42).run()
     final = port.engine(n, off, succ, bucket_bits=6, seed=42)
@@ -315,8 +334,10 @@ class EmulatedPeerShard:
 def _peer_worker(rank, world, port, spec, out):
     import sys
     sys.path.insert(0, ROOT)
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: a TCP port picked by the parent can be taken again
+    # before the workers bind it (`port` stays the run's unique tag)
+    dist.init_process_group("gloo", init_method=f"file:///tmp/hanf_gloo_{os.getppid()}_{port}",
+                            rank=rank, world_size=world)
     import paper_1011_5599_b200 as hanf
     from paper_1011_5599_b200.sharded import ShardedNfEngine, shard_ranges
     g = hanf.gen_uniform_random(*spec["graph"])
@@ -338,8 +359,10 @@ def test_peer_push_run_matches_single_engine(port, world, graph):
     spec = {"graph": graph, "b": 6, "seed": 42}
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_peer_worker, args=(world, _free_port(), spec, out), nprocs=world,
+    tag = _fresh_tag()
+    mp.start_processes(_peer_worker, args=(world, tag, spec, out), nprocs=world,
                        join=True, start_method="spawn")
+    _drop_rendezvous(tag)
     n, off, succ = port.gen_uniform_random(*graph)
     vals, mods = port.engine(n, off, succ, bucket_bits=6, seed=42).run()
     final = port.engine(n, off, succ, bucket_bits=6, seed=42)
